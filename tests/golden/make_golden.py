@@ -1,0 +1,105 @@
+"""Generate the golden fixtures in tests/golden/ by running the REFERENCE
+itself (branchpar, /root/reference/pkg/src) in float64.
+
+Run here (the reference does not exist on the GPU box):
+
+    python tests/golden/make_golden.py
+
+Outputs (committed, small):
+  step_<cfg>.npz   run_single(cfg, init_params(cfg, 32), seed=32): m_out,
+                   z_out, loss, dm, dz and every parameter gradient
+                   (keys "grad:<name>"), plus the tape madds of one block
+                   forward ("madds_block").  run_bp is asserted bitwise
+                   equal to run_single before saving.
+  subops_toy.npz   every sub-op of block 0 at the toy dims: forward delta
+                   and the VJP of a seeded random cotangent R with respect
+                   to m, z and the sub-op's parameters
+                   ("<subop>:delta", "<subop>:dm", "<subop>:dz",
+                   "<subop>:grad:<suffix>").
+"""
+
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+REF = "/root/reference/pkg/src"
+HERE = os.path.dirname(os.path.abspath(__file__))
+
+CONFIGS = {
+    # tests/test_schedules.py:15-19 toy dims
+    "toy": dict(s=8, r=16, c_m=8, c_z=8, h=2, c_opm=4, t_factor=4, n_blocks=2),
+    # tests/test_schedules.py:72-73 odd dims, three blocks
+    "odd": dict(s=5, r=6, c_m=4, c_z=6, h=2, c_opm=3, t_factor=4, n_blocks=3),
+    # BASELINE.json configs[0] (C1 tiny), h/c_opm/t from SURVEY.md 8(d)
+    "c1": dict(s=16, r=32, c_m=32, c_z=16, h=4, c_opm=8, t_factor=4, n_blocks=2),
+}
+
+
+def main():
+    sys.path.insert(0, REF)
+    from branchpar import tensor as T
+    from branchpar import evoformer as E
+    from branchpar.schedules import compare_runs, run_bp, run_single
+
+    for tag, kw in CONFIGS.items():
+        cfg = E.EvoConfig(**kw)
+        store = E.init_params(cfg, 32)
+        a = run_single(cfg, store, seed=32)
+        b = run_bp(cfg, store, seed=32)
+        assert compare_runs(a, b, rtol=0.0).bitwise, tag
+        g = T.Graph()
+        P = store.bind(g)
+        m, z = E.seeded_inputs(cfg, 32)
+        E.evoformer_block(P, 0, g.leaf(m), g.leaf(z), cfg)
+        out = dict(m_out=a.m_out, z_out=a.z_out, loss=np.float64(a.loss),
+                   dm=a.dm, dz=a.dz, madds_block=np.int64(g.madds))
+        for name, arr in a.grads.items():
+            out[f"grad:{name}"] = arr
+        np.savez_compressed(os.path.join(HERE, f"step_{tag}.npz"), **out)
+        print(tag, "saved", len(out), "arrays; madds/block", g.madds)
+
+    cfg = E.EvoConfig(**CONFIGS["toy"])
+    store = E.init_params(cfg, 32)
+    m, z = E.seeded_inputs(cfg, 33)
+    rng = np.random.default_rng(34)
+    out = {}
+    for name in E.SUBOPS:
+        g = T.Graph()
+        P = store.bind(g)
+        mt, zt = g.leaf(m), g.leaf(z)
+        px = f"blk0.{name}"
+        if name == "row_attn":
+            delta = E.row_attn(P, px, mt, zt, cfg)
+        elif name == "col_attn":
+            delta = E.col_attn(P, px, mt, cfg)
+        elif name == "msa_transition":
+            delta = E.msa_transition(P, px, mt, cfg)
+        elif name == "opm":
+            delta = E.opm(P, px, mt, cfg)
+        elif name == "pair_transition":
+            delta = E.pair_transition(P, px, zt, cfg)
+        elif name.startswith("tri_mult"):
+            delta = E.tri_mult(P, px, zt, cfg, name.endswith("_in"))
+        else:
+            delta = E.tri_attn(P, px, zt, cfg, name.endswith("_end"))
+        R = rng.standard_normal(delta.shape)
+        loss = T.reduce_sum(T.mul(delta, g.leaf(R)))
+        g.backward(loss)
+        out[f"{name}:R"] = R
+        out[f"{name}:delta"] = delta.data
+        out[f"{name}:dm"] = g.grad(mt)
+        out[f"{name}:dz"] = g.grad(zt)
+        for pname in store.names():
+            if pname.startswith(px + "."):
+                out[f"{name}:grad:{pname[len(px) + 1:]}"] = g.grad(P[pname])
+    out["m"] = m
+    out["z"] = z
+    np.savez_compressed(os.path.join(HERE, "subops_toy.npz"), **out)
+    print("subops saved", len(out), "arrays")
+
+
+if __name__ == "__main__":
+    main()
