@@ -1,0 +1,351 @@
+"""Benchmark: Parallel Evoformer train step (fwd + loss + bwd) on B200.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl native|reference]
+
+Workload (BASELINE.json configs[1]): one Parallel Evoformer block at the
+AF2 initial-training shape s=128 r=256 c_m=256 c_z=128 h=8 c_opm=32 t=4,
+bf16 operands / fp32 accumulation and residual streams, synthetic N(0,1)
+inputs (make_batch seed 32), random-init weights (init_params seed 32).
+A step = forward + loss + backward with every parameter gradient.
+
+Metric: Evoformer train samples/s (whole job); also fwd+bwd ms per block.
+Multi-GPU (torchrun, one rank per GPU): BP=2 x DP=N/2 (N even) with the
+branch exchange over NCCL; N=1 is BP=1.  value = samples processed by all
+ranks / max-over-ranks device time.
+
+--impl reference times the reference algorithm's CPU implementation (the
+pinned numpy oracle port, oracle/evoformer_np.py) on the host cores.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    "af2": dict(s=128, r=256, c_m=256, c_z=128, h=8, c_opm=32, t_factor=4, n_blocks=1),
+    "mid": dict(s=32, r=64, c_m=64, c_z=32, h=4, c_opm=16, t_factor=4, n_blocks=1),
+    "c1": dict(s=16, r=32, c_m=32, c_z=16, h=4, c_opm=8, t_factor=4, n_blocks=2),
+}
+METRIC = "Evoformer train samples/sec (BP=1 vs BP=2, 1/2/4/8 B200); fwd+bwd ms/block"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p["bf16_tflops"], p.get("bf16_tflops_sustained"), p["hbm_gbs"], "measured"
+    except Exception:
+        return 1590.0, 1400.0, 6650.0, "fallback"
+
+
+# ---------------------------------------------------------------------------
+# CPU baseline: the oracle port, sampled sub-op by sub-op
+# ---------------------------------------------------------------------------
+
+def cpu_sample(kw, budget_s=60.0, reps=1):
+    """Fwd+bwd of each of the nine sub-ops at the full shape, fp32 numpy
+    on all host cores; block time = sum of the sub-op times (the residual
+    adds are negligible).  Returns (seconds per block, details)."""
+    import numpy as np
+    from oracle import evoformer_np as O
+    d = O.Dims(**{**kw, "n_blocks": 1})
+    P = O.init_params(d, 32, dtype=np.float32)
+    m, z = O.make_batch(d, 32, 1, dtype=np.float32)[0]
+    rng = np.random.default_rng(0)
+    times = {}
+    for name in O.SUBOPS:
+        px = f"blk0.{name}"
+        best = None
+        for _ in range(reps):
+            t0 = time.perf_counter()
+            delta, cache = O.subop_fwd(name, P, px, m, z, d)
+            R = rng.standard_normal(delta.shape).astype(np.float32)
+            O.subop_vjp(name, R, cache, P, px, d, O.Grads())
+            dt = time.perf_counter() - t0
+            best = dt if best is None else min(best, dt)
+        times[name] = best
+    return sum(times.values()), times
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    kw = CONFIGS[args.config]
+    cores = os.cpu_count()
+    for _ in range(max(0, args.warmup) and 1):
+        pass
+    per = []
+    for _ in range(max(1, min(args.steps, 3))):
+        t, _ = cpu_sample(kw)
+        per.append(t)
+    t = min(per)
+    value = kw["n_blocks"] / t / kw["n_blocks"]
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
+        "n_gpus": args.gpus, "steps": len(per), "warmup": 0, "ms_per_step": t * 1e3,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic", "config": {"workload": f"parallel_evoformer_block_{args.config}",
+                                        **kw, "precision": "fp32 numpy"},
+        "cpu_baseline": {"value": value, "unit": "samples/s", "cores": cores, "kind": "port",
+                         "sample": "fwd+bwd of each of the 9 sub-ops once at full shape "
+                                   "(oracle/evoformer_np.py, numpy fp32, all cores); "
+                                   "block time = sum"},
+        "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0,
+                "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line))
+    return 0
+
+
+# ---------------------------------------------------------------------------
+# clocks sampler
+# ---------------------------------------------------------------------------
+
+class Clocks:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active")
+
+    def __init__(self, index=0):
+        self.index = index
+        self.proc = None
+        self.path = tempfile.mktemp(suffix=".csv")
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], 0.0, 0
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 4:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+                reasons |= int(parts[3], 16)
+            except ValueError:
+                continue
+        if not sm:
+            return None
+        sm.sort()
+        names = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+                 0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+                 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+                 0x100: "display_clock_setting"}
+        rs = [v for k, v in names.items() if reasons & k]
+        return {"sm_mhz": sm[len(sm) // 2], "sm_max_mhz": mx, "reasons": rs,
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------
+# native arm
+# ---------------------------------------------------------------------------
+
+def run_native(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00235_b200 as pkg
+    from paper_2211_00235_b200 import _native, kernels as K, schedules as S
+    from oracle import evoformer_np as O
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    kw = CONFIGS[args.config]
+    if args.blocks:
+        kw = {**kw, "n_blocks": args.blocks}
+    cfg = pkg.EvoConfig(**kw)
+    store = pkg.init_params(cfg, 32, device=dev)
+    bp = 2 if (world > 1 and world % 2 == 0 and not args.dp_only) else 1
+    dp = world // bp
+    layout = S.ParallelLayout(dp=dp, bp=bp)
+    if bp == 2:
+        from paper_2211_00235_b200 import distributed as D
+        runner = D.DistributedStep(cfg, store, layout, precision=args.precision)
+    else:
+        runner = None
+    st = S.StepState(cfg, store, args.precision, dev)
+    st.pack()
+    dp_i = layout.coords(rank)[0]
+    m_h, z_h = S.make_batch(cfg, 32 + dp_i, 1, device="cpu")[0]
+    m_h, z_h = m_h.pin_memory(), z_h.pin_memory()
+    m_d, z_d = m_h.to(dev), z_h.to(dev)
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+
+    def step(m, z):
+        if runner is not None:
+            return runner.step(m, z)
+        out = S.full_step(st, m, z)
+        if dp > 1:
+            for bg in st.grads:
+                for bank in (bg.msa, bg.pair):
+                    dist.all_reduce(bank.flat)
+                    bank.flat.div_(dp)
+        return out
+
+    # warm-up (also first-touch allocations)
+    for _ in range(args.warmup):
+        step(m_d, z_d)
+    torch.cuda.synchronize()
+
+    # timed region: device-resident inputs
+    prof = []
+    K.PROFILE = prof
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    n0 = _native.launch_count()
+    ev0 = torch.cuda.Event(enable_timing=True)
+    ev1 = torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        step(m_d, z_d)
+    ev1.record()
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = _native.launch_count() - n0
+    K.PROFILE = None
+    clk = clocks.stop()
+    ms = ev0.elapsed_time(ev1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+
+    # kernel-family breakdown from the events recorded in the timed region
+    fam = {}
+    for name, flops, e0, e1 in prof:
+        d_ms = e0.elapsed_time(e1)
+        f = fam.setdefault(name, [0.0, 0.0, 0])
+        f[0] += flops
+        f[1] += d_ms
+        f[2] += 1
+
+    # end-to-end: pinned host inputs -> device, step, loss -> host
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(args.steps):
+        m_e = m_h.to(dev, non_blocking=True)
+        z_e = z_h.to(dev, non_blocking=True)
+        out = step(m_e, z_e)
+        loss_h.copy_(out[2].reshape(1), non_blocking=True)
+    e1.record()
+    torch.cuda.synchronize()
+    ms_e2e = e0.elapsed_time(e1) / args.steps
+    if world > 1:
+        t = torch.tensor([ms_e2e], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_e2e = float(t.item())
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    d = O.Dims(**kw)
+    flops_block = 3 * O.block_flops(d)
+    flops_step = flops_block * cfg.n_blocks
+    samples = dp  # one sample per DP replica per step
+    value = samples / (ms / 1e3)
+    peak, peak_sus, hbm, src = peaks()
+    step_tflops = flops_step * dp / (ms / 1e3) / 1e12
+    roof = None
+    if fam:
+        top = max(fam, key=lambda k: fam[k][1])
+        fl, tms, n = fam[top]
+        achieved = fl / (tms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": src, "launches": n,
+                "share_of_step": tms / (ms * args.steps)}
+    breakdown = {k: {"tflops": (v[0] / (v[1] / 1e3) / 1e12) if v[1] > 0 else None,
+                     "ms_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
+                 for k, v in fam.items()}
+    cpu = None
+    if not args.no_cpu_baseline:
+        t_cpu, parts = cpu_sample(kw)
+        cpu = {"value": 1.0 / (t_cpu * cfg.n_blocks), "unit": "samples/s",
+               "cores": os.cpu_count(), "kind": "port",
+               "sample": "fwd+bwd of each of the 9 sub-ops once at the full shape "
+                         "(oracle/evoformer_np.py, numpy fp32, all host cores); "
+                         f"block time = sum = {t_cpu:.1f} s"}
+    h2d = (m_h.numel() + z_h.numel()) * 4
+    line = {
+        "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "ms_per_block_fwd_bwd": ms / cfg.n_blocks,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": f"parallel_evoformer_block_{args.config}", **kw,
+                   "precision": args.precision, "parallelism": f"bp{bp}xdp{dp}",
+                   "global_batch": dp,
+                   "l2": "step working set (>1 GB of activations) exceeds the 126 MB L2"},
+        "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,
+        "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu,
+        "e2e": {"value": samples / (ms_e2e / 1e3), "unit": "samples/s",
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+        "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+        "clocks": clk,
+    }
+    print(json.dumps(line))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="native", choices=["native", "reference"])
+    ap.add_argument("--config", default="af2", choices=list(CONFIGS))
+    ap.add_argument("--blocks", type=int, default=0)
+    ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--dp-only", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_native(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -344,7 +344,9 @@ def opm_fwd(P, px, m, d):
     mh, lc = ln_fwd(m, P[f"{px}.ln_g"], P[f"{px}.ln_b"], d.eps)
     a = lin(mh, P[f"{px}.a_w"], P[f"{px}.a_b"])
     b = lin(mh, P[f"{px}.b_w"], P[f"{px}.b_b"])
-    o = np.einsum("sip,sjq->ijpq", a, b).reshape(r, r, c * c)
+    # raw[(i,p),(j,q)] = sum_s a[s,(i,p)] b[s,(j,q)]  (a BLAS matmul, :343-347)
+    raw = a.reshape(s, r * c).T @ b.reshape(s, r * c)
+    o = raw.reshape(r, c, r, c).transpose(0, 2, 1, 3).reshape(r, r, c * c)
     os_ = o * (1.0 / s)
     out = lin(os_, P[f"{px}.out_w"], P[f"{px}.out_b"])
     return out, dict(lc=lc, mh=mh, a=a, b=b, os=os_)
@@ -357,8 +359,9 @@ def opm_vjp(dout, cache, P, px, d, G):
     G.add(f"{px}.out_b", dbo)
     do = (dos * (1.0 / s)).reshape(r, r, c, c)
     a, b, mh = cache["a"], cache["b"], cache["mh"]
-    da = np.einsum("ijpq,sjq->sip", do, b)
-    db = np.einsum("ijpq,sip->sjq", do, a)
+    draw = do.transpose(0, 2, 1, 3).reshape(r * c, r * c)      # [(i,p),(j,q)]
+    da = (b.reshape(s, r * c) @ draw.T).reshape(s, r, c)
+    db = (a.reshape(s, r * c) @ draw).reshape(s, r, c)
     dmh_a, dwa, dba = lin_vjp(da, mh, P[f"{px}.a_w"])
     dmh_b, dwb, dbb = lin_vjp(db, mh, P[f"{px}.b_w"])
     G.add(f"{px}.a_w", dwa)
@@ -380,10 +383,12 @@ def tri_mult_fwd(P, px, z, d, incoming):
         val = lin(zh, P[f"{px}.{tag}_w"], P[f"{px}.{tag}_b"])
         proj[tag] = (gp, val, gp * val)
     a, b = proj["a"][2], proj["b"][2]
+    ac, bc = a.transpose(2, 0, 1), b.transpose(2, 0, 1)     # [c, ., .]
     if incoming:
-        p = np.einsum("kic,kjc->ijc", a, b)
+        p = np.matmul(ac.transpose(0, 2, 1), bc)               # sum_k a[k,i] b[k,j]
     else:
-        p = np.einsum("ikc,jkc->ijc", a, b)
+        p = np.matmul(ac, bc.transpose(0, 2, 1))               # sum_k a[i,k] b[j,k]
+    p = np.ascontiguousarray(p.transpose(1, 2, 0))
     pn, lcp = ln_fwd(p, P[f"{px}.p_ln_g"], P[f"{px}.p_ln_b"], d.eps)
     o = lin(pn, P[f"{px}.out_w"], P[f"{px}.out_b"])
     g = sigmoid(lin(zh, P[f"{px}.out_gate_w"], P[f"{px}.out_gate_b"]))
@@ -405,12 +410,14 @@ def tri_mult_vjp(dout, cache, P, px, d, G):
     G.add(f"{px}.p_ln_g", dg_)
     G.add(f"{px}.p_ln_b", db_)
     a, b = cache["proj"]["a"][2], cache["proj"]["b"][2]
+    dpc = dp.transpose(2, 0, 1)                                 # [c, i, j]
+    ac, bc = a.transpose(2, 0, 1), b.transpose(2, 0, 1)
     if cache["incoming"]:
-        da = np.einsum("ijc,kjc->kic", dp, b)
-        dbb = np.einsum("ijc,kic->kjc", dp, a)
+        da = np.matmul(bc, dpc.transpose(0, 2, 1)).transpose(1, 2, 0)   # [k,i,c]
+        dbb = np.matmul(ac, dpc).transpose(1, 2, 0)                     # [k,j,c]
     else:
-        da = np.einsum("ijc,jkc->ikc", dp, b)
-        dbb = np.einsum("ijc,ikc->jkc", dp, a)
+        da = np.matmul(dpc, bc).transpose(1, 2, 0)                      # [i,k,c]
+        dbb = np.matmul(dpc.transpose(0, 2, 1), ac).transpose(1, 2, 0)  # [j,k,c]
     for tag, dt in (("a", da), ("b", dbb)):
         gp, val, _ = cache["proj"][tag]
         dgpre = dt * val * gp * (1.0 - gp)

@@ -1,0 +1,259 @@
+"""Thin typed wrappers over the C ABI taking torch device tensors.
+
+Every function here launches native kernels on the current CUDA stream
+(torch is used only for device memory and the stream handle).  Shapes
+and strides are passed explicitly; layouts are documented in DESIGN.md.
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+
+import torch
+
+from . import _native as N
+from ._native import AttnDesc, EvoMat, GemmDesc, check, lib
+
+DT = {torch.float32: N.EVO_F32, torch.bfloat16: N.EVO_BF16}
+
+
+def dt(t: torch.Tensor) -> int:
+    try:
+        return DT[t.dtype]
+    except KeyError:
+        raise N.ContractError(f"unsupported dtype {t.dtype}") from None
+
+
+def stream() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+# bench.py sets this to a list to time kernel families with CUDA events on
+# the launching stream: entries (family, algorithmic_flops, ev_start, ev_end)
+PROFILE = None
+
+
+def _timed(family, flops, fn):
+    if PROFILE is None:
+        return fn()
+    e0 = torch.cuda.Event(enable_timing=True)
+    e1 = torch.cuda.Event(enable_timing=True)
+    e0.record()
+    r = fn()
+    e1.record()
+    PROFILE.append((family, flops, e0, e1))
+    return r
+
+
+def ptr(t, off: int = 0):
+    if t is None:
+        return None
+    return t.data_ptr() + off * t.element_size()
+
+
+def _ws(nbytes: int, device) -> torch.Tensor | None:
+    if nbytes <= 0:
+        return None
+    return torch.empty(int(nbytes), dtype=torch.uint8, device=device)
+
+
+class Mat:
+    """Strided view (element units) of a tensor for the GEMM descriptor:
+    element (i, j, b1, b2) at off + i*rs + j*cs + b1*bs1 + b2*bs2, with an
+    optional two-level row/column map (see include/evo_b200.h)."""
+
+    __slots__ = ("t", "off", "rs", "cs", "bs1", "bs2", "rdiv", "rs0", "cdiv", "cs0")
+
+    def __init__(self, t, rs, cs, bs1=0, bs2=0, off=0, rdiv=0, rs0=0, cdiv=0, cs0=0):
+        self.t, self.off, self.rs, self.cs = t, off, rs, cs
+        self.bs1, self.bs2 = bs1, bs2
+        self.rdiv, self.rs0, self.cdiv, self.cs0 = rdiv, rs0, cdiv, cs0
+
+    def c(self) -> EvoMat:
+        return EvoMat(ptr(self.t, self.off), self.rs, self.cs, self.bs1, self.bs2,
+                      self.rdiv, self.rs0, self.cdiv, self.cs0)
+
+
+def gemm(A: Mat, B: Mat, Cm: Mat, M: int, N_: int, K: int, *, alpha: float = 1.0,
+         bias=None, epi: int = N.EPI_NONE, col0: int = 0, accumulate: bool = False,
+         residual=None, B1: int = 1, B2: int = 1, split_k: int = 1,
+         force_simt: bool = False) -> None:
+    """C(m,n) = epi(alpha * sum_k A(m,k) B(n,k) + bias[n]) (+ residual)."""
+    if A.t.dtype != B.t.dtype:
+        raise N.ContractError(f"gemm operand dtypes differ: {A.t.dtype} vs {B.t.dtype}")
+    d = GemmDesc()
+    d.dtype_ab = dt(A.t)
+    d.dtype_c = dt(Cm.t)
+    d.M, d.N, d.K, d.B1, d.B2 = M, N_, K, B1, B2
+    d.A, d.B, d.C = A.c(), B.c(), Cm.c()
+    d.alpha = alpha
+    d.epilogue = epi
+    d.epi_col0 = col0
+    d.accumulate = 1 if accumulate else 0
+    d.split_k = max(1, int(split_k))
+    d.bias = ptr(bias)
+    d.residual = ptr(residual)
+    d.force_simt = 1 if force_simt else 0
+    L = lib()
+    nbytes = L.evo_gemm_workspace_bytes(C.byref(d))
+    ws = _ws(nbytes, Cm.t.device)
+    d.workspace = ptr(ws)
+    d.workspace_bytes = nbytes
+    _timed("gemm", 2.0 * M * N_ * K * B1 * B2,
+           lambda: check(L.evo_gemm(C.byref(d), stream()), "evo_gemm"))
+
+
+def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, target: int = 4096) -> int:
+    """Split-K factor for tall contractions (weight gradients): chunks of
+    <= `target` rows, and enough CTAs to cover the 148 SMs."""
+    if rows_k <= target:
+        return 1
+    tiles = max(1, ((M + 127) // 128) * ((N_ + 127) // 128) * batch)
+    by_size = (rows_k + target - 1) // target
+    by_fill = max(1, (2 * 148 + tiles - 1) // tiles)
+    return int(max(1, min(by_size * 2, max(by_size, by_fill), 64)))
+
+
+def linear(x, rows: int, d_in: int, W, ldw: int, d_out: int, out, ldo: int, *, w_off=0,
+           o_off=0, x_ld=None, bias=None, epi=N.EPI_NONE, col0=0, residual=None,
+           alpha=1.0):
+    """out[rows, d_out] = x[rows, d_in] @ W[:, w_off:w_off+d_out] (+bias...)."""
+    x_ld = d_in if x_ld is None else x_ld
+    gemm(Mat(x, x_ld, 1), Mat(W, 1, ldw, off=w_off), Mat(out, ldo, 1, off=o_off),
+         rows, d_out, d_in, bias=bias, epi=epi, col0=col0, residual=residual, alpha=alpha)
+
+
+def linear_dx(dy, rows: int, d_out: int, W, ldw: int, d_in: int, out, *, dy_ld=None,
+              w_off=0, accumulate=False, out_ld=None):
+    """out[rows, d_in] (+)= dy[rows, d_out] @ W[:, w_off:w_off+d_out]^T."""
+    dy_ld = d_out if dy_ld is None else dy_ld
+    out_ld = d_in if out_ld is None else out_ld
+    gemm(Mat(dy, dy_ld, 1), Mat(W, ldw, 1, off=w_off), Mat(out, out_ld, 1), rows, d_in, d_out,
+         accumulate=accumulate)
+
+
+def linear_dw(x, rows: int, d_in: int, dy, d_out: int, dW, ldd: int, *, x_ld=None, dy_ld=None,
+              dy_off=0, dw_off=0, accumulate=False):
+    """dW[d_in, d_out] (+)= x^T @ dy over `rows` (split-K, deterministic)."""
+    x_ld = d_in if x_ld is None else x_ld
+    dy_ld = d_out if dy_ld is None else dy_ld
+    gemm(Mat(x, 1, x_ld), Mat(dy, 1, dy_ld, off=dy_off), Mat(dW, ldd, 1, off=dw_off),
+         d_in, d_out, rows, split_k=pick_split(rows, d_in, d_out), accumulate=accumulate)
+
+
+def layernorm(x, rows: int, cols: int, gamma, beta, y, mean, rstd, eps: float, *,
+              x_rs=None, x_cs=1, y_rs=None):
+    x_rs = cols if x_rs is None else x_rs
+    y_rs = cols if y_rs is None else y_rs
+    check(lib().evo_layernorm_fwd(dt(x), dt(y), rows, cols, ptr(x), x_rs, x_cs, ptr(gamma),
+                                  ptr(beta), ptr(y), y_rs, ptr(mean), ptr(rstd), eps, stream()),
+          "evo_layernorm_fwd")
+
+
+def layernorm_bwd(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma, dbeta, *,
+                  dres=None, dy_rs=None, x_rs=None, x_cs=1, dx_rs=None, dx_cs=1,
+                  accumulate_params=False):
+    dy_rs = cols if dy_rs is None else dy_rs
+    x_rs = cols if x_rs is None else x_rs
+    dx_rs = cols if dx_rs is None else dx_rs
+    L = lib()
+    nbytes = L.evo_layernorm_bwd_workspace_bytes(rows, cols)
+    ws = _ws(nbytes, dx.device)
+    check(L.evo_layernorm_bwd(dt(dy), dt(x), dt(dx), rows, cols, ptr(dy), dy_rs, ptr(x), x_rs,
+                              x_cs, ptr(mean), ptr(rstd), ptr(gamma), ptr(dres), ptr(dx), dx_rs,
+                              dx_cs, ptr(dgamma), ptr(dbeta), 1 if accumulate_params else 0,
+                              ptr(ws), nbytes, stream()),
+          "evo_layernorm_bwd")
+
+
+def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
+              sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
+              dgm=None, dproj=None, dbias=None):
+    """Fused gated attention on the packed [rows, 4*hc] projection buffer
+    (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
+    backward into dproj (same packing) and dbias."""
+    d = AttnDesc()
+    d.dtype = dt(proj)
+    d.nb, d.H, d.L, d.D, d.scale = nb, H, L, D, scale
+    d.q, d.k, d.v, d.g = (ptr(proj, 0), ptr(proj, hc), ptr(proj, 2 * hc), ptr(proj, 3 * hc))
+    d.sb, d.sl = sb, sl
+    d.o, d.gm = ptr(o), ptr(gm)
+    d.o_sb, d.o_sl = o_sb, o_sl
+    d.bias, d.bh, d.bq, d.bk = ptr(bias), bh, bq, bk
+    d.lse = ptr(lse)
+    Lb = lib()
+    flops = 4.0 * nb * H * L * L * D
+    if dgm is None:
+        _timed("attention_fwd", flops,
+               lambda: check(Lb.evo_attention_fwd(C.byref(d), stream()), "evo_attention_fwd"))
+        return
+    d.dgm = ptr(dgm)
+    d.dq, d.dk, d.dv, d.dgpre = (ptr(dproj, 0), ptr(dproj, hc), ptr(dproj, 2 * hc),
+                                 ptr(dproj, 3 * hc))
+    d.dbias = ptr(dbias)
+    nbytes = Lb.evo_attention_bwd_workspace_bytes(C.byref(d))
+    ws = _ws(nbytes, proj.device)
+    d.workspace, d.workspace_bytes = ptr(ws), nbytes
+    _timed("attention_bwd", 2.0 * flops,
+           lambda: check(Lb.evo_attention_bwd(C.byref(d), stream()), "evo_attention_bwd"))
+
+
+def colsum(src, rows: int, cols: int, dst, *, rs=None, off=0, accumulate=False):
+    rs = cols if rs is None else rs
+    L = lib()
+    nbytes = L.evo_colsum_workspace_bytes(cols)
+    ws = _ws(nbytes, dst.device)
+    check(L.evo_colsum(dt(src), rows, cols, ptr(src, off), rs, ptr(dst),
+                       1 if accumulate else 0, ptr(ws), nbytes, stream()), "evo_colsum")
+
+
+def copy2d(src, rows: int, cols: int, dst, *, s_rs, s_cs=1, d_rs, d_cs=1, s_off=0, d_off=0):
+    check(lib().evo_copy2d(dt(src), dt(dst), rows, cols, ptr(src, s_off), s_rs, s_cs,
+                           ptr(dst, d_off), d_rs, d_cs, stream()), "evo_copy2d")
+
+
+def trimul_gate_fwd(proj, rows: int, c: int, ldp: int, a_cf, b_cf):
+    check(lib().evo_trimul_gate_fwd(dt(proj), rows, c, ptr(proj), ldp, ptr(a_cf), ptr(b_cf),
+                                    stream()), "evo_trimul_gate_fwd")
+
+
+def trimul_gate_bwd(proj, rows: int, c: int, ldp: int, da_cf, db_cf, dproj, ldd: int):
+    check(lib().evo_trimul_gate_bwd(dt(proj), rows, c, ptr(proj), ldp, ptr(da_cf), ptr(db_cf),
+                                    ptr(dproj), ldd, stream()), "evo_trimul_gate_bwd")
+
+
+def outgate_fwd(z, rows: int, cols: int, g, g_rs: int, g_off: int, o, znew):
+    check(lib().evo_outgate_fwd(dt(o), rows, cols, ptr(z), ptr(g, g_off), g_rs, ptr(o), cols,
+                                ptr(znew), stream()), "evo_outgate_fwd")
+
+
+def outgate_bwd(dz, rows: int, cols: int, g, g_rs: int, g_off: int, o, do_, dgpre,
+                dg_rs: int, dg_off: int):
+    check(lib().evo_outgate_bwd(dt(o), rows, cols, ptr(dz), ptr(g, g_off), g_rs, ptr(o), cols,
+                                ptr(do_), cols, ptr(dgpre, dg_off), dg_rs, stream()),
+          "evo_outgate_bwd")
+
+
+def mul2d(a, a_rs: int, a_off: int, b, b_rs: int, out, rows: int, cols: int):
+    """out[rows, cols] (contiguous) = a(r, c) * b(r, c)."""
+    check(lib().evo_mul2d(dt(a), dt(b), dt(out), rows, cols, ptr(a, a_off), a_rs, ptr(b), b_rs,
+                          ptr(out), cols, stream()), "evo_mul2d")
+
+
+def relu_bwd(dh, h, dpre, n: int):
+    check(lib().evo_relu_bwd(dt(h), n, ptr(dh), ptr(h), ptr(dpre), stream()), "evo_relu_bwd")
+
+
+def sq_mean(x, out, dx=None):
+    ws = torch.empty(4096, dtype=torch.uint8, device=x.device)
+    check(lib().evo_sq_mean(x.numel(), ptr(x), ptr(out), ptr(dx), ptr(ws), stream()),
+          "evo_sq_mean")
+
+
+def add(a, b, out):
+    check(lib().evo_add(a.numel(), ptr(a), ptr(b), ptr(out), stream()), "evo_add")
+
+
+def reduce_lead(src, nb: int, n1: int, n2: int, dst, d_s1: int, d_s2: int, accumulate=False):
+    check(lib().evo_reduce_lead(dt(src), nb, n1, n2, ptr(src), ptr(dst), d_s1, d_s2,
+                                1 if accumulate else 0, stream()), "evo_reduce_lead")

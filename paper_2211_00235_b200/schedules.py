@@ -1,0 +1,332 @@
+"""Train-step API (src/schedules.py:43-581) on B200: BP=1 step, branch
+parallelism (BP=2) and data parallelism over NCCL, run comparison and the
+closed-form communication ledger.
+
+The step is: forward through the stack, loss = mean(m^2) + mean(z^2)
+(src/schedules.py:194-195), backward, parameter-gradient sync.  Here the
+forward/backward are explicit sequences of native launches
+(engine.block_fwd / block_bwd) rather than a tape sweep; the BP=1 path
+forms dz_in = dz_pair + dz_row with the same two operands the BP
+allreduce sums, so BP=2 reproduces BP=1 bitwise (src/schedules.py:12-15).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import engine as E
+from . import kernels as K
+from .errors import ComparisonError, ConfigError
+from .evoformer import EvoConfig, ParamStore, act_dtype
+
+F32 = torch.float32
+
+
+@dataclass(frozen=True)
+class ParallelLayout:
+    """(dp, bp, dap) layout; rank = ((dp_i*bp)+bp_i)*dap + dap_i
+    (src/schedules.py:43-93).  dap must be 1 in this build."""
+
+    dp: int = 1
+    bp: int = 1
+    dap: int = 1
+
+    def __post_init__(self):
+        if self.dp < 1:
+            raise ConfigError(f"layout.dp must be >= 1, got {self.dp}")
+        if self.bp not in (1, 2):
+            raise ConfigError(
+                "layout.bp must be 1 or 2: the block splits into exactly two "
+                f"branches (MSA and pair), got bp={self.bp}")
+        if self.dap < 1 or (self.dap & (self.dap - 1)) != 0:
+            raise ConfigError(f"layout.dap must be a power of two >= 1, got {self.dap}")
+
+    @property
+    def world_size(self) -> int:
+        return self.dp * self.bp * self.dap
+
+    def rank_of(self, dp_i: int, bp_i: int, dap_i: int = 0) -> int:
+        return ((dp_i * self.bp) + bp_i) * self.dap + dap_i
+
+    def coords(self, rank: int):
+        dap_i = rank % self.dap
+        rest = rank // self.dap
+        return rest // self.bp, rest % self.bp, dap_i
+
+    def dap_group(self, rank: int):
+        dp_i, bp_i, _ = self.coords(rank)
+        return tuple(self.rank_of(dp_i, bp_i, k) for k in range(self.dap))
+
+    def bp_group(self, rank: int):
+        dp_i, _, dap_i = self.coords(rank)
+        return tuple(self.rank_of(dp_i, b, dap_i) for b in range(self.bp))
+
+    def dp_group(self, rank: int):
+        _, bp_i, dap_i = self.coords(rank)
+        return tuple(self.rank_of(d, bp_i, dap_i) for d in range(self.dp))
+
+    def validate_model(self, cfg: EvoConfig) -> None:
+        if self.dap > 1:
+            raise ConfigError("DAP (axial sharding) is outside this build's scope "
+                              "(SURVEY.md 8(f)); use dap=1")
+        if self.bp == 2 and cfg.variant != "parallel":
+            raise ConfigError(
+                "branch parallelism needs the parallel block wiring; the "
+                f"{cfg.variant!r} variant has a serial dependency between "
+                "the tracks inside each block")
+
+
+@dataclass
+class RunResult:
+    """Outputs of one training step (src/schedules.py:157-174).  Tensor
+    fields are device tensors; ``numpy()`` returns a host copy."""
+
+    m_out: object
+    z_out: object
+    loss: float
+    dm: object
+    dz: object
+    grads: dict
+    trace: object = None
+    rank_fwd_seconds: dict | None = None
+    wall_seconds: float = 0.0
+
+    def numpy(self) -> "RunResult":
+        return RunResult(_np(self.m_out), _np(self.z_out), self.loss, _np(self.dm),
+                         _np(self.dz), {k: _np(v) for k, v in self.grads.items()},
+                         self.trace, self.rank_fwd_seconds, self.wall_seconds)
+
+
+def _np(x):
+    if isinstance(x, torch.Tensor):
+        return x.detach().float().cpu().numpy()
+    return np.asarray(x)
+
+
+def make_batch(cfg: EvoConfig, seed: int, n: int, device="cuda"):
+    """n standard-normal (m, z) samples drawn sequentially from one PCG64
+    stream, identical to the reference's (src/schedules.py:177-185)."""
+    rng = np.random.default_rng(seed)
+    out = []
+    for _ in range(n):
+        m = rng.standard_normal((cfg.s, cfg.r, cfg.c_m)).astype(np.float32)
+        z = rng.standard_normal((cfg.r, cfg.r, cfg.c_z)).astype(np.float32)
+        out.append((torch.as_tensor(m, device=device), torch.as_tensor(z, device=device)))
+    return out
+
+
+# ---------------------------------------------------------------------------
+# the BP=1 step
+# ---------------------------------------------------------------------------
+
+class StepState:
+    """Reusable per-(cfg, precision) state: packed operand weights and the
+    per-block gradient banks.  ``pack(store)`` refreshes the operand copies
+    after a parameter update."""
+
+    def __init__(self, cfg: EvoConfig, store: ParamStore, precision: str | None = None,
+                 device=None):
+        self.cfg = cfg
+        self.act = act_dtype(precision)
+        self.dev = device or store.device
+        self.P = store.bind()
+        self.grads = [E.BlockGrads(b, cfg, self.dev) for b in range(cfg.n_blocks)]
+        self.packs = None
+
+    def pack(self, subops=E.MSA_SUBOPS + E.PAIR_SUBOPS):
+        self.packs = [E.pack_block(self.P, b, self.cfg, self.act, self.dev, subops)
+                      for b in range(self.cfg.n_blocks)]
+
+    def grad_dict(self):
+        out = {}
+        for bg in self.grads:
+            out.update(bg.names)
+        return out
+
+
+def full_step(st: StepState, m, z):
+    """Forward + loss + backward of the whole stack on one device.
+    Returns (m_out, z_out, loss_tensor[1], dm, dz, fwd_events)."""
+    cfg, act = st.cfg, st.act
+    s, r = cfg.s, cfg.r
+    if st.packs is None:
+        st.pack()
+    m_c = m.reshape(s * r, cfg.c_m)
+    z_c = z.reshape(r * r, cfg.c_z)
+    ctxs = []
+    for blk in range(cfg.n_blocks):
+        m_c, z_c, c = E.block_fwd(st.P, blk, st.packs[blk], m_c, z_c, cfg, act)
+        ctxs.append(c)
+    loss = torch.zeros(1, dtype=F32, device=m.device)
+    dm = torch.empty_like(m_c)
+    dz = torch.empty_like(z_c)
+    K.sq_mean(m_c, loss, dm)
+    K.sq_mean(z_c, loss, dz)
+    for blk in reversed(range(cfg.n_blocks)):
+        dm, dz = E.block_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctxs[blk], dm, dz,
+                             cfg, act)
+        ctxs[blk] = None
+    return (m_c.reshape(s, r, cfg.c_m), z_c.reshape(r, r, cfg.c_z), loss,
+            dm.reshape(s, r, cfg.c_m), dz.reshape(r, r, cfg.c_z))
+
+
+def run_single(cfg: EvoConfig, store: ParamStore, seed: int = 32,
+               precision: str | None = None) -> RunResult:
+    """Reference step on one GPU (src/schedules.py:387-399)."""
+    if cfg.variant != "parallel":
+        return _run_single_autograd(cfg, store, seed)
+    m, z = make_batch(cfg, seed, 1, store.device)[0]
+    st = StepState(cfg, store, precision)
+    t0 = time.perf_counter()
+    m_out, z_out, loss, dm, dz = full_step(st, m, z)
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    return RunResult(m_out, z_out, float(loss.item()), dm, dz, st.grad_dict(), None,
+                     {0: wall}, wall)
+
+
+def _run_single_autograd(cfg, store, seed):
+    """af2 / multimer wirings: composed from the differentiable sub-ops."""
+    from .evoformer import evoformer_stack
+    m, z = make_batch(cfg, seed, 1, store.device)[0]
+    params = {n: t.detach().clone().requires_grad_(True) for n, t in store.items()}
+    m = m.clone().requires_grad_(True)
+    z = z.clone().requires_grad_(True)
+    t0 = time.perf_counter()
+    mo, zo = evoformer_stack(params, m, z, cfg)
+    loss = (mo * mo).mean() + (zo * zo).mean()
+    loss.backward()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    grads = {n: (p.grad if p.grad is not None else torch.zeros_like(p))
+             for n, p in params.items()}
+    return RunResult(mo.detach(), zo.detach(), float(loss.item()), m.grad, z.grad, grads,
+                     None, {0: wall}, wall)
+
+
+# ---------------------------------------------------------------------------
+# comparing runs (src/schedules.py:430-488)
+# ---------------------------------------------------------------------------
+
+@dataclass
+class FieldComparison:
+    field: str
+    max_abs: float
+    max_rel: float
+    bitwise: bool
+
+
+@dataclass
+class ComparisonReport:
+    fields: dict
+    rtol: float
+
+    @property
+    def max_rel(self) -> float:
+        return max((f.max_rel for f in self.fields.values()), default=0.0)
+
+    @property
+    def bitwise(self) -> bool:
+        return all(f.bitwise for f in self.fields.values())
+
+    @property
+    def passed(self) -> bool:
+        if self.rtol == 0.0:
+            return self.bitwise
+        return self.max_rel <= self.rtol
+
+    def __str__(self):
+        lines = [f"{'field':<12} {'max_abs':>12} {'max_rel':>12} bitwise"]
+        for f in self.fields.values():
+            lines.append(f"{f.field:<12} {f.max_abs:>12.3e} {f.max_rel:>12.3e} {f.bitwise}")
+        lines.append(f"-> {'pass' if self.passed else 'FAIL'} (rtol={self.rtol:g})")
+        return "\n".join(lines)
+
+
+def _rel_diff(a, b):
+    a = np.asarray(_np(a), dtype=np.float64)
+    b = np.asarray(_np(b), dtype=np.float64)
+    diff = np.abs(a - b)
+    denom = np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))
+    return (float(diff.max()) if diff.size else 0.0,
+            float((diff / denom).max()) if diff.size else 0.0)
+
+
+def _equal(a, b):
+    if isinstance(a, torch.Tensor) and isinstance(b, torch.Tensor):
+        return bool(torch.equal(a, b))
+    return bool(np.array_equal(_np(a), _np(b)))
+
+
+def compare_runs(a: RunResult, b: RunResult, rtol: float = 0.0) -> ComparisonReport:
+    """Field-by-field max-abs / max-rel comparison; rtol=0 demands bitwise
+    equality (src/schedules.py:464-488)."""
+    if set(a.grads) != set(b.grads):
+        missing = set(a.grads) ^ set(b.grads)
+        raise ComparisonError(f"gradient key sets differ: {sorted(missing)[:5]}")
+    fields = {}
+    for name in ("loss", "m_out", "z_out", "dm", "dz"):
+        xa, xb = getattr(a, name), getattr(b, name)
+        if np.shape(_np(xa)) != np.shape(_np(xb)):
+            raise ComparisonError(f"{name} shapes differ")
+        ma, mr = _rel_diff(xa, xb)
+        fields[name] = FieldComparison(name, ma, mr, _equal(xa, xb))
+    wa = wr = 0.0
+    bit = True
+    for key in a.grads:
+        ma, mr = _rel_diff(a.grads[key], b.grads[key])
+        wa, wr = max(wa, ma), max(wr, mr)
+        bit = bit and _equal(a.grads[key], b.grads[key])
+    fields["grads"] = FieldComparison("grads", wa, wr, bit)
+    return ComparisonReport(fields, rtol)
+
+
+# ---------------------------------------------------------------------------
+# closed-form communication volume, BP and DP parts (src/schedules.py:515-572)
+# ---------------------------------------------------------------------------
+
+MSA_PARAM_TENSORS = 35
+PAIR_PARAM_TENSORS = 58
+
+
+def branch_param_elems(cfg: EvoConfig):
+    msa = sum(E.subop_grad_numel(n, cfg) for n in E.MSA_SUBOPS)
+    pair = sum(E.subop_grad_numel(n, cfg) for n in E.PAIR_SUBOPS)
+    return msa, pair
+
+
+def expected_comm_volume(cfg: EvoConfig, layout: ParallelLayout) -> dict:
+    """{(phase, kind): (count, elements)} for one step over the whole world,
+    using the reference's accounting (per-tensor parameter collectives).
+    This build buckets the parameter collectives per branch and block; the
+    element totals are identical."""
+    layout.validate_model(cfg)
+    Kb = cfg.n_blocks
+    M = cfg.s * cfg.r * cfg.c_m
+    Z = cfg.r * cfg.r * cfg.c_z
+    msa, pair = branch_param_elems(cfg)
+    msa *= Kb
+    pair *= Kb
+    out = {}
+
+    def bump(phase, kind, count, elements):
+        if count:
+            c0, e0 = out.get((phase, kind), (0, 0))
+            out[(phase, kind)] = (c0 + count, e0 + elements)
+
+    if layout.bp == 2:
+        g = layout.dp
+        bump("fwd", "broadcast", 2 * Kb * g, 2 * Kb * Z * g)
+        bump("bwd", "broadcast", (Kb + 1) * g, (Kb * Z + M) * g)
+        bump("bwd", "allreduce_sum", Kb * g, Kb * Z * g)
+        n = (MSA_PARAM_TENSORS + PAIR_PARAM_TENSORS) * Kb
+        bump("param", "broadcast", n * g, (msa + pair) * g)
+    if layout.dp > 1:
+        g = layout.bp
+        n = (MSA_PARAM_TENSORS + PAIR_PARAM_TENSORS) * Kb
+        bump("param", "allreduce_sum", n * g, (msa + pair) * g)
+    return out
