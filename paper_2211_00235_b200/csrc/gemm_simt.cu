@@ -8,6 +8,7 @@
 // result is deterministic and the fp32 error stays at BLAS level.
 #include "common.cuh"
 #include "gemm.cuh"
+#include "gemm_epi.cuh"
 
 namespace evo {
 
@@ -120,7 +121,7 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(SimtArgs a) {
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
         int64_t n = n0 + tx * 4 + j;
-        if (n < a.N) out[m * a.N + n] = a.alpha * acc[i][j];
+        if (n < a.N) out[m * a.N + n] = acc[i][j];
       }
     }
     return;
@@ -138,22 +139,6 @@ __global__ void __launch_bounds__(NT) gemm_simt_kernel(SimtArgs a) {
   }
 }
 
-template <typename TC>
-__global__ void splitk_reduce_kernel(SimtArgs a) {
-  const int64_t nbatch = a.B1 * a.B2;
-  const int64_t total = nbatch * a.M * a.N;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t n = e % a.N;
-    int64_t m = (e / a.N) % a.M;
-    int64_t bidx = e / (a.M * a.N);
-    float v = 0.f;
-    for (int s = 0; s < a.split_k; ++s) v += a.partial[(int64_t)s * total + e];
-    int64_t b1 = bidx / a.B2, b2 = bidx % a.B2;
-    epilogue_store<TC>(a, m, n, b1 * a.c_b1 + b2 * a.c_b2, v);
-  }
-}
-
 SimtArgs make_args(const evo_gemm_desc *d, int split, int64_t k_chunk) {
   SimtArgs a;
   a.M = d->M; a.N = d->N; a.K = d->K; a.B1 = d->B1; a.B2 = d->B2;
@@ -167,7 +152,33 @@ SimtArgs make_args(const evo_gemm_desc *d, int split, int64_t k_chunk) {
   return a;
 }
 
+__global__ void splitk_reduce_kernel(EpiArgs e, int64_t M, int64_t N, int64_t B2,
+                                     int64_t nbatch, int split, const float *partial) {
+  const int64_t total = nbatch * M * N;
+  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
+       idx += (int64_t)gridDim.x * blockDim.x) {
+    int64_t n = idx % N;
+    int64_t m = (idx / N) % M;
+    int64_t bidx = idx / (M * N);
+    float v = 0.f;
+    for (int s = 0; s < split; ++s) v += partial[(int64_t)s * total + idx];
+    int64_t b1 = bidx / B2, b2 = bidx % B2;
+    int64_t off = b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m) + e.cmap.col(n);
+    epi_store(e, off, epi_value(e, n, v));
+  }
+}
+
 }  // namespace
+
+int gemm_splitk_reduce(const evo_gemm_desc *d, int split, const float *partial,
+                       cudaStream_t st) {
+  const int64_t total = d->B1 * d->B2 * d->M * d->N;
+  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(epi_args_of(d), d->M, d->N, d->B2,
+                                               d->B1 * d->B2, split, partial);
+  EVO_LAUNCHED("splitk_reduce_kernel");
+  return EVO_OK;
+}
 
 size_t gemm_simt_workspace(const evo_gemm_desc *d) {
   if (d->split_k <= 1) return 0;
@@ -199,12 +210,7 @@ int gemm_simt(const evo_gemm_desc *d, cudaStream_t st) {
 #define LAUNCH(TA, TCT)                                                        \
   gemm_simt_kernel<TA, TCT><<<grid, NT, 0, st>>>(a);                          \
   EVO_LAUNCHED("gemm_simt_kernel");                                           \
-  if (split > 1) {                                                             \
-    int64_t total = d->B1 * d->B2 * d->M * d->N;                               \
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);        \
-    splitk_reduce_kernel<TCT><<<blocks, 256, 0, st>>>(a);                     \
-    EVO_LAUNCHED("splitk_reduce_kernel");                                     \
-  }
+  if (split > 1) return gemm_splitk_reduce(d, split, a.partial, st);
   if (d->dtype_ab == EVO_F32) {
     if (d->dtype_c == EVO_F32) { LAUNCH(float, float) } else { LAUNCH(float, bf16) }
   } else {

@@ -1,7 +1,521 @@
-// placeholder: the tcgen05/TMA GEMM lands in the next milestone
+// tcgen05 / TMA / TMEM GEMM for sm_100a (bf16 operands, fp32 accumulate).
+//
+// C(m,n) = epi(alpha * sum_k A(m,k) B(n,k)) for strided, batched operands
+// whose unit stride runs along K ("K-major") or along M/N ("MN-major").
+// Every projection, weight-gradient, outer-product-mean and triangle
+// contraction of the bf16 path goes through here (src/tensor.py:287-345
+// and the einsums of src/evoformer.py:343-392).
+//
+// Structure (one CTA per SM, persistent, warp-specialised, 192 threads):
+//   warp 0      TMA producer: 128B-swizzled A/B tiles -> smem ring
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer
+//   warps 2..5  epilogue: tcgen05.ld TMEM -> registers -> fused epilogue
+//               (bias / relu / sigmoid / residual / strided or two-level
+//               stores) -> global
+// Pipelines: smem full/empty mbarriers (TMA <-> MMA) and a double-buffered
+// TMEM accumulator with full/empty mbarriers (MMA <-> epilogue), so the
+// epilogue of tile i overlaps the main loop of tile i+1.
+#include <cuda.h>
+
 #include "gemm.cuh"
+#include "gemm_epi.cuh"
+
 namespace evo {
-bool gemm_tc_accepts(const evo_gemm_desc *) { return false; }
-size_t gemm_tc_workspace(const evo_gemm_desc *) { return 0; }
-int gemm_tc(const evo_gemm_desc *, cudaStream_t) { return EVO_EUNSUP; }
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
+constexpr int NTHREADS = 192;
+constexpr int SMEM_A = BM * BK * 2;  // 16 KiB
+
+struct TcParams {
+  int64_t M, N, K, B2, nbatch;
+  int c_aligned;
+  int64_t tiles_m, tiles_n, num_tiles;
+  int64_t k_chunk;
+  int split;
+  int a_kmajor, b_kmajor;
+  int a_bat1, a_bat2, b_bat1, b_bat2;  // batch coordinate used by the map?
+  uint32_t idesc;
+  EpiArgs epi;
+  float *partial;
+};
+
+// ------------------------------------------------------------------ PTX
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "LAB_WAIT:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@P1 bra DONE;\n"
+      "bra LAB_WAIT;\n"
+      "DONE:\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_4d(void *dst, const CUtensorMap *map, uint64_t *bar,
+                                            int c0, int c1, int c2, int c3) {
+  asm volatile(
+      "cp.async.bulk.tensor.4d.shared::cluster.global.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%3, %4, %5, %6}], [%2];" ::"r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(c0), "r"(c1), "r"(c2),
+      "r"(c3)
+      : "memory");
+}
+__device__ __forceinline__ void prefetch_map(const CUtensorMap *map) {
+  asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(map)) : "memory");
+}
+__device__ __forceinline__ void fence_before() {
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void fence_after() {
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void umma_commit(uint64_t *bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          smem_u32(bar))
+      : "memory");
+}
+__device__ __forceinline__ void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "setp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n"
+      "}\n" ::"r"(d_tmem),
+      "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate));
+}
+// 32 lanes x 32 consecutive fp32 columns per warp.
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+        "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+        "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+        "=r"(v[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// UMMA shared-memory descriptor, 128-byte swizzle (layout type 2),
+// version 1 (sm_100).  lbo/sbo in bytes.
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);
+  d |= (uint64_t)((lbo >> 4) & 0x3FFFu) << 16;
+  d |= (uint64_t)((sbo >> 4) & 0x3FFFu) << 32;
+  d |= (uint64_t)1 << 46;
+  d |= (uint64_t)2 << 61;
+  return d;
+}
+
+__device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_t &bidx,
+                                            int &sp, int64_t &mt, int64_t &nt) {
+  nt = t % p.tiles_n;
+  int64_t r = t / p.tiles_n;
+  mt = r % p.tiles_m;
+  r /= p.tiles_m;
+  sp = (int)(r % p.split);
+  bidx = r / p.split;
+}
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(NTHREADS, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const TcParams p) {
+  constexpr int SMEM_B = BN * BK * 2;
+  constexpr uint32_t STAGE_BYTES = SMEM_A + SMEM_B;
+  constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *smem = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t *sA = smem;
+  uint8_t *sB = smem + STAGES * SMEM_A;
+  uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * SMEM_B);
+  uint64_t *empty = full + STAGES;
+  uint64_t *tfull = empty + STAGES;
+  uint64_t *tempty = tfull + 2;
+  uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+
+  const int warp = threadIdx.x >> 5;
+  const int lane = threadIdx.x & 31;
+
+  if (warp == 0 && lane == 0) {
+    prefetch_map(&tmA);
+    prefetch_map(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      mbar_init(&tfull[a], 1);
+      mbar_init(&tempty[a], 4);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     smem_u32(tmem_slot)),
+                 "r"(TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem_base = *tmem_slot;
+
+  if (warp == 0) {
+    // ---------------------------------------------------------- producer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int64_t bidx, mt, nt;
+        int sp;
+        decode_tile(p, t, bidx, sp, mt, nt);
+        const int b1 = (int)(bidx / p.B2), b2 = (int)(bidx % p.B2);
+        const int ab1 = p.a_bat1 ? b1 : 0, ab2 = p.a_bat2 ? b2 : 0;
+        const int bb1 = p.b_bat1 ? b1 : 0, bb2 = p.b_bat2 ? b2 : 0;
+        const int64_t k_lo = sp * p.k_chunk;
+        const int64_t k_hi = min(p.K, k_lo + p.k_chunk);
+        const int m0 = (int)(mt * BM), n0 = (int)(nt * BN);
+        for (int64_t k = k_lo; k < k_hi; k += BK) {
+          mbar_wait(&empty[stage], phase ^ 1);
+          mbar_expect_tx(&full[stage], STAGE_BYTES);
+          uint8_t *a_dst = sA + stage * SMEM_A;
+          uint8_t *b_dst = sB + stage * SMEM_B;
+          if (p.a_kmajor) {
+            tma_load_4d(a_dst, &tmA, &full[stage], (int)k, m0, ab1, ab2);
+          } else {
+#pragma unroll
+            for (int h = 0; h < BM / 64; ++h)
+              tma_load_4d(a_dst + h * 8192, &tmA, &full[stage], m0 + 64 * h, (int)k, ab1, ab2);
+          }
+          if (p.b_kmajor) {
+            tma_load_4d(b_dst, &tmB, &full[stage], (int)k, n0, bb1, bb2);
+          } else {
+#pragma unroll
+            for (int h = 0; h < BN / 64; ++h)
+              tma_load_4d(b_dst + h * 8192, &tmB, &full[stage], n0 + 64 * h, (int)k, bb1, bb2);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------------------------------------------------- MMA issuer
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t aphase = 0;
+      const uint32_t a_lbo = p.a_kmajor ? 16u : 8192u;
+      const uint32_t b_lbo = p.b_kmajor ? 16u : 8192u;
+      const uint32_t a_kstep = p.a_kmajor ? 32u : 2048u;  // bytes per 16-wide K slice
+      const uint32_t b_kstep = p.b_kmajor ? 32u : 2048u;
+      for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+        int64_t bidx, mt, nt;
+        int sp;
+        decode_tile(p, t, bidx, sp, mt, nt);
+        const int64_t k_lo = sp * p.k_chunk;
+        const int64_t k_hi = min(p.K, k_lo + p.k_chunk);
+        mbar_wait(&tempty[acc], aphase ^ 1);
+        fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        uint32_t first = 1;
+        for (int64_t k = k_lo; k < k_hi; k += BK) {
+          mbar_wait(&full[stage], phase);
+          fence_after();
+          const uint32_t a_addr = smem_u32(sA + stage * SMEM_A);
+          const uint32_t b_addr = smem_u32(sB + stage * SMEM_B);
+#pragma unroll
+          for (int ks = 0; ks < BK / 16; ++ks) {
+            uint64_t ad = sw128_desc(a_addr + ks * a_kstep, a_lbo, 1024);
+            uint64_t bd = sw128_desc(b_addr + ks * b_kstep, b_lbo, 1024);
+            umma_bf16(d_tmem, ad, bd, p.idesc, first ? 0u : 1u);
+            first = 0;
+          }
+          umma_commit(&empty[stage]);
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        umma_commit(&tfull[acc]);
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+      }
+    }
+  } else {
+    // ---------------------------------------------------------- epilogue
+    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    int acc = 0;
+    uint32_t aphase = 0;
+    const EpiArgs &e = p.epi;
+    const bool vec_ok = (e.cmap.cdiv == 0 && e.cmap.cs == 1 && p.c_aligned);
+    for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
+      int64_t bidx, mt, nt;
+      int sp;
+      decode_tile(p, t, bidx, sp, mt, nt);
+      mbar_wait(&tfull[acc], aphase);
+      fence_after();
+      const int64_t m = mt * BM + q * 32 + lane;
+      const int64_t n0 = nt * BN;
+      const int64_t b1 = bidx / p.B2, b2 = bidx % p.B2;
+      const bool row_ok = m < p.M;
+      const int64_t rbase = row_ok ? (b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m)) : 0;
+#pragma unroll 1
+      for (int c0 = 0; c0 < BN; c0 += 32) {
+        uint32_t v[32];
+        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
+        if (!row_ok) continue;
+        const int64_t nb = n0 + c0;
+        if (p.split > 1) {
+          float *dst = p.partial + (((int64_t)sp * p.nbatch + bidx) * p.M + m) * p.N;
+          for (int j = 0; j < 32; ++j)
+            if (nb + j < p.N) dst[nb + j] = __uint_as_float(v[j]);
+          continue;
+        }
+        int64_t base = rbase + nb;  // valid when vec_ok
+        bool full_chunk = (nb + 32 <= p.N);
+        if (vec_ok && full_chunk && !e.accumulate && e.dtype_c == EVO_BF16 && (base & 7) == 0 &&
+            (!e.residual)) {
+          uint32_t packed[16];
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            float x0 = epi_value(e, nb + 2 * j, __uint_as_float(v[2 * j]));
+            float x1 = epi_value(e, nb + 2 * j + 1, __uint_as_float(v[2 * j + 1]));
+            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
+            packed[j] = *reinterpret_cast<uint32_t *>(&h2);
+          }
+          uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + base);
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
+                                packed[4 * j + 3]);
+        } else if (vec_ok && full_chunk && !e.accumulate && e.dtype_c == EVO_F32 &&
+                   (base & 3) == 0) {
+          float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(e.C) + base);
+          const float4 *res =
+              e.residual ? reinterpret_cast<const float4 *>(e.residual + base) : nullptr;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float4 o;
+            o.x = epi_value(e, nb + 4 * j + 0, __uint_as_float(v[4 * j + 0]));
+            o.y = epi_value(e, nb + 4 * j + 1, __uint_as_float(v[4 * j + 1]));
+            o.z = epi_value(e, nb + 4 * j + 2, __uint_as_float(v[4 * j + 2]));
+            o.w = epi_value(e, nb + 4 * j + 3, __uint_as_float(v[4 * j + 3]));
+            if (res) {
+              float4 r = res[j];
+              o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+            }
+            dst[j] = o;
+          }
+        } else {
+          for (int j = 0; j < 32; ++j) {
+            const int64_t n = nb + j;
+            if (n < p.N)
+              epi_store(e, rbase + e.cmap.col(n), epi_value(e, n, __uint_as_float(v[j])));
+          }
+        }
+      }
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&tempty[acc]);
+      acc ^= 1;
+      if (acc == 0) aphase ^= 1;
+    }
+  }
+
+  fence_before();
+  __syncthreads();
+  fence_after();
+  if (warp == 1) {
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem_base),
+                 "r"(TMEM_COLS));
+  }
+}
+
+// ------------------------------------------------------------------ host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *,
+                                  const cuuint64_t *, const cuuint64_t *, const cuuint32_t *,
+                                  const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn() {
+  static EncodeTiledFn fn = nullptr;
+  static bool tried = false;
+  if (!tried) {
+    tried = true;
+    void *ptr = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &ptr, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeTiledFn>(ptr);
+  }
+  return fn;
+}
+
+struct OperandPlan {
+  bool kmajor;
+  bool bat1, bat2;
+};
+
+// Which layout does a (rows x K) operand view have?  rows = M or N.
+bool plan_operand(const evo_mat &x, int64_t rows, int64_t K, OperandPlan &pl) {
+  if ((reinterpret_cast<uintptr_t>(x.ptr) & 15) != 0) return false;
+  auto ok_batch = [](int64_t s) { return s == 0 || (s % 8 == 0 && s > 0); };
+  if (!ok_batch(x.bs1) || !ok_batch(x.bs2)) return false;
+  if (x.cs == 1 && (x.rs % 8 == 0) && x.rs > 0 && (rows > 1 || true)) {
+    pl.kmajor = true;
+  } else if (x.rs == 1 && (x.cs % 8 == 0) && x.cs > 0) {
+    pl.kmajor = false;
+  } else {
+    return false;
+  }
+  pl.bat1 = x.bs1 != 0;
+  pl.bat2 = x.bs2 != 0;
+  (void)K;
+  return true;
+}
+
+bool make_map(CUtensorMap *map, const evo_mat &x, const OperandPlan &pl, int64_t rows,
+              int64_t K, int64_t B1, int64_t B2, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+  if (pl.kmajor) {
+    dims[0] = (cuuint64_t)K;
+    dims[1] = (cuuint64_t)rows;
+    strides[0] = (cuuint64_t)x.rs * 2;
+    box[0] = BK;
+    box[1] = (cuuint32_t)box_rows;
+  } else {
+    dims[0] = (cuuint64_t)rows;
+    dims[1] = (cuuint64_t)K;
+    strides[0] = (cuuint64_t)x.cs * 2;
+    box[0] = 64;
+    box[1] = BK;
+  }
+  const cuuint64_t span = strides[0] * dims[1];
+  const cuuint64_t dummy = ((span + 15) / 16) * 16;
+  dims[2] = pl.bat1 ? (cuuint64_t)B1 : 1;
+  dims[3] = pl.bat2 ? (cuuint64_t)B2 : 1;
+  strides[1] = pl.bat1 ? (cuuint64_t)x.bs1 * 2 : dummy;
+  strides[2] = pl.bat2 ? (cuuint64_t)x.bs2 * 2 : strides[1] * dims[2];
+  if (strides[2] == 0) strides[2] = 16;
+  box[2] = 1;
+  box[3] = 1;
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, x.ptr, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+int choose_bn(const evo_gemm_desc *d) { return d->N > 128 ? 256 : 128; }
+
+int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
+  int split = d->split_k < 1 ? 1 : d->split_k;
+  k_chunk = (d->K + split - 1) / split;
+  k_chunk = ((k_chunk + BK - 1) / BK) * BK;
+  if (k_chunk < BK) k_chunk = BK;
+  split = (int)((d->K + k_chunk - 1) / k_chunk);
+  (void)BN;
+  return split < 1 ? 1 : split;
+}
+
+template <int BN, int STAGES>
+int launch(const evo_gemm_desc *d, cudaStream_t st) {
+  OperandPlan pa, pb;
+  plan_operand(d->A, d->M, d->K, pa);
+  plan_operand(d->B, d->N, d->K, pb);
+  CUtensorMap ma, mb;
+  if (!make_map(&ma, d->A, pa, d->M, d->K, d->B1, d->B2, BM) ||
+      !make_map(&mb, d->B, pb, d->N, d->K, d->B1, d->B2, BN))
+    return EVO_EUNSUP;
+  TcParams p;
+  p.M = d->M; p.N = d->N; p.K = d->K; p.B2 = d->B2; p.nbatch = d->B1 * d->B2;
+  p.c_aligned = (reinterpret_cast<uintptr_t>(d->C.ptr) & 15) == 0 &&
+                (!d->residual || (reinterpret_cast<uintptr_t>(d->residual) & 15) == 0);
+  p.tiles_m = (d->M + BM - 1) / BM;
+  p.tiles_n = (d->N + BN - 1) / BN;
+  p.split = choose_split(d, BN, p.k_chunk);
+  p.num_tiles = p.tiles_m * p.tiles_n * p.split * d->B1 * d->B2;
+  p.a_kmajor = pa.kmajor; p.b_kmajor = pb.kmajor;
+  p.a_bat1 = pa.bat1; p.a_bat2 = pa.bat2; p.b_bat1 = pb.bat1; p.b_bat2 = pb.bat2;
+  p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((pa.kmajor ? 0u : 1u) << 15) |
+            ((pb.kmajor ? 0u : 1u) << 16) | ((uint32_t)(BN >> 3) << 17) |
+            ((uint32_t)(BM >> 4) << 24);
+  p.epi = epi_args_of(d);
+  p.partial = reinterpret_cast<float *>(d->workspace);
+  if (p.split > 1) {
+    size_t need = (size_t)p.split * d->B1 * d->B2 * d->M * d->N * sizeof(float);
+    EVO_REQUIRE(d->workspace && d->workspace_bytes >= need, EVO_EARG,
+                "evo_gemm(tc): split=%d needs %zu workspace bytes", p.split, need);
+  }
+  const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) + 256;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set = true;
+  }
+  int64_t grid = std::min<int64_t>(p.num_tiles, (int64_t)num_sms());
+  gemm_tc_kernel<BN, STAGES><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, p);
+  EVO_LAUNCHED("gemm_tc_kernel");
+  if (p.split > 1) return gemm_splitk_reduce(d, p.split, p.partial, st);
+  return EVO_OK;
+}
+
+}  // namespace
+
+bool gemm_tc_accepts(const evo_gemm_desc *d) {
+  if (d->dtype_ab != EVO_BF16 || d->K < 1 || d->M < 1 || d->N < 1) return false;
+  if (d->B1 * d->B2 > 65535 || d->K > (1ll << 31) || d->M > (1ll << 31) || d->N > (1ll << 31))
+    return false;
+  if (!encode_fn()) return false;
+  OperandPlan pa, pb;
+  return plan_operand(d->A, d->M, d->K, pa) && plan_operand(d->B, d->N, d->K, pb);
+}
+
+size_t gemm_tc_workspace(const evo_gemm_desc *d) {
+  int64_t kc;
+  int split = choose_split(d, choose_bn(d), kc);
+  if (split <= 1) return 0;
+  return (size_t)split * d->B1 * d->B2 * d->M * d->N * sizeof(float);
+}
+
+int gemm_tc(const evo_gemm_desc *d, cudaStream_t st) {
+  if (!gemm_tc_accepts(d)) return EVO_EUNSUP;
+  if (choose_bn(d) == 256) return launch<256, 4>(d, st);
+  return launch<128, 6>(d, st);
+}
+
 }  // namespace evo

@@ -1,0 +1,130 @@
+"""The strided batched GEMM entry point (evo_gemm) against a plain PyTorch
+fp32 reference of the same op, on both the tcgen05/TMA kernel and the
+SIMT kernel: every operand-major combination, batching (incl. broadcast
+operands), split-K, every epilogue, two-level output maps, ragged sizes.
+"""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2211_00235_b200 import kernels
+    return kernels
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def make_operand(rows, k, kmajor, batch=1, dtype=torch.bfloat16):
+    """Returns (storage tensor, logical [batch, rows, k] fp32 view, rs, cs, bs)."""
+    if kmajor:
+        t = torch.randn(batch, rows, k, device="cuda").to(dtype)
+        return t, t.float(), k, 1, rows * k
+    t = torch.randn(batch, k, rows, device="cuda").to(dtype)
+    return t, t.float().transpose(1, 2), 1, rows, rows * k
+
+
+@pytest.mark.parametrize("a_k,b_k", [(True, True), (True, False), (False, True),
+                                     (False, False)])
+@pytest.mark.parametrize("M,N,Kd", [(128, 128, 64), (200, 72, 100), (300, 520, 256),
+                                    (64, 256, 1000)])
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_gemm_majors_and_ragged(K, a_k, b_k, M, N, Kd, force_simt):
+    A, Af, ars, acs, _ = make_operand(M, Kd, a_k)
+    B, Bf, brs, bcs, _ = make_operand(N, Kd, b_k)
+    C = torch.empty(M, N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd,
+           force_simt=force_simt)
+    want = Af[0] @ Bf[0].T
+    assert rel(C, want) < 1e-5
+
+
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_gemm_batched_broadcast_split_k(K, force_simt):
+    M, N, Kd, nb = 96, 160, 4096, 3
+    A, Af, ars, acs, _ = make_operand(M, Kd, False, 1)      # broadcast over batch
+    B, Bf, brs, bcs, bbs = make_operand(N, Kd, True, nb)
+    C = torch.zeros(nb, M, N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs, bs1=0), K.Mat(B, brs, bcs, bs1=bbs), K.Mat(C, N, 1, bs1=M * N),
+           M, N, Kd, B1=nb, split_k=8, force_simt=force_simt)
+    want = torch.stack([Af[0] @ Bf[i].T for i in range(nb)])
+    assert rel(C, want) < 1e-5
+
+
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_gemm_epilogues_bf16_out(K, force_simt):
+    M, N, Kd = 256, 384, 128
+    A, Af, ars, acs, _ = make_operand(M, Kd, True)
+    B, Bf, brs, bcs, _ = make_operand(N, Kd, False)
+    bias = torch.randn(N, device="cuda")
+    raw = Af[0] @ Bf[0].T * 0.5 + bias
+    from paper_2211_00235_b200._native import EPI_RELU, EPI_SIGMOID_FROM
+    C = torch.empty(M, N, device="cuda", dtype=torch.bfloat16)
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, alpha=0.5,
+           bias=bias, epi=EPI_RELU, force_simt=force_simt)
+    assert rel(C.float(), torch.relu(raw)) < 5e-3
+    col0 = 200
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, alpha=0.5,
+           bias=bias, epi=EPI_SIGMOID_FROM, col0=col0, force_simt=force_simt)
+    want = raw.clone()
+    want[:, col0:] = torch.sigmoid(raw[:, col0:])
+    assert rel(C.float(), want) < 5e-3
+
+
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_gemm_residual_accumulate_and_offsets(K, force_simt):
+    M, N, Kd = 130, 256, 192
+    A, Af, ars, acs, _ = make_operand(M, Kd, True)
+    B, Bf, brs, bcs, _ = make_operand(N, Kd, True)
+    R = torch.randn(M, N, device="cuda")
+    C = torch.empty(M, N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, residual=R,
+           force_simt=force_simt)
+    want = Af[0] @ Bf[0].T + R
+    assert rel(C, want) < 1e-5
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, accumulate=True,
+           force_simt=force_simt)
+    assert rel(C, want + Af[0] @ Bf[0].T) < 1e-5
+    # column-offset output into a wider buffer (packed projection layout)
+    W = torch.zeros(M, 3 * N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(W, 3 * N, 1, off=N), M, N, Kd,
+           force_simt=force_simt)
+    assert rel(W[:, N:2 * N], Af[0] @ Bf[0].T) < 1e-5
+    assert float(W[:, :N].abs().max()) == 0.0 and float(W[:, 2 * N:].abs().max()) == 0.0
+
+
+@pytest.mark.parametrize("force_simt", [False, True])
+def test_gemm_two_level_output_map(K, force_simt):
+    """The outer-product-mean store: m=(i,p), n=(j,q) -> o[i,j,p,q]."""
+    r, c, s = 24, 16, 40
+    a = torch.randn(s, r * c, device="cuda").to(torch.bfloat16)
+    b = torch.randn(s, r * c, device="cuda").to(torch.bfloat16)
+    o = torch.empty(r, r, c, c, device="cuda")
+    rc = r * c
+    K.gemm(K.Mat(a, 1, rc), K.Mat(b, 1, rc),
+           K.Mat(o, r * c * c, c * c, rdiv=c, rs0=c, cdiv=c, cs0=1), rc, rc, s, alpha=1.0 / s,
+           force_simt=force_simt)
+    want = torch.einsum("sip,sjq->ijpq", a.float().view(s, r, c), b.float().view(s, r, c)) / s
+    assert rel(o, want) < 1e-5
+
+
+def test_gemm_tc_path_is_taken(K):
+    from paper_2211_00235_b200 import _native
+    assert _native.lib().evo_tc_available() == 1
+    A = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
+    B = torch.randn(256, 256, device="cuda").to(torch.bfloat16)
+    C = torch.empty(512, 256, device="cuda")
+    prof = []
+    K.PROFILE = prof
+    try:
+        K.gemm(K.Mat(A, 256, 1), K.Mat(B, 256, 1), K.Mat(C, 256, 1), 512, 256, 256)
+    finally:
+        K.PROFILE = None
+    torch.cuda.synchronize()
+    assert rel(C, A.float() @ B.float().T) < 1e-5
