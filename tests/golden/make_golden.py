@@ -9,7 +9,8 @@ Outputs (committed, small):
   step_<cfg>.npz   run_single(cfg, init_params(cfg, 32), seed=32): m_out,
                    z_out, loss, dm, dz and every parameter gradient
                    (keys "grad:<name>"), plus the tape madds of one block
-                   forward ("madds_block").  run_bp is asserted bitwise
+                   forward ("madds_block") and the reference's own
+                   float32-vs-float64 rel-L2 per field ("f32err:<field>").  run_bp is asserted bitwise
                    equal to run_single before saving.
   subops_toy.npz   every sub-op of block 0 at the toy dims: forward delta
                    and the VJP of a seeded random cotangent R with respect
@@ -58,6 +59,24 @@ def main():
                    dm=a.dm, dz=a.dz, madds_block=np.int64(g.madds))
         for name, arr in a.grads.items():
             out[f"grad:{name}"] = arr
+        # the reference's OWN float32 deviation from its float64 run, per
+        # field: the floor any fp32 implementation is measured against
+        f = run_single(cfg, E.init_params(cfg, 32, dtype=np.float32), seed=32)
+        m_in, z_in = E.seeded_inputs(cfg, 32)
+
+        def rl(x, y):
+            x = np.asarray(x, np.float64)
+            y = np.asarray(y, np.float64)
+            return np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
+
+        m32 = m_in.astype(np.float32).astype(np.float64)
+        z32 = z_in.astype(np.float32).astype(np.float64)
+        out["f32err:m_delta"] = rl(f.m_out.astype(np.float64) - m32, a.m_out - m_in)
+        out["f32err:z_delta"] = rl(f.z_out.astype(np.float64) - z32, a.z_out - z_in)
+        out["f32err:dm"] = rl(f.dm, a.dm)
+        out["f32err:dz"] = rl(f.dz, a.dz)
+        for name in a.grads:
+            out[f"f32err:grad:{name}"] = rl(f.grads[name], a.grads[name])
         np.savez_compressed(os.path.join(HERE, f"step_{tag}.npz"), **out)
         print(tag, "saved", len(out), "arrays; madds/block", g.madds)
 

@@ -79,4 +79,16 @@ def step_errors(res, want, m_in, z_in, bar=None):
 
 def golden_as_want(gold):
     return dict(m_out=gold["m_out"], z_out=gold["z_out"], dm=gold["dm"], dz=gold["dz"],
-                grads={k[5:]: gold[k] for k in gold.files if k.startswith("grad:")})
+                grads={k[5:]: gold[k] for k in gold.files if k.startswith("grad:")},
+                f32err={k[7:]: float(gold[k]) for k in gold.files if k.startswith("f32err:")})
+
+
+def normalise_by_reference_f32(errs, want, bar):
+    """Hold each field to max(bar, 2 x the reference's own float32 error on
+    that field): errs[k] *= bar / allow, so one threshold `bar` applies."""
+    ref = want.get("f32err", {})
+    for k in list(errs):
+        e = ref.get(k)
+        if e is not None:
+            errs[k] *= bar / max(bar, 2.0 * e)
+    return errs

@@ -10,7 +10,8 @@ import numpy as np
 import pytest
 import torch
 
-from helpers import CONFIGS, golden_as_want, load_golden, rel_l2, step_errors, to_np
+from helpers import (CONFIGS, golden_as_want, load_golden, normalise_by_reference_f32,
+                     rel_l2, step_errors, to_np)
 
 pytestmark = pytest.mark.gpu
 
@@ -37,7 +38,9 @@ def test_step_fp32_matches_reference_golden(pkg, tag):
     res = pkg.run_single(cfg, store, seed=32, precision="fp32")
     m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
     gold = load_golden(tag)
-    errs = step_errors(res, golden_as_want(gold), m_in, z_in, bar=FP32_TOL)
+    want = golden_as_want(gold)
+    errs = normalise_by_reference_f32(step_errors(res, want, m_in, z_in, bar=FP32_TOL), want,
+                                      FP32_TOL)
     k, v = _worst(errs)
     assert v <= FP32_TOL, f"{tag}: worst {k} rel-L2 {v:.3e}"
     assert abs(res.loss - float(gold["loss"])) <= 1e-5 * abs(float(gold["loss"]))
