@@ -1,8 +1,810 @@
-// placeholder: the tensor-core attention lands in a later milestone
+// Fused gated attention with pair bias on 5th-gen tensor cores (sm_100a).
+//
+// Same contract as attention_simt.cu (src/evoformer.py:268-286): per
+// (batch row b, head h) Q,K,V [L, D] live in the packed projection buffer,
+// O = softmax(scale*QK^T + bias[h]) V, GM = G*O, lse saved.  L <= 256 keys
+// are resident, so the softmax is exact (one pass over TMEM for the max,
+// one for exp/sum); logits never leave the SM.
+//
+// Forward (grid: q-tiles x H x nb, 128 threads, thread t owns query row t):
+//   TMA: Q tile [128 x D], K, V [Lp x D] (swizzle = 2D bytes)
+//   tcgen05.mma  S = Q K^T        -> TMEM [128 x Lp] fp32
+//   softmax rows in registers (bias added from L2), P (bf16) -> smem
+//   tcgen05.mma  O = P V          -> TMEM [128 x D]  (V as MN-major B)
+//   epilogue: O/sum, gate, store o, gm, lse
+// Backward (deterministic, no atomics):
+//   prep:  dO = dGM*G, dGpre = dGM*O*G*(1-G), Dq = rowsum(dO*O)
+//   dq kernel (grid q-tiles x H x chunks; loops the chunk's batch rows):
+//     S = QK^T, P = exp(S + bias - lse) -> smem;  dP = dO V^T;
+//     dS = P*(dP - Dq) -> smem; dbias partial += dS (TMEM accumulator);
+//     dq = scale * dS K
+//   dkv kernel (grid k-tiles x H x nb): S^T = K Q^T, dP^T = V dO^T,
+//     P^T, dS^T -> smem; dv = P^T dO; dk = scale * dS^T Q
+//   dbias = ordered sum of the chunk partials.
 #include "common.cuh"
+#include "tc_common.cuh"
+
 namespace evo {
-bool attention_tc_accepts(const evo_attn_desc *) { return false; }
-size_t attention_tc_bwd_ws(const evo_attn_desc *) { return 0; }
-int attention_tc_fwd(const evo_attn_desc *, cudaStream_t) { return EVO_EUNSUP; }
-int attention_tc_bwd(const evo_attn_desc *, cudaStream_t) { return EVO_EUNSUP; }
+
+int reduce_lead(int, int64_t, int64_t, int64_t, const void *, float *, int64_t, int64_t, int,
+                cudaStream_t);
+
+namespace {
+using namespace tc;
+
+constexpr float LOG2E = 1.4426950408889634f;
+constexpr int QT = 128;      // query (or key) rows per CTA = UMMA M
+constexpr int PBYTES = 128 * 256 * 2;  // P / dS staging, [128 x 256] bf16 SW128
+
+struct AttnTcArgs {
+  int64_t nb;
+  int H, L, Lp, D;
+  float scale;
+  const bf16 *g;
+  int64_t sb, sl;
+  bf16 *o, *gm;
+  int64_t o_sb, o_sl;
+  const float *bias;
+  int64_t bh, bq, bk;
+  float *lse;
+  // backward
+  const bf16 *dO;   // prep output, o's strides
+  const float *Dq;  // [nb, H, L]
+  bf16 *dq, *dk, *dv;  // proj-gradient buffer (q's strides)
+  float *dbias_part;
+  int64_t chunk;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+        "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+        "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Load D consecutive fp32 TMEM columns of this thread's lane into out[].
+template <int D>
+__device__ __forceinline__ void tmem_ld_row(uint32_t taddr, float (&out)[D]) {
+  if constexpr (D == 16) {
+    uint32_t v[16];
+    tmem_ld16(taddr, v);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = __uint_as_float(v[j]);
+  } else {
+#pragma unroll
+    for (int c = 0; c < D; c += 32) {
+      uint32_t v[32];
+      tmem_ld32(taddr + c, v);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) out[c + j] = __uint_as_float(v[j]);
+    }
+  }
+}
+
+// swizzle code / atom for a [rows x D] bf16 tile with 2D-byte rows
+template <int D> struct Sw {
+  static constexpr uint32_t bytes = 2 * D;                      // row pitch
+  static constexpr uint32_t layout = D == 64 ? 2 : (D == 32 ? 4 : 6);
+  static constexpr uint32_t sbo = 8 * bytes;                    // 8-row group
+};
+
+// K-major descriptor of a [rows x D] tile, K slice ks (16 wide).
+template <int D>
+__device__ __forceinline__ uint64_t desc_kmajor_tile(uint32_t base, int ks) {
+  return umma_desc(base + ks * 32, 16, Sw<D>::sbo, Sw<D>::layout);
+}
+// MN-major descriptor of a [keys x D] tile used as B(n=d, k=key); K slice ks.
+template <int D>
+__device__ __forceinline__ uint64_t desc_mnmajor_tile(uint32_t base, int ks) {
+  // N = D is exactly one swizzle-atom wide, so LBO (MN-chunk stride) is unused
+  return umma_desc(base + ks * 16 * Sw<D>::bytes, 16, Sw<D>::sbo, Sw<D>::layout);
+}
+// K-major SW128 descriptor of the [128 x 256] P/dS staging buffer, K slice ks.
+__device__ __forceinline__ uint64_t desc_pbuf(uint32_t base, int ks) {
+  return umma_desc(base + (ks >> 2) * 16384 + (ks & 3) * 32, 16, 1024, 2);
+}
+// Write 8 bf16 (one 16-byte chunk: keys k8*8 .. k8*8+7) of row `row` into
+// the swizzled P buffer.
+__device__ __forceinline__ void pbuf_store8(uint8_t *pbuf, int row, int k8, uint4 val) {
+  const int atom = k8 >> 3, chunk = k8 & 7;
+  uint8_t *dst = pbuf + atom * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4);
+  *reinterpret_cast<uint4 *>(dst) = val;
+}
+__device__ __forceinline__ uint4 pbuf_load8(const uint8_t *pbuf, int row, int k8) {
+  const int atom = k8 >> 3, chunk = k8 & 7;
+  return *reinterpret_cast<const uint4 *>(pbuf + atom * 16384 + row * 128 +
+                                          ((chunk ^ (row & 7)) << 4));
+}
+__device__ __forceinline__ uint32_t pack2(float a, float b) {
+  __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<uint32_t *>(&h);
+}
+__device__ __forceinline__ float2 unpack2(uint32_t u) {
+  __nv_bfloat162 h = *reinterpret_cast<__nv_bfloat162 *>(&u);
+  return __bfloat1622float2(h);
+}
+
+__device__ __forceinline__ float bias_at(const AttnTcArgs &a, int h, int q, int k) {
+  return a.bias[(int64_t)h * a.bh + (int64_t)q * a.bq + (int64_t)k * a.bk];
+}
+
+// ====================================================================== fwd
+template <int D>
+__global__ void __launch_bounds__(128)
+attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                   const __grid_constant__ CUtensorMap mV, const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;       // 128-row tile bytes
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;      // up to 256 rows
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~uintptr_t(1023));
+  uint8_t *sP = sm;                  // 64 KiB
+  uint8_t *sQ = sP + PBYTES;
+  uint8_t *sK = sQ + TILE;
+  uint8_t *sV = sK + FULL;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+
+  const int t = threadIdx.x, warp = t >> 5;
+  const int q0 = blockIdx.x * QT, h = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int L = a.L, Lp = a.Lp;
+  const int q = q0 + t;
+
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 256);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+
+  if (t == 0) {
+    mbar_expect_tx(&bars[0], TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
+    tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
+    tma_load_4d(sK, &mK, &bars[0], 0, 0, (int)b, h);
+    tma_load_4d(sV, &mV, &bars[0], 0, 0, (int)b, h);
+    mbar_wait(&bars[0], 0);
+    fence_after();
+    const uint32_t idesc = idesc_bf16(128, Lp, false, false);
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sQ), ks), desc_kmajor_tile<D>(smem_u32(sK), ks),
+                idesc, ks > 0);
+    umma_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 0);
+  fence_after();
+
+  // pass 1: s = scale*acc + bias (masked keys -> -inf), row max; write back
+  float mx = -INFINITY;
+  const bool qv = q < L;
+  for (int c0 = 0; c0 < Lp; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(lane_addr + c0, v);
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int k = c0 + j;
+      float s = -INFINITY;
+      if (k < L) {
+        s = __uint_as_float(v[j]) * a.scale;
+        if (a.bias && qv) s += bias_at(a, h, q, k);
+      }
+      mx = fmaxf(mx, s);
+      v[j] = __float_as_uint(s);
+    }
+    tmem_st32(lane_addr + c0, v);
+  }
+  tmem_st_wait();
+  // pass 2: p = exp(s - max), row sum, P (bf16) -> smem
+  float sum = 0.f;
+  const float mxl = mx * LOG2E;
+  for (int c0 = 0; c0 < Lp; c0 += 32) {
+    uint32_t v[32];
+    tmem_ld32(lane_addr + c0, v);
+    uint32_t pk[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      float p0 = ex2(__uint_as_float(v[2 * j]) * LOG2E - mxl);
+      float p1 = ex2(__uint_as_float(v[2 * j + 1]) * LOG2E - mxl);
+      sum += p0 + p1;
+      pk[j] = pack2(p0, p1);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      pbuf_store8(sP, t, (c0 >> 3) + c, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
+                                                   pk[4 * c + 3]));
+  }
+  fence_proxy_async_smem();
+  fence_before();
+  __syncthreads();
+  if (t == 0) {
+    fence_after();
+    const uint32_t idesc = idesc_bf16(128, D, false, true);
+    for (int ks = 0; ks < Lp / 16; ++ks)
+      umma_bf16(tmem, desc_pbuf(smem_u32(sP), ks), desc_mnmajor_tile<D>(smem_u32(sV), ks), idesc,
+                ks > 0);
+    umma_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 1);
+  fence_after();
+  float o[D];
+  tmem_ld_row<D>(lane_addr, o);
+  if (qv) {
+    const float inv = 1.f / sum;
+    const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D;
+    const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D;
+#pragma unroll
+    for (int d8 = 0; d8 < D; d8 += 8) {
+      uint4 graw = *reinterpret_cast<const uint4 *>(gp + d8);
+      const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
+      uint32_t ov[4], gv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float o0 = o[d8 + 2 * j] * inv, o1 = o[d8 + 2 * j + 1] * inv;
+        float2 g2 = unpack2(gw[j]);
+        ov[j] = pack2(o0, o1);
+        gv[j] = pack2(g2.x * o0, g2.y * o1);
+      }
+      *reinterpret_cast<uint4 *>(a.o + ooff + d8) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+      *reinterpret_cast<uint4 *>(a.gm + ooff + d8) = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+    }
+    a.lse[(b * a.H + h) * (int64_t)L + q] = mx + logf(sum);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 256);
+}
+
+// ===================================================================== prep
+// dO = dGM*G (bf16, o's layout), dGpre = dGM*O*G*(1-G) (proj gate cols),
+// Dq[b,h,q] = sum_d dO*O.  One thread per (row(b,l), head).
+template <int D>
+__global__ void attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm, bf16 *dO_out,
+                                     bf16 *dgpre, float *Dq) {
+  const int64_t total = a.nb * (int64_t)a.L * a.H;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int h = (int)(e % a.H);
+    const int64_t r = e / a.H;
+    const int l = (int)(r % a.L);
+    const int64_t b = r / a.L;
+    const int64_t ooff = b * a.o_sb + (int64_t)l * a.o_sl + h * D;
+    const int64_t goff = b * a.sb + (int64_t)l * a.sl + h * D;
+    float acc = 0.f;
+#pragma unroll
+    for (int d8 = 0; d8 < D; d8 += 8) {
+      uint4 graw = *reinterpret_cast<const uint4 *>(a.g + goff + d8);
+      uint4 oraw = *reinterpret_cast<const uint4 *>(a.o + ooff + d8);
+      uint4 draw = *reinterpret_cast<const uint4 *>(dgm + ooff + d8);
+      const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
+      const uint32_t *ow = reinterpret_cast<const uint32_t *>(&oraw);
+      const uint32_t *dw = reinterpret_cast<const uint32_t *>(&draw);
+      uint32_t dov[4], dgv[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 g2 = unpack2(gw[j]), o2 = unpack2(ow[j]), d2 = unpack2(dw[j]);
+        float do0 = d2.x * g2.x, do1 = d2.y * g2.y;
+        acc += do0 * o2.x + do1 * o2.y;
+        dov[j] = pack2(do0, do1);
+        dgv[j] = pack2(d2.x * o2.x * g2.x * (1.f - g2.x), d2.y * o2.y * g2.y * (1.f - g2.y));
+      }
+      *reinterpret_cast<uint4 *>(dO_out + ooff + d8) = make_uint4(dov[0], dov[1], dov[2], dov[3]);
+      *reinterpret_cast<uint4 *>(dgpre + goff + d8) = make_uint4(dgv[0], dgv[1], dgv[2], dgv[3]);
+    }
+    Dq[(b * a.H + h) * (int64_t)a.L + l] = acc;
+  }
+}
+
+// ======================================================================= dq
+template <int D>
+__global__ void __launch_bounds__(128)
+attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                      const __grid_constant__ CUtensorMap mV,
+                      const __grid_constant__ CUtensorMap mdO, const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~uintptr_t(1023));
+  uint8_t *sP = sm;  // P, then dS (bf16, SW128 K-major [128 x 256])
+  uint8_t *sQ = sP + PBYTES;
+  uint8_t *sdO = sQ + TILE;
+  uint8_t *sK = sdO + TILE;
+  uint8_t *sV = sK + FULL;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);  // 0: tma, 1: mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+
+  const int t = threadIdx.x, warp = t >> 5;
+  const int q0 = blockIdx.x * QT, h = blockIdx.y;
+  const int L = a.L, Lp = a.Lp;
+  const int q = q0 + t;
+  const bool qv = q < L;
+  const bool want_bias = a.dbias_part != nullptr;
+
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t acc_db = lane_addr;        // cols [0, 256): dbias accumulator
+  const uint32_t work = lane_addr + 256;    // cols [256, 512): S -> dP -> dq
+  if (want_bias) {
+    uint32_t z[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) z[j] = 0u;
+    for (int c0 = 0; c0 < Lp; c0 += 32) tmem_st32(acc_db + c0, z);
+    tmem_st_wait();
+  }
+  uint32_t tphase = 0, mphase = 0;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
+  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+
+  for (int64_t b = b_lo; b < b_hi; ++b) {
+    if (t == 0) {
+      mbar_expect_tx(&bars[0], 2 * TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
+      tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
+      tma_load_4d(sdO, &mdO, &bars[0], 0, q0, (int)b, h);
+      tma_load_4d(sK, &mK, &bars[0], 0, 0, (int)b, h);
+      tma_load_4d(sV, &mV, &bars[0], 0, 0, (int)b, h);
+      mbar_wait(&bars[0], tphase);
+      fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sQ), ks),
+                  desc_kmajor_tile<D>(smem_u32(sK), ks), idesc_s, ks > 0);
+      umma_commit(&bars[1]);
+    }
+    tphase ^= 1;
+    mbar_wait(&bars[1], mphase);
+    mphase ^= 1;
+    fence_after();
+    const float lse_l2 = qv ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E : 0.f;
+    const float Dq = qv ? a.Dq[(b * a.H + h) * (int64_t)L + q] : 0.f;
+    // P = exp(scale*S + bias - lse) -> smem (bf16)
+    for (int c0 = 0; c0 < Lp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(work + c0, v);
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 32; j += 2) {
+        float p[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const int k = c0 + j + u;
+          float s = __uint_as_float(v[j + u]) * a.scale;
+          if (a.bias && qv && k < L) s += bias_at(a, h, q, k);
+          p[u] = (qv && k < L) ? ex2(s * LOG2E - lse_l2) : 0.f;
+        }
+        pk[j >> 1] = pack2(p[0], p[1]);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        pbuf_store8(sP, t, (c0 >> 3) + c,
+                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+    }
+    // dP = dO V^T  -> work cols (S consumed: all threads passed tcgen05.ld)
+    fence_before();
+    __syncthreads();
+    if (t == 0) {
+      fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sdO), ks),
+                  desc_kmajor_tile<D>(smem_u32(sV), ks), idesc_s, ks > 0);
+      umma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], mphase);
+    mphase ^= 1;
+    fence_after();
+    // dS = P * (dP - Dq); dbias += dS; dS (bf16) overwrites P in smem
+    for (int c0 = 0; c0 < Lp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(work + c0, v);
+      uint32_t acc[32];
+      if (want_bias) {
+        asm volatile("" ::: "memory");
+        tmem_ld32(acc_db + c0, acc);
+      }
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint4 praw = pbuf_load8(sP, t, (c0 >> 3) + c);
+        const uint32_t *pw = reinterpret_cast<const uint32_t *>(&praw);
+        uint32_t dsv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float2 p2 = unpack2(pw[j]);
+          const int i0 = 8 * c + 2 * j;
+          float ds0 = p2.x * (__uint_as_float(v[i0]) - Dq);
+          float ds1 = p2.y * (__uint_as_float(v[i0 + 1]) - Dq);
+          if (want_bias) {
+            acc[i0] = __float_as_uint(__uint_as_float(acc[i0]) + ds0);
+            acc[i0 + 1] = __float_as_uint(__uint_as_float(acc[i0 + 1]) + ds1);
+          }
+          dsv[j] = pack2(ds0, ds1);
+        }
+        pbuf_store8(sP, t, (c0 >> 3) + c, make_uint4(dsv[0], dsv[1], dsv[2], dsv[3]));
+      }
+      if (want_bias) tmem_st32(acc_db + c0, acc);
+    }
+    if (want_bias) tmem_st_wait();
+    fence_proxy_async_smem();
+    fence_before();
+    __syncthreads();
+    if (t == 0) {
+      fence_after();
+      for (int ks = 0; ks < Lp / 16; ++ks)
+        umma_bf16(tmem + 256, desc_pbuf(smem_u32(sP), ks), desc_mnmajor_tile<D>(smem_u32(sK), ks),
+                  idesc_o, ks > 0);
+      umma_commit(&bars[1]);
+    }
+    mbar_wait(&bars[1], mphase);
+    mphase ^= 1;
+    fence_after();
+    float dq[D];
+    tmem_ld_row<D>(work, dq);
+    if (qv) {
+      bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D;
+#pragma unroll
+      for (int d8 = 0; d8 < D; d8 += 8) {
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+          w[j] = pack2(dq[d8 + 2 * j] * a.scale, dq[d8 + 2 * j + 1] * a.scale);
+        *reinterpret_cast<uint4 *>(dst + d8) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+    }
+    fence_before();
+    __syncthreads();  // smem tiles / TMEM work cols free for the next row
+    fence_after();
+  }
+  if (want_bias) {
+    float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L;
+    for (int c0 = 0; c0 < Lp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(acc_db + c0, v);  // warp-collective: every lane loads
+      if (!qv) continue;
+      for (int j = 0; j < 32; ++j) {
+        const int k = c0 + j;
+        if (k < L)
+          dst[(int64_t)h * a.bh + (int64_t)q * a.bq + (int64_t)k * a.bk] = __uint_as_float(v[j]);
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ====================================================================== dkv
+template <int D>
+__global__ void __launch_bounds__(128)
+attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_constant__ CUtensorMap mVt,
+                       const __grid_constant__ CUtensorMap mQa,
+                       const __grid_constant__ CUtensorMap mdOa, const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                            ~uintptr_t(1023));
+  uint8_t *sPt = sm;              // P^T  [128 keys x 256 queries] bf16 SW128
+  uint8_t *sdSt = sPt + PBYTES;   // dS^T
+  uint8_t *sK = sdSt + PBYTES;
+  uint8_t *sV = sK + TILE;
+  uint8_t *sQ = sV + TILE;
+  uint8_t *sdO = sQ + FULL;
+  float *sLse = reinterpret_cast<float *>(sdO + FULL);
+  float *sDq = sLse + 256;
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+
+  const int t = threadIdx.x, warp = t >> 5;
+  const int k0 = blockIdx.x * QT, h = blockIdx.y;
+  const int64_t b = blockIdx.z;
+  const int L = a.L, Lp = a.Lp;
+  const int k = k0 + t;
+  const bool kv = k < L;
+
+  if (t == 0) {
+    mbar_init(&bars[0], 1);
+    mbar_init(&bars[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  for (int i = t; i < Lp; i += 128) {
+    const bool ok = i < L;
+    sLse[i] = ok ? a.lse[(b * a.H + h) * (int64_t)L + i] * LOG2E : 0.f;
+    sDq[i] = ok ? a.Dq[(b * a.H + h) * (int64_t)L + i] : 0.f;
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+
+  if (t == 0) {
+    mbar_expect_tx(&bars[0], 2 * TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
+    tma_load_4d(sK, &mKt, &bars[0], 0, k0, (int)b, h);
+    tma_load_4d(sV, &mVt, &bars[0], 0, k0, (int)b, h);
+    tma_load_4d(sQ, &mQa, &bars[0], 0, 0, (int)b, h);
+    tma_load_4d(sdO, &mdOa, &bars[0], 0, 0, (int)b, h);
+    mbar_wait(&bars[0], 0);
+    fence_after();
+    const uint32_t idesc = idesc_bf16(128, Lp, false, false);
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sK), ks), desc_kmajor_tile<D>(smem_u32(sQ), ks),
+                idesc, ks > 0);
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sV), ks),
+                desc_kmajor_tile<D>(smem_u32(sdO), ks), idesc, ks > 0);
+    umma_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 0);
+  fence_after();
+  for (int c0 = 0; c0 < Lp; c0 += 32) {
+    uint32_t sv[32], dv[32];
+    tmem_ld32(lane_addr + c0, sv);
+    tmem_ld32(lane_addr + 256 + c0, dv);
+    uint32_t pk[16], dk[16];
+#pragma unroll
+    for (int j = 0; j < 32; j += 2) {
+      float p[2], ds[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int qq = c0 + j + u;
+        float s = __uint_as_float(sv[j + u]) * a.scale;
+        const bool ok = kv && qq < L;
+        if (a.bias && ok) s += bias_at(a, h, qq, k);
+        p[u] = ok ? ex2(s * LOG2E - sLse[qq]) : 0.f;
+        ds[u] = p[u] * (__uint_as_float(dv[j + u]) - sDq[qq]);
+      }
+      pk[j >> 1] = pack2(p[0], p[1]);
+      dk[j >> 1] = pack2(ds[0], ds[1]);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      pbuf_store8(sPt, t, (c0 >> 3) + c,
+                  make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
+      pbuf_store8(sdSt, t, (c0 >> 3) + c,
+                  make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+    }
+  }
+  fence_proxy_async_smem();
+  fence_before();
+  __syncthreads();
+  if (t == 0) {
+    fence_after();
+    const uint32_t idesc = idesc_bf16(128, D, false, true);
+    for (int ks = 0; ks < Lp / 16; ++ks)
+      umma_bf16(tmem, desc_pbuf(smem_u32(sPt), ks), desc_mnmajor_tile<D>(smem_u32(sdO), ks), idesc,
+                ks > 0);
+    for (int ks = 0; ks < Lp / 16; ++ks)
+      umma_bf16(tmem + 256, desc_pbuf(smem_u32(sdSt), ks), desc_mnmajor_tile<D>(smem_u32(sQ), ks),
+                idesc, ks > 0);
+    umma_commit(&bars[1]);
+  }
+  mbar_wait(&bars[1], 1);
+  fence_after();
+  float dvr[D], dkr[D];
+  tmem_ld_row<D>(lane_addr, dvr);
+  tmem_ld_row<D>(lane_addr + 256, dkr);
+  if (kv) {
+    const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D;
+#pragma unroll
+    for (int d8 = 0; d8 < D; d8 += 8) {
+      uint32_t w1[4], w2[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        w1[j] = pack2(dvr[d8 + 2 * j], dvr[d8 + 2 * j + 1]);
+        w2[j] = pack2(dkr[d8 + 2 * j] * a.scale, dkr[d8 + 2 * j + 1] * a.scale);
+      }
+      *reinterpret_cast<uint4 *>(a.dv + off + d8) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+      *reinterpret_cast<uint4 *>(a.dk + off + d8) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ===================================================================== host
+// 4-D map over a (b, l, h, d) strided bf16 buffer: dims {D, L, nb, H}.
+bool head_map(CUtensorMap *m, const void *base, int D, int L, int64_t nb, int H, int64_t sl,
+              int64_t sb, int box_rows) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[4] = {(cuuint64_t)D, (cuuint64_t)L, (cuuint64_t)nb, (cuuint64_t)H};
+  cuuint64_t strides[3] = {(cuuint64_t)sl * 2, (cuuint64_t)sb * 2, (cuuint64_t)D * 2};
+  cuuint32_t box[4] = {(cuuint32_t)D, (cuuint32_t)box_rows, 1, 1};
+  cuuint32_t es[4] = {1, 1, 1, 1};
+  CUtensorMapSwizzle sw = D == 64 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : (D == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B);
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box,
+            es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+AttnTcArgs make_args(const evo_attn_desc *d) {
+  AttnTcArgs a;
+  a.nb = d->nb; a.H = d->H; a.L = d->L; a.Lp = (d->L + 15) / 16 * 16; a.D = d->D;
+  a.scale = d->scale;
+  a.g = reinterpret_cast<const bf16 *>(d->g);
+  a.sb = d->sb; a.sl = d->sl;
+  a.o = reinterpret_cast<bf16 *>(d->o); a.gm = reinterpret_cast<bf16 *>(d->gm);
+  a.o_sb = d->o_sb; a.o_sl = d->o_sl;
+  a.bias = d->bias; a.bh = d->bh; a.bq = d->bq; a.bk = d->bk;
+  a.lse = d->lse;
+  a.dO = nullptr; a.Dq = nullptr;
+  a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
+  a.dv = reinterpret_cast<bf16 *>(d->dv);
+  a.dbias_part = nullptr; a.chunk = 1;
+  return a;
+}
+
+int64_t dq_chunks(const evo_attn_desc *d) {
+  if (!d->dbias) return d->nb;
+  int64_t tiles = (int64_t)d->H * ((d->L + QT - 1) / QT);
+  int64_t want = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
+  return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
+}
+
+size_t fwd_smem(int D) { return 1024 + PBYTES + (size_t)QT * 2 * D + 2 * 256 * 2 * D + 64; }
+size_t dq_smem(int D) { return 1024 + PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 64; }
+size_t dkv_smem(int D) {
+  return 1024 + 2 * PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 2 * 256 * 4 + 64;
+}
+
+template <int D>
+int fwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+  AttnTcArgs a = make_args(d);
+  CUtensorMap mq, mk, mv;
+  if (!head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
+      !head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp) ||
+      !head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp))
+    return EVO_EUNSUP;
+  size_t smem = fwd_smem(D);
+  cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                       (int)smem);
+  dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
+  attn_fwd_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, a);
+  EVO_LAUNCHED("attn_fwd_tc_kernel");
+  return EVO_OK;
+}
+
+template <int D>
+int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+  AttnTcArgs a = make_args(d);
+  // workspace: dO (o's strides) | Dq [nb, H, L] | dbias chunk partials
+  const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * D;
+  const size_t dO_pad = ((size_t)span * 2 + 255) / 256 * 256;
+  const size_t Dq_pad = ((size_t)d->nb * d->H * d->L * 4 + 255) / 256 * 256;
+  const int64_t nch = dq_chunks(d);
+  const int64_t chunk = (d->nb + nch - 1) / nch;
+  const int64_t nch2 = (d->nb + chunk - 1) / chunk;
+  uint8_t *ws = reinterpret_cast<uint8_t *>(d->workspace);
+  bf16 *dObuf = reinterpret_cast<bf16 *>(ws);
+  float *Dq = reinterpret_cast<float *>(ws + dO_pad);
+  float *part = d->dbias ? reinterpret_cast<float *>(ws + dO_pad + Dq_pad) : nullptr;
+  {
+    int64_t total = d->nb * (int64_t)d->L * d->H;
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    attn_bwd_prep_kernel<D><<<blocks, 256, 0, st>>>(a, reinterpret_cast<const bf16 *>(d->dgm),
+                                                     dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq);
+    EVO_LAUNCHED("attn_bwd_prep_kernel");
+  }
+  a.dO = dObuf;
+  a.Dq = Dq;
+  a.dbias_part = part;
+  a.chunk = chunk;
+  CUtensorMap mq, mk, mv, mdo, mqa, mdoa, mkt, mvt;
+  const int Lp = a.Lp;
+  if (!head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
+      !head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, Lp) ||
+      !head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, Lp) ||
+      !head_map(&mdo, dObuf, D, d->L, d->nb, d->H, d->o_sl, d->o_sb, QT) ||
+      !head_map(&mqa, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, Lp) ||
+      !head_map(&mdoa, dObuf, D, d->L, d->nb, d->H, d->o_sl, d->o_sb, Lp) ||
+      !head_map(&mkt, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
+      !head_map(&mvt, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, QT))
+    return EVO_EUNSUP;
+  {
+    size_t smem = dq_smem(D);
+    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch2);
+    attn_bwd_dq_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, mdo, a);
+    EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
+  }
+  {
+    size_t smem = dkv_smem(D);
+    cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
+    attn_bwd_dkv_tc_kernel<D><<<grid, 128, smem, st>>>(mkt, mvt, mqa, mdoa, a);
+    EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");
+  }
+  if (d->dbias)
+    return reduce_lead(EVO_F32, nch2, 1, (int64_t)d->H * d->L * d->L, part, d->dbias, 0, 1, 0, st);
+  return EVO_OK;
+}
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
+
+}  // namespace
+
+bool attention_tc_accepts(const evo_attn_desc *d) {
+  if (d->dtype != EVO_BF16) return false;
+  if (!(d->D == 16 || d->D == 32 || d->D == 64)) return false;
+  if (d->L < 1 || d->L > 256 || d->nb < 1 || d->nb > 65535) return false;
+  if (d->sl % 8 || d->sb % 8 || d->o_sl % 8 || d->o_sb % 8) return false;
+  if (!aligned16(d->q) || !aligned16(d->k) || !aligned16(d->v) || !aligned16(d->g) ||
+      !aligned16(d->o))
+    return false;
+  if (d->gm && !aligned16(d->gm)) return false;
+  if (d->dq && !(aligned16(d->dq) && aligned16(d->dk) && aligned16(d->dv) && aligned16(d->dgpre)))
+    return false;
+  if (d->dgm && !aligned16(d->dgm)) return false;
+  return tc::encode_fn() != nullptr;
+}
+
+size_t attention_tc_bwd_ws(const evo_attn_desc *d) {
+  if (!attention_tc_accepts(d)) return 0;
+  // dO uses o's strides: size it by the extent those strides span.
+  const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * d->D;
+  const size_t dO_pad = ((size_t)span * 2 + 255) / 256 * 256;
+  const size_t Dq_pad = ((size_t)d->nb * d->H * d->L * 4 + 255) / 256 * 256;
+  size_t part = 0;
+  if (d->dbias) {
+    int64_t nch = dq_chunks(d);
+    int64_t chunk = (d->nb + nch - 1) / nch;
+    nch = (d->nb + chunk - 1) / chunk;
+    part = (size_t)nch * d->H * d->L * d->L * 4;
+  }
+  return dO_pad + Dq_pad + part;
+}
+
+int attention_tc_fwd(const evo_attn_desc *d, cudaStream_t st) {
+  switch (d->D) {
+    case 16: return fwd_launch<16>(d, st);
+    case 32: return fwd_launch<32>(d, st);
+    case 64: return fwd_launch<64>(d, st);
+  }
+  return EVO_EUNSUP;
+}
+
+int attention_tc_bwd(const evo_attn_desc *d, cudaStream_t st) {
+  EVO_REQUIRE(d->workspace && d->workspace_bytes >= attention_tc_bwd_ws(d), EVO_EARG,
+              "attention bwd (tc): workspace too small");
+  switch (d->D) {
+    case 16: return bwd_launch<16>(d, st);
+    case 32: return bwd_launch<32>(d, st);
+    case 64: return bwd_launch<64>(d, st);
+  }
+  return EVO_EUNSUP;
+}
+
 }  // namespace evo

@@ -1,0 +1,127 @@
+"""The fused gated attention entry points (evo_attention_fwd/bwd) against a
+plain PyTorch fp32 reference of the same op, on the tcgen05 path (bf16)
+and the SIMT path (fp32), over the four geometries of the block (row /
+column / triangle-start / triangle-end: batch-major or sequence-major rows,
+plain or transposed pair bias), ragged L and every supported head dim."""
+
+import pytest
+import torch
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def K():
+    from paper_2211_00235_b200 import kernels
+    return kernels
+
+
+def rel(a, b):
+    a, b = a.double(), b.double()
+    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+
+
+def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0):
+    torch.manual_seed(seed)
+    hc = H * D
+    rows = nb * L
+    # row index of (b, l): batch-major (row/tri-start) or sequence-major (col/tri-end)
+    if seq_major:
+        sb, sl = 1, nb
+    else:
+        sb, sl = L, 1
+    proj = torch.randn(rows, 4 * hc, device="cuda")
+    proj[:, 3 * hc:] = torch.sigmoid(proj[:, 3 * hc:])
+    proj = proj.to(dtype)
+    bias = None
+    bh = bq = bk = 0
+    if bias_mode != "none":
+        bias = torch.randn(H, L * L, device="cuda")
+        bh = L * L
+        bq, bk = (L, 1) if bias_mode == "plain" else (1, L)
+    o = torch.empty(rows, hc, device="cuda", dtype=dtype)
+    gm = torch.empty_like(o)
+    lse = torch.empty(nb, H, L, device="cuda")
+    scale = D ** -0.5
+    geo = dict(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb * 4 * hc,
+               sl=sl * 4 * hc, o=o, gm=gm, o_sb=sb * hc, o_sl=sl * hc, lse=lse, bias=bias,
+               bh=bh, bq=bq, bk=bk)
+    K.attention(**geo)
+    dgm = torch.randn(rows, hc, device="cuda").to(dtype)
+    dproj = torch.zeros(rows, 4 * hc, device="cuda", dtype=dtype)
+    dbias = torch.empty(H, L * L, device="cuda") if bias is not None else None
+    K.attention(**geo, dgm=dgm, dproj=dproj, dbias=dbias)
+    torch.cuda.synchronize()
+
+    # ---- torch fp32 reference on the same (rounded) inputs
+    pf = proj.float()
+    idx = (torch.arange(nb, device="cuda")[:, None] * sb +
+           torch.arange(L, device="cuda")[None, :] * sl)          # [nb, L] row ids
+
+    def heads(col0):
+        x = pf[idx][:, :, col0:col0 + hc]                         # [nb, L, hc]
+        return x.view(nb, L, H, D).permute(0, 2, 1, 3).contiguous()
+
+    q = heads(0).requires_grad_(True)
+    k = heads(hc).requires_grad_(True)
+    v = heads(2 * hc).requires_grad_(True)
+    g = heads(3 * hc)
+    bt = None
+    if bias is not None:
+        hh, qq, kk = torch.meshgrid(torch.arange(H), torch.arange(L), torch.arange(L),
+                                    indexing="ij")
+        bt = bias.view(-1)[(hh * bh + qq * bq + kk * bk).cuda()].clone().requires_grad_(True)
+    s = (q * scale) @ k.transpose(-1, -2)
+    if bt is not None:
+        s = s + bt
+    p = torch.softmax(s, -1)
+    O = p @ v
+    G = g * O
+    dG = dgm.float()[idx].view(nb, L, H, D).permute(0, 2, 1, 3)
+    (G * dG).sum().backward()
+    dgpre = dG * O.detach() * g * (1 - g)
+
+    def gather(t):  # [nb, H, L, D] -> [nb, L, hc] by rows
+        return t.permute(0, 2, 1, 3).reshape(nb, L, hc)
+
+    errs = {
+        "o": rel(o.float()[idx], gather(O.detach())),
+        "gm": rel(gm.float()[idx], gather(G.detach())),
+        "lse": rel(lse, torch.logsumexp(s.detach(), -1)),
+        "dq": rel(dproj.float()[idx][:, :, :hc], gather(q.grad)),
+        "dk": rel(dproj.float()[idx][:, :, hc:2 * hc], gather(k.grad)),
+        "dv": rel(dproj.float()[idx][:, :, 2 * hc:3 * hc], gather(v.grad)),
+        "dgpre": rel(dproj.float()[idx][:, :, 3 * hc:], gather(dgpre)),
+    }
+    if bt is not None:
+        hh, qq, kk = torch.meshgrid(torch.arange(H), torch.arange(L), torch.arange(L),
+                                    indexing="ij")
+        got = dbias.view(-1)[(hh * bh + qq * bq + kk * bk).cuda()]
+        errs["dbias"] = rel(got, bt.grad)
+    return errs
+
+
+CASES = [
+    # nb, L, H, D, seq_major, bias
+    (6, 256, 2, 32, False, "plain"),     # row attention / triangle start
+    (5, 256, 2, 32, True, "transposed"), # triangle end
+    (7, 128, 2, 32, True, "none"),       # column attention
+    (3, 100, 2, 32, False, "plain"),     # ragged L (masked keys, partial tile)
+    (4, 64, 4, 16, False, "plain"),      # mid config head dim
+    (4, 160, 2, 64, True, "transposed"),
+    (9, 48, 3, 16, True, "none"),
+]
+
+
+@pytest.mark.parametrize("case", CASES)
+def test_attention_tc_bf16(K, case):
+    errs = run_case(K, *case, dtype=torch.bfloat16)
+    bad = {k: v for k, v in errs.items() if v > 1.5e-2}
+    assert not bad, errs
+
+
+@pytest.mark.parametrize("case", CASES[:4])
+def test_attention_simt_fp32(K, case):
+    errs = run_case(K, *case, dtype=torch.float32)
+    bad = {k: v for k, v in errs.items() if v > 2e-6}
+    assert not bad, errs
