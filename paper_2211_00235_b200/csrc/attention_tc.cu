@@ -758,7 +758,8 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 bool attention_tc_accepts(const evo_attn_desc *d) {
   if (d->dtype != EVO_BF16) return false;
-  if (!(d->D == 16 || d->D == 32 || d->D == 64)) return false;
+  // D=64 would need 229 KB of smem in the dk/dv kernel: SIMT path
+  if (!(d->D == 16 || d->D == 32)) return false;
   if (d->L < 1 || d->L > 256 || d->nb < 1 || d->nb > 65535) return false;
   if (d->sl % 8 || d->sb % 8 || d->o_sl % 8 || d->o_sb % 8) return false;
   if (!aligned16(d->q) || !aligned16(d->k) || !aligned16(d->v) || !aligned16(d->g) ||
