@@ -220,6 +220,8 @@ def run_native(args):
     # timed region: device-resident inputs
     prof = []
     K.PROFILE = prof
+    shapes = [] if args.detail else None
+    K.PROFILE_SHAPES = shapes
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
@@ -238,6 +240,7 @@ def run_native(args):
         dist.barrier()
     launches = _native.launch_count() - n0
     K.PROFILE = None
+    K.PROFILE_SHAPES = None
     clk = clocks.stop()
     ms = ev0.elapsed_time(ev1) / args.steps
     if world > 1:
@@ -253,6 +256,18 @@ def run_native(args):
         f[0] += flops
         f[1] += d_ms
         f[2] += 1
+
+    if shapes is not None and rank == 0:
+        det = {}
+        for (name, flops, e0_, e1_), shp in zip(prof, shapes):
+            key = f"{name} {shp}" if shp else name
+            dd = det.setdefault(key, [0.0, 0.0, 0])
+            dd[0] += flops
+            dd[1] += e0_.elapsed_time(e1_)
+            dd[2] += 1
+        for key, (fl, tms, n) in sorted(det.items(), key=lambda kv: -kv[1][1]):
+            print(f"{tms / args.steps:8.3f} ms/step {n // args.steps:3d}x "
+                  f"{fl / (tms / 1e3) / 1e12 if tms else 0:8.1f} TF/s  {key}", file=sys.stderr)
 
     # end-to-end: pinned host inputs -> device, step, loss -> host
     torch.cuda.synchronize()
@@ -341,6 +356,7 @@ def main():
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--dp-only", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--detail", action="store_true", help="per-call GEMM/attention table on stderr")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)

@@ -33,7 +33,12 @@ def stream() -> int:
 PROFILE = None
 
 
-def _timed(family, flops, fn):
+DT_NAME = {N.EVO_F32: "f32", N.EVO_BF16: "bf16"}
+# optional list collecting (family, shape) per profiled call (bench --detail)
+PROFILE_SHAPES = None
+
+
+def _timed(family, flops, fn, shape=None):
     if PROFILE is None:
         return fn()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -42,6 +47,8 @@ def _timed(family, flops, fn):
     r = fn()
     e1.record()
     PROFILE.append((family, flops, e0, e1))
+    if PROFILE_SHAPES is not None:
+        PROFILE_SHAPES.append(shape)
     return r
 
 
@@ -100,7 +107,8 @@ def gemm(A: Mat, B: Mat, Cm: Mat, M: int, N_: int, K: int, *, alpha: float = 1.0
     d.workspace = ptr(ws)
     d.workspace_bytes = nbytes
     _timed("gemm", 2.0 * M * N_ * K * B1 * B2,
-           lambda: check(L.evo_gemm(C.byref(d), stream()), "evo_gemm"))
+           lambda: check(L.evo_gemm(C.byref(d), stream()), "evo_gemm"),
+           (M, N_, K, B1 * B2, d.split_k, int(A.rs == 1), int(B.rs == 1), DT_NAME[d.dtype_c]))
 
 
 def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, target: int = 4096) -> int:
