@@ -44,7 +44,8 @@ using namespace tc;
 
 constexpr int BM = 128;
 constexpr int BK = 64;           // one 128-byte swizzle atom of bf16
-constexpr int NTHREADS = 192;
+constexpr int EPI_WARPS = 8;
+constexpr int NTHREADS = 64 + 32 * EPI_WARPS;  // TMA warp, MMA warp, epilogue warps
 constexpr int SMEM_A = BM * BK * 2;  // 16 KiB
 
 struct TcParams {
@@ -70,7 +71,94 @@ __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_
   bidx = r / p.split;
 }
 
-template <int BN, int STAGES>
+
+// Compile-time epilogue kinds (runtime residual/accumulate stay per chunk).
+enum { EK_NONE = 0, EK_BIAS = 1, EK_BIAS_RELU = 2, EK_BIAS_SIGMOID = 3 };
+
+__device__ __forceinline__ float fast_sigmoid(float x) {
+  return __frcp_rn(1.f + __expf(-x));
+}
+
+// Finish one 32-column chunk of one output row: alpha, bias, activation,
+// residual, store.  Fully unrolled; vector stores when the chunk's 32
+// destination elements are contiguous and aligned.
+template <int EPI>
+__device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, const uint32_t (&v)[32],
+                                          int64_t rbase, int64_t nb) {
+  float x[32];
+  const bool full = nb + 32 <= p.N;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = e.alpha * __uint_as_float(v[j]);
+  if constexpr (EPI != EK_NONE) {
+    if (full && ((reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 b4 = reinterpret_cast<const float4 *>(e.bias + nb)[j];
+        x[4 * j] += b4.x; x[4 * j + 1] += b4.y; x[4 * j + 2] += b4.z; x[4 * j + 3] += b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] += (nb + j < p.N) ? e.bias[nb + j] : 0.f;
+    }
+  }
+  if constexpr (EPI == EK_BIAS_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaxf(x[j], 0.f);
+  }
+  if constexpr (EPI == EK_BIAS_SIGMOID) {
+    if (nb >= e.epi_col0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = fast_sigmoid(x[j]);
+    } else if (nb + 32 > e.epi_col0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (nb + j >= e.epi_col0) x[j] = fast_sigmoid(x[j]);
+    }
+  }
+  // destination: contiguous if plain unit-stride columns, or a two-level
+  // column map whose inner block is a multiple of 32 with unit stride
+  const IdxMap &cm = e.cmap;
+  const bool contig = full && ((cm.cdiv == 0 && cm.cs == 1) ||
+                               (cm.cdiv > 0 && (cm.cdiv % 32) == 0 && cm.cs0 == 1));
+  const int64_t base = rbase + cm.col(nb);
+  if (contig && !e.accumulate && p.c_aligned) {
+    if (e.dtype_c == EVO_BF16 && !e.residual && (base & 7) == 0) {
+      uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + base);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        uint32_t w[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * j + 2 * u], x[8 * j + 2 * u + 1]);
+          w[u] = *reinterpret_cast<uint32_t *>(&h2);
+        }
+        dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      return;
+    }
+    if (e.dtype_c == EVO_F32 && (base & 3) == 0) {
+      float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(e.C) + base);
+      const float4 *res = e.residual ? reinterpret_cast<const float4 *>(e.residual + base) : nullptr;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 o = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
+        if (res) {
+          float4 r = res[j];
+          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+        }
+        dst[j] = o;
+      }
+      return;
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 32; ++j) {
+    const int64_t n = nb + j;
+    if (n < p.N) epi_store(e, rbase + cm.col(n), x[j]);
+  }
+}
+
+template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const TcParams p) {
@@ -100,7 +188,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int a = 0; a < 2; ++a) {
       mbar_init(&tfull[a], 1);
-      mbar_init(&tempty[a], 4);
+      mbar_init(&tempty[a], EPI_WARPS);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -202,11 +290,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
   } else {
     // ---------------------------------------------------------- epilogue
-    const int q = warp & 3;  // TMEM lane quadrant this warp may access
+    // EPI_WARPS warps; warps w and w+4 share TMEM lane quadrant w%4 and
+    // split the 32-column chunks of the tile between them.
+    const int ew = warp - 2;
+    const int q = warp & 3;
+    const int half = ew >> 2;  // 0 or 1
     int acc = 0;
     uint32_t aphase = 0;
     const EpiArgs &e = p.epi;
-    const bool vec_ok = (e.cmap.cdiv == 0 && e.cmap.cs == 1 && p.c_aligned);
     for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int64_t bidx, mt, nt;
       int sp;
@@ -219,59 +310,27 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const bool row_ok = m < p.M;
       const int64_t rbase = row_ok ? (b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m)) : 0;
 #pragma unroll 1
-      for (int c0 = 0; c0 < BN; c0 += 32) {
+      for (int c0 = half * 32; c0 < BN; c0 += 64) {
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
-        if (!row_ok) continue;
         const int64_t nb = n0 + c0;
+        if (!row_ok || nb >= p.N) continue;
         if (p.split > 1) {
-          float *dst = p.partial + (((int64_t)sp * p.nbatch + bidx) * p.M + m) * p.N;
-          for (int j = 0; j < 32; ++j)
-            if (nb + j < p.N) dst[nb + j] = __uint_as_float(v[j]);
+          float *dst = p.partial + (((int64_t)sp * p.nbatch + bidx) * p.M + m) * p.N + nb;
+          if (nb + 32 <= p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              reinterpret_cast<float4 *>(dst)[j] =
+                  make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                              __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (nb + j < p.N) dst[j] = __uint_as_float(v[j]);
+          }
           continue;
         }
-        int64_t base = rbase + nb;  // valid when vec_ok
-        bool full_chunk = (nb + 32 <= p.N);
-        if (vec_ok && full_chunk && !e.accumulate && e.dtype_c == EVO_BF16 && (base & 7) == 0 &&
-            (!e.residual)) {
-          uint32_t packed[16];
-#pragma unroll
-          for (int j = 0; j < 16; ++j) {
-            float x0 = epi_value(e, nb + 2 * j, __uint_as_float(v[2 * j]));
-            float x1 = epi_value(e, nb + 2 * j + 1, __uint_as_float(v[2 * j + 1]));
-            __nv_bfloat162 h2 = __floats2bfloat162_rn(x0, x1);
-            packed[j] = *reinterpret_cast<uint32_t *>(&h2);
-          }
-          uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + base);
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-            dst[j] = make_uint4(packed[4 * j], packed[4 * j + 1], packed[4 * j + 2],
-                                packed[4 * j + 3]);
-        } else if (vec_ok && full_chunk && !e.accumulate && e.dtype_c == EVO_F32 &&
-                   (base & 3) == 0) {
-          float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(e.C) + base);
-          const float4 *res =
-              e.residual ? reinterpret_cast<const float4 *>(e.residual + base) : nullptr;
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float4 o;
-            o.x = epi_value(e, nb + 4 * j + 0, __uint_as_float(v[4 * j + 0]));
-            o.y = epi_value(e, nb + 4 * j + 1, __uint_as_float(v[4 * j + 1]));
-            o.z = epi_value(e, nb + 4 * j + 2, __uint_as_float(v[4 * j + 2]));
-            o.w = epi_value(e, nb + 4 * j + 3, __uint_as_float(v[4 * j + 3]));
-            if (res) {
-              float4 r = res[j];
-              o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
-            }
-            dst[j] = o;
-          }
-        } else {
-          for (int j = 0; j < 32; ++j) {
-            const int64_t n = nb + j;
-            if (n < p.N)
-              epi_store(e, rbase + e.cmap.col(n), epi_value(e, n, __uint_as_float(v[j])));
-          }
-        }
+        epi_chunk<EPI>(p, e, v, rbase, nb);
       }
       fence_before();
       __syncwarp();
@@ -360,7 +419,7 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
   return split < 1 ? 1 : split;
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, int EPI>
 int launch(const evo_gemm_desc *d, cudaStream_t st) {
   OperandPlan pa, pb;
   plan_operand(d->A, d->M, d->K, pa);
@@ -392,12 +451,12 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) + 256;
   static bool attr_set = false;
   if (!attr_set) {
-    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     attr_set = true;
   }
   int64_t grid = std::min<int64_t>(p.num_tiles, (int64_t)num_sms());
-  gemm_tc_kernel<BN, STAGES><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, p);
+  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, p);
   EVO_LAUNCHED("gemm_tc_kernel");
   if (p.split > 1) return gemm_splitk_reduce(d, p.split, p.partial, st);
   return EVO_OK;
@@ -421,10 +480,22 @@ size_t gemm_tc_workspace(const evo_gemm_desc *d) {
   return (size_t)split * d->B1 * d->B2 * d->M * d->N * sizeof(float);
 }
 
+template <int EPI>
+int launch_bn(const evo_gemm_desc *d, cudaStream_t st) {
+  if (choose_bn(d) == 256) return launch<256, 4, EPI>(d, st);
+  return launch<128, 6, EPI>(d, st);
+}
+
 int gemm_tc(const evo_gemm_desc *d, cudaStream_t st) {
   if (!gemm_tc_accepts(d)) return EVO_EUNSUP;
-  if (choose_bn(d) == 256) return launch<256, 4>(d, st);
-  return launch<128, 6>(d, st);
+  // split-K partials carry no epilogue (applied by the reducer)
+  int64_t kc;
+  const bool split = choose_split(d, choose_bn(d), kc) > 1;
+  if (split || (!d->bias && d->epilogue == EVO_EPI_NONE)) return launch_bn<EK_NONE>(d, st);
+  if (!d->bias) return EVO_EUNSUP;  // activation without bias: SIMT handles it
+  if (d->epilogue == EVO_EPI_RELU) return launch_bn<EK_BIAS_RELU>(d, st);
+  if (d->epilogue == EVO_EPI_SIGMOID_FROM) return launch_bn<EK_BIAS_SIGMOID>(d, st);
+  return launch_bn<EK_BIAS>(d, st);
 }
 
 }  // namespace evo
