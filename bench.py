@@ -217,38 +217,72 @@ def run_native(args):
         step(m_d, z_d)
     torch.cuda.synchronize()
 
-    # timed region: device-resident inputs
+    use_graph = args.graph and world == 1
+    graph = graph_e2e = None
+    if use_graph:
+        # one step captured as a CUDA graph (all native launches go to the
+        # capturing stream); inputs are static device buffers
+        m_s, z_s = m_d.clone(), z_d.clone()
+        side = torch.cuda.Stream()
+        side.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(side):
+            step(m_s, z_s)
+        torch.cuda.current_stream().wait_stream(side)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step(m_s, z_s)
+        # end-to-end graph: pinned H2D inputs -> step -> loss D2H
+        graph_e2e = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph_e2e):
+            m_s.copy_(m_h, non_blocking=True)
+            z_s.copy_(z_h, non_blocking=True)
+            out_e = step(m_s, z_s)
+            loss_h.copy_(out_e[2].reshape(1), non_blocking=True)
+        graph.replay()
+        graph_e2e.replay()
+        torch.cuda.synchronize()
+
+    def timed(fn, k):
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k):
+            fn()
+        a1.record()
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        t = a0.elapsed_time(a1) / k
+        if world > 1:
+            tt = torch.tensor([t], device=dev)
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+            t = float(tt.item())
+        return t
+
+    # timed region (device-resident inputs), clocks sampled during it
+    clocks = Clocks(local)
+    clocks.start()
+    time.sleep(0.3)
+    if use_graph:
+        ms = timed(graph.replay, args.steps)
+    else:
+        ms = timed(lambda: step(m_d, z_d), args.steps)
+    clk = clocks.stop()
+
+    # kernel-family breakdown: CUDA events around every GEMM / attention
+    # launch on the launching stream, over an eager pass of the same steps
     prof = []
     K.PROFILE = prof
     shapes = [] if args.detail else None
     K.PROFILE_SHAPES = shapes
-    clocks = Clocks(local)
-    clocks.start()
-    time.sleep(0.3)
-    if world > 1:
-        dist.barrier()
-    torch.cuda.synchronize()
     n0 = _native.launch_count()
-    ev0 = torch.cuda.Event(enable_timing=True)
-    ev1 = torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        step(m_d, z_d)
-    ev1.record()
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
+    ms_eager = timed(lambda: step(m_d, z_d), args.steps)
     launches = _native.launch_count() - n0
     K.PROFILE = None
     K.PROFILE_SHAPES = None
-    clk = clocks.stop()
-    ms = ev0.elapsed_time(ev1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
-
-    # kernel-family breakdown from the events recorded in the timed region
     fam = {}
     for name, flops, e0, e1 in prof:
         d_ms = e0.elapsed_time(e1)
@@ -256,7 +290,6 @@ def run_native(args):
         f[0] += flops
         f[1] += d_ms
         f[2] += 1
-
     if shapes is not None and rank == 0:
         det = {}
         for (name, flops, e0_, e1_), shp in zip(prof, shapes):
@@ -270,24 +303,13 @@ def run_native(args):
                   f"{fl / (tms / 1e3) / 1e12 if tms else 0:8.1f} TF/s  {key}", file=sys.stderr)
 
     # end-to-end: pinned host inputs -> device, step, loss -> host
-    torch.cuda.synchronize()
-    if world > 1:
-        dist.barrier()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(args.steps):
+    def e2e_eager():
         m_e = m_h.to(dev, non_blocking=True)
         z_e = z_h.to(dev, non_blocking=True)
         out = step(m_e, z_e)
         loss_h.copy_(out[2].reshape(1), non_blocking=True)
-    e1.record()
-    torch.cuda.synchronize()
-    ms_e2e = e0.elapsed_time(e1) / args.steps
-    if world > 1:
-        t = torch.tensor([ms_e2e], device=dev)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_e2e = float(t.item())
+
+    ms_e2e = timed(graph_e2e.replay if use_graph else e2e_eager, args.steps)
 
     if rank != 0:
         if world > 1:
@@ -309,7 +331,8 @@ def run_native(args):
         roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
                 "peak_source": src, "launches": n,
-                "share_of_step": tms / (ms * args.steps)}
+                "share_of_step": tms / (ms_eager * args.steps),
+                "timing": "CUDA events around each launch on its stream, eager pass"}
     breakdown = {k: {"tflops": (v[0] / (v[1] / 1e3) / 1e12) if v[1] > 0 else None,
                      "ms_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
                  for k, v in fam.items()}
@@ -337,6 +360,7 @@ def run_native(args):
         "e2e": {"value": samples / (ms_e2e / 1e3), "unit": "samples/s",
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
+        "launch_mode": "cuda_graph" if use_graph else "eager", "ms_per_step_eager": ms_eager,
         "clocks": clk,
     }
     print(json.dumps(line))
@@ -355,6 +379,8 @@ def main():
     ap.add_argument("--blocks", type=int, default=0)
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--dp-only", action="store_true")
+    ap.add_argument("--no-graph", dest="graph", action="store_false",
+                    help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--detail", action="store_true", help="per-call GEMM/attention table on stderr")
     args = ap.parse_args()

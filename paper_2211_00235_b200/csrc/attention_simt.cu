@@ -298,10 +298,10 @@ int attention_simt_fwd(const evo_attn_desc *a, cudaStream_t st) {
   dim3 grid((a->L + QT - 1) / QT, a->H, (unsigned)a->nb);
   size_t smem = (size_t)(2 * a->L * (a->D + 1) + AW * a->L + AW * a->D) * sizeof(float);
   if (a->dtype == EVO_F32) {
-    cudaFuncSetAttribute(attn_fwd_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    EVO_MAX_SMEM_ONCE((attn_fwd_kernel<float>));
     attn_fwd_kernel<float><<<grid, AW * 32, smem, st>>>(*a);
   } else {
-    cudaFuncSetAttribute(attn_fwd_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    EVO_MAX_SMEM_ONCE((attn_fwd_kernel<bf16>));
     attn_fwd_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a);
   }
   EVO_LAUNCHED("attn_fwd_kernel");
@@ -326,10 +326,10 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     size_t smem = (size_t)(2 * L * (D + 1) + AW * L + 2 * AW * D + (a->dbias ? QT * L : 0)) *
                   sizeof(float);
     if (a->dtype == EVO_F32) {
-      cudaFuncSetAttribute(attn_bwd_dq_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<float>));
       attn_bwd_dq_kernel<float><<<grid, AW * 32, smem, st>>>(*a, chunk, part);
     } else {
-      cudaFuncSetAttribute(attn_bwd_dq_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<bf16>));
       attn_bwd_dq_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a, chunk, part);
     }
     EVO_LAUNCHED("attn_bwd_dq_kernel");
@@ -338,10 +338,10 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     dim3 grid((L + QT - 1) / QT, a->H, (unsigned)a->nb);
     size_t smem = (size_t)(2 * L * (D + 1) + 2 * L + AW * 2 * L + AW * 2 * D) * sizeof(float);
     if (a->dtype == EVO_F32) {
-      cudaFuncSetAttribute(attn_bwd_dkv_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<float>));
       attn_bwd_dkv_kernel<float><<<grid, AW * 32, smem, st>>>(*a);
     } else {
-      cudaFuncSetAttribute(attn_bwd_dkv_kernel<bf16>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<bf16>));
       attn_bwd_dkv_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a);
     }
     EVO_LAUNCHED("attn_bwd_dkv_kernel");

@@ -687,8 +687,7 @@ int fwd_launch(const evo_attn_desc *d, cudaStream_t st) {
       !head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp))
     return EVO_EUNSUP;
   size_t smem = fwd_smem(D);
-  cudaFuncSetAttribute(attn_fwd_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                       (int)smem);
+  EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D>));
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
   attn_fwd_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, a);
   EVO_LAUNCHED("attn_fwd_tc_kernel");
@@ -733,16 +732,14 @@ int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
     return EVO_EUNSUP;
   {
     size_t smem = dq_smem(D);
-    cudaFuncSetAttribute(attn_bwd_dq_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D>));
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch2);
     attn_bwd_dq_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, mdo, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
   {
     size_t smem = dkv_smem(D);
-    cudaFuncSetAttribute(attn_bwd_dkv_tc_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
+    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D>));
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
     attn_bwd_dkv_tc_kernel<D><<<grid, 128, smem, st>>>(mkt, mvt, mqa, mdoa, a);
     EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");

@@ -96,6 +96,17 @@ inline size_t dtype_size(int dt) { return dt == EVO_BF16 ? 2 : 4; }
 inline bool valid_dtype(int dt) { return dt == EVO_F32 || dt == EVO_BF16; }
 inline cudaStream_t as_stream(void *s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Raise a kernel's dynamic-smem limit to the device maximum once per
+// process (kept out of the per-call path so launches stay graph-capturable).
+#define EVO_MAX_SMEM_ONCE(kernel)                                                       \
+  do {                                                                                  \
+    static bool _done = false;                                                          \
+    if (!_done) {                                                                       \
+      cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); \
+      _done = true;                                                                     \
+    }                                                                                   \
+  } while (0)
+
 inline int num_sms() {
   static int n = 0;
   if (n == 0) {
