@@ -139,135 +139,199 @@ __device__ __forceinline__ float bias_at(const AttnTcArgs &a, int h, int q, int 
 }
 
 // ====================================================================== fwd
-template <int D>
-__global__ void __launch_bounds__(128)
+// Pair-bias tile of one (head, 128-query tile) for all Lp keys, fp32,
+// resident in smem for the CTA's whole batch-row chunk:
+//   plain  (bk == 1): Lp/32 TMA boxes [128 q x 32 k], 128B-swizzled rows
+//   trans. (bq == 1): Lp/32 TMA boxes [32 k x 128 q] (q contiguous)
+constexpr uint32_t BIAS_BYTES = 128 * 256 * 4;
+
+template <bool TBIAS>
+__device__ __forceinline__ float bias_smem(const uint8_t *sb, int row, int k) {
+  if constexpr (TBIAS) {
+    return reinterpret_cast<const float *>(sb)[k * 128 + row];
+  } else {
+    const int box = k >> 5, kk = k & 31, chunk = kk >> 2;
+    const float *p = reinterpret_cast<const float *>(
+        sb + box * 16384 + row * 128 + ((chunk ^ (row & 7)) << 4));
+    return p[kk & 3];
+  }
+}
+// 32 consecutive keys [k0, k0+32) of one row (k0 % 32 == 0)
+template <bool TBIAS>
+__device__ __forceinline__ void bias_row32(const uint8_t *sb, int row, int k0, float (&out)[32]) {
+  if constexpr (TBIAS) {
+    const float *p = reinterpret_cast<const float *>(sb) + k0 * 128 + row;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) out[j] = p[j * 128];
+  } else {
+    const uint8_t *base = sb + (k0 >> 5) * 16384 + row * 128;
+#pragma unroll
+    for (int c = 0; c < 8; ++c) {
+      float4 v = *reinterpret_cast<const float4 *>(base + ((c ^ (row & 7)) << 4));
+      out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
+    }
+  }
+}
+
+// Load the bias tile (h, q0 .. q0+127, all keys) with TMA.
+template <bool TBIAS>
+__device__ __forceinline__ void load_bias_tile(uint8_t *sb, const CUtensorMap *map, uint64_t *bar,
+                                               int h, int q0, int Lp) {
+  const int nbox = (Lp + 31) / 32;
+  mbar_expect_tx(bar, (uint32_t)nbox * 16384u);
+  for (int j = 0; j < nbox; ++j) {
+    if constexpr (TBIAS)
+      tma_load_3d(sb + j * 16384, map, bar, q0, 32 * j, h);
+    else
+      tma_load_3d(sb + j * 16384, map, bar, 32 * j, q0, h);
+  }
+}
+
+// Two warpgroups ping-pong over the batch rows of the CTA's chunk; WG w
+// owns TMEM columns [256w, 256w+256): S (fp32) -> P (bf16 pairs, in place,
+// cols [0, Lp/2)) -> O (cols [128, 128+D)).
+template <int D, int BIASMODE>  // 0 none, 1 plain, 2 transposed
+__global__ void __launch_bounds__(256)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
-                   const __grid_constant__ CUtensorMap mV, const AttnTcArgs a) {
-  constexpr uint32_t TILE = QT * Sw<D>::bytes;       // 128-row tile bytes
-  constexpr uint32_t FULL = 256 * Sw<D>::bytes;      // up to 256 rows
+                   const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
+                   const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t WGB = TILE + 2 * FULL;  // per-warpgroup Q | K | V
+  constexpr bool TB = BIASMODE == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                             ~uintptr_t(1023));
-  uint8_t *sP = sm;                  // 64 KiB
-  uint8_t *sQ = sP + PBYTES;
-  uint8_t *sK = sQ + TILE;
-  uint8_t *sV = sK + FULL;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+  uint8_t *sBias = sm;
+  uint8_t *sWG = sBias + (BIASMODE ? BIAS_BYTES : 0);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sWG + 2 * WGB);  // 0 bias, 1-2 tma, 3-4 mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 5);
 
-  const int t = threadIdx.x, warp = t >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5;
+  const int w = tid >> 7, t = tid & 127;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
-  const int64_t b = blockIdx.z;
   const int L = a.L, Lp = a.Lp;
   const int q = q0 + t;
-
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (warp == 0) tmem_alloc(tslot, 256);
-  fence_before();
-  __syncthreads();
-  fence_after();
-  const uint32_t tmem = *tslot;
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-
-  if (t == 0) {
-    mbar_expect_tx(&bars[0], TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
-    tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
-    tma_load_4d(sK, &mK, &bars[0], 0, 0, (int)b, h);
-    tma_load_4d(sV, &mV, &bars[0], 0, 0, (int)b, h);
-    mbar_wait(&bars[0], 0);
-    fence_after();
-    const uint32_t idesc = idesc_bf16(128, Lp, false, false);
-#pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sQ), ks), desc_kmajor_tile<D>(smem_u32(sK), ks),
-                idesc, ks > 0);
-    umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 0);
-  fence_after();
-
-  // pass 1: s = scale*acc + bias (masked keys -> -inf), row max; write back
-  float mx = -INFINITY;
   const bool qv = q < L;
-  for (int c0 = 0; c0 < Lp; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld32(lane_addr + c0, v);
-#pragma unroll
-    for (int j = 0; j < 32; ++j) {
-      const int k = c0 + j;
-      float s = -INFINITY;
-      if (k < L) {
-        s = __uint_as_float(v[j]) * a.scale;
-        if (a.bias && qv) s += bias_at(a, h, q, k);
-      }
-      mx = fmaxf(mx, s);
-      v[j] = __float_as_uint(s);
-    }
-    tmem_st32(lane_addr + c0, v);
+  uint8_t *sQ = sWG + w * WGB;
+  uint8_t *sK = sQ + TILE;
+  uint8_t *sV = sK + FULL;
+  uint64_t *tbar = &bars[1 + w];
+  uint64_t *mbar = &bars[3 + w];
+
+  if (tid == 0) {
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, Lp);
   }
-  tmem_st_wait();
-  // pass 2: p = exp(s - max), row sum, P (bf16) -> smem
-  float sum = 0.f;
-  const float mxl = mx * LOG2E;
-  for (int c0 = 0; c0 < Lp; c0 += 32) {
-    uint32_t v[32];
-    tmem_ld32(lane_addr + c0, v);
-    uint32_t pk[16];
-#pragma unroll
-    for (int j = 0; j < 16; ++j) {
-      float p0 = ex2(__uint_as_float(v[2 * j]) * LOG2E - mxl);
-      float p1 = ex2(__uint_as_float(v[2 * j + 1]) * LOG2E - mxl);
-      sum += p0 + p1;
-      pk[j] = pack2(p0, p1);
-    }
-#pragma unroll
-    for (int c = 0; c < 4; ++c)
-      pbuf_store8(sP, t, (c0 >> 3) + c, make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2],
-                                                   pk[4 * c + 3]));
-  }
-  fence_proxy_async_smem();
+  if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
   __syncthreads();
-  if (t == 0) {
-    fence_after();
-    const uint32_t idesc = idesc_bf16(128, D, false, true);
-    for (int ks = 0; ks < Lp / 16; ++ks)
-      umma_bf16(tmem, desc_pbuf(smem_u32(sP), ks), desc_mnmajor_tile<D>(smem_u32(sV), ks), idesc,
-                ks > 0);
-    umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 1);
   fence_after();
-  float o[D];
-  tmem_ld_row<D>(lane_addr, o);
-  if (qv) {
-    const float inv = 1.f / sum;
-    const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D;
-    const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D;
+  const uint32_t tbase = *tslot + 256u * w;                       // lane 0, WG columns
+  const uint32_t lane_addr = tbase + ((uint32_t)((warp & 3) * 32) << 16);
+  if (BIASMODE) mbar_wait(&bars[0], 0);
+
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  uint32_t ph_t = 0, ph_m = 0;
+  const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
+  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+  for (int64_t b = b_lo + w; b < b_hi; b += 2) {
+    if (t == 0) {
+      mbar_expect_tx(tbar, TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
+      tma_load_4d(sQ, &mQ, tbar, 0, q0, (int)b, h);
+      tma_load_4d(sK, &mK, tbar, 0, 0, (int)b, h);
+      tma_load_4d(sV, &mV, tbar, 0, 0, (int)b, h);
+      mbar_wait(tbar, ph_t);
+      fence_after();
 #pragma unroll
-    for (int d8 = 0; d8 < D; d8 += 8) {
-      uint4 graw = *reinterpret_cast<const uint4 *>(gp + d8);
-      const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
-      uint32_t ov[4], gv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float o0 = o[d8 + 2 * j] * inv, o1 = o[d8 + 2 * j + 1] * inv;
-        float2 g2 = unpack2(gw[j]);
-        ov[j] = pack2(o0, o1);
-        gv[j] = pack2(g2.x * o0, g2.y * o1);
-      }
-      *reinterpret_cast<uint4 *>(a.o + ooff + d8) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
-      *reinterpret_cast<uint4 *>(a.gm + ooff + d8) = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tbase, desc_kmajor_tile<D>(smem_u32(sQ), ks),
+                  desc_kmajor_tile<D>(smem_u32(sK), ks), idesc_s, ks > 0);
+      umma_commit(mbar);
     }
-    a.lse[(b * a.H + h) * (int64_t)L + q] = mx + logf(sum);
+    ph_t ^= 1;
+    mbar_wait(mbar, ph_m);
+    ph_m ^= 1;
+    fence_after();
+    // pass 1: s = scale*acc + bias (masked keys -> -inf), row max, write back
+    float mx = -INFINITY;
+    for (int c0 = 0; c0 < Lp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(lane_addr + c0, v);
+      float bb[32];
+      if (BIASMODE) bias_row32<TB>(sBias, t, c0, bb);
+#pragma unroll
+      for (int j = 0; j < 32; ++j) {
+        float s = __uint_as_float(v[j]) * a.scale;
+        if (BIASMODE) s += bb[j];
+        s = (c0 + j < L) ? s : -INFINITY;
+        mx = fmaxf(mx, s);
+        v[j] = __float_as_uint(s);
+      }
+      tmem_st32(lane_addr + c0, v);
+    }
+    tmem_st_wait();
+    // pass 2: p = exp(s - max) -> bf16 pairs in place (cols c0/2 ..), row sum
+    float sum = 0.f;
+    const float mxl = mx * LOG2E;
+    for (int c0 = 0; c0 < Lp; c0 += 32) {
+      uint32_t v[32];
+      tmem_ld32(lane_addr + c0, v);
+      uint32_t pk[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        float p0 = ex2(__uint_as_float(v[2 * j]) * LOG2E - mxl);
+        float p1 = ex2(__uint_as_float(v[2 * j + 1]) * LOG2E - mxl);
+        sum += p0 + p1;
+        pk[j] = pack2(p0, p1);
+      }
+      tmem_st16(lane_addr + (c0 >> 1), pk);
+    }
+    tmem_st_wait();
+    fence_before();
+    named_bar_sync(1 + w, 128);
+    if (t == 0) {
+      fence_after();
+      for (int ks = 0; ks < Lp / 16; ++ks)
+        umma_bf16_ts(tbase + 128, tbase + ks * 8, desc_mnmajor_tile<D>(smem_u32(sV), ks),
+                     idesc_o, ks > 0);
+      umma_commit(mbar);
+    }
+    mbar_wait(mbar, ph_m);
+    ph_m ^= 1;
+    fence_after();
+    float o[D];
+    tmem_ld_row<D>(lane_addr + 128, o);
+    if (qv) {
+      const float inv = 1.f / sum;
+      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D;
+      const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D;
+#pragma unroll
+      for (int d8 = 0; d8 < D; d8 += 8) {
+        uint4 graw = *reinterpret_cast<const uint4 *>(gp + d8);
+        const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
+        uint32_t ov[4], gv[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          float o0 = o[d8 + 2 * j] * inv, o1 = o[d8 + 2 * j + 1] * inv;
+          float2 g2 = unpack2(gw[j]);
+          ov[j] = pack2(o0, o1);
+          gv[j] = pack2(g2.x * o0, g2.y * o1);
+        }
+        *reinterpret_cast<uint4 *>(a.o + ooff + d8) = make_uint4(ov[0], ov[1], ov[2], ov[3]);
+        *reinterpret_cast<uint4 *>(a.gm + ooff + d8) = make_uint4(gv[0], gv[1], gv[2], gv[3]);
+      }
+      a.lse[(b * a.H + h) * (int64_t)L + q] = mx + logf(sum);
+    }
+    fence_before();
+    named_bar_sync(1 + w, 128);  // TMEM + smem of this WG free for the next row
+    fence_after();
   }
   fence_before();
   __syncthreads();
-  if (warp == 0) tmem_dealloc(tmem, 256);
+  if (warp == 0) tmem_dealloc(*tslot, 512);
 }
 
 // ===================================================================== prep
@@ -672,26 +736,80 @@ int64_t dq_chunks(const evo_attn_desc *d) {
   return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
 }
 
-size_t fwd_smem(int D) { return 1024 + PBYTES + (size_t)QT * 2 * D + 2 * 256 * 2 * D + 64; }
 size_t dq_smem(int D) { return 1024 + PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 64; }
 size_t dkv_smem(int D) {
   return 1024 + 2 * PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 2 * 256 * 4 + 64;
 }
 
-template <int D>
-int fwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+// 3-D map over the fp32 bias buffer: plain {k, q, h} / transposed {q, k, h}
+bool bias_map(CUtensorMap *m, const evo_attn_desc *d, bool transposed) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const int L = d->L;
+  cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)L, (cuuint64_t)d->H};
+  cuuint64_t strides[2];
+  cuuint32_t box[3], es[3] = {1, 1, 1};
+  if (!transposed) {  // inner = k (stride 1), outer = q (stride bq)
+    strides[0] = (cuuint64_t)d->bq * 4;
+    box[0] = 32; box[1] = 128;
+  } else {            // inner = q (stride 1), outer = k (stride bk)
+    strides[0] = (cuuint64_t)d->bk * 4;
+    box[0] = 128; box[1] = 32;
+  }
+  strides[1] = (cuuint64_t)d->bh * 4;
+  box[2] = 1;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(d->bias), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            transposed ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+int bias_mode(const evo_attn_desc *d) {
+  if (!d->bias) return 0;
+  if (d->bk == 1 && d->bq % 4 == 0 && d->bh % 4 == 0) return 1;
+  if (d->bq == 1 && d->bk % 4 == 0 && d->bh % 4 == 0) return 2;
+  return -1;
+}
+
+int64_t row_chunks(const evo_attn_desc *d) {
+  int64_t tiles = (int64_t)d->H * ((d->L + QT - 1) / QT);
+  int64_t want = ((int64_t)num_sms() + tiles - 1) / tiles;
+  return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
+}
+
+template <int D, int BM_>
+int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   AttnTcArgs a = make_args(d);
-  CUtensorMap mq, mk, mv;
+  CUtensorMap mq, mk, mv, mb;
   if (!head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp) ||
       !head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp))
     return EVO_EUNSUP;
-  size_t smem = fwd_smem(D);
-  EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D>));
-  dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
-  attn_fwd_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, a);
+  if (BM_) {
+    if (!bias_map(&mb, d, BM_ == 2)) return EVO_EUNSUP;
+  } else {
+    mb = mq;  // unused
+  }
+  int64_t nch = row_chunks(d);
+  a.chunk = (d->nb + nch - 1) / nch;
+  nch = (d->nb + a.chunk - 1) / a.chunk;
+  const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) +
+                      2 * ((size_t)QT * 2 * D + 2 * 256 * 2 * D) + 128;
+  EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D, BM_>));
+  dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
+  attn_fwd_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_fwd_tc_kernel");
   return EVO_OK;
+}
+
+template <int D>
+int fwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+  switch (bias_mode(d)) {
+    case 0: return fwd_launch_mode<D, 0>(d, st);
+    case 1: return fwd_launch_mode<D, 1>(d, st);
+    case 2: return fwd_launch_mode<D, 2>(d, st);
+  }
+  return EVO_EUNSUP;
 }
 
 template <int D>
@@ -755,6 +873,7 @@ bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 
 
 bool attention_tc_accepts(const evo_attn_desc *d) {
   if (d->dtype != EVO_BF16) return false;
+  if (bias_mode(d) < 0) return false;
   // D=64 would need 229 KB of smem in the dk/dv kernel: SIMT path
   if (!(d->D == 16 || d->D == 32)) return false;
   if (d->L < 1 || d->L > 256 || d->nb < 1 || d->nb > 65535) return false;
