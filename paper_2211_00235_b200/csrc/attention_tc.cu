@@ -204,8 +204,8 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
                                             ~uintptr_t(1023));
   uint8_t *sBias = sm;
   uint8_t *sWG = sBias + (BIASMODE ? BIAS_BYTES : 0);
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sWG + 2 * WGB);  // 0 bias, 1-2 tma, 3-4 mma
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 5);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sWG + 2 * WGB);  // 0 bias, 1-2 qk, 3-4 mma, 5-6 v
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 7);
 
   const int tid = threadIdx.x, warp = tid >> 5;
   const int w = tid >> 7, t = tid & 127;
@@ -220,7 +220,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
   uint64_t *mbar = &bars[3 + w];
 
   if (tid == 0) {
-    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 7; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, Lp);
   }
@@ -234,16 +234,24 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
 
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
-  uint32_t ph_t = 0, ph_m = 0;
+  uint32_t ph_qk = 0, ph_v = 0, ph_m = 0;
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+  const uint32_t kv_bytes = (uint32_t)Lp * Sw<D>::bytes;
+  uint64_t *qkbar = tbar, *vbar = &bars[5 + w];
+  // prologue: loads for the WG's first row
+  if (t == 0 && b_lo + w < b_hi) {
+    const int b0 = (int)(b_lo + w);
+    mbar_expect_tx(qkbar, TILE + kv_bytes);
+    tma_load_4d(sQ, &mQ, qkbar, 0, q0, b0, h);
+    tma_load_4d(sK, &mK, qkbar, 0, 0, b0, h);
+    mbar_expect_tx(vbar, kv_bytes);
+    tma_load_4d(sV, &mV, vbar, 0, 0, b0, h);
+  }
   for (int64_t b = b_lo + w; b < b_hi; b += 2) {
+    const bool has_next = b + 2 < b_hi;
     if (t == 0) {
-      mbar_expect_tx(tbar, TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
-      tma_load_4d(sQ, &mQ, tbar, 0, q0, (int)b, h);
-      tma_load_4d(sK, &mK, tbar, 0, 0, (int)b, h);
-      tma_load_4d(sV, &mV, tbar, 0, 0, (int)b, h);
-      mbar_wait(tbar, ph_t);
+      mbar_wait(qkbar, ph_qk);
       fence_after();
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks)
@@ -251,10 +259,22 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
                   desc_kmajor_tile<D>(smem_u32(sK), ks), idesc_s, ks > 0);
       umma_commit(mbar);
     }
-    ph_t ^= 1;
+    ph_qk ^= 1;
+    // gate row prefetch (consumed in the epilogue)
+    uint4 graw[D / 8];
+    if (qv) {
+      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D;
+#pragma unroll
+      for (int i = 0; i < D / 8; ++i) graw[i] = *reinterpret_cast<const uint4 *>(gp + 8 * i);
+    }
     mbar_wait(mbar, ph_m);
     ph_m ^= 1;
     fence_after();
+    if (t == 0 && has_next) {  // Q, K consumed by the S MMA: prefetch the next row's
+      mbar_expect_tx(qkbar, TILE + kv_bytes);
+      tma_load_4d(sQ, &mQ, qkbar, 0, q0, (int)(b + 2), h);
+      tma_load_4d(sK, &mK, qkbar, 0, 0, (int)(b + 2), h);
+    }
     // pass 1: s = scale*acc + bias (masked keys -> -inf), row max, write back
     float mx = -INFINITY;
     for (int c0 = 0; c0 < Lp; c0 += 32) {
@@ -293,25 +313,29 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
     fence_before();
     named_bar_sync(1 + w, 128);
     if (t == 0) {
+      mbar_wait(vbar, ph_v);
       fence_after();
       for (int ks = 0; ks < Lp / 16; ++ks)
         umma_bf16_ts(tbase + 128, tbase + ks * 8, desc_mnmajor_tile<D>(smem_u32(sV), ks),
                      idesc_o, ks > 0);
       umma_commit(mbar);
     }
+    ph_v ^= 1;
     mbar_wait(mbar, ph_m);
     ph_m ^= 1;
     fence_after();
+    if (t == 0 && has_next) {  // V consumed: prefetch the next row's
+      mbar_expect_tx(vbar, kv_bytes);
+      tma_load_4d(sV, &mV, vbar, 0, 0, (int)(b + 2), h);
+    }
     float o[D];
     tmem_ld_row<D>(lane_addr + 128, o);
     if (qv) {
       const float inv = 1.f / sum;
-      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D;
       const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D;
 #pragma unroll
       for (int d8 = 0; d8 < D; d8 += 8) {
-        uint4 graw = *reinterpret_cast<const uint4 *>(gp + d8);
-        const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
+        const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw[d8 / 8]);
         uint32_t ov[4], gv[4];
 #pragma unroll
         for (int j = 0; j < 4; ++j) {
@@ -326,7 +350,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
       a.lse[(b * a.H + h) * (int64_t)L + q] = mx + logf(sum);
     }
     fence_before();
-    named_bar_sync(1 + w, 128);  // TMEM + smem of this WG free for the next row
+    named_bar_sync(1 + w, 128);  // TMEM of this WG free for the next row
     fence_after();
   }
   fence_before();
