@@ -399,185 +399,241 @@ __global__ void attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm, bf16 *
 }
 
 // ======================================================================= dq
-template <int D>
-__global__ void __launch_bounds__(128)
+// CTA = (128-query tile, head, chunk of batch rows); 256 threads, two per
+// query row (half hf = warp/4 owns keys [hf*Lp/2, (hf+1)*Lp/2)).
+// TMEM: [0,256) dbias accumulator (persists over the chunk), [256, 256+Lp)
+// S -> P (bf16 pairs, [256, 256+Lp/2)) -> dS (over P), [384, 512) dP rounds
+// of 128 keys, then dQ.
+template <int D, int BIASMODE>
+__global__ void __launch_bounds__(256)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV,
-                      const __grid_constant__ CUtensorMap mdO, const AttnTcArgs a) {
+                      const __grid_constant__ CUtensorMap mdO,
+                      const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr bool TB = BIASMODE == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                             ~uintptr_t(1023));
-  uint8_t *sP = sm;  // P, then dS (bf16, SW128 K-major [128 x 256])
-  uint8_t *sQ = sP + PBYTES;
+  uint8_t *sBias = sm;
+  uint8_t *sQ = sBias + (BIASMODE ? BIAS_BYTES : 0);
   uint8_t *sdO = sQ + TILE;
   uint8_t *sK = sdO + TILE;
   uint8_t *sV = sK + FULL;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);  // 0: tma, 1: mma
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);  // 0 bias, 1 q/dO/V, 2 K, 3 mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 4);
 
-  const int t = threadIdx.x, warp = t >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = (warp & 3) * 32 + lane;  // query row in the tile
+  const int hf = warp >> 2;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
-  const int L = a.L, Lp = a.Lp;
+  const int L = a.L, Lp = a.Lp, half = Lp / 2;
   const int q = q0 + t;
   const bool qv = q < L;
   const bool want_bias = a.dbias_part != nullptr;
 
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, Lp);
   }
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
-  const uint32_t acc_db = lane_addr;        // cols [0, 256): dbias accumulator
-  const uint32_t work = lane_addr + 256;    // cols [256, 512): S -> dP -> dq
+  const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const uint32_t ACC = 0, SP = 256, DP = 384;
   if (want_bias) {
     uint32_t z[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) z[j] = 0u;
-    for (int c0 = 0; c0 < Lp; c0 += 32) tmem_st32(acc_db + c0, z);
+    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) tmem_st32(lane_addr + ACC + c0, z);
     tmem_st_wait();
   }
-  uint32_t tphase = 0, mphase = 0;
+  if (BIASMODE) mbar_wait(&bars[0], 0);
+
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  uint32_t ph_a = 0, ph_k = 0, ph_m = 0;
+  const uint32_t kv_bytes = (uint32_t)Lp * Sw<D>::bytes;
+  auto load_qdv = [&](int64_t bb) {
+    mbar_expect_tx(&bars[1], 2 * TILE + kv_bytes);
+    tma_load_4d(sQ, &mQ, &bars[1], 0, q0, (int)bb, h);
+    tma_load_4d(sdO, &mdO, &bars[1], 0, q0, (int)bb, h);
+    tma_load_4d(sV, &mV, &bars[1], 0, 0, (int)bb, h);
+  };
+  auto load_k = [&](int64_t bb) {
+    mbar_expect_tx(&bars[2], kv_bytes);
+    tma_load_4d(sK, &mK, &bars[2], 0, 0, (int)bb, h);
+  };
+  if (tid == 0 && b_lo < b_hi) {
+    load_qdv(b_lo);
+    load_k(b_lo);
+  }
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
-    if (t == 0) {
-      mbar_expect_tx(&bars[0], 2 * TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
-      tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
-      tma_load_4d(sdO, &mdO, &bars[0], 0, q0, (int)b, h);
-      tma_load_4d(sK, &mK, &bars[0], 0, 0, (int)b, h);
-      tma_load_4d(sV, &mV, &bars[0], 0, 0, (int)b, h);
-      mbar_wait(&bars[0], tphase);
+    const bool has_next = b + 1 < b_hi;
+    if (tid == 0) {
+      mbar_wait(&bars[1], ph_a);
+      mbar_wait(&bars[2], ph_k);
       fence_after();
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks)
-        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sQ), ks),
+        umma_bf16(tmem + SP, desc_kmajor_tile<D>(smem_u32(sQ), ks),
                   desc_kmajor_tile<D>(smem_u32(sK), ks), idesc_s, ks > 0);
-      umma_commit(&bars[1]);
+      umma_commit(&bars[3]);
     }
-    tphase ^= 1;
-    mbar_wait(&bars[1], mphase);
-    mphase ^= 1;
-    fence_after();
+    ph_a ^= 1;
+    ph_k ^= 1;
     const float lse_l2 = qv ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E : 0.f;
     const float Dq = qv ? a.Dq[(b * a.H + h) * (int64_t)L + q] : 0.f;
-    // P = exp(scale*S + bias - lse) -> smem (bf16)
-    for (int c0 = 0; c0 < Lp; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(work + c0, v);
-      uint32_t pk[16];
-#pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float p[2];
-#pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int k = c0 + j + u;
-          float s = __uint_as_float(v[j + u]) * a.scale;
-          if (a.bias && qv && k < L) s += bias_at(a, h, q, k);
-          p[u] = (qv && k < L) ? ex2(s * LOG2E - lse_l2) : 0.f;
-        }
-        pk[j >> 1] = pack2(p[0], p[1]);
-      }
-#pragma unroll
-      for (int c = 0; c < 4; ++c)
-        pbuf_store8(sP, t, (c0 >> 3) + c,
-                    make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
-    }
-    // dP = dO V^T  -> work cols (S consumed: all threads passed tcgen05.ld)
-    fence_before();
-    __syncthreads();
-    if (t == 0) {
-      fence_after();
-#pragma unroll
-      for (int ks = 0; ks < D / 16; ++ks)
-        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sdO), ks),
-                  desc_kmajor_tile<D>(smem_u32(sV), ks), idesc_s, ks > 0);
-      umma_commit(&bars[1]);
-    }
-    mbar_wait(&bars[1], mphase);
-    mphase ^= 1;
+    mbar_wait(&bars[3], ph_m);
+    ph_m ^= 1;
     fence_after();
-    // dS = P * (dP - Dq); dbias += dS; dS (bf16) overwrites P in smem
-    for (int c0 = 0; c0 < Lp; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(work + c0, v);
-      uint32_t acc[32];
-      if (want_bias) {
-        asm volatile("" ::: "memory");
-        tmem_ld32(acc_db + c0, acc);
-      }
+    // P = exp(scale*S + bias - lse) for this thread's keys, staged packed
+    uint32_t stage[64];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        uint4 praw = pbuf_load8(sP, t, (c0 >> 3) + c);
-        const uint32_t *pw = reinterpret_cast<const uint32_t *>(&praw);
-        uint32_t dsv[4];
+    for (int i = 0; i < 4; ++i) {
+      const int c0 = hf * half + 32 * i;
+      if (32 * i < half) {
+        uint32_t v[32];
+        tmem_ld32(lane_addr + SP + c0, v);
+        float bb[32];
+        if (BIASMODE) bias_row32<TB>(sBias, t, c0, bb);
 #pragma unroll
-        for (int j = 0; j < 4; ++j) {
-          float2 p2 = unpack2(pw[j]);
-          const int i0 = 8 * c + 2 * j;
-          float ds0 = p2.x * (__uint_as_float(v[i0]) - Dq);
-          float ds1 = p2.y * (__uint_as_float(v[i0 + 1]) - Dq);
-          if (want_bias) {
-            acc[i0] = __float_as_uint(__uint_as_float(acc[i0]) + ds0);
-            acc[i0 + 1] = __float_as_uint(__uint_as_float(acc[i0 + 1]) + ds1);
+        for (int j = 0; j < 32; j += 2) {
+          float p[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int k = c0 + j + u;
+            float sc = __uint_as_float(v[j + u]) * a.scale;
+            if (BIASMODE) sc += bb[j + u];
+            p[u] = (qv && k < L) ? ex2(sc * LOG2E - lse_l2) : 0.f;
           }
-          dsv[j] = pack2(ds0, ds1);
+          stage[16 * i + (j >> 1)] = pack2(p[0], p[1]);
         }
-        pbuf_store8(sP, t, (c0 >> 3) + c, make_uint4(dsv[0], dsv[1], dsv[2], dsv[3]));
       }
-      if (want_bias) tmem_st32(acc_db + c0, acc);
     }
-    if (want_bias) tmem_st_wait();
-    fence_proxy_async_smem();
+    fence_before();
+    __syncthreads();  // every S read done before P overwrites it
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      if (32 * i < half) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) pk[j] = stage[16 * i + j];
+        tmem_st16(lane_addr + SP + ((hf * half + 32 * i) >> 1), pk);
+      }
+    }
+    tmem_st_wait();
+    // dP in rounds of 128 keys into [DP, DP+128); dS over P; dbias += dS
+    for (int r0 = 0; r0 < Lp; r0 += 128) {
+      const int nr = min(128, Lp - r0);
+      fence_before();
+      __syncthreads();
+      if (tid == 0) {
+        fence_after();
+        const uint32_t idesc_dp = idesc_bf16(128, nr, false, false);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          umma_bf16(tmem + DP, desc_kmajor_tile<D>(smem_u32(sdO), ks),
+                    desc_kmajor_tile<D>(smem_u32(sV) + r0 * Sw<D>::bytes, ks), idesc_dp, ks > 0);
+        umma_commit(&bars[3]);
+      }
+      mbar_wait(&bars[3], ph_m);
+      ph_m ^= 1;
+      fence_after();
+      for (int c0 = r0 + hf * (nr / 2); c0 < r0 + (hf + 1) * (nr / 2); c0 += 32) {
+        uint32_t dv[32], pv[16], acc[32];
+        tmem_ld32(lane_addr + DP + (c0 - r0), dv);
+        tmem_ld16(lane_addr + SP + (c0 >> 1), pv);
+        if (want_bias) tmem_ld32(lane_addr + ACC + c0, acc);
+        uint32_t dsk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float2 p2 = unpack2(pv[j]);
+          float ds0 = p2.x * (__uint_as_float(dv[2 * j]) - Dq);
+          float ds1 = p2.y * (__uint_as_float(dv[2 * j + 1]) - Dq);
+          if (want_bias) {
+            acc[2 * j] = __float_as_uint(__uint_as_float(acc[2 * j]) + ds0);
+            acc[2 * j + 1] = __float_as_uint(__uint_as_float(acc[2 * j + 1]) + ds1);
+          }
+          dsk[j] = pack2(ds0, ds1);
+        }
+        tmem_st16(lane_addr + SP + (c0 >> 1), dsk);
+        if (want_bias) tmem_st32(lane_addr + ACC + c0, acc);
+      }
+      tmem_st_wait();
+    }
     fence_before();
     __syncthreads();
-    if (t == 0) {
+    if (tid == 0) {
       fence_after();
+      if (has_next) load_qdv(b + 1);  // Q, dO, V consumed by the S / dP MMAs
       for (int ks = 0; ks < Lp / 16; ++ks)
-        umma_bf16(tmem + 256, desc_pbuf(smem_u32(sP), ks), desc_mnmajor_tile<D>(smem_u32(sK), ks),
-                  idesc_o, ks > 0);
-      umma_commit(&bars[1]);
+        umma_bf16_ts(tmem + DP, tmem + SP + ks * 8, desc_mnmajor_tile<D>(smem_u32(sK), ks),
+                     idesc_o, ks > 0);
+      umma_commit(&bars[3]);
     }
-    mbar_wait(&bars[1], mphase);
-    mphase ^= 1;
+    mbar_wait(&bars[3], ph_m);
+    ph_m ^= 1;
     fence_after();
-    float dq[D];
-    tmem_ld_row<D>(work, dq);
-    if (qv) {
-      bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D;
+    if (tid == 0 && has_next) load_k(b + 1);
+    {
+      constexpr int HD = D / 2;  // each half stores D/2 columns of dq
+      float dq[HD];
+      uint32_t v[16];
+      if constexpr (HD == 16) {
+        tmem_ld16(lane_addr + DP + hf * 16, v);
 #pragma unroll
-      for (int d8 = 0; d8 < D; d8 += 8) {
-        uint32_t w[4];
+        for (int j = 0; j < 16; ++j) dq[j] = __uint_as_float(v[j]);
+      } else {
+        uint32_t v8[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v8[0]), "=r"(v8[1]), "=r"(v8[2]), "=r"(v8[3]), "=r"(v8[4]), "=r"(v8[5]),
+              "=r"(v8[6]), "=r"(v8[7])
+            : "r"(lane_addr + DP + hf * 8));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-        for (int j = 0; j < 4; ++j)
-          w[j] = pack2(dq[d8 + 2 * j] * a.scale, dq[d8 + 2 * j + 1] * a.scale);
-        *reinterpret_cast<uint4 *>(dst + d8) = make_uint4(w[0], w[1], w[2], w[3]);
+        for (int j = 0; j < HD; ++j) dq[j] = __uint_as_float(v8[j]);
+      }
+      if (qv) {
+        bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D + hf * HD;
+#pragma unroll
+        for (int d8 = 0; d8 < HD; d8 += 8) {
+          uint32_t w4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            w4[j] = pack2(dq[d8 + 2 * j] * a.scale, dq[d8 + 2 * j + 1] * a.scale);
+          *reinterpret_cast<uint4 *>(dst + d8) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        }
       }
     }
     fence_before();
-    __syncthreads();  // smem tiles / TMEM work cols free for the next row
+    __syncthreads();  // TMEM work columns free for the next row
     fence_after();
   }
   if (want_bias) {
     float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L;
-    for (int c0 = 0; c0 < Lp; c0 += 32) {
+    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) {
       uint32_t v[32];
-      tmem_ld32(acc_db + c0, v);  // warp-collective: every lane loads
+      tmem_ld32(lane_addr + ACC + c0, v);  // warp-collective: every lane loads
       if (!qv) continue;
-      for (int j = 0; j < 32; ++j) {
-        const int k = c0 + j;
-        if (k < L)
-          dst[(int64_t)h * a.bh + (int64_t)q * a.bq + (int64_t)k * a.bk] = __uint_as_float(v[j]);
+      const int64_t rb = (int64_t)h * a.bh + (int64_t)q * a.bq;
+      if (a.bk == 1 && c0 + 32 <= L && ((rb + c0) & 3) == 0) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          reinterpret_cast<float4 *>(dst + rb + c0)[j] =
+              make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
+                          __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
+      } else {
+        for (int j = 0; j < 32; ++j)
+          if (c0 + j < L) dst[rb + (int64_t)(c0 + j) * a.bk] = __uint_as_float(v[j]);
       }
     }
   }
@@ -587,132 +643,215 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 }
 
 // ====================================================================== dkv
-template <int D>
-__global__ void __launch_bounds__(128)
+// CTA = (128-key tile, head, chunk of batch rows); 256 threads, two per key
+// row (half hf owns queries [hf*Lp/2, (hf+1)*Lp/2)).  Bias tile for the key
+// tile and all queries stays in smem.  TMEM: S^T [0, Lp), dP^T [256, 256+Lp);
+// P^T / dS^T bf16 pairs written in place inside each half's own columns:
+// half 0 -> [0, Lp/4), half 1 -> [Lp/2, 3Lp/4) (and +256 for dS^T).
+template <bool TBK>  // keys contiguous in smem tile (plain bias) ?
+__device__ __forceinline__ void load_bias_tile_k(uint8_t *sb, const CUtensorMap *map,
+                                                 uint64_t *bar, int h, int k0, int Lp) {
+  const int nbox = (Lp + 31) / 32;
+  mbar_expect_tx(bar, (uint32_t)nbox * 16384u);
+  for (int j = 0; j < nbox; ++j) {
+    if constexpr (TBK)
+      tma_load_3d(sb + j * 16384, map, bar, k0, 32 * j, h);   // {k inner 128, 32 q}
+    else
+      tma_load_3d(sb + j * 16384, map, bar, 32 * j, k0, h);   // {32 q inner, 128 k}
+  }
+}
+
+__device__ __forceinline__ uint32_t half_col(int c, int Lp) {
+  return (uint32_t)(c < Lp / 2 ? c / 2 : Lp / 2 + (c - Lp / 2) / 2);
+}
+
+template <int D, int BIASMODE>
+__global__ void __launch_bounds__(256)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_constant__ CUtensorMap mVt,
                        const __grid_constant__ CUtensorMap mQa,
-                       const __grid_constant__ CUtensorMap mdOa, const AttnTcArgs a) {
+                       const __grid_constant__ CUtensorMap mdOa,
+                       const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  // plain bias (bk == 1): smem [q][128 k] (keys contiguous, read by column)
+  // transposed (bq == 1): 32-query boxes [k][32 q], 128B-swizzled rows
+  constexpr bool KCONTIG = BIASMODE == 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                             ~uintptr_t(1023));
-  uint8_t *sPt = sm;              // P^T  [128 keys x 256 queries] bf16 SW128
-  uint8_t *sdSt = sPt + PBYTES;   // dS^T
-  uint8_t *sK = sdSt + PBYTES;
-  uint8_t *sV = sK + TILE;
-  uint8_t *sQ = sV + TILE;
+  uint8_t *sBias = sm;
+  uint8_t *sQ = sBias + (BIASMODE ? BIAS_BYTES : 0);
   uint8_t *sdO = sQ + FULL;
-  float *sLse = reinterpret_cast<float *>(sdO + FULL);
+  uint8_t *sK = sdO + FULL;
+  uint8_t *sV = sK + TILE;
+  float *sLse = reinterpret_cast<float *>(sV + TILE);
   float *sDq = sLse + 256;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 2);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);  // 0 bias, 1 K/V, 2 Q/dO, 3 mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 4);
 
-  const int t = threadIdx.x, warp = t >> 5;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = (warp & 3) * 32 + lane;  // key row in the tile
+  const int hf = warp >> 2;
   const int k0 = blockIdx.x * QT, h = blockIdx.y;
-  const int64_t b = blockIdx.z;
-  const int L = a.L, Lp = a.Lp;
+  const int L = a.L, Lp = a.Lp, half = Lp / 2;
   const int k = k0 + t;
   const bool kv = k < L;
 
-  if (t == 0) {
-    mbar_init(&bars[0], 1);
-    mbar_init(&bars[1], 1);
+  if (tid == 0) {
+    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars[0], h, k0, Lp);
   }
   if (warp == 0) tmem_alloc(tslot, 512);
-  for (int i = t; i < Lp; i += 128) {
-    const bool ok = i < L;
-    sLse[i] = ok ? a.lse[(b * a.H + h) * (int64_t)L + i] * LOG2E : 0.f;
-    sDq[i] = ok ? a.Dq[(b * a.H + h) * (int64_t)L + i] : 0.f;
-  }
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
-  const uint32_t lane_addr = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  if (BIASMODE) mbar_wait(&bars[0], 0);
+  const uint32_t DVC = Lp >= 256 ? 64u : 128u;  // free columns for dV (and +256 for dK)
 
-  if (t == 0) {
-    mbar_expect_tx(&bars[0], 2 * TILE + 2 * (uint32_t)Lp * Sw<D>::bytes);
-    tma_load_4d(sK, &mKt, &bars[0], 0, k0, (int)b, h);
-    tma_load_4d(sV, &mVt, &bars[0], 0, k0, (int)b, h);
-    tma_load_4d(sQ, &mQa, &bars[0], 0, 0, (int)b, h);
-    tma_load_4d(sdO, &mdOa, &bars[0], 0, 0, (int)b, h);
-    mbar_wait(&bars[0], 0);
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  uint32_t ph_kv = 0, ph_q = 0, ph_m = 0;
+  const uint32_t all_bytes = (uint32_t)Lp * Sw<D>::bytes;
+  auto load_kv = [&](int64_t bb) {
+    mbar_expect_tx(&bars[1], 2 * TILE);
+    tma_load_4d(sK, &mKt, &bars[1], 0, k0, (int)bb, h);
+    tma_load_4d(sV, &mVt, &bars[1], 0, k0, (int)bb, h);
+  };
+  auto load_q = [&](int64_t bb) {
+    mbar_expect_tx(&bars[2], 2 * all_bytes);
+    tma_load_4d(sQ, &mQa, &bars[2], 0, 0, (int)bb, h);
+    tma_load_4d(sdO, &mdOa, &bars[2], 0, 0, (int)bb, h);
+  };
+  if (tid == 0 && b_lo < b_hi) {
+    load_kv(b_lo);
+    load_q(b_lo);
+  }
+  const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
+  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+
+  for (int64_t b = b_lo; b < b_hi; ++b) {
+    const bool has_next = b + 1 < b_hi;
+    if (tid == 0) {
+      mbar_wait(&bars[1], ph_kv);
+      mbar_wait(&bars[2], ph_q);
+      fence_after();
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sK), ks),
+                  desc_kmajor_tile<D>(smem_u32(sQ), ks), idesc_s, ks > 0);
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sV), ks),
+                  desc_kmajor_tile<D>(smem_u32(sdO), ks), idesc_s, ks > 0);
+      umma_commit(&bars[3]);
+    }
+    ph_kv ^= 1;
+    ph_q ^= 1;
+    for (int i = tid; i < Lp; i += 256) {
+      const bool ok = i < L;
+      sLse[i] = ok ? a.lse[(b * a.H + h) * (int64_t)L + i] * LOG2E : 0.f;
+      sDq[i] = ok ? a.Dq[(b * a.H + h) * (int64_t)L + i] : 0.f;
+    }
+    mbar_wait(&bars[3], ph_m);
+    ph_m ^= 1;
     fence_after();
-    const uint32_t idesc = idesc_bf16(128, Lp, false, false);
+    __syncthreads();  // lse / Dq visible
+    if (tid == 0 && has_next) load_kv(b + 1);  // K, V tiles consumed
+    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) {
+      uint32_t sv[32], dv[32];
+      tmem_ld32(lane_addr + c0, sv);
+      tmem_ld32(lane_addr + 256 + c0, dv);
+      float bb[32];
+      if (BIASMODE) bias_row32<!KCONTIG>(sBias, t, c0, bb);
+      uint32_t pk[16], dk[16];
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sK), ks), desc_kmajor_tile<D>(smem_u32(sQ), ks),
-                idesc, ks > 0);
+      for (int j = 0; j < 32; j += 2) {
+        float p[2], ds[2];
 #pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sV), ks),
-                desc_kmajor_tile<D>(smem_u32(sdO), ks), idesc, ks > 0);
-    umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 0);
-  fence_after();
-  for (int c0 = 0; c0 < Lp; c0 += 32) {
-    uint32_t sv[32], dv[32];
-    tmem_ld32(lane_addr + c0, sv);
-    tmem_ld32(lane_addr + 256 + c0, dv);
-    uint32_t pk[16], dk[16];
-#pragma unroll
-    for (int j = 0; j < 32; j += 2) {
-      float p[2], ds[2];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int qq = c0 + j + u;
-        float s = __uint_as_float(sv[j + u]) * a.scale;
-        const bool ok = kv && qq < L;
-        if (a.bias && ok) s += bias_at(a, h, qq, k);
-        p[u] = ok ? ex2(s * LOG2E - sLse[qq]) : 0.f;
-        ds[u] = p[u] * (__uint_as_float(dv[j + u]) - sDq[qq]);
+        for (int u = 0; u < 2; ++u) {
+          const int qq = c0 + j + u;
+          float s = __uint_as_float(sv[j + u]) * a.scale;
+          if (BIASMODE) s += bb[j + u];
+          const bool ok = kv && qq < L;
+          p[u] = ok ? ex2(s * LOG2E - sLse[qq]) : 0.f;
+          ds[u] = p[u] * (__uint_as_float(dv[j + u]) - sDq[qq]);
+        }
+        pk[j >> 1] = pack2(p[0], p[1]);
+        dk[j >> 1] = pack2(ds[0], ds[1]);
       }
-      pk[j >> 1] = pack2(p[0], p[1]);
-      dk[j >> 1] = pack2(ds[0], ds[1]);
+      const uint32_t dc = half_col(c0, Lp);
+      tmem_st16(lane_addr + dc, pk);
+      tmem_st16(lane_addr + 256 + dc, dk);
     }
-#pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      pbuf_store8(sPt, t, (c0 >> 3) + c,
-                  make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]));
-      pbuf_store8(sdSt, t, (c0 >> 3) + c,
-                  make_uint4(dk[4 * c], dk[4 * c + 1], dk[4 * c + 2], dk[4 * c + 3]));
+    tmem_st_wait();
+    fence_before();
+    __syncthreads();
+    if (tid == 0) {
+      fence_after();
+      for (int ks = 0; ks < Lp / 16; ++ks)
+        umma_bf16_ts(tmem + DVC, tmem + half_col(16 * ks, Lp),
+                     desc_mnmajor_tile<D>(smem_u32(sdO), ks), idesc_o, ks > 0);
+      for (int ks = 0; ks < Lp / 16; ++ks)
+        umma_bf16_ts(tmem + 256 + DVC, tmem + 256 + half_col(16 * ks, Lp),
+                     desc_mnmajor_tile<D>(smem_u32(sQ), ks), idesc_o, ks > 0);
+      umma_commit(&bars[3]);
     }
-  }
-  fence_proxy_async_smem();
-  fence_before();
-  __syncthreads();
-  if (t == 0) {
+    mbar_wait(&bars[3], ph_m);
+    ph_m ^= 1;
     fence_after();
-    const uint32_t idesc = idesc_bf16(128, D, false, true);
-    for (int ks = 0; ks < Lp / 16; ++ks)
-      umma_bf16(tmem, desc_pbuf(smem_u32(sPt), ks), desc_mnmajor_tile<D>(smem_u32(sdO), ks), idesc,
-                ks > 0);
-    for (int ks = 0; ks < Lp / 16; ++ks)
-      umma_bf16(tmem + 256, desc_pbuf(smem_u32(sdSt), ks), desc_mnmajor_tile<D>(smem_u32(sQ), ks),
-                idesc, ks > 0);
-    umma_commit(&bars[1]);
-  }
-  mbar_wait(&bars[1], 1);
-  fence_after();
-  float dvr[D], dkr[D];
-  tmem_ld_row<D>(lane_addr, dvr);
-  tmem_ld_row<D>(lane_addr + 256, dkr);
-  if (kv) {
-    const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D;
+    if (tid == 0 && has_next) load_q(b + 1);  // Q, dO consumed
+    {
+      constexpr int HD = D / 2;
+      float dvr[HD], dkr[HD];
+      if constexpr (HD == 16) {
+        uint32_t v1[16], v2[16];
+        tmem_ld16(lane_addr + DVC + hf * 16, v1);
+        tmem_ld16(lane_addr + 256 + DVC + hf * 16, v2);
 #pragma unroll
-    for (int d8 = 0; d8 < D; d8 += 8) {
-      uint32_t w1[4], w2[4];
+        for (int j = 0; j < 16; ++j) {
+          dvr[j] = __uint_as_float(v1[j]);
+          dkr[j] = __uint_as_float(v2[j]);
+        }
+      } else {
+        uint32_t v1[8], v2[8];
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]),
+              "=r"(v1[6]), "=r"(v1[7])
+            : "r"(lane_addr + DVC + hf * 8));
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+            : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]),
+              "=r"(v2[6]), "=r"(v2[7])
+            : "r"(lane_addr + 256 + DVC + hf * 8));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        w1[j] = pack2(dvr[d8 + 2 * j], dvr[d8 + 2 * j + 1]);
-        w2[j] = pack2(dkr[d8 + 2 * j] * a.scale, dkr[d8 + 2 * j + 1] * a.scale);
+        for (int j = 0; j < HD; ++j) {
+          dvr[j] = __uint_as_float(v1[j]);
+          dkr[j] = __uint_as_float(v2[j]);
+        }
       }
-      *reinterpret_cast<uint4 *>(a.dv + off + d8) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-      *reinterpret_cast<uint4 *>(a.dk + off + d8) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      if (kv) {
+        const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D + hf * HD;
+#pragma unroll
+        for (int d8 = 0; d8 < HD; d8 += 8) {
+          uint32_t w1[4], w2[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            w1[j] = pack2(dvr[d8 + 2 * j], dvr[d8 + 2 * j + 1]);
+            w2[j] = pack2(dkr[d8 + 2 * j] * a.scale, dkr[d8 + 2 * j + 1] * a.scale);
+          }
+          *reinterpret_cast<uint4 *>(a.dv + off + d8) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+          *reinterpret_cast<uint4 *>(a.dk + off + d8) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+        }
+      }
     }
+    fence_before();
+    __syncthreads();
+    fence_after();
   }
   fence_before();
   __syncthreads();
@@ -753,17 +892,6 @@ AttnTcArgs make_args(const evo_attn_desc *d) {
   return a;
 }
 
-int64_t dq_chunks(const evo_attn_desc *d) {
-  if (!d->dbias) return d->nb;
-  int64_t tiles = (int64_t)d->H * ((d->L + QT - 1) / QT);
-  int64_t want = (2 * (int64_t)num_sms() + tiles - 1) / tiles;
-  return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
-}
-
-size_t dq_smem(int D) { return 1024 + PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 64; }
-size_t dkv_smem(int D) {
-  return 1024 + 2 * PBYTES + 2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D + 2 * 256 * 4 + 64;
-}
 
 // 3-D map over the fp32 bias buffer: plain {k, q, h} / transposed {q, k, h}
 bool bias_map(CUtensorMap *m, const evo_attn_desc *d, bool transposed) {
@@ -836,16 +964,41 @@ int fwd_launch(const evo_attn_desc *d, cudaStream_t st) {
   return EVO_EUNSUP;
 }
 
-template <int D>
-int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+// bias map for the dk/dv kernel: tiles over (all queries) x (128 keys)
+bool bias_map_k(CUtensorMap *m, const evo_attn_desc *d, bool kcontig) {
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return false;
+  const int L = d->L;
+  cuuint64_t dims[3] = {(cuuint64_t)L, (cuuint64_t)L, (cuuint64_t)d->H};
+  cuuint64_t strides[2];
+  cuuint32_t box[3], es[3] = {1, 1, 1};
+  if (kcontig) {  // plain: inner = k (stride 1), outer = q (stride bq); box {128 k, 32 q}
+    strides[0] = (cuuint64_t)d->bq * 4;
+    box[0] = 128; box[1] = 32;
+  } else {        // transposed: inner = q (stride 1), outer = k (stride bk); box {32 q, 128 k}
+    strides[0] = (cuuint64_t)d->bk * 4;
+    box[0] = 32; box[1] = 128;
+  }
+  strides[1] = (cuuint64_t)d->bh * 4;
+  box[2] = 1;
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float *>(d->bias), dims, strides,
+            box, es, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            kcontig ? CU_TENSOR_MAP_SWIZZLE_NONE : CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int D, int BM_>
+int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   AttnTcArgs a = make_args(d);
+  a.Lp = (d->L + 63) / 64 * 64;  // the backward works in 64-key granules
+  const int Lp = a.Lp;
   // workspace: dO (o's strides) | Dq [nb, H, L] | dbias chunk partials
   const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * D;
   const size_t dO_pad = ((size_t)span * 2 + 255) / 256 * 256;
   const size_t Dq_pad = ((size_t)d->nb * d->H * d->L * 4 + 255) / 256 * 256;
-  const int64_t nch = dq_chunks(d);
+  int64_t nch = row_chunks(d);
   const int64_t chunk = (d->nb + nch - 1) / nch;
-  const int64_t nch2 = (d->nb + chunk - 1) / chunk;
+  nch = (d->nb + chunk - 1) / chunk;
   uint8_t *ws = reinterpret_cast<uint8_t *>(d->workspace);
   bf16 *dObuf = reinterpret_cast<bf16 *>(ws);
   float *Dq = reinterpret_cast<float *>(ws + dO_pad);
@@ -861,8 +1014,7 @@ int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
   a.Dq = Dq;
   a.dbias_part = part;
   a.chunk = chunk;
-  CUtensorMap mq, mk, mv, mdo, mqa, mdoa, mkt, mvt;
-  const int Lp = a.Lp;
+  CUtensorMap mq, mk, mv, mdo, mqa, mdoa, mkt, mvt, mb, mbk;
   if (!head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, Lp) ||
       !head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, Lp) ||
@@ -872,23 +1024,42 @@ int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
       !head_map(&mkt, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !head_map(&mvt, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, QT))
     return EVO_EUNSUP;
+  if (BM_) {
+    if (!bias_map(&mb, d, BM_ == 2) || !bias_map_k(&mbk, d, BM_ == 1)) return EVO_EUNSUP;
+  } else {
+    mb = mq;
+    mbk = mq;
+  }
+  const int tiles = (d->L + QT - 1) / QT;
   {
-    size_t smem = dq_smem(D);
-    EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D>));
-    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch2);
-    attn_bwd_dq_tc_kernel<D><<<grid, 128, smem, st>>>(mq, mk, mv, mdo, a);
+    const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
+                        2 * 256 * 2 * D + 128;
+    EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D, BM_>));
+    dim3 grid(tiles, d->H, (unsigned)nch);
+    attn_bwd_dq_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
   {
-    size_t smem = dkv_smem(D);
-    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D>));
-    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
-    attn_bwd_dkv_tc_kernel<D><<<grid, 128, smem, st>>>(mkt, mvt, mqa, mdoa, a);
+    const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * 256 * 2 * D +
+                        2 * (size_t)QT * 2 * D + 2 * 256 * 4 + 128;
+    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D, BM_>));
+    dim3 grid(tiles, d->H, (unsigned)nch);
+    attn_bwd_dkv_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
     EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");
   }
   if (d->dbias)
-    return reduce_lead(EVO_F32, nch2, 1, (int64_t)d->H * d->L * d->L, part, d->dbias, 0, 1, 0, st);
+    return reduce_lead(EVO_F32, nch, 1, (int64_t)d->H * d->L * d->L, part, d->dbias, 0, 1, 0, st);
   return EVO_OK;
+}
+
+template <int D>
+int bwd_launch(const evo_attn_desc *d, cudaStream_t st) {
+  switch (bias_mode(d)) {
+    case 0: return bwd_launch_mode<D, 0>(d, st);
+    case 1: return bwd_launch_mode<D, 1>(d, st);
+    case 2: return bwd_launch_mode<D, 2>(d, st);
+  }
+  return EVO_EUNSUP;
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -920,7 +1091,7 @@ size_t attention_tc_bwd_ws(const evo_attn_desc *d) {
   const size_t Dq_pad = ((size_t)d->nb * d->H * d->L * 4 + 255) / 256 * 256;
   size_t part = 0;
   if (d->dbias) {
-    int64_t nch = dq_chunks(d);
+    int64_t nch = row_chunks(d);
     int64_t chunk = (d->nb + nch - 1) / nch;
     nch = (d->nb + chunk - 1) / chunk;
     part = (size_t)nch * d->H * d->L * d->L * 4;
