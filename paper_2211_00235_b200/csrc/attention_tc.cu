@@ -765,7 +765,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
       tmem_ld32(lane_addr + c0, sv);
       tmem_ld32(lane_addr + 256 + c0, dv);
       float bb[32];
-      if (BIASMODE) bias_row32<!KCONTIG>(sBias, t, c0, bb);
+      if (BIASMODE) bias_row32<KCONTIG>(sBias, t, c0, bb);
       uint32_t pk[16], dk[16];
 #pragma unroll
       for (int j = 0; j < 32; j += 2) {
