@@ -923,9 +923,11 @@ int bias_mode(const evo_attn_desc *d) {
   return -1;
 }
 
+// Batch-row chunks per (tile, head) so the whole grid is ONE wave of
+// one-CTA-per-SM blocks (a 149th CTA would double the kernel time).
 int64_t row_chunks(const evo_attn_desc *d) {
   int64_t tiles = (int64_t)d->H * ((d->L + QT - 1) / QT);
-  int64_t want = ((int64_t)num_sms() + tiles - 1) / tiles;
+  int64_t want = (int64_t)num_sms() / tiles;
   return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
 }
 
