@@ -38,19 +38,47 @@ __global__ void reduce_lead_kernel(int64_t nb, int64_t n1, int64_t n2, const voi
   }
 }
 
-// Column sums of a tall matrix with a two-stage deterministic reduction:
-// stage 1: block b sums rows [b*rpb, (b+1)*rpb) for every column.
+// Column sums of a tall matrix, deterministic two-stage reduction.
+// Stage 1: block (bx, by) covers rows [bx*rpb, (bx+1)*rpb) and 32 columns;
+// 8 row-lanes (threadIdx.y) stride the rows with 4 loads in flight each, then
+// combine in fixed order through smem.
 template <typename T>
 __global__ void colsum_stage1(int64_t rows, int64_t cols, const void *src, int64_t rs,
                               int64_t rpb, float *part) {
+  __shared__ float red[8][33];
+  const int64_t c = blockIdx.y * 32 + threadIdx.x;
   const int64_t r0 = blockIdx.x * rpb;
   const int64_t r1 = min(rows, r0 + rpb);
-  for (int64_t c = blockIdx.y * (int64_t)blockDim.x + threadIdx.x; c < cols;
-       c += (int64_t)gridDim.y * blockDim.x) {
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+  if (c < cols) {
+    int64_t r = r0 + threadIdx.y;
+    for (; r + 24 < r1; r += 32) {
+      a0 += LD<T>(src, r * rs + c);
+      a1 += LD<T>(src, (r + 8) * rs + c);
+      a2 += LD<T>(src, (r + 16) * rs + c);
+      a3 += LD<T>(src, (r + 24) * rs + c);
+    }
+    for (; r < r1; r += 8) a0 += LD<T>(src, r * rs + c);
+  }
+  red[threadIdx.y][threadIdx.x] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (threadIdx.y == 0 && c < cols) {
     float s = 0.f;
-    for (int64_t r = r0; r < r1; ++r) s += LD<T>(src, r * rs + c);
+#pragma unroll
+    for (int y = 0; y < 8; ++y) s += red[y][threadIdx.x];
     part[blockIdx.x * cols + c] = s;
   }
+}
+
+// Stage 2: warp per column, lanes stride the partials, fixed shuffle tree.
+__global__ void colsum_stage2(int nblk, int64_t cols, const float *part, float *dst, int acc) {
+  const int lane = threadIdx.x & 31;
+  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int b = lane; b < nblk; b += 32) s += part[(int64_t)b * cols + c];
+  s = warp_sum(s);
+  if (lane == 0) dst[c] = acc ? dst[c] + s : s;
 }
 
 template <typename TS, typename TD>
@@ -61,6 +89,49 @@ __global__ void copy2d_kernel(int64_t rows, int64_t cols, const void *src, int64
        e += (int64_t)gridDim.x * blockDim.x) {
     int64_t r = e / cols, c = e % cols;
     ST<TD>(dst, r * d_rs + c * d_cs, LD<TS>(src, r * s_rs + c * s_cs));
+  }
+}
+
+// Contiguous-row copy/cast, 8 elements per thread per step (16-byte
+// bf16 / 2x16-byte fp32 accesses).  cols % 8 == 0, rows 16-byte aligned.
+template <typename TS, typename TD>
+__global__ void copy2d_vec_kernel(int64_t rows, int64_t cols, const void *src, int64_t s_rs,
+                                  void *dst, int64_t d_rs) {
+  const int64_t per_row = cols / 8;
+  const int64_t total = rows * per_row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / per_row, c = (e % per_row) * 8;
+    float v[8];
+    if constexpr (sizeof(TS) == 4) {
+      const float4 *p = reinterpret_cast<const float4 *>(reinterpret_cast<const float *>(src) +
+                                                         r * s_rs + c);
+      float4 a = p[0], b = p[1];
+      v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+    } else {
+      uint4 a = *reinterpret_cast<const uint4 *>(reinterpret_cast<const bf16 *>(src) + r * s_rs + c);
+      const uint32_t *w = reinterpret_cast<const uint32_t *>(&a);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[j]));
+        v[2 * j] = f.x;
+        v[2 * j + 1] = f.y;
+      }
+    }
+    if constexpr (sizeof(TD) == 4) {
+      float4 *q = reinterpret_cast<float4 *>(reinterpret_cast<float *>(dst) + r * d_rs + c);
+      q[0] = make_float4(v[0], v[1], v[2], v[3]);
+      q[1] = make_float4(v[4], v[5], v[6], v[7]);
+    } else {
+      uint32_t w[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(v[2 * j], v[2 * j + 1]);
+        w[j] = *reinterpret_cast<uint32_t *>(&h2);
+      }
+      *reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(dst) + r * d_rs + c) =
+          make_uint4(w[0], w[1], w[2], w[3]);
+    }
   }
 }
 
@@ -199,6 +270,25 @@ __global__ void outgate_bwd_kernel(int64_t rows, int64_t cols, const float *dz, 
   }
 }
 
+__global__ void relu_bwd_bf16x8_kernel(int64_t n8, const uint4 *dh, const uint4 *h, uint4 *dpre) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    uint4 a = dh[e], b = h[e];
+    const uint32_t *aw = reinterpret_cast<const uint32_t *>(&a);
+    const uint32_t *bw = reinterpret_cast<const uint32_t *>(&b);
+    uint32_t o[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      // bf16 x > 0  <=>  sign bit clear and magnitude bits non-zero
+      const uint32_t l16 = bw[j] & 0xFFFFu, h16 = bw[j] >> 16;
+      uint32_t lo = ((l16 & 0x8000u) == 0u && (l16 & 0x7FFFu) != 0u) ? 0xFFFFu : 0u;
+      uint32_t hi = ((h16 & 0x8000u) == 0u && (h16 & 0x7FFFu) != 0u) ? 0xFFFF0000u : 0u;
+      o[j] = aw[j] & (lo | hi);
+    }
+    dpre[e] = make_uint4(o[0], o[1], o[2], o[3]);
+  }
+}
+
 template <typename T>
 __global__ void relu_bwd_kernel(int64_t n, const void *dh, const void *h, void *dpre) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
@@ -269,13 +359,19 @@ int reduce_lead(int dt, int64_t nb, int64_t n1, int64_t n2, const void *src, flo
 // Deterministic: fixed row partition, ordered sums.  ws >= 256*cols floats.
 int colsum(int dt, int64_t rows, int64_t cols, const void *src, int64_t rs, float *dst, int acc,
            float *ws, cudaStream_t st) {
-  const int64_t nblk = std::min<int64_t>(256, std::max<int64_t>(1, rows / 64));
+  const int64_t col_tiles = (cols + 31) / 32;
+  int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(256, (4 * num_sms() + col_tiles - 1) /
+                                                                 col_tiles));
+  nblk = std::min<int64_t>(nblk, std::max<int64_t>(1, rows / 64));
   const int64_t rpb = (rows + nblk - 1) / nblk;
-  dim3 grid((unsigned)nblk, (unsigned)std::min<int64_t>((cols + 255) / 256, 64));
-  if (dt == EVO_F32) colsum_stage1<float><<<grid, 256, 0, st>>>(rows, cols, src, rs, rpb, ws);
-  else colsum_stage1<bf16><<<grid, 256, 0, st>>>(rows, cols, src, rs, rpb, ws);
+  nblk = (rows + rpb - 1) / rpb;
+  dim3 grid((unsigned)nblk, (unsigned)col_tiles), blk(32, 8);
+  if (dt == EVO_F32) colsum_stage1<float><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
+  else colsum_stage1<bf16><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
   EVO_LAUNCHED("colsum_stage1");
-  return reduce_lead(EVO_F32, nblk, 1, cols, ws, dst, 0, 1, acc, st);
+  colsum_stage2<<<(unsigned)((cols + 7) / 8), 256, 0, st>>>((int)nblk, cols, ws, dst, acc);
+  EVO_LAUNCHED("colsum_stage2");
+  return EVO_OK;
 }
 
 int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t s_rs,
@@ -290,6 +386,17 @@ int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t 
     else { if (td == EVO_F32) T(bf16, float); else T(bf16, bf16); }
 #undef T
     EVO_LAUNCHED("transpose_kernel");
+    return EVO_OK;
+  }
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (s_cs == 1 && d_cs == 1 && cols % 8 == 0 && s_rs % 8 == 0 && d_rs % 8 == 0 && al16(src) &&
+      al16(dst)) {
+    int nb = ew_blocks(total / 8);
+#define CV(A, B) copy2d_vec_kernel<A, B><<<nb, 256, 0, st>>>(rows, cols, src, s_rs, dst, d_rs)
+    if (ts == EVO_F32) { if (td == EVO_F32) CV(float, float); else CV(float, bf16); }
+    else { if (td == EVO_F32) CV(bf16, float); else CV(bf16, bf16); }
+#undef CV
+    EVO_LAUNCHED("copy2d_vec_kernel");
     return EVO_OK;
   }
   int nb = ew_blocks(total);
@@ -376,6 +483,14 @@ int outgate_bwd(int dt, int64_t rows, int64_t cols, const float *dz, const void 
 }
 
 int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaStream_t st) {
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (dt == EVO_BF16 && n % 8 == 0 && al16(dh) && al16(h) && al16(dpre)) {
+    relu_bwd_bf16x8_kernel<<<ew_blocks(n / 8), 256, 0, st>>>(
+        n / 8, reinterpret_cast<const uint4 *>(dh), reinterpret_cast<const uint4 *>(h),
+        reinterpret_cast<uint4 *>(dpre));
+    EVO_LAUNCHED("relu_bwd_bf16x8_kernel");
+    return EVO_OK;
+  }
   int nb = ew_blocks(n);
   if (dt == EVO_F32) relu_bwd_kernel<float><<<nb, 256, 0, st>>>(n, dh, h, dpre);
   else relu_bwd_kernel<bf16><<<nb, 256, 0, st>>>(n, dh, h, dpre);

@@ -123,8 +123,8 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
   const bool contig = full && ((cm.cdiv == 0 && cm.cs == 1) ||
                                (cm.cdiv > 0 && (cm.cdiv % 32) == 0 && cm.cs0 == 1));
   const int64_t base = rbase + cm.col(nb);
-  if (contig && !e.accumulate && p.c_aligned) {
-    if (e.dtype_c == EVO_BF16 && !e.residual && (base & 7) == 0) {
+  if (contig && p.c_aligned) {
+    if (e.dtype_c == EVO_BF16 && !e.residual && !e.accumulate && (base & 7) == 0) {
       uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + base);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
@@ -147,6 +147,10 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
         if (res) {
           float4 r = res[j];
           o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+        }
+        if (e.accumulate) {
+          float4 c = dst[j];
+          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
         }
         dst[j] = o;
       }
@@ -409,7 +413,12 @@ bool make_map(CUtensorMap *map, const evo_mat &x, const OperandPlan &pl, int64_t
   return r == CUDA_SUCCESS;
 }
 
-int choose_bn(const evo_gemm_desc *d) { return d->N > 128 ? 256 : 128; }
+int choose_bn(const evo_gemm_desc *d) {
+  if (d->N <= 128) return 128;
+  const int64_t tiles256 = ((d->M + BM - 1) / BM) * ((d->N + 255) / 256) * d->B1 * d->B2 *
+                           std::max(1, d->split_k);
+  return tiles256 < (int64_t)num_sms() ? 128 : 256;
+}
 
 int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
   int split = d->split_k < 1 ? 1 : d->split_k;

@@ -1,16 +1,94 @@
 // LayerNorm forward/backward over the last axis (src/tensor.py:366-392).
-// Warp per row, the row held in registers (cols <= 512), two-pass
-// population variance like the reference; gamma/beta gradients reduced
-// deterministically (fixed grid, per-block partials, ordered final sum).
+// Warp per row with the row in registers; two-pass population variance as
+// in the reference.  Contiguous rows with cols % 128 == 0 (c_m = 256,
+// c_z = 128) take a vectorised fast path (16-byte loads/stores, ~8 rows in
+// flight per SM scheduler); other shapes (channel-first p of the triangle
+// multiplication, tiny test dims) a generic strided path.  gamma/beta
+// gradients: per-warp register partials -> per-block partials -> an ordered
+// warp-per-column reduction (fixed grid, bitwise reproducible).
 #include "common.cuh"
 
 namespace evo {
 namespace {
 
 constexpr int LN_WARPS = 8;
-constexpr int LN_BWD_BLOCKS = 512;  // fixed => bitwise-reproducible sums
-constexpr int MAXV = 16;            // cols <= 32*MAXV
+constexpr int LN_BWD_BLOCKS = 592;  // 4 x 148; fixed => reproducible sums
+constexpr int MAXV = 16;            // generic path: cols <= 32*MAXV
 
+// ----------------------------------------------------------- vector helpers
+template <typename T, int N> struct Vec;
+template <> struct Vec<float, 4> {
+  static __device__ __forceinline__ void load(const float *p, float (&v)[4]) {
+    float4 a = *reinterpret_cast<const float4 *>(p);
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+  }
+  static __device__ __forceinline__ void store(float *p, const float (&v)[4]) {
+    *reinterpret_cast<float4 *>(p) = make_float4(v[0], v[1], v[2], v[3]);
+  }
+};
+template <> struct Vec<bf16, 4> {
+  static __device__ __forceinline__ void load(const bf16 *p, float (&v)[4]) {
+    uint2 a = *reinterpret_cast<const uint2 *>(p);
+    float2 lo = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&a.x));
+    float2 hi = __bfloat1622float2(*reinterpret_cast<__nv_bfloat162 *>(&a.y));
+    v[0] = lo.x; v[1] = lo.y; v[2] = hi.x; v[3] = hi.y;
+  }
+  static __device__ __forceinline__ void store(bf16 *p, const float (&v)[4]) {
+    __nv_bfloat162 lo = __floats2bfloat162_rn(v[0], v[1]);
+    __nv_bfloat162 hi = __floats2bfloat162_rn(v[2], v[3]);
+    uint2 a;
+    a.x = *reinterpret_cast<uint32_t *>(&lo);
+    a.y = *reinterpret_cast<uint32_t *>(&hi);
+    *reinterpret_cast<uint2 *>(p) = a;
+  }
+};
+
+// ------------------------------------------------------------ fast forward
+// NV = cols / 128 float4-groups per lane; lane owns columns 4*lane + 128*i.
+template <typename TX, typename TY, int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+ln_fwd_vec_kernel(int64_t rows, const TX *__restrict__ x, int64_t x_rs,
+                  const float *__restrict__ gamma, const float *__restrict__ beta,
+                  TY *__restrict__ y, int64_t y_rs, float *__restrict__ mean_out,
+                  float *__restrict__ rstd_out, float eps) {
+  constexpr int cols = NV * 128;
+  const int lane = threadIdx.x & 31;
+  const int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
+  if (row >= rows) return;
+  float v[NV][4];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    Vec<TX, 4>::load(x + row * x_rs + 4 * lane + 128 * i, v[i]);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += v[i][j];
+  }
+  const float mu = warp_sum(s) * (1.f / cols);
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float d = v[i][j] - mu;
+      q += d * d;
+    }
+  const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const int c = 4 * lane + 128 * i;
+    float4 g4 = *reinterpret_cast<const float4 *>(gamma + c);
+    float4 b4 = *reinterpret_cast<const float4 *>(beta + c);
+    float o[4] = {(v[i][0] - mu) * rs * g4.x + b4.x, (v[i][1] - mu) * rs * g4.y + b4.y,
+                  (v[i][2] - mu) * rs * g4.z + b4.z, (v[i][3] - mu) * rs * g4.w + b4.w};
+    Vec<TY, 4>::store(y + row * y_rs + c, o);
+  }
+  if (lane == 0) {
+    mean_out[row] = mu;
+    rstd_out[row] = rs;
+  }
+}
+
+// --------------------------------------------------------- generic forward
 template <typename TX, typename TY, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
 ln_fwd_kernel(int64_t rows, int cols, const TX *__restrict__ x, int64_t x_rs, int64_t x_cs,
@@ -36,8 +114,7 @@ ln_fwd_kernel(int64_t rows, int cols, const TX *__restrict__ x, int64_t x_rs, in
     float d = (c < cols) ? v[j] - mu : 0.f;
     q += d * d;
   }
-  const float var = warp_sum(q) * inv_n;
-  const float rs = 1.f / sqrtf(var + eps);
+  const float rs = 1.f / sqrtf(warp_sum(q) * inv_n + eps);
 #pragma unroll
   for (int j = 0; j < V; ++j) {
     int c = lane + 32 * j;
@@ -49,6 +126,81 @@ ln_fwd_kernel(int64_t rows, int cols, const TX *__restrict__ x, int64_t x_rs, in
   }
 }
 
+// ----------------------------------------------------------- fast backward
+template <typename TDY, typename TX, typename TDX, int NV>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
+                  const TX *__restrict__ x, int64_t x_rs, const float *__restrict__ mean,
+                  const float *__restrict__ rstd, const float *__restrict__ gamma,
+                  const float *__restrict__ dres, TDX *__restrict__ dx, int64_t dx_rs,
+                  float *__restrict__ partial, int want_params) {
+  constexpr int cols = NV * 128;
+  __shared__ float red[LN_WARPS][2][cols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float pg[NV][4], pb[NV][4], g[NV][4];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane + 128 * i);
+    g[i][0] = g4.x; g[i][1] = g4.y; g[i][2] = g4.z; g[i][3] = g4.w;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pg[i][j] = pb[i][j] = 0.f;
+  }
+  constexpr float inv_n = 1.f / cols;
+  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + warp; row < rows;
+       row += (int64_t)gridDim.x * LN_WARPS) {
+    const float mu = mean[row], rs = rstd[row];
+    float xh[NV][4], dxh[NV][4];
+    float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = 4 * lane + 128 * i;
+      float dv[4], xv[4];
+      Vec<TDY, 4>::load(dy + row * dy_rs + c, dv);
+      Vec<TX, 4>::load(x + row * x_rs + c, xv);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        xh[i][j] = (xv[j] - mu) * rs;
+        dxh[i][j] = dv[j] * g[i][j];
+        s1 += dxh[i][j];
+        s2 += dxh[i][j] * xh[i][j];
+        pg[i][j] += dv[j] * xh[i][j];
+        pb[i][j] += dv[j];
+      }
+    }
+    const float m1 = warp_sum(s1) * inv_n;
+    const float m2 = warp_sum(s2) * inv_n;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = 4 * lane + 128 * i;
+      float r[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) r[j] = rs * (dxh[i][j] - m1 - xh[i][j] * m2);
+      if (dres) {
+        float4 d4 = *reinterpret_cast<const float4 *>(dres + row * dx_rs + c);
+        r[0] += d4.x; r[1] += d4.y; r[2] += d4.z; r[3] += d4.w;
+      }
+      Vec<TDX, 4>::store(dx + row * dx_rs + c, r);
+    }
+  }
+  if (!want_params) return;
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      red[warp][0][4 * lane + 128 * i + j] = pg[i][j];
+      red[warp][1][4 * lane + 128 * i + j] = pb[i][j];
+    }
+  __syncthreads();
+  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
+    const int which = c / cols, cc = c % cols;
+    float s = 0.f;
+#pragma unroll
+    for (int w = 0; w < LN_WARPS; ++w) s += red[w][which][cc];
+    partial[((int64_t)blockIdx.x * 2 + which) * cols + cc] = s;
+  }
+}
+
+// -------------------------------------------------------- generic backward
 template <typename TDY, typename TX, typename TDX, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
 ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
@@ -118,17 +270,25 @@ ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
   }
 }
 
+// Ordered reduction of the per-block partials: one warp per output value;
+// lane l sums partials l, l+32, ... then a fixed shuffle tree.
 __global__ void ln_param_reduce_kernel(int nblk, int cols, const float *__restrict__ partial,
                                        float *__restrict__ dgamma, float *__restrict__ dbeta,
                                        int accumulate) {
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < 2 * cols; c += gridDim.x * blockDim.x) {
-    int which = c / cols, cc = c % cols;
-    float s = 0.f;
-    for (int b = 0; b < nblk; ++b) s += partial[((int64_t)b * 2 + which) * cols + cc];
+  const int lane = threadIdx.x & 31;
+  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (c >= 2 * cols) return;
+  const int which = c / cols, cc = c % cols;
+  float s = 0.f;
+  for (int b = lane; b < nblk; b += 32) s += partial[((int64_t)b * 2 + which) * cols + cc];
+  s = warp_sum(s);
+  if (lane == 0) {
     float *dst = which == 0 ? dgamma : dbeta;
     if (dst) dst[cc] = accumulate ? dst[cc] + s : s;
   }
 }
+
+bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 template <typename TX, typename TY>
 int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x_cs,
@@ -137,6 +297,18 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   dim3 grid((unsigned)((rows + LN_WARPS - 1) / LN_WARPS));
   const TX *xp = reinterpret_cast<const TX *>(x);
   TY *yp = reinterpret_cast<TY *>(y);
+  const bool vec = x_cs == 1 && (cols == 128 || cols == 256) && x_rs % 4 == 0 && y_rs % 4 == 0 &&
+                   aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta);
+  if (vec) {
+    if (cols == 128)
+      ln_fwd_vec_kernel<TX, TY, 1><<<grid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+                                                                  y_rs, mean, rstd, eps);
+    else
+      ln_fwd_vec_kernel<TX, TY, 2><<<grid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+                                                                  y_rs, mean, rstd, eps);
+    EVO_LAUNCHED("ln_fwd_vec_kernel");
+    return EVO_OK;
+  }
 #define L(Vn)                                                                                \
   ln_fwd_kernel<TX, TY, Vn><<<grid, LN_WARPS * 32, 0, st>>>(rows, cols, xp, x_rs, x_cs, gamma, \
                                                             beta, yp, y_rs, mean, rstd, eps)
@@ -158,23 +330,36 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
   int want = (dgamma || dbeta) ? 1 : 0;
   int64_t need_blocks = (rows + LN_WARPS - 1) / LN_WARPS;
   int nblk = (int)std::min<int64_t>(LN_BWD_BLOCKS, std::max<int64_t>(need_blocks, 1));
-  size_t smem = (size_t)LN_WARPS * 2 * cols * sizeof(float);
   const TDY *dyp = reinterpret_cast<const TDY *>(dy);
   const TX *xp = reinterpret_cast<const TX *>(x);
   TDX *dxp = reinterpret_cast<TDX *>(dx);
+  const bool vec = x_cs == 1 && dx_cs == 1 && (cols == 128 || cols == 256) && dy_rs % 4 == 0 &&
+                   x_rs % 4 == 0 && dx_rs % 4 == 0 && aligned16(dy) && aligned16(x) &&
+                   aligned16(dx) && aligned16(gamma) && (!dres || aligned16(dres));
+  if (vec) {
+    if (cols == 128)
+      ln_bwd_vec_kernel<TDY, TX, TDX, 1><<<nblk, LN_WARPS * 32, 0, st>>>(
+          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, ws, want);
+    else
+      ln_bwd_vec_kernel<TDY, TX, TDX, 2><<<nblk, LN_WARPS * 32, 0, st>>>(
+          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, ws, want);
+    EVO_LAUNCHED("ln_bwd_vec_kernel");
+  } else {
+    size_t smem = (size_t)LN_WARPS * 2 * cols * sizeof(float);
 #define L(Vn)                                                                                 \
   ln_bwd_kernel<TDY, TX, TDX, Vn><<<nblk, LN_WARPS * 32, smem, st>>>(                          \
       rows, cols, dyp, dy_rs, xp, x_rs, x_cs, mean, rstd, gamma, dres, dxp, dx_rs, dx_cs, ws, want)
-  if (cols <= 32) L(1);
-  else if (cols <= 64) L(2);
-  else if (cols <= 128) L(4);
-  else if (cols <= 256) L(8);
-  else L(16);
+    if (cols <= 32) L(1);
+    else if (cols <= 64) L(2);
+    else if (cols <= 128) L(4);
+    else if (cols <= 256) L(8);
+    else L(16);
 #undef L
-  EVO_LAUNCHED("ln_bwd_kernel");
+    EVO_LAUNCHED("ln_bwd_kernel");
+  }
   if (want) {
-    ln_param_reduce_kernel<<<(2 * cols + 255) / 256, 256, 0, st>>>(nblk, cols, ws, dgamma, dbeta,
-                                                                   acc);
+    const int outs = 2 * cols;
+    ln_param_reduce_kernel<<<(outs + 7) / 8, 256, 0, st>>>(nblk, cols, ws, dgamma, dbeta, acc);
     EVO_LAUNCHED("ln_param_reduce_kernel");
   }
   return EVO_OK;
