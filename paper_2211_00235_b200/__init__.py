@@ -11,5 +11,6 @@ from .evoformer import (EvoConfig, ParamStore, col_attn, evoformer_block, evofor
                         set_precision, tri_attn, tri_mult)
 from .schedules import (ParallelLayout, RunResult, compare_runs, expected_comm_volume,
                         make_batch, run_single)
+from .distributed import run_bp, run_distributed, run_dp
 
 __version__ = "0.1.0"

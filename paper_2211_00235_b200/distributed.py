@@ -1,0 +1,336 @@
+"""Branch Parallelism (BP=2) x data parallelism over torch.distributed:
+the schedule of src/schedules.py:214-329 on real processes.
+
+One process per GPU (torchrun); rank = dp_i * bp + bp_i (dap = 1,
+src/schedules.py:22, 43-82).  In a BP pair, bp_i = 0 runs the MSA branch
+(row/column attention, MSA transition) plus the outer product mean, bp_i = 1
+the pair branch (triangle updates, triangle attentions, pair transition).
+Per block (the reference's literal order):
+
+  forward   rank0: m' = msa_track(m, z); o = opm(m')        broadcast o  (src 0)
+            rank1: z_b = pair_track(z); z'' = z_b + o        broadcast z'' (src 1)
+  backward  rank1: broadcast dz'' (src 1); rank0 seeds it into o
+            both:  segment backward; allreduce dz_in partials (dz_row + dz_pair)
+  end       rank0: broadcast dm (src 0)
+  params    owner broadcast of each branch's gradient bucket over the pair,
+            then sum / dp over the DP group.
+
+Every cross-rank sum in the BP pair has exactly two operands, and the BP=1
+path forms the same sums (dz_in = dz_pair + dz_row, z' = z_pair + o), so
+BP=2 reproduces BP=1 bitwise: float addition commutes.
+
+The schedule is written against a small executor interface (`CudaExec`
+here: the native kernels; the CPU tests substitute an oracle-backed executor
+and run the same schedule under the gloo backend).
+"""
+
+from __future__ import annotations
+
+import time
+from dataclasses import dataclass, field
+
+import torch
+import torch.distributed as dist
+
+from .errors import CollectiveError, ConfigError, WorldError
+from .schedules import ParallelLayout, RunResult, make_batch
+
+F32 = torch.float32
+
+
+@dataclass
+class CommRecord:
+    kind: str
+    group: tuple
+    src: int | None
+    elements: int
+    bytes: int
+    phase: str
+
+
+class Comm:
+    """Collectives over the BP-pair and DP groups of a layout, with a
+    trace of every call (the CommTrace equivalent, src/comm.py:41-110)."""
+
+    def __init__(self, layout: ParallelLayout, rank: int | None = None):
+        if not dist.is_initialized():
+            raise WorldError("torch.distributed is not initialised (launch with torchrun)")
+        self.layout = layout
+        self.rank = dist.get_rank() if rank is None else rank
+        if dist.get_world_size() != layout.world_size:
+            raise ConfigError(f"world size {dist.get_world_size()} != layout world size "
+                              f"{layout.world_size}")
+        self.groups = {}
+        # every rank creates every group, in the same order
+        for dp_i in range(layout.dp):
+            g = tuple(layout.rank_of(dp_i, b) for b in range(layout.bp))
+            self.groups[g] = dist.new_group(list(g)) if layout.bp > 1 else None
+        for bp_i in range(layout.bp):
+            g = tuple(layout.rank_of(d, bp_i) for d in range(layout.dp))
+            self.groups[g] = dist.new_group(list(g)) if layout.dp > 1 else None
+        self.pair = layout.bp_group(self.rank)
+        self.dpg = layout.dp_group(self.rank)
+        self.trace: list[CommRecord] = []
+
+    def _rec(self, kind, group, src, t, phase):
+        self.trace.append(CommRecord(kind, tuple(group), src, int(t.numel()),
+                                     int(t.numel() * t.element_size()), phase))
+
+    def broadcast(self, group, src, t, phase):
+        if src not in group:
+            raise CollectiveError(f"broadcast src {src} not in group {group}")
+        dist.broadcast(t, src=src, group=self.groups[tuple(group)])
+        self._rec("broadcast", group, src, t, phase)
+        return t
+
+    def allreduce_sum(self, group, t, phase):
+        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.groups[tuple(group)])
+        self._rec("allreduce_sum", group, None, t, phase)
+        return t
+
+    def volume(self, world_reduce=True) -> dict:
+        """{(phase, kind): (count, elements)} over the whole world (summed over
+        the groups this rank leads, then over ranks)."""
+        mine = {}
+        for r in self.trace:
+            if r.group[0] != self.rank:  # count each group once: by its lowest rank
+                continue
+            c0, e0 = mine.get((r.phase, r.kind), (0, 0))
+            mine[(r.phase, r.kind)] = (c0 + 1, e0 + r.elements)
+        if not world_reduce:
+            return mine
+        keys = [("fwd", "broadcast"), ("bwd", "broadcast"), ("bwd", "allreduce_sum"),
+                ("param", "broadcast"), ("param", "allreduce_sum")]
+        vec = torch.tensor([[mine.get(k, (0, 0))[0], mine.get(k, (0, 0))[1]] for k in keys],
+                           dtype=torch.float64)
+        dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+        vec = vec.to(dev)
+        dist.all_reduce(vec)
+        vec = vec.cpu()
+        return {k: (int(vec[i, 0]), int(vec[i, 1])) for i, k in enumerate(keys) if vec[i, 0] > 0}
+
+
+class CudaExec:
+    """Branch executor on the native kernels (engine.py)."""
+
+    def __init__(self, cfg, store, precision=None, device=None):
+        from . import engine as E
+        from . import kernels as K
+        from .schedules import StepState
+        self.E, self.K = E, K
+        self.st = StepState(cfg, store, precision, device)
+        self.cfg, self.act, self.dev = cfg, self.st.act, self.st.dev
+
+    def pack(self, branch):
+        """Operand copies of the parameters this rank computes with:
+        'msa', 'pair' or 'all'."""
+        E = self.E
+        subops = {"msa": E.MSA_SUBOPS, "pair": E.PAIR_SUBOPS}.get(branch,
+                                                                 E.MSA_SUBOPS + E.PAIR_SUBOPS)
+        self.st.pack(subops)
+
+    def grad_bank(self, blk, branch):
+        bg = self.st.grads[blk]
+        return (bg.msa if branch == "msa" else bg.pair).flat
+
+    def grad_dict(self):
+        return self.st.grad_dict()
+
+    def zero_grads(self):
+        for bg in self.st.grads:
+            bg.msa.flat.zero_()
+            bg.pair.flat.zero_()
+
+    def msa_fwd(self, blk, m, z):
+        E, st = self.E, self.st
+        m_new, ctxs = E.msa_branch_fwd(st.P, blk, st.packs[blk], m, z, self.cfg, self.act)
+        o, co = E.opm_fwd(st.P, f"blk{blk}.opm", st.packs[blk]["opm"], m_new, None, self.cfg,
+                          self.act)
+        return m_new, o, (ctxs, co)
+
+    def pair_fwd(self, blk, z):
+        E, st = self.E, self.st
+        return E.pair_branch_fwd(st.P, blk, st.packs[blk], z, self.cfg, self.act)
+
+    def add(self, a, b):
+        out = torch.empty_like(a)
+        self.K.add(a, b, out)
+        return out
+
+    def msa_bwd(self, blk, ctx, dm, d_o):
+        E, st = self.E, self.st
+        ctxs, co = ctx
+        G = st.grads[blk].packed
+        dm3 = E.opm_bwd(st.P, f"blk{blk}.opm", st.packs[blk]["opm"], G["opm"], co, d_o,
+                        E.cast_act(d_o, self.act), dm, self.cfg, self.act)
+        return E.msa_branch_bwd(st.P, blk, st.packs[blk], G, ctxs, dm3, self.cfg, self.act)
+
+    def pair_bwd(self, blk, ctx, dz):
+        E, st = self.E, self.st
+        return E.pair_branch_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctx, dz,
+                                 self.cfg, self.act)
+
+    def full_step(self, m, z):
+        from .schedules import full_step
+        return full_step(self.st, m, z)
+
+    def sq_mean(self, x):
+        loss = torch.zeros(1, dtype=F32, device=self.dev)
+        dx = torch.empty_like(x)
+        self.K.sq_mean(x, loss, dx)
+        return loss, dx
+
+
+def bp_msa_step(ex, comm, m, z, K_blocks, zshape_numel):
+    """Rank bp_i = 0 (src/schedules.py:214-258).  Returns dict."""
+    pair = comm.pair
+    r0, r1 = pair
+    z_cur = z
+    ctxs = []
+    m_cur = m
+    for blk in range(K_blocks):
+        m_cur, o, ctx = ex.msa_fwd(blk, m_cur, z_cur)
+        ctxs.append(ctx)
+        comm.broadcast(pair, r0, o, "fwd")
+        z_next = torch.empty_like(z_cur)
+        comm.broadcast(pair, r1, z_next, "fwd")
+        z_cur = z_next
+    loss_m, dm = ex.sq_mean(m_cur)
+    for blk in reversed(range(K_blocks)):
+        d_o = torch.empty_like(z_cur)
+        comm.broadcast(pair, r1, d_o, "bwd")
+        dm, dz_row = ex.msa_bwd(blk, ctxs[blk], dm, d_o)
+        ctxs[blk] = None
+        comm.allreduce_sum(pair, dz_row, "bwd")     # dz_row + dz_pair (rank order)
+    comm.broadcast(pair, r0, dm, "bwd")
+    return dict(m_out=m_cur, z_out=z_cur, loss=loss_m, dm=dm, dz=dz_row)
+
+
+def bp_pair_step(ex, comm, z, K_blocks, mshape):
+    """Rank bp_i = 1 (src/schedules.py:261-297)."""
+    pair = comm.pair
+    r0, r1 = pair
+    z_cur = z
+    ctxs = []
+    for blk in range(K_blocks):
+        z_b, ctx = ex.pair_fwd(blk, z_cur)
+        ctxs.append(ctx)
+        o = torch.empty_like(z_b)
+        comm.broadcast(pair, r0, o, "fwd")
+        z_cur = ex.add(z_b, o)                     # z'' = z_pair + o (:276-280)
+        comm.broadcast(pair, r1, z_cur, "fwd")
+    loss_z, dz = ex.sq_mean(z_cur)
+    for blk in reversed(range(K_blocks)):
+        comm.broadcast(pair, r1, dz, "bwd")        # dz'' -> seeds o on rank 0
+        dz_pair = ex.pair_bwd(blk, ctxs[blk], dz)
+        ctxs[blk] = None
+        comm.allreduce_sum(pair, dz_pair, "bwd")
+        dz = dz_pair
+    dm = torch.empty(mshape, dtype=z.dtype, device=z.device)
+    comm.broadcast(pair, r0, dm, "bwd")
+    return dict(z_out=z_cur, loss=loss_z, dz=dz)
+
+
+def sync_param_grads(ex, comm, K_blocks):
+    """src/schedules.py:300-329: owner broadcast over the BP pair (one
+    bucket per branch per block), then sum / dp over the DP group."""
+    lay = comm.layout
+    if lay.bp == 2:
+        r0, r1 = comm.pair
+        for blk in range(K_blocks):
+            comm.broadcast(comm.pair, r0, ex.grad_bank(blk, "msa"), "param")
+            comm.broadcast(comm.pair, r1, ex.grad_bank(blk, "pair"), "param")
+    if lay.dp > 1:
+        for blk in range(K_blocks):
+            for br in ("msa", "pair"):
+                g = ex.grad_bank(blk, br)
+                comm.allreduce_sum(comm.dpg, g, "param")
+                g.div_(lay.dp)
+
+
+class DistributedStep:
+    """One train step of the (dp, bp) layout on this rank's GPU."""
+
+    def __init__(self, cfg, store, layout: ParallelLayout, precision=None, comm=None,
+                 executor=None):
+        layout.validate_model(cfg)
+        self.cfg, self.layout = cfg, layout
+        self.comm = comm or Comm(layout)
+        self.rank = self.comm.rank
+        self.dp_i, self.bp_i, _ = layout.coords(self.rank)
+        self.ex = executor or CudaExec(cfg, store, precision)
+        if layout.bp == 2:
+            self.ex.pack("msa" if self.bp_i == 0 else "pair")
+        else:
+            self.ex.pack("all")
+
+    def step(self, m, z):
+        """m [s, r, c_m], z [r, r, c_z] on this rank's device.  Returns the
+        tuple (m_out, z_out, loss, dm, dz) of fields this rank owns (others
+        None); parameter gradients are left synchronised in the executor."""
+        cfg, lay, ex = self.cfg, self.layout, self.ex
+        s, r = cfg.s, cfg.r
+        m2 = m.reshape(s * r, cfg.c_m)
+        z2 = z.reshape(r * r, cfg.c_z)
+        if lay.bp == 1:
+            out = ex.full_step(m, z)
+            sync_param_grads(ex, self.comm, cfg.n_blocks)
+            return out
+        if self.bp_i == 0:
+            res = bp_msa_step(ex, self.comm, m2, z2, cfg.n_blocks, None)
+            out = (res["m_out"].reshape(s, r, cfg.c_m), None, res["loss"],
+                   res["dm"].reshape(s, r, cfg.c_m), None)
+        else:
+            res = bp_pair_step(ex, self.comm, z2, cfg.n_blocks, (s * r, cfg.c_m))
+            out = (None, res["z_out"].reshape(r, r, cfg.c_z), res["loss"], None,
+                   res["dz"].reshape(r, r, cfg.c_z))
+        sync_param_grads(ex, self.comm, cfg.n_blocks)
+        return out
+
+
+def run_distributed(cfg, store, layout: ParallelLayout, seed: int = 32, precision=None,
+                    comm=None, executor=None) -> RunResult:
+    """SPMD train step under `layout` (src/schedules.py:332-384).  Call on
+    every rank of an initialised process group.  The returned RunResult
+    carries the dp_idx = 0 replica's outputs and input gradients (gathered
+    within its BP pair) on every rank of that replica, the dp-mean loss, and
+    the synchronised parameter gradients."""
+    layout.validate_model(cfg)
+    runner = DistributedStep(cfg, store, layout, precision, comm, executor)
+    dev = runner.ex.dev
+    samples = make_batch(cfg, seed, layout.dp, device=dev)
+    m, z = samples[runner.dp_i]
+    t0 = time.perf_counter()
+    m_out, z_out, loss, dm, dz = runner.step(m, z)
+    # replica loss = loss_m + loss_z (pair), then mean over dp
+    lt = loss.reshape(1).to(torch.float64)
+    if layout.bp == 2:
+        runner.comm.allreduce_sum(runner.comm.pair, lt, "result")
+    if layout.dp > 1:
+        runner.comm.allreduce_sum(runner.comm.dpg, lt, "result")
+        lt /= layout.dp
+    if layout.bp == 2:
+        # complete the pair's view: rank0 owns m_out/dm, rank1 z_out/dz
+        r0, r1 = runner.comm.pair
+        if runner.bp_i == 0:
+            z_out_t, dz_t = torch.empty_like(z), torch.empty_like(z)
+            m_out_t, dm_t = m_out.contiguous(), dm.contiguous()
+        else:
+            m_out_t, dm_t = torch.empty_like(m), torch.empty_like(m)
+            z_out_t, dz_t = z_out.contiguous(), dz.contiguous()
+        for t, src in ((m_out_t, r0), (dm_t, r0), (z_out_t, r1), (dz_t, r1)):
+            runner.comm.broadcast(runner.comm.pair, src, t, "result")
+        m_out, dm, z_out, dz = m_out_t, dm_t, z_out_t, dz_t
+    if dev.type == "cuda":
+        torch.cuda.synchronize(dev)
+    wall = time.perf_counter() - t0
+    return RunResult(m_out, z_out, float(lt.item()), dm, dz, runner.ex.grad_dict(),
+                     runner.comm.trace, None, wall)
+
+
+def run_bp(cfg, store, seed: int = 32, precision=None) -> RunResult:
+    return run_distributed(cfg, store, ParallelLayout(bp=2), seed, precision)
+
+
+def run_dp(cfg, store, dp: int, seed: int = 32, precision=None) -> RunResult:
+    return run_distributed(cfg, store, ParallelLayout(dp=dp), seed, precision)
