@@ -188,13 +188,13 @@ def run_native(args):
     bp = 2 if (world > 1 and world % 2 == 0 and not args.dp_only) else 1
     dp = world // bp
     layout = S.ParallelLayout(dp=dp, bp=bp)
-    if bp == 2:
+    runner = None
+    if world > 1:
         from paper_2211_00235_b200 import distributed as D
         runner = D.DistributedStep(cfg, store, layout, precision=args.precision)
     else:
-        runner = None
-    st = S.StepState(cfg, store, args.precision, dev)
-    st.pack()
+        st = S.StepState(cfg, store, args.precision, dev)
+        st.pack()
     dp_i = layout.coords(rank)[0]
     m_h, z_h = S.make_batch(cfg, 32 + dp_i, 1, device="cpu")[0]
     m_h, z_h = m_h.pin_memory(), z_h.pin_memory()
@@ -204,13 +204,7 @@ def run_native(args):
     def step(m, z):
         if runner is not None:
             return runner.step(m, z)
-        out = S.full_step(st, m, z)
-        if dp > 1:
-            for bg in st.grads:
-                for bank in (bg.msa, bg.pair):
-                    dist.all_reduce(bank.flat)
-                    bank.flat.div_(dp)
-        return out
+        return S.full_step(st, m, z)
 
     # warm-up (also first-touch allocations)
     for _ in range(args.warmup):
