@@ -83,8 +83,11 @@ def run_reference(args):
         return 0
     kw = CONFIGS[args.config]
     cores = os.cpu_count()
-    for _ in range(max(0, args.warmup) and 1):
-        pass
+    # each "step" is one full-block sample (the nine sub-ops, ~10 s on 16
+    # cores); bounded to 1 warm-up + 3 timed samples so the run stays short
+    warm = min(max(args.warmup, 0), 1)
+    for _ in range(warm):
+        cpu_sample(kw)
     per = []
     for _ in range(max(1, min(args.steps, 3))):
         t, _ = cpu_sample(kw)
@@ -93,7 +96,7 @@ def run_reference(args):
     value = kw["n_blocks"] / t / kw["n_blocks"]
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "samples/s",
-        "n_gpus": args.gpus, "steps": len(per), "warmup": 0, "ms_per_step": t * 1e3,
+        "n_gpus": args.gpus, "steps": len(per), "warmup": warm, "ms_per_step": t * 1e3,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic", "config": {"workload": f"parallel_evoformer_block_{args.config}",
                                         **kw, "precision": "fp32 numpy"},
@@ -356,6 +359,7 @@ def run_native(args):
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "launch_mode": "cuda_graph" if use_graph else "eager", "ms_per_step_eager": ms_eager,
         "clocks": clk,
+        "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
     }
     print(json.dumps(line))
     if world > 1:
