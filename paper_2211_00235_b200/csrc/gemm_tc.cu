@@ -86,7 +86,7 @@ __device__ __forceinline__ float fast_sigmoid(float x) {
 // destination elements are contiguous and aligned.
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, const uint32_t (&v)[32],
-                                          int64_t rbase, int64_t nb) {
+                                          int64_t rbase, int64_t nb, bool row_ok_g, float *stage) {
   float x[32];
   const bool full = nb + 32 <= p.N;
 #pragma unroll
@@ -123,40 +123,62 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
   const bool contig = full && ((cm.cdiv == 0 && cm.cs == 1) ||
                                (cm.cdiv > 0 && (cm.cdiv % 32) == 0 && cm.cs0 == 1));
   const int64_t base = rbase + cm.col(nb);
-  if (contig && p.c_aligned) {
-    if (e.dtype_c == EVO_BF16 && !e.residual && !e.accumulate && (base & 7) == 0) {
-      uint4 *dst = reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + base);
+  // Every lane must take the same path through the staged store (shuffles).
+  const bool lane_ok = contig && p.c_aligned &&
+                       ((e.dtype_c == EVO_BF16 && (base & 7) == 0 && !e.residual && !e.accumulate) ||
+                        (e.dtype_c == EVO_F32 && (base & 3) == 0));
+  if (__all_sync(0xffffffffu, lane_ok || !row_ok_g)) {
+    // Stage the warp's 32 rows x 32 columns through padded smem, then write
+    // whole contiguous row segments per store instruction.
+    const int lane = threadIdx.x & 31;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) {
+    for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = x[j];
+    __syncwarp();
+    if (e.dtype_c == EVO_BF16) {
+      const int c = lane & 3;  // 8-column group
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        const int r = 8 * i + (lane >> 2);
+        const int64_t rb = __shfl_sync(0xffffffffu, base, r);
+        const bool ok = __shfl_sync(0xffffffffu, row_ok_g ? 1 : 0, r);
+        const float *src = stage + r * 33 + 8 * c;
         uint32_t w[4];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * j + 2 * u], x[8 * j + 2 * u + 1]);
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(src[2 * u], src[2 * u + 1]);
           w[u] = *reinterpret_cast<uint32_t *>(&h2);
         }
-        dst[j] = make_uint4(w[0], w[1], w[2], w[3]);
+        if (ok)
+          *reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + rb + 8 * c) =
+              make_uint4(w[0], w[1], w[2], w[3]);
       }
-      return;
-    }
-    if (e.dtype_c == EVO_F32 && (base & 3) == 0) {
-      float4 *dst = reinterpret_cast<float4 *>(reinterpret_cast<float *>(e.C) + base);
-      const float4 *res = e.residual ? reinterpret_cast<const float4 *>(e.residual + base) : nullptr;
+    } else {
+      const int c = lane & 7;  // 4-column group
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        float4 o = make_float4(x[4 * j], x[4 * j + 1], x[4 * j + 2], x[4 * j + 3]);
-        if (res) {
-          float4 r = res[j];
-          o.x += r.x; o.y += r.y; o.z += r.z; o.w += r.w;
+      for (int i = 0; i < 8; ++i) {
+        const int r = 4 * i + (lane >> 3);
+        const int64_t rb = __shfl_sync(0xffffffffu, base, r);
+        const bool ok = __shfl_sync(0xffffffffu, row_ok_g ? 1 : 0, r);
+        const float *src = stage + r * 33 + 4 * c;
+        float4 o = make_float4(src[0], src[1], src[2], src[3]);
+        if (ok) {
+          float *dst = reinterpret_cast<float *>(e.C) + rb + 4 * c;
+          if (e.residual) {
+            float4 q = *reinterpret_cast<const float4 *>(e.residual + rb + 4 * c);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          if (e.accumulate) {
+            float4 q = *reinterpret_cast<const float4 *>(dst);
+            o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+          }
+          *reinterpret_cast<float4 *>(dst) = o;
         }
-        if (e.accumulate) {
-          float4 c = dst[j];
-          o.x += c.x; o.y += c.y; o.z += c.z; o.w += c.w;
-        }
-        dst[j] = o;
       }
-      return;
     }
+    __syncwarp();
+    return;
   }
+  if (!row_ok_g) return;
 #pragma unroll
   for (int j = 0; j < 32; ++j) {
     const int64_t n = nb + j;
@@ -300,6 +322,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // split the 32-column chunks of the tile between them.
     const int ew = warp - 2;
     const int q = warp & 3;
+    float *stage = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16) +
+                   ew * (32 * 33);
     const int half = ew >> 2;  // 0 or 1
     int acc = 0;
     uint32_t aphase = 0;
@@ -320,8 +344,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         uint32_t v[32];
         tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
         const int64_t nb = n0 + c0;
-        if (!row_ok || nb >= p.N) continue;
+        if (nb >= p.N) continue;  // warp-uniform
         if (p.split > 1) {
+          if (!row_ok) continue;
           float *dst = p.partial + (((int64_t)sp * p.nbatch + bidx) * p.M + m) * p.N + nb;
           if (nb + 32 <= p.N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
@@ -336,7 +361,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
           continue;
         }
-        epi_chunk<EPI>(p, e, v, rbase, nb);
+        epi_chunk<EPI>(p, e, v, rbase, nb, row_ok, stage);
       }
       fence_before();
       __syncwarp();
@@ -459,7 +484,8 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
     EVO_REQUIRE(d->workspace && d->workspace_bytes >= need, EVO_EARG,
                 "evo_gemm(tc): split=%d needs %zu workspace bytes", p.split, need);
   }
-  const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) + 256;
+  const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) + 256 +
+                      (size_t)EPI_WARPS * 32 * 33 * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
