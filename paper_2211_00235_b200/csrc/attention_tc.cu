@@ -277,37 +277,47 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
     }
     // pass 1: s = scale*acc + bias (masked keys -> -inf), row max, write back
     float mx = -INFINITY;
-    for (int c0 = 0; c0 < Lp; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(lane_addr + c0, v);
-      float bb[32];
-      if (BIASMODE) bias_row32<TB>(sBias, t, c0, bb);
+    for (int c0 = 0; c0 < Lp; c0 += 64) {
+      uint32_t v[2][32];
+      tmem_ld32_nw(lane_addr + c0, v[0]);
+      tmem_ld32_nw(lane_addr + c0 + 32, v[1]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        float s = __uint_as_float(v[j]) * a.scale;
-        if (BIASMODE) s += bb[j];
-        s = (c0 + j < L) ? s : -INFINITY;
-        mx = fmaxf(mx, s);
-        v[j] = __float_as_uint(s);
+      for (int u = 0; u < 2; ++u) {
+        float bb[32];
+        if (BIASMODE) bias_row32<TB>(sBias, t, c0 + 32 * u, bb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float s = __uint_as_float(v[u][j]) * a.scale;
+          if (BIASMODE) s += bb[j];
+          s = (c0 + 32 * u + j < L) ? s : -INFINITY;
+          mx = fmaxf(mx, s);
+          v[u][j] = __float_as_uint(s);
+        }
+        tmem_st32(lane_addr + c0 + 32 * u, v[u]);
       }
-      tmem_st32(lane_addr + c0, v);
     }
     tmem_st_wait();
     // pass 2: p = exp(s - max) -> bf16 pairs in place (cols c0/2 ..), row sum
     float sum = 0.f;
     const float mxl = mx * LOG2E;
-    for (int c0 = 0; c0 < Lp; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(lane_addr + c0, v);
-      uint32_t pk[16];
+    for (int c0 = 0; c0 < Lp; c0 += 64) {
+      uint32_t v[2][32];
+      tmem_ld32_nw(lane_addr + c0, v[0]);
+      tmem_ld32_nw(lane_addr + c0 + 32, v[1]);
+      tmem_wait_ld();
 #pragma unroll
-      for (int j = 0; j < 16; ++j) {
-        float p0 = ex2(__uint_as_float(v[2 * j]) * LOG2E - mxl);
-        float p1 = ex2(__uint_as_float(v[2 * j + 1]) * LOG2E - mxl);
-        sum += p0 + p1;
-        pk[j] = pack2(p0, p1);
+      for (int u = 0; u < 2; ++u) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          float p0 = ex2(__uint_as_float(v[u][2 * j]) * LOG2E - mxl);
+          float p1 = ex2(__uint_as_float(v[u][2 * j + 1]) * LOG2E - mxl);
+          sum += p0 + p1;
+          pk[j] = pack2(p0, p1);
+        }
+        tmem_st16(lane_addr + ((c0 + 32 * u) >> 1), pk);
       }
-      tmem_st16(lane_addr + (c0 >> 1), pk);
     }
     tmem_st_wait();
     fence_before();
@@ -549,9 +559,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       fence_after();
       for (int c0 = r0 + hf * (nr / 2); c0 < r0 + (hf + 1) * (nr / 2); c0 += 32) {
         uint32_t dv[32], pv[16], acc[32];
-        tmem_ld32(lane_addr + DP + (c0 - r0), dv);
-        tmem_ld16(lane_addr + SP + (c0 >> 1), pv);
-        if (want_bias) tmem_ld32(lane_addr + ACC + c0, acc);
+        tmem_ld32_nw(lane_addr + DP + (c0 - r0), dv);
+        tmem_ld16_nw(lane_addr + SP + (c0 >> 1), pv);
+        if (want_bias) tmem_ld32_nw(lane_addr + ACC + c0, acc);
+        tmem_wait_ld();
         uint32_t dsk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -762,8 +773,9 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     if (tid == 0 && has_next) load_kv(b + 1);  // K, V tiles consumed
     for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) {
       uint32_t sv[32], dv[32];
-      tmem_ld32(lane_addr + c0, sv);
-      tmem_ld32(lane_addr + 256 + c0, dv);
+      tmem_ld32_nw(lane_addr + c0, sv);
+      tmem_ld32_nw(lane_addr + 256 + c0, dv);
+      tmem_wait_ld();
       float bb[32];
       if (BIASMODE) bias_row32<KCONTIG>(sBias, t, c0, bb);
       uint32_t pk[16], dk[16];
@@ -934,6 +946,7 @@ int64_t row_chunks(const evo_attn_desc *d) {
 template <int D, int BM_>
 int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   AttnTcArgs a = make_args(d);
+  a.Lp = (d->L + 63) / 64 * 64;  // softmax passes take 64-key steps (masked beyond L)
   CUtensorMap mq, mk, mv, mb;
   if (!head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, a.Lp) ||
