@@ -484,9 +484,21 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   }
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+  // per-row softmax statistics, prefetched one batch row ahead
+  float lse_n = 0.f, Dq_n = 0.f;
+  if (qv && b_lo < b_hi) {
+    lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
+    Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + q];
+  }
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
     const bool has_next = b + 1 < b_hi;
+    const float lse_l2 = lse_n * LOG2E;
+    const float Dq = Dq_n;
+    if (qv && has_next) {
+      lse_n = a.lse[((b + 1) * a.H + h) * (int64_t)L + q];
+      Dq_n = a.Dq[((b + 1) * a.H + h) * (int64_t)L + q];
+    }
     if (tid == 0) {
       mbar_wait(&bars[1], ph_a);
       mbar_wait(&bars[2], ph_k);
@@ -499,8 +511,6 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     }
     ph_a ^= 1;
     ph_k ^= 1;
-    const float lse_l2 = qv ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E : 0.f;
-    const float Dq = qv ? a.Dq[(b * a.H + h) * (int64_t)L + q] : 0.f;
     mbar_wait(&bars[3], ph_m);
     ph_m ^= 1;
     fence_after();
@@ -742,9 +752,26 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   }
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+  // this thread's slice of the per-query statistics, one batch row ahead
+  float lse_n = 0.f, Dq_n = 0.f;
+  if (tid < L && b_lo < b_hi) {
+    lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + tid] * LOG2E;
+    Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + tid];
+  }
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
     const bool has_next = b + 1 < b_hi;
+    if (tid < Lp) {
+      sLse[tid] = lse_n;
+      sDq[tid] = Dq_n;
+    }
+    if (tid < L && has_next) {
+      lse_n = a.lse[((b + 1) * a.H + h) * (int64_t)L + tid] * LOG2E;
+      Dq_n = a.Dq[((b + 1) * a.H + h) * (int64_t)L + tid];
+    } else {
+      lse_n = 0.f;
+      Dq_n = 0.f;
+    }
     if (tid == 0) {
       mbar_wait(&bars[1], ph_kv);
       mbar_wait(&bars[2], ph_q);
@@ -761,11 +788,6 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     }
     ph_kv ^= 1;
     ph_q ^= 1;
-    for (int i = tid; i < Lp; i += 256) {
-      const bool ok = i < L;
-      sLse[i] = ok ? a.lse[(b * a.H + h) * (int64_t)L + i] * LOG2E : 0.f;
-      sDq[i] = ok ? a.Dq[(b * a.H + h) * (int64_t)L + i] : 0.f;
-    }
     mbar_wait(&bars[3], ph_m);
     ph_m ^= 1;
     fence_after();
