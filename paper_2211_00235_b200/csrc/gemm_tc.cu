@@ -131,28 +131,30 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
     // Stage the warp's 32 rows x 32 columns through padded smem, then write
     // whole contiguous row segments per store instruction.
     const int lane = threadIdx.x & 31;
-#pragma unroll
-    for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = x[j];
-    __syncwarp();
     if (e.dtype_c == EVO_BF16) {
+      // packed bf16 pairs, row pitch 17 words (conflict-free both ways)
+      uint32_t *st32 = reinterpret_cast<uint32_t *>(stage);
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        __nv_bfloat162 h2 = __floats2bfloat162_rn(x[2 * j], x[2 * j + 1]);
+        st32[lane * 17 + j] = *reinterpret_cast<uint32_t *>(&h2);
+      }
+      __syncwarp();
       const int c = lane & 3;  // 8-column group
 #pragma unroll
       for (int i = 0; i < 4; ++i) {
         const int r = 8 * i + (lane >> 2);
         const int64_t rb = __shfl_sync(0xffffffffu, base, r);
         const bool ok = __shfl_sync(0xffffffffu, row_ok_g ? 1 : 0, r);
-        const float *src = stage + r * 33 + 8 * c;
-        uint32_t w[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          __nv_bfloat162 h2 = __floats2bfloat162_rn(src[2 * u], src[2 * u + 1]);
-          w[u] = *reinterpret_cast<uint32_t *>(&h2);
-        }
+        const uint32_t *src = st32 + r * 17 + 4 * c;
         if (ok)
           *reinterpret_cast<uint4 *>(reinterpret_cast<bf16 *>(e.C) + rb + 8 * c) =
-              make_uint4(w[0], w[1], w[2], w[3]);
+              make_uint4(src[0], src[1], src[2], src[3]);
       }
     } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) stage[lane * 33 + j] = x[j];
+      __syncwarp();
       const int c = lane & 7;  // 4-column group
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -322,7 +324,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // split the 32-column chunks of the tile between them.
     const int ew = warp - 2;
     const int q = warp & 3;
-    float *stage = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(tmem_slot) + 16) +
+    // derived from the __shared__ array itself so accesses stay LDS/STS
+    float *stage = reinterpret_cast<float *>(
+                       smem_raw + ((reinterpret_cast<uint8_t *>(tmem_slot) + 16) - smem_raw)) +
                    ew * (32 * 33);
     const int half = ew >> 2;  // 0 or 1
     int acc = 0;
