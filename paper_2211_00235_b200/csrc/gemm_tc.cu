@@ -66,6 +66,10 @@ __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_
   nt = t % p.tiles_n;
   int64_t r = t / p.tiles_n;
   mt = r % p.tiles_m;
+  // rotate n per m-row: consecutive tiles still share the A rows, but a CTA
+  // striding by the grid size no longer always lands on the same n-tile
+  // (148 % tiles_n == 0 would pin e.g. all sigmoid columns to 1/4 of the SMs)
+  nt = (nt + mt) % p.tiles_n;
   r /= p.tiles_m;
   sp = (int)(r % p.split);
   bidx = r / p.split;
