@@ -59,6 +59,8 @@ struct TcParams {
   uint32_t idesc;
   EpiArgs epi;
   float *partial;
+  int store_mode;  // 0: thread stores, 1: TMA 2-D, 2: TMA {cdiv, N/cdiv, M}, 3: TMA 4-D
+  int64_t cdiv, rdiv;
 };
 
 __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_t &bidx,
@@ -88,6 +90,41 @@ __device__ __forceinline__ float fast_sigmoid(float x) {
 // Finish one 32-column chunk of one output row: alpha, bias, activation,
 // residual, store.  Fully unrolled; vector stores when the chunk's 32
 // destination elements are contiguous and aligned.
+// alpha, bias and activation of one 32-column chunk (thread-per-row)
+template <int EPI>
+__device__ __forceinline__ void epi_math(const TcParams &p, const EpiArgs &e, const uint32_t (&v)[32],
+                                         int64_t nb, float (&x)[32]) {
+  const bool full = nb + 32 <= p.N;
+#pragma unroll
+  for (int j = 0; j < 32; ++j) x[j] = e.alpha * __uint_as_float(v[j]);
+  if constexpr (EPI != EK_NONE) {
+    if (full && ((reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0)) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        float4 b4 = reinterpret_cast<const float4 *>(e.bias + nb)[j];
+        x[4 * j] += b4.x; x[4 * j + 1] += b4.y; x[4 * j + 2] += b4.z; x[4 * j + 3] += b4.w;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] += (nb + j < p.N) ? e.bias[nb + j] : 0.f;
+    }
+  }
+  if constexpr (EPI == EK_BIAS_RELU) {
+#pragma unroll
+    for (int j = 0; j < 32; ++j) x[j] = fmaxf(x[j], 0.f);
+  }
+  if constexpr (EPI == EK_BIAS_SIGMOID) {
+    if (nb >= e.epi_col0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) x[j] = fast_sigmoid(x[j]);
+    } else if (nb + 32 > e.epi_col0) {
+#pragma unroll
+      for (int j = 0; j < 32; ++j)
+        if (nb + j >= e.epi_col0) x[j] = fast_sigmoid(x[j]);
+    }
+  }
+}
+
 template <int EPI>
 __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, const uint32_t (&v)[32],
                                           int64_t rbase, int64_t nb, bool row_ok_g, float *stage) {
@@ -195,7 +232,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const TcParams p) {
+               const __grid_constant__ CUtensorMap tmC, const TcParams p) {
   constexpr int SMEM_B = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = SMEM_A + SMEM_B;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
@@ -204,7 +241,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * SMEM_A;
-  uint64_t *full = reinterpret_cast<uint64_t *>(sB + STAGES * SMEM_B);
+  uint8_t *sW = sB + STAGES * SMEM_B;  // EPI_WARPS x 8 KiB, 1 KiB aligned
+  uint64_t *full = reinterpret_cast<uint64_t *>(sW + EPI_WARPS * 8192);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
@@ -216,6 +254,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     prefetch_map(&tmA);
     prefetch_map(&tmB);
+    if (p.store_mode) prefetch_map(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -328,10 +367,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     // split the 32-column chunks of the tile between them.
     const int ew = warp - 2;
     const int q = warp & 3;
-    // derived from the __shared__ array itself so accesses stay LDS/STS
-    float *stage = reinterpret_cast<float *>(
-                       smem_raw + ((reinterpret_cast<uint8_t *>(tmem_slot) + 16) - smem_raw)) +
-                   ew * (32 * 33);
+    // per-warp 8 KiB region (derived from the __shared__ array so accesses
+    // stay LDS/STS): two 4 KiB TMA-store boxes, or the padded staging tile
+    uint8_t *wreg = smem_raw + ((sW - smem_raw) + ew * 8192);
+    float *stage = reinterpret_cast<float *>(wreg);
+    uint32_t chunk_ctr = 0;
     const int half = ew >> 2;  // 0 or 1
     int acc = 0;
     uint32_t aphase = 0;
@@ -369,6 +409,48 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
           continue;
         }
+        if (p.store_mode != 0 && (mt * BM + q * 32) < p.M) {
+          // TMA bulk store of this warp's 32 x 32 chunk (rows/cols beyond
+          // M/N are clipped by the tensor map)
+          float x[32];
+          epi_math<EPI>(p, e, v, nb, x);
+          uint8_t *box = wreg + (chunk_ctr & 1) * 4096;
+          ++chunk_ctr;
+          if (lane == 0) bulk_wait_read<1>();  // box's previous store has read it
+          __syncwarp();
+          if (e.dtype_c == EVO_BF16) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
+                w[u] = *reinterpret_cast<uint32_t *>(&h2);
+              }
+              *reinterpret_cast<uint4 *>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          } else {
+#pragma unroll
+            for (int c = 0; c < 8; ++c)
+              *reinterpret_cast<float4 *>(box + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_float4(x[4 * c], x[4 * c + 1], x[4 * c + 2], x[4 * c + 3]);
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int mrow = (int)(mt * BM + q * 32);
+            if (p.store_mode == 1)
+              tma_store_2d(&tmC, box, (int)nb, mrow);
+            else if (p.store_mode == 2)
+              tma_store_3d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv), mrow);
+            else
+              tma_store_4d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv),
+                           (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+            bulk_commit();
+          }
+          continue;
+        }
         epi_chunk<EPI>(p, e, v, rbase, nb, row_ok, stage);
       }
       fence_before();
@@ -377,6 +459,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
+    if (lane == 0) bulk_wait_all();
   }
 
   fence_before();
@@ -463,6 +546,50 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
   return split < 1 ? 1 : split;
 }
 
+// TMA store map for C when its index map is expressible (no batching, no
+// residual / accumulate): returns the store mode (0 = not expressible).
+int make_store_map(CUtensorMap *map, const evo_gemm_desc *d) {
+  if (d->residual || d->accumulate || d->B1 * d->B2 != 1) return 0;
+  const evo_mat &c = d->C;
+  const int64_t es = d->dtype_c == EVO_BF16 ? 2 : 4;
+  if ((reinterpret_cast<uintptr_t>(c.ptr) & 15) != 0) return 0;
+  auto ok16 = [&](int64_t st) { return st > 0 && (st * es) % 16 == 0; };
+  cuuint64_t dims[4], strides[3];
+  cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
+  int rank, mode;
+  if (c.cdiv == 0 && c.rdiv == 0) {
+    if (c.cs != 1 || !ok16(c.rs)) return 0;
+    dims[0] = d->N; dims[1] = d->M;
+    strides[0] = c.rs * es;
+    box[0] = 32; box[1] = 32;
+    rank = 2; mode = 1;
+  } else if (c.cdiv > 0 && c.rdiv == 0) {
+    if (c.cs0 != 1 || c.cdiv % 32 || d->N % c.cdiv || !ok16(c.cs) || !ok16(c.rs)) return 0;
+    dims[0] = c.cdiv; dims[1] = d->N / c.cdiv; dims[2] = d->M;
+    strides[0] = c.cs * es; strides[1] = c.rs * es;
+    box[0] = 32; box[1] = 1; box[2] = 32;
+    rank = 3; mode = 2;
+  } else if (c.cdiv > 0 && c.rdiv > 0) {
+    if (c.cs0 != 1 || c.cdiv % 32 || d->N % c.cdiv || c.rdiv % 32 || d->M % c.rdiv ||
+        !ok16(c.cs) || !ok16(c.rs0) || !ok16(c.rs))
+      return 0;
+    dims[0] = c.cdiv; dims[1] = d->N / c.cdiv; dims[2] = c.rdiv; dims[3] = d->M / c.rdiv;
+    strides[0] = c.cs * es; strides[1] = c.rs0 * es; strides[2] = c.rs * es;
+    box[0] = 32; box[1] = 1; box[2] = 32; box[3] = 1;
+    rank = 4; mode = 3;
+  } else {
+    return 0;
+  }
+  EncodeTiledFn fn = encode_fn();
+  if (!fn) return 0;
+  CUresult r = fn(map, d->dtype_c == EVO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                                             : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
+                  rank, c.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  d->dtype_c == EVO_BF16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? mode : 0;
+}
+
 template <int BN, int STAGES, int EPI>
 int launch(const evo_gemm_desc *d, cudaStream_t st) {
   OperandPlan pa, pb;
@@ -487,13 +614,18 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
             ((uint32_t)(BM >> 4) << 24);
   p.epi = epi_args_of(d);
   p.partial = reinterpret_cast<float *>(d->workspace);
+  CUtensorMap mc;
+  p.store_mode = p.split > 1 ? 0 : make_store_map(&mc, d);
+  p.cdiv = d->C.cdiv > 0 ? d->C.cdiv : 1;
+  p.rdiv = d->C.rdiv > 0 ? d->C.rdiv : 1;
+  if (!p.store_mode) mc = ma;  // unused
   if (p.split > 1) {
     size_t need = (size_t)p.split * d->B1 * d->B2 * d->M * d->N * sizeof(float);
     EVO_REQUIRE(d->workspace && d->workspace_bytes >= need, EVO_EARG,
                 "evo_gemm(tc): split=%d needs %zu workspace bytes", p.split, need);
   }
-  const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) + 256 +
-                      (size_t)EPI_WARPS * 32 * 33 * 4;
+  const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) +
+                      (size_t)EPI_WARPS * 8192 + 256;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
@@ -501,7 +633,7 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
     attr_set = true;
   }
   int64_t grid = std::min<int64_t>(p.num_tiles, (int64_t)num_sms());
-  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, p);
+  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, mc, p);
   EVO_LAUNCHED("gemm_tc_kernel");
   if (p.split > 1) return gemm_splitk_reduce(d, p.split, p.partial, st);
   return EVO_OK;
@@ -527,8 +659,8 @@ size_t gemm_tc_workspace(const evo_gemm_desc *d) {
 
 template <int EPI>
 int launch_bn(const evo_gemm_desc *d, cudaStream_t st) {
-  if (choose_bn(d) == 256) return launch<256, 4, EPI>(d, st);
-  return launch<128, 6, EPI>(d, st);
+  if (choose_bn(d) == 256) return launch<256, 3, EPI>(d, st);
+  return launch<128, 4, EPI>(d, st);
 }
 
 int gemm_tc(const evo_gemm_desc *d, cudaStream_t st) {
