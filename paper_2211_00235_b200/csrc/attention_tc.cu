@@ -408,14 +408,63 @@ __global__ void attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm, bf16 *
   }
 }
 
+// ============================================================ bwd helpers
+__device__ __forceinline__ void tmem_st8(uint32_t taddr, const uint32_t (&v)[8]) {
+  asm volatile(
+      "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
+      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
+      : "memory");
+}
+__device__ __forceinline__ void tmem_ld8_nw(uint32_t taddr, uint32_t (&v)[8]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+               : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
+                 "=r"(v[6]), "=r"(v[7])
+               : "r"(taddr));
+}
+// 16 consecutive bias values of one row from a smem tile; ROWBOX: tile is
+// 32-key boxes of 128B-swizzled rows (read along the row), else a
+// [key][128 rows] tile read by column.
+template <bool ROWBOX>
+__device__ __forceinline__ void bias_row16(const uint8_t *sb, int row, int k0, float (&out)[16]) {
+  if constexpr (ROWBOX) {
+    const uint8_t *base = sb + (k0 >> 5) * 16384 + row * 128;
+    const int c0 = (k0 & 31) >> 2;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float4 v = *reinterpret_cast<const float4 *>(base + (((c0 + c) ^ (row & 7)) << 4));
+      out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
+    }
+  } else {
+    const float *p = reinterpret_cast<const float *>(sb) + k0 * 128 + row;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) out[j] = p[j * 128];
+  }
+}
+// Fold log2(e) into a resident bias tile once per CTA.
+__device__ __forceinline__ void scale_tile(uint8_t *sb, int nfloat4) {
+  float4 *p = reinterpret_cast<float4 *>(sb);
+  for (int i = threadIdx.x; i < nfloat4; i += blockDim.x) {
+    float4 v = p[i];
+    v.x *= LOG2E; v.y *= LOG2E; v.z *= LOG2E; v.w *= LOG2E;
+    p[i] = v;
+  }
+}
+// TMEM column of the 16-wide K slice `ks` of bf16-pair data written in place
+// into quarters: keys [i*KQ, (i+1)*KQ) -> cols [i*KQ, i*KQ + KQ/2).
+__device__ __forceinline__ uint32_t quarter_col(int ks, int KQ) {
+  const int k = 16 * ks;
+  return (uint32_t)((k / KQ) * KQ + (k % KQ) / 2);
+}
+
 // ======================================================================= dq
-// CTA = (128-query tile, head, chunk of batch rows); 256 threads, two per
-// query row (half hf = warp/4 owns keys [hf*Lp/2, (hf+1)*Lp/2)).
-// TMEM: [0,256) dbias accumulator (persists over the chunk), [256, 256+Lp)
-// S -> P (bf16 pairs, [256, 256+Lp/2)) -> dS (over P), [384, 512) dP rounds
-// of 128 keys, then dQ.
+// CTA = (128-query tile, head, chunk of batch rows), 512 threads: 4 threads
+// per query row, thread quarter `qr` owns keys [qr*KQ, (qr+1)*KQ) (KQ=Lp/4)
+// and keeps that slice of the dbias partial in REGISTERS across the chunk.
+// TMEM: S [0, Lp) and dP [256, 256+Lp) from back-to-back MMAs; one pass
+// computes P, dS, dbias and writes dS (bf16 pairs) in place into the
+// thread's own S columns; dq = scale * dS K as a TS MMA into [256, 256+D).
 template <int D, int BIASMODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512, 1)
 attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV,
                       const __grid_constant__ CUtensorMap mdO,
@@ -436,9 +485,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
-  const int hf = warp >> 2;
+  const int qr = warp >> 2;              // key quarter
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
-  const int L = a.L, Lp = a.Lp, half = Lp / 2;
+  const int L = a.L, Lp = a.Lp, KQ = Lp / 4;
   const int q = q0 + t;
   const bool qv = q < L;
   const bool want_bias = a.dbias_part != nullptr;
@@ -454,15 +503,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  const uint32_t ACC = 0, SP = 256, DP = 384;
-  if (want_bias) {
-    uint32_t z[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) z[j] = 0u;
-    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) tmem_st32(lane_addr + ACC + c0, z);
-    tmem_st_wait();
+  if (BIASMODE) {
+    mbar_wait(&bars[0], 0);
+    scale_tile(sBias, ((Lp + 31) / 32) * 16384 / 16);
+    __syncthreads();
   }
-  if (BIASMODE) mbar_wait(&bars[0], 0);
 
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
@@ -484,7 +529,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   }
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-  // per-row softmax statistics, prefetched one batch row ahead
+  const float sc_l2 = a.scale * LOG2E;
+  float acc[64];
+#pragma unroll
+  for (int j = 0; j < 64; ++j) acc[j] = 0.f;
   float lse_n = 0.f, Dq_n = 0.f;
   if (qv && b_lo < b_hi) {
     lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
@@ -505,8 +553,12 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       fence_after();
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks)
-        umma_bf16(tmem + SP, desc_kmajor_tile<D>(smem_u32(sQ), ks),
+        umma_bf16(tmem, desc_kmajor_tile<D>(smem_u32(sQ), ks),
                   desc_kmajor_tile<D>(smem_u32(sK), ks), idesc_s, ks > 0);
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sdO), ks),
+                  desc_kmajor_tile<D>(smem_u32(sV), ks), idesc_s, ks > 0);
       umma_commit(&bars[3]);
     }
     ph_a ^= 1;
@@ -514,148 +566,97 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     mbar_wait(&bars[3], ph_m);
     ph_m ^= 1;
     fence_after();
-    // P = exp(scale*S + bias - lse) for this thread's keys, staged packed
-    uint32_t stage[64];
+    if (tid == 0 && has_next) load_qdv(b + 1);  // Q, dO, V consumed
+    // one pass: P, dS, dbias for this thread's keys
 #pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      const int c0 = hf * half + 32 * i;
-      if (32 * i < half) {
-        uint32_t v[32];
-        tmem_ld32(lane_addr + SP + c0, v);
-        float bb[32];
-        if (BIASMODE) bias_row32<TB>(sBias, t, c0, bb);
+    for (int s = 0; s < 4; ++s) {
+      if (16 * s < KQ) {
+        const int k0 = qr * KQ + 16 * s;
+        uint32_t sv[16], dv[16];
+        tmem_ld16_nw(lane_addr + k0, sv);
+        tmem_ld16_nw(lane_addr + 256 + k0, dv);
+        tmem_wait_ld();
+        float bb[16];
+        if (BIASMODE) bias_row16<!TB>(sBias, t, k0, bb);
+        uint32_t pk[8];
 #pragma unroll
-        for (int j = 0; j < 32; j += 2) {
-          float p[2];
+        for (int j = 0; j < 16; j += 2) {
+          float ds[2];
 #pragma unroll
           for (int u = 0; u < 2; ++u) {
-            const int k = c0 + j + u;
-            float sc = __uint_as_float(v[j + u]) * a.scale;
-            if (BIASMODE) sc += bb[j + u];
-            p[u] = (qv && k < L) ? ex2(sc * LOG2E - lse_l2) : 0.f;
+            float x = __uint_as_float(sv[j + u]) * sc_l2 - lse_l2;
+            if (BIASMODE) x += bb[j + u];
+            float p = (qv && k0 + j + u < L) ? ex2(x) : 0.f;
+            ds[u] = p * (__uint_as_float(dv[j + u]) - Dq);
+            acc[16 * s + j + u] += ds[u];
           }
-          stage[16 * i + (j >> 1)] = pack2(p[0], p[1]);
+          pk[j >> 1] = pack2(ds[0], ds[1]);
         }
-      }
-    }
-    fence_before();
-    __syncthreads();  // every S read done before P overwrites it
-#pragma unroll
-    for (int i = 0; i < 4; ++i) {
-      if (32 * i < half) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) pk[j] = stage[16 * i + j];
-        tmem_st16(lane_addr + SP + ((hf * half + 32 * i) >> 1), pk);
+        tmem_st8(lane_addr + qr * KQ + 8 * s, pk);
       }
     }
     tmem_st_wait();
-    // dP in rounds of 128 keys into [DP, DP+128); dS over P; dbias += dS
-    for (int r0 = 0; r0 < Lp; r0 += 128) {
-      const int nr = min(128, Lp - r0);
-      fence_before();
-      __syncthreads();
-      if (tid == 0) {
-        fence_after();
-        const uint32_t idesc_dp = idesc_bf16(128, nr, false, false);
-#pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16(tmem + DP, desc_kmajor_tile<D>(smem_u32(sdO), ks),
-                    desc_kmajor_tile<D>(smem_u32(sV) + r0 * Sw<D>::bytes, ks), idesc_dp, ks > 0);
-        umma_commit(&bars[3]);
-      }
-      mbar_wait(&bars[3], ph_m);
-      ph_m ^= 1;
-      fence_after();
-      for (int c0 = r0 + hf * (nr / 2); c0 < r0 + (hf + 1) * (nr / 2); c0 += 32) {
-        uint32_t dv[32], pv[16], acc[32];
-        tmem_ld32_nw(lane_addr + DP + (c0 - r0), dv);
-        tmem_ld16_nw(lane_addr + SP + (c0 >> 1), pv);
-        if (want_bias) tmem_ld32_nw(lane_addr + ACC + c0, acc);
-        tmem_wait_ld();
-        uint32_t dsk[16];
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          float2 p2 = unpack2(pv[j]);
-          float ds0 = p2.x * (__uint_as_float(dv[2 * j]) - Dq);
-          float ds1 = p2.y * (__uint_as_float(dv[2 * j + 1]) - Dq);
-          if (want_bias) {
-            acc[2 * j] = __float_as_uint(__uint_as_float(acc[2 * j]) + ds0);
-            acc[2 * j + 1] = __float_as_uint(__uint_as_float(acc[2 * j + 1]) + ds1);
-          }
-          dsk[j] = pack2(ds0, ds1);
-        }
-        tmem_st16(lane_addr + SP + (c0 >> 1), dsk);
-        if (want_bias) tmem_st32(lane_addr + ACC + c0, acc);
-      }
-      tmem_st_wait();
-    }
     fence_before();
     __syncthreads();
     if (tid == 0) {
       fence_after();
-      if (has_next) load_qdv(b + 1);  // Q, dO, V consumed by the S / dP MMAs
       for (int ks = 0; ks < Lp / 16; ++ks)
-        umma_bf16_ts(tmem + DP, tmem + SP + ks * 8, desc_mnmajor_tile<D>(smem_u32(sK), ks),
-                     idesc_o, ks > 0);
+        umma_bf16_ts(tmem + 256, tmem + quarter_col(ks, KQ),
+                     desc_mnmajor_tile<D>(smem_u32(sK), ks), idesc_o, ks > 0);
       umma_commit(&bars[3]);
     }
     mbar_wait(&bars[3], ph_m);
     ph_m ^= 1;
     fence_after();
     if (tid == 0 && has_next) load_k(b + 1);
-    {
-      constexpr int HD = D / 2;  // each half stores D/2 columns of dq
-      float dq[HD];
-      uint32_t v[16];
-      if constexpr (HD == 16) {
-        tmem_ld16(lane_addr + DP + hf * 16, v);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) dq[j] = __uint_as_float(v[j]);
-      } else {
-        uint32_t v8[8];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(v8[0]), "=r"(v8[1]), "=r"(v8[2]), "=r"(v8[3]), "=r"(v8[4]), "=r"(v8[5]),
-              "=r"(v8[6]), "=r"(v8[7])
-            : "r"(lane_addr + DP + hf * 8));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < HD; ++j) dq[j] = __uint_as_float(v8[j]);
+    {  // dq row: 4 threads x D/4 columns
+      constexpr int QD = D / 4;
+      uint32_t v[8];
+      if constexpr (QD == 8) {
+        tmem_ld8_nw(lane_addr + 256 + qr * 8, v);
+      } else {  // D == 16: 4 columns each
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(lane_addr + 256 + qr * 4));
       }
+      tmem_wait_ld();
       if (qv) {
-        bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D + hf * HD;
-#pragma unroll
-        for (int d8 = 0; d8 < HD; d8 += 8) {
+        bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D + qr * QD;
+        if constexpr (QD == 8) {
           uint32_t w4[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
-            w4[j] = pack2(dq[d8 + 2 * j] * a.scale, dq[d8 + 2 * j + 1] * a.scale);
-          *reinterpret_cast<uint4 *>(dst + d8) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+            w4[j] = pack2(__uint_as_float(v[2 * j]) * a.scale,
+                          __uint_as_float(v[2 * j + 1]) * a.scale);
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        } else {
+          uint32_t w2[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            w2[j] = pack2(__uint_as_float(v[2 * j]) * a.scale,
+                          __uint_as_float(v[2 * j + 1]) * a.scale);
+          *reinterpret_cast<uint2 *>(dst) = make_uint2(w2[0], w2[1]);
         }
       }
     }
     fence_before();
-    __syncthreads();  // TMEM work columns free for the next row
+    __syncthreads();  // TMEM + smem free for the next row
     fence_after();
   }
-  if (want_bias) {
-    float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L;
-    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) {
-      uint32_t v[32];
-      tmem_ld32(lane_addr + ACC + c0, v);  // warp-collective: every lane loads
-      if (!qv) continue;
-      const int64_t rb = (int64_t)h * a.bh + (int64_t)q * a.bq;
-      if (a.bk == 1 && c0 + 32 <= L && ((rb + c0) & 3) == 0) {
+  if (want_bias && qv) {
+    float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
+                 (int64_t)h * a.bh + (int64_t)q * a.bq;
+    const int kbase = qr * KQ;
+    if (a.bk == 1 && kbase + KQ <= L && ((reinterpret_cast<uintptr_t>(dst + kbase) & 15) == 0)) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          reinterpret_cast<float4 *>(dst + rb + c0)[j] =
-              make_float4(__uint_as_float(v[4 * j]), __uint_as_float(v[4 * j + 1]),
-                          __uint_as_float(v[4 * j + 2]), __uint_as_float(v[4 * j + 3]));
-      } else {
-        for (int j = 0; j < 32; ++j)
-          if (c0 + j < L) dst[rb + (int64_t)(c0 + j) * a.bk] = __uint_as_float(v[j]);
-      }
+      for (int j = 0; j < 64; j += 4)
+        if (j < KQ)
+          *reinterpret_cast<float4 *>(dst + kbase + j) =
+              make_float4(acc[j], acc[j + 1], acc[j + 2], acc[j + 3]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 64; ++j)
+        if (j < KQ && kbase + j < L) dst[(int64_t)(kbase + j) * a.bk] = acc[j];
     }
   }
   fence_before();
@@ -664,12 +665,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 }
 
 // ====================================================================== dkv
-// CTA = (128-key tile, head, chunk of batch rows); 256 threads, two per key
-// row (half hf owns queries [hf*Lp/2, (hf+1)*Lp/2)).  Bias tile for the key
-// tile and all queries stays in smem.  TMEM: S^T [0, Lp), dP^T [256, 256+Lp);
-// P^T / dS^T bf16 pairs written in place inside each half's own columns:
-// half 0 -> [0, Lp/4), half 1 -> [Lp/2, 3Lp/4) (and +256 for dS^T).
-template <bool TBK>  // keys contiguous in smem tile (plain bias) ?
+// CTA = (128-key tile, head, chunk of batch rows), 512 threads, 4 per key
+// row; quarter qr owns queries [qr*QQ, (qr+1)*QQ).  TMEM: S^T [0, Lp),
+// dP^T [256, 256+Lp); P^T and dS^T written in place (bf16 pairs) into each
+// thread's own columns; dv = P^T dO and dk = scale * dS^T Q as TS MMAs.
+template <bool TBK>  // keys contiguous in the smem tile (plain bias)?
 __device__ __forceinline__ void load_bias_tile_k(uint8_t *sb, const CUtensorMap *map,
                                                  uint64_t *bar, int h, int k0, int Lp) {
   const int nbox = (Lp + 31) / 32;
@@ -682,19 +682,15 @@ __device__ __forceinline__ void load_bias_tile_k(uint8_t *sb, const CUtensorMap 
   }
 }
 
-__device__ __forceinline__ uint32_t half_col(int c, int Lp) {
-  return (uint32_t)(c < Lp / 2 ? c / 2 : Lp / 2 + (c - Lp / 2) / 2);
-}
-
 template <int D, int BIASMODE>
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(512, 1)
 attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_constant__ CUtensorMap mVt,
                        const __grid_constant__ CUtensorMap mQa,
                        const __grid_constant__ CUtensorMap mdOa,
                        const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
-  // plain bias (bk == 1): smem [q][128 k] (keys contiguous, read by column)
+  // plain bias (bk == 1): smem [q][128 k], read by column;
   // transposed (bq == 1): 32-query boxes [k][32 q], 128B-swizzled rows
   constexpr bool KCONTIG = BIASMODE == 1;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -712,9 +708,9 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // key row in the tile
-  const int hf = warp >> 2;
+  const int qr = warp >> 2;              // query quarter
   const int k0 = blockIdx.x * QT, h = blockIdx.y;
-  const int L = a.L, Lp = a.Lp, half = Lp / 2;
+  const int L = a.L, Lp = a.Lp, QQ = Lp / 4;
   const int k = k0 + t;
   const bool kv = k < L;
 
@@ -729,8 +725,13 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  if (BIASMODE) mbar_wait(&bars[0], 0);
-  const uint32_t DVC = Lp >= 256 ? 64u : 128u;  // free columns for dV (and +256 for dK)
+  if (BIASMODE) {
+    mbar_wait(&bars[0], 0);
+    scale_tile(sBias, ((Lp + 31) / 32) * 16384 / 16);
+    __syncthreads();
+  }
+  // free columns for dV / dK after the in-place P^T / dS^T packing
+  const uint32_t DVC = Lp >= 256 ? (uint32_t)(QQ / 2) : (uint32_t)Lp;
 
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
@@ -752,7 +753,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   }
   const uint32_t idesc_s = idesc_bf16(128, Lp, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-  // this thread's slice of the per-query statistics, one batch row ahead
+  const float sc_l2 = a.scale * LOG2E;
   float lse_n = 0.f, Dq_n = 0.f;
   if (tid < L && b_lo < b_hi) {
     lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + tid] * LOG2E;
@@ -791,34 +792,36 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     mbar_wait(&bars[3], ph_m);
     ph_m ^= 1;
     fence_after();
-    __syncthreads();  // lse / Dq visible
+    __syncthreads();  // lse / Dq of this row visible
     if (tid == 0 && has_next) load_kv(b + 1);  // K, V tiles consumed
-    for (int c0 = hf * half; c0 < (hf + 1) * half; c0 += 32) {
-      uint32_t sv[32], dv[32];
-      tmem_ld32_nw(lane_addr + c0, sv);
-      tmem_ld32_nw(lane_addr + 256 + c0, dv);
-      tmem_wait_ld();
-      float bb[32];
-      if (BIASMODE) bias_row32<KCONTIG>(sBias, t, c0, bb);
-      uint32_t pk[16], dk[16];
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        float p[2], ds[2];
+    for (int s = 0; s < 4; ++s) {
+      if (16 * s < QQ) {
+        const int c0 = qr * QQ + 16 * s;
+        uint32_t sv[16], dv[16];
+        tmem_ld16_nw(lane_addr + c0, sv);
+        tmem_ld16_nw(lane_addr + 256 + c0, dv);
+        tmem_wait_ld();
+        float bb[16];
+        if (BIASMODE) bias_row16<!KCONTIG>(sBias, t, c0, bb);
+        uint32_t pk[8], dk8[8];
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
-          const int qq = c0 + j + u;
-          float s = __uint_as_float(sv[j + u]) * a.scale;
-          if (BIASMODE) s += bb[j + u];
-          const bool ok = kv && qq < L;
-          p[u] = ok ? ex2(s * LOG2E - sLse[qq]) : 0.f;
-          ds[u] = p[u] * (__uint_as_float(dv[j + u]) - sDq[qq]);
+        for (int j = 0; j < 16; j += 2) {
+          float p[2], ds[2];
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            const int qq = c0 + j + u;
+            float x = __uint_as_float(sv[j + u]) * sc_l2 - sLse[qq];
+            if (BIASMODE) x += bb[j + u];
+            p[u] = (kv && qq < L) ? ex2(x) : 0.f;
+            ds[u] = p[u] * (__uint_as_float(dv[j + u]) - sDq[qq]);
+          }
+          pk[j >> 1] = pack2(p[0], p[1]);
+          dk8[j >> 1] = pack2(ds[0], ds[1]);
         }
-        pk[j >> 1] = pack2(p[0], p[1]);
-        dk[j >> 1] = pack2(ds[0], ds[1]);
+        tmem_st8(lane_addr + qr * QQ + 8 * s, pk);
+        tmem_st8(lane_addr + 256 + qr * QQ + 8 * s, dk8);
       }
-      const uint32_t dc = half_col(c0, Lp);
-      tmem_st16(lane_addr + dc, pk);
-      tmem_st16(lane_addr + 256 + dc, dk);
     }
     tmem_st_wait();
     fence_before();
@@ -826,10 +829,10 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     if (tid == 0) {
       fence_after();
       for (int ks = 0; ks < Lp / 16; ++ks)
-        umma_bf16_ts(tmem + DVC, tmem + half_col(16 * ks, Lp),
+        umma_bf16_ts(tmem + DVC, tmem + quarter_col(ks, QQ),
                      desc_mnmajor_tile<D>(smem_u32(sdO), ks), idesc_o, ks > 0);
       for (int ks = 0; ks < Lp / 16; ++ks)
-        umma_bf16_ts(tmem + 256 + DVC, tmem + 256 + half_col(16 * ks, Lp),
+        umma_bf16_ts(tmem + 256 + DVC, tmem + 256 + quarter_col(ks, QQ),
                      desc_mnmajor_tile<D>(smem_u32(sQ), ks), idesc_o, ks > 0);
       umma_commit(&bars[3]);
     }
@@ -837,49 +840,43 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     ph_m ^= 1;
     fence_after();
     if (tid == 0 && has_next) load_q(b + 1);  // Q, dO consumed
-    {
-      constexpr int HD = D / 2;
-      float dvr[HD], dkr[HD];
-      if constexpr (HD == 16) {
-        uint32_t v1[16], v2[16];
-        tmem_ld16(lane_addr + DVC + hf * 16, v1);
-        tmem_ld16(lane_addr + 256 + DVC + hf * 16, v2);
-#pragma unroll
-        for (int j = 0; j < 16; ++j) {
-          dvr[j] = __uint_as_float(v1[j]);
-          dkr[j] = __uint_as_float(v2[j]);
-        }
+    {  // dv, dk rows: 4 threads x D/4 columns
+      constexpr int QD = D / 4;
+      uint32_t v1[8], v2[8];
+      if constexpr (QD == 8) {
+        tmem_ld8_nw(lane_addr + DVC + qr * 8, v1);
+        tmem_ld8_nw(lane_addr + 256 + DVC + qr * 8, v2);
       } else {
-        uint32_t v1[8], v2[8];
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3]), "=r"(v1[4]), "=r"(v1[5]),
-              "=r"(v1[6]), "=r"(v1[7])
-            : "r"(lane_addr + DVC + hf * 8));
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
-            : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3]), "=r"(v2[4]), "=r"(v2[5]),
-              "=r"(v2[6]), "=r"(v2[7])
-            : "r"(lane_addr + 256 + DVC + hf * 8));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-#pragma unroll
-        for (int j = 0; j < HD; ++j) {
-          dvr[j] = __uint_as_float(v1[j]);
-          dkr[j] = __uint_as_float(v2[j]);
-        }
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3])
+                     : "r"(lane_addr + DVC + qr * 4));
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3])
+                     : "r"(lane_addr + 256 + DVC + qr * 4));
       }
+      tmem_wait_ld();
       if (kv) {
-        const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D + hf * HD;
-#pragma unroll
-        for (int d8 = 0; d8 < HD; d8 += 8) {
+        const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D + qr * QD;
+        if constexpr (QD == 8) {
           uint32_t w1[4], w2[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j) {
-            w1[j] = pack2(dvr[d8 + 2 * j], dvr[d8 + 2 * j + 1]);
-            w2[j] = pack2(dkr[d8 + 2 * j] * a.scale, dkr[d8 + 2 * j + 1] * a.scale);
+            w1[j] = pack2(__uint_as_float(v1[2 * j]), __uint_as_float(v1[2 * j + 1]));
+            w2[j] = pack2(__uint_as_float(v2[2 * j]) * a.scale,
+                          __uint_as_float(v2[2 * j + 1]) * a.scale);
           }
-          *reinterpret_cast<uint4 *>(a.dv + off + d8) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
-          *reinterpret_cast<uint4 *>(a.dk + off + d8) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+          *reinterpret_cast<uint4 *>(a.dv + off) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+          *reinterpret_cast<uint4 *>(a.dk + off) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+        } else {
+          uint32_t w1[2], w2[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j) {
+            w1[j] = pack2(__uint_as_float(v1[2 * j]), __uint_as_float(v1[2 * j + 1]));
+            w2[j] = pack2(__uint_as_float(v2[2 * j]) * a.scale,
+                          __uint_as_float(v2[2 * j + 1]) * a.scale);
+          }
+          *reinterpret_cast<uint2 *>(a.dv + off) = make_uint2(w1[0], w1[1]);
+          *reinterpret_cast<uint2 *>(a.dk + off) = make_uint2(w2[0], w2[1]);
         }
       }
     }
@@ -1073,7 +1070,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         2 * 256 * 2 * D + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dq_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    attn_bwd_dq_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
   {
@@ -1081,7 +1078,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         2 * (size_t)QT * 2 * D + 2 * 256 * 4 + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dkv_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    attn_bwd_dkv_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
     EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");
   }
   if (d->dbias)
