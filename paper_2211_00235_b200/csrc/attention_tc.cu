@@ -478,10 +478,10 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   uint8_t *sBias = sm;
   uint8_t *sQ = sBias + (BIASMODE ? BIAS_BYTES : 0);
   uint8_t *sdO = sQ + TILE;
-  uint8_t *sK = sdO + TILE;
-  uint8_t *sV = sK + FULL;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sV + FULL);  // 0 bias, 1 q/dO/V, 2 K, 3 mma
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 4);
+  uint8_t *sV = sdO + TILE;
+  uint8_t *sK2 = sV + FULL;  // two K buffers (K of row b+1 streams in during row b)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sK2 + 2 * FULL);  // 0 bias, 1 q/dO/V, 2-3 K, 4 mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 5);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
@@ -493,7 +493,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   const bool want_bias = a.dbias_part != nullptr;
 
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, Lp);
   }
@@ -511,7 +511,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
-  uint32_t ph_a = 0, ph_k = 0, ph_m = 0;
+  uint32_t ph_a = 0, ph_m = 0, ph_k2 = 0;  // ph_k2: bit i = phase of K buffer i
   const uint32_t kv_bytes = (uint32_t)Lp * Sw<D>::bytes;
   auto load_qdv = [&](int64_t bb) {
     mbar_expect_tx(&bars[1], 2 * TILE + kv_bytes);
@@ -520,8 +520,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     tma_load_4d(sV, &mV, &bars[1], 0, 0, (int)bb, h);
   };
   auto load_k = [&](int64_t bb) {
-    mbar_expect_tx(&bars[2], kv_bytes);
-    tma_load_4d(sK, &mK, &bars[2], 0, 0, (int)bb, h);
+    const int kb = (int)((bb - b_lo) & 1);
+    mbar_expect_tx(&bars[2 + kb], kv_bytes);
+    tma_load_4d(sK2 + kb * FULL, &mK, &bars[2 + kb], 0, 0, (int)bb, h);
   };
   if (tid == 0 && b_lo < b_hi) {
     load_qdv(b_lo);
@@ -541,6 +542,8 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
     const bool has_next = b + 1 < b_hi;
+    const int kb = (int)((b - b_lo) & 1);
+    uint8_t *sK = sK2 + kb * FULL;
     const float lse_l2 = lse_n * LOG2E;
     const float Dq = Dq_n;
     if (qv && has_next) {
@@ -548,8 +551,9 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       Dq_n = a.Dq[((b + 1) * a.H + h) * (int64_t)L + q];
     }
     if (tid == 0) {
+      if (has_next) load_k(b + 1);  // the other K buffer is idle since row b-1
       mbar_wait(&bars[1], ph_a);
-      mbar_wait(&bars[2], ph_k);
+      mbar_wait(&bars[2 + kb], (ph_k2 >> kb) & 1);
       fence_after();
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks)
@@ -559,11 +563,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       for (int ks = 0; ks < D / 16; ++ks)
         umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sdO), ks),
                   desc_kmajor_tile<D>(smem_u32(sV), ks), idesc_s, ks > 0);
-      umma_commit(&bars[3]);
+      umma_commit(&bars[4]);
     }
     ph_a ^= 1;
-    ph_k ^= 1;
-    mbar_wait(&bars[3], ph_m);
+    ph_k2 ^= 1u << kb;
+    mbar_wait(&bars[4], ph_m);
     ph_m ^= 1;
     fence_after();
     if (tid == 0 && has_next) load_qdv(b + 1);  // Q, dO, V consumed
@@ -603,12 +607,11 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       for (int ks = 0; ks < Lp / 16; ++ks)
         umma_bf16_ts(tmem + 256, tmem + quarter_col(ks, KQ),
                      desc_mnmajor_tile<D>(smem_u32(sK), ks), idesc_o, ks > 0);
-      umma_commit(&bars[3]);
+      umma_commit(&bars[4]);
     }
-    mbar_wait(&bars[3], ph_m);
+    mbar_wait(&bars[4], ph_m);
     ph_m ^= 1;
     fence_after();
-    if (tid == 0 && has_next) load_k(b + 1);
     {  // dq row: 4 threads x D/4 columns
       constexpr int QD = D / 4;
       uint32_t v[8];
@@ -697,14 +700,13 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   uint8_t *sm = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
                                             ~uintptr_t(1023));
   uint8_t *sBias = sm;
-  uint8_t *sQ = sBias + (BIASMODE ? BIAS_BYTES : 0);
-  uint8_t *sdO = sQ + FULL;
-  uint8_t *sK = sdO + FULL;
+  uint8_t *sQ2 = sBias + (BIASMODE ? BIAS_BYTES : 0);  // two (Q | dO) buffers
+  uint8_t *sK = sQ2 + 4 * FULL;
   uint8_t *sV = sK + TILE;
   float *sLse = reinterpret_cast<float *>(sV + TILE);
   float *sDq = sLse + 256;
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);  // 0 bias, 1 K/V, 2 Q/dO, 3 mma
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 4);
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);  // 0 bias, 1 K/V, 2-3 Q/dO, 4 mma
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 5);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // key row in the tile
@@ -715,7 +717,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   const bool kv = k < L;
 
   if (tid == 0) {
-    for (int i = 0; i < 4; ++i) mbar_init(&bars[i], 1);
+    for (int i = 0; i < 5; ++i) mbar_init(&bars[i], 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars[0], h, k0, Lp);
   }
@@ -735,7 +737,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
 
   const int64_t b_lo = blockIdx.z * a.chunk;
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
-  uint32_t ph_kv = 0, ph_q = 0, ph_m = 0;
+  uint32_t ph_kv = 0, ph_q2 = 0, ph_m = 0;
   const uint32_t all_bytes = (uint32_t)Lp * Sw<D>::bytes;
   auto load_kv = [&](int64_t bb) {
     mbar_expect_tx(&bars[1], 2 * TILE);
@@ -743,9 +745,10 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
     tma_load_4d(sV, &mVt, &bars[1], 0, k0, (int)bb, h);
   };
   auto load_q = [&](int64_t bb) {
-    mbar_expect_tx(&bars[2], 2 * all_bytes);
-    tma_load_4d(sQ, &mQa, &bars[2], 0, 0, (int)bb, h);
-    tma_load_4d(sdO, &mdOa, &bars[2], 0, 0, (int)bb, h);
+    const int qb = (int)((bb - b_lo) & 1);
+    mbar_expect_tx(&bars[2 + qb], 2 * all_bytes);
+    tma_load_4d(sQ2 + qb * 2 * FULL, &mQa, &bars[2 + qb], 0, 0, (int)bb, h);
+    tma_load_4d(sQ2 + qb * 2 * FULL + FULL, &mdOa, &bars[2 + qb], 0, 0, (int)bb, h);
   };
   if (tid == 0 && b_lo < b_hi) {
     load_kv(b_lo);
@@ -762,6 +765,9 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
 
   for (int64_t b = b_lo; b < b_hi; ++b) {
     const bool has_next = b + 1 < b_hi;
+    const int qb = (int)((b - b_lo) & 1);
+    uint8_t *sQ = sQ2 + qb * 2 * FULL;
+    uint8_t *sdO = sQ + FULL;
     if (tid < Lp) {
       sLse[tid] = lse_n;
       sDq[tid] = Dq_n;
@@ -774,8 +780,9 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
       Dq_n = 0.f;
     }
     if (tid == 0) {
+      if (has_next) load_q(b + 1);  // the other Q/dO buffer is idle since row b-1
       mbar_wait(&bars[1], ph_kv);
-      mbar_wait(&bars[2], ph_q);
+      mbar_wait(&bars[2 + qb], (ph_q2 >> qb) & 1);
       fence_after();
 #pragma unroll
       for (int ks = 0; ks < D / 16; ++ks)
@@ -785,11 +792,11 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
       for (int ks = 0; ks < D / 16; ++ks)
         umma_bf16(tmem + 256, desc_kmajor_tile<D>(smem_u32(sV), ks),
                   desc_kmajor_tile<D>(smem_u32(sdO), ks), idesc_s, ks > 0);
-      umma_commit(&bars[3]);
+      umma_commit(&bars[4]);
     }
     ph_kv ^= 1;
-    ph_q ^= 1;
-    mbar_wait(&bars[3], ph_m);
+    ph_q2 ^= 1u << qb;
+    mbar_wait(&bars[4], ph_m);
     ph_m ^= 1;
     fence_after();
     __syncthreads();  // lse / Dq of this row visible
@@ -834,12 +841,11 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
       for (int ks = 0; ks < Lp / 16; ++ks)
         umma_bf16_ts(tmem + 256 + DVC, tmem + 256 + quarter_col(ks, QQ),
                      desc_mnmajor_tile<D>(smem_u32(sQ), ks), idesc_o, ks > 0);
-      umma_commit(&bars[3]);
+      umma_commit(&bars[4]);
     }
-    mbar_wait(&bars[3], ph_m);
+    mbar_wait(&bars[4], ph_m);
     ph_m ^= 1;
     fence_after();
-    if (tid == 0 && has_next) load_q(b + 1);  // Q, dO consumed
     {  // dv, dk rows: 4 threads x D/4 columns
       constexpr int QD = D / 4;
       uint32_t v1[8], v2[8];
@@ -1067,14 +1073,14 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   const int tiles = (d->L + QT - 1) / QT;
   {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
-                        2 * 256 * 2 * D + 128;
+                        3 * 256 * 2 * D + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
     attn_bwd_dq_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
   {
-    const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * 256 * 2 * D +
+    const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 4 * 256 * 2 * D +
                         2 * (size_t)QT * 2 * D + 2 * 256 * 4 + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);

@@ -53,8 +53,11 @@ int relu_bwd(int, int64_t, const void *, const void *, void *, cudaStream_t);
 int sq_mean(int64_t, const float *, float *, float *, void *, cudaStream_t);
 int add(int64_t, const float *, const float *, float *, cudaStream_t);
 
+static bool use_skinny(const evo_gemm_desc *d) {
+  return g_gemm_policy == 0 && !d->force_simt && gemm_skinny_accepts(d);
+}
 static bool use_tc(const evo_gemm_desc *d) {
-  return g_gemm_policy == 0 && !d->force_simt && gemm_tc_accepts(d);
+  return g_gemm_policy == 0 && !d->force_simt && !gemm_skinny_accepts(d) && gemm_tc_accepts(d);
 }
 
 }  // namespace evo
@@ -74,6 +77,7 @@ int evo_tc_available(void) { return g_gemm_policy == 0 ? 1 : 0; }
 
 size_t evo_gemm_workspace_bytes(const evo_gemm_desc *d) {
   if (!d) return 0;
+  if (use_skinny(d)) return gemm_skinny_workspace(d);
   return use_tc(d) ? gemm_tc_workspace(d) : gemm_simt_workspace(d);
 }
 
@@ -95,6 +99,7 @@ int evo_gemm(const evo_gemm_desc *d, void *stream) {
     CHECK_PTR(d->B.ptr);
   }
   cudaStream_t st = as_stream(stream);
+  if (use_skinny(d) && d->K > 0) return gemm_skinny(d, st);
   if (use_tc(d)) {
     int rc = gemm_tc(d, st);
     if (rc != EVO_EUNSUP) return rc;

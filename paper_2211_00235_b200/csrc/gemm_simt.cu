@@ -152,19 +152,36 @@ SimtArgs make_args(const evo_gemm_desc *d, int split, int64_t k_chunk) {
   return a;
 }
 
-__global__ void splitk_reduce_kernel(EpiArgs e, int64_t M, int64_t N, int64_t B2,
-                                     int64_t nbatch, int split, const float *partial) {
+// P consecutive outputs per block; the 256/P thread groups take partials
+// g, g + 256/P, ... and the group sums are combined in order (fixed order:
+// deterministic).  P = 8 when there are few outputs and many partials, so
+// the reduction still spreads over every SM.
+template <int P>
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(EpiArgs e, int64_t M, int64_t N,
+                                                            int64_t B2, int64_t nbatch, int split,
+                                                            const float *partial) {
+  constexpr int G = 256 / P;
+  __shared__ float red[G][P + 1];
+  const int o = threadIdx.x % P, grp = threadIdx.x / P;
   const int64_t total = nbatch * M * N;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < total;
-       idx += (int64_t)gridDim.x * blockDim.x) {
-    int64_t n = idx % N;
-    int64_t m = (idx / N) % M;
-    int64_t bidx = idx / (M * N);
-    float v = 0.f;
-    for (int s = 0; s < split; ++s) v += partial[(int64_t)s * total + idx];
-    int64_t b1 = bidx / B2, b2 = bidx % B2;
-    int64_t off = b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m) + e.cmap.col(n);
-    epi_store(e, off, epi_value(e, n, v));
+  const int64_t idx = blockIdx.x * (int64_t)P + o;
+  float v = 0.f;
+  if (idx < total) {
+#pragma unroll 4
+    for (int s = grp; s < split; s += G) v += partial[(int64_t)s * total + idx];
+  }
+  red[grp][o] = v;
+  __syncthreads();
+  if (threadIdx.x < P && idx < total) {
+    float t = red[0][o];
+#pragma unroll 8
+    for (int j = 1; j < G; ++j) t += red[j][o];
+    const int64_t n = idx % N;
+    const int64_t m = (idx / N) % M;
+    const int64_t bidx = idx / (M * N);
+    const int64_t b1 = bidx / B2, b2 = bidx % B2;
+    const int64_t off = b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m) + e.cmap.col(n);
+    epi_store(e, off, epi_value(e, n, t));
   }
 }
 
@@ -173,9 +190,14 @@ __global__ void splitk_reduce_kernel(EpiArgs e, int64_t M, int64_t N, int64_t B2
 int gemm_splitk_reduce(const evo_gemm_desc *d, int split, const float *partial,
                        cudaStream_t st) {
   const int64_t total = d->B1 * d->B2 * d->M * d->N;
-  int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
-  splitk_reduce_kernel<<<blocks, 256, 0, st>>>(epi_args_of(d), d->M, d->N, d->B2,
-                                               d->B1 * d->B2, split, partial);
+  EVO_REQUIRE((total + 31) / 32 < (1ll << 31), EVO_EDIM, "evo_gemm: split-K output too large");
+  if (total / 32 < 2 * (int64_t)num_sms() && split > 32) {
+    splitk_reduce_kernel<8><<<(unsigned)((total + 7) / 8), 256, 0, st>>>(
+        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+  } else {
+    splitk_reduce_kernel<32><<<(unsigned)((total + 31) / 32), 256, 0, st>>>(
+        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+  }
   EVO_LAUNCHED("splitk_reduce_kernel");
   return EVO_OK;
 }

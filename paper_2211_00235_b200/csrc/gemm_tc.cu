@@ -410,10 +410,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           continue;
         }
         if (p.store_mode != 0 && (mt * BM + q * 32) < p.M) {
-          // TMA bulk store of this warp's 32 x 32 chunk (rows/cols beyond
-          // M/N are clipped by the tensor map)
+          // TMA bulk store (or reduce-add, for accumulate) of this warp's
+          // 32 x 32 chunk; rows/cols beyond M/N are clipped by the map
           float x[32];
           epi_math<EPI>(p, e, v, nb, x);
+          if (e.residual) {  // fp32, plain 2-D layout (same map as C)
+            if (row_ok) {
+              const float4 *rp = reinterpret_cast<const float4 *>(e.residual + rbase + nb);
+              if (nb + 32 <= p.N) {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                  const float4 r4 = __ldg(rp + j);
+                  x[4 * j] += r4.x; x[4 * j + 1] += r4.y; x[4 * j + 2] += r4.z; x[4 * j + 3] += r4.w;
+                }
+              } else {
+#pragma unroll
+                for (int j = 0; j < 32; ++j)
+                  if (nb + j < p.N) x[j] += e.residual[rbase + nb + j];
+              }
+            }
+          }
           uint8_t *box = wreg + (chunk_ctr & 1) * 4096;
           ++chunk_ctr;
           if (lane == 0) bulk_wait_read<1>();  // box's previous store has read it
@@ -440,13 +456,22 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           __syncwarp();
           if (lane == 0) {
             const int mrow = (int)(mt * BM + q * 32);
-            if (p.store_mode == 1)
+            if (e.accumulate) {
+              if (p.store_mode == 1)
+                tma_radd_2d(&tmC, box, (int)nb, mrow);
+              else if (p.store_mode == 2)
+                tma_radd_3d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv), mrow);
+              else
+                tma_radd_4d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv),
+                            (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+            } else if (p.store_mode == 1) {
               tma_store_2d(&tmC, box, (int)nb, mrow);
-            else if (p.store_mode == 2)
+            } else if (p.store_mode == 2) {
               tma_store_3d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv), mrow);
-            else
+            } else {
               tma_store_4d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv),
                            (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+            }
             bulk_commit();
           }
           continue;
@@ -546,10 +571,15 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
   return split < 1 ? 1 : split;
 }
 
-// TMA store map for C when its index map is expressible (no batching, no
-// residual / accumulate): returns the store mode (0 = not expressible).
+// TMA store map for C when its index map is expressible (no batching; a
+// residual only for fp32 plain 2-D outputs, accumulate only for fp32, done
+// as a bulk reduce-add): returns the store mode (0 = not expressible).
 int make_store_map(CUtensorMap *map, const evo_gemm_desc *d) {
-  if (d->residual || d->accumulate || d->B1 * d->B2 != 1) return 0;
+  if (d->B1 * d->B2 != 1) return 0;
+  if ((d->residual || d->accumulate) && d->dtype_c != EVO_F32) return 0;
+  if (d->residual && (d->accumulate || d->C.cdiv || d->C.rdiv ||
+                      (reinterpret_cast<uintptr_t>(d->residual) & 15) != 0))
+    return 0;
   const evo_mat &c = d->C;
   const int64_t es = d->dtype_c == EVO_BF16 ? 2 : 4;
   if ((reinterpret_cast<uintptr_t>(c.ptr) & 15) != 0) return 0;

@@ -385,10 +385,12 @@ def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act):
            Mat(dor, c * r * c, r * c, rdiv=r, rs0=c, cdiv=c, cs0=1), r2, c * c, cz,
            alpha=1.0 / s)
     dab = _empty((2, rows, c), act, dev)
-    # da[s,(i,p)] = sum_(j,q) do'[(i,p),(j,q)] b[s,(j,q)]
-    K.gemm(Mat(dor, rc, 1), Mat(ab[1], rc, 1), Mat(dab[0], 1, rc), rc, s, rc)
-    # db[s,(j,q)] = sum_(i,p) do'[(i,p),(j,q)] a[s,(i,p)]
-    K.gemm(Mat(dor, 1, rc), Mat(ab[0], rc, 1), Mat(dab[1], 1, rc), rc, s, rc)
+    # da[s,(i,p)] = sum_(j,q) b[s,(j,q)] do'[(i,p),(j,q)]   (m = s: row-major
+    # output for the TMA store; split-K fills the SMs: only s/128 x rc/128 tiles)
+    sk = K.pick_split(rc, s, rc)
+    K.gemm(Mat(ab[1], rc, 1), Mat(dor, rc, 1), Mat(dab[0], rc, 1), s, rc, rc, split_k=sk)
+    # db[s,(j,q)] = sum_(i,p) a[s,(i,p)] do'[(i,p),(j,q)]
+    K.gemm(Mat(ab[0], rc, 1), Mat(dor, 1, rc), Mat(dab[1], rc, 1), s, rc, rc, split_k=sk)
     mh = ctx["mh"]
     # dWab[:, w*c:(w+1)*c] = mh^T dab[w]   (batched over w)
     K.gemm(Mat(mh, 1, cm, bs1=0), Mat(dab, 1, c, bs1=rows * c), Mat(G["Wab"], 2 * c, 1, bs1=c),

@@ -111,15 +111,14 @@ def gemm(A: Mat, B: Mat, Cm: Mat, M: int, N_: int, K: int, *, alpha: float = 1.0
            (M, N_, K, B1 * B2, d.split_k, int(A.rs == 1), int(B.rs == 1), DT_NAME[d.dtype_c]))
 
 
-def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, target: int = 4096) -> int:
-    """Split-K factor for tall contractions (weight gradients): chunks of
-    <= `target` rows, and enough CTAs to cover the 148 SMs."""
-    if rows_k <= target:
-        return 1
+def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, min_rows: int = 512) -> int:
+    """Split-K factor for tall contractions (weight gradients, the OPM input
+    gradients): as many K chunks as fit one wave of the 148 SMs next to the
+    output tiles, each chunk >= `min_rows` (8 k-steps of the TMA pipeline)."""
     tiles = max(1, ((M + 127) // 128) * ((N_ + 127) // 128) * batch)
-    by_size = (rows_k + target - 1) // target
-    by_fill = max(1, (2 * 148 + tiles - 1) // tiles)
-    return int(max(1, min(by_size * 2, max(by_size, by_fill), 64)))
+    by_fill = 148 // tiles
+    by_size = rows_k // min_rows
+    return int(max(1, min(by_fill, by_size)))
 
 
 def linear(x, rows: int, d_in: int, W, ldw: int, d_out: int, out, ldo: int, *, w_off=0,

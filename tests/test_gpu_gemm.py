@@ -128,3 +128,73 @@ def test_gemm_tc_path_is_taken(K):
         K.PROFILE = None
     torch.cuda.synchronize()
     assert rel(C, A.float() @ B.float().T) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("M,N,Kd,a_k", [(5000, 8, 128, True), (4100, 12, 100, False),
+                                        (65536, 8, 128, True)])
+def test_gemm_skinny_rowdot(K, dtype, M, N, Kd, a_k):
+    """N <= 16 (the pair-bias projection): output in the [N, M] layout."""
+    A, Af, ars, acs, _ = make_operand(M, Kd, a_k, dtype=dtype)
+    B, Bf, brs, bcs, _ = make_operand(N, Kd, False, dtype=dtype)
+    C = torch.empty(N, M, device="cuda")
+    bias = torch.randn(N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, 1, M), M, N, Kd, bias=bias)
+    want = (Af[0] @ Bf[0].T + bias).T
+    assert rel(C, want) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("M,N,Kd", [(4096, 128, 8), (5003, 136, 12), (4096, 32, 4), (4100, 44, 5)])
+def test_gemm_skinny_expand_residual_accumulate(K, dtype, M, N, Kd):
+    """K <= 16 (the pair-bias input gradient), A column-major like dbias."""
+    A, Af, ars, acs, _ = make_operand(M, Kd, False, dtype=dtype)
+    B, Bf, brs, bcs, _ = make_operand(N, Kd, True, dtype=dtype)
+    R = torch.randn(M, N, device="cuda")
+    C = torch.empty(M, N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, residual=R)
+    want = Af[0] @ Bf[0].T + R
+    assert rel(C, want) < 1e-5
+    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd, accumulate=True,
+           alpha=0.5)
+    assert rel(C, want + 0.5 * (Af[0] @ Bf[0].T)) < 1e-5
+
+
+@pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
+@pytest.mark.parametrize("M,N,Kd,nb,a_k,b_k", [(128, 8, 20000, 1, False, True),
+                                               (32, 128, 16384, 1, False, False),
+                                               (48, 24, 9000, 2, False, True),
+                                               (200, 12, 8192, 1, True, False)])
+def test_gemm_skinny_tall_k(K, dtype, M, N, Kd, nb, a_k, b_k):
+    """Weight gradients of the narrow layers: tiny M*N, K = r*r rows."""
+    A, Af, ars, acs, abs_ = make_operand(M, Kd, a_k, nb, dtype=dtype)
+    B, Bf, brs, bcs, bbs = make_operand(N, Kd, b_k, nb, dtype=dtype)
+    C = torch.empty(nb, M, N, device="cuda")
+    K.gemm(K.Mat(A, ars, acs, bs1=abs_), K.Mat(B, brs, bcs, bs1=bbs), K.Mat(C, N, 1, bs1=M * N),
+           M, N, Kd, B1=nb)
+    want = torch.stack([Af[i].double() @ Bf[i].double().T for i in range(nb)])
+    # fp32 accumulation over K >= 8192 terms (tensor-core or SIMT partials)
+    assert rel(C, want) < 5e-5
+
+
+def test_gemm_tc_accumulate_two_level_map(K):
+    """TMA reduce-add epilogue through the 3-D / 4-D output maps."""
+    r, c, s = 32, 32, 64
+    rc = r * c
+    a = torch.randn(s, rc, device="cuda").to(torch.bfloat16)
+    b = torch.randn(s, rc, device="cuda").to(torch.bfloat16)
+    o = torch.randn(r, r, c, c, device="cuda")
+    o0 = o.clone()
+    K.gemm(K.Mat(a, 1, rc), K.Mat(b, 1, rc),
+           K.Mat(o, r * c * c, c * c, rdiv=c, rs0=c, cdiv=c, cs0=1), rc, rc, s, alpha=1.0 / s,
+           accumulate=True)
+    want = o0 + torch.einsum("sip,sjq->ijpq", a.float().view(s, r, c), b.float().view(s, r, c)) / s
+    assert rel(o, want) < 1e-6
+    # 3-D map (column blocks only): C(m, (j,q)) at j*(r*c) ... + m*c + q
+    C = torch.randn(r, rc, device="cuda")
+    C0 = C.clone()
+    K.gemm(K.Mat(a, 1, rc), K.Mat(b, 1, rc), K.Mat(C, c, r * c, cdiv=c, cs0=1), r, rc, s,
+           accumulate=True)
+    got = C.view(r, r, c).permute(1, 0, 2).reshape(r, rc)  # [m, (j,q)]
+    want2 = C0.view(r, r, c).permute(1, 0, 2).reshape(r, rc) + a.float()[:, :r].T @ b.float()
+    assert rel(got, want2) < 1e-6

@@ -47,17 +47,9 @@ def main():
     def run():
         K.gemm(Am, Bm, Cm, M, Nn, Kd, bias=bias, epi=epi, col0=Nn // 4 * 3, split_k=a.split)
 
-    for _ in range(3):
-        run()
-    torch.cuda.synchronize()
-    e0 = torch.cuda.Event(enable_timing=True)
-    e1 = torch.cuda.Event(enable_timing=True)
-    e0.record()
-    for _ in range(a.iters):
-        run()
-    e1.record()
-    torch.cuda.synchronize()
-    us = e0.elapsed_time(e1) / a.iters * 1e3
+    # graph-replayed (host launch overhead excluded)
+    from tools.ew_bench import timeit
+    us = timeit(run, a.iters)
     fl = 2.0 * M * Nn * Kd
     byt = (M * Kd + Nn * Kd) * 2 + M * Nn * C.element_size()
     print(f"M={M} N={Nn} K={Kd} a={a.a_major} b={a.b_major} epi={a.epi} out={a.out} "

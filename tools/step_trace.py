@@ -1,0 +1,115 @@
+"""Per-launch breakdown of one train step: run under ncu's launch list, then
+join the GEMM / attention launches with their shapes.
+
+    ncu --metrics gpu__time_duration.sum --clock-control none --cache-control none \
+        --profile-from-start off --csv --log-file gpurun_out/trace.csv \
+        python tools/step_trace.py --shapes gpurun_out/trace_shapes.json
+    python tools/step_trace.py --join gpurun_out/trace.csv gpurun_out/trace_shapes.json
+
+Only the one eager step between cudaProfilerStart/Stop is profiled.
+"""
+
+import argparse
+import csv
+import json
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+
+
+def run(args):
+    import torch
+
+    import paper_2211_00235_b200 as pkg
+    from bench import CONFIGS
+    from paper_2211_00235_b200 import kernels as K, schedules as S
+
+    dev = torch.device("cuda", 0)
+    cfg = pkg.EvoConfig(**CONFIGS[args.config])
+    store = pkg.init_params(cfg, 32, device=dev)
+    st = S.StepState(cfg, store, args.precision, dev)
+    st.pack()
+    m, z = S.make_batch(cfg, 32, 1, device=dev)[0]
+    for _ in range(3):
+        S.full_step(st, m, z)
+    torch.cuda.synchronize()
+    prof, shapes = [], []
+    K.PROFILE, K.PROFILE_SHAPES = prof, shapes
+    torch.cuda.profiler.start()
+    S.full_step(st, m, z)
+    torch.cuda.synchronize()
+    torch.cuda.profiler.stop()
+    K.PROFILE = K.PROFILE_SHAPES = None
+    out = [[fam, fl, list(shp) if shp else None] for (fam, fl, _, _), shp in zip(prof, shapes)]
+    with open(args.shapes, "w") as f:
+        json.dump(out, f)
+
+
+def family_of(name):
+    if "gemm_tc_kernel" in name or "gemm_simt_kernel" in name or "skinny_" in name:
+        return "gemm"
+    if "attn_fwd" in name:
+        return "attention_fwd"
+    if "attn_bwd_prep" in name:
+        return "attention_bwd"
+    return None
+
+
+def join(csv_path, shapes_path):
+    with open(shapes_path) as f:
+        calls = json.load(f)
+    rows = []
+    with open(csv_path) as f:
+        lines = [ln for ln in f if ln.startswith('"')]
+    for r in csv.DictReader(lines):
+        if r.get("Metric Name") != "gpu__time_duration.sum":
+            continue
+        v = float(r["Metric Value"].replace(",", ""))
+        unit = r.get("Metric Unit", "nsecond")
+        us = v / 1e3 if unit.startswith("n") else (v if unit.startswith("u") else v * 1e3)
+        rows.append((r["Kernel Name"], us))
+    # attach each family-starting launch to the next call of that family
+    queues = {}
+    for fam, fl, shp in calls:
+        queues.setdefault(fam, []).append((fl, shp))
+    cur = None
+    groups = []
+    for name, us in rows:
+        fam = family_of(name)
+        if fam is not None and queues.get(fam):
+            fl, shp = queues[fam].pop(0)
+            cur = [fam, shp, fl, 0.0, []]
+            groups.append(cur)
+        elif fam is not None or cur is None or not (
+                (cur[0] == "gemm" and ("splitk_reduce" in name or "skinny_reduce" in name)) or
+                (cur[0] == "attention_bwd" and ("attn_bwd" in name or "reduce_lead" in name))):
+            cur = [name.split("(")[0][:48], None, 0.0, 0.0, []]
+            groups.append(cur)
+        cur[3] += us
+        cur[4].append(name.split("(")[0].split("<")[0][-28:])
+    total = sum(g[3] for g in groups)
+    agg = {}
+    for fam, shp, fl, us, names in groups:
+        key = f"{fam} {shp}" if shp else fam
+        a = agg.setdefault(key, [0.0, 0.0, 0])
+        a[0] += us
+        a[1] += fl
+        a[2] += 1
+    print(f"total {total:.1f} us over {len(rows)} launches")
+    for key, (us, fl, n) in sorted(agg.items(), key=lambda kv: -kv[1][0]):
+        tf = fl / us / 1e6 if fl else 0.0
+        print(f"{us:9.1f} us {100 * us / total:5.1f}% {n:3d}x {tf:7.1f} TF/s  {key}")
+
+
+if __name__ == "__main__":
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", default="af2")
+    ap.add_argument("--precision", default="bf16")
+    ap.add_argument("--shapes", default="gpurun_out/trace_shapes.json")
+    ap.add_argument("--join", nargs=2, metavar=("CSV", "SHAPES"))
+    a = ap.parse_args()
+    if a.join:
+        join(*a.join)
+    else:
+        run(a)
