@@ -61,7 +61,10 @@ struct TcParams {
   float *partial;
   int store_mode;  // 0: thread stores, 1: TMA 2-D, 2: TMA {cdiv, N/cdiv, M}, 3: TMA 4-D
   int64_t cdiv, rdiv;
+  int bias_smem;   // bias[0..N) staged in smem by the epilogue warps
+  int box_w;       // TMA store box width in columns (64: bf16, 128-byte rows)
 };
+constexpr int BIAS_SMEM_MAX = 2048;
 
 __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_t &bidx,
                                             int &sp, int64_t &mt, int64_t &nt) {
@@ -81,10 +84,13 @@ __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_
 // Compile-time epilogue kinds (runtime residual/accumulate stay per chunk).
 enum { EK_NONE = 0, EK_BIAS = 1, EK_BIAS_RELU = 2, EK_BIAS_SIGMOID = 3 };
 
+// sigmoid(x) = 0.5 + 0.5 tanh(x/2): one MUFU op (tanh.approx, rel. error
+// ~2^-11, below the bf16 rounding of the stored gate) instead of ex2 + rcp;
+// the gate columns made the epilogue MUFU-bound.  Saturates to exactly 0/1.
 __device__ __forceinline__ float fast_sigmoid(float x) {
-  float e = __expf(-x), r;
-  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(1.f + e));
-  return r;  // exp(-x) = inf for x << 0 gives rcp(inf) = 0: the exact limit
+  float t;
+  asm("tanh.approx.f32 %0, %1;" : "=f"(t) : "f"(0.5f * x));
+  return fmaf(0.5f, t, 0.5f);
 }
 
 // Finish one 32-column chunk of one output row: alpha, bias, activation,
@@ -93,20 +99,20 @@ __device__ __forceinline__ float fast_sigmoid(float x) {
 // alpha, bias and activation of one 32-column chunk (thread-per-row)
 template <int EPI>
 __device__ __forceinline__ void epi_math(const TcParams &p, const EpiArgs &e, const uint32_t (&v)[32],
-                                         int64_t nb, float (&x)[32]) {
+                                         int64_t nb, float (&x)[32], const float *bias) {
   const bool full = nb + 32 <= p.N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = e.alpha * __uint_as_float(v[j]);
   if constexpr (EPI != EK_NONE) {
-    if (full && ((reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0)) {
+    if (full && ((reinterpret_cast<uintptr_t>(bias + nb) & 15) == 0)) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        float4 b4 = reinterpret_cast<const float4 *>(e.bias + nb)[j];
+        float4 b4 = reinterpret_cast<const float4 *>(bias + nb)[j];
         x[4 * j] += b4.x; x[4 * j + 1] += b4.y; x[4 * j + 2] += b4.z; x[4 * j + 3] += b4.w;
       }
     } else {
 #pragma unroll
-      for (int j = 0; j < 32; ++j) x[j] += (nb + j < p.N) ? e.bias[nb + j] : 0.f;
+      for (int j = 0; j < 32; ++j) x[j] += (nb + j < p.N) ? bias[nb + j] : 0.f;
     }
   }
   if constexpr (EPI == EK_BIAS_RELU) {
@@ -376,6 +382,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int acc = 0;
     uint32_t aphase = 0;
     const EpiArgs &e = p.epi;
+    const float *bias = e.bias;
+    if (p.bias_smem) {
+      float *sb = reinterpret_cast<float *>(smem_raw + ((reinterpret_cast<uint8_t *>(tmem_slot) -
+                                                         smem_raw) + 16));
+      for (int64_t i = threadIdx.x - 64; i < p.N; i += 32 * EPI_WARPS) sb[i] = e.bias[i];
+      named_bar_sync(1, 32 * EPI_WARPS);
+      bias = sb;
+    }
     for (int64_t t = blockIdx.x; t < p.num_tiles; t += gridDim.x) {
       int64_t bidx, mt, nt;
       int sp;
@@ -387,12 +401,109 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       const int64_t b1 = bidx / p.B2, b2 = bidx % p.B2;
       const bool row_ok = m < p.M;
       const int64_t rbase = row_ok ? (b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m)) : 0;
+      // this warp's chunks: c0 = half*32 + 64*i with n0 + c0 < N; the next
+      // chunk's TMEM load is in flight while the current one is finished,
+      // and the accumulator is released as soon as its last chunk is read
+      const int64_t ncols = min((int64_t)BN, p.N - n0);
+      if (p.box_w == 64) {
+        // 64-column units (two TMEM loads, one 32 x 64 bf16 box, SW128)
+        const int nun = ncols > half * 64 ? (int)((ncols - half * 64 + 127) / 128) : 0;
+        const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+        if (nun == 0) {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
 #pragma unroll 1
-      for (int c0 = half * 32; c0 < BN; c0 += 64) {
+        for (int ui = 0; ui < nun; ++ui) {
+          const int c0 = half * 64 + 128 * ui;
+          uint32_t va[32], vb[32];
+          tmem_ld32_nw(tb + c0, va);
+          tmem_ld32_nw(tb + c0 + 32, vb);
+          tmem_wait_ld();
+          if (ui + 1 == nun) {
+            fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&tempty[acc]);
+          }
+          const int64_t nb = n0 + c0;
+          if ((mt * BM + q * 32) >= p.M) continue;
+          uint8_t *box = wreg + (chunk_ctr & 1) * 4096;
+          ++chunk_ctr;
+          if (lane == 0) bulk_wait_read<1>();
+          __syncwarp();
+          {
+            float x[32];
+            epi_math<EPI>(p, e, va, nb, x, bias);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
+                w[u] = *reinterpret_cast<uint32_t *>(&h2);
+              }
+              *reinterpret_cast<uint4 *>(box + lane * 128 + ((c ^ (lane & 7)) << 4)) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          if (nb + 32 < p.N) {
+            float x[32];
+            epi_math<EPI>(p, e, vb, nb + 32, x, bias);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+              uint32_t w[4];
+#pragma unroll
+              for (int u = 0; u < 4; ++u) {
+                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
+                w[u] = *reinterpret_cast<uint32_t *>(&h2);
+              }
+              *reinterpret_cast<uint4 *>(box + lane * 128 + (((c + 4) ^ (lane & 7)) << 4)) =
+                  make_uint4(w[0], w[1], w[2], w[3]);
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            const int mrow = (int)(mt * BM + q * 32);
+            if (p.store_mode == 1)
+              tma_store_2d(&tmC, box, (int)nb, mrow);
+            else if (p.store_mode == 2)
+              tma_store_3d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv), mrow);
+            else
+              tma_store_4d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv),
+                           (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+            bulk_commit();
+          }
+        }
+        acc ^= 1;
+        if (acc == 0) aphase ^= 1;
+        continue;
+      }
+      const int nch = ncols > half * 32 ? (int)((ncols - half * 32 + 63) / 64) : 0;
+      const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 32;
+      uint32_t vn[32];
+      if (nch > 0) tmem_ld32_nw(tbase, vn);
+      if (nch == 0) {
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tempty[acc]);
+      }
+#pragma unroll 1
+      for (int ci = 0; ci < nch; ++ci) {
+        const int c0 = half * 32 + 64 * ci;
         uint32_t v[32];
-        tmem_ld32(tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + c0, v);
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 32; ++j) v[j] = vn[j];
+        if (ci + 1 < nch) {
+          tmem_ld32_nw(tbase + 64 * (ci + 1), vn);
+        } else {
+          fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tempty[acc]);
+        }
         const int64_t nb = n0 + c0;
-        if (nb >= p.N) continue;  // warp-uniform
         if (p.split > 1) {
           if (!row_ok) continue;
           float *dst = p.partial + (((int64_t)sp * p.nbatch + bidx) * p.M + m) * p.N + nb;
@@ -413,7 +524,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           // TMA bulk store (or reduce-add, for accumulate) of this warp's
           // 32 x 32 chunk; rows/cols beyond M/N are clipped by the map
           float x[32];
-          epi_math<EPI>(p, e, v, nb, x);
+          epi_math<EPI>(p, e, v, nb, x, bias);
           if (e.residual) {  // fp32, plain 2-D layout (same map as C)
             if (row_ok) {
               const float4 *rp = reinterpret_cast<const float4 *>(e.residual + rbase + nb);
@@ -478,9 +589,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         epi_chunk<EPI>(p, e, v, rbase, nb, row_ok, stage);
       }
-      fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&tempty[acc]);
       acc ^= 1;
       if (acc == 0) aphase ^= 1;
     }
@@ -574,7 +682,7 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
 // TMA store map for C when its index map is expressible (no batching; a
 // residual only for fp32 plain 2-D outputs, accumulate only for fp32, done
 // as a bulk reduce-add): returns the store mode (0 = not expressible).
-int make_store_map(CUtensorMap *map, const evo_gemm_desc *d) {
+int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   if (d->B1 * d->B2 != 1) return 0;
   if ((d->residual || d->accumulate) && d->dtype_c != EVO_F32) return 0;
   if (d->residual && (d->accumulate || d->C.cdiv || d->C.rdiv ||
@@ -587,17 +695,22 @@ int make_store_map(CUtensorMap *map, const evo_gemm_desc *d) {
   cuuint64_t dims[4], strides[3];
   cuuint32_t box[4], estr[4] = {1, 1, 1, 1};
   int rank, mode;
+  // bf16 rows of 64 columns (128 B) halve the number of store requests;
+  // needs 64-aligned column blocks
+  const bool wide = d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate &&
+                    (c.cdiv == 0 ? true : c.cdiv % 64 == 0);
+  const cuuint32_t bw = wide ? 64 : 32;
   if (c.cdiv == 0 && c.rdiv == 0) {
     if (c.cs != 1 || !ok16(c.rs)) return 0;
     dims[0] = d->N; dims[1] = d->M;
     strides[0] = c.rs * es;
-    box[0] = 32; box[1] = 32;
+    box[0] = bw; box[1] = 32;
     rank = 2; mode = 1;
   } else if (c.cdiv > 0 && c.rdiv == 0) {
     if (c.cs0 != 1 || c.cdiv % 32 || d->N % c.cdiv || !ok16(c.cs) || !ok16(c.rs)) return 0;
     dims[0] = c.cdiv; dims[1] = d->N / c.cdiv; dims[2] = d->M;
     strides[0] = c.cs * es; strides[1] = c.rs * es;
-    box[0] = 32; box[1] = 1; box[2] = 32;
+    box[0] = bw; box[1] = 1; box[2] = 32;
     rank = 3; mode = 2;
   } else if (c.cdiv > 0 && c.rdiv > 0) {
     if (c.cs0 != 1 || c.cdiv % 32 || d->N % c.cdiv || c.rdiv % 32 || d->M % c.rdiv ||
@@ -605,17 +718,19 @@ int make_store_map(CUtensorMap *map, const evo_gemm_desc *d) {
       return 0;
     dims[0] = c.cdiv; dims[1] = d->N / c.cdiv; dims[2] = c.rdiv; dims[3] = d->M / c.rdiv;
     strides[0] = c.cs * es; strides[1] = c.rs0 * es; strides[2] = c.rs * es;
-    box[0] = 32; box[1] = 1; box[2] = 32; box[3] = 1;
+    box[0] = bw; box[1] = 1; box[2] = 32; box[3] = 1;
     rank = 4; mode = 3;
   } else {
     return 0;
   }
+  *box_w = (int)bw;
   EncodeTiledFn fn = encode_fn();
   if (!fn) return 0;
   CUresult r = fn(map, d->dtype_c == EVO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   rank, c.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  d->dtype_c == EVO_BF16 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  (d->dtype_c == EVO_BF16 && bw == 32) ? CU_TENSOR_MAP_SWIZZLE_64B
+                                                       : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS ? mode : 0;
 }
@@ -645,7 +760,8 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   p.epi = epi_args_of(d);
   p.partial = reinterpret_cast<float *>(d->workspace);
   CUtensorMap mc;
-  p.store_mode = p.split > 1 ? 0 : make_store_map(&mc, d);
+  p.box_w = 32;
+  p.store_mode = p.split > 1 ? 0 : make_store_map(&mc, d, &p.box_w);
   p.cdiv = d->C.cdiv > 0 ? d->C.cdiv : 1;
   p.rdiv = d->C.rdiv > 0 ? d->C.rdiv : 1;
   if (!p.store_mode) mc = ma;  // unused
@@ -654,8 +770,9 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
     EVO_REQUIRE(d->workspace && d->workspace_bytes >= need, EVO_EARG,
                 "evo_gemm(tc): split=%d needs %zu workspace bytes", p.split, need);
   }
+  p.bias_smem = (d->bias && d->N <= BIAS_SMEM_MAX && p.split == 1) ? 1 : 0;
   const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) +
-                      (size_t)EPI_WARPS * 8192 + 256;
+                      (size_t)EPI_WARPS * 8192 + 256 + (size_t)BIAS_SMEM_MAX * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
