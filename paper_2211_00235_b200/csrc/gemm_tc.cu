@@ -66,18 +66,23 @@ struct TcParams {
 };
 constexpr int BIAS_SMEM_MAX = 2048;
 
-__device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t, int64_t &bidx,
+// 32-bit index math (num_tiles < 2^31, checked on the host): the 64-bit
+// divisions cost the epilogue warps ~300 instructions per tile
+__device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t64, int64_t &bidx,
                                             int &sp, int64_t &mt, int64_t &nt) {
-  nt = t % p.tiles_n;
-  int64_t r = t / p.tiles_n;
-  mt = r % p.tiles_m;
+  const uint32_t t = (uint32_t)t64, tn = (uint32_t)p.tiles_n, tm = (uint32_t)p.tiles_m;
+  uint32_t ntl = t % tn;
+  uint32_t r = t / tn;
+  const uint32_t mtl = r % tm;
   // rotate n per m-row: consecutive tiles still share the A rows, but a CTA
   // striding by the grid size no longer always lands on the same n-tile
   // (148 % tiles_n == 0 would pin e.g. all sigmoid columns to 1/4 of the SMs)
-  nt = (nt + mt) % p.tiles_n;
-  r /= p.tiles_m;
-  sp = (int)(r % p.split);
-  bidx = r / p.split;
+  ntl = (ntl + mtl) % tn;
+  r /= tm;
+  sp = (int)(r % (uint32_t)p.split);
+  bidx = (int64_t)(r / (uint32_t)p.split);
+  mt = mtl;
+  nt = ntl;
 }
 
 
@@ -260,7 +265,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     prefetch_map(&tmA);
     prefetch_map(&tmB);
-    if (p.store_mode) prefetch_map(&tmC);
+    if (p.store_mode >= 1 && p.store_mode <= 3) prefetch_map(&tmC);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
@@ -405,8 +410,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       // chunk's TMEM load is in flight while the current one is finished,
       // and the accumulator is released as soon as its last chunk is read
       const int64_t ncols = min((int64_t)BN, p.N - n0);
-      if (p.box_w == 64) {
-        // 64-column units (two TMEM loads, one 32 x 64 bf16 box, SW128)
+      if (p.epi.dtype_c == EVO_BF16 && p.store_mode != 0 && p.split == 1) {
+        // 64-column units (two TMEM loads, both halves finished together for
+        // ILP): one 32 x 64 SW128 box (box_w 64) or two 32 x 32 boxes (SW64
+        // for the tensor maps, plain rows for the mode-4 block store)
         const int nun = ncols > half * 64 ? (int)((ncols - half * 64 + 127) / 128) : 0;
         const uint32_t tb = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
         if (nun == 0) {
@@ -432,9 +439,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           ++chunk_ctr;
           if (lane == 0) bulk_wait_read<1>();
           __syncwarp();
-          {
+          const bool second = nb + 32 < p.N;  // warp-uniform
+          // byte offset of 16-byte chunk c (0..7) of this lane's row
+          auto off = [&](int c) -> int {
+            if (p.box_w == 64) return lane * 128 + ((c ^ (lane & 7)) << 4);
+            const int hh = c >> 2, cc = c & 3;
+            const int sw = p.store_mode == 4 ? 0 : ((lane >> 1) & 3);
+            return hh * 2048 + lane * 64 + ((cc ^ sw) << 4);
+          };
+          // finish and stage one 32-column half at a time (register budget:
+          // 10 warps cap the kernel at 168 registers per thread)
+          auto half_out = [&](const uint32_t(&v)[32], int64_t nbh, int cbase) {
             float x[32];
-            epi_math<EPI>(p, e, va, nb, x, bias);
+            epi_math<EPI>(p, e, v, nbh, x, bias);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               uint32_t w[4];
@@ -443,36 +460,31 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
                 w[u] = *reinterpret_cast<uint32_t *>(&h2);
               }
-              *reinterpret_cast<uint4 *>(box + lane * 128 + ((c ^ (lane & 7)) << 4)) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
+              *reinterpret_cast<uint4 *>(box + off(cbase + c)) = make_uint4(w[0], w[1], w[2], w[3]);
             }
-          }
-          if (nb + 32 < p.N) {
-            float x[32];
-            epi_math<EPI>(p, e, vb, nb + 32, x, bias);
-#pragma unroll
-            for (int c = 0; c < 4; ++c) {
-              uint32_t w[4];
-#pragma unroll
-              for (int u = 0; u < 4; ++u) {
-                __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
-                w[u] = *reinterpret_cast<uint32_t *>(&h2);
-              }
-              *reinterpret_cast<uint4 *>(box + lane * 128 + (((c + 4) ^ (lane & 7)) << 4)) =
-                  make_uint4(w[0], w[1], w[2], w[3]);
-            }
-          }
+          };
+          half_out(va, nb, 0);
+          if (second) half_out(vb, nb + 32, 4);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
             const int mrow = (int)(mt * BM + q * 32);
-            if (p.store_mode == 1)
-              tma_store_2d(&tmC, box, (int)nb, mrow);
-            else if (p.store_mode == 2)
-              tma_store_3d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv), mrow);
-            else
-              tma_store_4d(&tmC, box, (int)(nb % p.cdiv), (int)(nb / p.cdiv),
-                           (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+            const int nsub = p.box_w == 64 ? 1 : (second ? 2 : 1);
+            for (int sb = 0; sb < nsub; ++sb) {
+              const int64_t nbs = nb + 32 * sb;
+              const uint8_t *bx = box + sb * 2048;
+              if (p.store_mode == 4) {
+                bf16 *dst = reinterpret_cast<bf16 *>(e.C) + e.cmap.row(mrow) + e.cmap.col(nbs);
+                bulk_store(dst, bx, 2048);
+              } else if (p.store_mode == 1) {
+                tma_store_2d(&tmC, bx, (int)nbs, mrow);
+              } else if (p.store_mode == 2) {
+                tma_store_3d(&tmC, bx, (int)(nbs % p.cdiv), (int)(nbs / p.cdiv), mrow);
+              } else {
+                tma_store_4d(&tmC, bx, (int)(nbs % p.cdiv), (int)(nbs / p.cdiv),
+                             (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
+              }
+            }
             bulk_commit();
           }
         }
@@ -546,6 +558,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (lane == 0) bulk_wait_read<1>();  // box's previous store has read it
           __syncwarp();
           if (e.dtype_c == EVO_BF16) {
+            // SW64 box for the tensor map; plain 64-byte rows for mode 4
+            const int sw = p.store_mode == 4 ? 0 : ((lane >> 1) & 3);
 #pragma unroll
             for (int c = 0; c < 4; ++c) {
               uint32_t w[4];
@@ -554,7 +568,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 __nv_bfloat162 h2 = __floats2bfloat162_rn(x[8 * c + 2 * u], x[8 * c + 2 * u + 1]);
                 w[u] = *reinterpret_cast<uint32_t *>(&h2);
               }
-              *reinterpret_cast<uint4 *>(box + lane * 64 + ((c ^ ((lane >> 1) & 3)) << 4)) =
+              *reinterpret_cast<uint4 *>(box + lane * 64 + ((c ^ sw) << 4)) =
                   make_uint4(w[0], w[1], w[2], w[3]);
             }
           } else {
@@ -565,7 +579,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           }
           fence_proxy_async_smem();
           __syncwarp();
-          if (lane == 0) {
+          if (lane == 0 && p.store_mode == 4) {
+            const int64_t mrow = mt * BM + q * 32;
+            bf16 *dst = reinterpret_cast<bf16 *>(e.C) + e.cmap.row(mrow) + e.cmap.col(nb);
+            bulk_store(dst, box, 2048);
+            bulk_commit();
+          } else if (lane == 0) {
             const int mrow = (int)(mt * BM + q * 32);
             if (e.accumulate) {
               if (p.store_mode == 1)
@@ -684,6 +703,18 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
 // as a bulk reduce-add): returns the store mode (0 = not expressible).
 int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   if (d->B1 * d->B2 != 1) return 0;
+  {
+    // mode 4: every warp chunk (32 rows x 32 columns) is one contiguous
+    // 2 KiB bf16 block (the outer-product-mean layouts o[i,j,p,q] and
+    // do'[i,p,j,q]): rows 32 elements apart inside a 32-aligned row group,
+    // columns unit-stride inside a 32-aligned column group
+    const evo_mat &c = d->C;
+    if (d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate && c.rdiv > 0 &&
+        c.rdiv % 32 == 0 && c.rs0 == 32 && c.cdiv > 0 && c.cdiv % 32 == 0 && c.cs0 == 1 &&
+        d->M % 32 == 0 && d->N % 32 == 0 &&
+        (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0 && (c.rs % 8) == 0 && (c.cs % 8) == 0)
+      return 4;
+  }
   if ((d->residual || d->accumulate) && d->dtype_c != EVO_F32) return 0;
   if (d->residual && (d->accumulate || d->C.cdiv || d->C.rdiv ||
                       (reinterpret_cast<uintptr_t>(d->residual) & 15) != 0))
@@ -752,6 +783,7 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   p.tiles_n = (d->N + BN - 1) / BN;
   p.split = choose_split(d, BN, p.k_chunk);
   p.num_tiles = p.tiles_m * p.tiles_n * p.split * d->B1 * d->B2;
+  if (p.num_tiles >= (1ll << 31)) return EVO_EUNSUP;
   p.a_kmajor = pa.kmajor; p.b_kmajor = pb.kmajor;
   p.a_bat1 = pa.bat1; p.a_bat2 = pa.bat2; p.b_bat1 = pb.bat1; p.b_bat2 = pb.bat2;
   p.idesc = (1u << 4) | (1u << 7) | (1u << 10) | ((pa.kmajor ? 0u : 1u) << 15) |
@@ -764,7 +796,7 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   p.store_mode = p.split > 1 ? 0 : make_store_map(&mc, d, &p.box_w);
   p.cdiv = d->C.cdiv > 0 ? d->C.cdiv : 1;
   p.rdiv = d->C.rdiv > 0 ? d->C.rdiv : 1;
-  if (!p.store_mode) mc = ma;  // unused
+  if (p.store_mode == 0 || p.store_mode == 4) mc = ma;  // unused
   if (p.split > 1) {
     size_t need = (size_t)p.split * d->B1 * d->B2 * d->M * d->N * sizeof(float);
     EVO_REQUIRE(d->workspace && d->workspace_bytes >= need, EVO_EARG,
