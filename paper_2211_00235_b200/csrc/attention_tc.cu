@@ -144,6 +144,12 @@ __device__ __forceinline__ float bias_at(const AttnTcArgs &a, int h, int q, int 
 //   plain  (bk == 1): Lp/32 TMA boxes [128 q x 32 k], 128B-swizzled rows
 //   trans. (bq == 1): Lp/32 TMA boxes [32 k x 128 q] (q contiguous)
 constexpr uint32_t BIAS_BYTES = 128 * 256 * 4;
+// A/B switch for the pipelined backward kernels (EVO_ATTN_NO_PIPE=1 in the
+// environment selects the previous one-row-at-a-time kernels)
+static const bool g_attn_no_pipe = [] {
+  const char *e = getenv("EVO_ATTN_NO_PIPE");
+  return e && e[0] == '1';
+}();
 
 template <bool TBIAS>
 __device__ __forceinline__ float bias_smem(const uint8_t *sb, int row, int k) {
@@ -441,9 +447,10 @@ __device__ __forceinline__ void bias_row16(const uint8_t *sb, int row, int k0, f
   }
 }
 // Fold log2(e) into a resident bias tile once per CTA.
-__device__ __forceinline__ void scale_tile(uint8_t *sb, int nfloat4) {
+__device__ __forceinline__ void scale_tile(uint8_t *sb, int nfloat4, int nthreads = 0) {
   float4 *p = reinterpret_cast<float4 *>(sb);
-  for (int i = threadIdx.x; i < nfloat4; i += blockDim.x) {
+  const int stride = nthreads ? nthreads : (int)blockDim.x;
+  for (int i = threadIdx.x; i < nfloat4; i += stride) {
     float4 v = p[i];
     v.x *= LOG2E; v.y *= LOG2E; v.z *= LOG2E; v.w *= LOG2E;
     p[i] = v;
@@ -895,6 +902,265 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
   if (warp == 0) tmem_dealloc(tmem, 512);
 }
 
+// ============================================================ dkv, pipelined
+// Lp == 256.  Units of 64 queries (four per batch row) flow through three
+// TMEM regions [S^T 64 | dP^T 64] at 128*(u%3); the S^T / dP^T MMAs of unit
+// u+2 are issued while the threads run the elementwise pass of unit u, so
+// the tensor core and the CUDA cores overlap instead of taking turns.  P^T
+// and dS^T are packed in place into each thread's own columns (a 16-query
+// K slice = one thread quarter = 8 packed columns), dV / dK accumulate in
+// TMEM across the row's four units (row-parity accumulators [dV 32 | dK 32]
+// at 384 + 64*(r&1)) and are read back one unit into the next row, and the
+// TMA loads of row r+1 go out as soon as row r-1's accumulators are read.
+// Warps 0-15 run the elementwise passes (4 lane quadrants x 4 query
+// quarters); warp 16 only issues: MMAs, TMA loads, commits, so no
+// elementwise warp ever waits on issue latency.
+// smem: bias 128 KiB + two rows of K|V|Q|dO (96 KiB) + lse/Dq: no 1 KiB
+// alignment slack, the dynamic smem base is 1 KiB aligned (checked).
+template <int D, int BIASMODE>
+__global__ void __launch_bounds__(544, 1)
+attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
+                         const __grid_constant__ CUtensorMap mVt,
+                         const __grid_constant__ CUtensorMap mQa,
+                         const __grid_constant__ CUtensorMap mdOa,
+                         const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // K | V | Q | dO of one batch row
+  constexpr bool KCONTIG = BIASMODE == 1;
+  constexpr int NU = 4, UW = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+  uint8_t *sBias = smem_raw;
+  uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
+  float *sLse = reinterpret_cast<float *>(sRow + 2 * ROWB);
+  float *sDq = sLse + 256;
+  // 0 bias, 1-2 row data (row parity), 3-5 S^T/dP^T MMAs (region),
+  // 6-7 the row's last dV/dK MMAs (row parity), 8 unit's elementwise pass
+  // done (one arrival per warp), 9-11 a unit's dV/dK MMAs done (region):
+  // the region is rewritten by the S^T MMA two units later only after its
+  // packed P^T / dS^T were consumed
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 12);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = (warp & 3) * 32 + lane;  // key row in the tile
+  const int qr = warp >> 2;              // 16-query quarter of each unit
+  const int k0 = blockIdx.x * QT, h = blockIdx.y;
+  const int L = a.L;
+  const int k = k0 + t;
+  const bool kv = k < L;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  const int64_t nrows = b_hi - b_lo;
+  const int64_t U = nrows > 0 ? nrows * NU : 0;
+
+  constexpr int ISSUER = 512;
+  const bool ew = tid < 512;  // elementwise warps
+  if (tid == ISSUER) {
+    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], i == 8 ? 16 : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars[0], h, k0, 256);
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
+  auto load_row = [&](int64_t r) {
+    uint8_t *rb = rowbuf(r);
+    uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+    mbar_expect_tx(bar, ROWB);
+    tma_load_4d(rb, &mKt, bar, 0, k0, (int)r, h);
+    tma_load_4d(rb + TILE, &mVt, bar, 0, k0, (int)r, h);
+    tma_load_4d(rb + 2 * TILE, &mQa, bar, 0, 0, (int)r, h);
+    tma_load_4d(rb + 2 * TILE + FULL, &mdOa, bar, 0, 0, (int)r, h);
+  };
+  const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
+  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+  auto issue_mma1 = [&](int64_t u) {  // thread 0
+    const int64_t r = b_lo + u / NU;
+    const int ui = (int)(u % NU), reg = (int)(u % 3);
+    if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
+    fence_after();
+    const uint32_t sK = smem_u32(rowbuf(r)), sV = sK + TILE;
+    const uint32_t sQ = sK + 2 * TILE + ui * UW * Sw<D>::bytes;
+    const uint32_t sdO = sQ + FULL;
+    const uint32_t d = tmem + reg * 128;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16(d, desc_kmajor_tile<D>(sK, ks), desc_kmajor_tile<D>(sQ, ks), idesc_s, ks > 0);
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16(d + 64, desc_kmajor_tile<D>(sV, ks), desc_kmajor_tile<D>(sdO, ks), idesc_s,
+                ks > 0);
+    umma_commit(&bars[3 + reg]);
+  };
+  auto readout = [&](int64_t rr) {  // dV, dK rows of batch row rr -> global
+    const int pp = (int)((rr - b_lo) & 1);
+    mbar_wait(&bars[6 + pp], (uint32_t)(((rr - b_lo) >> 1) & 1));
+    fence_after();
+    constexpr int QD = D / 4;
+    const uint32_t acc = lane_addr + 384 + pp * 64;
+    uint32_t v1[8], v2[8];
+    if constexpr (QD == 8) {
+      tmem_ld8_nw(acc + qr * 8, v1);
+      tmem_ld8_nw(acc + 32 + qr * 8, v2);
+    } else {
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v1[0]), "=r"(v1[1]), "=r"(v1[2]), "=r"(v1[3])
+                   : "r"(acc + qr * 4));
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                   : "=r"(v2[0]), "=r"(v2[1]), "=r"(v2[2]), "=r"(v2[3])
+                   : "r"(acc + 32 + qr * 4));
+    }
+    tmem_wait_ld();
+    if (kv) {
+      const int64_t off = rr * a.sb + (int64_t)k * a.sl + h * D + qr * QD;
+      if constexpr (QD == 8) {
+        uint32_t w1[4], w2[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          w1[j] = pack2(__uint_as_float(v1[2 * j]), __uint_as_float(v1[2 * j + 1]));
+          w2[j] = pack2(__uint_as_float(v2[2 * j]) * a.scale,
+                        __uint_as_float(v2[2 * j + 1]) * a.scale);
+        }
+        *reinterpret_cast<uint4 *>(a.dv + off) = make_uint4(w1[0], w1[1], w1[2], w1[3]);
+        *reinterpret_cast<uint4 *>(a.dk + off) = make_uint4(w2[0], w2[1], w2[2], w2[3]);
+      } else {
+        uint32_t w1[2], w2[2];
+#pragma unroll
+        for (int j = 0; j < 2; ++j) {
+          w1[j] = pack2(__uint_as_float(v1[2 * j]), __uint_as_float(v1[2 * j + 1]));
+          w2[j] = pack2(__uint_as_float(v2[2 * j]) * a.scale,
+                        __uint_as_float(v2[2 * j + 1]) * a.scale);
+        }
+        *reinterpret_cast<uint2 *>(a.dv + off) = make_uint2(w1[0], w1[1]);
+        *reinterpret_cast<uint2 *>(a.dk + off) = make_uint2(w2[0], w2[1]);
+      }
+    }
+  };
+
+  if (!ew) {
+    // ------------------------------------------------------------ issuer
+    if (lane == 0 && nrows > 0) {
+      load_row(b_lo);
+      if (nrows > 1) load_row(b_lo + 1);
+      issue_mma1(0);
+      if (U > 1) issue_mma1(1);
+      for (int64_t u = 0; u < U; ++u) {
+        const int64_t r = b_lo + u / NU;
+        const int ui = (int)(u % NU), reg = (int)(u % 3);
+        const int rp = (int)((r - b_lo) & 1);
+        mbar_wait(&bars[8], (uint32_t)(u & 1));  // all 16 warps packed unit u
+        fence_after();
+        // at a row's first unit the warps have read row r-1's accumulators,
+        // so row r-1's smem buffers are free for row r+1
+        if (ui == 0 && r > b_lo && r + 1 < b_hi) load_row(r + 1);
+        const uint32_t acc = tmem + 384 + rp * 64;
+        const uint32_t sQ = smem_u32(rowbuf(r)) + 2 * TILE, sdO = sQ + FULL;
+        const uint32_t reg_col = tmem + reg * 128;
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          umma_bf16_ts(acc, reg_col + ks * 16, desc_mnmajor_tile<D>(sdO, ui * 4 + ks), idesc_o,
+                       (ui > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < 4; ++ks)
+          umma_bf16_ts(acc + 32, reg_col + 64 + ks * 16, desc_mnmajor_tile<D>(sQ, ui * 4 + ks),
+                       idesc_o, (ui > 0 || ks > 0) ? 1u : 0u);
+        if (ui == NU - 1) umma_commit(&bars[6 + rp]);
+        umma_commit(&bars[9 + reg]);
+        if (u + 2 < U) {
+          if (u >= 1) mbar_wait(&bars[9 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
+          issue_mma1(u + 2);
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+  // ------------------------------------------------------------ elementwise
+  float lse_n = 0.f, Dq_n = 0.f;
+  if (tid < L && nrows > 0) {
+    lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + tid] * LOG2E;
+    Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + tid];
+  }
+  if (BIASMODE) {
+    mbar_wait(&bars[0], 0);
+    scale_tile(sBias, 8 * 16384 / 16, 512);
+  }
+  const float sc_l2 = a.scale * LOG2E;
+
+  for (int64_t u = 0; u < U; ++u) {
+    const int64_t r = b_lo + u / NU;
+    const int ui = (int)(u % NU), reg = (int)(u % 3);
+    const int rp = (int)((r - b_lo) & 1);
+    if (ui == 0) {  // this row's lse / Dq into smem; prefetch the next row's
+      if (r > b_lo) named_bar_sync(1, 512);  // every warp is done with row r-1's lse / Dq
+      if (tid < 256) {
+        sLse[tid] = lse_n;
+        sDq[tid] = Dq_n;
+      }
+      if (tid < L && r + 1 < b_hi) {
+        lse_n = a.lse[((r + 1) * a.H + h) * (int64_t)L + tid] * LOG2E;
+        Dq_n = a.Dq[((r + 1) * a.H + h) * (int64_t)L + tid];
+      } else {
+        lse_n = 0.f;
+        Dq_n = 0.f;
+      }
+      named_bar_sync(1, 512);
+    }
+    mbar_wait(&bars[3 + reg], (uint32_t)((u / 3) & 1));
+    fence_after();
+    const uint32_t rb = lane_addr + reg * 128;
+    const int c0 = qr * 16;
+    const int qb = ui * UW + c0;  // first query of this thread's 16
+    uint32_t sv[16], dv[16];
+    tmem_ld16_nw(rb + c0, sv);
+    tmem_ld16_nw(rb + 64 + c0, dv);
+    tmem_wait_ld();
+    float bb[16], ls[16], dq[16];
+    if (BIASMODE) bias_row16<!KCONTIG>(sBias, t, qb, bb);
+#pragma unroll
+    for (int j = 0; j < 16; j += 4) {  // warp-uniform 16-byte broadcasts
+      const float4 l4 = *reinterpret_cast<const float4 *>(sLse + qb + j);
+      const float4 d4 = *reinterpret_cast<const float4 *>(sDq + qb + j);
+      ls[j] = l4.x; ls[j + 1] = l4.y; ls[j + 2] = l4.z; ls[j + 3] = l4.w;
+      dq[j] = d4.x; dq[j + 1] = d4.y; dq[j + 2] = d4.z; dq[j + 3] = d4.w;
+    }
+    const bool full = kv && qb + 16 <= L;
+    uint32_t pk[8], dk8[8];
+#pragma unroll
+    for (int j = 0; j < 16; j += 2) {
+      float pp2[2], ds[2];
+#pragma unroll
+      for (int w2 = 0; w2 < 2; ++w2) {
+        float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -ls[j + w2]);
+        if (BIASMODE) x += bb[j + w2];
+        const float e = ex2(x);
+        pp2[w2] = full ? e : ((kv && qb + j + w2 < L) ? e : 0.f);
+        ds[w2] = pp2[w2] * (__uint_as_float(dv[j + w2]) - dq[j + w2]);
+      }
+      pk[j >> 1] = pack2(pp2[0], pp2[1]);
+      dk8[j >> 1] = pack2(ds[0], ds[1]);
+    }
+    tmem_st8(rb + c0, pk);
+    tmem_st8(rb + 64 + c0, dk8);
+    if (ui == 0 && r > b_lo) readout(r - 1);
+    tmem_st_wait();
+    fence_before();
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bars[8]);
+  }
+  if (nrows > 0) readout(b_hi - 1);
+  }  // elementwise warps
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 // ===================================================================== host
 // 4-D map over a (b, l, h, d) strided bf16 buffer: dims {D, L, nb, H}.
 bool head_map(CUtensorMap *m, const void *base, int D, int L, int64_t nb, int H, int64_t sl,
@@ -1079,7 +1345,14 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     attn_bwd_dq_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
-  {
+  if (Lp == 256 && !g_attn_no_pipe) {
+    const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
+                        2 * 256 * 4 + 12 * 8 + 16;
+    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_>));
+    dim3 grid(tiles, d->H, (unsigned)nch);
+    attn_bwd_dkv_pipe_kernel<D, BM_><<<grid, 544, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    EVO_LAUNCHED("attn_bwd_dkv_pipe_kernel");
+  } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 4 * 256 * 2 * D +
                         2 * (size_t)QT * 2 * D + 2 * 256 * 4 + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D, BM_>));

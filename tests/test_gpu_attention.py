@@ -110,6 +110,10 @@ CASES = [
     (4, 64, 4, 16, False, "plain"),      # mid config head dim
     (4, 160, 2, 64, True, "transposed"),
     (9, 48, 3, 16, True, "none"),
+    (3, 200, 2, 32, False, "plain"),     # ragged L in the pipelined (Lp = 256) path
+    (5, 230, 3, 16, True, "transposed"),
+    (150, 256, 4, 32, False, "plain"),   # 9-row chunks per CTA: row pipeline wrap-around
+    (64, 256, 2, 32, True, "none"),
 ]
 
 
