@@ -21,6 +21,9 @@
 //   dkv kernel (grid k-tiles x H x nb): S^T = K Q^T, dP^T = V dO^T,
 //     P^T, dS^T -> smem; dv = P^T dO; dk = scale * dS^T Q
 //   dbias = ordered sum of the chunk partials.
+#include <cstdio>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
@@ -53,7 +56,13 @@ struct AttnTcArgs {
   bf16 *dq, *dk, *dv;  // proj-gradient buffer (q's strides)
   float *dbias_part;
   int64_t chunk;
+  long long *trace;  // EVO_ATTN_TRACE=1: per-unit clock64 stamps of CTA 0
 };
+__device__ __forceinline__ long long clk() {
+  long long c;
+  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
+  return c;
+}
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -936,12 +945,14 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   float *sLse = reinterpret_cast<float *>(sRow + 2 * ROWB);
   float *sDq = sLse + 256;
   // 0 bias, 1-2 row data (row parity), 3-5 S^T/dP^T MMAs (region),
-  // 6-7 the row's last dV/dK MMAs (row parity), 8 unit's elementwise pass
-  // done (one arrival per warp), 9-11 a unit's dV/dK MMAs done (region):
+  // 6-7 the row's last dV/dK MMAs (row parity), 8-9 unit's elementwise pass
+  // done (one arrival per warp; unit parity: a warp can be one unit ahead of
+  // the slowest, never two, since unit u+2's S MMAs wait for unit u's
+  // arrivals), 10-12 a unit's dV/dK MMAs done (region):
   // the region is rewritten by the S^T MMA two units later only after its
   // packed P^T / dS^T were consumed
   uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 12);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 13);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // key row in the tile
@@ -958,7 +969,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   constexpr int ISSUER = 512;
   const bool ew = tid < 512;  // elementwise warps
   if (tid == ISSUER) {
-    for (int i = 0; i < 12; ++i) mbar_init(&bars[i], i == 8 ? 16 : 1);
+    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], (i == 8 || i == 9) ? 16 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars[0], h, k0, 256);
   }
@@ -981,7 +992,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   };
   const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-  auto issue_mma1 = [&](int64_t u) {  // thread 0
+  auto issue_mma1 = [&](int64_t u) {  // warp-collective (issuer warp)
     const int64_t r = b_lo + u / NU;
     const int ui = (int)(u % NU), reg = (int)(u % 3);
     if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
@@ -992,12 +1003,12 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     const uint32_t d = tmem + reg * 128;
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16(d, desc_kmajor_tile<D>(sK, ks), desc_kmajor_tile<D>(sQ, ks), idesc_s, ks > 0);
+      umma_bf16_el(d, desc_kmajor_tile<D>(sK, ks), desc_kmajor_tile<D>(sQ, ks), idesc_s, ks > 0);
 #pragma unroll
     for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16(d + 64, desc_kmajor_tile<D>(sV, ks), desc_kmajor_tile<D>(sdO, ks), idesc_s,
-                ks > 0);
-    umma_commit(&bars[3 + reg]);
+      umma_bf16_el(d + 64, desc_kmajor_tile<D>(sV, ks), desc_kmajor_tile<D>(sdO, ks), idesc_s,
+                   ks > 0);
+    umma_commit_el(&bars[3 + reg]);
   };
   auto readout = [&](int64_t rr) {  // dV, dK rows of batch row rr -> global
     const int pp = (int)((rr - b_lo) & 1);
@@ -1046,35 +1057,41 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
 
   if (!ew) {
     // ------------------------------------------------------------ issuer
-    if (lane == 0 && nrows > 0) {
-      load_row(b_lo);
-      if (nrows > 1) load_row(b_lo + 1);
+    if (nrows > 0) {  // the whole warp runs the loop; one elected lane issues
+      if (lane == 0) {
+        load_row(b_lo);
+        if (nrows > 1) load_row(b_lo + 1);
+      }
+      __syncwarp();
       issue_mma1(0);
       if (U > 1) issue_mma1(1);
       for (int64_t u = 0; u < U; ++u) {
         const int64_t r = b_lo + u / NU;
         const int ui = (int)(u % NU), reg = (int)(u % 3);
         const int rp = (int)((r - b_lo) & 1);
-        mbar_wait(&bars[8], (uint32_t)(u & 1));  // all 16 warps packed unit u
+        mbar_wait(&bars[8 + (int)(u & 1)], (uint32_t)((u >> 1) & 1));  // all 16 warps packed unit u
         fence_after();
         // at a row's first unit the warps have read row r-1's accumulators,
         // so row r-1's smem buffers are free for row r+1
-        if (ui == 0 && r > b_lo && r + 1 < b_hi) load_row(r + 1);
+        if (ui == 0 && r > b_lo && r + 1 < b_hi) {
+          if (lane == 0) load_row(r + 1);
+          __syncwarp();
+        }
         const uint32_t acc = tmem + 384 + rp * 64;
         const uint32_t sQ = smem_u32(rowbuf(r)) + 2 * TILE, sdO = sQ + FULL;
         const uint32_t reg_col = tmem + reg * 128;
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          umma_bf16_ts(acc, reg_col + ks * 16, desc_mnmajor_tile<D>(sdO, ui * 4 + ks), idesc_o,
-                       (ui > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_ts_el(acc, reg_col + ks * 16, desc_mnmajor_tile<D>(sdO, ui * 4 + ks), idesc_o,
+                          (ui > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
         for (int ks = 0; ks < 4; ++ks)
-          umma_bf16_ts(acc + 32, reg_col + 64 + ks * 16, desc_mnmajor_tile<D>(sQ, ui * 4 + ks),
-                       idesc_o, (ui > 0 || ks > 0) ? 1u : 0u);
-        if (ui == NU - 1) umma_commit(&bars[6 + rp]);
-        umma_commit(&bars[9 + reg]);
+          umma_bf16_ts_el(acc + 32, reg_col + 64 + ks * 16, desc_mnmajor_tile<D>(sQ, ui * 4 + ks),
+                          idesc_o, (ui > 0 || ks > 0) ? 1u : 0u);
+        if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
+        umma_commit_el(&bars[10 + reg]);
         if (u + 2 < U) {
-          if (u >= 1) mbar_wait(&bars[9 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
+          if (u >= 1) mbar_wait(&bars[10 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
           issue_mma1(u + 2);
         }
       }
@@ -1152,10 +1169,286 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     tmem_st_wait();
     fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&bars[8]);
+    if (lane == 0) mbar_arrive(&bars[8 + (int)(u & 1)]);
   }
   if (nrows > 0) readout(b_hi - 1);
   }  // elementwise warps
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
+// ============================================================= dq, pipelined
+// Lp == 256, same scheme as the pipelined dk/dv kernel: units of 64 keys
+// (four per batch row) through three TMEM regions [S 64 | dP 64]; S/dP MMAs
+// two units ahead; dS packed in place (a 16-key K slice = one thread
+// quarter); dQ accumulated in TMEM per row (row-parity accumulators at
+// 384 + 64*(r&1)); lse / Dq of the thread's query row live in registers, the
+// dbias partial for its 64 keys too (one batch-row loop with the four units
+// unrolled keeps that indexing static).  The dbias registers rule out a
+// 17th (issue-only) warp (it would cap every thread at 96 registers), so
+// the LAST warp to finish packing unit u (a shared-memory arrival counter
+// per unit parity) issues its dQ MMAs, the S/dP MMAs of unit u+2 and the
+// TMA loads: nobody waits for the issue, and the counter's acquire/release
+// chain (with tcgen05 fences) orders MMAs issued by different threads.
+template <int D, int BIASMODE>
+__global__ void __launch_bounds__(512, 1)
+attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
+                        const __grid_constant__ CUtensorMap mK,
+                        const __grid_constant__ CUtensorMap mV,
+                        const __grid_constant__ CUtensorMap mdO,
+                        const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // Q | dO | K | V of one batch row
+  constexpr bool TB = BIASMODE == 2;
+  constexpr int NU = 4, UW = 64;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+  uint8_t *sBias = smem_raw;
+  uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
+  // 0 bias, 1-2 row data, 3-5 S/dP MMAs (region), 6-7 row's last dQ MMAs,
+  // 8-9 arrival counters of a unit's packing (unit parity), 10-12 unit's dQ
+  // MMAs done (region)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sRow + 2 * ROWB);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 13);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = (warp & 3) * 32 + lane;  // query row in the tile
+  const int qr = warp >> 2;              // 16-key quarter of each unit
+  const int q0 = blockIdx.x * QT, h = blockIdx.y;
+  const int L = a.L;
+  const int q = q0 + t;
+  const bool qv = q < L;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  const int64_t nrows = b_hi - b_lo;
+  const int64_t U = nrows > 0 ? nrows * NU : 0;
+  if (tid == 0) {
+    for (int i = 0; i < 13; ++i) {
+      if (i == 8 || i == 9) bars[i] = 0;  // arrival counters, not mbarriers
+      else mbar_init(&bars[i], 1);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, 256);
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+
+  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
+  const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
+  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+
+  auto load_row = [&](int64_t r) {
+    uint8_t *rb = rowbuf(r);
+    uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+    mbar_expect_tx(bar, ROWB);
+    tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
+    tma_load_4d(rb + TILE, &mdO, bar, 0, q0, (int)r, h);
+    tma_load_4d(rb + 2 * TILE, &mK, bar, 0, 0, (int)r, h);
+    tma_load_4d(rb + 2 * TILE + FULL, &mV, bar, 0, 0, (int)r, h);
+  };
+  auto issue_mma1 = [&](int64_t u) {  // warp-collective
+    const int64_t r = b_lo + u / NU;
+    const int ui = (int)(u % NU), reg = (int)(u % 3);
+    if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
+    fence_after();
+    const uint32_t sQ = smem_u32(rowbuf(r)), sdO = sQ + TILE;
+    const uint32_t sK = sQ + 2 * TILE + ui * UW * Sw<D>::bytes, sV = sK + FULL;
+    const uint32_t d = tmem + reg * 128;
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16_el(d, desc_kmajor_tile<D>(sQ, ks), desc_kmajor_tile<D>(sK, ks), idesc_s, ks > 0);
+#pragma unroll
+    for (int ks = 0; ks < D / 16; ++ks)
+      umma_bf16_el(d + 64, desc_kmajor_tile<D>(sdO, ks), desc_kmajor_tile<D>(sV, ks), idesc_s,
+                   ks > 0);
+    umma_commit_el(&bars[3 + reg]);
+    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && u < 64 &&
+        (threadIdx.x & 31) == 0)
+      a.trace[u * 8 + 5] = clk();
+  };
+  // the issuing step after unit u was packed by every warp (warp-collective)
+  auto issue_unit = [&](int64_t u) {
+    const int64_t r = b_lo + u / NU;
+    const int ui = (int)(u % NU), reg = (int)(u % 3);
+    const int rp = (int)((r - b_lo) & 1);
+    fence_after();
+    if (ui == 0 && r > b_lo && r + 1 < b_hi) {  // row r-1 read back
+      if ((threadIdx.x & 31) == 0) load_row(r + 1);
+      __syncwarp();
+    }
+    const uint32_t acc = tmem + 384 + rp * 64;
+    const uint32_t sK = smem_u32(rowbuf(r)) + 2 * TILE;
+    const uint32_t reg_col = tmem + reg * 128;
+#pragma unroll
+    for (int ks = 0; ks < 4; ++ks)
+      umma_bf16_ts_el(acc, reg_col + ks * 16, desc_mnmajor_tile<D>(sK, ui * 4 + ks), idesc_o,
+                      (ui > 0 || ks > 0) ? 1u : 0u);
+    if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
+    umma_commit_el(&bars[10 + reg]);
+    const bool tri = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && u < 64 &&
+                     (threadIdx.x & 31) == 0;
+    if (tri) a.trace[u * 8 + 6] = clk();
+    if (u + 2 < U) {
+      if (u >= 1) mbar_wait(&bars[10 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
+      if (tri) a.trace[u * 8 + 7] = clk();
+      issue_mma1(u + 2);
+    }
+  };
+  if (warp == 0 && nrows > 0) {
+    if (lane == 0) {
+      load_row(b_lo);
+      if (nrows > 1) load_row(b_lo + 1);
+    }
+    __syncwarp();
+    issue_mma1(0);
+    if (U > 1) issue_mma1(1);
+  }
+  {
+    // ------------------------------------------------------------ elementwise
+    auto readout = [&](int64_t rr) {  // dq row of batch row rr -> global
+      const int pp = (int)((rr - b_lo) & 1);
+      mbar_wait(&bars[6 + pp], (uint32_t)(((rr - b_lo) >> 1) & 1));
+      fence_after();
+      constexpr int QD = D / 4;
+      const uint32_t acc = lane_addr + 384 + pp * 64;
+      uint32_t v[8];
+      if constexpr (QD == 8) {
+        tmem_ld8_nw(acc + qr * 8, v);
+      } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
+                     : "r"(acc + qr * 4));
+      }
+      tmem_wait_ld();
+      if (qv) {
+        bf16 *dst = a.dq + rr * a.sb + (int64_t)q * a.sl + h * D + qr * QD;
+        if constexpr (QD == 8) {
+          uint32_t w4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            w4[j] = pack2(__uint_as_float(v[2 * j]) * a.scale,
+                          __uint_as_float(v[2 * j + 1]) * a.scale);
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(w4[0], w4[1], w4[2], w4[3]);
+        } else {
+          uint32_t w2[2];
+#pragma unroll
+          for (int j = 0; j < 2; ++j)
+            w2[j] = pack2(__uint_as_float(v[2 * j]) * a.scale,
+                          __uint_as_float(v[2 * j + 1]) * a.scale);
+          *reinterpret_cast<uint2 *>(dst) = make_uint2(w2[0], w2[1]);
+        }
+      }
+    };
+    if (BIASMODE) {
+      mbar_wait(&bars[0], 0);
+      scale_tile(sBias, 8 * 16384 / 16, 512);
+      named_bar_sync(1, 512);
+    }
+    const float sc_l2 = a.scale * LOG2E;
+    float acc[64];
+#pragma unroll
+    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
+    float lse_n = 0.f, Dq_n = 0.f;
+    if (qv && nrows > 0) {
+      lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
+      Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + q];
+    }
+    for (int64_t r = b_lo; r < b_hi; ++r) {
+      const float lse_l2 = lse_n * LOG2E;
+      const float Dq = Dq_n;
+      if (qv && r + 1 < b_hi) {
+        lse_n = a.lse[((r + 1) * a.H + h) * (int64_t)L + q];
+        Dq_n = a.Dq[((r + 1) * a.H + h) * (int64_t)L + q];
+      }
+#pragma unroll
+      for (int ui = 0; ui < NU; ++ui) {
+        const int64_t u = (r - b_lo) * NU + ui;
+        const int reg = (int)(u % 3);
+        const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+                        tid == 0 && u < 64;
+        if (tr) a.trace[u * 8 + 0] = clk();
+        mbar_wait(&bars[3 + reg], (uint32_t)((u / 3) & 1));
+        fence_after();
+        if (tr) a.trace[u * 8 + 1] = clk();
+        const uint32_t rb = lane_addr + reg * 128;
+        const int c0 = qr * 16;
+        const int kb = ui * UW + c0;  // first key of this thread's 16
+        uint32_t sv[16], dv[16];
+        tmem_ld16_nw(rb + c0, sv);
+        tmem_ld16_nw(rb + 64 + c0, dv);
+        tmem_wait_ld();
+        float bb[16];
+        if (BIASMODE) bias_row16<!TB>(sBias, t, kb, bb);
+        const bool full = qv && kb + 16 <= L;
+        uint32_t pk[8];
+#pragma unroll
+        for (int j = 0; j < 16; j += 2) {
+          float ds[2];
+#pragma unroll
+          for (int w2 = 0; w2 < 2; ++w2) {
+            float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
+            if (BIASMODE) x += bb[j + w2];
+            const float e = ex2(x);
+            const float p = full ? e : ((qv && kb + j + w2 < L) ? e : 0.f);
+            ds[w2] = p * (__uint_as_float(dv[j + w2]) - Dq);
+            acc[16 * ui + j + w2] += ds[w2];
+          }
+          pk[j >> 1] = pack2(ds[0], ds[1]);
+        }
+        tmem_st8(rb + c0, pk);
+        if (ui == 0 && r > b_lo) readout(r - 1);
+        tmem_st_wait();
+        fence_before();
+        __syncwarp();
+        int last = 0;
+        if (lane == 0) {
+          int *cnt = reinterpret_cast<int *>(&bars[8 + (int)(u & 1)]);
+          __threadfence_block();
+          if (tr) a.trace[u * 8 + 2] = clk();
+          if (atomicAdd(cnt, 1) == 15) {  // last of the 16 warps
+            atomicExch(cnt, 0);             // reused by unit u+2 (issued below)
+            __threadfence_block();
+            last = 1;
+          }
+        }
+        last = __shfl_sync(0xffffffffu, last, 0);
+        if (last) {  // warp-uniform
+          const bool tri = a.trace && blockIdx.x == 0 && blockIdx.y == 0 &&
+                           blockIdx.z == 0 && u < 64 && lane == 0;
+          if (tri) a.trace[u * 8 + 3] = clk();
+          issue_unit(u);
+          if (tri) a.trace[u * 8 + 4] = clk();
+        }
+      }
+    }
+    if (nrows > 0) readout(b_hi - 1);
+    // dbias partial of this chunk: keys ui*64 + qr*16 + j  <- acc[16*ui + j]
+    if (a.dbias_part != nullptr && qv) {
+      float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
+                   (int64_t)h * a.bh + (int64_t)q * a.bq;
+#pragma unroll
+      for (int ui = 0; ui < NU; ++ui) {
+        const int kb = ui * UW + qr * 16;
+        if (a.bk == 1 && kb + 16 <= L && ((reinterpret_cast<uintptr_t>(dst + kb) & 15) == 0)) {
+#pragma unroll
+          for (int j = 0; j < 16; j += 4)
+            *reinterpret_cast<float4 *>(dst + kb + j) =
+                make_float4(acc[16 * ui + j], acc[16 * ui + j + 1], acc[16 * ui + j + 2],
+                            acc[16 * ui + j + 3]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < 16; ++j)
+            if (kb + j < L) dst[(int64_t)(kb + j) * a.bk] = acc[16 * ui + j];
+        }
+      }
+    }
+  }
   fence_before();
   __syncthreads();
   if (warp == 0) tmem_dealloc(tmem, 512);
@@ -1191,7 +1484,7 @@ AttnTcArgs make_args(const evo_attn_desc *d) {
   a.dO = nullptr; a.Dq = nullptr;
   a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
   a.dv = reinterpret_cast<bf16 *>(d->dv);
-  a.dbias_part = nullptr; a.chunk = 1;
+  a.dbias_part = nullptr; a.chunk = 1; a.trace = nullptr;
   return a;
 }
 
@@ -1337,7 +1630,34 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     mbk = mq;
   }
   const int tiles = (d->L + QT - 1) / QT;
-  {
+  if (Lp == 256 && !g_attn_no_pipe) {
+    const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
+                        13 * 8 + 16;
+    EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_>));
+    dim3 grid(tiles, d->H, (unsigned)nch);
+    static long long *trace_buf = nullptr;
+    static const bool want_trace = getenv("EVO_ATTN_TRACE") && getenv("EVO_ATTN_TRACE")[0] == '1';
+    if (want_trace) {
+      if (!trace_buf) cudaMalloc(&trace_buf, 64 * 8 * sizeof(long long));
+      cudaMemsetAsync(trace_buf, 0, 64 * 8 * sizeof(long long), st);
+      a.trace = trace_buf;
+    }
+    attn_bwd_dq_pipe_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
+    a.trace = nullptr;
+    if (want_trace) {
+      long long h[64 * 8];
+      cudaStreamSynchronize(st);
+      cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
+      const long long t0 = h[0];
+      fprintf(stderr, "unit: wait_start mma1_ready packed | issue_start mma2_done_issue waited issue_end | mma1_issued(u)\n");
+      for (int u = 0; u < 24; ++u)
+        fprintf(stderr, "%2d: %7lld %7lld %7lld | %7lld %7lld %7lld %7lld | %7lld\n", u, h[u * 8] - t0,
+                h[u * 8 + 1] - t0, h[u * 8 + 2] - t0, h[u * 8 + 3] ? h[u * 8 + 3] - t0 : -1,
+                h[u * 8 + 6] ? h[u * 8 + 6] - t0 : -1, h[u * 8 + 7] ? h[u * 8 + 7] - t0 : -1,
+                h[u * 8 + 4] ? h[u * 8 + 4] - t0 : -1, h[u * 8 + 5] ? h[u * 8 + 5] - t0 : -1);
+    }
+  } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
                         3 * 256 * 2 * D + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D, BM_>));
@@ -1347,7 +1667,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   }
   if (Lp == 256 && !g_attn_no_pipe) {
     const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
-                        2 * 256 * 4 + 12 * 8 + 16;
+                        2 * 256 * 4 + 13 * 8 + 16;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
     attn_bwd_dkv_pipe_kernel<D, BM_><<<grid, 544, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
