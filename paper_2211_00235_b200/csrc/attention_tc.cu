@@ -1179,20 +1179,39 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
 }
 
 // ============================================================= dq, pipelined
-// Lp == 256, same scheme as the pipelined dk/dv kernel: units of 64 keys
-// (four per batch row) through three TMEM regions [S 64 | dP 64]; S/dP MMAs
-// two units ahead; dS packed in place (a 16-key K slice = one thread
-// quarter); dQ accumulated in TMEM per row (row-parity accumulators at
-// 384 + 64*(r&1)); lse / Dq of the thread's query row live in registers, the
-// dbias partial for its 64 keys too (one batch-row loop with the four units
-// unrolled keeps that indexing static).  The dbias registers rule out a
-// 17th (issue-only) warp (it would cap every thread at 96 registers), so
-// the LAST warp to finish packing unit u (a shared-memory arrival counter
-// per unit parity) issues its dQ MMAs, the S/dP MMAs of unit u+2 and the
-// TMA loads: nobody waits for the issue, and the counter's acquire/release
-// chain (with tcgen05 fences) orders MMAs issued by different threads.
+// Lp == 256.  Units of 32 keys (eight per batch row) flow through three TMEM
+// regions [S 32 | dP 32] at 64*(u%3); the S/dP MMAs run two units ahead of
+// the elementwise pass.  dS (bf16 pairs) is packed into the region's first
+// 16 columns (a per-lane-quadrant named barrier separates the loads from the
+// in-place stores of the four warps sharing those TMEM lanes), then:
+//   dQ   += dS K_u          (TS MMA; row-parity accumulators at 192 + 32*(r&1))
+//   dbias[ui] += dS I_32    (TS MMA against a 32x32 identity in smem: the
+//                            batch-row sum of dS accumulates in TMEM cols
+//                            256 + 32*ui for the whole chunk)
+// so no thread keeps a dbias partial in registers and two dedicated issuer
+// warps fit the register budget: warp 16 issues the S/dP MMAs (each one as
+// soon as its region's previous dQ/dbias MMAs completed), warp 17 the
+// dQ/dbias MMAs and the TMA loads (warp-collective, one elected lane).
+// dbias sums bf16-rounded dS (the values the dQ MMA consumes).
+template <bool ROWBOX>
+__device__ __forceinline__ void bias_row8(const uint8_t *sb, int row, int k0, float (&out)[8]) {
+  if constexpr (ROWBOX) {
+    const uint8_t *base = sb + (k0 >> 5) * 16384 + row * 128;
+    const int c0 = (k0 & 31) >> 2;
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      float4 v = *reinterpret_cast<const float4 *>(base + (((c0 + c) ^ (row & 7)) << 4));
+      out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
+    }
+  } else {
+    const float *p = reinterpret_cast<const float *>(sb) + k0 * 128 + row;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) out[j] = p[j * 128];
+  }
+}
+
 template <int D, int BIASMODE>
-__global__ void __launch_bounds__(512, 1)
+__global__ void __launch_bounds__(576, 1)
 attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
                         const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV,
@@ -1202,20 +1221,21 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
   constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // Q | dO | K | V of one batch row
   constexpr bool TB = BIASMODE == 2;
-  constexpr int NU = 4, UW = 64;
+  constexpr int NU = 8, UW = 32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sBias = smem_raw;
   uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
-  // 0 bias, 1-2 row data, 3-5 S/dP MMAs (region), 6-7 row's last dQ MMAs,
-  // 8-9 arrival counters of a unit's packing (unit parity), 10-12 unit's dQ
-  // MMAs done (region)
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sRow + 2 * ROWB);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 13);
+  uint8_t *sI = sRow + 2 * ROWB;  // 32 x 32 bf16 identity, K-major SW64
+  // 0 bias, 1-2 row data (row parity), 3-5 S/dP MMAs (region), 6-7 row's
+  // last dQ MMAs (row parity), 8-9 unit packed (16 warp arrivals, unit
+  // parity), 10-12 unit's MMAs done (region), 13 chunk's last MMAs
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sI + 2048);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 14);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
-  const int qr = warp >> 2;              // 16-key quarter of each unit
+  const int qr = warp >> 2;              // 8-key quarter of each unit
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
   const int L = a.L;
   const int q = q0 + t;
@@ -1224,99 +1244,123 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
   const int64_t nrows = b_hi - b_lo;
   const int64_t U = nrows > 0 ? nrows * NU : 0;
-  if (tid == 0) {
-    for (int i = 0; i < 13; ++i) {
-      if (i == 8 || i == 9) bars[i] = 0;  // arrival counters, not mbarriers
-      else mbar_init(&bars[i], 1);
-    }
+
+  if (tid == 512) {
+    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], (i == 8 || i == 9) ? 16 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, 256);
   }
+  // identity: row n has bf16 1.0 at column n (SW64: 16-byte chunk c of row n
+  // sits at chunk c ^ ((n >> 1) & 3))
+  for (int i = tid; i < 2048 / 16; i += blockDim.x) {
+    const int n = i >> 2, c = i & 3;  // physical chunk c of row n
+    uint4 z = make_uint4(0u, 0u, 0u, 0u);
+    const int lc = c ^ ((n >> 1) & 3);  // logical chunk stored here
+    if (lc == (n >> 3)) {
+      const int pos = n & 7;  // bf16 slot within the chunk
+      uint32_t w = 0x3f80u << (16 * (pos & 1));
+      if ((pos >> 1) == 0) z.x = w; else if ((pos >> 1) == 1) z.y = w;
+      else if ((pos >> 1) == 2) z.z = w; else z.w = w;
+    }
+    *reinterpret_cast<uint4 *>(sI + n * 64 + c * 16) = z;
+  }
+  fence_proxy_async_smem();
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-
   auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
-  const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
-  const uint32_t idesc_o = idesc_bf16(128, D, false, true);
 
-  auto load_row = [&](int64_t r) {
-    uint8_t *rb = rowbuf(r);
-    uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
-    mbar_expect_tx(bar, ROWB);
-    tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
-    tma_load_4d(rb + TILE, &mdO, bar, 0, q0, (int)r, h);
-    tma_load_4d(rb + 2 * TILE, &mK, bar, 0, 0, (int)r, h);
-    tma_load_4d(rb + 2 * TILE + FULL, &mV, bar, 0, 0, (int)r, h);
-  };
-  auto issue_mma1 = [&](int64_t u) {  // warp-collective
-    const int64_t r = b_lo + u / NU;
-    const int ui = (int)(u % NU), reg = (int)(u % 3);
-    if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
-    fence_after();
-    const uint32_t sQ = smem_u32(rowbuf(r)), sdO = sQ + TILE;
-    const uint32_t sK = sQ + 2 * TILE + ui * UW * Sw<D>::bytes, sV = sK + FULL;
-    const uint32_t d = tmem + reg * 128;
-#pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16_el(d, desc_kmajor_tile<D>(sQ, ks), desc_kmajor_tile<D>(sK, ks), idesc_s, ks > 0);
-#pragma unroll
-    for (int ks = 0; ks < D / 16; ++ks)
-      umma_bf16_el(d + 64, desc_kmajor_tile<D>(sdO, ks), desc_kmajor_tile<D>(sV, ks), idesc_s,
-                   ks > 0);
-    umma_commit_el(&bars[3 + reg]);
-    if (a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && u < 64 &&
-        (threadIdx.x & 31) == 0)
-      a.trace[u * 8 + 5] = clk();
-  };
-  // the issuing step after unit u was packed by every warp (warp-collective)
-  auto issue_unit = [&](int64_t u) {
-    const int64_t r = b_lo + u / NU;
-    const int ui = (int)(u % NU), reg = (int)(u % 3);
-    const int rp = (int)((r - b_lo) & 1);
-    fence_after();
-    if (ui == 0 && r > b_lo && r + 1 < b_hi) {  // row r-1 read back
-      if ((threadIdx.x & 31) == 0) load_row(r + 1);
+  if (warp >= 16) {
+    // ------------------------------------------------------------ issuers
+    const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
+    const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    const uint32_t idesc_i = idesc_bf16(128, 32, false, false);
+    auto load_row = [&](int64_t r) {
+      uint8_t *rb = rowbuf(r);
+      uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+      mbar_expect_tx(bar, ROWB);
+      tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
+      tma_load_4d(rb + TILE, &mdO, bar, 0, q0, (int)r, h);
+      tma_load_4d(rb + 2 * TILE, &mK, bar, 0, 0, (int)r, h);
+      tma_load_4d(rb + 2 * TILE + FULL, &mV, bar, 0, 0, (int)r, h);
+    };
+    if (warp == 16 && nrows > 0) {
+      // S/dP MMAs: unit v into region v%3 once unit v-3's dQ/dbias MMAs
+      // (the region's previous readers) completed
+      if (lane == 0) {
+        load_row(b_lo);
+        if (nrows > 1) load_row(b_lo + 1);
+      }
       __syncwarp();
-    }
-    const uint32_t acc = tmem + 384 + rp * 64;
-    const uint32_t sK = smem_u32(rowbuf(r)) + 2 * TILE;
-    const uint32_t reg_col = tmem + reg * 128;
+      int reg = 0;
+      uint32_t ph3 = 0;  // bit i: parity of region i's dQ/dbias-done barrier
+      for (int v = 0; v < (int)U; ++v) {
+        const int64_t r = b_lo + (v >> 3);
+        const int ui = v & (NU - 1);
+        if (v >= 3) {
+          mbar_wait(&bars[10 + reg], (ph3 >> reg) & 1u);
+          ph3 ^= 1u << reg;
+        }
+        if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
+        fence_after();
+        const uint32_t sQ = smem_u32(rowbuf(r)), sdO = sQ + TILE;
+        const uint32_t sK = sQ + 2 * TILE + ui * UW * Sw<D>::bytes, sV = sK + FULL;
+        const uint32_t d = tmem + reg * 64;
 #pragma unroll
-    for (int ks = 0; ks < 4; ++ks)
-      umma_bf16_ts_el(acc, reg_col + ks * 16, desc_mnmajor_tile<D>(sK, ui * 4 + ks), idesc_o,
-                      (ui > 0 || ks > 0) ? 1u : 0u);
-    if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
-    umma_commit_el(&bars[10 + reg]);
-    const bool tri = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && u < 64 &&
-                     (threadIdx.x & 31) == 0;
-    if (tri) a.trace[u * 8 + 6] = clk();
-    if (u + 2 < U) {
-      if (u >= 1) mbar_wait(&bars[10 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
-      if (tri) a.trace[u * 8 + 7] = clk();
-      issue_mma1(u + 2);
-    }
-  };
-  if (warp == 0 && nrows > 0) {
-    if (lane == 0) {
-      load_row(b_lo);
-      if (nrows > 1) load_row(b_lo + 1);
+        for (int ks = 0; ks < D / 16; ++ks)
+          umma_bf16_el(d, desc_kmajor_tile<D>(sQ, ks), desc_kmajor_tile<D>(sK, ks), idesc_s,
+                       ks > 0);
+#pragma unroll
+        for (int ks = 0; ks < D / 16; ++ks)
+          umma_bf16_el(d + 32, desc_kmajor_tile<D>(sdO, ks), desc_kmajor_tile<D>(sV, ks),
+                       idesc_s, ks > 0);
+        umma_commit_el(&bars[3 + reg]);
+        reg = reg == 2 ? 0 : reg + 1;
+      }
+    } else if (warp == 17 && nrows > 0) {
+      // dQ / dbias MMAs of unit u once all 16 warps packed its dS
+      const uint32_t sIa = smem_u32(sI);
+      int reg = 0;
+      for (int u = 0; u < (int)U; ++u) {
+        const int64_t r = b_lo + (u >> 3);
+        const int ui = u & (NU - 1);
+        const int rp = (int)((r - b_lo) & 1);
+        mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));
+        fence_after();
+        if (ui == 0 && r > b_lo && r + 1 < b_hi) {  // row r-1 read back: its buffers are free
+          if (lane == 0) load_row(r + 1);
+          __syncwarp();
+        }
+        const uint32_t sK = smem_u32(rowbuf(r)) + 2 * TILE;
+        const uint32_t reg_col = tmem + reg * 64;
+        const uint32_t acc = tmem + 192 + rp * 32;
+        const uint32_t dba = tmem + 256 + ui * 32;
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          umma_bf16_ts_el(acc, reg_col + ks * 8, desc_mnmajor_tile<D>(sK, ui * 2 + ks), idesc_o,
+                          (ui > 0 || ks > 0) ? 1u : 0u);
+#pragma unroll
+        for (int ks = 0; ks < 2; ++ks)
+          umma_bf16_ts_el(dba, reg_col + ks * 8, desc_kmajor_tile<32>(sIa, ks), idesc_i,
+                          (r > b_lo || ks > 0) ? 1u : 0u);
+        if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
+        umma_commit_el(&bars[10 + reg]);
+        reg = reg == 2 ? 0 : reg + 1;
+      }
+      umma_commit_el(&bars[13]);  // every MMA of the chunk (dbias sums) done
     }
     __syncwarp();
-    issue_mma1(0);
-    if (U > 1) issue_mma1(1);
-  }
-  {
+  } else {
     // ------------------------------------------------------------ elementwise
     auto readout = [&](int64_t rr) {  // dq row of batch row rr -> global
       const int pp = (int)((rr - b_lo) & 1);
       mbar_wait(&bars[6 + pp], (uint32_t)(((rr - b_lo) >> 1) & 1));
       fence_after();
       constexpr int QD = D / 4;
-      const uint32_t acc = lane_addr + 384 + pp * 64;
+      const uint32_t acc = lane_addr + 192 + pp * 32;
       uint32_t v[8];
       if constexpr (QD == 8) {
         tmem_ld8_nw(acc + qr * 8, v);
@@ -1351,100 +1395,98 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       named_bar_sync(1, 512);
     }
     const float sc_l2 = a.scale * LOG2E;
-    float acc[64];
-#pragma unroll
-    for (int j = 0; j < 64; ++j) acc[j] = 0.f;
     float lse_n = 0.f, Dq_n = 0.f;
     if (qv && nrows > 0) {
       lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
       Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + q];
     }
-    for (int64_t r = b_lo; r < b_hi; ++r) {
-      const float lse_l2 = lse_n * LOG2E;
-      const float Dq = Dq_n;
-      if (qv && r + 1 < b_hi) {
-        lse_n = a.lse[((r + 1) * a.H + h) * (int64_t)L + q];
-        Dq_n = a.Dq[((r + 1) * a.H + h) * (int64_t)L + q];
-      }
-#pragma unroll
-      for (int ui = 0; ui < NU; ++ui) {
-        const int64_t u = (r - b_lo) * NU + ui;
-        const int reg = (int)(u % 3);
-        const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
-                        tid == 0 && u < 64;
-        if (tr) a.trace[u * 8 + 0] = clk();
-        mbar_wait(&bars[3 + reg], (uint32_t)((u / 3) & 1));
-        fence_after();
-        if (tr) a.trace[u * 8 + 1] = clk();
-        const uint32_t rb = lane_addr + reg * 128;
-        const int c0 = qr * 16;
-        const int kb = ui * UW + c0;  // first key of this thread's 16
-        uint32_t sv[16], dv[16];
-        tmem_ld16_nw(rb + c0, sv);
-        tmem_ld16_nw(rb + 64 + c0, dv);
-        tmem_wait_ld();
-        float bb[16];
-        if (BIASMODE) bias_row16<!TB>(sBias, t, kb, bb);
-        const bool full = qv && kb + 16 <= L;
-        uint32_t pk[8];
-#pragma unroll
-        for (int j = 0; j < 16; j += 2) {
-          float ds[2];
-#pragma unroll
-          for (int w2 = 0; w2 < 2; ++w2) {
-            float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
-            if (BIASMODE) x += bb[j + w2];
-            const float e = ex2(x);
-            const float p = full ? e : ((qv && kb + j + w2 < L) ? e : 0.f);
-            ds[w2] = p * (__uint_as_float(dv[j + w2]) - Dq);
-            acc[16 * ui + j + w2] += ds[w2];
-          }
-          pk[j >> 1] = pack2(ds[0], ds[1]);
-        }
-        tmem_st8(rb + c0, pk);
-        if (ui == 0 && r > b_lo) readout(r - 1);
-        tmem_st_wait();
-        fence_before();
-        __syncwarp();
-        int last = 0;
-        if (lane == 0) {
-          int *cnt = reinterpret_cast<int *>(&bars[8 + (int)(u & 1)]);
-          __threadfence_block();
-          if (tr) a.trace[u * 8 + 2] = clk();
-          if (atomicAdd(cnt, 1) == 15) {  // last of the 16 warps
-            atomicExch(cnt, 0);             // reused by unit u+2 (issued below)
-            __threadfence_block();
-            last = 1;
-          }
-        }
-        last = __shfl_sync(0xffffffffu, last, 0);
-        if (last) {  // warp-uniform
-          const bool tri = a.trace && blockIdx.x == 0 && blockIdx.y == 0 &&
-                           blockIdx.z == 0 && u < 64 && lane == 0;
-          if (tri) a.trace[u * 8 + 3] = clk();
-          issue_unit(u);
-          if (tri) a.trace[u * 8 + 4] = clk();
+    float lse_l2 = 0.f, Dq = 0.f;
+    int reg = 0;
+    uint32_t ph3 = 0;  // bit i: parity of region i's S/dP barrier
+    const int U32 = (int)U;
+    for (int u = 0; u < U32; ++u) {
+      const int64_t r = b_lo + (u >> 3);
+      const int ui = u & (NU - 1);
+      if (ui == 0) {
+        lse_l2 = lse_n * LOG2E;
+        Dq = Dq_n;
+        if (qv && r + 1 < b_hi) {
+          lse_n = a.lse[((r + 1) * a.H + h) * (int64_t)L + q];
+          Dq_n = a.Dq[((r + 1) * a.H + h) * (int64_t)L + q];
         }
       }
+      const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
+                      tid == 0 && u < 64;
+      if (tr) a.trace[u * 8 + 0] = clk();
+      mbar_wait(&bars[3 + reg], (ph3 >> reg) & 1u);
+      ph3 ^= 1u << reg;
+      fence_after();
+      if (tr) a.trace[u * 8 + 1] = clk();
+      const uint32_t rb = lane_addr + reg * 64;
+      const int c0 = qr * 8;
+      const int kb = ui * UW + c0;  // first key of this thread's 8
+      uint32_t sv[8], dv[8];
+      tmem_ld8_nw(rb + c0, sv);
+      tmem_ld8_nw(rb + 32 + c0, dv);
+      tmem_wait_ld();
+      float bb[8];
+      if (BIASMODE) bias_row8<!TB>(sBias, t, kb, bb);
+      const bool full = qv && kb + 8 <= L;
+      uint32_t pk[4];
+#pragma unroll
+      for (int j = 0; j < 8; j += 2) {
+        float ds[2];
+#pragma unroll
+        for (int w2 = 0; w2 < 2; ++w2) {
+          float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
+          if (BIASMODE) x += bb[j + w2];
+          const float e = ex2(x);
+          const float p = full ? e : ((qv && kb + j + w2 < L) ? e : 0.f);
+          ds[w2] = p * (__uint_as_float(dv[j + w2]) - Dq);
+        }
+        pk[j >> 1] = pack2(ds[0], ds[1]);
+      }
+      // the four warps of this lane quadrant have loaded the region's S
+      // columns before any of them overwrites them with packed dS
+      named_bar_sync(2 + (warp & 3), 128);
+      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                       rb + qr * 4),
+                   "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
+                   : "memory");
+      if (ui == 0 && r > b_lo) readout(r - 1);
+      tmem_st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[8 + (u & 1)]);
+      if (tr) a.trace[u * 8 + 2] = clk();
+      reg = reg == 2 ? 0 : reg + 1;
     }
-    if (nrows > 0) readout(b_hi - 1);
-    // dbias partial of this chunk: keys ui*64 + qr*16 + j  <- acc[16*ui + j]
-    if (a.dbias_part != nullptr && qv) {
-      float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
-                   (int64_t)h * a.bh + (int64_t)q * a.bq;
+    if (nrows > 0) {
+      readout(b_hi - 1);
+      // dbias partial of this chunk: TMEM cols 256 + key -> global
+      mbar_wait(&bars[13], 0);
+      fence_after();
+      if (a.dbias_part != nullptr) {
+        float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
+                     (int64_t)h * a.bh + (int64_t)q * a.bq;
 #pragma unroll
-      for (int ui = 0; ui < NU; ++ui) {
-        const int kb = ui * UW + qr * 16;
-        if (a.bk == 1 && kb + 16 <= L && ((reinterpret_cast<uintptr_t>(dst + kb) & 15) == 0)) {
+        for (int c = 0; c < 2; ++c) {
+          const int kb = qr * 64 + 32 * c;
+          uint32_t v[32];
+          tmem_ld32(lane_addr + 256 + kb, v);
+          if (qv) {
+            if (a.bk == 1 && kb + 32 <= L && ((reinterpret_cast<uintptr_t>(dst + kb) & 15) == 0)) {
 #pragma unroll
-          for (int j = 0; j < 16; j += 4)
-            *reinterpret_cast<float4 *>(dst + kb + j) =
-                make_float4(acc[16 * ui + j], acc[16 * ui + j + 1], acc[16 * ui + j + 2],
-                            acc[16 * ui + j + 3]);
-        } else {
+              for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<float4 *>(dst + kb + j) =
+                    make_float4(__uint_as_float(v[j]), __uint_as_float(v[j + 1]),
+                                __uint_as_float(v[j + 2]), __uint_as_float(v[j + 3]));
+            } else {
 #pragma unroll
-          for (int j = 0; j < 16; ++j)
-            if (kb + j < L) dst[(int64_t)(kb + j) * a.bk] = acc[16 * ui + j];
+              for (int j = 0; j < 32; ++j)
+                if (kb + j < L) dst[(int64_t)(kb + j) * a.bk] = __uint_as_float(v[j]);
+            }
+          }
         }
       }
     }
@@ -1632,7 +1674,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   const int tiles = (d->L + QT - 1) / QT;
   if (Lp == 256 && !g_attn_no_pipe) {
     const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
-                        13 * 8 + 16;
+                        2048 + 14 * 8 + 16;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
     static long long *trace_buf = nullptr;
@@ -1642,20 +1684,21 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
       cudaMemsetAsync(trace_buf, 0, 64 * 8 * sizeof(long long), st);
       a.trace = trace_buf;
     }
-    attn_bwd_dq_pipe_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    attn_bwd_dq_pipe_kernel<D, BM_><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
     a.trace = nullptr;
-    if (want_trace) {
-      long long h[64 * 8];
+    if (want_trace) {  // debugging aid: per-unit clock64 stamps of CTA 0
+      long long hb[64 * 8];
       cudaStreamSynchronize(st);
-      cudaMemcpy(h, trace_buf, sizeof(h), cudaMemcpyDeviceToHost);
-      const long long t0 = h[0];
-      fprintf(stderr, "unit: wait_start mma1_ready packed | issue_start mma2_done_issue waited issue_end | mma1_issued(u)\n");
-      for (int u = 0; u < 24; ++u)
-        fprintf(stderr, "%2d: %7lld %7lld %7lld | %7lld %7lld %7lld %7lld | %7lld\n", u, h[u * 8] - t0,
-                h[u * 8 + 1] - t0, h[u * 8 + 2] - t0, h[u * 8 + 3] ? h[u * 8 + 3] - t0 : -1,
-                h[u * 8 + 6] ? h[u * 8 + 6] - t0 : -1, h[u * 8 + 7] ? h[u * 8 + 7] - t0 : -1,
-                h[u * 8 + 4] ? h[u * 8 + 4] - t0 : -1, h[u * 8 + 5] ? h[u * 8 + 5] - t0 : -1);
+      cudaMemcpy(hb, trace_buf, sizeof(hb), cudaMemcpyDeviceToHost);
+      const long long t0 = hb[0];
+      fprintf(stderr, "unit: ew_wait ew_ready ew_packed | is_wait is_go is_mma2 is_w2 is_end\n");
+      for (int u = 0; u < 40; ++u) {
+        fprintf(stderr, "%2d:", u);
+        for (int j = 0; j < 8; ++j)
+          fprintf(stderr, " %7lld%s", hb[u * 8 + j] ? hb[u * 8 + j] - t0 : -1, j == 2 ? " |" : "");
+        fprintf(stderr, "\n");
+      }
     }
   } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
