@@ -922,12 +922,13 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
 // at 384 + 64*(r&1)) and are read back one unit into the next row, and the
 // TMA loads of row r+1 go out as soon as row r-1's accumulators are read.
 // Warps 0-15 run the elementwise passes (4 lane quadrants x 4 query
-// quarters); warp 16 only issues: MMAs, TMA loads, commits, so no
-// elementwise warp ever waits on issue latency.
+// quarters); warps 16 and 17 only issue (16: the S^T/dP^T MMAs, each as soon
+// as its region's previous dV/dK MMAs completed; 17: the dV/dK MMAs and the
+// TMA loads), so no elementwise warp ever waits on issue latency.
 // smem: bias 128 KiB + two rows of K|V|Q|dO (96 KiB) + lse/Dq: no 1 KiB
 // alignment slack, the dynamic smem base is 1 KiB aligned (checked).
 template <int D, int BIASMODE>
-__global__ void __launch_bounds__(544, 1)
+__global__ void __launch_bounds__(576, 1)
 attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
                          const __grid_constant__ CUtensorMap mVt,
                          const __grid_constant__ CUtensorMap mQa,
@@ -992,9 +993,9 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   };
   const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-  auto issue_mma1 = [&](int64_t u) {  // warp-collective (issuer warp)
-    const int64_t r = b_lo + u / NU;
-    const int ui = (int)(u % NU), reg = (int)(u % 3);
+  auto issue_mma1 = [&](int u, int reg) {  // warp-collective (issuer warp)
+    const int64_t r = b_lo + (u >> 2);
+    const int ui = u & (NU - 1);
     if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
     fence_after();
     const uint32_t sK = smem_u32(rowbuf(r)), sV = sK + TILE;
@@ -1057,19 +1058,31 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
 
   if (!ew) {
     // ------------------------------------------------------------ issuer
-    if (nrows > 0) {  // the whole warp runs the loop; one elected lane issues
+    if (warp == 16 && nrows > 0) {
+      // S^T/dP^T MMAs: unit v into region v%3 once unit v-3's dV/dK MMAs
+      // (the region's previous readers) completed
       if (lane == 0) {
         load_row(b_lo);
         if (nrows > 1) load_row(b_lo + 1);
       }
       __syncwarp();
-      issue_mma1(0);
-      if (U > 1) issue_mma1(1);
-      for (int64_t u = 0; u < U; ++u) {
-        const int64_t r = b_lo + u / NU;
-        const int ui = (int)(u % NU), reg = (int)(u % 3);
+      int reg = 0;
+      uint32_t ph3 = 0;
+      for (int v = 0; v < (int)U; ++v) {
+        if (v >= 3) {
+          mbar_wait(&bars[10 + reg], (ph3 >> reg) & 1u);
+          ph3 ^= 1u << reg;
+        }
+        issue_mma1(v, reg);
+        reg = reg == 2 ? 0 : reg + 1;
+      }
+    } else if (warp == 17 && nrows > 0) {
+      int reg = 0;
+      for (int u = 0; u < (int)U; ++u) {
+        const int64_t r = b_lo + (u >> 2);
+        const int ui = u & (NU - 1);
         const int rp = (int)((r - b_lo) & 1);
-        mbar_wait(&bars[8 + (int)(u & 1)], (uint32_t)((u >> 1) & 1));  // all 16 warps packed unit u
+        mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));  // all 16 warps packed unit u
         fence_after();
         // at a row's first unit the warps have read row r-1's accumulators,
         // so row r-1's smem buffers are free for row r+1
@@ -1090,10 +1103,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
                           idesc_o, (ui > 0 || ks > 0) ? 1u : 0u);
         if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
         umma_commit_el(&bars[10 + reg]);
-        if (u + 2 < U) {
-          if (u >= 1) mbar_wait(&bars[10 + (int)((u + 2) % 3)], (uint32_t)(((u - 1) / 3) & 1));
-          issue_mma1(u + 2);
-        }
+        reg = reg == 2 ? 0 : reg + 1;
       }
     }
     __syncwarp();
@@ -1110,10 +1120,11 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   }
   const float sc_l2 = a.scale * LOG2E;
 
-  for (int64_t u = 0; u < U; ++u) {
-    const int64_t r = b_lo + u / NU;
-    const int ui = (int)(u % NU), reg = (int)(u % 3);
-    const int rp = (int)((r - b_lo) & 1);
+  int reg = 0;
+  uint32_t ph3 = 0;  // bit i: parity of region i's S^T/dP^T barrier
+  for (int u = 0; u < (int)U; ++u) {
+    const int64_t r = b_lo + (u >> 2);
+    const int ui = u & (NU - 1);
     if (ui == 0) {  // this row's lse / Dq into smem; prefetch the next row's
       if (r > b_lo) named_bar_sync(1, 512);  // every warp is done with row r-1's lse / Dq
       if (tid < 256) {
@@ -1129,7 +1140,8 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
       }
       named_bar_sync(1, 512);
     }
-    mbar_wait(&bars[3 + reg], (uint32_t)((u / 3) & 1));
+    mbar_wait(&bars[3 + reg], (ph3 >> reg) & 1u);
+    ph3 ^= 1u << reg;
     fence_after();
     const uint32_t rb = lane_addr + reg * 128;
     const int c0 = qr * 16;
@@ -1169,7 +1181,8 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     tmem_st_wait();
     fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&bars[8 + (int)(u & 1)]);
+    if (lane == 0) mbar_arrive(&bars[8 + (u & 1)]);
+    reg = reg == 2 ? 0 : reg + 1;
   }
   if (nrows > 0) readout(b_hi - 1);
   }  // elementwise warps
@@ -1713,7 +1726,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         2 * 256 * 4 + 13 * 8 + 16;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dkv_pipe_kernel<D, BM_><<<grid, 544, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    attn_bwd_dkv_pipe_kernel<D, BM_><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
     EVO_LAUNCHED("attn_bwd_dkv_pipe_kernel");
   } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 4 * 256 * 2 * D +
