@@ -125,6 +125,21 @@ EVO_API int evo_layernorm_bwd(int dtype_dy, int dtype_x, int dtype_dx, int64_t r
                       size_t workspace_bytes, void *stream);
 EVO_API size_t evo_layernorm_bwd_workspace_bytes(int64_t rows, int cols);
 
+/* LayerNorm backward of a contiguous [rows, cols] fp32 gradient (cols 128
+ * or 256) with two by-products of its fp32 output dx fused in, for the
+ * next sub-op's backward (src/evoformer.py:456-461 chains the sub-ops):
+ *   dx_act    (bf16, may be NULL): a copy of dx, that sub-op's GEMM operand
+ *   dx_colsum (fp32, may be NULL): sum over rows of dx, that sub-op's
+ *             output-bias gradient (src/tensor.py:343), written
+ * dgamma / dbeta are written (not accumulated); x is fp32 or bf16
+ * (dtype_x); dres as in evo_layernorm_bwd.  Same workspace.            */
+EVO_API int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const float *dy,
+                                 const void *x, const float *mean, const float *rstd,
+                                 const float *gamma, const float *dres, float *dx,
+                                 void *dx_act, float *dgamma, float *dbeta,
+                                 float *dx_colsum, void *workspace, size_t workspace_bytes,
+                                 void *stream);
+
 /* Fused gated attention forward over the middle axis
  * (_gated_attention core, src/evoformer.py:274-286):
  *   O[b,l,h,:] = softmax_k( scale*q.k + bias[h,l,k] ) v

@@ -56,6 +56,8 @@ _SIGS = {
                                   c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                                   c_i32, c_vp, c_sz, c_vp]),
     "evo_layernorm_bwd_workspace_bytes": (c_sz, [c_i64, c_i32]),
+    "evo_layernorm_bwd_ex": (c_i32, [c_i32, c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
+                                     c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "evo_attention_fwd": (c_i32, [C.POINTER(AttnDesc), c_vp]),
     "evo_attention_bwd": (c_i32, [C.POINTER(AttnDesc), c_vp]),
     "evo_attention_bwd_workspace_bytes": (c_sz, [C.POINTER(AttnDesc)]),

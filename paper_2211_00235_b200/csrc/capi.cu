@@ -26,6 +26,9 @@ int layernorm_fwd(int, int, int64_t, int, const void *, int64_t, int64_t, const 
 int layernorm_bwd(int, int, int, int64_t, int, const void *, int64_t, const void *, int64_t,
                   int64_t, const float *, const float *, const float *, const float *, void *,
                   int64_t, int64_t, float *, float *, int, void *, size_t, cudaStream_t);
+int layernorm_bwd_ex(int64_t, int, const float *, const void *, int, const float *, const float *,
+                     const float *, const float *, float *, void *, float *, float *, float *,
+                     void *, size_t, cudaStream_t);
 int attention_simt_fwd(const evo_attn_desc *, cudaStream_t);
 int attention_simt_bwd(const evo_attn_desc *, cudaStream_t);
 size_t attention_simt_bwd_ws(const evo_attn_desc *);
@@ -141,6 +144,20 @@ int evo_layernorm_bwd(int dtype_dy, int dtype_x, int dtype_dx, int64_t rows, int
   return layernorm_bwd(dtype_dy, dtype_x, dtype_dx, rows, cols, dy, dy_rs, x, x_rs, x_cs, mean,
                        rstd, gamma, dres, dx, dx_rs, dx_cs, dgamma, dbeta, accumulate_params,
                        workspace, workspace_bytes, as_stream(stream));
+}
+
+int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const float *dy, const void *x,
+                         const float *mean, const float *rstd, const float *gamma,
+                         const float *dres, float *dx, void *dx_act, float *dgamma, float *dbeta,
+                         float *dx_colsum, void *workspace, size_t workspace_bytes,
+                         void *stream) {
+  CHECK_DT(dtype_x);
+  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_layernorm_bwd_ex: rows=%lld cols=%d",
+              (long long)rows, cols);
+  if (rows == 0) return EVO_OK;
+  CHECK_PTR(dy); CHECK_PTR(x); CHECK_PTR(mean); CHECK_PTR(rstd); CHECK_PTR(gamma); CHECK_PTR(dx);
+  return layernorm_bwd_ex(rows, cols, dy, x, dtype_x, mean, rstd, gamma, dres, dx, dx_act, dgamma,
+                          dbeta, dx_colsum, workspace, workspace_bytes, as_stream(stream));
 }
 
 static int check_attn(const evo_attn_desc *d, bool bwd) {

@@ -133,17 +133,20 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
                   const TX *__restrict__ x, int64_t x_rs, const float *__restrict__ mean,
                   const float *__restrict__ rstd, const float *__restrict__ gamma,
                   const float *__restrict__ dres, TDX *__restrict__ dx, int64_t dx_rs,
-                  float *__restrict__ partial, int want_params) {
+                  bf16 *__restrict__ dxa, int64_t dxa_rs, float *__restrict__ partial,
+                  int nparts) {
+  // partial[block][0..nparts)[cols]: dgamma, dbeta, and (nparts == 3) the
+  // column sums of dx itself (the next consumer's bias gradient)
   constexpr int cols = NV * 128;
-  __shared__ float red[LN_WARPS][2][cols];
+  __shared__ float red[LN_WARPS][3][cols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  float pg[NV][4], pb[NV][4], g[NV][4];
+  float pg[NV][4], pb[NV][4], pc[NV][4], g[NV][4];
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
     float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane + 128 * i);
     g[i][0] = g4.x; g[i][1] = g4.y; g[i][2] = g4.z; g[i][3] = g4.w;
 #pragma unroll
-    for (int j = 0; j < 4; ++j) pg[i][j] = pb[i][j] = 0.f;
+    for (int j = 0; j < 4; ++j) pg[i][j] = pb[i][j] = pc[i][j] = 0.f;
   }
   constexpr float inv_n = 1.f / cols;
   for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + warp; row < rows;
@@ -180,23 +183,27 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
         r[0] += d4.x; r[1] += d4.y; r[2] += d4.z; r[3] += d4.w;
       }
       Vec<TDX, 4>::store(dx + row * dx_rs + c, r);
+      if (dxa) Vec<bf16, 4>::store(dxa + row * dxa_rs + c, r);
+#pragma unroll
+      for (int j = 0; j < 4; ++j) pc[i][j] += r[j];
     }
   }
-  if (!want_params) return;
+  if (!nparts) return;
 #pragma unroll
   for (int i = 0; i < NV; ++i)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       red[warp][0][4 * lane + 128 * i + j] = pg[i][j];
       red[warp][1][4 * lane + 128 * i + j] = pb[i][j];
+      red[warp][2][4 * lane + 128 * i + j] = pc[i][j];
     }
   __syncthreads();
-  for (int c = threadIdx.x; c < 2 * cols; c += blockDim.x) {
+  for (int c = threadIdx.x; c < nparts * cols; c += blockDim.x) {
     const int which = c / cols, cc = c % cols;
     float s = 0.f;
 #pragma unroll
     for (int w = 0; w < LN_WARPS; ++w) s += red[w][which][cc];
-    partial[((int64_t)blockIdx.x * 2 + which) * cols + cc] = s;
+    partial[((int64_t)blockIdx.x * nparts + which) * cols + cc] = s;
   }
 }
 
@@ -272,19 +279,23 @@ ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
 
 // Ordered reduction of the per-block partials: one warp per output value;
 // lane l sums partials l, l+32, ... then a fixed shuffle tree.
-__global__ void ln_param_reduce_kernel(int nblk, int cols, const float *__restrict__ partial,
+// One warp per output column: lane l sums partials l, l+32, ... (unrolled,
+// independent loads in flight), then a fixed-order warp tree.
+__global__ void ln_param_reduce_kernel(int nblk, int cols, int nparts,
+                                       const float *__restrict__ partial,
                                        float *__restrict__ dgamma, float *__restrict__ dbeta,
-                                       int accumulate) {
+                                       float *__restrict__ dcol, int accumulate) {
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= 2 * cols) return;
+  if (c >= nparts * cols) return;
   const int which = c / cols, cc = c % cols;
   float s = 0.f;
-  for (int b = lane; b < nblk; b += 32) s += partial[((int64_t)b * 2 + which) * cols + cc];
+#pragma unroll 4
+  for (int b = lane; b < nblk; b += 32) s += __ldg(&partial[((int64_t)b * nparts + which) * cols + cc]);
   s = warp_sum(s);
   if (lane == 0) {
-    float *dst = which == 0 ? dgamma : dbeta;
-    if (dst) dst[cc] = accumulate ? dst[cc] + s : s;
+    float *dst = which == 0 ? dgamma : (which == 1 ? dbeta : dcol);
+    if (dst) dst[cc] = (accumulate && which < 2) ? dst[cc] + s : s;
   }
 }
 
@@ -326,8 +337,9 @@ template <typename TDY, typename TX, typename TDX>
 int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const void *x,
                   int64_t x_rs, int64_t x_cs, const float *mean, const float *rstd,
                   const float *gamma, const float *dres, void *dx, int64_t dx_rs, int64_t dx_cs,
-                  float *dgamma, float *dbeta, int acc, float *ws, cudaStream_t st) {
-  int want = (dgamma || dbeta) ? 1 : 0;
+                  float *dgamma, float *dbeta, int acc, float *ws, cudaStream_t st,
+                  void *dx_act = nullptr, int64_t dxa_rs = 0, float *dx_colsum = nullptr) {
+  int want = (dgamma || dbeta || dx_colsum) ? 1 : 0;
   int64_t need_blocks = (rows + LN_WARPS - 1) / LN_WARPS;
   int nblk = (int)std::min<int64_t>(LN_BWD_BLOCKS, std::max<int64_t>(need_blocks, 1));
   const TDY *dyp = reinterpret_cast<const TDY *>(dy);
@@ -335,16 +347,22 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
   TDX *dxp = reinterpret_cast<TDX *>(dx);
   const bool vec = x_cs == 1 && dx_cs == 1 && (cols == 128 || cols == 256) && dy_rs % 4 == 0 &&
                    x_rs % 4 == 0 && dx_rs % 4 == 0 && aligned16(dy) && aligned16(x) &&
-                   aligned16(dx) && aligned16(gamma) && (!dres || aligned16(dres));
+                   aligned16(dx) && aligned16(gamma) && (!dres || aligned16(dres)) &&
+                   (!dx_act || (aligned16(dx_act) && dxa_rs % 4 == 0));
+  int nparts = 2;
   if (vec) {
+    bf16 *dxa = reinterpret_cast<bf16 *>(dx_act);
+    nparts = want ? (dx_colsum ? 3 : 2) : 0;
     if (cols == 128)
       ln_bwd_vec_kernel<TDY, TX, TDX, 1><<<nblk, LN_WARPS * 32, 0, st>>>(
-          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, ws, want);
+          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
     else
       ln_bwd_vec_kernel<TDY, TX, TDX, 2><<<nblk, LN_WARPS * 32, 0, st>>>(
-          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, ws, want);
+          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
     EVO_LAUNCHED("ln_bwd_vec_kernel");
   } else {
+    EVO_REQUIRE(!dx_act && !dx_colsum, EVO_EUNSUP,
+                "layernorm_bwd: fused dx copy / column sums need the vectorised layout");
     size_t smem = (size_t)LN_WARPS * 2 * cols * sizeof(float);
 #define L(Vn)                                                                                 \
   ln_bwd_kernel<TDY, TX, TDX, Vn><<<nblk, LN_WARPS * 32, smem, st>>>(                          \
@@ -358,8 +376,9 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
     EVO_LAUNCHED("ln_bwd_kernel");
   }
   if (want) {
-    const int outs = 2 * cols;
-    ln_param_reduce_kernel<<<(outs + 7) / 8, 256, 0, st>>>(nblk, cols, ws, dgamma, dbeta, acc);
+    const int outs = nparts * cols;
+    ln_param_reduce_kernel<<<(outs + 7) / 8, 256, 0, st>>>(nblk, cols, nparts, ws, dgamma, dbeta,
+                                                           dx_colsum, acc);
     EVO_LAUNCHED("ln_param_reduce_kernel");
   }
   return EVO_OK;
@@ -369,7 +388,7 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
 
 size_t layernorm_bwd_ws(int64_t rows, int cols) {
   (void)rows;
-  return (size_t)LN_BWD_BLOCKS * 2 * cols * sizeof(float);
+  return (size_t)LN_BWD_BLOCKS * 3 * cols * sizeof(float);
 }
 
 int layernorm_fwd(int tx, int ty, int64_t rows, int cols, const void *x, int64_t x_rs,
@@ -384,6 +403,25 @@ int layernorm_fwd(int tx, int ty, int64_t rows, int cols, const void *x, int64_t
   if (tx == EVO_BF16 && ty == EVO_BF16)
     return ln_fwd_launch<bf16, bf16>(rows, cols, x, x_rs, x_cs, gamma, beta, y, y_rs, mean, rstd, eps, st);
   return ln_fwd_launch<bf16, float>(rows, cols, x, x_rs, x_cs, gamma, beta, y, y_rs, mean, rstd, eps, st);
+}
+
+int layernorm_bwd_ex(int64_t rows, int cols, const float *dy, const void *x, int tx,
+                     const float *mean, const float *rstd, const float *gamma, const float *dres,
+                     float *dx, void *dx_act, float *dgamma, float *dbeta, float *dx_colsum,
+                     void *ws, size_t ws_bytes, cudaStream_t st) {
+  EVO_REQUIRE(cols == 128 || cols == 256, EVO_EUNSUP,
+              "layernorm_bwd_ex: cols=%d (fused path: 128 or 256)", cols);
+  EVO_REQUIRE(ws && ws_bytes >= layernorm_bwd_ws(rows, cols), EVO_EARG,
+              "layernorm_bwd_ex: workspace too small");
+  if (rows == 0) return EVO_OK;
+  float *w = reinterpret_cast<float *>(ws);
+  if (tx == EVO_F32)
+    return ln_bwd_launch<float, float, float>(rows, cols, dy, cols, x, cols, 1, mean, rstd, gamma,
+                                              dres, dx, cols, 1, dgamma, dbeta, 0, w, st, dx_act,
+                                              cols, dx_colsum);
+  return ln_bwd_launch<float, bf16, float>(rows, cols, dy, cols, x, cols, 1, mean, rstd, gamma,
+                                           dres, dx, cols, 1, dgamma, dbeta, 0, w, st, dx_act, cols,
+                                           dx_colsum);
 }
 
 int layernorm_bwd(int tdy, int tx, int tdx, int64_t rows, int cols, const void *dy, int64_t dy_rs,

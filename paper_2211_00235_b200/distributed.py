@@ -161,14 +161,16 @@ class CudaExec:
         E, st = self.E, self.st
         ctxs, co = ctx
         G = st.grads[blk].packed
+        e0 = E.msa_emit(G)
         dm3 = E.opm_bwd(st.P, f"blk{blk}.opm", st.packs[blk]["opm"], G["opm"], co, d_o,
-                        E.cast_act(d_o, self.act), dm, self.cfg, self.act)
-        return E.msa_branch_bwd(st.P, blk, st.packs[blk], G, ctxs, dm3, self.cfg, self.act)
+                        E.cast_act(d_o, self.act), dm, self.cfg, self.act, emit=e0)
+        return E.msa_branch_bwd(st.P, blk, st.packs[blk], G, ctxs, dm3, self.cfg, self.act,
+                                handoff=e0)
 
     def pair_bwd(self, blk, ctx, dz):
         E, st = self.E, self.st
         return E.pair_branch_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctx, dz,
-                                 self.cfg, self.act)
+                                 self.cfg, self.act, dz_act=E.cast_act(dz, self.act))
 
     def full_step(self, m, z):
         from .schedules import full_step

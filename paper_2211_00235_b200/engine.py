@@ -190,6 +190,41 @@ def subop_grad_numel(name, cfg) -> int:
 
 
 # ---------------------------------------------------------------------------
+# gradient hand-off between consecutive sub-op backwards
+# ---------------------------------------------------------------------------
+
+def _ln_bwd_out(dy, x, rows, cols, mu, rs, gamma, dgamma, dbeta, dres, act, emit, dev):
+    """LayerNorm backward producing a sub-op's input gradient dx (fp32).
+    emit (a dict with the consumer's output-bias gradient slot under "bias",
+    or None): when the layout allows, the same kernel also writes dx's bf16
+    copy (emit["act"], the consumer's GEMM operand) and dx's column sums
+    into emit["bias"] (emit["done"] = True), so the consumer skips its cast
+    and its bias-gradient column sum."""
+    dx = _empty((rows, cols), F32, dev)
+    if (emit is not None and cols in (128, 256) and dy.dtype == F32 and dy.is_contiguous()
+            and x.is_contiguous() and (dres is None or dres.is_contiguous())):
+        dxa = _empty((rows, cols), act, dev) if act != F32 else None
+        K.layernorm_bwd_ex(dy, x, rows, cols, mu, rs, gamma, dx, dgamma, dbeta, dres=dres,
+                           dx_act=dxa, dx_colsum=emit["bias"])
+        emit["act"] = dxa if dxa is not None else dx
+        emit["done"] = True
+        return dx
+    K.layernorm_bwd(dy, x, rows, cols, mu, rs, gamma, dx, dgamma, dbeta, dres=dres)
+    return dx
+
+
+def _grad_in(dx_new, rows, cols, act, dev, handoff):
+    """(bf16 operand copy of an incoming gradient, bias colsum already done?)"""
+    if handoff is not None and handoff.get("act") is not None:
+        return handoff["act"], bool(handoff.get("done"))
+    if act == F32:
+        return dx_new, False
+    dxa = _empty((rows, cols), act, dev)
+    K.copy2d(dx_new, rows, cols, dxa, s_rs=cols, d_rs=cols)
+    return dxa, False
+
+
+# ---------------------------------------------------------------------------
 # geometry of the four attentions (rows of the position-major buffers)
 # ---------------------------------------------------------------------------
 
@@ -253,18 +288,19 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     return x_new, ctx
 
 
-def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act):
-    """Returns (dx [rows, c_io] fp32, dz_row or None)."""
+def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None):
+    """Returns (dx [rows, c_io] fp32, dz_row or None).  handoff: the emit
+    dict of the producer of dx_new (see _ln_bwd_out); emit: this sub-op's."""
     dev = dx_new.device
     h, hc, ch = cfg.h, cfg.hc, cfg.c_head
     nb, L, rb, rl, rows = attn_geometry(name, cfg)
     c_io = dx_new.shape[-1]
     r2 = cfg.r * cfg.r
-    dxa = _empty((rows, c_io), act, dev)
-    K.copy2d(dx_new, rows, c_io, dxa, s_rs=c_io, d_rs=c_io)
+    dxa, bias_done = _grad_in(dx_new, rows, c_io, act, dev, handoff)
     # out-projection
     K.linear_dw(ctx["gm"], rows, hc, dxa, c_io, G["Wo"], c_io)
-    K.colsum(dx_new, rows, c_io, G["bo"])
+    if not bias_done:
+        K.colsum(dx_new, rows, c_io, G["bo"])
     dgm = _empty((rows, hc), act, dev)
     K.linear_dx(dxa, rows, c_io, pk["Wo"], c_io, hc, dgm)
     # attention core (+ gate) backward
@@ -299,9 +335,8 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act):
         else:
             K.gemm(Mat(dbias_a, 1, r2), Mat(pk["Wb"], h, 1), Mat(dxh, cfg.c_z, 1), r2,
                    cfg.c_z, h, accumulate=True)
-    dx = _empty((rows, c_io), F32, dev)
-    K.layernorm_bwd(dxh, ctx["x"], rows, c_io, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"], dx,
-                    G["ln_g"], G["ln_b"], dres=dx_new if ctx["resid"] else None)
+    dx = _ln_bwd_out(dxh, ctx["x"], rows, c_io, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                     G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
     return dx, dz_row
 
 
@@ -324,14 +359,14 @@ def transition_fwd(P, px, pk, x, cfg, act, resid=True):
     return x_new, dict(x=x, xh=xh, mu=mu, rs=rs, hid=hid, resid=resid)
 
 
-def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act):
+def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None):
     dev = dx_new.device
     rows, cx = dx_new.shape[0], dx_new.shape[1]
     tc = cfg.t_factor * cx
-    dxa = _empty((rows, cx), act, dev)
-    K.copy2d(dx_new, rows, cx, dxa, s_rs=cx, d_rs=cx)
+    dxa, bias_done = _grad_in(dx_new, rows, cx, act, dev, handoff)
     K.linear_dw(ctx["hid"], rows, tc, dxa, cx, G["W2"], cx)
-    K.colsum(dx_new, rows, cx, G["b2"])
+    if not bias_done:
+        K.colsum(dx_new, rows, cx, G["b2"])
     dhid = _empty((rows, tc), act, dev)
     K.linear_dx(dxa, rows, cx, pk["W2"], cx, tc, dhid)
     K.relu_bwd(dhid, ctx["hid"], dhid, rows * tc)
@@ -339,10 +374,8 @@ def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act):
     K.colsum(dhid, rows, tc, G["b1"])
     dxh = _empty((rows, cx), F32, dev)
     K.linear_dx(dhid, rows, tc, pk["W1"], tc, cx, dxh)
-    dx = _empty((rows, cx), F32, dev)
-    K.layernorm_bwd(dxh, ctx["x"], rows, cx, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"], dx,
-                    G["ln_g"], G["ln_b"], dres=dx_new if ctx["resid"] else None)
-    return dx
+    return _ln_bwd_out(dxh, ctx["x"], rows, cx, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                       G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
 
 
 # ---------------------------------------------------------------------------
@@ -371,7 +404,7 @@ def opm_fwd(P, px, pk, m, z_pair, cfg, act):
     return z_out, dict(m=m, mh=mh, mu=mu, rs=rs, ab=ab, o=o)
 
 
-def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act):
+def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None):
     """Returns dm = dm_res + d(opm)/dm."""
     dev = dz_out.device
     s, r, cm, c, cz = cfg.s, cfg.r, cfg.c_m, cfg.c_opm, cfg.c_z
@@ -401,10 +434,8 @@ def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act):
     K.gemm(Mat(dab[0], c, 1), Mat(pk["Wab"], 2 * c, 1), Mat(dmh, cm, 1), rows, cm, c)
     K.gemm(Mat(dab[1], c, 1), Mat(pk["Wab"], 2 * c, 1, off=c), Mat(dmh, cm, 1), rows, cm, c,
            accumulate=True)
-    dm = _empty((rows, cm), F32, dev)
-    K.layernorm_bwd(dmh, ctx["m"], rows, cm, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"], dm,
-                    G["ln_g"], G["ln_b"], dres=dm_res)
-    return dm
+    return _ln_bwd_out(dmh, ctx["m"], rows, cm, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                       G["ln_g"], G["ln_b"], dm_res, act, emit, dev)
 
 
 # ---------------------------------------------------------------------------
@@ -544,27 +575,43 @@ def pair_branch_fwd(P, blk, pk, z, cfg, act):
     return z2, ctxs
 
 
-def pair_branch_bwd(P, blk, pk, G, ctxs, dz, cfg, act):
-    """dz: grad of the pair-track output; returns dz_pair (grad of z_in
-    through the pair track, residual included)."""
+def pair_branch_bwd(P, blk, pk, G, ctxs, dz, cfg, act, dz_act=None):
+    """dz: grad of the pair-track output (dz_act: its bf16 copy, if made);
+    returns dz_pair (grad of z_in through the pair track, residual included).
+    Each LayerNorm backward hands its output's bf16 copy and column sums to
+    the next sub-op (_ln_bwd_out)."""
+    h0 = None if dz_act is None else dict(act=dz_act, done=False)
+    e1 = dict(bias=G["tri_attn_end"]["bo"])
     dz = transition_bwd(P, f"blk{blk}.pair_transition", pk["pair_transition"],
-                        G["pair_transition"], ctxs["pair_transition"], dz, cfg, act)
-    for n in ("tri_attn_end", "tri_attn_start"):
-        dz, _ = attn_bwd(n, P, f"blk{blk}.{n}", pk[n], G[n], ctxs[n], dz, cfg, act)
+                        G["pair_transition"], ctxs["pair_transition"], dz, cfg, act,
+                        handoff=h0, emit=e1)
+    e2 = dict(bias=G["tri_attn_start"]["bo"])
+    dz, _ = attn_bwd("tri_attn_end", P, f"blk{blk}.tri_attn_end", pk["tri_attn_end"],
+                     G["tri_attn_end"], ctxs["tri_attn_end"], dz, cfg, act, handoff=e1, emit=e2)
+    dz, _ = attn_bwd("tri_attn_start", P, f"blk{blk}.tri_attn_start", pk["tri_attn_start"],
+                     G["tri_attn_start"], ctxs["tri_attn_start"], dz, cfg, act, handoff=e2)
     for n in ("tri_mult_in", "tri_mult_out"):
         dz = trimul_bwd(P, f"blk{blk}.{n}", pk[n], G[n], ctxs[n], dz, cfg, act)
     return dz
 
 
-def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act):
-    """dm: grad of the MSA-track output (incl. the OPM contribution);
-    returns (dm_in, dz_row)."""
+def msa_emit(G):
+    """Hand-off slot for the OPM backward's output (-> msa_transition)."""
+    return dict(bias=G["msa_transition"]["b2"])
+
+
+def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None):
+    """dm: grad of the MSA-track output (incl. the OPM contribution; handoff:
+    the OPM backward's emit dict); returns (dm_in, dz_row)."""
+    e1 = dict(bias=G["col_attn"]["bo"])
     dm = transition_bwd(P, f"blk{blk}.msa_transition", pk["msa_transition"],
-                        G["msa_transition"], ctxs["msa_transition"], dm, cfg, act)
+                        G["msa_transition"], ctxs["msa_transition"], dm, cfg, act,
+                        handoff=handoff, emit=e1)
+    e2 = dict(bias=G["row_attn"]["bo"])
     dm, _ = attn_bwd("col_attn", P, f"blk{blk}.col_attn", pk["col_attn"], G["col_attn"],
-                     ctxs["col_attn"], dm, cfg, act)
+                     ctxs["col_attn"], dm, cfg, act, handoff=e1, emit=e2)
     dm, dz_row = attn_bwd("row_attn", P, f"blk{blk}.row_attn", pk["row_attn"], G["row_attn"],
-                          ctxs["row_attn"], dm, cfg, act)
+                          ctxs["row_attn"], dm, cfg, act, handoff=e2)
     return dm, dz_row
 
 
@@ -589,10 +636,11 @@ def block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act):
     """Returns (dm_in, dz_in) with dz_in = dz_pair + dz_row: the same two
     operands, in the same order, as the BP allreduce (src/comm.py:206-210)."""
     dz_act = cast_act(dz_out, act)
+    e0 = msa_emit(G)
     dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act, dm_out,
-                  cfg, act)
-    dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act)
-    dm_in, dz_row = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm3, cfg, act)
+                  cfg, act, emit=e0)
+    dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act, dz_act=dz_act)
+    dm_in, dz_row = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm3, cfg, act, handoff=e0)
     dz_in = torch.empty_like(dz_pair)
     K.add(dz_pair, dz_row, dz_in)
     return dm_in, dz_in

@@ -173,6 +173,20 @@ def layernorm_bwd(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma, db
           "evo_layernorm_bwd")
 
 
+def layernorm_bwd_ex(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma, dbeta, *,
+                     dres=None, dx_act=None, dx_colsum=None):
+    """LayerNorm backward (contiguous fp32 dy/dx, cols 128|256) that also
+    emits a bf16 copy of dx and/or its column sums (the next sub-op's GEMM
+    operand and output-bias gradient)."""
+    L = lib()
+    nbytes = L.evo_layernorm_bwd_workspace_bytes(rows, cols)
+    ws = _ws(nbytes, dx.device)
+    check(L.evo_layernorm_bwd_ex(dt(x), rows, cols, ptr(dy), ptr(x), ptr(mean), ptr(rstd),
+                                 ptr(gamma), ptr(dres), ptr(dx), ptr(dx_act), ptr(dgamma),
+                                 ptr(dbeta), ptr(dx_colsum), ptr(ws), nbytes, stream()),
+          "evo_layernorm_bwd_ex")
+
+
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
               sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
               dgm=None, dproj=None, dbias=None):
