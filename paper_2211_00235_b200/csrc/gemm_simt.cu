@@ -185,13 +185,42 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(EpiArgs e, int64_t M
   }
 }
 
+// Few partials: one thread per 4 consecutive outputs (16-byte loads, the
+// split loads independent and in flight), partials summed in split order.
+__global__ void __launch_bounds__(256) splitk_reduce_vec_kernel(EpiArgs e, int64_t M, int64_t N,
+                                                                int64_t B2, int64_t nbatch,
+                                                                int split,
+                                                                const float *__restrict__ partial) {
+  const int64_t total = nbatch * M * N;
+  const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t idx = 4 * q;
+  if (idx >= total) return;
+  float4 v = __ldg(reinterpret_cast<const float4 *>(partial + idx));
+#pragma unroll 4
+  for (int s = 1; s < split; ++s) {
+    const float4 w = __ldg(reinterpret_cast<const float4 *>(partial + (int64_t)s * total + idx));
+    v.x += w.x; v.y += w.y; v.z += w.z; v.w += w.w;
+  }
+  const int64_t n = idx % N;
+  const int64_t m = (idx / N) % M;
+  const int64_t bidx = idx / (M * N);
+  const int64_t b1 = bidx / B2, b2 = bidx % B2;
+  const int64_t rb = b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m);
+  const float t[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+  for (int j = 0; j < 4; ++j) epi_store(e, rb + e.cmap.col(n + j), epi_value(e, n + j, t[j]));
+}
+
 }  // namespace
 
 int gemm_splitk_reduce(const evo_gemm_desc *d, int split, const float *partial,
                        cudaStream_t st) {
   const int64_t total = d->B1 * d->B2 * d->M * d->N;
   EVO_REQUIRE((total + 31) / 32 < (1ll << 31), EVO_EDIM, "evo_gemm: split-K output too large");
-  if (total / 32 < 2 * (int64_t)num_sms() && split > 32) {
+  if (split <= 32 && d->N % 4 == 0 && (reinterpret_cast<uintptr_t>(partial) & 15) == 0) {
+    splitk_reduce_vec_kernel<<<(unsigned)((total / 4 + 255) / 256), 256, 0, st>>>(
+        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+  } else if (total / 32 < 2 * (int64_t)num_sms() && split > 32) {
     splitk_reduce_kernel<8><<<(unsigned)((total + 7) / 8), 256, 0, st>>>(
         epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
   } else {
