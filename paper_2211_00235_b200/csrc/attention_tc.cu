@@ -472,6 +472,242 @@ __device__ __forceinline__ uint32_t quarter_col(int ks, int KQ) {
   return (uint32_t)((k / KQ) * KQ + (k % KQ) / 2);
 }
 
+// ================================================================= fwd, v2
+// Lp == 256.  Four threads per query row (warps w, w+4, w+8, w+12 share the
+// row's TMEM lane; quarter qr owns keys [64qr, 64qr+64)), so each thread
+// keeps its 64 logits x = S*scale*log2e + bias*log2e in registers between
+// the max and the exp pass: one TMEM read and one bias read per element.
+// Two TMEM row slots [256s, 256s+256) hold S, then P (bf16 pairs, packed in
+// place into each quarter's first 32 columns), then O at col 32.  Warp 16
+// issues: the PV MMA of row b once all 16 warps packed P(b), the S MMA of
+// row b+2 once row b's epilogue has read O, the TMA loads of row b+2 once
+// PV(b) completed.  Row b's epilogue runs between row b+1's two passes, so
+// the PV MMA of b and the S MMA of b+2 overlap elementwise work.
+template <int D, int BIASMODE>
+__global__ void __launch_bounds__(544, 1)
+attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
+                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
+                    const AttnTcArgs a) {
+  constexpr uint32_t TILE = QT * Sw<D>::bytes;
+  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t ROWB = TILE + 2 * FULL;  // Q | K | V of one batch row
+  constexpr bool TB = BIASMODE == 2;
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
+  uint8_t *sBias = smem_raw;
+  uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
+  float *sMax = reinterpret_cast<float *>(sRow + 2 * ROWB);  // [parity][quarter][128]
+  float *sSum = sMax + 2 * 4 * 128;
+  // 0 bias, 1-2 row data, 3-4 S MMA done, 5-6 PV MMA done, 7-8 P packed
+  // (16 warps), 9-10 epilogue read O (16 warps)   [all by row parity]
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sSum + 2 * 4 * 128);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 11);
+
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int t = (warp & 3) * 32 + lane;  // query row (TMEM lane)
+  const int qr = (warp >> 2) & 3;        // key quarter
+  const int q0 = blockIdx.x * QT, h = blockIdx.y;
+  const int L = a.L;
+  const int q = q0 + t;
+  const bool qv = q < L;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+
+  if (tid == 512) {
+    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i >= 7) ? 16 : 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, 256);
+  }
+  if (warp == 0) tmem_alloc(tslot, 512);
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tslot;
+  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
+
+  if (warp == 16) {
+    // ------------------------------------------------------------ issuer
+    {
+    const uint32_t idesc_s = idesc_bf16(128, 256, false, false);
+    const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    auto load_row = [&](int64_t r) {
+      uint8_t *rb = rowbuf(r);
+      uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+      mbar_expect_tx(bar, ROWB);
+      tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
+      tma_load_4d(rb + TILE, &mK, bar, 0, 0, (int)r, h);
+      tma_load_4d(rb + TILE + FULL, &mV, bar, 0, 0, (int)r, h);
+    };
+    auto issue_s = [&](int64_t r) {
+      const int p = (int)((r - b_lo) & 1);
+      const uint32_t ph = (uint32_t)(((r - b_lo) >> 1) & 1);
+      mbar_wait(&bars[1 + p], ph);
+      fence_after();
+      const uint32_t sQ = smem_u32(rowbuf(r)), sK = sQ + TILE;
+#pragma unroll
+      for (int ks = 0; ks < D / 16; ++ks)
+        umma_bf16_el(tmem + 256 * p, desc_kmajor_tile<D>(sQ, ks), desc_kmajor_tile<D>(sK, ks),
+                     idesc_s, ks > 0);
+      umma_commit_el(&bars[3 + p]);
+    };
+    if (b_lo < b_hi) {
+      if (lane == 0) {
+        load_row(b_lo);
+        if (b_lo + 1 < b_hi) load_row(b_lo + 1);
+      }
+      __syncwarp();
+      issue_s(b_lo);
+      if (b_lo + 1 < b_hi) issue_s(b_lo + 1);
+      for (int64_t r = b_lo; r < b_hi; ++r) {
+        const int p = (int)((r - b_lo) & 1);
+        const uint32_t ph = (uint32_t)(((r - b_lo) >> 1) & 1);
+        mbar_wait(&bars[7 + p], ph);  // P(r) packed by all 16 warps
+        fence_after();
+        const uint32_t sV = smem_u32(rowbuf(r)) + TILE + FULL;
+        const uint32_t slot = tmem + 256 * p;
+#pragma unroll
+        for (int ks = 0; ks < 16; ++ks)
+          umma_bf16_ts_el(slot + 32, slot + 64 * (ks >> 2) + 8 * (ks & 3),
+                          desc_mnmajor_tile<D>(sV, ks), idesc_o, ks > 0);
+        umma_commit_el(&bars[5 + p]);
+        if (r + 2 < b_hi) {
+          mbar_wait(&bars[5 + p], ph);  // PV(r) done: row r's smem is free
+          if (lane == 0) load_row(r + 2);
+          __syncwarp();
+          mbar_wait(&bars[9 + p], ph);  // epilogue(r) read O: slot p is free
+          fence_after();
+          issue_s(r + 2);
+        }
+      }
+    }
+    __syncwarp();
+    }
+  } else {
+    // ------------------------------------------------------------ softmax
+    const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    if (BIASMODE) {
+      mbar_wait(&bars[0], 0);
+      scale_tile(sBias, 8 * 16384 / 16, 512);
+      named_bar_sync(1, 512);
+    }
+    const float sc_l2 = a.scale * LOG2E;
+    uint4 gq_prev = make_uint4(0u, 0u, 0u, 0u);
+    float mx_prev = 0.f;
+    auto epilogue = [&](int64_t rr) {  // O of batch row rr -> o, gm, lse
+      const int p = (int)((rr - b_lo) & 1);
+      mbar_wait(&bars[5 + p], (uint32_t)(((rr - b_lo) >> 1) & 1));
+      fence_after();
+      uint32_t ov[8];
+      constexpr int QD = D / 4;
+      if constexpr (QD == 8) {
+        tmem_ld8_nw(lane_addr + 256 * p + 32 + 8 * qr, ov);
+      } else {
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                     : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3])
+                     : "r"(lane_addr + 256 * p + 32 + 4 * qr));
+      }
+      tmem_wait_ld();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[9 + p]);  // slot p's O read
+      const float *ss = sSum + p * 512;
+      const float sum = (ss[t] + ss[128 + t]) + (ss[256 + t] + ss[384 + t]);
+      if (qv) {
+        const float inv = 1.f / sum;
+        const int64_t ooff = rr * a.o_sb + (int64_t)q * a.o_sl + h * D + qr * QD;
+        const uint32_t *gw = reinterpret_cast<const uint32_t *>(&gq_prev);
+        uint32_t o2[4], g2v[4];
+#pragma unroll
+        for (int j = 0; j < QD / 2; ++j) {
+          const float o0 = __uint_as_float(ov[2 * j]) * inv;
+          const float o1 = __uint_as_float(ov[2 * j + 1]) * inv;
+          const float2 g2 = unpack2(gw[j]);
+          o2[j] = pack2(o0, o1);
+          g2v[j] = pack2(g2.x * o0, g2.y * o1);
+        }
+        if constexpr (QD == 8) {
+          *reinterpret_cast<uint4 *>(a.o + ooff) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+          *reinterpret_cast<uint4 *>(a.gm + ooff) = make_uint4(g2v[0], g2v[1], g2v[2], g2v[3]);
+        } else {
+          *reinterpret_cast<uint2 *>(a.o + ooff) = make_uint2(o2[0], o2[1]);
+          *reinterpret_cast<uint2 *>(a.gm + ooff) = make_uint2(g2v[0], g2v[1]);
+        }
+        if (qr == 0) a.lse[(rr * a.H + h) * (int64_t)L + q] = mx_prev * (1.f / LOG2E) + logf(sum);
+      }
+    };
+    for (int64_t r = b_lo; r < b_hi; ++r) {
+      const int p = (int)((r - b_lo) & 1);
+      const uint32_t ph = (uint32_t)(((r - b_lo) >> 1) & 1);
+      const uint32_t slot = lane_addr + 256 * p;
+      const int kb = 64 * qr;
+      // gate slice of this row (consumed by its epilogue, one row later)
+      // (volatile: issued here, a row ahead of its use, not sunk to the use)
+      uint4 gq = make_uint4(0u, 0u, 0u, 0u);
+      if (qv) {
+        const bf16 *gp = a.g + r * a.sb + (int64_t)q * a.sl + h * D + qr * (D / 4);
+        if constexpr (D == 32) {
+          asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                       : "=r"(gq.x), "=r"(gq.y), "=r"(gq.z), "=r"(gq.w)
+                       : "l"(gp));
+        } else {
+          asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(gq.x), "=r"(gq.y) : "l"(gp));
+        }
+      }
+      mbar_wait(&bars[3 + p], ph);
+      fence_after();
+      // pass 1: logits of this thread's 64 keys -> registers, local max
+      float x[64];
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t v[32];
+        tmem_ld32(slot + kb + 32 * c, v);
+        float bb[32];
+        if (BIASMODE) bias_row32<TB>(sBias, t, kb + 32 * c, bb);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          float xx = __uint_as_float(v[j]) * sc_l2;
+          if (BIASMODE) xx += bb[j];
+          if (kb + 32 * c + j >= L) xx = -INFINITY;
+          x[32 * c + j] = xx;
+          mx = fmaxf(mx, xx);
+        }
+      }
+      float *sm_ = sMax + p * 512;
+      sm_[qr * 128 + t] = mx;
+      named_bar_sync(2 + (warp & 3), 128);  // the row's four quarters
+      mx = fmaxf(fmaxf(sm_[t], sm_[128 + t]), fmaxf(sm_[256 + t], sm_[384 + t]));
+      // the previous row's epilogue (its PV MMA overlapped pass 1)
+      if (r > b_lo) epilogue(r - 1);
+      // pass 2: p = exp2(x - max) -> bf16 pairs in this quarter's first 32 cols
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) {
+          const float p0 = ex2(x[32 * c + 2 * j] - mx);
+          const float p1 = ex2(x[32 * c + 2 * j + 1] - mx);
+          sum += p0 + p1;
+          pk[j] = pack2(p0, p1);
+        }
+        tmem_st16(slot + kb + 16 * c, pk);
+      }
+      sSum[p * 512 + qr * 128 + t] = sum;
+      gq_prev = gq;
+      mx_prev = mx;
+      tmem_st_wait();
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bars[7 + p]);
+    }
+    if (b_lo < b_hi) epilogue(b_hi - 1);
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc(tmem, 512);
+}
+
 // ======================================================================= dq
 // CTA = (128-query tile, head, chunk of batch rows), 512 threads: 4 threads
 // per query row, thread quarter `qr` owns keys [qr*KQ, (qr+1)*KQ) (KQ=Lp/4)
@@ -1601,8 +1837,16 @@ int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   nch = (d->nb + a.chunk - 1) / a.chunk;
   const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) +
                       2 * ((size_t)QT * 2 * D + 2 * 256 * 2 * D) + 128;
-  EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D, BM_>));
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
+  if (a.Lp == 256 && D <= 32 && !g_attn_no_pipe) {
+    const size_t smem2 = (BM_ ? BIAS_BYTES : 0) + 2 * ((size_t)QT * 2 * D + 2 * 256 * 2 * D) +
+                         2 * 2 * 4 * 128 * 4 + 11 * 8 + 16;
+    EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_>));
+    attn_fwd_tc2_kernel<D, BM_><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+    EVO_LAUNCHED("attn_fwd_tc2_kernel");
+    return EVO_OK;
+  }
+  EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D, BM_>));
   attn_fwd_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_fwd_tc_kernel");
   return EVO_OK;
