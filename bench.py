@@ -228,15 +228,22 @@ def run_native(args):
         graph = torch.cuda.CUDAGraph()
         with torch.cuda.graph(graph):
             step(m_s, z_s)
-        # end-to-end graph: pinned H2D inputs -> step -> loss D2H
-        graph_e2e = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph_e2e):
-            m_s.copy_(m_h, non_blocking=True)
-            z_s.copy_(z_h, non_blocking=True)
-            out_e = step(m_s, z_s)
-            loss_h.copy_(out_e[2].reshape(1), non_blocking=True)
+        # end-to-end: two input buffer sets, one graph each (step + loss D2H);
+        # the H2D of step i+1's inputs runs on a copy stream while step i
+        # computes (a double-buffered input pipeline)
+        graph_e2e = []
+        e2e_in = []
+        for _ in range(2):
+            mb, zb = m_d.clone(), z_d.clone()
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                out_e = step(mb, zb)
+                loss_h.copy_(out_e[2].reshape(1), non_blocking=True)
+            graph_e2e.append(g)
+            e2e_in.append((mb, zb))
         graph.replay()
-        graph_e2e.replay()
+        for g in graph_e2e:
+            g.replay()
         torch.cuda.synchronize()
 
     def timed(fn, k):
@@ -299,14 +306,78 @@ def run_native(args):
             print(f"{tms / args.steps:8.3f} ms/step {n // args.steps:3d}x "
                   f"{fl / (tms / 1e3) / 1e12 if tms else 0:8.1f} TF/s  {key}", file=sys.stderr)
 
-    # end-to-end: pinned host inputs -> device, step, loss -> host
+    # end-to-end: pinned host inputs -> device, step, loss -> host, every step
     def e2e_eager():
         m_e = m_h.to(dev, non_blocking=True)
         z_e = z_h.to(dev, non_blocking=True)
         out = step(m_e, z_e)
         loss_h.copy_(out[2].reshape(1), non_blocking=True)
 
-    ms_e2e = timed(graph_e2e.replay if use_graph else e2e_eager, args.steps)
+    def e2e_pipelined(k):
+        comp = torch.cuda.current_stream()
+        copy = torch.cuda.Stream()
+        h2d = [torch.cuda.Event() for _ in range(2)]
+        free = [torch.cuda.Event() for _ in range(2)]
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record(comp)
+        copy.wait_event(a0)
+
+        def load(i):
+            with torch.cuda.stream(copy):
+                if i >= 2:
+                    copy.wait_event(free[i % 2])  # step i-2 done with this buffer set
+                mb, zb = e2e_in[i % 2]
+                mb.copy_(m_h, non_blocking=True)
+                zb.copy_(z_h, non_blocking=True)
+                h2d[i % 2].record(copy)
+
+        load(0)
+        for i in range(k):
+            if i + 1 < k:
+                load(i + 1)
+            comp.wait_event(h2d[i % 2])
+            graph_e2e[i % 2].replay()
+            free[i % 2].record(comp)
+        a1.record(comp)
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / k
+
+    if use_graph:
+        e2e_pipelined(2)
+        ms_e2e = e2e_pipelined(args.steps)
+        e2e_mode = "double-buffered H2D on a copy stream overlapping the previous step"
+    else:
+        ms_e2e = timed(e2e_eager, args.steps)
+        e2e_mode = "serial H2D -> step -> D2H"
+
+    # roofline timing: one step's launches of each kernel family re-issued
+    # back to back inside a CUDA graph (device time, no host gaps)
+    fam_graph = {}
+    if use_graph:
+        rec = []
+        K.RECORD = rec
+        step(m_d, z_d)
+        K.RECORD = None
+        torch.cuda.synchronize()
+        for famname in sorted({r[0] for r in rec}):
+            calls = [r for r in rec if r[0] == famname]
+            g = torch.cuda.CUDAGraph()
+            side = torch.cuda.Stream()
+            side.wait_stream(torch.cuda.current_stream())
+            with torch.cuda.stream(side):
+                for _, _, fn, _ in calls:
+                    fn()
+            torch.cuda.current_stream().wait_stream(side)
+            with torch.cuda.graph(g):
+                for _, _, fn, _ in calls:
+                    fn()
+            g.replay()
+            reps = max(3, args.steps)
+            t_ms = timed(g.replay, reps)
+            fam_graph[famname] = (sum(c[1] for c in calls), t_ms, len(calls))
+        del rec
 
     if rank != 0:
         if world > 1:
@@ -321,7 +392,19 @@ def run_native(args):
     peak, peak_sus, hbm, src = peaks()
     step_tflops = flops_step * dp / (ms / 1e3) / 1e12
     roof = None
-    if fam:
+    if fam_graph:
+        top = max(fam_graph, key=lambda k: fam_graph[k][1])
+        fl, tms, n = fam_graph[top]
+        achieved = fl / (tms / 1e3) / 1e12
+        roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "peak_source": src, "launches": n, "share_of_step": tms / ms,
+                "timing": "CUDA events around one step's launches of this family, "
+                          "re-issued back to back in a CUDA graph on the launching stream"}
+        breakdown = {k: {"tflops": v[0] / (v[1] / 1e3) / 1e12, "ms_per_step": v[1],
+                         "launches_per_step": v[2], "share_of_step": v[1] / ms}
+                     for k, v in fam_graph.items()}
+    elif fam:
         top = max(fam, key=lambda k: fam[k][1])
         fl, tms, n = fam[top]
         achieved = fl / (tms / 1e3) / 1e12
@@ -330,9 +413,11 @@ def run_native(args):
                 "peak_source": src, "launches": n,
                 "share_of_step": tms / (ms_eager * args.steps),
                 "timing": "CUDA events around each launch on its stream, eager pass"}
-    breakdown = {k: {"tflops": (v[0] / (v[1] / 1e3) / 1e12) if v[1] > 0 else None,
-                     "ms_per_step": v[1] / args.steps, "launches_per_step": v[2] / args.steps}
-                 for k, v in fam.items()}
+    if not fam_graph:
+        breakdown = {k: {"tflops": (v[0] / (v[1] / 1e3) / 1e12) if v[1] > 0 else None,
+                         "ms_per_step": v[1] / args.steps,
+                         "launches_per_step": v[2] / args.steps}
+                     for k, v in fam.items()}
     cpu = None
     if not args.no_cpu_baseline:
         t_cpu, parts = cpu_sample(kw)
@@ -355,7 +440,8 @@ def run_native(args):
         "step_tflops": step_tflops, "step_frac_of_peak": step_tflops / peak,
         "roofline": roof, "kernels": breakdown, "cpu_baseline": cpu,
         "e2e": {"value": samples / (ms_e2e / 1e3), "unit": "samples/s",
-                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4},
+                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e,
+                "mode": e2e_mode},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
         "launch_mode": "cuda_graph" if use_graph else "eager", "ms_per_step_eager": ms_eager,
         "clocks": clk,

@@ -56,13 +56,8 @@ struct AttnTcArgs {
   bf16 *dq, *dk, *dv;  // proj-gradient buffer (q's strides)
   float *dbias_part;
   int64_t chunk;
-  long long *trace;  // EVO_ATTN_TRACE=1: per-unit clock64 stamps of CTA 0
 };
-__device__ __forceinline__ long long clk() {
-  long long c;
-  asm volatile("mov.u64 %0, %%clock64;" : "=l"(c));
-  return c;
-}
+
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
@@ -1664,13 +1659,9 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
           Dq_n = a.Dq[((r + 1) * a.H + h) * (int64_t)L + q];
         }
       }
-      const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 &&
-                      tid == 0 && u < 64;
-      if (tr) a.trace[u * 8 + 0] = clk();
       mbar_wait(&bars[3 + reg], (ph3 >> reg) & 1u);
       ph3 ^= 1u << reg;
       fence_after();
-      if (tr) a.trace[u * 8 + 1] = clk();
       const uint32_t rb = lane_addr + reg * 64;
       const int c0 = qr * 8;
       const int kb = ui * UW + c0;  // first key of this thread's 8
@@ -1707,7 +1698,6 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&bars[8 + (u & 1)]);
-      if (tr) a.trace[u * 8 + 2] = clk();
       reg = reg == 2 ? 0 : reg + 1;
     }
     if (nrows > 0) {
@@ -1775,7 +1765,7 @@ AttnTcArgs make_args(const evo_attn_desc *d) {
   a.dO = nullptr; a.Dq = nullptr;
   a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
   a.dv = reinterpret_cast<bf16 *>(d->dv);
-  a.dbias_part = nullptr; a.chunk = 1; a.trace = nullptr;
+  a.dbias_part = nullptr; a.chunk = 1;
   return a;
 }
 
@@ -1934,29 +1924,8 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         2048 + 14 * 8 + 16;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    static long long *trace_buf = nullptr;
-    static const bool want_trace = getenv("EVO_ATTN_TRACE") && getenv("EVO_ATTN_TRACE")[0] == '1';
-    if (want_trace) {
-      if (!trace_buf) cudaMalloc(&trace_buf, 64 * 8 * sizeof(long long));
-      cudaMemsetAsync(trace_buf, 0, 64 * 8 * sizeof(long long), st);
-      a.trace = trace_buf;
-    }
     attn_bwd_dq_pipe_kernel<D, BM_><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
-    a.trace = nullptr;
-    if (want_trace) {  // debugging aid: per-unit clock64 stamps of CTA 0
-      long long hb[64 * 8];
-      cudaStreamSynchronize(st);
-      cudaMemcpy(hb, trace_buf, sizeof(hb), cudaMemcpyDeviceToHost);
-      const long long t0 = hb[0];
-      fprintf(stderr, "unit: ew_wait ew_ready ew_packed | is_wait is_go is_mma2 is_w2 is_end\n");
-      for (int u = 0; u < 40; ++u) {
-        fprintf(stderr, "%2d:", u);
-        for (int j = 0; j < 8; ++j)
-          fprintf(stderr, " %7lld%s", hb[u * 8 + j] ? hb[u * 8 + j] - t0 : -1, j == 2 ? " |" : "");
-        fprintf(stderr, "\n");
-      }
-    }
   } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
                         3 * 256 * 2 * D + 128;

@@ -36,9 +36,16 @@ PROFILE = None
 DT_NAME = {N.EVO_F32: "f32", N.EVO_BF16: "bf16"}
 # optional list collecting (family, shape) per profiled call (bench --detail)
 PROFILE_SHAPES = None
+# bench.py sets this to a list to record replayable launches: entries
+# (family, algorithmic_flops, launch_fn, keep_alive_tensors); replaying the
+# recorded launches of one family inside a CUDA graph times that family's
+# kernels back to back on the device, free of host launch gaps
+RECORD = None
 
 
-def _timed(family, flops, fn, shape=None):
+def _timed(family, flops, fn, shape=None, keep=()):
+    if RECORD is not None:
+        RECORD.append((family, flops, fn, keep))
     if PROFILE is None:
         return fn()
     e0 = torch.cuda.Event(enable_timing=True)
@@ -108,7 +115,8 @@ def gemm(A: Mat, B: Mat, Cm: Mat, M: int, N_: int, K: int, *, alpha: float = 1.0
     d.workspace_bytes = nbytes
     _timed("gemm", 2.0 * M * N_ * K * B1 * B2,
            lambda: check(L.evo_gemm(C.byref(d), stream()), "evo_gemm"),
-           (M, N_, K, B1 * B2, d.split_k, int(A.rs == 1), int(B.rs == 1), DT_NAME[d.dtype_c]))
+           (M, N_, K, B1 * B2, d.split_k, int(A.rs == 1), int(B.rs == 1), DT_NAME[d.dtype_c]),
+           keep=(A.t, B.t, Cm.t, bias, residual, ws))
 
 
 def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, min_rows: int = 512) -> int:
@@ -206,7 +214,8 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
     flops = 4.0 * nb * H * L * L * D
     if dgm is None:
         _timed("attention_fwd", flops,
-               lambda: check(Lb.evo_attention_fwd(C.byref(d), stream()), "evo_attention_fwd"))
+               lambda: check(Lb.evo_attention_fwd(C.byref(d), stream()), "evo_attention_fwd"),
+               keep=(proj, o, gm, lse, bias))
         return
     d.dgm = ptr(dgm)
     d.dq, d.dk, d.dv, d.dgpre = (ptr(dproj, 0), ptr(dproj, hc), ptr(dproj, 2 * hc),
@@ -216,7 +225,8 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
     ws = _ws(nbytes, proj.device)
     d.workspace, d.workspace_bytes = ptr(ws), nbytes
     _timed("attention_bwd", 2.0 * flops,
-           lambda: check(Lb.evo_attention_bwd(C.byref(d), stream()), "evo_attention_bwd"))
+           lambda: check(Lb.evo_attention_bwd(C.byref(d), stream()), "evo_attention_bwd"),
+           keep=(proj, o, gm, lse, bias, dgm, dproj, dbias, ws))
 
 
 def colsum(src, rows: int, cols: int, dst, *, rs=None, off=0, accumulate=False):
