@@ -380,41 +380,53 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
 
 // ===================================================================== prep
 // dO = dGM*G (bf16, o's layout), dGpre = dGM*O*G*(1-G) (proj gate cols),
-// Dq[b,h,q] = sum_d dO*O.  One thread per (row(b,l), head).
+// Dq[b,h,q] = sum_d dO*O.  One thread per 8-column chunk of a (row, head)
+// (consecutive lanes read consecutive 16-byte chunks); the D/8 chunk
+// threads of a head reduce Dq with shuffles.
 template <int D>
-__global__ void attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm, bf16 *dO_out,
-                                     bf16 *dgpre, float *Dq) {
-  const int64_t total = a.nb * (int64_t)a.L * a.H;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    const int h = (int)(e % a.H);
-    const int64_t r = e / a.H;
+__global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm,
+                                                            bf16 *dO_out, bf16 *dgpre, float *Dq) {
+  constexpr int CH = D / 8;  // chunks per head (2 or 4)
+  const int64_t total = a.nb * (int64_t)a.L * a.H * CH;
+  const int lane = threadIdx.x & 31;
+  // warp-uniform trip count (the shuffles below need every lane)
+  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x - lane); e0 < total;
+       e0 += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t e = e0 + lane;
+    const bool ok = e < total;
+    const int c = (int)(e % CH);
+    const int64_t eh = e / CH;
+    const int h = (int)(eh % a.H);
+    const int64_t r = eh / a.H;
     const int l = (int)(r % a.L);
     const int64_t b = r / a.L;
-    const int64_t ooff = b * a.o_sb + (int64_t)l * a.o_sl + h * D;
-    const int64_t goff = b * a.sb + (int64_t)l * a.sl + h * D;
+    const int64_t ooff = b * a.o_sb + (int64_t)l * a.o_sl + h * D + 8 * c;
+    const int64_t goff = b * a.sb + (int64_t)l * a.sl + h * D + 8 * c;
+    const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
+    const uint4 graw = ok ? __ldg(reinterpret_cast<const uint4 *>(a.g + goff)) : z4;
+    const uint4 oraw = ok ? __ldg(reinterpret_cast<const uint4 *>(a.o + ooff)) : z4;
+    const uint4 draw = ok ? __ldg(reinterpret_cast<const uint4 *>(dgm + ooff)) : z4;
+    const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
+    const uint32_t *ow = reinterpret_cast<const uint32_t *>(&oraw);
+    const uint32_t *dw = reinterpret_cast<const uint32_t *>(&draw);
+    uint32_t dov[4], dgv[4];
     float acc = 0.f;
 #pragma unroll
-    for (int d8 = 0; d8 < D; d8 += 8) {
-      uint4 graw = *reinterpret_cast<const uint4 *>(a.g + goff + d8);
-      uint4 oraw = *reinterpret_cast<const uint4 *>(a.o + ooff + d8);
-      uint4 draw = *reinterpret_cast<const uint4 *>(dgm + ooff + d8);
-      const uint32_t *gw = reinterpret_cast<const uint32_t *>(&graw);
-      const uint32_t *ow = reinterpret_cast<const uint32_t *>(&oraw);
-      const uint32_t *dw = reinterpret_cast<const uint32_t *>(&draw);
-      uint32_t dov[4], dgv[4];
-#pragma unroll
-      for (int j = 0; j < 4; ++j) {
-        float2 g2 = unpack2(gw[j]), o2 = unpack2(ow[j]), d2 = unpack2(dw[j]);
-        float do0 = d2.x * g2.x, do1 = d2.y * g2.y;
-        acc += do0 * o2.x + do1 * o2.y;
-        dov[j] = pack2(do0, do1);
-        dgv[j] = pack2(d2.x * o2.x * g2.x * (1.f - g2.x), d2.y * o2.y * g2.y * (1.f - g2.y));
-      }
-      *reinterpret_cast<uint4 *>(dO_out + ooff + d8) = make_uint4(dov[0], dov[1], dov[2], dov[3]);
-      *reinterpret_cast<uint4 *>(dgpre + goff + d8) = make_uint4(dgv[0], dgv[1], dgv[2], dgv[3]);
+    for (int j = 0; j < 4; ++j) {
+      float2 g2 = unpack2(gw[j]), o2 = unpack2(ow[j]), d2 = unpack2(dw[j]);
+      float do0 = d2.x * g2.x, do1 = d2.y * g2.y;
+      acc += do0 * o2.x + do1 * o2.y;
+      dov[j] = pack2(do0, do1);
+      dgv[j] = pack2(d2.x * o2.x * g2.x * (1.f - g2.x), d2.y * o2.y * g2.y * (1.f - g2.y));
     }
-    Dq[(b * a.H + h) * (int64_t)a.L + l] = acc;
+    if (ok) {
+      *reinterpret_cast<uint4 *>(dO_out + ooff) = make_uint4(dov[0], dov[1], dov[2], dov[3]);
+      *reinterpret_cast<uint4 *>(dgpre + goff) = make_uint4(dgv[0], dgv[1], dgv[2], dgv[3]);
+    }
+    // fixed-order reduction over the CH chunk lanes (aligned groups of CH)
+#pragma unroll
+    for (int off = 1; off < CH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
+    if (ok && c == 0) Dq[(b * a.H + h) * (int64_t)a.L + l] = acc;
   }
 }
 
@@ -1892,8 +1904,8 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   float *Dq = reinterpret_cast<float *>(ws + dO_pad);
   float *part = d->dbias ? reinterpret_cast<float *>(ws + dO_pad + Dq_pad) : nullptr;
   {
-    int64_t total = d->nb * (int64_t)d->L * d->H;
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 16);
+    int64_t total = d->nb * (int64_t)d->L * d->H * (D / 8);
+    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
     attn_bwd_prep_kernel<D><<<blocks, 256, 0, st>>>(a, reinterpret_cast<const bf16 *>(d->dgm),
                                                      dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq);
     EVO_LAUNCHED("attn_bwd_prep_kernel");
