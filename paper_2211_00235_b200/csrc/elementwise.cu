@@ -118,14 +118,27 @@ __global__ void colsum_stage1_vec(int64_t rows, int64_t cols, const void *src, i
 }
 
 // Stage 2: warp per column, lanes stride the partials, fixed shuffle tree.
-__global__ void colsum_stage2(int nblk, int64_t cols, const float *part, float *dst, int acc) {
-  const int lane = threadIdx.x & 31;
-  const int64_t c = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= cols) return;
+// Column sums of the [nblk, cols] partials: a 512-thread block owns 32
+// columns, lanes across columns (coalesced 128-byte rows), the 16 warps
+// take partial rows w, w+16, ... and the 16 warp sums are combined in order.
+__global__ void __launch_bounds__(512) colsum_stage2(int nblk, int64_t cols, const float *part,
+                                                     float *dst, int acc) {
+  __shared__ float red[16][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t c = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int b = lane; b < nblk; b += 32) s += part[(int64_t)b * cols + c];
-  s = warp_sum(s);
-  if (lane == 0) dst[c] = acc ? dst[c] + s : s;
+  if (c < cols) {
+#pragma unroll 4
+    for (int b = w; b < nblk; b += 16) s += __ldg(&part[(int64_t)b * cols + c]);
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < cols) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) t += red[j][lane];
+    dst[c] = acc ? dst[c] + t : t;
+  }
 }
 
 template <typename TS, typename TD>
@@ -426,7 +439,7 @@ int colsum(int dt, int64_t rows, int64_t cols, const void *src, int64_t rs, floa
     else colsum_stage1<bf16><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
     EVO_LAUNCHED("colsum_stage1");
   }
-  colsum_stage2<<<(unsigned)((cols + 7) / 8), 256, 0, st>>>((int)nblk, cols, ws, dst, acc);
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>((int)nblk, cols, ws, dst, acc);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }

@@ -279,23 +279,33 @@ ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
 
 // Ordered reduction of the per-block partials: one warp per output value;
 // lane l sums partials l, l+32, ... then a fixed shuffle tree.
-// One warp per output column: lane l sums partials l, l+32, ... (unrolled,
-// independent loads in flight), then a fixed-order warp tree.
-__global__ void ln_param_reduce_kernel(int nblk, int cols, int nparts,
-                                       const float *__restrict__ partial,
-                                       float *__restrict__ dgamma, float *__restrict__ dbeta,
-                                       float *__restrict__ dcol, int accumulate) {
-  const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (c >= nparts * cols) return;
-  const int which = c / cols, cc = c % cols;
+// Column sums of the [nblk, nparts*cols] partials (see colsum_stage2): a
+// 512-thread block owns 32 output columns with lanes across columns
+// (coalesced), the 16 warps take partial rows w, w+16, ..., combined in order.
+__global__ void __launch_bounds__(512) ln_param_reduce_kernel(int nblk, int cols, int nparts,
+                                                              const float *__restrict__ partial,
+                                                              float *__restrict__ dgamma,
+                                                              float *__restrict__ dbeta,
+                                                              float *__restrict__ dcol,
+                                                              int accumulate) {
+  __shared__ float red[16][33];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int width = nparts * cols;
+  const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
+  if (c < width) {
 #pragma unroll 4
-  for (int b = lane; b < nblk; b += 32) s += __ldg(&partial[((int64_t)b * nparts + which) * cols + cc]);
-  s = warp_sum(s);
-  if (lane == 0) {
+    for (int b = w; b < nblk; b += 16) s += __ldg(&partial[(int64_t)b * width + c]);
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w == 0 && c < width) {
+    float t = red[0][lane];
+#pragma unroll
+    for (int j = 1; j < 16; ++j) t += red[j][lane];
+    const int which = c / cols, cc = c % cols;
     float *dst = which == 0 ? dgamma : (which == 1 ? dbeta : dcol);
-    if (dst) dst[cc] = (accumulate && which < 2) ? dst[cc] + s : s;
+    if (dst) dst[cc] = (accumulate && which < 2) ? dst[cc] + t : t;
   }
 }
 
@@ -377,8 +387,8 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
   }
   if (want) {
     const int outs = nparts * cols;
-    ln_param_reduce_kernel<<<(outs + 7) / 8, 256, 0, st>>>(nblk, cols, nparts, ws, dgamma, dbeta,
-                                                           dx_colsum, acc);
+    ln_param_reduce_kernel<<<(outs + 31) / 32, 512, 0, st>>>(nblk, cols, nparts, ws, dgamma,
+                                                             dbeta, dx_colsum, acc);
     EVO_LAUNCHED("ln_param_reduce_kernel");
   }
   return EVO_OK;

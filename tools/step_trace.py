@@ -60,37 +60,55 @@ def join(csv_path, shapes_path):
     with open(shapes_path) as f:
         calls = json.load(f)
     rows = []
+    dram = {}  # launch id -> bytes (when the dram metrics were collected)
     with open(csv_path) as f:
         lines = [ln for ln in f if ln.startswith('"')]
     for r in csv.DictReader(lines):
-        if r.get("Metric Name") != "gpu__time_duration.sum":
-            continue
+        name = r.get("Metric Name")
         v = float(r["Metric Value"].replace(",", ""))
-        unit = r.get("Metric Unit", "nsecond")
+        unit = r.get("Metric Unit", "")
+        if name in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}.get(unit, 1)
+            dram[r["ID"]] = dram.get(r["ID"], 0.0) + v * scale
+            continue
+        if name != "gpu__time_duration.sum":
+            continue
         us = v / 1e3 if unit.startswith("n") else (v if unit.startswith("u") else v * 1e3)
-        rows.append((r["Kernel Name"], us))
+        rows.append((r["Kernel Name"], us, r["ID"]))
     # attach each family-starting launch to the next call of that family
     queues = {}
     for fam, fl, shp in calls:
         queues.setdefault(fam, []).append((fl, shp))
     cur = None
     groups = []
-    for name, us in rows:
+    for name, us, lid in rows:
         fam = family_of(name)
         if fam is not None and queues.get(fam):
             fl, shp = queues[fam].pop(0)
-            cur = [fam, shp, fl, 0.0, []]
+            cur = [fam, shp, fl, 0.0, [], 0.0]
             groups.append(cur)
         elif fam is not None or cur is None or not (
                 (cur[0] == "gemm" and ("splitk_reduce" in name or "skinny_reduce" in name)) or
                 (cur[0] == "attention_bwd" and ("attn_bwd" in name or "reduce_lead" in name))):
-            cur = [name.split("(")[0][:48], None, 0.0, 0.0, []]
+            cur = [name.split("(")[0][:48], None, 0.0, 0.0, [], 0.0]
             groups.append(cur)
         cur[3] += us
         cur[4].append(name.split("(")[0].split("<")[0][-28:])
+        cur[5] += dram.get(lid, 0.0)
     total = sum(g[3] for g in groups)
+    fam_tot = {}
+    for g in groups:
+        if g[0] in ("gemm", "attention_fwd", "attention_bwd"):
+            f = fam_tot.setdefault(g[0], [0.0, 0.0, 0, 0.0])
+            f[0] += g[3]
+            f[1] += g[2]
+            f[2] += 1
+            f[3] += g[5]
+    for k, (us, fl, n, byt) in fam_tot.items():
+        print(f"family {k}: {n} launches, {us:.1f} us, {fl / us / 1e6:.1f} TF/s, "
+              f"DRAM {byt / 1e6:.1f} MB ({byt / max(n, 1) / 1e6:.2f} MB per launch)")
     agg = {}
-    for fam, shp, fl, us, names in groups:
+    for fam, shp, fl, us, names, _b in groups:
         key = f"{fam} {shp}" if shp else fam
         a = agg.setdefault(key, [0.0, 0.0, 0])
         a[0] += us
