@@ -396,8 +396,16 @@ def run_native(args):
         top = max(fam_graph, key=lambda k: fam_graph[k][1])
         fl, tms, n = fam_graph[top]
         achieved = fl / (tms / 1e3) / 1e12
+        traffic = None
+        try:  # DRAM bytes per launch of this family from the committed ncu capture
+            with open(os.path.join(ROOT, "profiles", "r01_family_dram.json")) as f:
+                traffic = json.load(f)["families"][top]["dram_bytes_per_launch"]
+        except Exception:
+            traffic = None
         roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": peak,
-                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": None,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "traffic_unit": "DRAM bytes per launch (profiles/r01_family_dram.json)",
+                "algorithmic_flops_per_launch": fl / n,
                 "peak_source": src, "launches": n, "share_of_step": tms / ms,
                 "timing": "CUDA events around one step's launches of this family, "
                           "re-issued back to back in a CUDA graph on the launching stream"}
