@@ -140,6 +140,30 @@ EVO_API int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const floa
                                  float *dx_colsum, void *workspace, size_t workspace_bytes,
                                  void *stream);
 
+/* LayerNorm forward of a contiguous fp32 [rows, 128] input (c_z rows) with
+ * the pair-bias projection of the attention sub-ops fused in
+ * (src/evoformer.py:279, bias = LN(z) Wb):
+ *   y (bf16, may be NULL) = LN(x);  mean/rstd as evo_layernorm_fwd;
+ *   proj[hh*p_rs + row] = sum_c bf16(y[row,c]) * Wp[c*nh + hh]   (fp32)
+ * Wp: bf16 [128][nh], nh <= 8.                                          */
+EVO_API int evo_layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
+                                   const float *beta, void *y, float *mean, float *rstd,
+                                   float eps, const void *Wp, int nh, float *proj,
+                                   int64_t p_rs, void *stream);
+
+/* Its backward, fused with the projection's backward:
+ *   dy_tot = dy (fp32 [rows,128], may be NULL = 0) + sum_hh dproj[hh*p_rs+row] Wp[c*nh+hh]
+ *   dx = LN_bwd(dy_tot) + dres;  dx_act / dx_colsum as evo_layernorm_bwd_ex;
+ *   dgamma, dbeta, and dWp[c*nh + hh] = sum_rows bf16(LN(x))[row,c] * dproj[hh,row]
+ *   (all written).  dproj fp32.  Workspace as evo_layernorm_bwd.        */
+EVO_API int evo_layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x,
+                                   const float *mean, const float *rstd, const float *gamma,
+                                   const float *beta, const float *dres, const float *dproj,
+                                   int64_t p_rs, const void *Wp, int nh, float *dx,
+                                   void *dx_act, float *dgamma, float *dbeta,
+                                   float *dx_colsum, float *dWp, void *workspace,
+                                   size_t workspace_bytes, void *stream);
+
 /* Fused gated attention forward over the middle axis
  * (_gated_attention core, src/evoformer.py:274-286):
  *   O[b,l,h,:] = softmax_k( scale*q.k + bias[h,l,k] ) v

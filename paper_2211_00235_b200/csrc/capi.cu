@@ -29,6 +29,12 @@ int layernorm_bwd(int, int, int, int64_t, int, const void *, int64_t, const void
 int layernorm_bwd_ex(int64_t, int, const float *, const void *, int, const float *, const float *,
                      const float *, const float *, float *, void *, float *, float *, float *,
                      void *, size_t, cudaStream_t);
+int layernorm_fwd_proj(int64_t, int, const float *, const float *, const float *, void *, float *,
+                       float *, float, const void *, int, float *, int64_t, cudaStream_t);
+int layernorm_bwd_proj(int64_t, int, const float *, const float *, const float *, const float *,
+                       const float *, const float *, const float *, const float *, int64_t,
+                       const void *, int, float *, void *, float *, float *, float *, float *,
+                       void *, size_t, cudaStream_t);
 int attention_simt_fwd(const evo_attn_desc *, cudaStream_t);
 int attention_simt_bwd(const evo_attn_desc *, cudaStream_t);
 size_t attention_simt_bwd_ws(const evo_attn_desc *);
@@ -158,6 +164,35 @@ int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const float *dy, c
   CHECK_PTR(dy); CHECK_PTR(x); CHECK_PTR(mean); CHECK_PTR(rstd); CHECK_PTR(gamma); CHECK_PTR(dx);
   return layernorm_bwd_ex(rows, cols, dy, x, dtype_x, mean, rstd, gamma, dres, dx, dx_act, dgamma,
                           dbeta, dx_colsum, workspace, workspace_bytes, as_stream(stream));
+}
+
+int evo_layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
+                           const float *beta, void *y, float *mean, float *rstd, float eps,
+                           const void *Wp, int nh, float *proj, int64_t p_rs, void *stream) {
+  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_layernorm_fwd_proj: rows=%lld cols=%d",
+              (long long)rows, cols);
+  EVO_REQUIRE(eps > 0.f, EVO_EARG, "evo_layernorm_fwd_proj: eps must be > 0");
+  if (rows == 0) return EVO_OK;
+  CHECK_PTR(x); CHECK_PTR(gamma); CHECK_PTR(beta); CHECK_PTR(mean); CHECK_PTR(rstd);
+  CHECK_PTR(Wp); CHECK_PTR(proj);
+  return layernorm_fwd_proj(rows, cols, x, gamma, beta, y, mean, rstd, eps, Wp, nh, proj, p_rs,
+                            as_stream(stream));
+}
+
+int evo_layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x,
+                           const float *mean, const float *rstd, const float *gamma,
+                           const float *beta, const float *dres, const float *dproj, int64_t p_rs,
+                           const void *Wp, int nh, float *dx, void *dx_act, float *dgamma,
+                           float *dbeta, float *dx_colsum, float *dWp, void *workspace,
+                           size_t workspace_bytes, void *stream) {
+  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_layernorm_bwd_proj: rows=%lld cols=%d",
+              (long long)rows, cols);
+  if (rows == 0) return EVO_OK;
+  CHECK_PTR(x); CHECK_PTR(mean); CHECK_PTR(rstd); CHECK_PTR(gamma); CHECK_PTR(beta);
+  CHECK_PTR(dproj); CHECK_PTR(Wp); CHECK_PTR(dx); CHECK_PTR(dWp);
+  return layernorm_bwd_proj(rows, cols, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs, Wp, nh,
+                            dx, dx_act, dgamma, dbeta, dx_colsum, dWp, workspace,
+                            workspace_bytes, as_stream(stream));
 }
 
 static int check_attn(const evo_attn_desc *d, bool bwd) {

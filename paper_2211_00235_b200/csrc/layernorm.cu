@@ -88,6 +88,68 @@ ln_fwd_vec_kernel(int64_t rows, const TX *__restrict__ x, int64_t x_rs,
   }
 }
 
+// -------------------------------------- forward + pair-bias projection
+// c_z = 128 rows (NV = 1): y = LN(x) (bf16, optional) and
+// proj[hh*p_rs + row] = sum_c bf16(y[row,c]) * Wp[c*NH + hh]   (NH <= 8)
+// (the pair-bias projection of the attention sub-ops, src/evoformer.py:279).
+template <int NH>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+ln_fwd_proj_kernel(int64_t rows, const float *__restrict__ x, const float *__restrict__ gamma,
+                   const float *__restrict__ beta, bf16 *__restrict__ y,
+                   float *__restrict__ mean_out, float *__restrict__ rstd_out, float eps,
+                   const bf16 *__restrict__ Wp, int nh, float *__restrict__ proj, int64_t p_rs) {
+  constexpr int cols = 128;
+  const int lane = threadIdx.x & 31;
+  float W[4][NH];
+#pragma unroll
+  for (int j = 0; j < 4; ++j)
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh)
+      W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
+  const float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane);
+  const float4 b4 = *reinterpret_cast<const float4 *>(beta + 4 * lane);
+  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < rows;
+       row += (int64_t)gridDim.x * LN_WARPS) {
+    float v[4];
+    Vec<float, 4>::load(x + row * cols + 4 * lane, v);
+    float s = 0.f;  // same summation order as ln_fwd_vec_kernel (bitwise equal y, mu, rstd)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) s += v[j];
+    const float mu = warp_sum(s) * (1.f / cols);
+    float q = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float d = v[j] - mu;
+      q += d * d;
+    }
+    const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
+    float o[4] = {(v[0] - mu) * rs * g4.x + b4.x, (v[1] - mu) * rs * g4.y + b4.y,
+                  (v[2] - mu) * rs * g4.z + b4.z, (v[3] - mu) * rs * g4.w + b4.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) o[j] = __bfloat162float(__float2bfloat16_rn(o[j]));
+    if (y) Vec<bf16, 4>::store(y + row * cols + 4 * lane, o);
+    float pr[NH];
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) {
+      float t = 0.f;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) t = fmaf(o[j], W[j][hh], t);
+      pr[hh] = warp_sum(t);
+    }
+    if (lane < nh) {
+      float val = 0.f;
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+        if (lane == hh) val = pr[hh];
+      proj[(int64_t)lane * p_rs + row] = val;
+    }
+    if (lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
+  }
+}
+
 // --------------------------------------------------------- generic forward
 template <typename TX, typename TY, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
@@ -207,6 +269,99 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
   }
 }
 
+// ------------------------------------- backward + pair-bias projection
+// c_z = 128 rows.  dy_tot = dy (may be NULL) + dproj^T Wp^T with dproj fp32
+// [NH, p_rs] (the pair-bias gradient summed over heads' batch rows);
+// dx = LN_bwd(dy_tot) (+ dres), optional bf16 copy and column sums of dx as
+// in ln_bwd_vec_kernel; partials [block][3 + NH][128]: dgamma, dbeta, colsum,
+// and dWp^T[hh][c] = sum_rows bf16(y[row,c]) * dproj[hh,row] with y = LN(x)
+// recomputed exactly as the forward rounded it.
+template <int NH>
+__global__ void __launch_bounds__(LN_WARPS * 32)
+ln_bwd_proj_kernel(int64_t rows, const float *__restrict__ dy, const float *__restrict__ x,
+                   const float *__restrict__ mean, const float *__restrict__ rstd,
+                   const float *__restrict__ gamma, const float *__restrict__ beta,
+                   const float *__restrict__ dres, const float *__restrict__ dproj, int64_t p_rs,
+                   const bf16 *__restrict__ Wp, int nh, float *__restrict__ dx,
+                   bf16 *__restrict__ dxa, float *__restrict__ partial) {
+  constexpr int cols = 128, NP = 3 + NH;
+  __shared__ float red[LN_WARPS][NP][cols];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  float W[4][NH], pw[4][NH], pg[4], pb[4], pc[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    pg[j] = pb[j] = pc[j] = 0.f;
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) {
+      W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
+      pw[j][hh] = 0.f;
+    }
+  }
+  const float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane);
+  const float4 b4 = *reinterpret_cast<const float4 *>(beta + 4 * lane);
+  const float g[4] = {g4.x, g4.y, g4.z, g4.w}, bt[4] = {b4.x, b4.y, b4.z, b4.w};
+  constexpr float inv_n = 1.f / cols;
+  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + warp; row < rows;
+       row += (int64_t)gridDim.x * LN_WARPS) {
+    const float mu = mean[row], rs = rstd[row];
+    // this row's NH projection gradients: lane hh loads, shuffles broadcast
+    const float mine = lane < nh ? __ldg(&dproj[(int64_t)lane * p_rs + row]) : 0.f;
+    float dp[NH];
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) dp[hh] = __shfl_sync(0xffffffffu, mine, hh);
+    float dv[4] = {0.f, 0.f, 0.f, 0.f}, xv[4];
+    if (dy) Vec<float, 4>::load(dy + row * cols + 4 * lane, dv);
+    Vec<float, 4>::load(x + row * cols + 4 * lane, xv);
+    float xh[4], dxh[4], s1 = 0.f, s2 = 0.f;
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float d = dv[j];
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) d = fmaf(dp[hh], W[j][hh], d);
+      xh[j] = (xv[j] - mu) * rs;
+      // y exactly as the forward produced it (bf16), for dWp
+      const float yv = __bfloat162float(__float2bfloat16_rn((xv[j] - mu) * rs * g[j] + bt[j]));
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) pw[j][hh] = fmaf(yv, dp[hh], pw[j][hh]);
+      dxh[j] = d * g[j];
+      s1 += dxh[j];
+      s2 += dxh[j] * xh[j];
+      pg[j] += d * xh[j];
+      pb[j] += d;
+    }
+    const float m1 = warp_sum(s1) * inv_n;
+    const float m2 = warp_sum(s2) * inv_n;
+    float r[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) r[j] = rs * (dxh[j] - m1 - xh[j] * m2);
+    if (dres) {
+      float4 d4 = *reinterpret_cast<const float4 *>(dres + row * cols + 4 * lane);
+      r[0] += d4.x; r[1] += d4.y; r[2] += d4.z; r[3] += d4.w;
+    }
+    Vec<float, 4>::store(dx + row * cols + 4 * lane, r);
+    if (dxa) Vec<bf16, 4>::store(dxa + row * cols + 4 * lane, r);
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pc[j] += r[j];
+  }
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const int c = 4 * lane + j;
+    red[warp][0][c] = pg[j];
+    red[warp][1][c] = pb[j];
+    red[warp][2][c] = pc[j];
+#pragma unroll
+    for (int hh = 0; hh < NH; ++hh) red[warp][3 + hh][c] = pw[j][hh];
+  }
+  __syncthreads();
+  for (int c = threadIdx.x; c < NP * cols; c += blockDim.x) {
+    const int which = c / cols, cc = c % cols;
+    float sacc = 0.f;
+#pragma unroll
+    for (int w = 0; w < LN_WARPS; ++w) sacc += red[w][which][cc];
+    partial[((int64_t)blockIdx.x * NP + which) * cols + cc] = sacc;
+  }
+}
+
 // -------------------------------------------------------- generic backward
 template <typename TDY, typename TX, typename TDX, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
@@ -287,7 +442,9 @@ __global__ void __launch_bounds__(512) ln_param_reduce_kernel(int nblk, int cols
                                                               float *__restrict__ dgamma,
                                                               float *__restrict__ dbeta,
                                                               float *__restrict__ dcol,
-                                                              int accumulate) {
+                                                              int accumulate,
+                                                              float *__restrict__ dWp = nullptr,
+                                                              int nh = 0) {
   __shared__ float red[16][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int width = nparts * cols;
@@ -304,8 +461,12 @@ __global__ void __launch_bounds__(512) ln_param_reduce_kernel(int nblk, int cols
 #pragma unroll
     for (int j = 1; j < 16; ++j) t += red[j][lane];
     const int which = c / cols, cc = c % cols;
-    float *dst = which == 0 ? dgamma : (which == 1 ? dbeta : dcol);
-    if (dst) dst[cc] = (accumulate && which < 2) ? dst[cc] + t : t;
+    if (which >= 3) {
+      if (which - 3 < nh) dWp[cc * nh + (which - 3)] = t;
+    } else {
+      float *dst = which == 0 ? dgamma : (which == 1 ? dbeta : dcol);
+      if (dst) dst[cc] = (accumulate && which < 2) ? dst[cc] + t : t;
+    }
   }
 }
 
@@ -398,7 +559,8 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
 
 size_t layernorm_bwd_ws(int64_t rows, int cols) {
   (void)rows;
-  return (size_t)LN_BWD_BLOCKS * 3 * cols * sizeof(float);
+  // dgamma, dbeta, column sums, and up to 8 projection-weight gradients
+  return (size_t)LN_BWD_BLOCKS * 11 * cols * sizeof(float);
 }
 
 int layernorm_fwd(int tx, int ty, int64_t rows, int cols, const void *x, int64_t x_rs,
@@ -432,6 +594,49 @@ int layernorm_bwd_ex(int64_t rows, int cols, const float *dy, const void *x, int
   return ln_bwd_launch<float, bf16, float>(rows, cols, dy, cols, x, cols, 1, mean, rstd, gamma,
                                            dres, dx, cols, 1, dgamma, dbeta, 0, w, st, dx_act, cols,
                                            dx_colsum);
+}
+
+int layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
+                       const float *beta, void *y, float *mean, float *rstd, float eps,
+                       const void *Wp, int nh, float *proj, int64_t p_rs, cudaStream_t st) {
+  EVO_REQUIRE(cols == 128 && nh >= 1 && nh <= 8, EVO_EUNSUP,
+              "layernorm_fwd_proj: cols=%d nh=%d (fused path: cols 128, nh <= 8)", cols, nh);
+  EVO_REQUIRE(aligned16(x) && aligned16(gamma) && aligned16(beta) && (!y || aligned16(y)), EVO_EARG,
+              "layernorm_fwd_proj: operands must be 16-byte aligned");
+  if (rows == 0) return EVO_OK;
+  const int blocks = (int)std::min<int64_t>((rows + LN_WARPS - 1) / LN_WARPS, (int64_t)num_sms() * 8);
+  ln_fwd_proj_kernel<8><<<blocks, LN_WARPS * 32, 0, st>>>(
+      rows, x, gamma, beta, reinterpret_cast<bf16 *>(y), mean, rstd, eps,
+      reinterpret_cast<const bf16 *>(Wp), nh, proj, p_rs);
+  EVO_LAUNCHED("ln_fwd_proj_kernel");
+  return EVO_OK;
+}
+
+int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, const float *mean,
+                       const float *rstd, const float *gamma, const float *beta,
+                       const float *dres, const float *dproj, int64_t p_rs, const void *Wp, int nh,
+                       float *dx, void *dx_act, float *dgamma, float *dbeta, float *dx_colsum,
+                       float *dWp, void *ws, size_t ws_bytes, cudaStream_t st) {
+  EVO_REQUIRE(cols == 128 && nh >= 1 && nh <= 8, EVO_EUNSUP,
+              "layernorm_bwd_proj: cols=%d nh=%d (fused path: cols 128, nh <= 8)", cols, nh);
+  EVO_REQUIRE(ws && ws_bytes >= layernorm_bwd_ws(rows, cols), EVO_EARG,
+              "layernorm_bwd_proj: workspace too small");
+  EVO_REQUIRE(aligned16(x) && aligned16(dx) && (!dy || aligned16(dy)) && (!dres || aligned16(dres)) &&
+                  (!dx_act || aligned16(dx_act)),
+              EVO_EARG, "layernorm_bwd_proj: operands must be 16-byte aligned");
+  if (rows == 0) return EVO_OK;
+  const int64_t need_blocks = (rows + LN_WARPS - 1) / LN_WARPS;
+  const int nblk = (int)std::min<int64_t>(LN_BWD_BLOCKS, std::max<int64_t>(need_blocks, 1));
+  float *w = reinterpret_cast<float *>(ws);
+  ln_bwd_proj_kernel<8><<<nblk, LN_WARPS * 32, 0, st>>>(
+      rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
+      reinterpret_cast<const bf16 *>(Wp), nh, dx, reinterpret_cast<bf16 *>(dx_act), w);
+  EVO_LAUNCHED("ln_bwd_proj_kernel");
+  const int nparts = 3 + 8;
+  ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
+      nblk, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
+  EVO_LAUNCHED("ln_param_reduce_kernel");
+  return EVO_OK;
 }
 
 int layernorm_bwd(int tdy, int tx, int tdx, int64_t rows, int cols, const void *dy, int64_t dy_rs,

@@ -213,6 +213,11 @@ def _ln_bwd_out(dy, x, rows, cols, mu, rs, gamma, dgamma, dbeta, dres, act, emit
     return dx
 
 
+def _bias_fusable(cfg, act):
+    """Pair-bias projection fused into the LayerNorm kernels (bf16 path)?"""
+    return act != F32 and cfg.c_z == 128 and cfg.h <= 8
+
+
 def _grad_in(dx_new, rows, cols, act, dev, handoff):
     """(bf16 operand copy of an incoming gradient, bias colsum already done?)"""
     if handoff is not None and handoff.get("act") is not None:
@@ -255,21 +260,33 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     ctx = {}
     xh = _empty((rows, c_io), act, dev)
     mu, rs = _empty(rows, F32, dev), _empty(rows, F32, dev)
-    K.layernorm(x, rows, c_io, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
-    ctx.update(x=x, xh=xh, mu=mu, rs=rs)
-    bias = None
+    # the pair-bias projection fuses into the LayerNorm of its input on the
+    # bf16 path (c_z = 128, h <= 8): bias = LN(z) Wb without re-reading LN(z)
+    fuse_bias = name != "col_attn" and _bias_fusable(cfg, act)
+    bias = _empty((h, r2), F32, dev) if name != "col_attn" else None
+    if fuse_bias and name != "row_attn":
+        K.layernorm_proj(x, rows, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps,
+                         pk["Wb"], h, bias, r2)
+    else:
+        K.layernorm(x, rows, c_io, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
+    ctx.update(x=x, xh=xh, mu=mu, rs=rs, fuse_bias=fuse_bias)
     if name != "col_attn":
         if name == "row_attn":
-            zh = _empty((r2, cfg.c_z), act, dev)
             zmu, zrs = _empty(r2, F32, dev), _empty(r2, F32, dev)
-            K.layernorm(z, r2, cfg.c_z, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], zh, zmu, zrs,
-                        cfg.eps)
-            ctx.update(z=z, zh=zh, zmu=zmu, zrs=zrs)
+            if fuse_bias:  # LN_z(z) itself is not needed: the backward recomputes it
+                K.layernorm_proj(z, r2, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], None, zmu, zrs,
+                                 cfg.eps, pk["Wb"], h, bias, r2)
+                ctx.update(z=z, zmu=zmu, zrs=zrs)
+            else:
+                zh = _empty((r2, cfg.c_z), act, dev)
+                K.layernorm(z, r2, cfg.c_z, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], zh, zmu, zrs,
+                            cfg.eps)
+                ctx.update(z=z, zh=zh, zmu=zmu, zrs=zrs)
         else:
             zh = xh
-        bias = _empty((h, r2), F32, dev)
-        # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*r2 + row)
-        K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, r2), r2, h, cfg.c_z)
+        if not fuse_bias:
+            # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*r2 + row)
+            K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, r2), r2, h, cfg.c_z)
         ctx["bias"] = bias
     proj = _empty((rows, 4 * hc), act, dev)
     K.linear(xh, rows, c_io, pk["Wqkvg"], 4 * hc, 4 * hc, proj, 4 * hc, bias=pk["bqkvg"],
@@ -317,7 +334,30 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
     dxh = _empty((rows, c_io), F32, dev)
     K.linear_dx(dproj, rows, 4 * hc, pk["Wqkvg"], 4 * hc, c_io, dxh)
     dz_row = None
-    if dbias is not None:
+    if dbias is not None and ctx["fuse_bias"]:
+        # the pair-bias projection's backward (dz += dbias Wb^T, dWb = LN(z)^T
+        # dbias) fuses into the LayerNorm backward of its input
+        if name == "row_attn":
+            dz_row = _empty((r2, cfg.c_z), F32, dev)
+            K.layernorm_bwd_proj(None, ctx["z"], r2, ctx["zmu"], ctx["zrs"], P[f"{px}.lnz_g"],
+                                 P[f"{px}.lnz_b"], dbias, r2, pk["Wb"], h, dz_row, G["lnz_g"],
+                                 G["lnz_b"], G["Wb"])
+        else:
+            dres = dx_new if ctx["resid"] else None
+            dx = _empty((rows, c_io), F32, dev)
+            colsum = None
+            dxa_out = None
+            if emit is not None:
+                dxa_out = _empty((rows, c_io), act, dev)
+                colsum = emit["bias"]
+            K.layernorm_bwd_proj(dxh, ctx["x"], rows, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                                 P[f"{px}.ln_b"], dbias, r2, pk["Wb"], h, dx, G["ln_g"],
+                                 G["ln_b"], G["Wb"], dres=dres, dx_act=dxa_out,
+                                 dx_colsum=colsum)
+            if emit is not None:
+                emit["act"], emit["done"] = dxa_out, True
+            return dx, None
+    if dbias is not None and not ctx["fuse_bias"]:
         dbias_a = dbias if act == F32 else _empty((h, r2), act, dev)
         if act != F32:
             K.copy2d(dbias, h, r2, dbias_a, s_rs=r2, d_rs=r2)

@@ -195,6 +195,30 @@ def layernorm_bwd_ex(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma,
           "evo_layernorm_bwd_ex")
 
 
+def layernorm_proj(x, rows: int, gamma, beta, y, mean, rstd, eps: float, Wp, nh: int, proj,
+                   p_rs: int):
+    """y = LN(x) (bf16, or None) with the pair-bias projection
+    proj[hh*p_rs + row] = y[row] . Wp[:, hh] fused in (c_z = 128 rows)."""
+    check(lib().evo_layernorm_fwd_proj(rows, 128, ptr(x), ptr(gamma), ptr(beta), ptr(y),
+                                       ptr(mean), ptr(rstd), eps, ptr(Wp), nh, ptr(proj), p_rs,
+                                       stream()),
+          "evo_layernorm_fwd_proj")
+
+
+def layernorm_bwd_proj(dy, x, rows: int, mean, rstd, gamma, beta, dproj, p_rs: int, Wp, nh: int,
+                       dx, dgamma, dbeta, dWp, *, dres=None, dx_act=None, dx_colsum=None):
+    """LayerNorm backward with the pair-bias projection's backward fused in
+    (dy may be None); writes dx (+ dx_act / dx_colsum), dgamma, dbeta, dWp."""
+    L = lib()
+    nbytes = L.evo_layernorm_bwd_workspace_bytes(rows, 128)
+    ws = _ws(nbytes, dx.device)
+    check(L.evo_layernorm_bwd_proj(rows, 128, ptr(dy), ptr(x), ptr(mean), ptr(rstd), ptr(gamma),
+                                   ptr(beta), ptr(dres), ptr(dproj), p_rs, ptr(Wp), nh, ptr(dx),
+                                   ptr(dx_act), ptr(dgamma), ptr(dbeta), ptr(dx_colsum), ptr(dWp),
+                                   ptr(ws), nbytes, stream()),
+          "evo_layernorm_bwd_proj")
+
+
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
               sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
               dgm=None, dproj=None, dbias=None):

@@ -12,6 +12,9 @@ CONFIGS = {
     "c1": dict(s=16, r=32, c_m=32, c_z=16, h=4, c_opm=8, t_factor=4, n_blocks=2),
     # tensor-core-eligible dims (multiples of 16) that the oracle runs in ~1 s
     "mid": dict(s=32, r=64, c_m=64, c_z=32, h=4, c_opm=16, t_factor=4, n_blocks=1),
+    # AF2 channel widths at a small sequence shape: exercises the c_z = 128 /
+    # c_m = 256 fused paths (LayerNorm hand-off, fused pair-bias projection)
+    "wide": dict(s=64, r=64, c_m=256, c_z=128, h=8, c_opm=32, t_factor=4, n_blocks=1),
     # BASELINE.json configs[1]: AF2 initial-training block
     "af2": dict(s=128, r=256, c_m=256, c_z=128, h=8, c_opm=32, t_factor=4, n_blocks=1),
 }

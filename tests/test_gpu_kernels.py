@@ -100,3 +100,47 @@ def test_relu_bwd_and_sq_mean(K):
     K.sq_mean(x, loss, dx)
     assert rel(loss, (x.double() ** 2).mean().reshape(1)) < 1e-6
     assert rel(dx, 2 * x / x.numel()) < 1e-6
+
+
+def test_layernorm_pair_bias_projection_fused(K):
+    """LN(z) + bias = LN(z) Wb and its backward, fused vs unfused kernels."""
+    from paper_2211_00235_b200.kernels import Mat
+    torch.manual_seed(2)
+    rows, cols, h = 4096, 128, 8
+    bf = torch.bfloat16
+    x = torch.randn(rows, cols, device="cuda")
+    g = torch.randn(cols, device="cuda")
+    b = torch.randn(cols, device="cuda")
+    Wb = (torch.randn(cols, h, device="cuda") * 0.1).to(bf)
+    # unfused reference path
+    y0 = torch.empty(rows, cols, device="cuda", dtype=bf)
+    mu0, rs0 = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    K.layernorm(x, rows, cols, g, b, y0, mu0, rs0, 1e-5)
+    bias0 = y0.float() @ Wb.float()                       # [rows, h]
+    # fused
+    y = torch.empty(rows, cols, device="cuda", dtype=bf)
+    mu, rs = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    bias = torch.empty(h, rows, device="cuda")
+    K.layernorm_proj(x, rows, g, b, y, mu, rs, 1e-5, Wb, h, bias, rows)
+    assert torch.equal(y, y0) and torch.equal(mu, mu0) and torch.equal(rs, rs0)
+    assert rel(bias, bias0.T) < 1e-5
+    # backward: dz = LN_bwd(dy + dbias Wb^T), dWb = y^T dbias
+    dy = torch.randn(rows, cols, device="cuda")
+    dbias = torch.randn(h, rows, device="cuda")
+    dytot = dy + dbias.T @ Wb.float().T
+    dx0 = torch.empty(rows, cols, device="cuda")
+    dg0, db0 = torch.empty(cols, device="cuda"), torch.empty(cols, device="cuda")
+    K.layernorm_bwd(dytot, x, rows, cols, mu0, rs0, g, dx0, dg0, db0)
+    dW0 = y0.double().T @ dbias.double().T                # [cols, h]
+    dx = torch.empty(rows, cols, device="cuda")
+    dg, db = torch.empty(cols, device="cuda"), torch.empty(cols, device="cuda")
+    dW = torch.empty(cols, h, device="cuda")
+    K.layernorm_bwd_proj(dy, x, rows, mu, rs, g, b, dbias, rows, Wb, h, dx, dg, db, dW)
+    assert rel(dx, dx0) < 1e-5
+    assert rel(dg, dg0) < 1e-5 and rel(db, db0) < 1e-5
+    assert rel(dW, dW0) < 1e-5
+    # dy absent (row attention: the projection is the only consumer)
+    K.layernorm_bwd_proj(None, x, rows, mu, rs, g, b, dbias, rows, Wb, h, dx, dg, db, dW)
+    dytot = dbias.T @ Wb.float().T
+    K.layernorm_bwd(dytot, x, rows, cols, mu0, rs0, g, dx0, dg0, db0)
+    assert rel(dx, dx0) < 1e-5

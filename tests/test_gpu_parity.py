@@ -65,6 +65,32 @@ def test_step_mid_matches_oracle(pkg, precision, tol):
     assert v <= tol, f"{precision}: worst {k} rel-L2 {v:.3e}"
 
 
+def test_step_wide_bf16_matches_oracle(pkg):
+    """AF2 channel widths: the fused LayerNorm paths are the ones running."""
+    cfg = pkg.EvoConfig(**CONFIGS["wide"])
+    store = pkg.init_params(cfg, 32)
+    res = pkg.run_single(cfg, store, seed=32, precision="bf16")
+    want = _oracle_step("wide")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, want, m_in, z_in, bar=BF16_TOL)
+    k, v = _worst(errs)
+    assert v <= BF16_TOL, f"worst {k} rel-L2 {v:.3e}"
+
+
+def test_step_af2_bf16_matches_oracle(pkg):
+    """The headline configuration itself (BASELINE.json configs[1]): one block
+    at s=128, r=256, c_m=256, c_z=128 on the bf16 path vs the pinned oracle
+    (numpy, ~20 s on the host)."""
+    cfg = pkg.EvoConfig(**CONFIGS["af2"])
+    store = pkg.init_params(cfg, 32)
+    res = pkg.run_single(cfg, store, seed=32, precision="bf16")
+    want = _oracle_step("af2")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, want, m_in, z_in, bar=BF16_TOL)
+    k, v = _worst(errs)
+    assert v <= BF16_TOL, f"worst {k} rel-L2 {v:.3e}"
+
+
 def test_step_c1_bf16_matches_reference(pkg):
     cfg = pkg.EvoConfig(**CONFIGS["c1"])
     store = pkg.init_params(cfg, 32)
