@@ -63,6 +63,7 @@ struct TcParams {
   int64_t cdiv, rdiv;
   int bias_smem;   // bias[0..N) staged in smem by the epilogue warps
   int box_w;       // TMA store box width in columns (64: bf16, 128-byte rows)
+  int res_tma;     // fp32 residual TMA-loaded into the staging boxes
 };
 constexpr int BIAS_SMEM_MAX = 2048;
 
@@ -243,7 +244,8 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
 template <int BN, int STAGES, int EPI>
 __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmC, const TcParams p) {
+               const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
+               const TcParams p) {
   constexpr int SMEM_B = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = SMEM_A + SMEM_B;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
@@ -258,6 +260,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
   uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(tempty + 2);
+  // residual boxes: per epilogue warp, one mbarrier per staging box
+  uint64_t *rbar = reinterpret_cast<uint64_t *>(tmem_slot + 4);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -274,6 +278,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&tfull[a], 1);
       mbar_init(&tempty[a], EPI_WARPS);
     }
+    for (int i = 0; i < 2 * EPI_WARPS; ++i) mbar_init(&rbar[i], 1);
+    if (p.res_tma) prefetch_map(&tmR);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 1) {
@@ -383,14 +389,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     uint8_t *wreg = smem_raw + ((sW - smem_raw) + ew * 8192);
     float *stage = reinterpret_cast<float *>(wreg);
     uint32_t chunk_ctr = 0;
+    uint32_t rph = 0;  // residual box mbarrier parities
     const int half = ew >> 2;  // 0 or 1
     int acc = 0;
     uint32_t aphase = 0;
     const EpiArgs &e = p.epi;
     const float *bias = e.bias;
     if (p.bias_smem) {
+      // after the slot (16 B) and the residual mbarriers (128 B), 16-B aligned
       float *sb = reinterpret_cast<float *>(smem_raw + ((reinterpret_cast<uint8_t *>(tmem_slot) -
-                                                         smem_raw) + 16));
+                                                         smem_raw) + 160));
       for (int64_t i = threadIdx.x - 64; i < p.N; i += 32 * EPI_WARPS) sb[i] = e.bias[i];
       named_bar_sync(1, 32 * EPI_WARPS);
       bias = sb;
@@ -537,7 +545,28 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           // 32 x 32 chunk; rows/cols beyond M/N are clipped by the map
           float x[32];
           epi_math<EPI>(p, e, v, nb, x, bias);
-          if (e.residual) {  // fp32, plain 2-D layout (same map as C)
+          if (p.res_tma) {
+            // residual chunk arrives in this chunk's box (TMA, SW128 like the
+            // store); issued one chunk ahead (or now, at a tile's first chunk)
+            const int bx = (int)(chunk_ctr & 1);
+            uint8_t *rbox = wreg + bx * 4096;
+            uint64_t *rb = &rbar[ew * 2 + bx];
+            if (ci == 0) {
+              if (lane == 0) {
+                bulk_wait_read<1>();
+                mbar_expect_tx(rb, 4096);
+                tma_load_2d(rbox, &tmR, rb, (int)nb, (int)(mt * BM + q * 32));
+              }
+              __syncwarp();
+            }
+            mbar_wait(rb, (rph >> bx) & 1u);
+            rph ^= 1u << bx;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) {
+              const float4 r4 = *reinterpret_cast<const float4 *>(rbox + lane * 128 + ((c ^ (lane & 7)) << 4));
+              x[4 * c] += r4.x; x[4 * c + 1] += r4.y; x[4 * c + 2] += r4.z; x[4 * c + 3] += r4.w;
+            }
+          } else if (e.residual) {  // fp32, plain 2-D layout (same map as C)
             if (row_ok) {
               const float4 *rp = reinterpret_cast<const float4 *>(e.residual + rbase + nb);
               if (nb + 32 <= p.N) {
@@ -603,6 +632,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                            (int)(mrow % p.rdiv), (int)(mrow / p.rdiv));
             }
             bulk_commit();
+            if (p.res_tma && ci + 1 < nch) {  // next chunk's residual into the other box
+              const int bx = (int)(chunk_ctr & 1);
+              bulk_wait_read<1>();  // that box's previous store has read it
+              mbar_expect_tx(&rbar[ew * 2 + bx], 4096);
+              tma_load_2d(wreg + bx * 4096, &tmR, &rbar[ew * 2 + bx], (int)(nb + 64), mrow);
+            }
           }
           continue;
         }
@@ -794,6 +829,16 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   CUtensorMap mc;
   p.box_w = 32;
   p.store_mode = p.split > 1 ? 0 : make_store_map(&mc, d, &p.box_w);
+  // fp32 residual through TMA (same geometry as C's 2-D map, its own pointer)
+  CUtensorMap mr = mc;
+  p.res_tma = 0;
+  if (p.store_mode == 1 && d->residual && d->dtype_c == EVO_F32) {
+    evo_gemm_desc dr = *d;
+    dr.C.ptr = const_cast<float *>(d->residual);
+    dr.residual = nullptr;
+    int bw = 32;
+    if (make_store_map(&mr, &dr, &bw) == 1) p.res_tma = 1;
+  }
   p.cdiv = d->C.cdiv > 0 ? d->C.cdiv : 1;
   p.rdiv = d->C.rdiv > 0 ? d->C.rdiv : 1;
   if (p.store_mode == 0 || p.store_mode == 4) mc = ma;  // unused
@@ -804,7 +849,7 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   }
   p.bias_smem = (d->bias && d->N <= BIAS_SMEM_MAX && p.split == 1) ? 1 : 0;
   const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) +
-                      (size_t)EPI_WARPS * 8192 + 256 + (size_t)BIAS_SMEM_MAX * 4;
+                      (size_t)EPI_WARPS * 8192 + 512 + (size_t)BIAS_SMEM_MAX * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
@@ -812,7 +857,8 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
     attr_set = true;
   }
   int64_t grid = std::min<int64_t>(p.num_tiles, (int64_t)num_sms());
-  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, mc, p);
+  if (!p.res_tma) mr = mc;  // unused
+  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, mc, mr, p);
   EVO_LAUNCHED("gemm_tc_kernel");
   if (p.split > 1) return gemm_splitk_reduce(d, p.split, p.partial, st);
   return EVO_OK;

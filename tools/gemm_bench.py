@@ -25,6 +25,7 @@ def main():
     ap.add_argument("--out", default="bf16", choices=["bf16", "f32"])
     ap.add_argument("--opm-map", action="store_true", help="two-level [i,j,p,q] output map")
     ap.add_argument("--split", type=int, default=1)
+    ap.add_argument("--residual", action="store_true", help="fp32 residual operand (f32 out)")
     ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
     M, Nn, Kd = a.M, a.N, a.K
@@ -44,8 +45,11 @@ def main():
     epi = {"none": N.EPI_NONE, "bias": N.EPI_NONE, "relu": N.EPI_RELU,
            "sigmoid": N.EPI_SIGMOID_FROM}[a.epi]
 
+    R = torch.randn(M * Nn, device="cuda") if a.residual else None
+
     def run():
-        K.gemm(Am, Bm, Cm, M, Nn, Kd, bias=bias, epi=epi, col0=Nn // 4 * 3, split_k=a.split)
+        K.gemm(Am, Bm, Cm, M, Nn, Kd, bias=bias, epi=epi, col0=Nn // 4 * 3, split_k=a.split,
+               residual=R)
 
     # graph-replayed (host launch overhead excluded)
     from tools.ew_bench import timeit
