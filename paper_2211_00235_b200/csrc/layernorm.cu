@@ -88,6 +88,33 @@ ln_fwd_vec_kernel(int64_t rows, const TX *__restrict__ x, int64_t x_rs,
   }
 }
 
+// Sum 8 per-lane values over the warp with a transposing butterfly (9
+// shuffles instead of 8 x 5): returns, in every lane, the total of value
+// h8(lane) = 4*bit4 + 2*bit3 + bit2 of the lane id (fixed order: bitwise
+// reproducible).
+__device__ __forceinline__ float warp_sum8_scatter(const float (&v)[8], int lane) {
+  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
+  float w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float send = u16 ? v[k] : v[k + 4];
+    const float keep = u16 ? v[k + 4] : v[k];
+    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
+  }
+  float x2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float send = u8 ? w[k] : w[k + 2];
+    const float keep = u8 ? w[k + 2] : w[k];
+    x2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
+  }
+  const float send = u4 ? x2[0] : x2[1];
+  float y = (u4 ? x2[1] : x2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
+  y += __shfl_xor_sync(0xffffffffu, y, 2);
+  y += __shfl_xor_sync(0xffffffffu, y, 1);
+  return y;
+}
+
 // -------------------------------------- forward + pair-bias projection
 // c_z = 128 rows (NV = 1): y = LN(x) (bf16, optional) and
 // proj[hh*p_rs + row] = sum_c bf16(y[row,c]) * Wp[c*NH + hh]   (NH <= 8)
@@ -98,51 +125,58 @@ ln_fwd_proj_kernel(int64_t rows, const float *__restrict__ x, const float *__res
                    const float *__restrict__ beta, bf16 *__restrict__ y,
                    float *__restrict__ mean_out, float *__restrict__ rstd_out, float eps,
                    const bf16 *__restrict__ Wp, int nh, float *__restrict__ proj, int64_t p_rs) {
-  constexpr int cols = 128;
+  // Like ln_fwd_vec_kernel (a few rows per warp, many small blocks, loads
+  // issued before any reduction) with the projection weights staged in smem
+  // as fp32 [128][NH] (read as 16-byte vectors, no registers held).
+  static_assert(NH == 8, "transposing reduction is written for 8 heads");
+  constexpr int cols = 128, RPW = 2;
+  __shared__ __align__(16) float sW[cols * NH];
+  for (int i = threadIdx.x; i < cols * NH; i += blockDim.x) {
+    const int c = i / NH, hh = i % NH;
+    sW[i] = hh < nh ? __bfloat162float(Wp[c * nh + hh]) : 0.f;
+  }
+  __syncthreads();
   const int lane = threadIdx.x & 31;
-  float W[4][NH];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int hh = 0; hh < NH; ++hh)
-      W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
+  const int64_t row0 = ((int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * RPW;
   const float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane);
   const float4 b4 = *reinterpret_cast<const float4 *>(beta + 4 * lane);
-  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5); row < rows;
-       row += (int64_t)gridDim.x * LN_WARPS) {
-    float v[4];
-    Vec<float, 4>::load(x + row * cols + 4 * lane, v);
+  const int hsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  float v[RPW][4];
+#pragma unroll
+  for (int r = 0; r < RPW; ++r)
+    if (row0 + r < rows) Vec<float, 4>::load(x + (row0 + r) * cols + 4 * lane, v[r]);
+#pragma unroll
+  for (int r = 0; r < RPW; ++r) {
+    const int64_t row = row0 + r;
+    if (row >= rows) break;
     float s = 0.f;  // same summation order as ln_fwd_vec_kernel (bitwise equal y, mu, rstd)
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s += v[j];
+    for (int j = 0; j < 4; ++j) s += v[r][j];
     const float mu = warp_sum(s) * (1.f / cols);
     float q = 0.f;
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
-      const float d = v[j] - mu;
+      const float d = v[r][j] - mu;
       q += d * d;
     }
     const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
-    float o[4] = {(v[0] - mu) * rs * g4.x + b4.x, (v[1] - mu) * rs * g4.y + b4.y,
-                  (v[2] - mu) * rs * g4.z + b4.z, (v[3] - mu) * rs * g4.w + b4.w};
+    float o[4] = {(v[r][0] - mu) * rs * g4.x + b4.x, (v[r][1] - mu) * rs * g4.y + b4.y,
+                  (v[r][2] - mu) * rs * g4.z + b4.z, (v[r][3] - mu) * rs * g4.w + b4.w};
 #pragma unroll
     for (int j = 0; j < 4; ++j) o[j] = __bfloat162float(__float2bfloat16_rn(o[j]));
     if (y) Vec<bf16, 4>::store(y + row * cols + 4 * lane, o);
-    float pr[NH];
+    float pr[NH] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
 #pragma unroll
-    for (int hh = 0; hh < NH; ++hh) {
-      float t = 0.f;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) t = fmaf(o[j], W[j][hh], t);
-      pr[hh] = warp_sum(t);
+    for (int j = 0; j < 4; ++j) {
+      const float4 w0 = *reinterpret_cast<const float4 *>(sW + (4 * lane + j) * NH);
+      const float4 w1 = *reinterpret_cast<const float4 *>(sW + (4 * lane + j) * NH + 4);
+      pr[0] = fmaf(o[j], w0.x, pr[0]); pr[1] = fmaf(o[j], w0.y, pr[1]);
+      pr[2] = fmaf(o[j], w0.z, pr[2]); pr[3] = fmaf(o[j], w0.w, pr[3]);
+      pr[4] = fmaf(o[j], w1.x, pr[4]); pr[5] = fmaf(o[j], w1.y, pr[5]);
+      pr[6] = fmaf(o[j], w1.z, pr[6]); pr[7] = fmaf(o[j], w1.w, pr[7]);
     }
-    if (lane < nh) {
-      float val = 0.f;
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh)
-        if (lane == hh) val = pr[hh];
-      proj[(int64_t)lane * p_rs + row] = val;
-    }
+    const float tot = warp_sum8_scatter(pr, lane);
+    if ((lane & 3) == 0 && hsel < nh) proj[(int64_t)hsel * p_rs + row] = tot;
     if (lane == 0) {
       mean_out[row] = mu;
       rstd_out[row] = rs;
@@ -604,8 +638,8 @@ int layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamm
   EVO_REQUIRE(aligned16(x) && aligned16(gamma) && aligned16(beta) && (!y || aligned16(y)), EVO_EARG,
               "layernorm_fwd_proj: operands must be 16-byte aligned");
   if (rows == 0) return EVO_OK;
-  const int blocks = (int)std::min<int64_t>((rows + LN_WARPS - 1) / LN_WARPS, (int64_t)num_sms() * 8);
-  ln_fwd_proj_kernel<8><<<blocks, LN_WARPS * 32, 0, st>>>(
+  const int64_t blocks = (rows + 2 * LN_WARPS - 1) / (2 * LN_WARPS);
+  ln_fwd_proj_kernel<8><<<(unsigned)blocks, LN_WARPS * 32, 0, st>>>(
       rows, x, gamma, beta, reinterpret_cast<bf16 *>(y), mean, rstd, eps,
       reinterpret_cast<const bf16 *>(Wp), nh, proj, p_rs);
   EVO_LAUNCHED("ln_fwd_proj_kernel");

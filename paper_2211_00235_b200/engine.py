@@ -260,33 +260,26 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     ctx = {}
     xh = _empty((rows, c_io), act, dev)
     mu, rs = _empty(rows, F32, dev), _empty(rows, F32, dev)
-    # the pair-bias projection fuses into the LayerNorm of its input on the
-    # bf16 path (c_z = 128, h <= 8): bias = LN(z) Wb without re-reading LN(z)
+    K.layernorm(x, rows, c_io, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
+    # the pair-bias projection's backward fuses into the LayerNorm backward of
+    # its input on the bf16 path (c_z = 128, h <= 8); in the forward the
+    # separate projection kernel is faster than a fused LayerNorm
+    # (evo_layernorm_fwd_proj: the per-row 8-way reduction costs occupancy)
     fuse_bias = name != "col_attn" and _bias_fusable(cfg, act)
-    bias = _empty((h, r2), F32, dev) if name != "col_attn" else None
-    if fuse_bias and name != "row_attn":
-        K.layernorm_proj(x, rows, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps,
-                         pk["Wb"], h, bias, r2)
-    else:
-        K.layernorm(x, rows, c_io, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
     ctx.update(x=x, xh=xh, mu=mu, rs=rs, fuse_bias=fuse_bias)
+    bias = None
     if name != "col_attn":
         if name == "row_attn":
+            zh = _empty((r2, cfg.c_z), act, dev)
             zmu, zrs = _empty(r2, F32, dev), _empty(r2, F32, dev)
-            if fuse_bias:  # LN_z(z) itself is not needed: the backward recomputes it
-                K.layernorm_proj(z, r2, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], None, zmu, zrs,
-                                 cfg.eps, pk["Wb"], h, bias, r2)
-                ctx.update(z=z, zmu=zmu, zrs=zrs)
-            else:
-                zh = _empty((r2, cfg.c_z), act, dev)
-                K.layernorm(z, r2, cfg.c_z, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], zh, zmu, zrs,
-                            cfg.eps)
-                ctx.update(z=z, zh=zh, zmu=zmu, zrs=zrs)
+            K.layernorm(z, r2, cfg.c_z, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], zh, zmu, zrs,
+                        cfg.eps)
+            ctx.update(z=z, zh=zh, zmu=zmu, zrs=zrs)
         else:
             zh = xh
-        if not fuse_bias:
-            # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*r2 + row)
-            K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, r2), r2, h, cfg.c_z)
+        bias = _empty((h, r2), F32, dev)
+        # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*r2 + row)
+        K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, r2), r2, h, cfg.c_z)
         ctx["bias"] = bias
     proj = _empty((rows, 4 * hc), act, dev)
     K.linear(xh, rows, c_io, pk["Wqkvg"], 4 * hc, 4 * hc, proj, 4 * hc, bias=pk["bqkvg"],
