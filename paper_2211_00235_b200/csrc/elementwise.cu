@@ -360,12 +360,26 @@ __global__ void relu_bwd_kernel(int64_t n, const void *dh, const void *h, void *
 
 constexpr int SQ_BLOCKS = 512;
 
-__global__ void sq_partial_kernel(int64_t n, const float *x, float *part) {
+// One pass over x: per-block partial sums of x^2 and (dx != NULL) the
+// gradient dx = (2/n) x of mean(x^2), 16-byte vectors when aligned.
+__global__ void sq_partial_kernel(int64_t n, const float *x, float *part, float *dx) {
   __shared__ float red[32];
   float s = 0.f;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    s += x[e] * x[e];
+  const float sc = 2.0f / (float)n;
+  const bool vec = ((reinterpret_cast<uintptr_t>(x) | reinterpret_cast<uintptr_t>(dx)) & 15) == 0;
+  const int64_t n4 = vec ? n / 4 : 0;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4 *>(x) + e);
+    s += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+    if (dx) reinterpret_cast<float4 *>(dx)[e] = make_float4(sc * v.x, sc * v.y, sc * v.z, sc * v.w);
+  }
+  for (int64_t e = 4 * n4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const float v = x[e];
+    s += v * v;
+    if (dx) dx[e] = sc * v;
+  }
   s = warp_sum(s);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
@@ -376,18 +390,19 @@ __global__ void sq_partial_kernel(int64_t n, const float *x, float *part) {
   }
 }
 
+// Fixed-order double-precision sum of the block partials (one 256-thread
+// block: strided per-thread sums, then an ordered tree).
 __global__ void sq_final_kernel(int nblk, int64_t n, const float *part, float *out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double s = 0.0;
-    for (int b = 0; b < nblk; ++b) s += part[b];
-    out[0] += (float)(s / (double)n);
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += part[b];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
   }
-}
-
-__global__ void scale_kernel(int64_t n, const float *x, float alpha, float *y) {
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
-       e += (int64_t)gridDim.x * blockDim.x)
-    y[e] = alpha * x[e];
+  if (threadIdx.x == 0) out[0] += (float)(red[0] / (double)n);
 }
 
 __global__ void add_kernel(int64_t n, const float *a, const float *b, float *o) {
@@ -570,14 +585,10 @@ int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaS
 
 int sq_mean(int64_t n, const float *x, float *out, float *dx, void *ws, cudaStream_t st) {
   float *part = reinterpret_cast<float *>(ws);
-  sq_partial_kernel<<<SQ_BLOCKS, 256, 0, st>>>(n, x, part);
+  sq_partial_kernel<<<SQ_BLOCKS, 256, 0, st>>>(n, x, part, dx);
   EVO_LAUNCHED("sq_partial_kernel");
-  sq_final_kernel<<<1, 32, 0, st>>>(SQ_BLOCKS, n, part, out);
+  sq_final_kernel<<<1, 256, 0, st>>>(SQ_BLOCKS, n, part, out);
   EVO_LAUNCHED("sq_final_kernel");
-  if (dx) {
-    scale_kernel<<<ew_blocks(n), 256, 0, st>>>(n, x, 2.0f / (float)n, dx);
-    EVO_LAUNCHED("scale_kernel");
-  }
   return EVO_OK;
 }
 

@@ -298,9 +298,12 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     return x_new, ctx
 
 
-def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None):
+def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None, dz_res=None):
     """Returns (dx [rows, c_io] fp32, dz_row or None).  handoff: the emit
-    dict of the producer of dx_new (see _ln_bwd_out); emit: this sub-op's."""
+    dict of the producer of dx_new (see _ln_bwd_out); emit: this sub-op's.
+    dz_res (row attention, fused path only): added to dz_row inside its
+    LayerNorm backward (the block join dz_in = dz_pair + dz_row, one fp32
+    addition either way); returns (dx, dz_row + dz_res, True) then."""
     dev = dx_new.device
     h, hc, ch = cfg.h, cfg.hc, cfg.c_head
     nb, L, rb, rl, rows = attn_geometry(name, cfg)
@@ -334,7 +337,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
             dz_row = _empty((r2, cfg.c_z), F32, dev)
             K.layernorm_bwd_proj(None, ctx["z"], r2, ctx["zmu"], ctx["zrs"], P[f"{px}.lnz_g"],
                                  P[f"{px}.lnz_b"], dbias, r2, pk["Wb"], h, dz_row, G["lnz_g"],
-                                 G["lnz_b"], G["Wb"])
+                                 G["lnz_b"], G["Wb"], dres=dz_res)
         else:
             dres = dx_new if ctx["resid"] else None
             dx = _empty((rows, c_io), F32, dev)
@@ -370,6 +373,10 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
                    cfg.c_z, h, accumulate=True)
     dx = _ln_bwd_out(dxh, ctx["x"], rows, c_io, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
                      G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
+    if dz_res is not None:
+        if ctx["fuse_bias"]:
+            return dx, dz_row, True
+        return dx, dz_row, False
     return dx, dz_row
 
 
@@ -633,9 +640,10 @@ def msa_emit(G):
     return dict(bias=G["msa_transition"]["b2"])
 
 
-def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None):
+def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None, dz_pair=None):
     """dm: grad of the MSA-track output (incl. the OPM contribution; handoff:
-    the OPM backward's emit dict); returns (dm_in, dz_row)."""
+    the OPM backward's emit dict); returns (dm_in, dz_row), or with dz_pair
+    given (single-process block) (dm_in, dz_in = dz_pair + dz_row)."""
     e1 = dict(bias=G["col_attn"]["bo"])
     dm = transition_bwd(P, f"blk{blk}.msa_transition", pk["msa_transition"],
                         G["msa_transition"], ctxs["msa_transition"], dm, cfg, act,
@@ -643,9 +651,18 @@ def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None):
     e2 = dict(bias=G["row_attn"]["bo"])
     dm, _ = attn_bwd("col_attn", P, f"blk{blk}.col_attn", pk["col_attn"], G["col_attn"],
                      ctxs["col_attn"], dm, cfg, act, handoff=e1, emit=e2)
-    dm, dz_row = attn_bwd("row_attn", P, f"blk{blk}.row_attn", pk["row_attn"], G["row_attn"],
-                          ctxs["row_attn"], dm, cfg, act, handoff=e2)
-    return dm, dz_row
+    if dz_pair is None:
+        dm, dz_row = attn_bwd("row_attn", P, f"blk{blk}.row_attn", pk["row_attn"],
+                              G["row_attn"], ctxs["row_attn"], dm, cfg, act, handoff=e2)
+        return dm, dz_row
+    dm, dz, joined = attn_bwd("row_attn", P, f"blk{blk}.row_attn", pk["row_attn"],
+                              G["row_attn"], ctxs["row_attn"], dm, cfg, act, handoff=e2,
+                              dz_res=dz_pair)
+    if not joined:
+        dz_in = torch.empty_like(dz_pair)
+        K.add(dz_pair, dz, dz_in)
+        dz = dz_in
+    return dm, dz
 
 
 def block_fwd(P, blk, pk, m, z, cfg, act):
@@ -673,7 +690,8 @@ def block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act):
     dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act, dm_out,
                   cfg, act, emit=e0)
     dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act, dz_act=dz_act)
-    dm_in, dz_row = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm3, cfg, act, handoff=e0)
-    dz_in = torch.empty_like(dz_pair)
-    K.add(dz_pair, dz_row, dz_in)
+    # dz_in = dz_pair + dz_row (the BP allreduce's two operands), joined
+    # inside the row attention's LayerNorm backward when fused
+    dm_in, dz_in = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm3, cfg, act, handoff=e0,
+                                  dz_pair=dz_pair)
     return dm_in, dz_in
