@@ -330,6 +330,70 @@ __global__ void outgate_bwd_kernel(int64_t rows, int64_t cols, const float *dz, 
   }
 }
 
+// bf16 fast paths of the out-gate (cols % 8 == 0, 16-byte aligned rows):
+// one thread per 8 consecutive columns.
+__device__ __forceinline__ void unpack8(const uint4 &u, float (&f)[8]) {
+  const uint32_t *w = reinterpret_cast<const uint32_t *>(&u);
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    const float2 t = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&w[j]));
+    f[2 * j] = t.x;
+    f[2 * j + 1] = t.y;
+  }
+}
+__device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
+  uint32_t w[4];
+#pragma unroll
+  for (int j = 0; j < 4; ++j) {
+    __nv_bfloat162 h = __floats2bfloat162_rn(f[2 * j], f[2 * j + 1]);
+    w[j] = *reinterpret_cast<uint32_t *>(&h);
+  }
+  return make_uint4(w[0], w[1], w[2], w[3]);
+}
+__global__ void outgate_fwd_bf16x8_kernel(int64_t rows, int64_t cols, const float *z,
+                                          const bf16 *g, int64_t g_rs, const bf16 *o,
+                                          int64_t o_rs, float *znew) {
+  const int64_t per_row = cols / 8, total = rows * per_row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / per_row, c = (e % per_row) * 8;
+    float gv[8], ov[8];
+    unpack8(__ldg(reinterpret_cast<const uint4 *>(g + r * g_rs + c)), gv);
+    unpack8(__ldg(reinterpret_cast<const uint4 *>(o + r * o_rs + c)), ov);
+    const float4 *zp = reinterpret_cast<const float4 *>(z + r * cols + c);
+    const float4 z0 = __ldg(zp), z1 = __ldg(zp + 1);
+    float4 *dst = reinterpret_cast<float4 *>(znew + r * cols + c);
+    dst[0] = make_float4(z0.x + gv[0] * ov[0], z0.y + gv[1] * ov[1], z0.z + gv[2] * ov[2],
+                         z0.w + gv[3] * ov[3]);
+    dst[1] = make_float4(z1.x + gv[4] * ov[4], z1.y + gv[5] * ov[5], z1.z + gv[6] * ov[6],
+                         z1.w + gv[7] * ov[7]);
+  }
+}
+__global__ void outgate_bwd_bf16x8_kernel(int64_t rows, int64_t cols, const float *dz,
+                                          const bf16 *g, int64_t g_rs, const bf16 *o,
+                                          int64_t o_rs, bf16 *do_, int64_t do_rs, bf16 *dgp,
+                                          int64_t dg_rs) {
+  const int64_t per_row = cols / 8, total = rows * per_row;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / per_row, c = (e % per_row) * 8;
+    float gv[8], ov[8], d[8], a[8], b[8];
+    unpack8(__ldg(reinterpret_cast<const uint4 *>(g + r * g_rs + c)), gv);
+    unpack8(__ldg(reinterpret_cast<const uint4 *>(o + r * o_rs + c)), ov);
+    const float4 *dp = reinterpret_cast<const float4 *>(dz + r * cols + c);
+    const float4 d0 = __ldg(dp), d1 = __ldg(dp + 1);
+    d[0] = d0.x; d[1] = d0.y; d[2] = d0.z; d[3] = d0.w;
+    d[4] = d1.x; d[5] = d1.y; d[6] = d1.z; d[7] = d1.w;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      a[j] = d[j] * gv[j];
+      b[j] = d[j] * ov[j] * gv[j] * (1.f - gv[j]);
+    }
+    *reinterpret_cast<uint4 *>(do_ + r * do_rs + c) = pack8(a);
+    *reinterpret_cast<uint4 *>(dgp + r * dg_rs + c) = pack8(b);
+  }
+}
+
 __global__ void relu_bwd_bf16x8_kernel(int64_t n8, const uint4 *dh, const uint4 *h, uint4 *dpre) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -549,6 +613,15 @@ int trimul_gate_bwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, 
 int outgate_fwd(int dt, int64_t rows, int64_t cols, const float *z, const void *g, int64_t g_rs,
                 const void *o, int64_t o_rs, float *znew, cudaStream_t st) {
   int nb = ew_blocks(rows * cols);
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (dt == EVO_BF16 && cols % 8 == 0 && g_rs % 8 == 0 && o_rs % 8 == 0 && al16(z) && al16(g) &&
+      al16(o) && al16(znew)) {
+    outgate_fwd_bf16x8_kernel<<<ew_blocks(rows * cols / 8), 256, 0, st>>>(
+        rows, cols, z, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
+        o_rs, znew);
+    EVO_LAUNCHED("outgate_fwd_bf16x8_kernel");
+    return EVO_OK;
+  }
   if (dt == EVO_F32) outgate_fwd_kernel<float><<<nb, 256, 0, st>>>(rows, cols, z, g, g_rs, o, o_rs, znew);
   else outgate_fwd_kernel<bf16><<<nb, 256, 0, st>>>(rows, cols, z, g, g_rs, o, o_rs, znew);
   EVO_LAUNCHED("outgate_fwd_kernel");
@@ -559,6 +632,16 @@ int outgate_bwd(int dt, int64_t rows, int64_t cols, const float *dz, const void 
                 const void *o, int64_t o_rs, void *do_, int64_t do_rs, void *dgp, int64_t dg_rs,
                 cudaStream_t st) {
   int nb = ew_blocks(rows * cols);
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  if (dt == EVO_BF16 && cols % 8 == 0 && g_rs % 8 == 0 && o_rs % 8 == 0 && do_rs % 8 == 0 &&
+      dg_rs % 8 == 0 && al16(dz) && al16(g) && al16(o) && al16(do_) && al16(dgp)) {
+    outgate_bwd_bf16x8_kernel<<<ew_blocks(rows * cols / 8), 256, 0, st>>>(
+        rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs,
+        reinterpret_cast<const bf16 *>(o), o_rs, reinterpret_cast<bf16 *>(do_), do_rs,
+        reinterpret_cast<bf16 *>(dgp), dg_rs);
+    EVO_LAUNCHED("outgate_bwd_bf16x8_kernel");
+    return EVO_OK;
+  }
   if (dt == EVO_F32)
     outgate_bwd_kernel<float><<<nb, 256, 0, st>>>(rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgp, dg_rs);
   else

@@ -396,6 +396,89 @@ ln_bwd_proj_kernel(int64_t rows, const float *__restrict__ dy, const float *__re
   }
 }
 
+// ---------------------------------------------- channel-first (c <= 32)
+// The triangle multiplication normalises p[c, i, j] over c with the data
+// channel-first (x[c*rows + row]): one thread per row, the C channel values
+// in registers, loads coalesced across threads for each channel.
+template <int C, typename TY>
+__global__ void __launch_bounds__(128)
+ln_fwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ x,
+                 const float *__restrict__ gamma, const float *__restrict__ beta,
+                 TY *__restrict__ y, int64_t y_rs, float *__restrict__ mean_out,
+                 float *__restrict__ rstd_out, float eps) {
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  if (row >= rows) return;
+  float v[C];
+  float s = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    v[c] = c < cols ? __ldg(&x[(int64_t)c * rows + row]) : 0.f;
+    s += v[c];
+  }
+  const float inv_n = 1.f / (float)cols;
+  const float mu = s * inv_n;
+  float q = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float d = c < cols ? v[c] - mu : 0.f;
+    q += d * d;
+  }
+  const float rs = 1.f / sqrtf(q * inv_n + eps);
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (c < cols) y[row * y_rs + c] = from_f<TY>((v[c] - mu) * rs * gamma[c] + beta[c]);
+  mean_out[row] = mu;
+  rstd_out[row] = rs;
+}
+
+// partial[block][2][C]: dgamma, dbeta of the block's 128 rows (fixed order)
+template <int C, typename TDX>
+__global__ void __launch_bounds__(128)
+ln_bwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ dy, int64_t dy_rs,
+                 const float *__restrict__ x, const float *__restrict__ mean,
+                 const float *__restrict__ rstd, const float *__restrict__ gamma,
+                 TDX *__restrict__ dx, float *__restrict__ partial) {
+  __shared__ float wred[4][2 * C];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const bool ok = row < rows;
+  const float mu = ok ? mean[row] : 0.f, rs = ok ? rstd[row] : 0.f;
+  float xh[C], dv[C];
+  float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const bool in = ok && c < cols;
+    const float xv = in ? __ldg(&x[(int64_t)c * rows + row]) : 0.f;
+    dv[c] = in ? __ldg(&dy[row * dy_rs + c]) : 0.f;
+    xh[c] = (xv - mu) * rs;
+    const float d = dv[c] * (in ? gamma[c] : 0.f);
+    s1 += d;
+    s2 += d * xh[c];
+  }
+  const float inv_n = 1.f / (float)cols;
+  const float m1 = s1 * inv_n, m2 = s2 * inv_n;
+#pragma unroll
+  for (int c = 0; c < C; ++c)
+    if (ok && c < cols)
+      dx[(int64_t)c * rows + row] = from_f<TDX>(rs * (dv[c] * gamma[c] - m1 - xh[c] * m2));
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const float pg = warp_sum(dv[c] * xh[c]);
+    const float pb = warp_sum(dv[c]);
+    if (lane == 0) {
+      wred[warp][c] = pg;
+      wred[warp][C + c] = pb;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < 2 * C) {
+    const int which = threadIdx.x / C, c = threadIdx.x % C;
+    const float t = (wred[0][threadIdx.x] + wred[1][threadIdx.x]) +
+                    (wred[2][threadIdx.x] + wred[3][threadIdx.x]);
+    if (c < cols) partial[((int64_t)blockIdx.x * 2 + which) * cols + c] = t;
+  }
+}
+
 // -------------------------------------------------------- generic backward
 template <typename TDY, typename TX, typename TDX, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
@@ -513,6 +596,14 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   dim3 grid((unsigned)((rows + LN_WARPS - 1) / LN_WARPS));
   const TX *xp = reinterpret_cast<const TX *>(x);
   TY *yp = reinterpret_cast<TY *>(y);
+  if constexpr (std::is_same<TX, float>::value) {
+    if (x_rs == 1 && x_cs == rows && cols <= 32) {  // channel-first
+      ln_fwd_cf_kernel<32, TY><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
+          rows, cols, xp, gamma, beta, yp, y_rs, mean, rstd, eps);
+      EVO_LAUNCHED("ln_fwd_cf_kernel");
+      return EVO_OK;
+    }
+  }
   const bool vec = x_cs == 1 && (cols == 128 || cols == 256) && x_rs % 4 == 0 && y_rs % 4 == 0 &&
                    aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta);
   if (vec) {
@@ -555,6 +646,23 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
                    aligned16(dx) && aligned16(gamma) && (!dres || aligned16(dres)) &&
                    (!dx_act || (aligned16(dx_act) && dxa_rs % 4 == 0));
   int nparts = 2;
+  if constexpr (std::is_same<TDY, float>::value && std::is_same<TX, float>::value) {
+    if (x_rs == 1 && x_cs == rows && dx_rs == 1 && dx_cs == rows && cols <= 32 && !dres &&
+        !dx_act && !dx_colsum) {  // channel-first (triangle multiplication p)
+      const int nb = (int)((rows + 127) / 128);
+      EVO_REQUIRE(!want || nb * 2 <= LN_BWD_BLOCKS * 11, EVO_EUNSUP,
+                  "layernorm_bwd: channel-first rows=%lld exceed the workspace", (long long)rows);
+      ln_bwd_cf_kernel<32, TDX><<<nb, 128, 0, st>>>(rows, cols, dyp, dy_rs, xp, mean, rstd, gamma,
+                                                  dxp, ws);
+      EVO_LAUNCHED("ln_bwd_cf_kernel");
+      if (want) {
+        ln_param_reduce_kernel<<<(2 * cols + 31) / 32, 512, 0, st>>>(nb, cols, 2, ws, dgamma,
+                                                                     dbeta, nullptr, acc);
+        EVO_LAUNCHED("ln_param_reduce_kernel");
+      }
+      return EVO_OK;
+    }
+  }
   if (vec) {
     bf16 *dxa = reinterpret_cast<bf16 *>(dx_act);
     nparts = want ? (dx_colsum ? 3 : 2) : 0;
