@@ -424,6 +424,26 @@ ln_fwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ x,
     q += d * d;
   }
   const float rs = 1.f / sqrtf(q * inv_n + eps);
+  if constexpr (std::is_same<TY, bf16>::value && C % 8 == 0) {
+    if (cols == C && (y_rs % 8) == 0 && ((reinterpret_cast<uintptr_t>(y) & 15) == 0)) {
+#pragma unroll
+      for (int c8 = 0; c8 < C; c8 += 8) {  // 16-byte stores of the row
+        float o[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) o[j] = (v[c8 + j] - mu) * rs * gamma[c8 + j] + beta[c8 + j];
+        uint32_t w[4];
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          __nv_bfloat162 h2 = __floats2bfloat162_rn(o[2 * j], o[2 * j + 1]);
+          w[j] = *reinterpret_cast<uint32_t *>(&h2);
+        }
+        *reinterpret_cast<uint4 *>(y + row * y_rs + c8) = make_uint4(w[0], w[1], w[2], w[3]);
+      }
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+      return;
+    }
+  }
 #pragma unroll
   for (int c = 0; c < C; ++c)
     if (c < cols) y[row * y_rs + c] = from_f<TY>((v[c] - mu) * rs * gamma[c] + beta[c]);
@@ -445,11 +465,20 @@ ln_bwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ dy, int64_t d
   const float mu = ok ? mean[row] : 0.f, rs = ok ? rstd[row] : 0.f;
   float xh[C], dv[C];
   float s1 = 0.f, s2 = 0.f;
+  const bool dvec = ok && cols == C && (dy_rs % 4) == 0 &&
+                    ((reinterpret_cast<uintptr_t>(dy) & 15) == 0);
+  if (dvec) {  // the row's gradients as 16-byte loads
+#pragma unroll
+    for (int c4 = 0; c4 < C; c4 += 4) {
+      const float4 t = __ldg(reinterpret_cast<const float4 *>(dy + row * dy_rs + c4));
+      dv[c4] = t.x; dv[c4 + 1] = t.y; dv[c4 + 2] = t.z; dv[c4 + 3] = t.w;
+    }
+  }
 #pragma unroll
   for (int c = 0; c < C; ++c) {
     const bool in = ok && c < cols;
     const float xv = in ? __ldg(&x[(int64_t)c * rows + row]) : 0.f;
-    dv[c] = in ? __ldg(&dy[row * dy_rs + c]) : 0.f;
+    if (!dvec) dv[c] = in ? __ldg(&dy[row * dy_rs + c]) : 0.f;
     xh[c] = (xv - mu) * rs;
     const float d = dv[c] * (in ? gamma[c] : 0.f);
     s1 += d;
