@@ -245,25 +245,42 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
     for (int j = 0; j < 4; ++j) pg[i][j] = pb[i][j] = pc[i][j] = 0.f;
   }
   constexpr float inv_n = 1.f / cols;
-  for (int64_t row = (int64_t)blockIdx.x * LN_WARPS + warp; row < rows;
-       row += (int64_t)gridDim.x * LN_WARPS) {
-    const float mu = mean[row], rs = rstd[row];
+  // A warp walks rows with a stride; the loads of its next row are issued
+  // before the current row's reductions (two row buffers, swapped by
+  // unrolling the loop by two), so each warp keeps two rows in flight.
+  struct RowIn {
+    float dv[NV][4], xv[NV][4], dr[NV][4];
+    float mu, rs;
+  };
+  auto load = [&](int64_t row, RowIn &in) {
+    in.mu = mean[row];
+    in.rs = rstd[row];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = 4 * lane + 128 * i;
+      Vec<TDY, 4>::load(dy + row * dy_rs + c, in.dv[i]);
+      Vec<TX, 4>::load(x + row * x_rs + c, in.xv[i]);
+      if (dres) {
+        const float4 d4 = *reinterpret_cast<const float4 *>(dres + row * dx_rs + c);
+        in.dr[i][0] = d4.x; in.dr[i][1] = d4.y; in.dr[i][2] = d4.z; in.dr[i][3] = d4.w;
+      }
+    }
+  };
+  auto process = [&](int64_t row, const RowIn &in) {
+    const float mu = in.mu, rs = in.rs;
     float xh[NV][4], dxh[NV][4];
     float s1 = 0.f, s2 = 0.f;
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const int c = 4 * lane + 128 * i;
-      float dv[4], xv[4];
-      Vec<TDY, 4>::load(dy + row * dy_rs + c, dv);
-      Vec<TX, 4>::load(x + row * x_rs + c, xv);
 #pragma unroll
       for (int j = 0; j < 4; ++j) {
-        xh[i][j] = (xv[j] - mu) * rs;
-        dxh[i][j] = dv[j] * g[i][j];
+        const float dv = in.dv[i][j];
+        xh[i][j] = (in.xv[i][j] - mu) * rs;
+        dxh[i][j] = dv * g[i][j];
         s1 += dxh[i][j];
         s2 += dxh[i][j] * xh[i][j];
-        pg[i][j] += dv[j] * xh[i][j];
-        pb[i][j] += dv[j];
+        pg[i][j] += dv * xh[i][j];
+        pb[i][j] += dv;
       }
     }
     const float m1 = warp_sum(s1) * inv_n;
@@ -275,14 +292,25 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
 #pragma unroll
       for (int j = 0; j < 4; ++j) r[j] = rs * (dxh[i][j] - m1 - xh[i][j] * m2);
       if (dres) {
-        float4 d4 = *reinterpret_cast<const float4 *>(dres + row * dx_rs + c);
-        r[0] += d4.x; r[1] += d4.y; r[2] += d4.z; r[3] += d4.w;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) r[j] += in.dr[i][j];
       }
       Vec<TDX, 4>::store(dx + row * dx_rs + c, r);
       if (dxa) Vec<bf16, 4>::store(dxa + row * dxa_rs + c, r);
 #pragma unroll
       for (int j = 0; j < 4; ++j) pc[i][j] += r[j];
     }
+  };
+  const int64_t stride = (int64_t)gridDim.x * LN_WARPS;
+  int64_t row = (int64_t)blockIdx.x * LN_WARPS + warp;
+  RowIn ra, rb;
+  if (row < rows) load(row, ra);
+  for (; row < rows; row += 2 * stride) {
+    if (row + stride < rows) load(row + stride, rb);
+    process(row, ra);
+    if (row + stride >= rows) break;
+    if (row + 2 * stride < rows) load(row + 2 * stride, ra);
+    process(row + stride, rb);
   }
   if (!nparts) return;
 #pragma unroll
