@@ -259,6 +259,15 @@ EVO_API int evo_outgate_bwd(int dtype, int64_t rows, int64_t cols, const float *
 EVO_API int evo_relu_bwd(int dtype, int64_t n, const void *dh, const void *h,
                  void *dpre, void *stream);
 
+/* ReLU backward of a contiguous bf16 [rows, cols] (cols % 8 == 0) with the
+ * column sums of its output fused in (the transition's first-layer bias
+ * gradient, src/evoformer.py:314-329 / src/tensor.py:343):
+ *   dpre = dh * (h > 0);  colsum_dst[c] = sum_rows dpre[:, c]  (fp32, written)
+ * workspace: evo_colsum_workspace_bytes(cols).                          */
+EVO_API int evo_relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h,
+                                void *dpre, float *colsum_dst, void *workspace,
+                                size_t workspace_bytes, void *stream);
+
 /* Loss (src/schedules.py:194-195): out[0] += sum(x^2)/n (fp32,
  * deterministic two-pass); grad = 2*x/n written to dx (fp32, may be
  * NULL).  workspace >= 4 KiB.                                           */

@@ -59,6 +59,8 @@ int outgate_fwd(int, int64_t, int64_t, const float *, const void *, int64_t, con
 int outgate_bwd(int, int64_t, int64_t, const float *, const void *, int64_t, const void *,
                 int64_t, void *, int64_t, void *, int64_t, cudaStream_t);
 int relu_bwd(int, int64_t, const void *, const void *, void *, cudaStream_t);
+int relu_bwd_colsum(int64_t, int64_t, const void *, const void *, void *, float *, float *,
+                    cudaStream_t);
 int sq_mean(int64_t, const float *, float *, float *, void *, cudaStream_t);
 int add(int64_t, const float *, const float *, float *, cudaStream_t);
 
@@ -339,6 +341,19 @@ int evo_relu_bwd(int dtype, int64_t n, const void *dh, const void *h, void *dpre
   if (n == 0) return EVO_OK;
   CHECK_PTR(dh); CHECK_PTR(h); CHECK_PTR(dpre);
   return relu_bwd(dtype, n, dh, h, dpre, as_stream(stream));
+}
+
+int evo_relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h, void *dpre,
+                        float *colsum_dst, void *workspace, size_t workspace_bytes,
+                        void *stream) {
+  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_relu_bwd_colsum: rows=%lld cols=%lld",
+              (long long)rows, (long long)cols);
+  if (rows == 0) return EVO_OK;
+  CHECK_PTR(dh); CHECK_PTR(h); CHECK_PTR(dpre); CHECK_PTR(colsum_dst);
+  EVO_REQUIRE(workspace && workspace_bytes >= evo_colsum_workspace_bytes(cols), EVO_EARG,
+              "evo_relu_bwd_colsum: workspace too small");
+  return relu_bwd_colsum(rows, cols, dh, h, dpre, colsum_dst, reinterpret_cast<float *>(workspace),
+                         as_stream(stream));
 }
 
 int evo_sq_mean(int64_t n, const float *x, float *out, float *dx, void *workspace,

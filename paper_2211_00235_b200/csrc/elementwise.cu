@@ -394,6 +394,52 @@ __global__ void outgate_bwd_bf16x8_kernel(int64_t rows, int64_t cols, const floa
   }
 }
 
+// ReLU backward with the bias-gradient column sums of its output fused in
+// (the transition's b1 gradient, src/tensor.py:343): the tiling of
+// colsum_stage1_vec (thread = 8 consecutive columns, rows ty, ty+8, ... of
+// the block's row chunk), so stage 2 is shared.
+__global__ void relu_bwd_colsum_kernel(int64_t rows, int64_t cols, const bf16 *dh, const bf16 *h,
+                                       bf16 *dpre, int64_t rpb, float *part) {
+  __shared__ float red[8][32 * 8 + 4];
+  const int64_t c0 = (blockIdx.y * 32 + threadIdx.x) * 8;
+  const int64_t r0 = blockIdx.x * rpb;
+  const int64_t r1 = min(rows, r0 + rpb);
+  float acc[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) acc[j] = 0.f;
+  if (c0 < cols) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      const uint4 a = __ldg(reinterpret_cast<const uint4 *>(dh + r * cols + c0));
+      const uint4 b = __ldg(reinterpret_cast<const uint4 *>(h + r * cols + c0));
+      const uint32_t *aw = reinterpret_cast<const uint32_t *>(&a);
+      const uint32_t *bw = reinterpret_cast<const uint32_t *>(&b);
+      uint32_t o[4];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const uint32_t l16 = bw[j] & 0xFFFFu, h16 = bw[j] >> 16;
+        const uint32_t lo = ((l16 & 0x8000u) == 0u && (l16 & 0x7FFFu) != 0u) ? 0xFFFFu : 0u;
+        const uint32_t hi = ((h16 & 0x8000u) == 0u && (h16 & 0x7FFFu) != 0u) ? 0xFFFF0000u : 0u;
+        o[j] = aw[j] & (lo | hi);
+        const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&o[j]));
+        acc[2 * j] += f.x;
+        acc[2 * j + 1] += f.y;
+      }
+      *reinterpret_cast<uint4 *>(dpre + r * cols + c0) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) red[threadIdx.y][threadIdx.x * 8 + j] = acc[j];
+  __syncthreads();
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int64_t c = blockIdx.y * 256 + t;
+  if (t < 256 && c < cols) {
+    float sacc = 0.f;
+#pragma unroll
+    for (int y = 0; y < 8; ++y) sacc += red[y][t];
+    part[blockIdx.x * cols + c] = sacc;
+  }
+}
+
 __global__ void relu_bwd_bf16x8_kernel(int64_t n8, const uint4 *dh, const uint4 *h, uint4 *dpre) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -663,6 +709,27 @@ int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaS
   if (dt == EVO_F32) relu_bwd_kernel<float><<<nb, 256, 0, st>>>(n, dh, h, dpre);
   else relu_bwd_kernel<bf16><<<nb, 256, 0, st>>>(n, dh, h, dpre);
   EVO_LAUNCHED("relu_bwd_kernel");
+  return EVO_OK;
+}
+
+int relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h, void *dpre,
+                    float *dst, float *ws, cudaStream_t st) {
+  auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+  EVO_REQUIRE(cols % 8 == 0 && al16(dh) && al16(h) && al16(dpre), EVO_EUNSUP,
+              "relu_bwd_colsum: bf16 rows of 8k columns, 16-byte aligned");
+  if (rows == 0) return EVO_OK;
+  const int64_t col_tiles = (cols + 255) / 256;
+  int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(256, (4 * num_sms() + col_tiles - 1) /
+                                                                 col_tiles));
+  nblk = std::min<int64_t>(nblk, std::max<int64_t>(1, rows / 64));
+  const int64_t rpb = (rows + nblk - 1) / nblk;
+  nblk = (rows + rpb - 1) / rpb;
+  relu_bwd_colsum_kernel<<<dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st>>>(
+      rows, cols, reinterpret_cast<const bf16 *>(dh), reinterpret_cast<const bf16 *>(h),
+      reinterpret_cast<bf16 *>(dpre), rpb, ws);
+  EVO_LAUNCHED("relu_bwd_colsum_kernel");
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>((int)nblk, cols, ws, dst, 0);
+  EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
 

@@ -409,9 +409,13 @@ def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
         K.colsum(dx_new, rows, cx, G["b2"])
     dhid = _empty((rows, tc), act, dev)
     K.linear_dx(dxa, rows, cx, pk["W2"], cx, tc, dhid)
-    K.relu_bwd(dhid, ctx["hid"], dhid, rows * tc)
-    K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc)
-    K.colsum(dhid, rows, tc, G["b1"])
+    if act != F32 and tc % 8 == 0:
+        K.relu_bwd_colsum(dhid, ctx["hid"], dhid, rows, tc, G["b1"])
+        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc)
+    else:
+        K.relu_bwd(dhid, ctx["hid"], dhid, rows * tc)
+        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc)
+        K.colsum(dhid, rows, tc, G["b1"])
     dxh = _empty((rows, cx), F32, dev)
     K.linear_dx(dhid, rows, tc, pk["W1"], tc, cx, dxh)
     return _ln_bwd_out(dxh, ctx["x"], rows, cx, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],

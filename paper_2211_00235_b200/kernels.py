@@ -299,6 +299,15 @@ def relu_bwd(dh, h, dpre, n: int):
     check(lib().evo_relu_bwd(dt(h), n, ptr(dh), ptr(h), ptr(dpre), stream()), "evo_relu_bwd")
 
 
+def relu_bwd_colsum(dh, h, dpre, rows: int, cols: int, colsum_dst):
+    """dpre = dh * (h > 0) (bf16, contiguous) and its column sums (fp32)."""
+    L = lib()
+    nbytes = L.evo_colsum_workspace_bytes(cols)
+    ws = _ws(nbytes, dpre.device)
+    check(L.evo_relu_bwd_colsum(rows, cols, ptr(dh), ptr(h), ptr(dpre), ptr(colsum_dst), ptr(ws),
+                                nbytes, stream()), "evo_relu_bwd_colsum")
+
+
 def sq_mean(x, out, dx=None):
     ws = torch.empty(4096, dtype=torch.uint8, device=x.device)
     check(lib().evo_sq_mean(x.numel(), ptr(x), ptr(out), ptr(dx), ptr(ws), stream()),

@@ -144,3 +144,15 @@ def test_layernorm_pair_bias_projection_fused(K):
     dytot = dbias.T @ Wb.float().T
     K.layernorm_bwd(dytot, x, rows, cols, mu0, rs0, g, dx0, dg0, db0)
     assert rel(dx, dx0) < 1e-5
+
+
+def test_relu_bwd_colsum_fused(K):
+    rows, cols = 5000, 1024
+    h = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
+    dh = torch.randn(rows, cols, device="cuda").to(torch.bfloat16)
+    out = torch.empty_like(dh)
+    cs = torch.empty(cols, device="cuda")
+    K.relu_bwd_colsum(dh, h, out, rows, cols, cs)
+    want = torch.where(h > 0, dh, torch.zeros_like(dh))
+    assert torch.equal(out, want)
+    assert rel(cs, want.double().sum(0)) < 1e-6
