@@ -189,6 +189,9 @@ typedef struct evo_attn_desc {
   float *dbias;            /* fp32 at h*bh+q*bq+k*bk (a dense [H,L,L] map); may be NULL */
   void *workspace;
   size_t workspace_bytes;
+  float *dgate_bias;       /* backward, may be NULL: fp32 [H*D] column sums of
+                              dGpre over all (b, l) (the gate bias gradient,
+                              src/tensor.py:343), written */
 } evo_attn_desc;
 
 EVO_API int evo_attention_fwd(const evo_attn_desc *d, void *stream);

@@ -43,7 +43,7 @@ class AttnDesc(C.Structure):
                 ("o_sl", c_i64), ("bias", c_vp), ("bh", c_i64), ("bq", c_i64),
                 ("bk", c_i64), ("lse", c_vp), ("dgm", c_vp), ("dq", c_vp), ("dk", c_vp),
                 ("dv", c_vp), ("dgpre", c_vp), ("dbias", c_vp), ("workspace", c_vp),
-                ("workspace_bytes", c_sz)]
+                ("workspace_bytes", c_sz), ("dgate_bias", c_vp)]
 
 
 # name -> (restype, argtypes)

@@ -308,6 +308,19 @@ int attention_simt_fwd(const evo_attn_desc *a, cudaStream_t st) {
   return EVO_OK;
 }
 
+// dgate_bias[h*D + d] = sum over (b, l) of dGpre (parity path: one thread
+// per column, rows in order)
+template <typename T>
+__global__ void gate_bias_colsum_kernel(const evo_attn_desc a) {
+  const int col = blockIdx.x * blockDim.x + threadIdx.x;
+  if (col >= a.H * a.D) return;
+  const T *g = reinterpret_cast<const T *>(a.dgpre);
+  float s = 0.f;
+  for (int64_t b = 0; b < a.nb; ++b)
+    for (int l = 0; l < a.L; ++l) s += to_f(g[b * a.sb + (int64_t)l * a.sl + col]);
+  a.dgate_bias[col] = s;
+}
+
 int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
   EVO_REQUIRE(a->L >= 1 && a->L <= MAXL && a->D >= 1 && a->D <= MAXD, EVO_EUNSUP,
               "attention bwd: L=%d D=%d unsupported", a->L, a->D);
@@ -350,6 +363,14 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     // dbias = ordered sum of the chunk slabs (same dense index map)
     int rc = reduce_lead(EVO_F32, nch, 1, (int64_t)a->H * L * L, part, a->dbias, 0, 1, 0, st);
     if (rc != EVO_OK) return rc;
+  }
+  if (a->dgate_bias) {
+    const int cols = a->H * a->D;
+    if (a->dtype == EVO_F32)
+      gate_bias_colsum_kernel<float><<<(cols + 127) / 128, 128, 0, st>>>(*a);
+    else
+      gate_bias_colsum_kernel<bf16><<<(cols + 127) / 128, 128, 0, st>>>(*a);
+    EVO_LAUNCHED("gate_bias_colsum_kernel");
   }
   return EVO_OK;
 }

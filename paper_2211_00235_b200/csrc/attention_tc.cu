@@ -29,6 +29,8 @@
 
 namespace evo {
 
+int colsum_partials(int nblk, int64_t cols, const float *part, float *dst, int acc,
+                    cudaStream_t st);
 int reduce_lead(int, int64_t, int64_t, int64_t, const void *, float *, int64_t, int64_t, int,
                 cudaStream_t);
 
@@ -383,12 +385,17 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
 // Dq[b,h,q] = sum_d dO*O.  One thread per 8-column chunk of a (row, head)
 // (consecutive lanes read consecutive 16-byte chunks); the D/8 chunk
 // threads of a head reduce Dq with shuffles.
+// gpart (may be NULL; needs 256 % (H*CH) == 0 so a thread's column group is
+// fixed across the grid stride): per-block column sums of dGpre,
+// [gridDim.x][H*D], reduced over blocks afterwards (fixed order).
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm,
-                                                            bf16 *dO_out, bf16 *dgpre, float *Dq) {
+                                                            bf16 *dO_out, bf16 *dgpre, float *Dq,
+                                                            float *gpart) {
   constexpr int CH = D / 8;  // chunks per head (2 or 4)
   const int64_t total = a.nb * (int64_t)a.L * a.H * CH;
   const int lane = threadIdx.x & 31;
+  float gacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   // warp-uniform trip count (the shuffles below need every lane)
   for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x - lane); e0 < total;
        e0 += (int64_t)gridDim.x * blockDim.x) {
@@ -422,11 +429,33 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, 
     if (ok) {
       *reinterpret_cast<uint4 *>(dO_out + ooff) = make_uint4(dov[0], dov[1], dov[2], dov[3]);
       *reinterpret_cast<uint4 *>(dgpre + goff) = make_uint4(dgv[0], dgv[1], dgv[2], dgv[3]);
+      if (gpart) {  // the gate-bias gradient sums the bf16 values stored
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float2 f = unpack2(dgv[j]);
+          gacc[2 * j] += f.x;
+          gacc[2 * j + 1] += f.y;
+        }
+      }
     }
     // fixed-order reduction over the CH chunk lanes (aligned groups of CH)
 #pragma unroll
     for (int off = 1; off < CH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
     if (ok && c == 0) Dq[(b * a.H + h) * (int64_t)a.L + l] = acc;
+  }
+  if (gpart) {
+    // threads t, t + G, t + 2G, ... (G = H*CH column groups) share columns
+    __shared__ float red[256][9];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[threadIdx.x][j] = gacc[j];
+    __syncthreads();
+    const int G = a.H * CH;
+    for (int i = threadIdx.x; i < G * 8; i += blockDim.x) {
+      const int grp = i / 8, j = i % 8;
+      float t = 0.f;
+      for (int k = grp; k < (int)blockDim.x; k += G) t += red[k][j];
+      gpart[(int64_t)blockIdx.x * (a.H * D) + grp * 8 + j] = t;
+    }
   }
 }
 
@@ -1820,6 +1849,22 @@ int64_t row_chunks(const evo_attn_desc *d) {
   return std::max<int64_t>(1, std::min<int64_t>(d->nb, want));
 }
 
+// byte offset of the gate-bias partials in the backward workspace (after
+// dO, Dq and the dbias chunk partials); sized for SMs*8 prep blocks
+size_t gate_part_offset(const evo_attn_desc *d) {
+  const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * d->D;
+  const size_t dO_pad = ((size_t)span * 2 + 255) / 256 * 256;
+  const size_t Dq_pad = ((size_t)d->nb * d->H * d->L * 4 + 255) / 256 * 256;
+  size_t part = 0;
+  if (d->dbias) {
+    int64_t nch = row_chunks(d);
+    int64_t chunk = (d->nb + nch - 1) / nch;
+    nch = (d->nb + chunk - 1) / chunk;
+    part = ((size_t)nch * d->H * d->L * d->L * 4 + 255) / 256 * 256;
+  }
+  return dO_pad + Dq_pad + part;
+}
+
 template <int D, int BM_>
 int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   AttnTcArgs a = make_args(d);
@@ -1905,10 +1950,22 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   float *part = d->dbias ? reinterpret_cast<float *>(ws + dO_pad + Dq_pad) : nullptr;
   {
     int64_t total = d->nb * (int64_t)d->L * d->H * (D / 8);
-    int blocks = (int)std::min<int64_t>((total + 255) / 256, (int64_t)num_sms() * 32);
+    const bool fuse_gb = d->dgate_bias && (256 % (d->H * (D / 8)) == 0);
+    int blocks = (int)std::min<int64_t>((total + 255) / 256,
+                                        (int64_t)num_sms() * (fuse_gb ? 8 : 32));
+    float *gpart = fuse_gb ? reinterpret_cast<float *>(ws + gate_part_offset(d)) : nullptr;
     attn_bwd_prep_kernel<D><<<blocks, 256, 0, st>>>(a, reinterpret_cast<const bf16 *>(d->dgm),
-                                                     dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq);
+                                                     dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq,
+                                                     gpart);
     EVO_LAUNCHED("attn_bwd_prep_kernel");
+    if (d->dgate_bias) {
+      if (fuse_gb) {
+        const int rc = colsum_partials(blocks, (int64_t)d->H * D, gpart, d->dgate_bias, 0, st);
+        if (rc != EVO_OK) return rc;
+      } else {
+        EVO_REQUIRE(false, EVO_EUNSUP, "attention bwd: gate-bias sums need 256 %% (H*D/8) == 0");
+      }
+    }
   }
   a.dO = dObuf;
   a.Dq = Dq;
@@ -1999,6 +2056,8 @@ bool attention_tc_accepts(const evo_attn_desc *d) {
 
 size_t attention_tc_bwd_ws(const evo_attn_desc *d) {
   if (!attention_tc_accepts(d)) return 0;
+  if (d->dgate_bias)
+    return gate_part_offset(d) + (size_t)num_sms() * 8 * d->H * d->D * 4;
   // dO uses o's strides: size it by the extent those strides span.
   const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * d->D;
   const size_t dO_pad = ((size_t)span * 2 + 255) / 256 * 256;

@@ -712,6 +712,14 @@ int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaS
   return EVO_OK;
 }
 
+// Ordered column sums of [nblk, cols] fp32 partials (coalesced stage 2).
+int colsum_partials(int nblk, int64_t cols, const float *part, float *dst, int acc,
+                    cudaStream_t st) {
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>(nblk, cols, part, dst, acc);
+  EVO_LAUNCHED("colsum_stage2");
+  return EVO_OK;
+}
+
 int relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h, void *dpre,
                     float *dst, float *ws, cudaStream_t st) {
   auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };

@@ -320,13 +320,14 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
     dproj = _empty((rows, 4 * hc), act, dev)
     dbias = _empty((h, r2), F32, dev) if name != "col_attn" else None
     bq, bk = (cfg.r, 1) if name != "tri_attn_end" else (1, cfg.r)
+    # the gate-bias gradient (column sums of dGpre) comes out of the
+    # attention backward's prep pass
     K.attention(proj=ctx["proj"], hc=hc, nb=nb, H=h, L=L, D=ch, scale=ch ** -0.5,
                 sb=rb * 4 * hc, sl=rl * 4 * hc, o=ctx["o"], gm=ctx["gm"], o_sb=rb * hc,
                 o_sl=rl * hc, lse=ctx["lse"], bias=ctx.get("bias"), bh=r2, bq=bq, bk=bk,
-                dgm=dgm, dproj=dproj, dbias=dbias)
+                dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=G["gate_b"])
     xh = ctx["xh"]
     K.linear_dw(xh, rows, c_io, dproj, 4 * hc, G["Wqkvg"], 4 * hc)
-    K.colsum(dproj, rows, hc, G["gate_b"], rs=4 * hc, off=3 * hc)
     dxh = _empty((rows, c_io), F32, dev)
     K.linear_dx(dproj, rows, 4 * hc, pk["Wqkvg"], 4 * hc, c_io, dxh)
     dz_row = None

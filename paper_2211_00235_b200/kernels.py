@@ -221,7 +221,7 @@ def layernorm_bwd_proj(dy, x, rows: int, mean, rstd, gamma, beta, dproj, p_rs: i
 
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
               sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
-              dgm=None, dproj=None, dbias=None):
+              dgm=None, dproj=None, dbias=None, dgate_bias=None):
     """Fused gated attention on the packed [rows, 4*hc] projection buffer
     (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
     backward into dproj (same packing) and dbias."""
@@ -245,12 +245,13 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
     d.dq, d.dk, d.dv, d.dgpre = (ptr(dproj, 0), ptr(dproj, hc), ptr(dproj, 2 * hc),
                                  ptr(dproj, 3 * hc))
     d.dbias = ptr(dbias)
+    d.dgate_bias = ptr(dgate_bias)
     nbytes = Lb.evo_attention_bwd_workspace_bytes(C.byref(d))
     ws = _ws(nbytes, proj.device)
     d.workspace, d.workspace_bytes = ptr(ws), nbytes
     _timed("attention_bwd", 2.0 * flops,
            lambda: check(Lb.evo_attention_bwd(C.byref(d), stream()), "evo_attention_bwd"),
-           keep=(proj, o, gm, lse, bias, dgm, dproj, dbias, ws))
+           keep=(proj, o, gm, lse, bias, dgm, dproj, dbias, dgate_bias, ws))
 
 
 def colsum(src, rows: int, cols: int, dst, *, rs=None, off=0, accumulate=False):
