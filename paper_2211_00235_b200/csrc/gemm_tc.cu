@@ -88,7 +88,10 @@ __device__ __forceinline__ void decode_tile(const TcParams &p, int64_t t64, int6
 
 
 // Compile-time epilogue kinds (runtime residual/accumulate stay per chunk).
-enum { EK_NONE = 0, EK_BIAS = 1, EK_BIAS_RELU = 2, EK_BIAS_SIGMOID = 3 };
+// EK_SPLIT: split-K partial writer (no store staging boxes, so the smem
+// goes to a deeper TMA ring: the weight-gradient GEMMs are bound by the
+// bytes in flight per SM, ring depth x stage size / memory latency).
+enum { EK_NONE = 0, EK_BIAS = 1, EK_BIAS_RELU = 2, EK_BIAS_SIGMOID = 3, EK_SPLIT = 4 };
 
 // sigmoid(x) = 0.5 + 0.5 tanh(x/2): one MUFU op (tanh.approx, rel. error
 // ~2^-11, below the bf16 rounding of the stored gate) instead of ex2 + rcp;
@@ -109,7 +112,7 @@ __device__ __forceinline__ void epi_math(const TcParams &p, const EpiArgs &e, co
   const bool full = nb + 32 <= p.N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = e.alpha * __uint_as_float(v[j]);
-  if constexpr (EPI != EK_NONE) {
+  if constexpr (EPI == EK_BIAS || EPI == EK_BIAS_RELU || EPI == EK_BIAS_SIGMOID) {
     if (full && ((reinterpret_cast<uintptr_t>(bias + nb) & 15) == 0)) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -144,7 +147,7 @@ __device__ __forceinline__ void epi_chunk(const TcParams &p, const EpiArgs &e, c
   const bool full = nb + 32 <= p.N;
 #pragma unroll
   for (int j = 0; j < 32; ++j) x[j] = e.alpha * __uint_as_float(v[j]);
-  if constexpr (EPI != EK_NONE) {
+  if constexpr (EPI == EK_BIAS || EPI == EK_BIAS_RELU || EPI == EK_BIAS_SIGMOID) {
     if (full && ((reinterpret_cast<uintptr_t>(e.bias + nb) & 15) == 0)) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
@@ -254,8 +257,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint8_t *sA = smem;
   uint8_t *sB = smem + STAGES * SMEM_A;
+  constexpr int SW_BYTES = EPI == EK_SPLIT ? 0 : EPI_WARPS * 8192;
   uint8_t *sW = sB + STAGES * SMEM_B;  // EPI_WARPS x 8 KiB, 1 KiB aligned
-  uint64_t *full = reinterpret_cast<uint64_t *>(sW + EPI_WARPS * 8192);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sW + SW_BYTES);
   uint64_t *empty = full + STAGES;
   uint64_t *tfull = empty + STAGES;
   uint64_t *tempty = tfull + 2;
@@ -849,7 +853,8 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   }
   p.bias_smem = (d->bias && d->N <= BIAS_SMEM_MAX && p.split == 1) ? 1 : 0;
   const size_t smem = 1024 + (size_t)STAGES * (SMEM_A + BN * BK * 2) +
-                      (size_t)EPI_WARPS * 8192 + 512 + (size_t)BIAS_SMEM_MAX * 4;
+                      (EPI == EK_SPLIT ? (size_t)0 : (size_t)EPI_WARPS * 8192) + 512 +
+                      (size_t)BIAS_SMEM_MAX * 4;
   static bool attr_set = false;
   if (!attr_set) {
     cudaFuncSetAttribute(gemm_tc_kernel<BN, STAGES, EPI>,
@@ -893,7 +898,11 @@ int gemm_tc(const evo_gemm_desc *d, cudaStream_t st) {
   // split-K partials carry no epilogue (applied by the reducer)
   int64_t kc;
   const bool split = choose_split(d, choose_bn(d), kc) > 1;
-  if (split || (!d->bias && d->epilogue == EVO_EPI_NONE)) return launch_bn<EK_NONE>(d, st);
+  if (split) {
+    if (choose_bn(d) == 256) return launch<256, 4, EK_SPLIT>(d, st);
+    return launch<128, 6, EK_SPLIT>(d, st);
+  }
+  if (!d->bias && d->epilogue == EVO_EPI_NONE) return launch_bn<EK_NONE>(d, st);
   if (!d->bias) return EVO_EUNSUP;  // activation without bias: SIMT handles it
   if (d->epilogue == EVO_EPI_RELU) return launch_bn<EK_BIAS_RELU>(d, st);
   if (d->epilogue == EVO_EPI_SIGMOID_FROM) return launch_bn<EK_BIAS_SIGMOID>(d, st);
