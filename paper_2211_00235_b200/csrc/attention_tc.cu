@@ -1199,23 +1199,26 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
 // TMA loads), so no elementwise warp ever waits on issue latency.
 // smem: bias 128 KiB + two rows of K|V|Q|dO (96 KiB) + lse/Dq: no 1 KiB
 // alignment slack, the dynamic smem base is 1 KiB aligned (checked).
-template <int D, int BIASMODE>
+template <int D, int BIASMODE, int NU>
 __global__ void __launch_bounds__(576, 1)
 attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
                          const __grid_constant__ CUtensorMap mVt,
                          const __grid_constant__ CUtensorMap mQa,
                          const __grid_constant__ CUtensorMap mdOa,
                          const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  constexpr int UW = 64, LPC = NU * UW;           // Lp = 64 NU (128 or 256)
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
-  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t FULL = LPC * Sw<D>::bytes;
   constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // K | V | Q | dO of one batch row
+  // row buffers: with no bias tile the smem takes a third, so row r+2's
+  // loads go out at row r's first unit (short rows still hide TMA latency)
+  constexpr int NBUF = BIASMODE ? 2 : 3;
   constexpr bool KCONTIG = BIASMODE == 1;
-  constexpr int NU = 4, UW = 64;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sBias = smem_raw;
   uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
-  float *sLse = reinterpret_cast<float *>(sRow + 2 * ROWB);
+  float *sLse = reinterpret_cast<float *>(sRow + NBUF * ROWB);
   float *sDq = sLse + 256;
   // 0 bias, 1-2 row data (row parity), 3-5 S^T/dP^T MMAs (region),
   // 6-7 the row's last dV/dK MMAs (row parity), 8-9 unit's elementwise pass
@@ -1224,8 +1227,11 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   // arrivals), 10-12 a unit's dV/dK MMAs done (region):
   // the region is rewritten by the S^T MMA two units later only after its
   // packed P^T / dS^T were consumed
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + 256);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 13);
+  // (row-data barriers 1..NBUF; the others shifted by 1 when NBUF == 3)
+  uint64_t *bars_all = reinterpret_cast<uint64_t *>(sDq + 256);
+  uint64_t *rowbar = bars_all + 1;
+  uint64_t *bars = bars_all + (NBUF - 2);  // bars[3..12] as documented above
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 14);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // key row in the tile
@@ -1242,9 +1248,12 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   constexpr int ISSUER = 512;
   const bool ew = tid < 512;  // elementwise warps
   if (tid == ISSUER) {
-    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], (i == 8 || i == 9) ? 16 : 1);
+    for (int i = 0; i < 14; ++i) {
+      const bool ewd = &bars_all[i] == &bars[8] || &bars_all[i] == &bars[9];
+      mbar_init(&bars_all[i], ewd ? 16 : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars[0], h, k0, 256);
+    if (BIASMODE) load_bias_tile_k<KCONTIG>(sBias, &mB, &bars_all[0], h, k0, LPC);
   }
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
@@ -1253,10 +1262,10 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   const uint32_t tmem = *tslot;
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
 
-  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
+  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) % NBUF) * ROWB; };
   auto load_row = [&](int64_t r) {
     uint8_t *rb = rowbuf(r);
-    uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+    uint64_t *bar = &rowbar[(r - b_lo) % NBUF];
     mbar_expect_tx(bar, ROWB);
     tma_load_4d(rb, &mKt, bar, 0, k0, (int)r, h);
     tma_load_4d(rb + TILE, &mVt, bar, 0, k0, (int)r, h);
@@ -1266,9 +1275,9 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
   const uint32_t idesc_o = idesc_bf16(128, D, false, true);
   auto issue_mma1 = [&](int u, int reg) {  // warp-collective (issuer warp)
-    const int64_t r = b_lo + (u >> 2);
-    const int ui = u & (NU - 1);
-    if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
+    const int64_t r = b_lo + u / NU;
+    const int ui = u % NU;
+    if (ui == 0) mbar_wait(&rowbar[(r - b_lo) % NBUF], (uint32_t)(((r - b_lo) / NBUF) & 1));
     fence_after();
     const uint32_t sK = smem_u32(rowbuf(r)), sV = sK + TILE;
     const uint32_t sQ = sK + 2 * TILE + ui * UW * Sw<D>::bytes;
@@ -1333,10 +1342,8 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     if (warp == 16 && nrows > 0) {
       // S^T/dP^T MMAs: unit v into region v%3 once unit v-3's dV/dK MMAs
       // (the region's previous readers) completed
-      if (lane == 0) {
-        load_row(b_lo);
-        if (nrows > 1) load_row(b_lo + 1);
-      }
+      if (lane == 0)
+        for (int i = 0; i < NBUF && i < nrows; ++i) load_row(b_lo + i);
       __syncwarp();
       int reg = 0;
       uint32_t ph3 = 0;
@@ -1351,15 +1358,15 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     } else if (warp == 17 && nrows > 0) {
       int reg = 0;
       for (int u = 0; u < (int)U; ++u) {
-        const int64_t r = b_lo + (u >> 2);
-        const int ui = u & (NU - 1);
+        const int64_t r = b_lo + u / NU;
+        const int ui = u % NU;
         const int rp = (int)((r - b_lo) & 1);
         mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));  // all 16 warps packed unit u
         fence_after();
         // at a row's first unit the warps have read row r-1's accumulators,
-        // so row r-1's smem buffers are free for row r+1
-        if (ui == 0 && r > b_lo && r + 1 < b_hi) {
-          if (lane == 0) load_row(r + 1);
+        // so row r-1's smem buffer is free for row r-1+NBUF
+        if (ui == 0 && r > b_lo && r - 1 + NBUF < b_hi) {
+          if (lane == 0) load_row(r - 1 + NBUF);
           __syncwarp();
         }
         const uint32_t acc = tmem + 384 + rp * 64;
@@ -1387,16 +1394,16 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     Dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + tid];
   }
   if (BIASMODE) {
-    mbar_wait(&bars[0], 0);
-    scale_tile(sBias, 8 * 16384 / 16, 512);
+    mbar_wait(&bars_all[0], 0);
+    scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
   }
   const float sc_l2 = a.scale * LOG2E;
 
   int reg = 0;
   uint32_t ph3 = 0;  // bit i: parity of region i's S^T/dP^T barrier
   for (int u = 0; u < (int)U; ++u) {
-    const int64_t r = b_lo + (u >> 2);
-    const int ui = u & (NU - 1);
+    const int64_t r = b_lo + u / NU;
+    const int ui = u % NU;
     if (ui == 0) {  // this row's lse / Dq into smem; prefetch the next row's
       if (r > b_lo) named_bar_sync(1, 512);  // every warp is done with row r-1's lse / Dq
       if (tid < 256) {
@@ -1495,28 +1502,32 @@ __device__ __forceinline__ void bias_row8(const uint8_t *sb, int row, int k0, fl
   }
 }
 
-template <int D, int BIASMODE>
+template <int D, int BIASMODE, int NU>
 __global__ void __launch_bounds__(576, 1)
 attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
                         const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV,
                         const __grid_constant__ CUtensorMap mdO,
                         const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  constexpr int UW = 32, LPC = NU * UW;           // Lp = 32 NU (128 or 256)
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
-  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  constexpr uint32_t FULL = LPC * Sw<D>::bytes;
   constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // Q | dO | K | V of one batch row
+  constexpr int NBUF = BIASMODE ? 2 : 3;          // see the dk/dv kernel
   constexpr bool TB = BIASMODE == 2;
-  constexpr int NU = 8, UW = 32;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sBias = smem_raw;
   uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
-  uint8_t *sI = sRow + 2 * ROWB;  // 32 x 32 bf16 identity, K-major SW64
+  uint8_t *sI = sRow + NBUF * ROWB;  // 32 x 32 bf16 identity, K-major SW64
   // 0 bias, 1-2 row data (row parity), 3-5 S/dP MMAs (region), 6-7 row's
   // last dQ MMAs (row parity), 8-9 unit packed (16 warp arrivals, unit
   // parity), 10-12 unit's MMAs done (region), 13 chunk's last MMAs
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sI + 2048);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 14);
+  // (row-data barriers 1..NBUF; the others shifted by 1 when NBUF == 3)
+  uint64_t *bars_all = reinterpret_cast<uint64_t *>(sI + 2048);
+  uint64_t *rowbar = bars_all + 1;
+  uint64_t *bars = bars_all + (NBUF - 2);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 15);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
@@ -1531,9 +1542,12 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   const int64_t U = nrows > 0 ? nrows * NU : 0;
 
   if (tid == 512) {
-    for (int i = 0; i < 14; ++i) mbar_init(&bars[i], (i == 8 || i == 9) ? 16 : 1);
+    for (int i = 0; i < 15; ++i) {
+      const bool ewd = &bars_all[i] == &bars[8] || &bars_all[i] == &bars[9];
+      mbar_init(&bars_all[i], ewd ? 16 : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, 256);
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars_all[0], h, q0, LPC);
   }
   // identity: row n has bf16 1.0 at column n (SW64: 16-byte chunk c of row n
   // sits at chunk c ^ ((n >> 1) & 3))
@@ -1556,7 +1570,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   fence_after();
   const uint32_t tmem = *tslot;
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) & 1) * ROWB; };
+  auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) % NBUF) * ROWB; };
 
   if (warp >= 16) {
     // ------------------------------------------------------------ issuers
@@ -1565,7 +1579,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
     const uint32_t idesc_i = idesc_bf16(128, 32, false, false);
     auto load_row = [&](int64_t r) {
       uint8_t *rb = rowbuf(r);
-      uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
+      uint64_t *bar = &rowbar[(r - b_lo) % NBUF];
       mbar_expect_tx(bar, ROWB);
       tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
       tma_load_4d(rb + TILE, &mdO, bar, 0, q0, (int)r, h);
@@ -1575,21 +1589,19 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
     if (warp == 16 && nrows > 0) {
       // S/dP MMAs: unit v into region v%3 once unit v-3's dQ/dbias MMAs
       // (the region's previous readers) completed
-      if (lane == 0) {
-        load_row(b_lo);
-        if (nrows > 1) load_row(b_lo + 1);
-      }
+      if (lane == 0)
+        for (int i = 0; i < NBUF && i < nrows; ++i) load_row(b_lo + i);
       __syncwarp();
       int reg = 0;
       uint32_t ph3 = 0;  // bit i: parity of region i's dQ/dbias-done barrier
       for (int v = 0; v < (int)U; ++v) {
-        const int64_t r = b_lo + (v >> 3);
-        const int ui = v & (NU - 1);
+        const int64_t r = b_lo + v / NU;
+        const int ui = v % NU;
         if (v >= 3) {
           mbar_wait(&bars[10 + reg], (ph3 >> reg) & 1u);
           ph3 ^= 1u << reg;
         }
-        if (ui == 0) mbar_wait(&bars[1 + ((r - b_lo) & 1)], (uint32_t)(((r - b_lo) >> 1) & 1));
+        if (ui == 0) mbar_wait(&rowbar[(r - b_lo) % NBUF], (uint32_t)(((r - b_lo) / NBUF) & 1));
         fence_after();
         const uint32_t sQ = smem_u32(rowbuf(r)), sdO = sQ + TILE;
         const uint32_t sK = sQ + 2 * TILE + ui * UW * Sw<D>::bytes, sV = sK + FULL;
@@ -1610,13 +1622,13 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       const uint32_t sIa = smem_u32(sI);
       int reg = 0;
       for (int u = 0; u < (int)U; ++u) {
-        const int64_t r = b_lo + (u >> 3);
-        const int ui = u & (NU - 1);
+        const int64_t r = b_lo + u / NU;
+        const int ui = u % NU;
         const int rp = (int)((r - b_lo) & 1);
         mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));
         fence_after();
-        if (ui == 0 && r > b_lo && r + 1 < b_hi) {  // row r-1 read back: its buffers are free
-          if (lane == 0) load_row(r + 1);
+        if (ui == 0 && r > b_lo && r - 1 + NBUF < b_hi) {  // row r-1 read back: buffer free
+          if (lane == 0) load_row(r - 1 + NBUF);
           __syncwarp();
         }
         const uint32_t sK = smem_u32(rowbuf(r)) + 2 * TILE;
@@ -1627,10 +1639,12 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
         for (int ks = 0; ks < 2; ++ks)
           umma_bf16_ts_el(acc, reg_col + ks * 8, desc_mnmajor_tile<D>(sK, ui * 2 + ks), idesc_o,
                           (ui > 0 || ks > 0) ? 1u : 0u);
+        if (BIASMODE) {
 #pragma unroll
-        for (int ks = 0; ks < 2; ++ks)
-          umma_bf16_ts_el(dba, reg_col + ks * 8, desc_kmajor_tile<32>(sIa, ks), idesc_i,
-                          (r > b_lo || ks > 0) ? 1u : 0u);
+          for (int ks = 0; ks < 2; ++ks)
+            umma_bf16_ts_el(dba, reg_col + ks * 8, desc_kmajor_tile<32>(sIa, ks), idesc_i,
+                            (r > b_lo || ks > 0) ? 1u : 0u);
+        }
         if (ui == NU - 1) umma_commit_el(&bars[6 + rp]);
         umma_commit_el(&bars[10 + reg]);
         reg = reg == 2 ? 0 : reg + 1;
@@ -1675,8 +1689,8 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       }
     };
     if (BIASMODE) {
-      mbar_wait(&bars[0], 0);
-      scale_tile(sBias, 8 * 16384 / 16, 512);
+      mbar_wait(&bars_all[0], 0);
+      scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
       named_bar_sync(1, 512);
     }
     const float sc_l2 = a.scale * LOG2E;
@@ -1690,8 +1704,8 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
     uint32_t ph3 = 0;  // bit i: parity of region i's S/dP barrier
     const int U32 = (int)U;
     for (int u = 0; u < U32; ++u) {
-      const int64_t r = b_lo + (u >> 3);
-      const int ui = u & (NU - 1);
+      const int64_t r = b_lo + u / NU;
+      const int ui = u % NU;
       if (ui == 0) {
         lse_l2 = lse_n * LOG2E;
         Dq = Dq_n;
@@ -1988,12 +2002,20 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     mbk = mq;
   }
   const int tiles = (d->L + QT - 1) / QT;
-  if (Lp == 256 && !g_attn_no_pipe) {
-    const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
-                        2048 + 14 * 8 + 16;
-    EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_>));
+  const bool pipe = (Lp == 256 || Lp == 128) && !g_attn_no_pipe;
+  const size_t nbuf = BM_ ? 2 : 3;
+  if (pipe) {
+    const size_t smem = (BM_ ? BIAS_BYTES : 0) +
+                        nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2048 + 15 * 8 +
+                        16;
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dq_pipe_kernel<D, BM_><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    if (Lp == 256) {
+      EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8>));
+      attn_bwd_dq_pipe_kernel<D, BM_, 8><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    } else {
+      EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4>));
+      attn_bwd_dq_pipe_kernel<D, BM_, 4><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    }
     EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
   } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 2 * (size_t)QT * 2 * D +
@@ -2003,12 +2025,18 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     attn_bwd_dq_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
-  if (Lp == 256 && !g_attn_no_pipe) {
-    const size_t smem = (BM_ ? BIAS_BYTES : 0) + 2 * (2 * (size_t)QT * 2 * D + 2 * 256 * 2 * D) +
-                        2 * 256 * 4 + 13 * 8 + 16;
-    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_>));
+  if (pipe) {
+    const size_t smem = (BM_ ? BIAS_BYTES : 0) +
+                        nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2 * 256 * 4 +
+                        14 * 8 + 16;
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dkv_pipe_kernel<D, BM_><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    if (Lp == 256) {
+      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_, 4>));
+      attn_bwd_dkv_pipe_kernel<D, BM_, 4><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    } else {
+      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_, 2>));
+      attn_bwd_dkv_pipe_kernel<D, BM_, 2><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    }
     EVO_LAUNCHED("attn_bwd_dkv_pipe_kernel");
   } else {
     const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) + 4 * 256 * 2 * D +

@@ -114,6 +114,8 @@ CASES = [
     (5, 230, 3, 16, True, "transposed"),
     (150, 256, 4, 32, False, "plain"),   # 9-row chunks per CTA: row pipeline wrap-around
     (64, 256, 2, 32, True, "none"),
+    (130, 128, 4, 32, True, "none"),     # column attention, many rows per CTA (Lp = 128 pipe)
+    (40, 120, 2, 16, False, "transposed"),
 ]
 
 
