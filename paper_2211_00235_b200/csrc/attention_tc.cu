@@ -509,7 +509,7 @@ __device__ __forceinline__ uint32_t quarter_col(int ks, int KQ) {
 }
 
 // ================================================================= fwd, v2
-// Lp == 256.  Four threads per query row (warps w, w+4, w+8, w+12 share the
+// Lp = 128 or 256.  Four threads per query row (warps w, w+4, w+8, w+12 share the
 // row's TMEM lane; quarter qr owns keys [64qr, 64qr+64)), so each thread
 // keeps its 64 logits x = S*scale*log2e + bias*log2e in registers between
 // the max and the exp pass: one TMEM read and one bias read per element.
@@ -519,13 +519,17 @@ __device__ __forceinline__ uint32_t quarter_col(int ks, int KQ) {
 // row b+2 once row b's epilogue has read O, the TMA loads of row b+2 once
 // PV(b) completed.  Row b's epilogue runs between row b+1's two passes, so
 // the PV MMA of b and the S MMA of b+2 overlap elementwise work.
-template <int D, int BIASMODE>
+template <int D, int BIASMODE, int LPC>
 __global__ void __launch_bounds__(544, 1)
 attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                     const AttnTcArgs a) {
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
-  constexpr uint32_t FULL = 256 * Sw<D>::bytes;
+  // LPC = Lp (128 or 256): each thread owns KQ = LPC/4 keys; O sits in
+  // quarter 0's freed half (Lp 256) or past S (Lp 128)
+  constexpr int KQ = LPC / 4;
+  constexpr uint32_t OCOL = LPC == 256 ? 32 : 128;
+  constexpr uint32_t FULL = LPC * Sw<D>::bytes;
   constexpr uint32_t ROWB = TILE + 2 * FULL;  // Q | K | V of one batch row
   constexpr bool TB = BIASMODE == 2;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -552,7 +556,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   if (tid == 512) {
     for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i >= 7) ? 16 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, 256);
+    if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, LPC);
   }
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
@@ -564,7 +568,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   if (warp == 16) {
     // ------------------------------------------------------------ issuer
     {
-    const uint32_t idesc_s = idesc_bf16(128, 256, false, false);
+    const uint32_t idesc_s = idesc_bf16(128, LPC, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
     auto load_row = [&](int64_t r) {
       uint8_t *rb = rowbuf(r);
@@ -601,9 +605,10 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
         fence_after();
         const uint32_t sV = smem_u32(rowbuf(r)) + TILE + FULL;
         const uint32_t slot = tmem + 256 * p;
+        constexpr int SPQ = KQ / 16;  // K slices per quarter
 #pragma unroll
-        for (int ks = 0; ks < 16; ++ks)
-          umma_bf16_ts_el(slot + 32, slot + 64 * (ks >> 2) + 8 * (ks & 3),
+        for (int ks = 0; ks < LPC / 16; ++ks)
+          umma_bf16_ts_el(slot + OCOL, slot + KQ * (ks / SPQ) + 8 * (ks % SPQ),
                           desc_mnmajor_tile<D>(sV, ks), idesc_o, ks > 0);
         umma_commit_el(&bars[5 + p]);
         if (r + 2 < b_hi) {
@@ -636,11 +641,11 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       uint32_t ov[8];
       constexpr int QD = D / 4;
       if constexpr (QD == 8) {
-        tmem_ld8_nw(lane_addr + 256 * p + 32 + 8 * qr, ov);
+        tmem_ld8_nw(lane_addr + 256 * p + OCOL + 8 * qr, ov);
       } else {
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(ov[0]), "=r"(ov[1]), "=r"(ov[2]), "=r"(ov[3])
-                     : "r"(lane_addr + 256 * p + 32 + 4 * qr));
+                     : "r"(lane_addr + 256 * p + OCOL + 4 * qr));
       }
       tmem_wait_ld();
       fence_before();
@@ -675,7 +680,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       const int p = (int)((r - b_lo) & 1);
       const uint32_t ph = (uint32_t)(((r - b_lo) >> 1) & 1);
       const uint32_t slot = lane_addr + 256 * p;
-      const int kb = 64 * qr;
+      const int kb = KQ * qr;
       // gate slice of this row (consumed by its epilogue, one row later)
       // (volatile: issued here, a row ahead of its use, not sunk to the use)
       uint4 gq = make_uint4(0u, 0u, 0u, 0u);
@@ -691,11 +696,11 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       }
       mbar_wait(&bars[3 + p], ph);
       fence_after();
-      // pass 1: logits of this thread's 64 keys -> registers, local max
-      float x[64];
+      // pass 1: logits of this thread's KQ keys -> registers, local max
+      float x[KQ];
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < KQ / 32; ++c) {
         uint32_t v[32];
         tmem_ld32(slot + kb + 32 * c, v);
         float bb[32];
@@ -718,7 +723,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       // pass 2: p = exp2(x - max) -> bf16 pairs in this quarter's first 32 cols
       float sum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < KQ / 32; ++c) {
         uint32_t pk[16];
 #pragma unroll
         for (int j = 0; j < 16; ++j) {
@@ -1899,11 +1904,16 @@ int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   const size_t smem = 1024 + (BM_ ? BIAS_BYTES : 0) +
                       2 * ((size_t)QT * 2 * D + 2 * 256 * 2 * D) + 128;
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-  if (a.Lp == 256 && D <= 32 && !g_attn_no_pipe) {
-    const size_t smem2 = (BM_ ? BIAS_BYTES : 0) + 2 * ((size_t)QT * 2 * D + 2 * 256 * 2 * D) +
+  if ((a.Lp == 256 || a.Lp == 128) && D <= 32 && !g_attn_no_pipe) {
+    const size_t smem2 = (BM_ ? BIAS_BYTES : 0) + 2 * ((size_t)QT * 2 * D + 2 * (size_t)a.Lp * 2 * D) +
                          2 * 2 * 4 * 128 * 4 + 11 * 8 + 16;
-    EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_>));
-    attn_fwd_tc2_kernel<D, BM_><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+    if (a.Lp == 256) {
+      EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_, 256>));
+      attn_fwd_tc2_kernel<D, BM_, 256><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+    } else {
+      EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_, 128>));
+      attn_fwd_tc2_kernel<D, BM_, 128><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+    }
     EVO_LAUNCHED("attn_fwd_tc2_kernel");
     return EVO_OK;
   }
