@@ -51,40 +51,51 @@ ln_fwd_vec_kernel(int64_t rows, const TX *__restrict__ x, int64_t x_rs,
                   const float *__restrict__ gamma, const float *__restrict__ beta,
                   TY *__restrict__ y, int64_t y_rs, float *__restrict__ mean_out,
                   float *__restrict__ rstd_out, float eps) {
-  constexpr int cols = NV * 128;
+  // RPW rows per warp, all loads issued before the first reduction
+  constexpr int cols = NV * 128, RPW = 4;
   const int lane = threadIdx.x & 31;
-  const int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
-  if (row >= rows) return;
-  float v[NV][4];
-  float s = 0.f;
+  const int64_t row0 = ((int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * RPW;
+  if (row0 >= rows) return;
+  float v[RPW][NV][4];
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    Vec<TX, 4>::load(x + row * x_rs + 4 * lane + 128 * i, v[i]);
+  for (int r = 0; r < RPW; ++r)
+    if (row0 + r < rows) {
 #pragma unroll
-    for (int j = 0; j < 4; ++j) s += v[i][j];
-  }
-  const float mu = warp_sum(s) * (1.f / cols);
-  float q = 0.f;
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      float d = v[i][j] - mu;
-      q += d * d;
+      for (int i = 0; i < NV; ++i)
+        Vec<TX, 4>::load(x + (row0 + r) * x_rs + 4 * lane + 128 * i, v[r][i]);
     }
-  const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    const int c = 4 * lane + 128 * i;
-    float4 g4 = *reinterpret_cast<const float4 *>(gamma + c);
-    float4 b4 = *reinterpret_cast<const float4 *>(beta + c);
-    float o[4] = {(v[i][0] - mu) * rs * g4.x + b4.x, (v[i][1] - mu) * rs * g4.y + b4.y,
-                  (v[i][2] - mu) * rs * g4.z + b4.z, (v[i][3] - mu) * rs * g4.w + b4.w};
-    Vec<TY, 4>::store(y + row * y_rs + c, o);
-  }
-  if (lane == 0) {
-    mean_out[row] = mu;
-    rstd_out[row] = rs;
+  for (int r = 0; r < RPW; ++r) {
+    const int64_t row = row0 + r;
+    if (row >= rows) break;
+    float s = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) s += v[r][i][j];
+    const float mu = warp_sum(s) * (1.f / cols);
+    float q = 0.f;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        float d = v[r][i][j] - mu;
+        q += d * d;
+      }
+    const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const int c = 4 * lane + 128 * i;
+      float4 g4 = *reinterpret_cast<const float4 *>(gamma + c);
+      float4 b4 = *reinterpret_cast<const float4 *>(beta + c);
+      float o[4] = {(v[r][i][0] - mu) * rs * g4.x + b4.x, (v[r][i][1] - mu) * rs * g4.y + b4.y,
+                    (v[r][i][2] - mu) * rs * g4.z + b4.z, (v[r][i][3] - mu) * rs * g4.w + b4.w};
+      Vec<TY, 4>::store(y + row * y_rs + c, o);
+    }
+    if (lane == 0) {
+      mean_out[row] = mu;
+      rstd_out[row] = rs;
+    }
   }
 }
 
@@ -664,12 +675,13 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   const bool vec = x_cs == 1 && (cols == 128 || cols == 256) && x_rs % 4 == 0 && y_rs % 4 == 0 &&
                    aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta);
   if (vec) {
+    dim3 vgrid((unsigned)((rows + 4 * LN_WARPS - 1) / (4 * LN_WARPS)));  // 4 rows per warp
     if (cols == 128)
-      ln_fwd_vec_kernel<TX, TY, 1><<<grid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
-                                                                  y_rs, mean, rstd, eps);
+      ln_fwd_vec_kernel<TX, TY, 1><<<vgrid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+                                                                   y_rs, mean, rstd, eps);
     else
-      ln_fwd_vec_kernel<TX, TY, 2><<<grid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
-                                                                  y_rs, mean, rstd, eps);
+      ln_fwd_vec_kernel<TX, TY, 2><<<vgrid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+                                                                   y_rs, mean, rstd, eps);
     EVO_LAUNCHED("ln_fwd_vec_kernel");
     return EVO_OK;
   }
