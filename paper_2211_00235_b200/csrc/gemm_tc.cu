@@ -415,9 +415,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       fence_after();
       const int64_t m = mt * BM + q * 32 + lane;
       const int64_t n0 = nt * BN;
-      const int64_t b1 = bidx / p.B2, b2 = bidx % p.B2;
       const bool row_ok = m < p.M;
-      const int64_t rbase = row_ok ? (b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m)) : 0;
       // this warp's chunks: c0 = half*32 + 64*i with n0 + c0 < N; the next
       // chunk's TMEM load is in flight while the current one is finished,
       // and the accumulator is released as soon as its last chunk is read
@@ -503,6 +501,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         acc ^= 1;
         if (acc == 0) aphase ^= 1;
         continue;
+      }
+      // destination row base: only the thread-store / plain-residual paths
+      // need it (64-bit divisions kept off the bf16 TMA-store path)
+      int64_t rbase = 0;
+      if (row_ok && p.split == 1) {
+        const int64_t b1 = bidx / p.B2, b2 = bidx % p.B2;
+        rbase = b1 * e.c_b1 + b2 * e.c_b2 + e.cmap.row(m);
       }
       const int nch = ncols > half * 32 ? (int)((ncols - half * 32 + 63) / 64) : 0;
       const uint32_t tbase = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN + half * 32;

@@ -6,7 +6,7 @@
 // multiplication, tiny test dims) a generic strided path.  gamma/beta
 // gradients: per-warp register partials -> per-block partials -> an ordered
 // warp-per-column reduction (fixed grid, bitwise reproducible).
-#include "common.cuh"
+#include "tc_common.cuh"
 
 namespace evo {
 namespace {
@@ -435,6 +435,226 @@ ln_bwd_proj_kernel(int64_t rows, const float *__restrict__ dy, const float *__re
   }
 }
 
+// ------------------------------------------- TMA-staged backward (fp32)
+// The register-staged kernels above keep ~1.5 rows in flight per warp and
+// stall at ~4 TB/s (the proj variant, 128 registers for W / dW, at ~2).
+// Here one persistent CTA per SM splits producer and consumers: a producer
+// lane streams chunks of RCH contiguous rows -- x, dy, dres, mean, rstd and
+// the NH projection-gradient rows -- into an LNT_NS-deep smem ring with
+// bulk async copies (cp.async.bulk, mbarrier completion), so ~3 chunks
+// (~150 KB) per SM are in flight regardless of the consumers' reduction
+// latency; 12 consumer warps finish two rows per pass from smem with
+// exactly the per-row arithmetic of ln_bwd_vec_kernel / ln_bwd_proj_kernel.
+// Partials: [block][nparts][cols], reduced by ln_param_reduce_kernel.
+
+// consumer warps: 12 (registers cap 128) / 8 with the projection's W, dW
+template <int NH> constexpr int lnt_cw() { return NH > 0 ? 8 : 12; }
+
+template <int NV, int NH>
+struct LntLayout {
+  static constexpr int CW = lnt_cw<NH>();
+  static constexpr int cols = NV * 128, RCH = (NH > 0 ? 4 : 2) * CW / NV;
+  static constexpr uint32_t RB = RCH * cols * 4;  // 12 KB per row tensor
+  static constexpr uint32_t OFF_DY = RB, OFF_DR = 2 * RB, OFF_MU = 3 * RB;
+  static constexpr uint32_t OFF_RS = OFF_MU + 128, OFF_DP = OFF_RS + 128;
+  static constexpr uint32_t STAGE = OFF_DP + (NH > 0 ? NH : 1) * 128;
+  static constexpr int NS = 5 * STAGE <= 200 * 1024 ? 5 : 4;  // ring depth
+  static constexpr uint32_t SMEM = NS * STAGE + 2 * NS * 8;
+  static_assert(RCH * 4 <= 128 && NS * STAGE <= 200 * 1024, "ring layout");
+};
+
+template <int NV, int NH>
+__global__ void __launch_bounds__((lnt_cw<NH>() + 1) * 32, 1)
+ln_bwd_tma_kernel(int64_t rows, const float *__restrict__ dy, const float *__restrict__ x,
+                  const float *__restrict__ mean, const float *__restrict__ rstd,
+                  const float *__restrict__ gamma, const float *__restrict__ beta,
+                  const float *__restrict__ dres, const float *__restrict__ dproj, int64_t p_rs,
+                  const bf16 *__restrict__ Wp, int nh, float *__restrict__ dx,
+                  bf16 *__restrict__ dxa, float *__restrict__ partial, int nparts) {
+  using Lay = LntLayout<NV, NH>;
+  constexpr int LNT_CW = Lay::CW, LNT_NS = Lay::NS;
+  constexpr int cols = Lay::cols, RCH = Lay::RCH;
+  constexpr int NHR = NH > 0 ? NH : 1;
+  extern __shared__ __align__(128) uint8_t sm[];
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + LNT_NS * Lay::STAGE);
+  uint64_t *empty = full + LNT_NS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (rows + RCH - 1) / RCH;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LNT_NS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], LNT_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  float pg[NV][4], pb[NV][4], pc[NV][4], g[NV][4], bt[NV][4];
+  float W[4][NHR], pw[4][NHR];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane + 128 * i);
+    g[i][0] = g4.x; g[i][1] = g4.y; g[i][2] = g4.z; g[i][3] = g4.w;
+    if constexpr (NH > 0) {
+      const float4 b4 = *reinterpret_cast<const float4 *>(beta + 4 * lane + 128 * i);
+      bt[i][0] = b4.x; bt[i][1] = b4.y; bt[i][2] = b4.z; bt[i][3] = b4.w;
+    }
+#pragma unroll
+    for (int j = 0; j < 4; ++j) pg[i][j] = pb[i][j] = pc[i][j] = 0.f;
+  }
+  if constexpr (NH > 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh) {
+        W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
+        pw[j][hh] = 0.f;
+      }
+  }
+  if (warp == LNT_CW) {
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int s = it % LNT_NS;
+        if (it >= LNT_NS) tc::mbar_wait(&empty[s], ((it / LNT_NS) - 1) & 1);
+        const int64_t r0 = c * RCH;
+        const uint32_t nr = (uint32_t)(rows - r0 < RCH ? rows - r0 : RCH);
+        const uint32_t rb = nr * cols * 4, sb = nr * 4;
+        uint8_t *st = sm + s * Lay::STAGE;
+        uint32_t tx = rb + 2 * sb + (dy ? rb : 0) + (dres ? rb : 0);
+        if constexpr (NH > 0) tx += (uint32_t)nh * sb;
+        tc::mbar_expect_tx(&full[s], tx);
+        tc::bulk_load(st, x + r0 * cols, rb, &full[s]);
+        if (dy) tc::bulk_load(st + Lay::OFF_DY, dy + r0 * cols, rb, &full[s]);
+        if (dres) tc::bulk_load(st + Lay::OFF_DR, dres + r0 * cols, rb, &full[s]);
+        tc::bulk_load(st + Lay::OFF_MU, mean + r0, sb, &full[s]);
+        tc::bulk_load(st + Lay::OFF_RS, rstd + r0, sb, &full[s]);
+        if constexpr (NH > 0) {
+          for (int hh = 0; hh < nh; ++hh)
+            tc::bulk_load(st + Lay::OFF_DP + hh * 128, dproj + hh * p_rs + r0, sb, &full[s]);
+        }
+      }
+    }
+  } else {
+    constexpr float inv_n = 1.f / cols;
+    int it = 0;
+    for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+      const int s = it % LNT_NS;
+      tc::mbar_wait(&full[s], (it / LNT_NS) & 1);
+      const int64_t r0 = c * RCH;
+      const int nr = (int)(rows - r0 < RCH ? rows - r0 : RCH);
+      const uint8_t *st = sm + s * Lay::STAGE;
+      // two rows per pass (r, r + LNT_CW): their shuffle reductions interleave
+      for (int rp = warp; rp < nr; rp += 2 * LNT_CW) {
+        float xh[2][NV][4], dxh[2][NV][4], rsv[2], m1[2], m2[2];
+        bool ok[2];
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          const int r = rp + q * LNT_CW;
+          ok[q] = r < nr;  // warp-uniform
+          if (!ok[q]) continue;
+          const float mu = reinterpret_cast<const float *>(st + Lay::OFF_MU)[r];
+          const float rs = reinterpret_cast<const float *>(st + Lay::OFF_RS)[r];
+          rsv[q] = rs;
+          float dp[NHR];
+          if constexpr (NH > 0) {
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh)
+              dp[hh] = hh < nh ? reinterpret_cast<const float *>(st + Lay::OFF_DP + hh * 128)[r] : 0.f;
+          }
+          float s1 = 0.f, s2 = 0.f;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            const uint32_t o = (uint32_t)(r * cols + 4 * lane + 128 * i) * 4;
+            float xv[4], dv[4] = {0.f, 0.f, 0.f, 0.f};
+            Vec<float, 4>::load(reinterpret_cast<const float *>(st + o), xv);
+            if (dy) Vec<float, 4>::load(reinterpret_cast<const float *>(st + Lay::OFF_DY + o), dv);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) {
+              float d = dv[j];
+              xh[q][i][j] = (xv[j] - mu) * rs;
+              if constexpr (NH > 0) {
+#pragma unroll
+                for (int hh = 0; hh < NH; ++hh) d = fmaf(dp[hh], W[j][hh], d);
+                const float yv =
+                    __bfloat162float(__float2bfloat16_rn((xv[j] - mu) * rs * g[i][j] + bt[i][j]));
+#pragma unroll
+                for (int hh = 0; hh < NH; ++hh) pw[j][hh] = fmaf(yv, dp[hh], pw[j][hh]);
+              }
+              dxh[q][i][j] = d * g[i][j];
+              s1 += dxh[q][i][j];
+              s2 += dxh[q][i][j] * xh[q][i][j];
+              pg[i][j] += d * xh[q][i][j];
+              pb[i][j] += d;
+            }
+          }
+          m1[q] = s1;
+          m2[q] = s2;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (!ok[q]) continue;
+          m1[q] = warp_sum(m1[q]) * inv_n;
+          m2[q] = warp_sum(m2[q]) * inv_n;
+        }
+#pragma unroll
+        for (int q = 0; q < 2; ++q) {
+          if (!ok[q]) continue;
+          const int r = rp + q * LNT_CW;
+          const int64_t row = r0 + r;
+#pragma unroll
+          for (int i = 0; i < NV; ++i) {
+            const int cc = 4 * lane + 128 * i;
+            float rr[4];
+#pragma unroll
+            for (int j = 0; j < 4; ++j) rr[j] = rsv[q] * (dxh[q][i][j] - m1[q] - xh[q][i][j] * m2[q]);
+            if (dres) {
+              float d4[4];
+              Vec<float, 4>::load(
+                  reinterpret_cast<const float *>(st + Lay::OFF_DR + (uint32_t)(r * cols + cc) * 4), d4);
+#pragma unroll
+              for (int j = 0; j < 4; ++j) rr[j] += d4[j];
+            }
+            Vec<float, 4>::store(dx + row * cols + cc, rr);
+            if (dxa) Vec<bf16, 4>::store(dxa + row * cols + cc, rr);
+#pragma unroll
+            for (int j = 0; j < 4; ++j) pc[i][j] += rr[j];
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&empty[s]);
+    }
+  }
+  // every chunk consumed => every bulk copy landed; the ring becomes the
+  // partials buffer [LNT_CW][nparts][cols]
+  __syncthreads();
+  if (!nparts) return;
+  if (warp < LNT_CW) {
+    float *red = reinterpret_cast<float *>(sm);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) {
+        const int cc = 4 * lane + 128 * i + j;
+        red[(warp * nparts + 0) * cols + cc] = pg[i][j];
+        red[(warp * nparts + 1) * cols + cc] = pb[i][j];
+        if (nparts > 2) red[(warp * nparts + 2) * cols + cc] = pc[i][j];
+        if constexpr (NH > 0) {
+#pragma unroll
+          for (int hh = 0; hh < NH; ++hh) red[(warp * nparts + 3 + hh) * cols + cc] = pw[j][hh];
+        }
+      }
+  }
+  __syncthreads();
+  const float *red = reinterpret_cast<const float *>(sm);
+  for (int c = threadIdx.x; c < nparts * cols; c += blockDim.x) {
+    float sacc = 0.f;
+#pragma unroll
+    for (int w = 0; w < LNT_CW; ++w) sacc += red[w * nparts * cols + c];
+    partial[(int64_t)blockIdx.x * nparts * cols + c] = sacc;
+  }
+}
+
 // ---------------------------------------------- channel-first (c <= 32)
 // The triangle multiplication normalises p[c, i, j] over c with the data
 // channel-first (x[c*rows + row]): one thread per row, the C channel values
@@ -698,6 +918,29 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   return EVO_OK;
 }
 
+// returns the grid size (= number of partial blocks)
+int ln_bwd_tma_launch(int64_t rows, int cols, const float *dy, const float *x, const float *mean,
+                      const float *rstd, const float *gamma, const float *beta,
+                      const float *dres, const float *dproj, int64_t p_rs, const bf16 *Wp,
+                      int nh, float *dx, bf16 *dxa, float *ws, int nparts, cudaStream_t st) {
+  const int rch = dproj ? LntLayout<1, 8>::RCH : (cols == 128 ? LntLayout<1, 0>::RCH : LntLayout<2, 0>::RCH);
+  const int64_t nchunks = (rows + rch - 1) / rch;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), nchunks));
+#define LT(NV_, NH_)                                                                        \
+  do {                                                                                      \
+    auto kfn = ln_bwd_tma_kernel<NV_, NH_>;                                                 \
+    EVO_MAX_SMEM_ONCE(kfn);                                                                 \
+    kfn<<<nb, (LntLayout<NV_, NH_>::CW + 1) * 32, LntLayout<NV_, NH_>::SMEM, st>>>(                          \
+        rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs, Wp, nh, dx, dxa, ws, nparts); \
+  } while (0)
+  if (dproj) LT(1, 8);
+  else if (cols == 128) LT(1, 0);
+  else LT(2, 0);
+#undef LT
+  EVO_LAUNCHED("ln_bwd_tma_kernel");
+  return nb;
+}
+
 template <typename TDY, typename TX, typename TDX>
 int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const void *x,
                   int64_t x_rs, int64_t x_cs, const float *mean, const float *rstd,
@@ -727,6 +970,23 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
       if (want) {
         ln_param_reduce_kernel<<<(2 * cols + 31) / 32, 512, 0, st>>>(nb, cols, 2, ws, dgamma,
                                                                      dbeta, nullptr, acc);
+        EVO_LAUNCHED("ln_param_reduce_kernel");
+      }
+      return EVO_OK;
+    }
+  }
+  if constexpr (std::is_same<TDY, float>::value && std::is_same<TX, float>::value &&
+                std::is_same<TDX, float>::value) {
+    if (vec && dy_rs == cols && x_rs == cols && dx_rs == cols && (!dx_act || dxa_rs == cols) &&
+        rows % 4 == 0 && aligned16(mean) && aligned16(rstd)) {
+      nparts = want ? (dx_colsum ? 3 : 2) : 0;
+      const int nb = ln_bwd_tma_launch(rows, cols, dyp, xp, mean, rstd, gamma, nullptr, dres,
+                                       nullptr, 0, nullptr, 0, dxp,
+                                       reinterpret_cast<bf16 *>(dx_act), ws, nparts, st);
+      if (want) {
+        ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(nb, cols, nparts, ws,
+                                                                          dgamma, dbeta,
+                                                                          dx_colsum, acc);
         EVO_LAUNCHED("ln_param_reduce_kernel");
       }
       return EVO_OK;
@@ -836,14 +1096,23 @@ int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, 
                   (!dx_act || aligned16(dx_act)),
               EVO_EARG, "layernorm_bwd_proj: operands must be 16-byte aligned");
   if (rows == 0) return EVO_OK;
+  float *w = reinterpret_cast<float *>(ws);
+  const int nparts = 3 + 8;
+  if (rows % 4 == 0 && p_rs % 4 == 0 && aligned16(dproj) && aligned16(mean) && aligned16(rstd)) {
+    const int nb = ln_bwd_tma_launch(rows, cols, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
+                                     reinterpret_cast<const bf16 *>(Wp), nh, dx,
+                                     reinterpret_cast<bf16 *>(dx_act), w, nparts, st);
+    ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
+        nb, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
+    EVO_LAUNCHED("ln_param_reduce_kernel");
+    return EVO_OK;
+  }
   const int64_t need_blocks = (rows + LN_WARPS - 1) / LN_WARPS;
   const int nblk = (int)std::min<int64_t>(LN_BWD_BLOCKS, std::max<int64_t>(need_blocks, 1));
-  float *w = reinterpret_cast<float *>(ws);
   ln_bwd_proj_kernel<8><<<nblk, LN_WARPS * 32, 0, st>>>(
       rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
       reinterpret_cast<const bf16 *>(Wp), nh, dx, reinterpret_cast<bf16 *>(dx_act), w);
   EVO_LAUNCHED("ln_bwd_proj_kernel");
-  const int nparts = 3 + 8;
   ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
       nblk, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
   EVO_LAUNCHED("ln_param_reduce_kernel");

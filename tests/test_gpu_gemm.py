@@ -76,6 +76,9 @@ def test_gemm_epilogues_bf16_out(K, force_simt):
     want = raw.clone()
     want[:, col0:] = torch.sigmoid(raw[:, col0:])
     assert rel(C.float(), want) < 5e-3
+    # the gate columns alone (bf16 out: packed bf16x2 tanh on whole chunks)
+    assert rel(C.float()[:, col0:], want[:, col0:]) < 5e-3
+    assert float((C.float()[:, col0:] - want[:, col0:]).abs().max()) < 1e-2
 
 
 @pytest.mark.parametrize("force_simt", [False, True])
