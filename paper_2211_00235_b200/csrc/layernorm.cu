@@ -126,75 +126,6 @@ __device__ __forceinline__ float warp_sum8_scatter(const float (&v)[8], int lane
   return y;
 }
 
-// -------------------------------------- forward + pair-bias projection
-// c_z = 128 rows (NV = 1): y = LN(x) (bf16, optional) and
-// proj[hh*p_rs + row] = sum_c bf16(y[row,c]) * Wp[c*NH + hh]   (NH <= 8)
-// (the pair-bias projection of the attention sub-ops, src/evoformer.py:279).
-template <int NH>
-__global__ void __launch_bounds__(LN_WARPS * 32)
-ln_fwd_proj_kernel(int64_t rows, const float *__restrict__ x, const float *__restrict__ gamma,
-                   const float *__restrict__ beta, bf16 *__restrict__ y,
-                   float *__restrict__ mean_out, float *__restrict__ rstd_out, float eps,
-                   const bf16 *__restrict__ Wp, int nh, float *__restrict__ proj, int64_t p_rs) {
-  // Like ln_fwd_vec_kernel (a few rows per warp, many small blocks, loads
-  // issued before any reduction) with the projection weights staged in smem
-  // as fp32 [128][NH] (read as 16-byte vectors, no registers held).
-  static_assert(NH == 8, "transposing reduction is written for 8 heads");
-  constexpr int cols = 128, RPW = 2;
-  __shared__ __align__(16) float sW[cols * NH];
-  for (int i = threadIdx.x; i < cols * NH; i += blockDim.x) {
-    const int c = i / NH, hh = i % NH;
-    sW[i] = hh < nh ? __bfloat162float(Wp[c * nh + hh]) : 0.f;
-  }
-  __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int64_t row0 = ((int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5)) * RPW;
-  const float4 g4 = *reinterpret_cast<const float4 *>(gamma + 4 * lane);
-  const float4 b4 = *reinterpret_cast<const float4 *>(beta + 4 * lane);
-  const int hsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  float v[RPW][4];
-#pragma unroll
-  for (int r = 0; r < RPW; ++r)
-    if (row0 + r < rows) Vec<float, 4>::load(x + (row0 + r) * cols + 4 * lane, v[r]);
-#pragma unroll
-  for (int r = 0; r < RPW; ++r) {
-    const int64_t row = row0 + r;
-    if (row >= rows) break;
-    float s = 0.f;  // same summation order as ln_fwd_vec_kernel (bitwise equal y, mu, rstd)
-#pragma unroll
-    for (int j = 0; j < 4; ++j) s += v[r][j];
-    const float mu = warp_sum(s) * (1.f / cols);
-    float q = 0.f;
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float d = v[r][j] - mu;
-      q += d * d;
-    }
-    const float rs = 1.f / sqrtf(warp_sum(q) * (1.f / cols) + eps);
-    float o[4] = {(v[r][0] - mu) * rs * g4.x + b4.x, (v[r][1] - mu) * rs * g4.y + b4.y,
-                  (v[r][2] - mu) * rs * g4.z + b4.z, (v[r][3] - mu) * rs * g4.w + b4.w};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) o[j] = __bfloat162float(__float2bfloat16_rn(o[j]));
-    if (y) Vec<bf16, 4>::store(y + row * cols + 4 * lane, o);
-    float pr[NH] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
-#pragma unroll
-    for (int j = 0; j < 4; ++j) {
-      const float4 w0 = *reinterpret_cast<const float4 *>(sW + (4 * lane + j) * NH);
-      const float4 w1 = *reinterpret_cast<const float4 *>(sW + (4 * lane + j) * NH + 4);
-      pr[0] = fmaf(o[j], w0.x, pr[0]); pr[1] = fmaf(o[j], w0.y, pr[1]);
-      pr[2] = fmaf(o[j], w0.z, pr[2]); pr[3] = fmaf(o[j], w0.w, pr[3]);
-      pr[4] = fmaf(o[j], w1.x, pr[4]); pr[5] = fmaf(o[j], w1.y, pr[5]);
-      pr[6] = fmaf(o[j], w1.z, pr[6]); pr[7] = fmaf(o[j], w1.w, pr[7]);
-    }
-    const float tot = warp_sum8_scatter(pr, lane);
-    if ((lane & 3) == 0 && hsel < nh) proj[(int64_t)hsel * p_rs + row] = tot;
-    if (lane == 0) {
-      mean_out[row] = mu;
-      rstd_out[row] = rs;
-    }
-  }
-}
-
 // --------------------------------------------------------- generic forward
 template <typename TX, typename TY, int V>
 __global__ void __launch_bounds__(LN_WARPS * 32)
@@ -655,6 +586,203 @@ ln_bwd_tma_kernel(int64_t rows, const float *__restrict__ dy, const float *__res
   }
 }
 
+// --------------------------------------------- TMA-staged forward (fp32 x)
+// Same producer / consumer split as the backward: the producer lane streams
+// RCH-row chunks of x into an LNF_NS-deep ring.  The forward has no
+// per-column accumulators, so a consumer warp normalises FOUR rows at once,
+// eight lanes per row (lane l8 owns columns 4*l8 + 32*i): the two dependent
+// row reductions are 3-level 8-lane butterflies shared by the four rows
+// instead of 5-level full-warp ones per row (the 32-lane mapping measured
+// shuffle-latency bound at ~2.7 TB/s).  gamma / beta (and the projection
+// weights) sit in smem.  NH > 0 fuses the pair-bias projection of the bf16 y
+// (staged per warp in smem, then a 32-lane pass with W in registers):
+// proj[hh * p_rs + row] = sum_c y[row, c] * Wp[c, hh]  (src/evoformer.py:279).
+constexpr int LNF_CW = 12, LNF_NS = 6;
+
+template <int NV>
+struct LnfLayout {
+  static constexpr int cols = NV * 128, RCH = 4 * LNF_CW / NV;
+  static constexpr uint32_t STAGE = RCH * cols * 4;
+  static constexpr uint32_t OFF_P = LNF_NS * STAGE;  // gamma, beta, per-warp y rows
+  static constexpr uint32_t OFF_BAR = OFF_P + 2 * cols * 4 + LNF_CW * 4 * 32 * 8;
+  static constexpr uint32_t SMEM = OFF_BAR + 2 * LNF_NS * 8;
+};
+
+// Sum 8 per-lane values over the 8 lanes of a row group (xor 4, 2, 1) with a
+// transposing butterfly: lane l8 ends with the total of value l8.
+__device__ __forceinline__ float group8_sum8_scatter(const float (&v)[8], int l8) {
+  const bool u4 = l8 & 4, u2 = l8 & 2, u1 = l8 & 1;
+  float w[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float send = u4 ? v[k] : v[k + 4];
+    const float keep = u4 ? v[k + 4] : v[k];
+    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 4);
+  }
+  float x2[2];
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const float send = u2 ? w[k] : w[k + 2];
+    const float keep = u2 ? w[k + 2] : w[k];
+    x2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 2);
+  }
+  const float send = u1 ? x2[0] : x2[1];
+  return (u1 ? x2[1] : x2[0]) + __shfl_xor_sync(0xffffffffu, send, 1);
+}
+
+__device__ __forceinline__ float group8_sum(float v) {
+  v += __shfl_xor_sync(0xffffffffu, v, 4);
+  v += __shfl_xor_sync(0xffffffffu, v, 2);
+  v += __shfl_xor_sync(0xffffffffu, v, 1);
+  return v;
+}
+
+template <int NV, int NH, typename TY>
+__global__ void __launch_bounds__((LNF_CW + 1) * 32, 1)
+ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__restrict__ gamma,
+                  const float *__restrict__ beta, TY *__restrict__ y, float *__restrict__ mean_out,
+                  float *__restrict__ rstd_out, float eps, const bf16 *__restrict__ Wp, int nh,
+                  float *__restrict__ proj, int64_t p_rs) {
+  using Lay = LnfLayout<NV>;
+  constexpr int cols = Lay::cols, RCH = Lay::RCH, NI = 4 * NV;
+  static_assert(NH == 0 || (NH == 8 && NV == 1), "projection: c_z = 128, 8 heads");
+  extern __shared__ __align__(128) uint8_t sm[];
+  float *sg = reinterpret_cast<float *>(sm + Lay::OFF_P), *sbt = sg + cols, *sW = sbt + cols;  // sW: y staging
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + Lay::OFF_BAR);
+  uint64_t *empty = full + LNF_NS;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int64_t nchunks = (rows + RCH - 1) / RCH;
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < LNF_NS; ++s) {
+      tc::mbar_init(&full[s], 1);
+      tc::mbar_init(&empty[s], LNF_CW);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  for (int i = threadIdx.x; i < cols; i += blockDim.x) {
+    sg[i] = gamma[i];
+    sbt[i] = beta[i];
+  }
+  __syncthreads();
+  if (warp == LNF_CW) {
+    if (lane == 0) {
+      int it = 0;
+      for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+        const int s = it % LNF_NS;
+        if (it >= LNF_NS) tc::mbar_wait(&empty[s], ((it / LNF_NS) - 1) & 1);
+        const int64_t r0 = c * RCH;
+        const uint32_t nr = (uint32_t)(rows - r0 < RCH ? rows - r0 : RCH);
+        tc::mbar_expect_tx(&full[s], nr * cols * 4);
+        tc::bulk_load(sm + s * Lay::STAGE, x + r0 * cols, nr * cols * 4, &full[s]);
+      }
+    }
+    return;
+  }
+  const int l8 = lane & 7, rg = lane >> 3;
+  constexpr float inv_n = 1.f / cols;
+  // projection: 32-lane layout (lane owns columns 4*lane..+3, W in registers)
+  // over the warp's four bf16 y rows staged in smem
+  float W[4][NH > 0 ? NH : 1];
+  uint2 *sy = reinterpret_cast<uint2 *>(sW) + warp * 4 * 32;  // [4 rows][32 lanes] x 4 bf16
+  if constexpr (NH > 0) {
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int hh = 0; hh < NH; ++hh)
+        W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
+  }
+  const int hsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+  int it = 0;
+  for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
+    const int s = it % LNF_NS;
+    tc::mbar_wait(&full[s], (it / LNF_NS) & 1);
+    const int64_t r0 = c * RCH;
+    const int nr = (int)(rows - r0 < RCH ? rows - r0 : RCH);
+    const float *st = reinterpret_cast<const float *>(sm + s * Lay::STAGE);
+    for (int q4 = warp; 4 * q4 < nr; q4 += LNF_CW) {
+      const int r = 4 * q4 + rg;
+      const bool ok = r < nr;  // per row group; the shuffles stay in-group
+      float v[NI][4];
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        if (ok) Vec<float, 4>::load(st + r * cols + 4 * l8 + 32 * i, v[i]);
+        else v[i][0] = v[i][1] = v[i][2] = v[i][3] = 0.f;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) sum += v[i][j];
+      }
+      const float mu = group8_sum(sum) * inv_n;
+      float qq = 0.f;
+#pragma unroll
+      for (int i = 0; i < NI; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+          const float d = v[i][j] - mu;
+          qq += d * d;
+        }
+      const float rs = 1.f / sqrtf(group8_sum(qq) * inv_n + eps);
+      const int64_t row = r0 + r;
+#pragma unroll
+      for (int i = 0; i < NI; ++i) {
+        const int cc = 4 * l8 + 32 * i;
+        const float4 g4 = *reinterpret_cast<const float4 *>(sg + cc);
+        const float4 b4 = *reinterpret_cast<const float4 *>(sbt + cc);
+        float o[4] = {(v[i][0] - mu) * rs * g4.x + b4.x, (v[i][1] - mu) * rs * g4.y + b4.y,
+                      (v[i][2] - mu) * rs * g4.z + b4.z, (v[i][3] - mu) * rs * g4.w + b4.w};
+        if (y && ok) Vec<TY, 4>::store(y + row * cols + cc, o);
+        if constexpr (NH > 0) {  // column group cc/4 = l8 + 8 i of row rg
+          __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);
+          __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
+          sy[rg * 32 + l8 + 8 * i] = make_uint2(*reinterpret_cast<uint32_t *>(&lo),
+                                                *reinterpret_cast<uint32_t *>(&hi));
+        }
+      }
+      if constexpr (NH > 0) {
+        __syncwarp();
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          if (4 * q4 + rr >= nr) break;  // warp-uniform
+          const uint2 u = sy[rr * 32 + lane];
+          const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
+          const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
+          const float yv[4] = {f01.x, f01.y, f23.x, f23.y};
+          float pr[8];
+#pragma unroll
+          for (int hh = 0; hh < 8; ++hh) pr[hh] = 0.f;
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+#pragma unroll
+            for (int hh = 0; hh < NH; ++hh) pr[hh] = fmaf(yv[j], W[j][hh], pr[hh]);
+          const float tot = warp_sum8_scatter(pr, lane);
+          if ((lane & 3) == 0 && hsel < nh) proj[(int64_t)hsel * p_rs + r0 + 4 * q4 + rr] = tot;
+        }
+        __syncwarp();
+      }
+      if (ok && l8 == 0) {
+        mean_out[row] = mu;
+        rstd_out[row] = rs;
+      }
+    }
+    __syncwarp();
+    if (lane == 0) tc::mbar_arrive(&empty[s]);
+  }
+}
+
+template <int NV, int NH, typename TY>
+int ln_fwd_tma_launch(int64_t rows, const float *x, const float *gamma, const float *beta, TY *y,
+                      float *mean, float *rstd, float eps, const bf16 *Wp, int nh, float *proj,
+                      int64_t p_rs, cudaStream_t st) {
+  using Lay = LnfLayout<NV>;
+  const int64_t nchunks = (rows + Lay::RCH - 1) / Lay::RCH;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), nchunks));
+  auto kfn = ln_fwd_tma_kernel<NV, NH, TY>;
+  EVO_MAX_SMEM_ONCE(kfn);
+  kfn<<<nb, (LNF_CW + 1) * 32, Lay::SMEM, st>>>(rows, x, gamma, beta, y, mean, rstd, eps, Wp, nh,
+                                                proj, p_rs);
+  EVO_LAUNCHED("ln_fwd_tma_kernel");
+  return EVO_OK;
+}
+
 // ---------------------------------------------- channel-first (c <= 32)
 // The triangle multiplication normalises p[c, i, j] over c with the data
 // channel-first (x[c*rows + row]): one thread per row, the C channel values
@@ -894,6 +1022,15 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   }
   const bool vec = x_cs == 1 && (cols == 128 || cols == 256) && x_rs % 4 == 0 && y_rs % 4 == 0 &&
                    aligned16(x) && aligned16(y) && aligned16(gamma) && aligned16(beta);
+  if constexpr (std::is_same<TX, float>::value) {
+    if (vec && x_rs == cols && y_rs == cols) {
+      if (cols == 128)
+        return ln_fwd_tma_launch<1, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, nullptr, 0,
+                                           nullptr, 0, st);
+      return ln_fwd_tma_launch<2, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, nullptr, 0,
+                                         nullptr, 0, st);
+    }
+  }
   if (vec) {
     dim3 vgrid((unsigned)((rows + 4 * LN_WARPS - 1) / (4 * LN_WARPS)));  // 4 rows per warp
     if (cols == 128)
@@ -918,11 +1055,12 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   return EVO_OK;
 }
 
-// returns the grid size (= number of partial blocks)
+// *nb_out = the grid size (= number of partial blocks)
 int ln_bwd_tma_launch(int64_t rows, int cols, const float *dy, const float *x, const float *mean,
                       const float *rstd, const float *gamma, const float *beta,
                       const float *dres, const float *dproj, int64_t p_rs, const bf16 *Wp,
-                      int nh, float *dx, bf16 *dxa, float *ws, int nparts, cudaStream_t st) {
+                      int nh, float *dx, bf16 *dxa, float *ws, int nparts, cudaStream_t st,
+                      int *nb_out) {
   const int rch = dproj ? LntLayout<1, 8>::RCH : (cols == 128 ? LntLayout<1, 0>::RCH : LntLayout<2, 0>::RCH);
   const int64_t nchunks = (rows + rch - 1) / rch;
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), nchunks));
@@ -938,7 +1076,8 @@ int ln_bwd_tma_launch(int64_t rows, int cols, const float *dy, const float *x, c
   else LT(2, 0);
 #undef LT
   EVO_LAUNCHED("ln_bwd_tma_kernel");
-  return nb;
+  *nb_out = nb;
+  return EVO_OK;
 }
 
 template <typename TDY, typename TX, typename TDX>
@@ -980,9 +1119,11 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
     if (vec && dy_rs == cols && x_rs == cols && dx_rs == cols && (!dx_act || dxa_rs == cols) &&
         rows % 4 == 0 && aligned16(mean) && aligned16(rstd)) {
       nparts = want ? (dx_colsum ? 3 : 2) : 0;
-      const int nb = ln_bwd_tma_launch(rows, cols, dyp, xp, mean, rstd, gamma, nullptr, dres,
+      int nb = 0;
+      const int rc = ln_bwd_tma_launch(rows, cols, dyp, xp, mean, rstd, gamma, nullptr, dres,
                                        nullptr, 0, nullptr, 0, dxp,
-                                       reinterpret_cast<bf16 *>(dx_act), ws, nparts, st);
+                                       reinterpret_cast<bf16 *>(dx_act), ws, nparts, st, &nb);
+      if (rc != EVO_OK) return rc;
       if (want) {
         ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(nb, cols, nparts, ws,
                                                                           dgamma, dbeta,
@@ -1075,12 +1216,9 @@ int layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamm
   EVO_REQUIRE(aligned16(x) && aligned16(gamma) && aligned16(beta) && (!y || aligned16(y)), EVO_EARG,
               "layernorm_fwd_proj: operands must be 16-byte aligned");
   if (rows == 0) return EVO_OK;
-  const int64_t blocks = (rows + 2 * LN_WARPS - 1) / (2 * LN_WARPS);
-  ln_fwd_proj_kernel<8><<<(unsigned)blocks, LN_WARPS * 32, 0, st>>>(
-      rows, x, gamma, beta, reinterpret_cast<bf16 *>(y), mean, rstd, eps,
-      reinterpret_cast<const bf16 *>(Wp), nh, proj, p_rs);
-  EVO_LAUNCHED("ln_fwd_proj_kernel");
-  return EVO_OK;
+  return ln_fwd_tma_launch<1, 8, bf16>(rows, x, gamma, beta, reinterpret_cast<bf16 *>(y), mean,
+                                       rstd, eps, reinterpret_cast<const bf16 *>(Wp), nh, proj,
+                                       p_rs, st);
 }
 
 int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, const float *mean,
@@ -1099,9 +1237,11 @@ int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, 
   float *w = reinterpret_cast<float *>(ws);
   const int nparts = 3 + 8;
   if (rows % 4 == 0 && p_rs % 4 == 0 && aligned16(dproj) && aligned16(mean) && aligned16(rstd)) {
-    const int nb = ln_bwd_tma_launch(rows, cols, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
+    int nb = 0;
+    const int rc = ln_bwd_tma_launch(rows, cols, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
                                      reinterpret_cast<const bf16 *>(Wp), nh, dx,
-                                     reinterpret_cast<bf16 *>(dx_act), w, nparts, st);
+                                     reinterpret_cast<bf16 *>(dx_act), w, nparts, st, &nb);
+    if (rc != EVO_OK) return rc;
     ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
         nb, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
     EVO_LAUNCHED("ln_param_reduce_kernel");

@@ -16,7 +16,8 @@ from tools.ew_bench import timeit  # noqa: E402
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--rows", type=int, default=65536)
-    ap.add_argument("--what", default="all", choices=["all", "vec", "ex", "proj", "proj_tri", "proj_row"])
+    ap.add_argument("--what", default="all")
+    ap.add_argument("--unused", default=None)
     ap.add_argument("--iters", type=int, default=20)
     a = ap.parse_args()
     rows, cols, h = a.rows, 128, 8
@@ -51,6 +52,21 @@ def main():
                                                   dx, dg, db, dW, dres=dres),
                      3 * rows * cols * 4 + h * rows * 4),
     }
+    yb = torch.empty(rows, cols, device=dev, dtype=bf)
+    pb = torch.empty(h, rows, device=dev)
+    from paper_2211_00235_b200.kernels import Mat
+    cases["fwd_bf16"] = (lambda: K.layernorm(x, rows, cols, g, b, yb, mu, rs, 1e-5),
+                         rows * cols * 6 + rows * 8)
+    cases["fwd_f32"] = (lambda: K.layernorm(x, rows, cols, g, b, y, mu, rs, 1e-5),
+                        rows * cols * 8 + rows * 8)
+    cases["fwd_proj"] = (lambda: K.layernorm_proj(x, rows, g, b, yb, mu, rs, 1e-5, Wb, h, pb, rows),
+                         rows * cols * 6 + rows * 8 + h * rows * 4)
+    cases["fwd_proj_noy"] = (lambda: K.layernorm_proj(x, rows, g, b, None, mu, rs, 1e-5, Wb, h, pb,
+                                                      rows),
+                             rows * cols * 4 + rows * 8 + h * rows * 4)
+    cases["fwd_rowdot"] = (lambda: K.gemm(Mat(yb, cols, 1), Mat(Wb, 1, h), Mat(pb, 1, rows), rows, h,
+                                          cols),
+                           rows * cols * 2 + h * rows * 4)
     for name, (fn, byt) in cases.items():
         if a.what != "all" and not name.startswith(a.what):
             continue
