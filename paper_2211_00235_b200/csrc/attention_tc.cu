@@ -699,6 +699,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       // pass 1: logits of this thread's KQ keys -> registers, local max
       float x[KQ];
       float mx = -INFINITY;
+      const bool kfull = kb + KQ <= L;  // interior key slices skip the mask
 #pragma unroll
       for (int c = 0; c < KQ / 32; ++c) {
         uint32_t v[32];
@@ -709,10 +710,15 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
         for (int j = 0; j < 32; ++j) {
           float xx = __uint_as_float(v[j]) * sc_l2;
           if (BIASMODE) xx += bb[j];
-          if (kb + 32 * c + j >= L) xx = -INFINITY;
           x[32 * c + j] = xx;
-          mx = fmaxf(mx, xx);
         }
+        if (!kfull) {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (kb + 32 * c + j >= L) x[32 * c + j] = -INFINITY;
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j) mx = fmaxf(mx, x[32 * c + j]);
       }
       float *sm_ = sMax + p * 512;
       sm_[qr * 128 + t] = mx;
@@ -1226,17 +1232,21 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   float *sLse = reinterpret_cast<float *>(sRow + NBUF * ROWB);
   float *sDq = sLse + 256;
   // 0 bias, 1-2 row data (row parity), 3-5 S^T/dP^T MMAs (region),
-  // 6-7 the row's last dV/dK MMAs (row parity), 8-9 unit's elementwise pass
-  // done (one arrival per warp; unit parity: a warp can be one unit ahead of
-  // the slowest, never two, since unit u+2's S MMAs wait for unit u's
-  // arrivals), 10-12 a unit's dV/dK MMAs done (region):
+  // 6-7 the row's last dV/dK MMAs (row parity), 8-9 and 13 unit's
+  // elementwise pass done (one arrival per warp; by region u % 3, see
+  // ewdone below), 10-12 a unit's dV/dK MMAs done (region):
   // the region is rewritten by the S^T MMA two units later only after its
   // packed P^T / dS^T were consumed
   // (row-data barriers 1..NBUF; the others shifted by 1 when NBUF == 3)
   uint64_t *bars_all = reinterpret_cast<uint64_t *>(sDq + 256);
   uint64_t *rowbar = bars_all + 1;
-  uint64_t *bars = bars_all + (NBUF - 2);  // bars[3..12] as documented above
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 14);
+  uint64_t *bars = bars_all + (NBUF - 2);  // bars[3..13] as documented above
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 15);
+  // unit-done barriers by REGION (u % 3): unit u+3's arrivals need unit u+3's
+  // S^T MMA, which waits for unit u's dV/dK MMAs, which wait for unit u's
+  // arrivals -- so a barrier never completes twice before its waiter looked
+  // (two per-parity barriers could: u+2's S^T MMA only waits for u-1)
+  auto ewdone = [&](int rg) -> uint64_t * { return rg < 2 ? &bars[8 + rg] : &bars[13]; };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // key row in the tile
@@ -1253,8 +1263,9 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   constexpr int ISSUER = 512;
   const bool ew = tid < 512;  // elementwise warps
   if (tid == ISSUER) {
-    for (int i = 0; i < 14; ++i) {
-      const bool ewd = &bars_all[i] == &bars[8] || &bars_all[i] == &bars[9];
+    for (int i = 0; i < 15; ++i) {
+      const bool ewd = &bars_all[i] == ewdone(0) || &bars_all[i] == ewdone(1) ||
+                       &bars_all[i] == ewdone(2);
       mbar_init(&bars_all[i], ewd ? 16 : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1366,7 +1377,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
         const int64_t r = b_lo + u / NU;
         const int ui = u % NU;
         const int rp = (int)((r - b_lo) & 1);
-        mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));  // all 16 warps packed unit u
+        mbar_wait(ewdone((int)(u % 3)), (uint32_t)((u / 3) & 1));  // all 16 warps packed unit u
         fence_after();
         // at a row's first unit the warps have read row r-1's accumulators,
         // so row r-1's smem buffer is free for row r-1+NBUF
@@ -1465,7 +1476,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     tmem_st_wait();
     fence_before();
     __syncwarp();
-    if (lane == 0) mbar_arrive(&bars[8 + (u & 1)]);
+    if (lane == 0) mbar_arrive(ewdone(reg));
     reg = reg == 2 ? 0 : reg + 1;
   }
   if (nrows > 0) readout(b_hi - 1);
@@ -1526,13 +1537,15 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
   uint8_t *sI = sRow + NBUF * ROWB;  // 32 x 32 bf16 identity, K-major SW64
   // 0 bias, 1-2 row data (row parity), 3-5 S/dP MMAs (region), 6-7 row's
-  // last dQ MMAs (row parity), 8-9 unit packed (16 warp arrivals, unit
-  // parity), 10-12 unit's MMAs done (region), 13 chunk's last MMAs
+  // last dQ MMAs (row parity), 8-9 and 14 unit packed (16 warp arrivals, by
+  // region u % 3), 10-12 unit's MMAs done (region), 13 chunk's last MMAs
   // (row-data barriers 1..NBUF; the others shifted by 1 when NBUF == 3)
   uint64_t *bars_all = reinterpret_cast<uint64_t *>(sI + 2048);
   uint64_t *rowbar = bars_all + 1;
   uint64_t *bars = bars_all + (NBUF - 2);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 15);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars_all + 16);
+  // unit-done barriers by region (u % 3), see the dk/dv kernel
+  auto ewdone = [&](int rg) -> uint64_t * { return rg < 2 ? &bars[8 + rg] : &bars[14]; };
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
@@ -1547,8 +1560,9 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   const int64_t U = nrows > 0 ? nrows * NU : 0;
 
   if (tid == 512) {
-    for (int i = 0; i < 15; ++i) {
-      const bool ewd = &bars_all[i] == &bars[8] || &bars_all[i] == &bars[9];
+    for (int i = 0; i < 16; ++i) {
+      const bool ewd = &bars_all[i] == ewdone(0) || &bars_all[i] == ewdone(1) ||
+                       &bars_all[i] == ewdone(2);
       mbar_init(&bars_all[i], ewd ? 16 : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -1630,7 +1644,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
         const int64_t r = b_lo + u / NU;
         const int ui = u % NU;
         const int rp = (int)((r - b_lo) & 1);
-        mbar_wait(&bars[8 + (u & 1)], (uint32_t)((u >> 1) & 1));
+        mbar_wait(ewdone((int)(u % 3)), (uint32_t)((u / 3) & 1));
         fence_after();
         if (ui == 0 && r > b_lo && r - 1 + NBUF < b_hi) {  // row r-1 read back: buffer free
           if (lane == 0) load_row(r - 1 + NBUF);
@@ -1757,7 +1771,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       tmem_st_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[8 + (u & 1)]);
+      if (lane == 0) mbar_arrive(ewdone(reg));
       reg = reg == 2 ? 0 : reg + 1;
     }
     if (nrows > 0) {
@@ -2016,7 +2030,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   const size_t nbuf = BM_ ? 2 : 3;
   if (pipe) {
     const size_t smem = (BM_ ? BIAS_BYTES : 0) +
-                        nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2048 + 15 * 8 +
+                        nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2048 + 16 * 8 +
                         16;
     dim3 grid(tiles, d->H, (unsigned)nch);
     if (Lp == 256) {
@@ -2038,7 +2052,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   if (pipe) {
     const size_t smem = (BM_ ? BIAS_BYTES : 0) +
                         nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2 * 256 * 4 +
-                        14 * 8 + 16;
+                        15 * 8 + 16;
     dim3 grid(tiles, d->H, (unsigned)nch);
     if (Lp == 256) {
       EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_, 4>));
