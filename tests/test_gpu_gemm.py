@@ -135,7 +135,7 @@ def test_gemm_tc_path_is_taken(K):
 
 
 @pytest.mark.parametrize("dtype", [torch.bfloat16, torch.float32])
-@pytest.mark.parametrize("M,N,Kd,a_k", [(5000, 8, 128, True), (4100, 12, 100, False),
+@pytest.mark.parametrize("M,N,Kd,a_k", [(5000, 8, 128, True), (4100, 12, 100, False), (4099, 4, 128, True),
                                         (65536, 8, 128, True)])
 def test_gemm_skinny_rowdot(K, dtype, M, N, Kd, a_k):
     """N <= 16 (the pair-bias projection): output in the [N, M] layout."""
