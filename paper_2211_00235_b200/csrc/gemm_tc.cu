@@ -748,6 +748,34 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
 int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   if (d->B1 * d->B2 != 1) return 0;
   {
+    // 32-column groups (the outer-product-mean o[i,j,p,q], c = 32): a 4-D
+    // box {32 q, 2 j, 32 p, 1 i} stores a whole 64-column unit (4 KiB) per
+    // TMA op from the same SW128 staging image as a plain 64-wide box (the
+    // two 64-byte q runs of a row p form one 128-byte swizzle row); the
+    // 2 KiB bulk-copy blocks of mode 4 measured ~1.7x slower
+    const evo_mat &c = d->C;
+    const int64_t es = 2;
+    auto ok16 = [&](int64_t st) { return st > 0 && (st * es) % 16 == 0; };
+    if (d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate && c.cdiv == 32 &&
+        c.cs0 == 1 && c.rdiv > 0 && c.rdiv % 32 == 0 && d->M % c.rdiv == 0 &&
+        d->N % 64 == 0 && ok16(c.cs) && ok16(c.rs0) && ok16(c.rs) &&
+        (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0) {
+      cuuint64_t dims[4] = {32, (cuuint64_t)(d->N / 32), (cuuint64_t)c.rdiv,
+                            (cuuint64_t)(d->M / c.rdiv)};
+      cuuint64_t strides[3] = {(cuuint64_t)(c.cs * es), (cuuint64_t)(c.rs0 * es),
+                               (cuuint64_t)(c.rs * es)};
+      cuuint32_t box[4] = {32, 2, 32, 1}, estr[4] = {1, 1, 1, 1};
+      EncodeTiledFn fn = encode_fn();
+      if (fn && fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, c.ptr, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        *box_w = 64;
+        return 3;
+      }
+    }
+  }
+  {
     // mode 4: every warp chunk (32 rows x 32 columns) is one contiguous
     // 2 KiB bf16 block (the outer-product-mean layouts o[i,j,p,q] and
     // do'[i,p,j,q]): rows 32 elements apart inside a 32-aligned row group,
