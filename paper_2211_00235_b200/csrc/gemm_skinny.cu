@@ -86,87 +86,6 @@ __global__ void __launch_bounds__(256) skinny_rowdot_kernel(const SkArgs a) {
   }
 }
 
-// rowdot, K = 128 bf16 rows, N <= 8 (the pair-bias projection proper):
-// the thread-per-row kernel above reads 256-byte rows with one lane per row
-// (uncoalesced, ~1.5 TB/s).  Here a warp owns 32 consecutive rows and reads
-// each row coalesced (lane l: columns 4l..4l+3, 8 bytes), holds B for its
-// four columns in registers, reduces the eight per-lane partial products
-// with a transposing butterfly (9 shuffles per row, lane group hsel ends
-// with output column hsel), and stages the 32 x 8 results in smem so each
-// output column is written as one coalesced 32-row segment.
-__device__ __forceinline__ float warp_sum8_scatter_sk(const float (&v)[8], int lane) {
-  const bool u16 = lane & 16, u8 = lane & 8, u4 = lane & 4;
-  float w[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float send = u16 ? v[k] : v[k + 4];
-    const float keep = u16 ? v[k + 4] : v[k];
-    w[k] = keep + __shfl_xor_sync(0xffffffffu, send, 16);
-  }
-  float x2[2];
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const float send = u8 ? w[k] : w[k + 2];
-    const float keep = u8 ? w[k + 2] : w[k];
-    x2[k] = keep + __shfl_xor_sync(0xffffffffu, send, 8);
-  }
-  const float send = u4 ? x2[0] : x2[1];
-  float y = (u4 ? x2[1] : x2[0]) + __shfl_xor_sync(0xffffffffu, send, 4);
-  y += __shfl_xor_sync(0xffffffffu, y, 2);
-  y += __shfl_xor_sync(0xffffffffu, y, 1);
-  return y;
-}
-
-template <typename TB>
-__global__ void __launch_bounds__(256) skinny_rowdot128_kernel(const SkArgs a) {
-  __shared__ float sOut[8][8][33];  // [warp][column][row]
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const bf16 *A = reinterpret_cast<const bf16 *>(a.A);
-  const TB *B = reinterpret_cast<const TB *>(a.B);
-  float W[4][8];
-#pragma unroll
-  for (int j = 0; j < 4; ++j)
-#pragma unroll
-    for (int n = 0; n < 8; ++n)
-      W[j][n] = n < a.N ? ldf(B, n * a.brs + (4 * lane + j) * a.bcs) : 0.f;
-  const int hsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
-  const int64_t groups = (a.M + 31) / 32;
-  for (int64_t g = (int64_t)blockIdx.x * 8 + warp; g < groups; g += (int64_t)gridDim.x * 8) {
-    const int64_t m0 = g * 32;
-    const int nr = (int)(a.M - m0 < 32 ? a.M - m0 : 32);
-#pragma unroll 1
-    for (int half = 0; half < 4; ++half) {
-      uint2 u[8];
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {  // eight rows' loads in flight first
-        const int r = 8 * half + i;
-        u[i] = r < nr ? __ldg(reinterpret_cast<const uint2 *>(A + (m0 + r) * a.ars) + lane)
-                      : make_uint2(0u, 0u);
-      }
-#pragma unroll
-      for (int i = 0; i < 8; ++i) {
-        const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u[i].x));
-        const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u[i].y));
-        const float x[4] = {f01.x, f01.y, f23.x, f23.y};
-        float pr[8];
-#pragma unroll
-        for (int n = 0; n < 8; ++n)
-          pr[n] = fmaf(x[0], W[0][n], fmaf(x[1], W[1][n], fmaf(x[2], W[2][n], x[3] * W[3][n])));
-        const float tot = warp_sum8_scatter_sk(pr, lane);
-        if ((lane & 3) == 0) sOut[warp][hsel][8 * half + i] = tot;
-      }
-    }
-    __syncwarp();
-    if (lane < nr) {
-      const int64_t rb = a.e.cmap.row(m0 + lane);
-#pragma unroll
-      for (int n = 0; n < 8; ++n)
-        if (n < a.N) epi_store(a.e, rb + a.e.cmap.col(n), epi_value(a.e, n, sOut[warp][n][lane]));
-    }
-    __syncwarp();
-  }
-}
-
 // ---------------------------------------------------------------- expand
 // A warp owns 32 consecutive rows: lane l loads row m0+l's K <= 16 A values
 // (coalesced when A is column-major, like dbias [h][r*r]), then for each of
@@ -559,16 +478,6 @@ int run(const evo_gemm_desc *d, Kind kind, cudaStream_t st) {
     EVO_MAX_SMEM_ONCE((skinny_rowdot_kernel<T, 16>));
     EVO_MAX_SMEM_ONCE((skinny_rowdot_kernel<T, 8>));
     const int blocks = (int)std::min<int64_t>((d->M + 255) / 256, (int64_t)num_sms() * 4);
-    if constexpr (std::is_same<T, bf16>::value) {
-      if (d->K == 128 && d->N <= 8 && d->A.cs == 1 && (d->A.rs % 4) == 0 &&
-          (reinterpret_cast<uintptr_t>(d->A.ptr) & 7) == 0) {
-        const int64_t groups = (d->M + 31) / 32;
-        const int nb = (int)std::min<int64_t>((groups + 7) / 8, (int64_t)num_sms() * 8);
-        skinny_rowdot128_kernel<T><<<nb, 256, 0, st>>>(a);
-        EVO_LAUNCHED("skinny_rowdot128_kernel");
-        return EVO_OK;
-      }
-    }
     if (d->N <= 8) {
       skinny_rowdot_kernel<T, 8><<<blocks, 256, (size_t)d->K * 8 * sizeof(float), st>>>(a);
     } else {
