@@ -123,7 +123,8 @@ def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, min_rows: int = 512
     """Split-K factor for tall contractions (weight gradients, the OPM input
     gradients): as many K chunks as fit one wave of the 148 SMs next to the
     output tiles, each chunk >= `min_rows` (8 k-steps of the TMA pipeline)."""
-    tiles = max(1, ((M + 127) // 128) * ((N_ + 127) // 128) * batch)
+    tn = 256 if N_ > 128 else 128  # evo_gemm's split-K tile width (gemm_tc.cu choose_bn)
+    tiles = max(1, ((M + 127) // 128) * ((N_ + tn - 1) // tn) * batch)
     by_fill = 148 // tiles
     by_size = rows_k // min_rows
     return int(max(1, min(by_fill, by_size)))
