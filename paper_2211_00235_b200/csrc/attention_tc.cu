@@ -501,6 +501,30 @@ __device__ __forceinline__ void scale_tile(uint8_t *sb, int nfloat4, int nthread
     p[i] = v;
   }
 }
+// A bias tile whose rows run along the thread's index (boxes of [32 outer][128
+// inner] plain floats, outer = the index a thread iterates) rewritten in
+// place, box by box, into the 128B-swizzled [128 inner][32 outer] box layout
+// the row-box readers use, scaled by log2(e): the backward kernels then read
+// a thread's consecutive bias values as 16-byte vectors instead of one
+// strided scalar per element (once per CTA; the tile serves every batch row).
+// All 512 elementwise threads call it (named barrier 1).
+__device__ __forceinline__ void transpose_scale_bias_boxes(uint8_t *sb, int nbox, int tid) {
+  for (int j = 0; j < nbox; ++j) {
+    float *box = reinterpret_cast<float *>(sb + j * 16384);
+    float v[8];
+#pragma unroll
+    for (int i = 0; i < 8; ++i) v[i] = box[tid + 512 * i] * LOG2E;
+    named_bar_sync(1, 512);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int e = tid + 512 * i, o = e >> 7, in = e & 127;
+      *reinterpret_cast<float *>(sb + j * 16384 + in * 128 + ((((o >> 2) ^ (in & 7))) << 4) +
+                                 (o & 3) * 4) = v[i];
+    }
+    named_bar_sync(1, 512);
+  }
+}
+
 // TMEM column of the 16-wide K slice `ks` of bf16-pair data written in place
 // into quarters: keys [i*KQ, (i+1)*KQ) -> cols [i*KQ, i*KQ + KQ/2).
 __device__ __forceinline__ uint32_t quarter_col(int ks, int KQ) {
@@ -1411,7 +1435,8 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
   }
   if (BIASMODE) {
     mbar_wait(&bars_all[0], 0);
-    scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
+    if constexpr (KCONTIG) transpose_scale_bias_boxes(sBias, LPC / 32, tid);
+    else scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
   }
   const float sc_l2 = a.scale * LOG2E;
 
@@ -1446,7 +1471,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     tmem_ld16_nw(rb + 64 + c0, dv);
     tmem_wait_ld();
     float bb[16], ls[16], dq[16];
-    if (BIASMODE) bias_row16<!KCONTIG>(sBias, t, qb, bb);
+    if (BIASMODE) bias_row16<true>(sBias, t, qb, bb);  // row boxes in both modes (see above)
 #pragma unroll
     for (int j = 0; j < 16; j += 4) {  // warp-uniform 16-byte broadcasts
       const float4 l4 = *reinterpret_cast<const float4 *>(sLse + qb + j);
@@ -1709,7 +1734,8 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
     };
     if (BIASMODE) {
       mbar_wait(&bars_all[0], 0);
-      scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
+      if constexpr (TB) transpose_scale_bias_boxes(sBias, LPC / 32, tid);
+      else scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
       named_bar_sync(1, 512);
     }
     const float sc_l2 = a.scale * LOG2E;
@@ -1744,7 +1770,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       tmem_ld8_nw(rb + 32 + c0, dv);
       tmem_wait_ld();
       float bb[8];
-      if (BIASMODE) bias_row8<!TB>(sBias, t, kb, bb);
+      if (BIASMODE) bias_row8<true>(sBias, t, kb, bb);  // row boxes in both modes
       const bool full = qv && kb + 8 <= L;
       uint32_t pk[4];
 #pragma unroll
