@@ -379,11 +379,11 @@ ln_bwd_proj_kernel(int64_t rows, const float *__restrict__ dy, const float *__re
 // Partials: [block][nparts][cols], reduced by ln_param_reduce_kernel.
 
 // consumer warps: 12 (registers cap 128) / 8 with the projection's W, dW
-template <int NH> constexpr int lnt_cw() { return NH > 0 ? 8 : 12; }
+template <int NV, int NH> constexpr int lnt_cw() { return NH > 0 ? 8 : 12; }
 
 template <int NV, int NH>
 struct LntLayout {
-  static constexpr int CW = lnt_cw<NH>();
+  static constexpr int CW = lnt_cw<NV, NH>();
   static constexpr int cols = NV * 128, RCH = (NH > 0 ? 4 : 2) * CW / NV;
   static constexpr uint32_t RB = RCH * cols * 4;  // 12 KB per row tensor
   static constexpr uint32_t OFF_DY = RB, OFF_DR = 2 * RB, OFF_MU = 3 * RB;
@@ -395,7 +395,7 @@ struct LntLayout {
 };
 
 template <int NV, int NH>
-__global__ void __launch_bounds__((lnt_cw<NH>() + 1) * 32, 1)
+__global__ void __launch_bounds__((lnt_cw<NV, NH>() + 1) * 32, 1)
 ln_bwd_tma_kernel(int64_t rows, const float *__restrict__ dy, const float *__restrict__ x,
                   const float *__restrict__ mean, const float *__restrict__ rstd,
                   const float *__restrict__ gamma, const float *__restrict__ beta,
@@ -597,7 +597,7 @@ ln_bwd_tma_kernel(int64_t rows, const float *__restrict__ dy, const float *__res
 // weights) sit in smem.  NH > 0 fuses the pair-bias projection of the bf16 y
 // (staged per warp in smem, then a 32-lane pass with W in registers):
 // proj[hh * p_rs + row] = sum_c y[row, c] * Wp[c, hh]  (src/evoformer.py:279).
-constexpr int LNF_CW = 12, LNF_NS = 6;
+constexpr int LNF_CW = 16, LNF_NS = 6;
 
 template <int NV>
 struct LnfLayout {
