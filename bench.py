@@ -186,6 +186,8 @@ def run_native(args):
     kw = CONFIGS[args.config]
     if args.blocks:
         kw = {**kw, "n_blocks": args.blocks}
+    if args.crop:
+        kw = {**kw, "r": args.crop}
     cfg = pkg.EvoConfig(**kw)
     store = pkg.init_params(cfg, 32, device=dev)
     bp = 2 if (world > 1 and world % 2 == 0 and not args.dp_only) else 1
@@ -461,6 +463,100 @@ def run_native(args):
     return 0
 
 
+EXTRA_AF2 = dict(s=1024, r=256, c_m=64, c_z=128, h=8, c_opm=32, t_factor=4, n_blocks=4)
+
+
+def run_stack(args):
+    """C3 on one GPU: the 4-block extra-MSA stack feeding
+    the main stack (schedules.composed_step), one step = fwd + loss + bwd of
+    both stacks with every parameter gradient, captured as one CUDA graph.
+    The main-stack depth is --blocks (default 48)."""
+    import numpy as np
+    import torch
+
+    import paper_2211_00235_b200 as pkg
+    from paper_2211_00235_b200 import _native, schedules as S
+    from oracle import evoformer_np as O
+
+    dev = torch.device("cuda", 0)
+    torch.cuda.set_device(dev)
+    kw_m = {**CONFIGS["af2"], "n_blocks": args.blocks or 48}
+    if args.crop:
+        kw_m["r"] = args.crop
+    kw_e = {**EXTRA_AF2, "r": kw_m["r"]}
+    ce, cm = pkg.EvoConfig(**kw_e), pkg.EvoConfig(**kw_m)
+    ste = S.StepState(ce, pkg.init_params(ce, 33, device=dev), args.precision, dev)
+    stm = S.StepState(cm, pkg.init_params(cm, 32, device=dev), args.precision, dev)
+    ste.pack()
+    stm.pack()
+    rng = np.random.default_rng(32)
+    host = [torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).pin_memory()
+            for shape in ((ce.s, ce.r, ce.c_m), (cm.s, cm.r, cm.c_m), (cm.r, cm.r, cm.c_z))]
+    dev_in = [h.to(dev) for h in host]
+    loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
+    for _ in range(args.warmup):
+        S.composed_step(ste, stm, *dev_in)
+    torch.cuda.synchronize()
+    torch.cuda.empty_cache()
+    graph = torch.cuda.CUDAGraph()
+    n0 = _native.launch_count()
+    with torch.cuda.graph(graph):
+        out = S.composed_step(ste, stm, *dev_in)
+        loss_h.copy_(out[2].reshape(1), non_blocking=True)
+    launches_per_step = _native.launch_count() - n0
+    graph.replay()
+    torch.cuda.synchronize()
+
+    def timed(fn, k):
+        torch.cuda.synchronize()
+        a0 = torch.cuda.Event(enable_timing=True)
+        a1 = torch.cuda.Event(enable_timing=True)
+        a0.record()
+        for _ in range(k):
+            fn()
+        a1.record()
+        torch.cuda.synchronize()
+        return a0.elapsed_time(a1) / k
+
+    clocks = Clocks(0)
+    clocks.start()
+    time.sleep(0.3)
+    ms = timed(graph.replay, args.steps)
+    clk = clocks.stop()
+
+    def e2e():  # pinned host inputs -> static device buffers, step, loss -> host
+        for h, d in zip(host, dev_in):
+            d.copy_(h, non_blocking=True)
+        graph.replay()
+
+    ms_e2e = timed(e2e, args.steps)
+    flops = 3 * (O.block_flops(O.Dims(**kw_e)) * ce.n_blocks
+                 + O.block_flops(O.Dims(**kw_m)) * cm.n_blocks)
+    peak, _, _, src = peaks()
+    tflops = flops / (ms / 1e3) / 1e12
+    line = {
+        "metric": METRIC, "value": 1e3 / ms, "unit": "samples/s", "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "ms_per_block_fwd_bwd": ms / (ce.n_blocks + cm.n_blocks),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
+        "config": {"workload": "evoformer_stack_c3", "main": kw_m, "extra": kw_e,
+                   "precision": args.precision, "parallelism": "bp1xdp1", "global_batch": 1,
+                   "l2": "step working set exceeds the 126 MB L2"},
+        "flops_per_step": flops, "step_tflops": tflops, "step_frac_of_peak": tflops / peak,
+        "peak_source": src,
+        "e2e": {"value": 1e3 / ms_e2e, "unit": "samples/s",
+                "h2d_bytes_per_step": sum(h.numel() * 4 for h in host),
+                "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e,
+                "mode": "serial H2D -> graph replay (step + loss D2H)"},
+        "gpu_launches": launches_per_step * args.steps,
+        "gpu_launches_per_step": launches_per_step, "launch_mode": "cuda_graph",
+        "clocks": clk, "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+    }
+    print(json.dumps(line))
+    return 0
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -469,6 +565,11 @@ def main():
     ap.add_argument("--impl", default="native", choices=["native", "reference"])
     ap.add_argument("--config", default="af2", choices=list(CONFIGS))
     ap.add_argument("--blocks", type=int, default=0)
+    ap.add_argument("--crop", type=int, default=0,
+                    help="override the crop size r (C5 sweep: 128 / 256 / 384)")
+    ap.add_argument("--stack", action="store_true",
+                    help="C3: 4-block extra-MSA stack (s_e=1024, c_e=64) feeding a "
+                         "--blocks (default 48) main stack, one GPU")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--dp-only", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
@@ -478,6 +579,8 @@ def main():
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.stack:
+        return run_stack(args)
     return run_native(args)
 
 

@@ -564,6 +564,39 @@ def train_step(P, m, z, d):
                 grads=dict(G))
 
 
+def composed_step(Pe, de: Dims, Pm, dm_: Dims, m_e, m, z):
+    """two ``evoformer_stack`` calls on one tape
+    (src/evoformer.py:464-467): the extra-MSA stack (Pe, de) runs on
+    (m_e, z), its m_e output is dropped, its z output feeds the main stack
+    (Pm, dm_); loss on the main outputs (src/schedules.py:194-195).
+
+    Returns dict(m_out, z_out, loss, dm_e, dm, dz, grads_e, grads_m)."""
+    ce, cm = [], []
+    me_c, z_c = m_e, z
+    for blk in range(de.n_blocks):
+        me_c, z_c, c = block_fwd(Pe, blk, me_c, z_c, de)
+        ce.append(c)
+    m_c = m
+    for blk in range(dm_.n_blocks):
+        m_c, z_c, c = block_fwd(Pm, blk, m_c, z_c, dm_)
+        cm.append(c)
+    loss = np.mean(m_c * m_c) + np.mean(z_c * z_c)
+    dm = m_c * (2.0 / m_c.size)
+    dz = z_c * (2.0 / z_c.size)
+    Gm, Ge = Grads(), Grads()
+    for blk in reversed(range(dm_.n_blocks)):
+        dm, dz = block_vjp(dm, dz, cm[blk], Pm, blk, dm_, Gm)
+    dme = np.zeros_like(me_c)
+    for blk in reversed(range(de.n_blocks)):
+        dme, dz = block_vjp(dme, dz, ce[blk], Pe, blk, de, Ge)
+    for P, G in ((Pe, Ge), (Pm, Gm)):
+        for name in P:
+            if name not in G:
+                G[name] = np.zeros_like(P[name])
+    return dict(m_out=m_c, z_out=z_c, loss=float(loss), dm_e=dme, dm=dm, dz=dz,
+                grads_e=dict(Ge), grads_m=dict(Gm))
+
+
 def run_single(d: Dims, P: dict, seed: int = 32, dtype=np.float64):
     """Oracle counterpart of src/schedules.py:387-399."""
     m, z = make_batch(d, seed, 1, dtype)[0]

@@ -174,6 +174,51 @@ def full_step(st: StepState, m, z):
             dm.reshape(s, r, cfg.c_m), dz.reshape(r, r, cfg.c_z))
 
 
+def composed_step(extra: StepState, main: StepState, m_e, m, z):
+    """an extra-MSA stack (its own EvoConfig: s_e rows,
+    c_e channels, c_head = c_e / h) whose pair output feeds the main stack;
+    its MSA output m_e' is dropped.  The reference has no extra-MSA module
+    (it composes two ``evoformer_stack`` calls, src/evoformer.py:464-467, on
+    one tape); the loss is the main stack's (src/schedules.py:194-195), so
+    the extra stack's backward is seeded with dm_e' = 0 and the main stack's
+    dz_in.  Returns (m_out, z_out, loss[1], dm_e, dm, dz)."""
+    ce, cm = extra.cfg, main.cfg
+    if (ce.r, ce.c_z) != (cm.r, cm.c_z):
+        raise ConfigError(f"extra stack (r={ce.r}, c_z={ce.c_z}) does not feed the main "
+                          f"stack (r={cm.r}, c_z={cm.c_z})")
+    for st in (extra, main):
+        if st.packs is None:
+            st.pack()
+    me_c = m_e.reshape(ce.s * ce.r, ce.c_m)
+    z_c = z.reshape(ce.r * ce.r, ce.c_z)
+    ctx_e = []
+    for blk in range(ce.n_blocks):
+        me_c, z_c, c = E.block_fwd(extra.P, blk, extra.packs[blk], me_c, z_c, ce, extra.act)
+        ctx_e.append(c)
+    m_c = m.reshape(cm.s * cm.r, cm.c_m)
+    ctx_m = []
+    for blk in range(cm.n_blocks):
+        m_c, z_c, c = E.block_fwd(main.P, blk, main.packs[blk], m_c, z_c, cm, main.act)
+        ctx_m.append(c)
+    loss = torch.zeros(1, dtype=F32, device=m.device)
+    dm = torch.empty_like(m_c)
+    dz = torch.empty_like(z_c)
+    K.sq_mean(m_c, loss, dm)
+    K.sq_mean(z_c, loss, dz)
+    for blk in reversed(range(cm.n_blocks)):
+        dm, dz = E.block_bwd(main.P, blk, main.packs[blk], main.grads[blk].packed, ctx_m[blk],
+                             dm, dz, cm, main.act)
+        ctx_m[blk] = None
+    dm_e = torch.zeros(me_c.shape, dtype=F32, device=m.device)
+    for blk in reversed(range(ce.n_blocks)):
+        dm_e, dz = E.block_bwd(extra.P, blk, extra.packs[blk], extra.grads[blk].packed,
+                               ctx_e[blk], dm_e, dz, ce, extra.act)
+        ctx_e[blk] = None
+    return (m_c.reshape(cm.s, cm.r, cm.c_m), z_c.reshape(cm.r, cm.r, cm.c_z), loss,
+            dm_e.reshape(ce.s, ce.r, ce.c_m), dm.reshape(cm.s, cm.r, cm.c_m),
+            dz.reshape(cm.r, cm.r, cm.c_z))
+
+
 def run_single(cfg: EvoConfig, store: ParamStore, seed: int = 32,
                precision: str | None = None) -> RunResult:
     """Reference step on one GPU (src/schedules.py:387-399)."""

@@ -101,3 +101,29 @@ def test_init_params_match_reference_rng_order():
     q = rng.uniform(-0.02, 0.02, size=(8, 8))
     assert np.array_equal(P["blk0.row_attn.q_w"], q)
     assert len(P) == 93 * d.n_blocks
+
+
+def test_composed_step_reduces_to_train_step_and_matches_finite_difference():
+    """The C3 composition (extra stack -> main stack) is two stacks on one
+    tape: with no extra blocks it is the plain step, and its dm_e agrees with
+    a central finite difference of the loss along a random direction."""
+    dm_ = O.Dims(s=4, r=6, c_m=4, c_z=4, h=2, c_opm=2, n_blocks=1)
+    de = O.Dims(s=6, r=6, c_m=2, c_z=4, h=2, c_opm=2, n_blocks=1)
+    Pm, Pe = O.init_params(dm_, 32), O.init_params(de, 33)
+    rng = np.random.default_rng(5)
+    m_e = rng.standard_normal((de.s, de.r, de.c_m))
+    m = rng.standard_normal((dm_.s, dm_.r, dm_.c_m))
+    z = rng.standard_normal((dm_.r, dm_.r, dm_.c_z))
+    d0 = O.Dims(s=6, r=6, c_m=2, c_z=4, h=2, c_opm=2, n_blocks=0)
+    plain = O.train_step(Pm, m, z, dm_)
+    comp0 = O.composed_step({}, d0, Pm, dm_, m_e, m, z)
+    for key in ("m_out", "z_out", "dm", "dz"):
+        assert np.array_equal(plain[key], comp0[key])
+    out = O.composed_step(Pe, de, Pm, dm_, m_e, m, z)
+    v = rng.standard_normal(m_e.shape)
+    eps = 1e-6
+    lp = O.composed_step(Pe, de, Pm, dm_, m_e + eps * v, m, z)["loss"]
+    lm = O.composed_step(Pe, de, Pm, dm_, m_e - eps * v, m, z)["loss"]
+    fd = (lp - lm) / (2 * eps)
+    an = float(np.sum(out["dm_e"] * v))
+    assert abs(fd - an) <= 1e-6 * max(1.0, abs(an)), (fd, an)
