@@ -15,6 +15,10 @@ ranks / max-over-ranks device time.
 
 --impl reference times the reference algorithm's CPU implementation (the
 pinned numpy oracle port, oracle/evoformer_np.py) on the host cores.
+
+Other SURVEY.md §8(d) configurations (1 GPU): --crop R (C5 crop sweep,
+r = 128 / 384), --stack [--blocks K] (C3: the 4-block extra-MSA stack,
+s_e=1024 c_e=64, feeding a K-block main stack, default 48).
 """
 
 from __future__ import annotations

@@ -8,7 +8,8 @@
 //   dO = dGM*G,  dGpre = dGM*O*G*(1-G),  Dq = sum_d dO*O
 //   dS = P*(dO.v - Dq),  dq = scale*dS k,  dk = scale*dS^T q,  dv = P^T dO
 //   dbias[h,q,k] = sum_b dS  (chunk partials + ordered reduce: deterministic)
-// All keys of one (b,h) are resident in shared memory (L <= 256), so the
+// All keys of one (b,h) are resident in shared memory (L <= 1024, the
+// register row of logits sized per instantiation: 256 / 512 / 1024), so the
 // softmax is exact single-pass; no logits ever reach HBM.
 #include "common.cuh"
 
@@ -16,12 +17,14 @@ namespace evo {
 
 int reduce_lead(int dt, int64_t nb, int64_t n1, int64_t n2, const void *src, float *dst,
                 int64_t d_s1, int64_t d_s2, int acc, cudaStream_t st);
+int colsum_partials(int nblk, int64_t cols, const float *part, float *dst, int acc,
+                    cudaStream_t st);
 
 namespace {
 
 constexpr int AW = 8;      // warps per block
 constexpr int QT = 32;     // queries (or keys) per block
-constexpr int MAXL = 256;  // resident keys
+constexpr int MAXL = 1024; // resident keys (kernels instantiated for 256 / 512 / 1024)
 constexpr int MAXD = 64;
 
 template <typename T>
@@ -44,7 +47,7 @@ __device__ void load_rows(float *dst, const void *src, int64_t base, int64_t sl,
   }
 }
 
-template <typename T>
+template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
   extern __shared__ float sm[];
   const int L = a.L, D = a.D, Dp = D + 1;
@@ -68,10 +71,10 @@ __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
     const int64_t qoff = base + (int64_t)q * a.sl;
     for (int d = lane; d < D; d += 32) Qv[d] = ld<T>(a.q, qoff + d);
     __syncwarp();
-    float s[MAXL / 32];
+    float s[ML / 32];
     float mx = -INFINITY;
 #pragma unroll
-    for (int j = 0; j < MAXL / 32; ++j) {
+    for (int j = 0; j < ML / 32; ++j) {
       int k = lane + 32 * j;
       s[j] = -INFINITY;
       if (j < nk && k < L) {
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
     mx = warp_max(mx);
     float sum = 0.f;
 #pragma unroll
-    for (int j = 0; j < MAXL / 32; ++j) {
+    for (int j = 0; j < ML / 32; ++j) {
       int k = lane + 32 * j;
       float p = (j < nk && k < L) ? expf(s[j] - mx) : 0.f;
       s[j] = p;
@@ -95,7 +98,7 @@ __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
     sum = warp_sum(sum);
     const float inv = 1.f / sum;
 #pragma unroll
-    for (int j = 0; j < MAXL / 32; ++j) {
+    for (int j = 0; j < ML / 32; ++j) {
       int k = lane + 32 * j;
       if (j < nk && k < L) P[k] = s[j] * inv;
     }
@@ -114,7 +117,7 @@ __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
 }
 
 // dq, dgpre and per-chunk dbias partials.  grid (ceil(L/QT), H, nchunk).
-template <typename T>
+template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32)
 attn_bwd_dq_kernel(evo_attn_desc a, int64_t chunk, float *dbias_part) {
   extern __shared__ float sm[];
@@ -163,7 +166,7 @@ attn_bwd_dq_kernel(evo_attn_desc a, int64_t chunk, float *dbias_part) {
       __syncwarp();
       const float lse = a.lse[(b * a.H + h) * (int64_t)L + q];
 #pragma unroll
-      for (int j = 0; j < MAXL / 32; ++j) {
+      for (int j = 0; j < ML / 32; ++j) {
         int k = lane + 32 * j;
         if (j < nk && k < L) {
           float sc = 0.f, dp = 0.f;
@@ -200,7 +203,7 @@ attn_bwd_dq_kernel(evo_attn_desc a, int64_t chunk, float *dbias_part) {
 }
 
 // dk, dv.  grid (ceil(L/QT) key tiles, H, nb).
-template <typename T>
+template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32) attn_bwd_dkv_kernel(evo_attn_desc a) {
   extern __shared__ float sm[];
   const int L = a.L, D = a.D, Dp = D + 1;
@@ -249,7 +252,7 @@ __global__ void __launch_bounds__(AW * 32) attn_bwd_dkv_kernel(evo_attn_desc a) 
     }
     __syncwarp();
 #pragma unroll
-    for (int j = 0; j < MAXL / 32; ++j) {
+    for (int j = 0; j < ML / 32; ++j) {
       int q = lane + 32 * j;
       if (j < nq && q < L) {
         float sc = 0.f, dp = 0.f;
@@ -286,39 +289,59 @@ int64_t dbias_chunks(const evo_attn_desc *a) {
 
 }  // namespace
 
-size_t attention_simt_bwd_ws(const evo_attn_desc *a) {
+// gate-bias column sums: GB_PARTS ordered row ranges, then colsum_partials
+constexpr int GB_PARTS = 4 * 148;
+
+size_t dbias_ws_bytes(const evo_attn_desc *a) {
   if (!a->dbias) return 0;
-  int64_t nch = dbias_chunks(a);
-  return (size_t)nch * a->H * a->L * a->L * sizeof(float);
+  return ((size_t)dbias_chunks(a) * a->H * a->L * a->L * sizeof(float) + 255) & ~(size_t)255;
+}
+
+size_t attention_simt_bwd_ws(const evo_attn_desc *a) {
+  return dbias_ws_bytes(a) +
+         (a->dgate_bias ? (size_t)GB_PARTS * a->H * a->D * sizeof(float) : 0);
 }
 
 int attention_simt_fwd(const evo_attn_desc *a, cudaStream_t st) {
   EVO_REQUIRE(a->L >= 1 && a->L <= MAXL && a->D >= 1 && a->D <= MAXD, EVO_EUNSUP,
-              "attention: L=%d D=%d unsupported (L<=256, D<=64)", a->L, a->D);
+              "attention: L=%d D=%d unsupported (L<=1024, D<=64)", a->L, a->D);
   dim3 grid((a->L + QT - 1) / QT, a->H, (unsigned)a->nb);
   size_t smem = (size_t)(2 * a->L * (a->D + 1) + AW * a->L + AW * a->D) * sizeof(float);
-  if (a->dtype == EVO_F32) {
-    EVO_MAX_SMEM_ONCE((attn_fwd_kernel<float>));
-    attn_fwd_kernel<float><<<grid, AW * 32, smem, st>>>(*a);
-  } else {
-    EVO_MAX_SMEM_ONCE((attn_fwd_kernel<bf16>));
-    attn_fwd_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a);
+  EVO_REQUIRE(smem <= 227 * 1024, EVO_EUNSUP, "attention: L=%d D=%d exceeds shared memory",
+              a->L, a->D);
+#define EVO_SIMT_FWD(T, ML)                                             \
+  {                                                                    \
+    EVO_MAX_SMEM_ONCE((attn_fwd_kernel<T, ML>));                       \
+    attn_fwd_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a);           \
   }
+  const bool f32 = a->dtype == EVO_F32;
+  if (a->L <= 256) { if (f32) EVO_SIMT_FWD(float, 256) else EVO_SIMT_FWD(bf16, 256) }
+  else if (a->L <= 512) { if (f32) EVO_SIMT_FWD(float, 512) else EVO_SIMT_FWD(bf16, 512) }
+  else { if (f32) EVO_SIMT_FWD(float, 1024) else EVO_SIMT_FWD(bf16, 1024) }
+#undef EVO_SIMT_FWD
   EVO_LAUNCHED("attn_fwd_kernel");
   return EVO_OK;
 }
 
-// dgate_bias[h*D + d] = sum over (b, l) of dGpre (parity path: one thread
-// per column, rows in order)
+// dgate_bias[h*D + d] = sum over (b, l) of dGpre, deterministic two-stage:
+// block p sums the (b, l) rows [p*rpp, (p+1)*rpp) in order (threads across
+// columns), then colsum_partials adds the GB_PARTS partials in order.
 template <typename T>
-__global__ void gate_bias_colsum_kernel(const evo_attn_desc a) {
-  const int col = blockIdx.x * blockDim.x + threadIdx.x;
-  if (col >= a.H * a.D) return;
+__global__ void gate_bias_part_kernel(const evo_attn_desc a, int64_t rpp, float *part) {
+  const int cols = a.H * a.D;
+  const int64_t n = a.nb * (int64_t)a.L;
+  const int64_t r0 = blockIdx.x * rpp, r1 = min(n, r0 + rpp);
   const T *g = reinterpret_cast<const T *>(a.dgpre);
-  float s = 0.f;
-  for (int64_t b = 0; b < a.nb; ++b)
-    for (int l = 0; l < a.L; ++l) s += to_f(g[b * a.sb + (int64_t)l * a.sl + col]);
-  a.dgate_bias[col] = s;
+  for (int col = threadIdx.x; col < cols; col += blockDim.x) {
+    float s = 0.f;
+#pragma unroll 8
+    for (int64_t r = r0; r < r1; ++r) {
+      const int64_t b = r / a.L;
+      const int l = (int)(r - b * a.L);
+      s += to_f(g[b * a.sb + (int64_t)l * a.sl + col]);
+    }
+    part[(int64_t)blockIdx.x * cols + col] = s;
+  }
 }
 
 int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
@@ -338,25 +361,35 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     dim3 grid((L + QT - 1) / QT, a->H, (unsigned)nch);
     size_t smem = (size_t)(2 * L * (D + 1) + AW * L + 2 * AW * D + (a->dbias ? QT * L : 0)) *
                   sizeof(float);
-    if (a->dtype == EVO_F32) {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<float>));
-      attn_bwd_dq_kernel<float><<<grid, AW * 32, smem, st>>>(*a, chunk, part);
-    } else {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<bf16>));
-      attn_bwd_dq_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a, chunk, part);
-    }
+    EVO_REQUIRE(smem <= 227 * 1024, EVO_EUNSUP,
+                "attention bwd: L=%d D=%d exceeds shared memory", L, D);
+#define EVO_SIMT_DQ(T, ML)                                                   \
+  {                                                                         \
+    EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<T, ML>));                         \
+    attn_bwd_dq_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a, chunk, part); \
+  }
+    const bool f32 = a->dtype == EVO_F32;
+    if (L <= 256) { if (f32) EVO_SIMT_DQ(float, 256) else EVO_SIMT_DQ(bf16, 256) }
+    else if (L <= 512) { if (f32) EVO_SIMT_DQ(float, 512) else EVO_SIMT_DQ(bf16, 512) }
+    else { if (f32) EVO_SIMT_DQ(float, 1024) else EVO_SIMT_DQ(bf16, 1024) }
+#undef EVO_SIMT_DQ
     EVO_LAUNCHED("attn_bwd_dq_kernel");
   }
   {
     dim3 grid((L + QT - 1) / QT, a->H, (unsigned)a->nb);
     size_t smem = (size_t)(2 * L * (D + 1) + 2 * L + AW * 2 * L + AW * 2 * D) * sizeof(float);
-    if (a->dtype == EVO_F32) {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<float>));
-      attn_bwd_dkv_kernel<float><<<grid, AW * 32, smem, st>>>(*a);
-    } else {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<bf16>));
-      attn_bwd_dkv_kernel<bf16><<<grid, AW * 32, smem, st>>>(*a);
-    }
+    EVO_REQUIRE(smem <= 227 * 1024, EVO_EUNSUP,
+                "attention bwd: L=%d D=%d exceeds shared memory", L, D);
+#define EVO_SIMT_DKV(T, ML)                                      \
+  {                                                             \
+    EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<T, ML>));            \
+    attn_bwd_dkv_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a); \
+  }
+    const bool f32 = a->dtype == EVO_F32;
+    if (L <= 256) { if (f32) EVO_SIMT_DKV(float, 256) else EVO_SIMT_DKV(bf16, 256) }
+    else if (L <= 512) { if (f32) EVO_SIMT_DKV(float, 512) else EVO_SIMT_DKV(bf16, 512) }
+    else { if (f32) EVO_SIMT_DKV(float, 1024) else EVO_SIMT_DKV(bf16, 1024) }
+#undef EVO_SIMT_DKV
     EVO_LAUNCHED("attn_bwd_dkv_kernel");
   }
   if (a->dbias) {
@@ -365,12 +398,22 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     if (rc != EVO_OK) return rc;
   }
   if (a->dgate_bias) {
+    EVO_REQUIRE(a->workspace && a->workspace_bytes >= attention_simt_bwd_ws(a), EVO_EARG,
+                "attention bwd: workspace too small");
     const int cols = a->H * a->D;
+    float *gpart = reinterpret_cast<float *>(reinterpret_cast<uint8_t *>(a->workspace) +
+                                             dbias_ws_bytes(a));
+    const int64_t n = a->nb * (int64_t)L;
+    const int64_t rpp = (n + GB_PARTS - 1) / GB_PARTS;
+    const int parts = (int)((n + rpp - 1) / rpp);
+    const int thr = std::min(256, ((cols + 31) / 32) * 32);
     if (a->dtype == EVO_F32)
-      gate_bias_colsum_kernel<float><<<(cols + 127) / 128, 128, 0, st>>>(*a);
+      gate_bias_part_kernel<float><<<parts, thr, 0, st>>>(*a, rpp, gpart);
     else
-      gate_bias_colsum_kernel<bf16><<<(cols + 127) / 128, 128, 0, st>>>(*a);
-    EVO_LAUNCHED("gate_bias_colsum_kernel");
+      gate_bias_part_kernel<bf16><<<parts, thr, 0, st>>>(*a, rpp, gpart);
+    EVO_LAUNCHED("gate_bias_part_kernel");
+    int rc = colsum_partials(parts, cols, gpart, a->dgate_bias, 0, st);
+    if (rc != EVO_OK) return rc;
   }
   return EVO_OK;
 }

@@ -137,26 +137,26 @@ __global__ void colsum_stage1_vec(int64_t rows, int64_t cols, const void *src, i
   }
 }
 
-// Stage 2: warp per column, lanes stride the partials, fixed shuffle tree.
-// Column sums of the [nblk, cols] partials: a 512-thread block owns 32
-// columns, lanes across columns (coalesced 128-byte rows), the 16 warps
-// take partial rows w, w+16, ... and the 16 warp sums are combined in order.
-__global__ void __launch_bounds__(512) colsum_stage2(int nblk, int64_t cols, const float *part,
-                                                     float *dst, int acc) {
-  __shared__ float red[16][33];
+// Stage 2: column sums of the [nblk, cols] partials: a 1024-thread block
+// owns 32 columns, lanes across columns (coalesced 128-byte rows), the 32
+// warps take partial rows w, w+32, ... (8 loads in flight each) and the 32
+// warp sums are combined in order.  Deterministic.
+__global__ void __launch_bounds__(1024) colsum_stage2(int nblk, int64_t cols, const float *part,
+                                                      float *dst, int acc) {
+  __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (c < cols) {
-#pragma unroll 4
-    for (int b = w; b < nblk; b += 16) s += __ldg(&part[(int64_t)b * cols + c]);
+#pragma unroll 8
+    for (int b = w; b < nblk; b += 32) s += __ldg(&part[(int64_t)b * cols + c]);
   }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < cols) {
     float t = red[0][lane];
 #pragma unroll
-    for (int j = 1; j < 16; ++j) t += red[j][lane];
+    for (int j = 1; j < 32; ++j) t += red[j][lane];
     dst[c] = acc ? dst[c] + t : t;
   }
 }
@@ -591,7 +591,7 @@ int colsum(int dt, int64_t rows, int64_t cols, const void *src, int64_t rs, floa
     else colsum_stage1<bf16><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
     EVO_LAUNCHED("colsum_stage1");
   }
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>((int)nblk, cols, ws, dst, acc);
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, ws, dst, acc);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
@@ -742,7 +742,7 @@ int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaS
 // Ordered column sums of [nblk, cols] fp32 partials (coalesced stage 2).
 int colsum_partials(int nblk, int64_t cols, const float *part, float *dst, int acc,
                     cudaStream_t st) {
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>(nblk, cols, part, dst, acc);
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(nblk, cols, part, dst, acc);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
@@ -763,7 +763,7 @@ int relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h, v
       rows, cols, reinterpret_cast<const bf16 *>(dh), reinterpret_cast<const bf16 *>(h),
       reinterpret_cast<bf16 *>(dpre), rpb, ws);
   EVO_LAUNCHED("relu_bwd_colsum_kernel");
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 512, 0, st>>>((int)nblk, cols, ws, dst, 0);
+  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, ws, dst, 0);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }

@@ -968,9 +968,9 @@ ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
 // Ordered reduction of the per-block partials: one warp per output value;
 // lane l sums partials l, l+32, ... then a fixed shuffle tree.
 // Column sums of the [nblk, nparts*cols] partials (see colsum_stage2): a
-// 512-thread block owns 32 output columns with lanes across columns
-// (coalesced), the 16 warps take partial rows w, w+16, ..., combined in order.
-__global__ void __launch_bounds__(512) ln_param_reduce_kernel(int nblk, int cols, int nparts,
+// 1024-thread block owns 32 output columns with lanes across columns
+// (coalesced), the 32 warps take partial rows w, w+32, ..., combined in order.
+__global__ void __launch_bounds__(1024) ln_param_reduce_kernel(int nblk, int cols, int nparts,
                                                               const float *__restrict__ partial,
                                                               float *__restrict__ dgamma,
                                                               float *__restrict__ dbeta,
@@ -978,21 +978,21 @@ __global__ void __launch_bounds__(512) ln_param_reduce_kernel(int nblk, int cols
                                                               int accumulate,
                                                               float *__restrict__ dWp = nullptr,
                                                               int nh = 0) {
-  __shared__ float red[16][33];
+  __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int width = nparts * cols;
   const int c = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (c < width) {
-#pragma unroll 4
-    for (int b = w; b < nblk; b += 16) s += __ldg(&partial[(int64_t)b * width + c]);
+#pragma unroll 8
+    for (int b = w; b < nblk; b += 32) s += __ldg(&partial[(int64_t)b * width + c]);
   }
   red[w][lane] = s;
   __syncthreads();
   if (w == 0 && c < width) {
     float t = red[0][lane];
 #pragma unroll
-    for (int j = 1; j < 16; ++j) t += red[j][lane];
+    for (int j = 1; j < 32; ++j) t += red[j][lane];
     const int which = c / cols, cc = c % cols;
     if (which >= 3) {
       if (which - 3 < nh) dWp[cc * nh + (which - 3)] = t;
@@ -1107,7 +1107,7 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
                                                   dxp, ws);
       EVO_LAUNCHED("ln_bwd_cf_kernel");
       if (want) {
-        ln_param_reduce_kernel<<<(2 * cols + 31) / 32, 512, 0, st>>>(nb, cols, 2, ws, dgamma,
+        ln_param_reduce_kernel<<<(2 * cols + 31) / 32, 1024, 0, st>>>(nb, cols, 2, ws, dgamma,
                                                                      dbeta, nullptr, acc);
         EVO_LAUNCHED("ln_param_reduce_kernel");
       }
@@ -1125,7 +1125,7 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
                                        reinterpret_cast<bf16 *>(dx_act), ws, nparts, st, &nb);
       if (rc != EVO_OK) return rc;
       if (want) {
-        ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(nb, cols, nparts, ws,
+        ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(nb, cols, nparts, ws,
                                                                           dgamma, dbeta,
                                                                           dx_colsum, acc);
         EVO_LAUNCHED("ln_param_reduce_kernel");
@@ -1160,7 +1160,7 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
   }
   if (want) {
     const int outs = nparts * cols;
-    ln_param_reduce_kernel<<<(outs + 31) / 32, 512, 0, st>>>(nblk, cols, nparts, ws, dgamma,
+    ln_param_reduce_kernel<<<(outs + 31) / 32, 1024, 0, st>>>(nblk, cols, nparts, ws, dgamma,
                                                              dbeta, dx_colsum, acc);
     EVO_LAUNCHED("ln_param_reduce_kernel");
   }
@@ -1242,7 +1242,7 @@ int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, 
                                      reinterpret_cast<const bf16 *>(Wp), nh, dx,
                                      reinterpret_cast<bf16 *>(dx_act), w, nparts, st, &nb);
     if (rc != EVO_OK) return rc;
-    ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
+    ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(
         nb, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
     EVO_LAUNCHED("ln_param_reduce_kernel");
     return EVO_OK;
@@ -1253,7 +1253,7 @@ int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, 
       rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
       reinterpret_cast<const bf16 *>(Wp), nh, dx, reinterpret_cast<bf16 *>(dx_act), w);
   EVO_LAUNCHED("ln_bwd_proj_kernel");
-  ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 512, 0, st>>>(
+  ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(
       nblk, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
   EVO_LAUNCHED("ln_param_reduce_kernel");
   return EVO_OK;

@@ -21,7 +21,7 @@ def rel(a, b):
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
 
 
-def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0):
+def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=False):
     torch.manual_seed(seed)
     hc = H * D
     rows = nb * L
@@ -50,7 +50,8 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0):
     dgm = torch.randn(rows, hc, device="cuda").to(dtype)
     dproj = torch.zeros(rows, 4 * hc, device="cuda", dtype=dtype)
     dbias = torch.empty(H, L * L, device="cuda") if bias is not None else None
-    K.attention(**geo, dgm=dgm, dproj=dproj, dbias=dbias)
+    dgb = torch.empty(hc, device="cuda") if gate_bias else None
+    K.attention(**geo, dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=dgb)
     torch.cuda.synchronize()
 
     # ---- torch fp32 reference on the same (rounded) inputs
@@ -98,6 +99,8 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0):
                                     indexing="ij")
         got = dbias.view(-1)[(hh * bh + qq * bq + kk * bk).cuda()]
         errs["dbias"] = rel(got, bt.grad)
+    if gate_bias:
+        errs["dgate_bias"] = rel(dgb, gather(dgpre).sum((0, 1)))
     return errs
 
 
@@ -130,4 +133,23 @@ def test_attention_tc_bf16(K, case):
 def test_attention_simt_fp32(K, case):
     errs = run_case(K, *case, dtype=torch.float32)
     bad = {k: v for k, v in errs.items() if v > 2e-6}
+    assert not bad, errs
+
+
+# keys beyond the tensor-core kernel's 256: the SIMT kernels with 512 / 1024
+# resident keys (crop r = 384 row / triangle attention, the extra-MSA column
+# attention over s_e = 1024 at c_head = 8), gate-bias sums included
+LONG = [
+    (3, 384, 2, 32, False, "plain"),
+    (2, 384, 2, 32, True, "transposed"),
+    (4, 1024, 2, 8, True, "none"),
+    (2, 700, 2, 16, False, "plain"),
+]
+
+
+@pytest.mark.parametrize("case", LONG)
+@pytest.mark.parametrize("dtype,tol", [(torch.float32, 2e-6), (torch.bfloat16, 1.5e-2)])
+def test_attention_long_keys(K, case, dtype, tol):
+    errs = run_case(K, *case, dtype=dtype, gate_bias=True)
+    bad = {k: v for k, v in errs.items() if v > tol}
     assert not bad, errs
