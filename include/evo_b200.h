@@ -198,6 +198,28 @@ EVO_API int evo_attention_fwd(const evo_attn_desc *d, void *stream);
 EVO_API int evo_attention_bwd(const evo_attn_desc *d, void *stream);
 EVO_API size_t evo_attention_bwd_workspace_bytes(const evo_attn_desc *d);
 
+/* Row work of the long-key (L > 256) bf16 attention, whose contractions run
+ * as strided-batched evo_gemm calls over chunks of batch rows (the reference
+ * op is the same _gated_attention, src/evoformer.py:268-286; softmax
+ * src/tensor.py:352-361).  S/dP: fp32 [nbc, H, L, L]; P/dS: bf16, same
+ * shape; lse: fp32 [nbc, H, L]; bias/dbias: fp32 with the (bh, bq, bk) map
+ * of evo_attn_desc; Dq: fp32 [rows, H] by activation row id
+ * row0 + b*rb + q*rl.  dbias sums the chunk's batch rows in order and, with
+ * acc, adds to the previous chunks' sum (deterministic).                */
+EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, const float *bias,
+                                  int64_t bh, int64_t bq, int64_t bk, void *P, float *lse,
+                                  void *stream);
+EVO_API int evo_attn_long_gate(int64_t rows, int hc, const float *O, const void *g, int64_t g_rs,
+                               void *o, void *gm, void *stream);
+EVO_API int evo_attn_long_prep(int64_t rows, int H, int D, const void *dgm, const void *g,
+                               int64_t g_rs, const void *o, void *dO, void *dgpre, int64_t dg_rs,
+                               float *Dq, void *stream);
+EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, const float *S, const float *dP,
+                                   const float *bias, int64_t bh, int64_t bq, int64_t bk,
+                                   const float *lse, const float *Dq, int64_t row0, int64_t rb,
+                                   int64_t rl, void *P, void *dS, float *dbias, int acc,
+                                   void *stream);
+
 /* Deterministic reduction over the leading axis:
  * dst(i, j) (+)= sum_{b<nb} src[b*n1*n2 + i*n2 + j], dst at
  * dst[i*d_s1 + j*d_s2] fp32.  src dtype_src.  Replaces the bias-gradient

@@ -69,6 +69,14 @@ _SIGS = {
     "evo_attention_bwd_workspace_bytes": (c_sz, [C.POINTER(AttnDesc)]),
     "evo_reduce_lead": (c_i32, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i32,
                                 c_vp]),
+    "evo_attn_long_softmax": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_i64, c_i64,
+                                      c_vp, c_vp, c_vp]),
+    "evo_attn_long_gate": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
+    "evo_attn_long_prep": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
+                                   c_i64, c_vp, c_vp]),
+    "evo_attn_long_dsoftmax": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i64, c_i64,
+                                       c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp,
+                                       c_vp, c_i32, c_vp]),
     "evo_colsum": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i64, c_vp, c_i32, c_vp, c_sz, c_vp]),
     "evo_colsum_workspace_bytes": (c_sz, [c_i64]),
     "evo_copy2d": (c_i32, [c_i32, c_i32, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64,

@@ -220,12 +220,90 @@ def layernorm_bwd_proj(dy, x, rows: int, mean, rstd, gamma, beta, dproj, p_rs: i
           "evo_layernorm_bwd_proj")
 
 
+# keys beyond the resident-key tensor-core attention (Lp <= 256)
+LONG_L = 256
+# fp32 logits elements per chunk of batch rows in the long-key path
+LONG_CHUNK_ELEMS = 1 << 27
+
+
+def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias=None,
+                   bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None):
+    """L > 256 on the bf16 path: S = scale*QK^T, O = PV, dP = dO V^T, dQ, dK,
+    dV as strided-batched tcgen05 GEMMs (batch = (row chunk, head)) over
+    chunks of batch rows, with the softmax / gate / dsoftmax row work in
+    csrc/attention_long.cu.  Same argument meaning as ``attention``."""
+    four = 4 * hc
+    if sb % four or sl % four or o_sb != sb // 4 or o_sl != sl // 4:
+        raise N.ContractError("attention_long: proj / o row maps must be the same row ids")
+    rb, rl = sb // four, sl // four
+    rows = nb * L
+    dev = proj.device
+    Lb = lib()
+    nbc_max = max(1, LONG_CHUNK_ELEMS // (H * L * L))
+    csz = min(nb, nbc_max)
+    S = torch.empty(csz * H * L * L, dtype=torch.float32, device=dev)
+    P = torch.empty(csz * H * L * L, dtype=torch.bfloat16, device=dev)
+    HLL = H * L * L
+    lse_f = lse.view(-1)
+
+    if dgm is None:
+        O32 = torch.empty(rows, hc, dtype=torch.float32, device=dev)
+        for b0 in range(0, nb, csz):
+            nbc = min(csz, nb - b0)
+            # S = scale * Q K^T
+            gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
+                 Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(bias), bh, bq, bk, ptr(P),
+                                           ptr(lse_f, b0 * H * L), stream()),
+                  "evo_attn_long_softmax")
+            # O[row(b,q), h*D+d] = sum_k P[b,h,q,k] V[row(b,k), 2hc + h*D + d]
+            gemm(Mat(P, L, 1, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb + 2 * hc),
+                 Mat(O32, rl * hc, 1, rb * hc, D, off=b0 * rb * hc), L, D, L, B1=nbc, B2=H)
+        check(Lb.evo_attn_long_gate(rows, hc, ptr(O32), ptr(proj, 3 * hc), four, ptr(o), ptr(gm),
+                                    stream()), "evo_attn_long_gate")
+        return
+    # backward
+    dO = torch.empty(rows, hc, dtype=torch.bfloat16, device=dev)
+    Dq = torch.empty(rows, H, dtype=torch.float32, device=dev)
+    check(Lb.evo_attn_long_prep(rows, H, D, ptr(dgm), ptr(proj, 3 * hc), four, ptr(o), ptr(dO),
+                                ptr(dproj, 3 * hc), four, ptr(Dq), stream()), "evo_attn_long_prep")
+    dP = torch.empty(csz * HLL, dtype=torch.float32, device=dev)
+    dS = torch.empty(csz * HLL, dtype=torch.bfloat16, device=dev)
+    for b0 in range(0, nb, csz):
+        nbc = min(csz, nb - b0)
+        gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
+             Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+        # dP[b,h,q,k] = sum_d dO[row(b,q), h*D+d] V[row(b,k), 2hc + h*D + d]
+        gemm(Mat(dO, rl * hc, 1, rb * hc, D, off=b0 * rb * hc),
+             Mat(proj, sl, 1, sb, D, off=b0 * sb + 2 * hc),
+             Mat(dP, L, 1, HLL, L * L), L, L, D, B1=nbc, B2=H)
+        check(Lb.evo_attn_long_dsoftmax(nbc, H, L, ptr(S), ptr(dP), ptr(bias), bh, bq, bk,
+                                        ptr(lse_f, b0 * H * L), ptr(Dq), b0 * rb, rb, rl, ptr(P),
+                                        ptr(dS), ptr(dbias), 1 if b0 > 0 else 0, stream()),
+              "evo_attn_long_dsoftmax")
+        # dV[row(b,k), 2hc+h*D+d] = sum_q P[b,h,q,k] dO[row(b,q), h*D+d]
+        gemm(Mat(P, 1, L, HLL, L * L), Mat(dO, 1, rl * hc, rb * hc, D, off=b0 * rb * hc),
+             Mat(dproj, sl, 1, sb, D, off=b0 * sb + 2 * hc), L, D, L, B1=nbc, B2=H)
+        # dQ = scale * dS K ;  dK = scale * dS^T Q
+        gemm(Mat(dS, L, 1, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb + hc),
+             Mat(dproj, sl, 1, sb, D, off=b0 * sb), L, D, L, alpha=scale, B1=nbc, B2=H)
+        gemm(Mat(dS, 1, L, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb),
+             Mat(dproj, sl, 1, sb, D, off=b0 * sb + hc), L, D, L, alpha=scale, B1=nbc, B2=H)
+    if dgate_bias is not None:
+        colsum(dproj, rows, hc, dgate_bias, rs=four, off=3 * hc)
+
+
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
               sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
               dgm=None, dproj=None, dbias=None, dgate_bias=None):
     """Fused gated attention on the packed [rows, 4*hc] projection buffer
     (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
     backward into dproj (same packing) and dbias."""
+    if L > LONG_L and proj.dtype == torch.bfloat16:
+        return attention_long(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb,
+                              sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,
+                              bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj, dbias=dbias,
+                              dgate_bias=dgate_bias)
     d = AttnDesc()
     d.dtype = dt(proj)
     d.nb, d.H, d.L, d.D, d.scale = nb, H, L, D, scale
