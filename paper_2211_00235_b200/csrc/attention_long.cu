@@ -27,7 +27,12 @@ __device__ __forceinline__ float warp_sum(float v) {
   return v;
 }
 
-// one warp per (b, h, q) logits row of S [nbc, H, L, L] fp32
+// one warp per (b, h, q) logits row of S [nbc, H, L, L] fp32; the row
+// (S + bias) stays in registers between the max, sum and normalise passes
+// (L <= 32 * MAXJ; longer rows re-read S)
+constexpr int MAXJ = 32;
+
+template <bool REG>
 __global__ void long_softmax_kernel(int64_t nrows, int H, int L, const float *__restrict__ S,
                                     const float *__restrict__ bias, int64_t bh, int64_t bq,
                                     int64_t bk, bf16 *__restrict__ P, float *__restrict__ lse) {
@@ -38,16 +43,38 @@ __global__ void long_softmax_kernel(int64_t nrows, int H, int L, const float *__
   const int h = (int)((row / L) % H);
   const float *s = S + row * L;
   const float *bb = bias ? bias + h * bh + q * bq : nullptr;
-  float mx = -INFINITY;
-  for (int k = lane; k < L; k += 32) mx = fmaxf(mx, s[k] + (bb ? bb[k * bk] : 0.f));
-  mx = warp_max(mx);
-  float sum = 0.f;
-  for (int k = lane; k < L; k += 32) sum += __expf(s[k] + (bb ? bb[k * bk] : 0.f) - mx);
-  sum = warp_sum(sum);
-  const float inv = 1.f / sum;
   bf16 *p = P + row * L;
-  for (int k = lane; k < L; k += 32)
-    p[k] = __float2bfloat16(__expf(s[k] + (bb ? bb[k * bk] : 0.f) - mx) * inv);
+  float mx = -INFINITY, sum = 0.f;
+  if constexpr (REG) {
+    float v[MAXJ];
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int k = j * 32 + lane;
+      v[j] = k < L ? s[k] + (bb ? bb[k * bk] : 0.f) : -INFINITY;
+      mx = fmaxf(mx, v[j]);
+    }
+    mx = warp_max(mx);
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      v[j] = __expf(v[j] - mx);
+      sum += v[j];
+    }
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+#pragma unroll
+    for (int j = 0; j < MAXJ; ++j) {
+      const int k = j * 32 + lane;
+      if (k < L) p[k] = __float2bfloat16(v[j] * inv);
+    }
+  } else {
+    for (int k = lane; k < L; k += 32) mx = fmaxf(mx, s[k] + (bb ? bb[k * bk] : 0.f));
+    mx = warp_max(mx);
+    for (int k = lane; k < L; k += 32) sum += __expf(s[k] + (bb ? bb[k * bk] : 0.f) - mx);
+    sum = warp_sum(sum);
+    const float inv = 1.f / sum;
+    for (int k = lane; k < L; k += 32)
+      p[k] = __float2bfloat16(__expf(s[k] + (bb ? bb[k * bk] : 0.f) - mx) * inv);
+  }
   if (lane == 0) lse[row] = mx + logf(sum);
 }
 
@@ -93,7 +120,8 @@ __global__ void long_prep_kernel(int64_t rows, int H, int D, const bf16 *__restr
   if (lane == 0) Dq[r * H + h] = acc;
 }
 
-// warp per (h, q) row, lanes over keys, batch rows of the chunk in order
+// thread per (h, q, k) (consecutive threads along k: coalesced), batch rows
+// of the chunk in order
 __global__ void long_dsoftmax_kernel(int nbc, int H, int L, const float *__restrict__ S,
                                      const float *__restrict__ dP,
                                      const float *__restrict__ bias, int64_t bh, int64_t bq,
@@ -101,25 +129,26 @@ __global__ void long_dsoftmax_kernel(int nbc, int H, int L, const float *__restr
                                      const float *__restrict__ Dq, int64_t row0, int64_t rb,
                                      int64_t rl, bf16 *__restrict__ P, bf16 *__restrict__ dS,
                                      float *__restrict__ dbias, int acc) {
-  const int lane = threadIdx.x & 31;
-  const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (w >= (int64_t)H * L) return;
-  const int h = (int)(w / L), q = (int)(w - (int64_t)h * L);
-  const float *bb = bias ? bias + h * bh + q * bq : nullptr;
-  float *db = dbias ? dbias + h * bh + q * bq : nullptr;
-  for (int k = lane; k < L; k += 32) {
-    const float bv = bb ? bb[k * bk] : 0.f;
-    float sum = 0.f;
-    for (int b = 0; b < nbc; ++b) {
-      const int64_t lrow = ((int64_t)b * H + h) * L + q;   // logits row in the chunk
-      const int64_t arow = row0 + b * rb + q * rl;         // activation row id
-      const float p = __expf(S[lrow * L + k] + bv - lse[lrow]);
-      const float ds = p * (dP[lrow * L + k] - Dq[arow * H + h]);
-      P[lrow * L + k] = __float2bfloat16(p);
-      dS[lrow * L + k] = __float2bfloat16(ds);
-      sum += ds;
-    }
-    if (db) db[k * bk] = acc ? db[k * bk] + sum : sum;
+  const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+  const int64_t LL = (int64_t)L * L;
+  if (e >= H * LL) return;
+  const int h = (int)(e / LL);
+  const int q = (int)((e / L) % L), k = (int)(e % L);
+  const float bv = bias ? bias[h * bh + q * bq + k * bk] : 0.f;
+  float sum = 0.f;
+#pragma unroll 4
+  for (int b = 0; b < nbc; ++b) {
+    const int64_t lrow = ((int64_t)b * H + h) * L + q;   // logits row in the chunk
+    const int64_t arow = row0 + b * rb + q * rl;         // activation row id
+    const float p = __expf(S[lrow * L + k] + bv - lse[lrow]);
+    const float ds = p * (dP[lrow * L + k] - Dq[arow * H + h]);
+    P[lrow * L + k] = __float2bfloat16(p);
+    dS[lrow * L + k] = __float2bfloat16(ds);
+    sum += ds;
+  }
+  if (dbias) {
+    float *db = dbias + h * bh + q * bq + k * bk;
+    *db = acc ? *db + sum : sum;
   }
 }
 
@@ -139,8 +168,12 @@ EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, con
               "attn_long_softmax: bad arguments");
   const int64_t rows = nbc * H * L;
   if (rows == 0) return EVO_OK;
-  long_softmax_kernel<<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(
-      rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse);
+  if (L <= 32 * MAXJ)
+    long_softmax_kernel<true><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+        rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse);
+  else
+    long_softmax_kernel<false><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(
+        rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse);
   EVO_LAUNCHED("long_softmax_kernel");
   return EVO_OK;
 }
@@ -181,7 +214,8 @@ EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, const float *S, const 
   EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && S && dP && lse && Dq && P && dS, EVO_EARG,
               "attn_long_dsoftmax: bad arguments");
   if (nbc == 0) return EVO_OK;
-  long_dsoftmax_kernel<<<warps_grid((int64_t)H * L, 8), 256, 0, (cudaStream_t)stream>>>(
+  const int64_t n = (int64_t)H * L * L;
+  long_dsoftmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
       nbc, H, L, S, dP, bias, bh, bq, bk, lse, Dq, row0, rb, rl, reinterpret_cast<bf16 *>(P),
       reinterpret_cast<bf16 *>(dS), dbias, acc);
   EVO_LAUNCHED("long_dsoftmax_kernel");

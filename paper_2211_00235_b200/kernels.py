@@ -246,6 +246,16 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
     HLL = H * L * L
     lse_f = lse.view(-1)
 
+    # the softmax reads the bias once per batch row: give it a plain
+    # [H, L, L] copy when the bias is transposed (triangle end), so those
+    # reads are coalesced
+    sbias, sbh, sbq, sbk = bias, bh, bq, bk
+    if bias is not None and bk != 1:
+        sbias = torch.empty(H * L * L, dtype=torch.float32, device=dev)
+        for hh in range(H):
+            copy2d(bias, L, L, sbias, s_rs=bq, s_cs=bk, d_rs=L, s_off=hh * bh,
+                   d_off=hh * L * L)
+        sbh, sbq, sbk = L * L, L, 1
     if dgm is None:
         O32 = torch.empty(rows, hc, dtype=torch.float32, device=dev)
         for b0 in range(0, nb, csz):
@@ -253,7 +263,7 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
             # S = scale * Q K^T
             gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
                  Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
-            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(bias), bh, bq, bk, ptr(P),
+            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(sbias), sbh, sbq, sbk, ptr(P),
                                            ptr(lse_f, b0 * H * L), stream()),
                   "evo_attn_long_softmax")
             # O[row(b,q), h*D+d] = sum_k P[b,h,q,k] V[row(b,k), 2hc + h*D + d]
