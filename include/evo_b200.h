@@ -205,7 +205,9 @@ EVO_API size_t evo_attention_bwd_workspace_bytes(const evo_attn_desc *d);
  * shape; lse: fp32 [nbc, H, L]; bias/dbias: fp32 with the (bh, bq, bk) map
  * of evo_attn_desc; Dq: fp32 [rows, H] by activation row id
  * row0 + b*rb + q*rl.  dbias sums the chunk's batch rows in order and, with
- * acc, adds to the previous chunks' sum (deterministic).                */
+ * acc, adds to the previous chunks' sum (deterministic).  dsoftmax with
+ * S == NULL takes P as an input (the forward's probabilities) instead of
+ * recomputing it from S, bias and lse.                                  */
 EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, const float *bias,
                                   int64_t bh, int64_t bq, int64_t bk, void *P, float *lse,
                                   void *stream);

@@ -134,15 +134,20 @@ __global__ void long_dsoftmax_kernel(int nbc, int H, int L, const float *__restr
   if (e >= H * LL) return;
   const int h = (int)(e / LL);
   const int q = (int)((e / L) % L), k = (int)(e % L);
-  const float bv = bias ? bias[h * bh + q * bq + k * bk] : 0.f;
+  const float bv = (S && bias) ? bias[h * bh + q * bq + k * bk] : 0.f;
   float sum = 0.f;
 #pragma unroll 4
   for (int b = 0; b < nbc; ++b) {
     const int64_t lrow = ((int64_t)b * H + h) * L + q;   // logits row in the chunk
     const int64_t arow = row0 + b * rb + q * rl;         // activation row id
-    const float p = __expf(S[lrow * L + k] + bv - lse[lrow]);
+    float p;
+    if (S) {  // recompute P from the logits and lse
+      p = __expf(S[lrow * L + k] + bv - lse[lrow]);
+      P[lrow * L + k] = __float2bfloat16(p);
+    } else {  // the forward's P
+      p = __bfloat162float(P[lrow * L + k]);
+    }
     const float ds = p * (dP[lrow * L + k] - Dq[arow * H + h]);
-    P[lrow * L + k] = __float2bfloat16(p);
     dS[lrow * L + k] = __float2bfloat16(ds);
     sum += ds;
   }
@@ -211,7 +216,7 @@ EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, const float *S, const 
                                    const float *lse, const float *Dq, int64_t row0, int64_t rb,
                                    int64_t rl, void *P, void *dS, float *dbias, int acc,
                                    void *stream) {
-  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && S && dP && lse && Dq && P && dS, EVO_EARG,
+  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && dP && Dq && P && dS && (!S || lse), EVO_EARG,
               "attn_long_dsoftmax: bad arguments");
   if (nbc == 0) return EVO_OK;
   const int64_t n = (int64_t)H * L * L;

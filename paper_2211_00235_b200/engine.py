@@ -288,9 +288,14 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     gm = _empty((rows, hc), act, dev)
     lse = _empty((nb, h, L), F32, dev)
     bq, bk = (cfg.r, 1) if name != "tri_attn_end" else (1, cfg.r)
+    # long-key path (L > 256, bf16): keep the forward's probabilities for the
+    # backward instead of recomputing the logits
+    p_store = (_empty(K.long_p_elems(nb, h, L), act, dev)
+               if L > K.LONG_L and act == torch.bfloat16 else None)
     K.attention(proj=proj, hc=hc, nb=nb, H=h, L=L, D=ch, scale=ch ** -0.5,
                 sb=rb * 4 * hc, sl=rl * 4 * hc, o=o, gm=gm, o_sb=rb * hc, o_sl=rl * hc,
-                lse=lse, bias=bias, bh=r2, bq=bq, bk=bk)
+                lse=lse, bias=bias, bh=r2, bq=bq, bk=bk, p_store=p_store)
+    ctx["p_store"] = p_store
     x_new = _empty(x.shape, F32, dev)
     K.linear(gm, rows, hc, pk["Wo"], c_io, c_io, x_new, c_io, bias=P[f"{px}.out_b"],
              residual=x if resid else None)
@@ -325,7 +330,8 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
     K.attention(proj=ctx["proj"], hc=hc, nb=nb, H=h, L=L, D=ch, scale=ch ** -0.5,
                 sb=rb * 4 * hc, sl=rl * 4 * hc, o=ctx["o"], gm=ctx["gm"], o_sb=rb * hc,
                 o_sl=rl * hc, lse=ctx["lse"], bias=ctx.get("bias"), bh=r2, bq=bq, bk=bk,
-                dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=G["gate_b"])
+                dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=G["gate_b"],
+                p_store=ctx.get("p_store"))
     xh = ctx["xh"]
     K.linear_dw(xh, rows, c_io, dproj, 4 * hc, G["Wqkvg"], 4 * hc)
     dxh = _empty((rows, c_io), F32, dev)

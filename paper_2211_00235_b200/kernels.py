@@ -226,12 +226,21 @@ LONG_L = 256
 LONG_CHUNK_ELEMS = 1 << 27
 
 
+def long_p_elems(nb, H, L):
+    """bf16 elements of the forward probabilities kept for the backward."""
+    return nb * H * L * L
+
+
 def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias=None,
-                   bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None):
+                   bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None,
+                   p_store=None):
     """L > 256 on the bf16 path: S = scale*QK^T, O = PV, dP = dO V^T, dQ, dK,
     dV as strided-batched tcgen05 GEMMs (batch = (row chunk, head)) over
     chunks of batch rows, with the softmax / gate / dsoftmax row work in
-    csrc/attention_long.cu.  Same argument meaning as ``attention``."""
+    csrc/attention_long.cu.  Same argument meaning as ``attention``.
+    p_store (bf16, long_p_elems): the forward writes P there and the
+    backward reads it (no QK^T recompute); without it the backward
+    recomputes P from the logits and lse."""
     four = 4 * hc
     if sb % four or sl % four or o_sb != sb // 4 or o_sl != sl // 4:
         raise N.ContractError("attention_long: proj / o row maps must be the same row ids")
@@ -241,8 +250,12 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
     Lb = lib()
     nbc_max = max(1, LONG_CHUNK_ELEMS // (H * L * L))
     csz = min(nb, nbc_max)
-    S = torch.empty(csz * H * L * L, dtype=torch.float32, device=dev)
-    P = torch.empty(csz * H * L * L, dtype=torch.bfloat16, device=dev)
+    if p_store is not None and p_store.numel() < long_p_elems(nb, H, L):
+        raise N.ContractError("attention_long: p_store too small")
+    S = (torch.empty(csz * H * L * L, dtype=torch.float32, device=dev)
+         if dgm is None or p_store is None else None)
+    P = (torch.empty(csz * H * L * L, dtype=torch.bfloat16, device=dev)
+         if p_store is None else None)
     HLL = H * L * L
     lse_f = lse.view(-1)
 
@@ -263,11 +276,12 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
             # S = scale * Q K^T
             gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
                  Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
-            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(sbias), sbh, sbq, sbk, ptr(P),
-                                           ptr(lse_f, b0 * H * L), stream()),
+            Pc, poff = (P, 0) if p_store is None else (p_store, b0 * HLL)
+            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(sbias), sbh, sbq, sbk,
+                                           ptr(Pc, poff), ptr(lse_f, b0 * H * L), stream()),
                   "evo_attn_long_softmax")
             # O[row(b,q), h*D+d] = sum_k P[b,h,q,k] V[row(b,k), 2hc + h*D + d]
-            gemm(Mat(P, L, 1, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb + 2 * hc),
+            gemm(Mat(Pc, L, 1, HLL, L * L, off=poff), Mat(proj, 1, sl, sb, D, off=b0 * sb + 2 * hc),
                  Mat(O32, rl * hc, 1, rb * hc, D, off=b0 * rb * hc), L, D, L, B1=nbc, B2=H)
         check(Lb.evo_attn_long_gate(rows, hc, ptr(O32), ptr(proj, 3 * hc), four, ptr(o), ptr(gm),
                                     stream()), "evo_attn_long_gate")
@@ -281,18 +295,23 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
     dS = torch.empty(csz * HLL, dtype=torch.bfloat16, device=dev)
     for b0 in range(0, nb, csz):
         nbc = min(csz, nb - b0)
-        gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
-             Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+        if p_store is None:
+            gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
+                 Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+            Pc, poff, Sp = P, 0, ptr(S)
+        else:
+            Pc, poff, Sp = p_store, b0 * HLL, None
         # dP[b,h,q,k] = sum_d dO[row(b,q), h*D+d] V[row(b,k), 2hc + h*D + d]
         gemm(Mat(dO, rl * hc, 1, rb * hc, D, off=b0 * rb * hc),
              Mat(proj, sl, 1, sb, D, off=b0 * sb + 2 * hc),
              Mat(dP, L, 1, HLL, L * L), L, L, D, B1=nbc, B2=H)
-        check(Lb.evo_attn_long_dsoftmax(nbc, H, L, ptr(S), ptr(dP), ptr(bias), bh, bq, bk,
-                                        ptr(lse_f, b0 * H * L), ptr(Dq), b0 * rb, rb, rl, ptr(P),
-                                        ptr(dS), ptr(dbias), 1 if b0 > 0 else 0, stream()),
+        check(Lb.evo_attn_long_dsoftmax(nbc, H, L, Sp, ptr(dP), ptr(bias), bh, bq, bk,
+                                        ptr(lse_f, b0 * H * L), ptr(Dq), b0 * rb, rb, rl,
+                                        ptr(Pc, poff), ptr(dS), ptr(dbias), 1 if b0 > 0 else 0,
+                                        stream()),
               "evo_attn_long_dsoftmax")
         # dV[row(b,k), 2hc+h*D+d] = sum_q P[b,h,q,k] dO[row(b,q), h*D+d]
-        gemm(Mat(P, 1, L, HLL, L * L), Mat(dO, 1, rl * hc, rb * hc, D, off=b0 * rb * hc),
+        gemm(Mat(Pc, 1, L, HLL, L * L, off=poff), Mat(dO, 1, rl * hc, rb * hc, D, off=b0 * rb * hc),
              Mat(dproj, sl, 1, sb, D, off=b0 * sb + 2 * hc), L, D, L, B1=nbc, B2=H)
         # dQ = scale * dS K ;  dK = scale * dS^T Q
         gemm(Mat(dS, L, 1, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb + hc),
@@ -305,7 +324,7 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
 
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
               sl: int, o, gm, o_sb: int, o_sl: int, lse, bias=None, bh=0, bq=0, bk=0,
-              dgm=None, dproj=None, dbias=None, dgate_bias=None):
+              dgm=None, dproj=None, dbias=None, dgate_bias=None, p_store=None):
     """Fused gated attention on the packed [rows, 4*hc] projection buffer
     (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
     backward into dproj (same packing) and dbias."""
@@ -313,7 +332,7 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
         return attention_long(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb,
                               sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,
                               bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj, dbias=dbias,
-                              dgate_bias=dgate_bias)
+                              dgate_bias=dgate_bias, p_store=p_store)
     d = AttnDesc()
     d.dtype = dt(proj)
     d.nb, d.H, d.L, d.D, d.scale = nb, H, L, D, scale

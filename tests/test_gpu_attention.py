@@ -21,7 +21,8 @@ def rel(a, b):
     return float((a - b).norm() / b.norm().clamp_min(1e-30))
 
 
-def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=False):
+def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=False,
+             keep_p=False):
     torch.manual_seed(seed)
     hc = H * D
     rows = nb * L
@@ -46,6 +47,8 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=Fals
     geo = dict(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb * 4 * hc,
                sl=sl * 4 * hc, o=o, gm=gm, o_sb=sb * hc, o_sl=sl * hc, lse=lse, bias=bias,
                bh=bh, bq=bq, bk=bk)
+    if keep_p:
+        geo["p_store"] = torch.empty(K.long_p_elems(nb, H, L), device="cuda", dtype=dtype)
     K.attention(**geo)
     dgm = torch.randn(rows, hc, device="cuda").to(dtype)
     dproj = torch.zeros(rows, 4 * hc, device="cuda", dtype=dtype)
@@ -152,4 +155,12 @@ LONG = [
 def test_attention_long_keys(K, case, dtype, tol):
     errs = run_case(K, *case, dtype=dtype, gate_bias=True)
     bad = {k: v for k, v in errs.items() if v > tol}
+    assert not bad, errs
+
+
+@pytest.mark.parametrize("case", LONG)
+def test_attention_long_keys_forward_p_kept(K, case):
+    """The engine's long-key path: the forward keeps P for the backward."""
+    errs = run_case(K, *case, dtype=torch.bfloat16, gate_bias=True, keep_p=True)
+    bad = {k: v for k, v in errs.items() if v > 1.5e-2}
     assert not bad, errs
