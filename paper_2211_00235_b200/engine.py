@@ -288,10 +288,9 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     gm = _empty((rows, hc), act, dev)
     lse = _empty((nb, h, L), F32, dev)
     bq, bk = (cfg.r, 1) if name != "tri_attn_end" else (1, cfg.r)
-    # long-key path (L > 256, bf16): keep the forward's probabilities for the
-    # backward instead of recomputing the logits
-    p_store = (_empty(K.long_p_elems(nb, h, L), act, dev)
-               if L > K.LONG_L and act == torch.bfloat16 else None)
+    # GEMM-composed path (bf16, L > 256 or c_head not 16 / 32): keep the
+    # forward's probabilities for the backward instead of recomputing them
+    p_store = _empty(K.long_p_elems(nb, h, L), act, dev) if K.use_long(act, L, ch) else None
     K.attention(proj=proj, hc=hc, nb=nb, H=h, L=L, D=ch, scale=ch ** -0.5,
                 sb=rb * 4 * hc, sl=rl * 4 * hc, o=o, gm=gm, o_sb=rb * hc, o_sl=rl * hc,
                 lse=lse, bias=bias, bh=r2, bq=bq, bk=bk, p_store=p_store)

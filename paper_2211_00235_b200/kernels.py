@@ -226,6 +226,13 @@ LONG_L = 256
 LONG_CHUNK_ELEMS = 1 << 27
 
 
+def use_long(dtype, L: int, D: int) -> bool:
+    """bf16 shapes the fused tcgen05 attention does not take (L > 256 keys,
+    or head dims other than 16 / 32: the extra-MSA stack's c_head = 8) run
+    on the GEMM-composed path instead of the SIMT kernels."""
+    return dtype == torch.bfloat16 and (L > LONG_L or D not in (16, 32))
+
+
 def long_p_elems(nb, H, L):
     """bf16 elements of the forward probabilities kept for the backward."""
     return nb * H * L * L
@@ -328,7 +335,7 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
     """Fused gated attention on the packed [rows, 4*hc] projection buffer
     (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
     backward into dproj (same packing) and dbias."""
-    if L > LONG_L and proj.dtype == torch.bfloat16:
+    if use_long(proj.dtype, L, D):
         return attention_long(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb,
                               sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,
                               bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj, dbias=dbias,
