@@ -32,7 +32,7 @@ __device__ __forceinline__ float warp_sum(float v) {
 // (L <= 32 * MAXJ; longer rows re-read S)
 constexpr int MAXJ = 32;
 
-template <bool REG>
+template <int NJ>  // NJ > 0: row in NJ registers per lane (L <= 32 * NJ)
 __global__ void long_softmax_kernel(int64_t nrows, int H, int L, const float *__restrict__ S,
                                     const float *__restrict__ bias, int64_t bh, int64_t bq,
                                     int64_t bk, bf16 *__restrict__ P, float *__restrict__ lse) {
@@ -45,24 +45,24 @@ __global__ void long_softmax_kernel(int64_t nrows, int H, int L, const float *__
   const float *bb = bias ? bias + h * bh + q * bq : nullptr;
   bf16 *p = P + row * L;
   float mx = -INFINITY, sum = 0.f;
-  if constexpr (REG) {
-    float v[MAXJ];
+  if constexpr (NJ > 0) {
+    float v[NJ];
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int k = j * 32 + lane;
       v[j] = k < L ? s[k] + (bb ? bb[k * bk] : 0.f) : -INFINITY;
       mx = fmaxf(mx, v[j]);
     }
     mx = warp_max(mx);
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       v[j] = __expf(v[j] - mx);
       sum += v[j];
     }
     sum = warp_sum(sum);
     const float inv = 1.f / sum;
 #pragma unroll
-    for (int j = 0; j < MAXJ; ++j) {
+    for (int j = 0; j < NJ; ++j) {
       const int k = j * 32 + lane;
       if (k < L) p[k] = __float2bfloat16(v[j] * inv);
     }
@@ -173,12 +173,14 @@ EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, con
               "attn_long_softmax: bad arguments");
   const int64_t rows = nbc * H * L;
   if (rows == 0) return EVO_OK;
-  if (L <= 32 * MAXJ)
-    long_softmax_kernel<true><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(
-        rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse);
-  else
-    long_softmax_kernel<false><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(
-        rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse);
+#define EVO_LONG_SOFTMAX(NJ)                                                            \
+  long_softmax_kernel<NJ><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(        \
+      rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse)
+  if (L <= 256) EVO_LONG_SOFTMAX(8);
+  else if (L <= 512) EVO_LONG_SOFTMAX(16);
+  else if (L <= 32 * MAXJ) EVO_LONG_SOFTMAX(32);
+  else EVO_LONG_SOFTMAX(0);
+#undef EVO_LONG_SOFTMAX
   EVO_LAUNCHED("long_softmax_kernel");
   return EVO_OK;
 }
