@@ -140,18 +140,10 @@ EVO_API int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const floa
                                  float *dx_colsum, void *workspace, size_t workspace_bytes,
                                  void *stream);
 
-/* LayerNorm forward of a contiguous fp32 [rows, 128] input (c_z rows) with
- * the pair-bias projection of the attention sub-ops fused in
- * (src/evoformer.py:279, bias = LN(z) Wb):
- *   y (bf16, may be NULL) = LN(x);  mean/rstd as evo_layernorm_fwd;
- *   proj[hh*p_rs + row] = sum_c bf16(y[row,c]) * Wp[c*nh + hh]   (fp32)
- * Wp: bf16 [128][nh], nh <= 8.                                          */
-EVO_API int evo_layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
-                                   const float *beta, void *y, float *mean, float *rstd,
-                                   float eps, const void *Wp, int nh, float *proj,
-                                   int64_t p_rs, void *stream);
-
-/* Its backward, fused with the projection's backward:
+/* LayerNorm backward of a contiguous fp32 [rows, 128] input (c_z rows)
+ * fused with the backward of the attention pair-bias projection that
+ * consumed LN(x) (src/evoformer.py:279, bias = LN(z) Wb; Wp bf16 [128][nh],
+ * nh <= 8):
  *   dy_tot = dy (fp32 [rows,128], may be NULL = 0) + sum_hh dproj[hh*p_rs+row] Wp[c*nh+hh]
  *   dx = LN_bwd(dy_tot) + dres;  dx_act / dx_colsum as evo_layernorm_bwd_ex;
  *   dgamma, dbeta, and dWp[c*nh + hh] = sum_rows bf16(LN(x))[row,c] * dproj[hh,row]
@@ -201,22 +193,24 @@ EVO_API size_t evo_attention_bwd_workspace_bytes(const evo_attn_desc *d);
 /* Row work of the long-key (L > 256) bf16 attention, whose contractions run
  * as strided-batched evo_gemm calls over chunks of batch rows (the reference
  * op is the same _gated_attention, src/evoformer.py:268-286; softmax
- * src/tensor.py:352-361).  S/dP: fp32 [nbc, H, L, L]; P/dS: bf16, same
- * shape; lse: fp32 [nbc, H, L]; bias/dbias: fp32 with the (bh, bq, bk) map
+ * src/tensor.py:352-361).  S/dP: fp32 [nbc, H, L, ld] (ld >= L, the row
+ * stride: L rounded up to 8 so the GEMM operand rows stay 16-byte aligned);
+ * P/dS: bf16, same shape; lse: fp32 [nbc, H, L]; bias/dbias: fp32 with the (bh, bq, bk) map
  * of evo_attn_desc; Dq: fp32 [rows, H] by activation row id
  * row0 + b*rb + q*rl.  dbias sums the chunk's batch rows in order and, with
  * acc, adds to the previous chunks' sum (deterministic).  dsoftmax with
  * S == NULL takes P as an input (the forward's probabilities) instead of
  * recomputing it from S, bias and lse.                                  */
-EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, const float *bias,
-                                  int64_t bh, int64_t bq, int64_t bk, void *P, float *lse,
-                                  void *stream);
+EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, int64_t ld, const float *S,
+                                  const float *bias, int64_t bh, int64_t bq, int64_t bk, void *P,
+                                  float *lse, void *stream);
 EVO_API int evo_attn_long_gate(int64_t rows, int hc, const float *O, const void *g, int64_t g_rs,
                                void *o, void *gm, void *stream);
 EVO_API int evo_attn_long_prep(int64_t rows, int H, int D, const void *dgm, const void *g,
                                int64_t g_rs, const void *o, void *dO, void *dgpre, int64_t dg_rs,
                                float *Dq, void *stream);
-EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, const float *S, const float *dP,
+EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, int64_t ld, const float *S,
+                                   const float *dP,
                                    const float *bias, int64_t bh, int64_t bq, int64_t bk,
                                    const float *lse, const float *Dq, int64_t row0, int64_t rb,
                                    int64_t rl, void *P, void *dS, float *dbias, int acc,
@@ -250,14 +244,6 @@ EVO_API int evo_mul2d(int dtype_a, int dtype_b, int dtype_out, int64_t rows,
               int64_t cols, const void *a, int64_t a_rs, const void *b,
               int64_t b_rs, void *out, int64_t o_rs, void *stream);
 
-/* Attention-gate backward (sigmoid gate before the out-projection,
- * src/evoformer.py:285-286 and src/tensor.py:247-269):
- *   dO = dgm * g ;  dgpre = dgm * o * g * (1 - g)                     */
-EVO_API int evo_gate_bwd(int dtype, int64_t rows, int64_t cols, const void *dgm,
-                 int64_t dgm_rs, const void *g, int64_t g_rs, const void *o,
-                 int64_t o_rs, void *dO, int64_t dO_rs, void *dgpre,
-                 int64_t dgpre_rs, void *stream);
-
 /* Triangle-multiplication gating (src/evoformer.py:370-375).
  * proj rows (i,k) [r*r, ldp]: cols [0,c)=a value, [c,2c)=b value,
  * [2c,3c)=sigmoid(a gate), [3c,4c)=sigmoid(b gate).
@@ -265,10 +251,15 @@ EVO_API int evo_gate_bwd(int dtype, int64_t rows, int64_t cols, const void *dgm,
 EVO_API int evo_trimul_gate_fwd(int dtype, int64_t rows, int c, const void *proj,
                         int64_t ldp, void *a_cf, void *b_cf, void *stream);
 /* bwd: from da_cf/db_cf (fp32, channel-first) write dproj[:, 0:4c]
- * (dvalue = d*g, dgate_pre = d*value*g*(1-g)).                          */
+ * (dvalue = d*g, dgate_pre = d*value*g*(1-g)).  colsum (fp32 [4c], may be
+ * NULL): the column sums of those fp32 values before rounding to dtype (the
+ * a_b | b_b | a_gate_b | b_gate_b gradients, deterministic order); needs
+ * evo_trimul_gate_bwd_workspace_bytes of workspace.                     */
+EVO_API size_t evo_trimul_gate_bwd_workspace_bytes(int64_t rows, int c);
 EVO_API int evo_trimul_gate_bwd(int dtype, int64_t rows, int c, const void *proj,
                         int64_t ldp, const float *da_cf, const float *db_cf,
-                        void *dproj, int64_t ldd, void *stream);
+                        void *dproj, int64_t ldd, float *colsum, void *workspace,
+                        size_t workspace_bytes, void *stream);
 
 /* Output gate of the triangle multiplication (src/evoformer.py:394-396):
  * fwd: znew = z + g*o ;  bwd: do = dz*g, dgpre = dz*o*g*(1-g).
@@ -276,10 +267,15 @@ EVO_API int evo_trimul_gate_bwd(int dtype, int64_t rows, int c, const void *proj
 EVO_API int evo_outgate_fwd(int dtype, int64_t rows, int64_t cols, const float *z,
                     const void *g, int64_t g_rs, const void *o, int64_t o_rs,
                     float *znew, void *stream);
+/* do_colsum / dg_colsum (fp32 [cols], both or neither; bf16, cols % 8 == 0):
+ * column sums of do and dgpre from the fp32 values (the out_b and out_gate_b
+ * gradients); workspace evo_outgate_bwd_workspace_bytes.                 */
+EVO_API size_t evo_outgate_bwd_workspace_bytes(int64_t rows, int64_t cols);
 EVO_API int evo_outgate_bwd(int dtype, int64_t rows, int64_t cols, const float *dz,
                     const void *g, int64_t g_rs, const void *o, int64_t o_rs,
                     void *do_, int64_t do_rs, void *dgpre, int64_t dg_rs,
-                    void *stream);
+                    float *do_colsum, float *dg_colsum, void *workspace,
+                    size_t workspace_bytes, void *stream);
 
 /* ReLU backward (src/tensor.py:274-280): dpre = dh * (pre > 0); `h` is
  * relu(pre) so h > 0 iff pre > 0.  Contiguous [n].                      */
@@ -306,15 +302,40 @@ EVO_API int evo_sq_mean(int64_t n, const float *x, float *out, float *dx,
 EVO_API int evo_add(int64_t n, const float *a, const float *b, float *out,
             void *stream);
 
+/* Split an fp32 [rows, cols] operand into bf16 hi = bf16(x) and
+ * lo = bf16(x - hi) (hi also to hi2 when non-NULL), element strides per row.
+ * Used for the 3-product bf16 GEMM (A3 = [hi | lo | hi], W3 = [W_hi; W_hi;
+ * W_lo], K tripled) that gives the transitions' first projection fp32-grade
+ * pre-activations, so the ReLU mask (src/tensor.py:274-280) matches the
+ * reference's (src/evoformer.py:314-319).                                 */
+EVO_API int evo_split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *hi,
+                           int64_t h_rs, void *lo, int64_t l_rs, void *hi2, int64_t h2_rs,
+                           void *stream);
+
 /* Library identity / diagnostics. */
 EVO_API const char *evo_last_error(void);
 EVO_API int evo_version(void);
 /* Number of kernels this library has launched (all threads). */
 EVO_API int64_t evo_launch_count(void);
-/* 1 if the tcgen05 GEMM path is compiled in and enabled. */
+/* 1 if the tcgen05 GEMM path is compiled in (the TMA encoder resolved). */
 EVO_API int evo_tc_available(void);
-/* 0 = auto (default), 1 = force SIMT for every GEMM (debug/parity). */
-EVO_API void evo_set_gemm_policy(int policy);
+/* Backend accounting: number of evo_gemm / evo_attention_* calls served by
+ * each engine since load (EVO_BK_* below), and the engine of the last call
+ * on this thread.  Tests assert the tensor-core path actually ran.        */
+#define EVO_BK_GEMM_TC 0
+#define EVO_BK_GEMM_SIMT 1
+#define EVO_BK_GEMM_SKINNY 2
+#define EVO_BK_ATTN_TC 3
+#define EVO_BK_ATTN_SIMT 4
+#define EVO_BK_COUNT 5
+EVO_API int64_t evo_backend_count(int backend);
+EVO_API int evo_last_backend(void);
+/* Strict tensor-core mode (default ON): a bf16 evo_gemm / evo_attention_*
+ * call the tensor-core kernels do not take fails with EVO_EUNSUP instead of
+ * running the SIMT kernels (the fp32 parity path is SIMT by design and is
+ * unaffected).  0 = allow the SIMT fallback for bf16 (small test shapes). */
+EVO_API void evo_set_strict_tc(int on);
+EVO_API int evo_get_strict_tc(void);
 
 #ifdef __cplusplus
 }

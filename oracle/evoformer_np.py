@@ -190,7 +190,7 @@ def lin_vjp(dy, x, w, with_bias=True):
     dx = np.matmul(dy, w.T)
     x2 = x.reshape(-1, d_in)
     g2 = dy.reshape(-1, d_out)
-    dw = x2.T @ g2
+    dw = np.matmul(x2.T, g2)
     db = g2.sum(axis=0) if with_bias else None
     return dx, dw, db
 
@@ -345,7 +345,7 @@ def opm_fwd(P, px, m, d):
     a = lin(mh, P[f"{px}.a_w"], P[f"{px}.a_b"])
     b = lin(mh, P[f"{px}.b_w"], P[f"{px}.b_b"])
     # raw[(i,p),(j,q)] = sum_s a[s,(i,p)] b[s,(j,q)]  (a BLAS matmul, :343-347)
-    raw = a.reshape(s, r * c).T @ b.reshape(s, r * c)
+    raw = np.matmul(a.reshape(s, r * c).T, b.reshape(s, r * c))
     o = raw.reshape(r, c, r, c).transpose(0, 2, 1, 3).reshape(r, r, c * c)
     os_ = o * (1.0 / s)
     out = lin(os_, P[f"{px}.out_w"], P[f"{px}.out_b"])
@@ -360,8 +360,8 @@ def opm_vjp(dout, cache, P, px, d, G):
     do = (dos * (1.0 / s)).reshape(r, r, c, c)
     a, b, mh = cache["a"], cache["b"], cache["mh"]
     draw = do.transpose(0, 2, 1, 3).reshape(r * c, r * c)      # [(i,p),(j,q)]
-    da = (b.reshape(s, r * c) @ draw.T).reshape(s, r, c)
-    db = (a.reshape(s, r * c) @ draw).reshape(s, r, c)
+    da = np.matmul(b.reshape(s, r * c), draw.T).reshape(s, r, c)
+    db = np.matmul(a.reshape(s, r * c), draw).reshape(s, r, c)
     dmh_a, dwa, dba = lin_vjp(da, mh, P[f"{px}.a_w"])
     dmh_b, dwb, dbb = lin_vjp(db, mh, P[f"{px}.b_w"])
     G.add(f"{px}.a_w", dwa)
@@ -507,9 +507,71 @@ MSA_TRACK = ("row_attn", "col_attn", "msa_transition")
 PAIR_TRACK = PAIR_SUBOPS
 
 
+def _msa_track_fwd(P, blk, m, z, d, caches):
+    for name in MSA_TRACK:
+        delta, caches[name] = subop_fwd(name, P, f"blk{blk}.{name}", m, z, d)
+        m = m + delta
+    return m
+
+
+def _pair_track_fwd(P, blk, z, d, caches):
+    for name in PAIR_TRACK:
+        delta, caches[name] = subop_fwd(name, P, f"blk{blk}.{name}", None, z, d)
+        z = z + delta
+    return z
+
+
+def _pair_track_vjp(dz, caches, P, blk, d, G):
+    """Gradient wrt the pair-track input (residuals included)."""
+    for name in reversed(PAIR_TRACK):
+        dz = dz + subop_vjp(name, dz, caches[name], P, f"blk{blk}.{name}", d, G)[1]
+    return dz
+
+
+def _msa_track_vjp(dm, caches, P, blk, d, G):
+    """(gradient wrt the MSA-track input m, its gradient wrt z: dz_row)."""
+    dz_row = None
+    for name in reversed(MSA_TRACK):
+        dm_part, dz_part = subop_vjp(name, dm, caches[name], P, f"blk{blk}.{name}", d, G)
+        dm = dm + dm_part
+        if dz_part is not None:
+            dz_row = dz_part
+    return dm, dz_row
+
+
+def block_fwd_variant(P, blk, m, z, d):
+    """af2 / multimer wirings (src/evoformer.py:448-455).
+    af2:      m' = msa_track(m, z); z1 = z + opm(m'); z' = pair_track(z1)
+    multimer: z1 = z + opm(m); m' = msa_track(m, z1); z' = pair_track(z1)"""
+    caches = {}
+    if d.variant == "af2":
+        m_c = _msa_track_fwd(P, blk, m, z, d, caches)
+        o, caches["opm"] = opm_fwd(P, f"blk{blk}.opm", m_c, d)
+        z1 = z + o
+    else:
+        o, caches["opm"] = opm_fwd(P, f"blk{blk}.opm", m, d)
+        z1 = z + o
+        m_c = _msa_track_fwd(P, blk, m, z1, d, caches)
+    return m_c, _pair_track_fwd(P, blk, z1, d, caches), caches
+
+
+def block_vjp_variant(dm_out, dz_out, caches, P, blk, d, G):
+    dz1 = _pair_track_vjp(dz_out, caches, P, blk, d, G)
+    if d.variant == "af2":
+        dm1 = dm_out + subop_vjp("opm", dz1, caches["opm"], P, f"blk{blk}.opm", d, G)[0]
+        dm, dz_row = _msa_track_vjp(dm1, caches, P, blk, d, G)
+        return dm, dz1 + dz_row
+    dm1, dz_row = _msa_track_vjp(dm_out, caches, P, blk, d, G)
+    dz1 = dz1 + dz_row
+    dm = dm1 + subop_vjp("opm", dz1, caches["opm"], P, f"blk{blk}.opm", d, G)[0]
+    return dm, dz1
+
+
 def block_fwd(P, blk, m, z, d):
     """Parallel wiring (src/evoformer.py:456-461): both tracks read the
     block inputs; z' = pair_track(z) + opm(msa_track(m, z))."""
+    if d.variant != "parallel":
+        return block_fwd_variant(P, blk, m, z, d)
     caches = {}
     m_c = m
     for name in MSA_TRACK:
@@ -526,6 +588,8 @@ def block_fwd(P, blk, m, z, d):
 def block_vjp(dm_out, dz_out, caches, P, blk, d, G):
     """Returns (dm_in, dz_in).  dz_in = dz_pair + dz_row, the same two
     operands the BP schedule sums (src/schedules.py:253, 293)."""
+    if d.variant != "parallel":
+        return block_vjp_variant(dm_out, dz_out, caches, P, blk, d, G)
     dm = dm_out + subop_vjp("opm", dz_out, caches["opm"], P, f"blk{blk}.opm",
                             d, G)[0]
     dz = dz_out

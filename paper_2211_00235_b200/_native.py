@@ -57,8 +57,6 @@ _SIGS = {
                                   c_i32, c_vp, c_sz, c_vp]),
     "evo_layernorm_bwd_workspace_bytes": (c_sz, [c_i64, c_i32]),
     "evo_relu_bwd_colsum": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
-    "evo_layernorm_fwd_proj": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f32,
-                                       c_vp, c_i32, c_vp, c_i64, c_vp]),
     "evo_layernorm_bwd_proj": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_vp, c_sz, c_vp]),
@@ -69,12 +67,12 @@ _SIGS = {
     "evo_attention_bwd_workspace_bytes": (c_sz, [C.POINTER(AttnDesc)]),
     "evo_reduce_lead": (c_i32, [c_i32, c_i64, c_i64, c_i64, c_vp, c_vp, c_i64, c_i64, c_i32,
                                 c_vp]),
-    "evo_attn_long_softmax": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_i64, c_i64,
-                                      c_vp, c_vp, c_vp]),
+    "evo_attn_long_softmax": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_vp, c_vp, c_i64, c_i64,
+                                      c_i64, c_vp, c_vp, c_vp]),
     "evo_attn_long_gate": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "evo_attn_long_prep": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_vp]),
-    "evo_attn_long_dsoftmax": (c_i32, [c_i32, c_i32, c_i32, c_vp, c_vp, c_vp, c_i64, c_i64,
+    "evo_attn_long_dsoftmax": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_vp, c_vp, c_vp, c_i64, c_i64,
                                        c_i64, c_vp, c_vp, c_i64, c_i64, c_i64, c_vp, c_vp,
                                        c_vp, c_i32, c_vp]),
     "evo_colsum": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i64, c_vp, c_i32, c_vp, c_sz, c_vp]),
@@ -83,23 +81,28 @@ _SIGS = {
                            c_vp]),
     "evo_mul2d": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
                           c_i64, c_vp]),
-    "evo_gate_bwd": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
-                             c_i64, c_vp, c_i64, c_vp]),
     "evo_trimul_gate_fwd": (c_i32, [c_i32, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "evo_trimul_gate_bwd": (c_i32, [c_i32, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp, c_i64,
-                                    c_vp]),
+                                    c_vp, c_vp, c_sz, c_vp]),
+    "evo_trimul_gate_bwd_workspace_bytes": (c_sz, [c_i64, c_i32]),
     "evo_outgate_fwd": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
                                 c_vp]),
     "evo_outgate_bwd": (c_i32, [c_i32, c_i64, c_i64, c_vp, c_vp, c_i64, c_vp, c_i64, c_vp,
-                                c_i64, c_vp, c_i64, c_vp]),
+                                c_i64, c_vp, c_i64, c_vp, c_vp, c_vp, c_sz, c_vp]),
+    "evo_outgate_bwd_workspace_bytes": (c_sz, [c_i64, c_i64]),
     "evo_relu_bwd": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "evo_sq_mean": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "evo_add": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "evo_split_bf16": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
+                               c_vp]),
     "evo_last_error": (C.c_char_p, []),
     "evo_version": (c_i32, []),
     "evo_launch_count": (c_i64, []),
     "evo_tc_available": (c_i32, []),
-    "evo_set_gemm_policy": (None, [c_i32]),
+    "evo_backend_count": (c_i64, [c_i32]),
+    "evo_last_backend": (c_i32, []),
+    "evo_set_strict_tc": (None, [c_i32]),
+    "evo_get_strict_tc": (c_i32, []),
 }
 
 EXPORTED = tuple(_SIGS)
@@ -140,3 +143,38 @@ def check(rc: int, what: str) -> None:
 
 def launch_count() -> int:
     return int(lib().evo_launch_count())
+
+
+# engines (include/evo_b200.h EVO_BK_*)
+BACKENDS = ("gemm_tc", "gemm_simt", "gemm_skinny", "attn_tc", "attn_simt")
+
+
+def backend_counts() -> dict:
+    """Calls served by each engine since the library was loaded."""
+    L = lib()
+    return {name: int(L.evo_backend_count(i)) for i, name in enumerate(BACKENDS)}
+
+
+def last_backend() -> str | None:
+    b = int(lib().evo_last_backend())
+    return BACKENDS[b] if 0 <= b < len(BACKENDS) else None
+
+
+class strict_tc:
+    """Context manager for strict tensor-core mode (default ON): inside
+    ``strict_tc(False)`` a bf16 GEMM / attention the tensor-core kernels do
+    not take may run on the SIMT kernels instead of raising."""
+
+    def __init__(self, on: bool = True):
+        self.on = on
+        self.prev = None
+
+    def __enter__(self):
+        L = lib()
+        self.prev = int(L.evo_get_strict_tc())
+        L.evo_set_strict_tc(1 if self.on else 0)
+        return self
+
+    def __exit__(self, *exc):
+        lib().evo_set_strict_tc(self.prev)
+        return False

@@ -33,17 +33,18 @@ __device__ __forceinline__ float warp_sum(float v) {
 constexpr int MAXJ = 32;
 
 template <int NJ>  // NJ > 0: row in NJ registers per lane (L <= 32 * NJ)
-__global__ void long_softmax_kernel(int64_t nrows, int H, int L, const float *__restrict__ S,
-                                    const float *__restrict__ bias, int64_t bh, int64_t bq,
-                                    int64_t bk, bf16 *__restrict__ P, float *__restrict__ lse) {
+__global__ void long_softmax_kernel(int64_t nrows, int H, int L, int64_t ld,
+                                    const float *__restrict__ S, const float *__restrict__ bias,
+                                    int64_t bh, int64_t bq, int64_t bk, bf16 *__restrict__ P,
+                                    float *__restrict__ lse) {
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= nrows) return;
   const int q = (int)(row % L);
   const int h = (int)((row / L) % H);
-  const float *s = S + row * L;
+  const float *s = S + row * ld;
   const float *bb = bias ? bias + h * bh + q * bq : nullptr;
-  bf16 *p = P + row * L;
+  bf16 *p = P + row * ld;
   float mx = -INFINITY, sum = 0.f;
   if constexpr (NJ > 0) {
     float v[NJ];
@@ -122,7 +123,8 @@ __global__ void long_prep_kernel(int64_t rows, int H, int D, const bf16 *__restr
 
 // thread per (h, q, k) (consecutive threads along k: coalesced), batch rows
 // of the chunk in order
-__global__ void long_dsoftmax_kernel(int nbc, int H, int L, const float *__restrict__ S,
+__global__ void long_dsoftmax_kernel(int nbc, int H, int L, int64_t ld,
+                                     const float *__restrict__ S,
                                      const float *__restrict__ dP,
                                      const float *__restrict__ bias, int64_t bh, int64_t bq,
                                      int64_t bk, const float *__restrict__ lse,
@@ -140,15 +142,16 @@ __global__ void long_dsoftmax_kernel(int nbc, int H, int L, const float *__restr
   for (int b = 0; b < nbc; ++b) {
     const int64_t lrow = ((int64_t)b * H + h) * L + q;   // logits row in the chunk
     const int64_t arow = row0 + b * rb + q * rl;         // activation row id
+    const int64_t ei = lrow * ld + k;
     float p;
     if (S) {  // recompute P from the logits and lse
-      p = __expf(S[lrow * L + k] + bv - lse[lrow]);
-      P[lrow * L + k] = __float2bfloat16(p);
+      p = __expf(S[ei] + bv - lse[lrow]);
+      P[ei] = __float2bfloat16(p);
     } else {  // the forward's P
-      p = __bfloat162float(P[lrow * L + k]);
+      p = __bfloat162float(P[ei]);
     }
-    const float ds = p * (dP[lrow * L + k] - Dq[arow * H + h]);
-    dS[lrow * L + k] = __float2bfloat16(ds);
+    const float ds = p * (dP[ei] - Dq[arow * H + h]);
+    dS[ei] = __float2bfloat16(ds);
     sum += ds;
   }
   if (dbias) {
@@ -166,16 +169,16 @@ using namespace evo;
 
 extern "C" {
 
-EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, const float *S, const float *bias,
-                                  int64_t bh, int64_t bq, int64_t bk, void *P, float *lse,
-                                  void *stream) {
-  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && S && P && lse, EVO_EARG,
+EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, int64_t ld, const float *S,
+                                  const float *bias, int64_t bh, int64_t bq, int64_t bk, void *P,
+                                  float *lse, void *stream) {
+  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && ld >= L && S && P && lse, EVO_EARG,
               "attn_long_softmax: bad arguments");
   const int64_t rows = nbc * H * L;
   if (rows == 0) return EVO_OK;
 #define EVO_LONG_SOFTMAX(NJ)                                                            \
   long_softmax_kernel<NJ><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(        \
-      rows, H, L, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse)
+      rows, H, L, ld, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse)
   if (L <= 256) EVO_LONG_SOFTMAX(8);
   else if (L <= 512) EVO_LONG_SOFTMAX(16);
   else if (L <= 32 * MAXJ) EVO_LONG_SOFTMAX(32);
@@ -213,17 +216,19 @@ EVO_API int evo_attn_long_prep(int64_t rows, int H, int D, const void *dgm, cons
   return EVO_OK;
 }
 
-EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, const float *S, const float *dP,
+EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, int64_t ld, const float *S,
+                                   const float *dP,
                                    const float *bias, int64_t bh, int64_t bq, int64_t bk,
                                    const float *lse, const float *Dq, int64_t row0, int64_t rb,
                                    int64_t rl, void *P, void *dS, float *dbias, int acc,
                                    void *stream) {
-  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && dP && Dq && P && dS && (!S || lse), EVO_EARG,
+  EVO_REQUIRE(nbc >= 0 && H >= 1 && L >= 1 && ld >= L && dP && Dq && P && dS && (!S || lse),
+              EVO_EARG,
               "attn_long_dsoftmax: bad arguments");
   if (nbc == 0) return EVO_OK;
   const int64_t n = (int64_t)H * L * L;
   long_dsoftmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      nbc, H, L, S, dP, bias, bh, bq, bk, lse, Dq, row0, rb, rl, reinterpret_cast<bf16 *>(P),
+      nbc, H, L, ld, S, dP, bias, bh, bq, bk, lse, Dq, row0, rb, rl, reinterpret_cast<bf16 *>(P),
       reinterpret_cast<bf16 *>(dS), dbias, acc);
   EVO_LAUNCHED("long_dsoftmax_kernel");
   return EVO_OK;

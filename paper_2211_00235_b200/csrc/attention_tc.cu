@@ -970,7 +970,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     fence_after();
   }
   if (want_bias && qv) {
-    float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
+    float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * a.bh +
                  (int64_t)h * a.bh + (int64_t)q * a.bq;
     const int kbase = qr * KQ;
     if (a.bk == 1 && kbase + KQ <= L && ((reinterpret_cast<uintptr_t>(dst + kbase) & 15) == 0)) {
@@ -1806,7 +1806,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       mbar_wait(&bars[13], 0);
       fence_after();
       if (a.dbias_part != nullptr) {
-        float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * (int64_t)L * L +
+        float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * a.bh +
                      (int64_t)h * a.bh + (int64_t)q * a.bq;
 #pragma unroll
         for (int c = 0; c < 2; ++c) {
@@ -1893,8 +1893,12 @@ bool bias_map(CUtensorMap *m, const evo_attn_desc *d, bool transposed) {
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// The per-chunk dbias partials are [H][bh] images of the bias layout (the
+// reducer writes H*bh elements, padding between rows included), so the
+// rows must tile one head's span: bh >= L * (row stride).
 int bias_mode(const evo_attn_desc *d) {
   if (!d->bias) return 0;
+  if (d->bh < (int64_t)d->L * std::max(d->bq, d->bk)) return -1;
   if (d->bk == 1 && d->bq % 4 == 0 && d->bh % 4 == 0) return 1;
   if (d->bq == 1 && d->bk % 4 == 0 && d->bh % 4 == 0) return 2;
   return -1;
@@ -1919,7 +1923,7 @@ size_t gate_part_offset(const evo_attn_desc *d) {
     int64_t nch = row_chunks(d);
     int64_t chunk = (d->nb + nch - 1) / nch;
     nch = (d->nb + chunk - 1) / chunk;
-    part = ((size_t)nch * d->H * d->L * d->L * 4 + 255) / 256 * 256;
+    part = ((size_t)nch * d->H * d->bh * 4 + 255) / 256 * 256;
   }
   return dO_pad + Dq_pad + part;
 }
@@ -2097,7 +2101,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");
   }
   if (d->dbias)
-    return reduce_lead(EVO_F32, nch, 1, (int64_t)d->H * d->L * d->L, part, d->dbias, 0, 1, 0, st);
+    return reduce_lead(EVO_F32, nch, 1, (int64_t)d->H * d->bh, part, d->dbias, 0, 1, 0, st);
   return EVO_OK;
 }
 
@@ -2145,7 +2149,7 @@ size_t attention_tc_bwd_ws(const evo_attn_desc *d) {
     int64_t nch = row_chunks(d);
     int64_t chunk = (d->nb + nch - 1) / nch;
     nch = (d->nb + chunk - 1) / chunk;
-    part = (size_t)nch * d->H * d->L * d->L * 4;
+    part = (size_t)nch * d->H * d->bh * 4;
   }
   return dO_pad + Dq_pad + part;
 }

@@ -5,12 +5,20 @@
 
 #include "common.cuh"
 #include "gemm.cuh"
+#include "tc_common.cuh"
 
 namespace evo {
 
 std::atomic<int64_t> g_launches{0};
 static thread_local char g_err[512] = "";
-static int g_gemm_policy = 0;
+static std::atomic<int> g_strict_tc{1};
+static std::atomic<int64_t> g_backend[EVO_BK_COUNT];
+static thread_local int g_last_backend = -1;
+
+static void note_backend(int b) {
+  g_backend[b].fetch_add(1, std::memory_order_relaxed);
+  g_last_backend = b;
+}
 
 void set_error(const char *fmt, ...) {
   va_list ap;
@@ -29,8 +37,6 @@ int layernorm_bwd(int, int, int, int64_t, int, const void *, int64_t, const void
 int layernorm_bwd_ex(int64_t, int, const float *, const void *, int, const float *, const float *,
                      const float *, const float *, float *, void *, float *, float *, float *,
                      void *, size_t, cudaStream_t);
-int layernorm_fwd_proj(int64_t, int, const float *, const float *, const float *, void *, float *,
-                       float *, float, const void *, int, float *, int64_t, cudaStream_t);
 int layernorm_bwd_proj(int64_t, int, const float *, const float *, const float *, const float *,
                        const float *, const float *, const float *, const float *, int64_t,
                        const void *, int, float *, void *, float *, float *, float *, float *,
@@ -49,26 +55,29 @@ int copy2d(int, int, int64_t, int64_t, const void *, int64_t, int64_t, void *, i
            cudaStream_t);
 int mul2d(int, int, int, int64_t, int64_t, const void *, int64_t, const void *, int64_t, void *,
           int64_t, cudaStream_t);
-int gate_bwd(int, int64_t, int64_t, const void *, int64_t, const void *, int64_t, const void *,
-             int64_t, void *, int64_t, void *, int64_t, cudaStream_t);
 int trimul_gate_fwd(int, int64_t, int, const void *, int64_t, void *, void *, cudaStream_t);
 int trimul_gate_bwd(int, int64_t, int, const void *, int64_t, const float *, const float *, void *,
-                    int64_t, cudaStream_t);
+                    int64_t, float *, float *, cudaStream_t);
+size_t trimul_gate_bwd_ws(int64_t, int);
+size_t outgate_bwd_ws(int64_t, int64_t);
 int outgate_fwd(int, int64_t, int64_t, const float *, const void *, int64_t, const void *,
                 int64_t, float *, cudaStream_t);
 int outgate_bwd(int, int64_t, int64_t, const float *, const void *, int64_t, const void *,
-                int64_t, void *, int64_t, void *, int64_t, cudaStream_t);
+                int64_t, void *, int64_t, void *, int64_t, float *, float *, float *,
+                cudaStream_t);
 int relu_bwd(int, int64_t, const void *, const void *, void *, cudaStream_t);
 int relu_bwd_colsum(int64_t, int64_t, const void *, const void *, void *, float *, float *,
                     cudaStream_t);
 int sq_mean(int64_t, const float *, float *, float *, void *, cudaStream_t);
 int add(int64_t, const float *, const float *, float *, cudaStream_t);
+int split_bf16(int64_t, int64_t, const float *, int64_t, void *, int64_t, void *, int64_t, void *,
+               int64_t, cudaStream_t);
 
 static bool use_skinny(const evo_gemm_desc *d) {
-  return g_gemm_policy == 0 && !d->force_simt && gemm_skinny_accepts(d);
+  return !d->force_simt && gemm_skinny_accepts(d);
 }
 static bool use_tc(const evo_gemm_desc *d) {
-  return g_gemm_policy == 0 && !d->force_simt && !gemm_skinny_accepts(d) && gemm_tc_accepts(d);
+  return !d->force_simt && !gemm_skinny_accepts(d) && gemm_tc_accepts(d);
 }
 
 }  // namespace evo
@@ -83,8 +92,13 @@ extern "C" {
 const char *evo_last_error(void) { return g_err; }
 int evo_version(void) { return 1; }
 int64_t evo_launch_count(void) { return g_launches.load(); }
-void evo_set_gemm_policy(int policy) { g_gemm_policy = policy; }
-int evo_tc_available(void) { return g_gemm_policy == 0 ? 1 : 0; }
+int evo_tc_available(void) { return tc::encode_fn() != nullptr ? 1 : 0; }
+int64_t evo_backend_count(int b) {
+  return (b >= 0 && b < EVO_BK_COUNT) ? g_backend[b].load() : -1;
+}
+int evo_last_backend(void) { return g_last_backend; }
+void evo_set_strict_tc(int on) { g_strict_tc.store(on ? 1 : 0); }
+int evo_get_strict_tc(void) { return g_strict_tc.load(); }
 
 size_t evo_gemm_workspace_bytes(const evo_gemm_desc *d) {
   if (!d) return 0;
@@ -110,11 +124,25 @@ int evo_gemm(const evo_gemm_desc *d, void *stream) {
     CHECK_PTR(d->B.ptr);
   }
   cudaStream_t st = as_stream(stream);
-  if (use_skinny(d) && d->K > 0) return gemm_skinny(d, st);
+  if (use_skinny(d) && d->K > 0) {
+    note_backend(EVO_BK_GEMM_SKINNY);
+    return gemm_skinny(d, st);
+  }
   if (use_tc(d)) {
     int rc = gemm_tc(d, st);
-    if (rc != EVO_EUNSUP) return rc;
+    if (rc != EVO_EUNSUP) {
+      note_backend(EVO_BK_GEMM_TC);
+      return rc;
+    }
   }
+  EVO_REQUIRE(!(g_strict_tc.load() && d->dtype_ab == EVO_BF16 && !d->force_simt), EVO_EUNSUP,
+              "evo_gemm: bf16 M=%lld N=%lld K=%lld B=%lldx%lld (A rs=%lld cs=%lld, B rs=%lld "
+              "cs=%lld, epi=%d bias=%d) is not taken by the tensor-core kernel and strict "
+              "tensor-core mode forbids the SIMT fallback",
+              (long long)d->M, (long long)d->N, (long long)d->K, (long long)d->B1,
+              (long long)d->B2, (long long)d->A.rs, (long long)d->A.cs, (long long)d->B.rs,
+              (long long)d->B.cs, d->epilogue, d->bias ? 1 : 0);
+  note_backend(EVO_BK_GEMM_SIMT);
   return gemm_simt(d, st);
 }
 
@@ -168,19 +196,6 @@ int evo_layernorm_bwd_ex(int dtype_x, int64_t rows, int cols, const float *dy, c
                           dbeta, dx_colsum, workspace, workspace_bytes, as_stream(stream));
 }
 
-int evo_layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
-                           const float *beta, void *y, float *mean, float *rstd, float eps,
-                           const void *Wp, int nh, float *proj, int64_t p_rs, void *stream) {
-  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_layernorm_fwd_proj: rows=%lld cols=%d",
-              (long long)rows, cols);
-  EVO_REQUIRE(eps > 0.f, EVO_EARG, "evo_layernorm_fwd_proj: eps must be > 0");
-  if (rows == 0) return EVO_OK;
-  CHECK_PTR(x); CHECK_PTR(gamma); CHECK_PTR(beta); CHECK_PTR(mean); CHECK_PTR(rstd);
-  CHECK_PTR(Wp); CHECK_PTR(proj);
-  return layernorm_fwd_proj(rows, cols, x, gamma, beta, y, mean, rstd, eps, Wp, nh, proj, p_rs,
-                            as_stream(stream));
-}
-
 int evo_layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x,
                            const float *mean, const float *rstd, const float *gamma,
                            const float *beta, const float *dres, const float *dproj, int64_t p_rs,
@@ -215,10 +230,18 @@ static int check_attn(const evo_attn_desc *d, bool bwd) {
 int evo_attention_fwd(const evo_attn_desc *d, void *stream) {
   int rc = check_attn(d, false);
   if (rc != EVO_OK || d->nb == 0) return rc;
-  if (g_gemm_policy == 0 && attention_tc_accepts(d)) {
+  if (attention_tc_accepts(d)) {
     rc = attention_tc_fwd(d, as_stream(stream));
-    if (rc != EVO_EUNSUP) return rc;
+    if (rc != EVO_EUNSUP) {
+      note_backend(EVO_BK_ATTN_TC);
+      return rc;
+    }
   }
+  EVO_REQUIRE(!(g_strict_tc.load() && d->dtype == EVO_BF16), EVO_EUNSUP,
+              "evo_attention_fwd: bf16 nb=%lld H=%d L=%d D=%d is not taken by the tensor-core "
+              "kernel and strict tensor-core mode forbids the SIMT fallback",
+              (long long)d->nb, d->H, d->L, d->D);
+  note_backend(EVO_BK_ATTN_SIMT);
   return attention_simt_fwd(d, as_stream(stream));
 }
 
@@ -230,10 +253,18 @@ size_t evo_attention_bwd_workspace_bytes(const evo_attn_desc *d) {
 int evo_attention_bwd(const evo_attn_desc *d, void *stream) {
   int rc = check_attn(d, true);
   if (rc != EVO_OK || d->nb == 0) return rc;
-  if (g_gemm_policy == 0 && attention_tc_accepts(d)) {
+  if (attention_tc_accepts(d)) {
     rc = attention_tc_bwd(d, as_stream(stream));
-    if (rc != EVO_EUNSUP) return rc;
+    if (rc != EVO_EUNSUP) {
+      note_backend(EVO_BK_ATTN_TC);
+      return rc;
+    }
   }
+  EVO_REQUIRE(!(g_strict_tc.load() && d->dtype == EVO_BF16), EVO_EUNSUP,
+              "evo_attention_bwd: bf16 nb=%lld H=%d L=%d D=%d is not taken by the tensor-core "
+              "kernel and strict tensor-core mode forbids the SIMT fallback",
+              (long long)d->nb, d->H, d->L, d->D);
+  note_backend(EVO_BK_ATTN_SIMT);
   return attention_simt_bwd(d, as_stream(stream));
 }
 
@@ -287,16 +318,6 @@ int evo_mul2d(int dtype_a, int dtype_b, int dtype_out, int64_t rows, int64_t col
                as_stream(stream));
 }
 
-int evo_gate_bwd(int dtype, int64_t rows, int64_t cols, const void *dgm, int64_t dgm_rs,
-                 const void *g, int64_t g_rs, const void *o, int64_t o_rs, void *dO,
-                 int64_t dO_rs, void *dgpre, int64_t dgpre_rs, void *stream) {
-  CHECK_DT(dtype);
-  if (rows * cols == 0) return EVO_OK;
-  CHECK_PTR(dgm); CHECK_PTR(g); CHECK_PTR(o); CHECK_PTR(dgpre);
-  return gate_bwd(dtype, rows, cols, dgm, dgm_rs, g, g_rs, o, o_rs, dO, dO_rs, dgpre, dgpre_rs,
-                  as_stream(stream));
-}
-
 int evo_trimul_gate_fwd(int dtype, int64_t rows, int c, const void *proj, int64_t ldp,
                         void *a_cf, void *b_cf, void *stream) {
   CHECK_DT(dtype);
@@ -307,15 +328,22 @@ int evo_trimul_gate_fwd(int dtype, int64_t rows, int c, const void *proj, int64_
   return trimul_gate_fwd(dtype, rows, c, proj, ldp, a_cf, b_cf, as_stream(stream));
 }
 
+size_t evo_trimul_gate_bwd_workspace_bytes(int64_t rows, int c) {
+  return trimul_gate_bwd_ws(rows, c);
+}
+
 int evo_trimul_gate_bwd(int dtype, int64_t rows, int c, const void *proj, int64_t ldp,
                         const float *da_cf, const float *db_cf, void *dproj, int64_t ldd,
-                        void *stream) {
+                        float *colsum, void *workspace, size_t workspace_bytes, void *stream) {
   CHECK_DT(dtype);
   EVO_REQUIRE(c >= 1 && c <= 256 && ldp >= 4 * c && ldd >= 4 * c, EVO_EDIM,
               "evo_trimul_gate_bwd: c=%d", c);
   if (rows == 0) return EVO_OK;
   CHECK_PTR(proj); CHECK_PTR(da_cf); CHECK_PTR(db_cf); CHECK_PTR(dproj);
-  return trimul_gate_bwd(dtype, rows, c, proj, ldp, da_cf, db_cf, dproj, ldd, as_stream(stream));
+  EVO_REQUIRE(!colsum || (workspace && workspace_bytes >= trimul_gate_bwd_ws(rows, c)), EVO_EARG,
+              "evo_trimul_gate_bwd: workspace too small for the column sums");
+  return trimul_gate_bwd(dtype, rows, c, proj, ldp, da_cf, db_cf, dproj, ldd, colsum,
+                         reinterpret_cast<float *>(workspace), as_stream(stream));
 }
 
 int evo_outgate_fwd(int dtype, int64_t rows, int64_t cols, const float *z, const void *g,
@@ -326,13 +354,22 @@ int evo_outgate_fwd(int dtype, int64_t rows, int64_t cols, const float *z, const
   return outgate_fwd(dtype, rows, cols, z, g, g_rs, o, o_rs, znew, as_stream(stream));
 }
 
+size_t evo_outgate_bwd_workspace_bytes(int64_t rows, int64_t cols) {
+  return outgate_bwd_ws(rows, cols);
+}
+
 int evo_outgate_bwd(int dtype, int64_t rows, int64_t cols, const float *dz, const void *g,
                     int64_t g_rs, const void *o, int64_t o_rs, void *do_, int64_t do_rs,
-                    void *dgpre, int64_t dg_rs, void *stream) {
+                    void *dgpre, int64_t dg_rs, float *do_colsum, float *dg_colsum,
+                    void *workspace, size_t workspace_bytes, void *stream) {
   CHECK_DT(dtype);
   if (rows * cols == 0) return EVO_OK;
   CHECK_PTR(dz); CHECK_PTR(g); CHECK_PTR(o); CHECK_PTR(do_); CHECK_PTR(dgpre);
+  EVO_REQUIRE(!(do_colsum || dg_colsum) ||
+                  (workspace && workspace_bytes >= outgate_bwd_ws(rows, cols)),
+              EVO_EARG, "evo_outgate_bwd: workspace too small for the column sums");
   return outgate_bwd(dtype, rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgpre, dg_rs,
+                     do_colsum, dg_colsum, reinterpret_cast<float *>(workspace),
                      as_stream(stream));
 }
 
@@ -367,6 +404,14 @@ int evo_add(int64_t n, const float *a, const float *b, float *out, void *stream)
   if (n == 0) return EVO_OK;
   CHECK_PTR(a); CHECK_PTR(b); CHECK_PTR(out);
   return add(n, a, b, out, as_stream(stream));
+}
+
+int evo_split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *hi,
+                   int64_t h_rs, void *lo, int64_t l_rs, void *hi2, int64_t h2_rs, void *stream) {
+  EVO_REQUIRE(rows >= 0 && cols >= 0, EVO_EDIM, "evo_split_bf16: negative size");
+  if (rows * cols == 0) return EVO_OK;
+  CHECK_PTR(x); CHECK_PTR(hi); CHECK_PTR(lo);
+  return split_bf16(rows, cols, x, x_rs, hi, h_rs, lo, l_rs, hi2, h2_rs, as_stream(stream));
 }
 
 }  // extern "C"

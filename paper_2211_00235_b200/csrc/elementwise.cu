@@ -244,21 +244,6 @@ __global__ void mul2d_kernel(int64_t rows, int64_t cols, const void *a, int64_t 
   }
 }
 
-template <typename T>
-__global__ void gate_bwd_kernel(int64_t rows, int64_t cols, const void *dgm, int64_t dgm_rs,
-                                const void *g, int64_t g_rs, const void *o, int64_t o_rs,
-                                void *dO, int64_t dO_rs, void *dgp, int64_t dgp_rs) {
-  const int64_t total = rows * cols;
-  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
-       e += (int64_t)gridDim.x * blockDim.x) {
-    int64_t r = e / cols, c = e % cols;
-    float d = LD<T>(dgm, r * dgm_rs + c), gv = LD<T>(g, r * g_rs + c);
-    float ov = LD<T>(o, r * o_rs + c);
-    if (dO) ST<T>(dO, r * dO_rs + c, d * gv);
-    ST<T>(dgp, r * dgp_rs + c, d * ov * gv * (1.f - gv));
-  }
-}
-
 // a_cf[ch][row] = sig(ga)*a ; proj cols [a | b | ga | gb] (ga, gb already
 // sigmoid-activated by the projection GEMM epilogue).  Tile: 32 rows x c
 // channels through smem so both the channel-last read and the
@@ -294,8 +279,8 @@ __global__ void trimul_gate_fwd_kernel(int64_t rows, int c, const void *proj, in
 template <typename T>
 __global__ void trimul_gate_bwd_kernel(int64_t rows, int c, const void *proj, int64_t ldp,
                                        const float *da_cf, const float *db_cf, void *dproj,
-                                       int64_t ldd) {
-  extern __shared__ float t2[];  // [2][c][33]
+                                       int64_t ldd, float *part) {
+  extern __shared__ float t2[];  // [2][c][33], then (part) [4c][33] fp32 outputs
   const int64_t r0 = blockIdx.x * 32;
   for (int e = threadIdx.x; e < 32 * c; e += blockDim.x) {
     int ch = e / 32, rr = e % 32;
@@ -319,8 +304,27 @@ __global__ void trimul_gate_bwd_kernel(int64_t rows, int c, const void *proj, in
       float d = t2[(which * c + ch) * 33 + rr];
       float v = LD<T>(proj, base + which * c + ch);
       float g = LD<T>(proj, base + (2 + which) * c + ch);
-      ST<T>(dproj, dbase + which * c + ch, d * g);
-      ST<T>(dproj, dbase + (2 + which) * c + ch, d * v * g * (1.f - g));
+      const float dv = d * g, dg = d * v * g * (1.f - g);
+      ST<T>(dproj, dbase + which * c + ch, dv);
+      ST<T>(dproj, dbase + (2 + which) * c + ch, dg);
+      if (part) {
+        float *so = t2 + 2 * c * 33;
+        so[(which * c + ch) * 33 + rr] = dv;
+        so[((2 + which) * c + ch) * 33 + rr] = dg;
+      }
+    }
+  }
+  if (part) {
+    // the bias gradients a_b | b_b | a_gate_b | b_gate_b from the fp32 values
+    // (not the bf16-rounded dproj): per-block column sums over the 32 rows in
+    // order, reduced over blocks by colsum_stage2 (deterministic)
+    __syncthreads();
+    const float *so = t2 + 2 * c * 33;
+    const int nrow = (int)(rows - r0 < 32 ? rows - r0 : 32);
+    for (int col = threadIdx.x; col < 4 * c; col += blockDim.x) {
+      float acc = 0.f;
+      for (int rr = 0; rr < nrow; ++rr) acc += so[col * 33 + rr];
+      part[blockIdx.x * (int64_t)(4 * c) + col] = acc;
     }
   }
 }
@@ -411,6 +415,58 @@ __global__ void outgate_bwd_bf16x8_kernel(int64_t rows, int64_t cols, const floa
     }
     *reinterpret_cast<uint4 *>(do_ + r * do_rs + c) = pack8(a);
     *reinterpret_cast<uint4 *>(dgp + r * dg_rs + c) = pack8(b);
+  }
+}
+
+// Out-gate backward (bf16 g / o, fp32 dz, cols % 8 == 0) with the column sums
+// of both outputs fused in, taken from the fp32 values before rounding: the
+// out_b gradient (sum of do) and the out_gate_b gradient (sum of dgpre).
+// Tiling of relu_bwd_colsum_kernel: thread = 8 columns, rows ty, ty+8, ...
+__global__ void outgate_bwd_colsum_kernel(int64_t rows, int64_t cols, const float *dz,
+                                          const bf16 *g, int64_t g_rs, const bf16 *o,
+                                          int64_t o_rs, bf16 *do_, int64_t do_rs, bf16 *dgp,
+                                          int64_t dg_rs, int64_t rpb, float *part_do,
+                                          float *part_dg) {
+  __shared__ float red[8][32 * 8 + 4];
+  const int64_t c0 = (blockIdx.y * 32 + threadIdx.x) * 8;
+  const int64_t r0 = blockIdx.x * rpb;
+  const int64_t r1 = min(rows, r0 + rpb);
+  float a_do[8], a_dg[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) a_do[j] = a_dg[j] = 0.f;
+  if (c0 < cols) {
+    for (int64_t r = r0 + threadIdx.y; r < r1; r += 8) {
+      float gv[8], ov[8], dv[8], gg[8];
+      unpack8(__ldg(reinterpret_cast<const uint4 *>(g + r * g_rs + c0)), gv);
+      unpack8(__ldg(reinterpret_cast<const uint4 *>(o + r * o_rs + c0)), ov);
+      const float4 *zp = reinterpret_cast<const float4 *>(dz + r * cols + c0);
+      const float4 z0 = __ldg(zp), z1 = __ldg(zp + 1);
+      const float d[8] = {z0.x, z0.y, z0.z, z0.w, z1.x, z1.y, z1.z, z1.w};
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        dv[j] = d[j] * gv[j];
+        gg[j] = d[j] * ov[j] * gv[j] * (1.f - gv[j]);
+        a_do[j] += dv[j];
+        a_dg[j] += gg[j];
+      }
+      *reinterpret_cast<uint4 *>(do_ + r * do_rs + c0) = pack8(dv);
+      *reinterpret_cast<uint4 *>(dgp + r * dg_rs + c0) = pack8(gg);
+    }
+  }
+  const int t = threadIdx.y * 32 + threadIdx.x;
+  const int64_t c = blockIdx.y * 256 + t;
+#pragma unroll
+  for (int pass = 0; pass < 2; ++pass) {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) red[threadIdx.y][threadIdx.x * 8 + j] = pass ? a_dg[j] : a_do[j];
+    __syncthreads();
+    if (t < 256 && c < cols) {
+      float sacc = 0.f;
+#pragma unroll
+      for (int y = 0; y < 8; ++y) sacc += red[y][t];
+      (pass ? part_dg : part_do)[blockIdx.x * cols + c] = sacc;
+    }
+    __syncthreads();
   }
 }
 
@@ -647,18 +703,6 @@ int mul2d(int ta, int tb, int to, int64_t rows, int64_t cols, const void *a, int
   return EVO_OK;
 }
 
-int gate_bwd(int dt, int64_t rows, int64_t cols, const void *dgm, int64_t dgm_rs, const void *g,
-             int64_t g_rs, const void *o, int64_t o_rs, void *dO, int64_t dO_rs, void *dgp,
-             int64_t dgp_rs, cudaStream_t st) {
-  int nb = ew_blocks(rows * cols);
-  if (dt == EVO_F32)
-    gate_bwd_kernel<float><<<nb, 256, 0, st>>>(rows, cols, dgm, dgm_rs, g, g_rs, o, o_rs, dO, dO_rs, dgp, dgp_rs);
-  else
-    gate_bwd_kernel<bf16><<<nb, 256, 0, st>>>(rows, cols, dgm, dgm_rs, g, g_rs, o, o_rs, dO, dO_rs, dgp, dgp_rs);
-  EVO_LAUNCHED("gate_bwd_kernel");
-  return EVO_OK;
-}
-
 int trimul_gate_fwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, void *a_cf,
                     void *b_cf, cudaStream_t st) {
   unsigned nb = (unsigned)((rows + 31) / 32);
@@ -672,15 +716,27 @@ int trimul_gate_fwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, 
 }
 
 int trimul_gate_bwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, const float *da,
-                    const float *db, void *dproj, int64_t ldd, cudaStream_t st) {
+                    const float *db, void *dproj, int64_t ldd, float *colsum, float *ws,
+                    cudaStream_t st) {
   unsigned nb = (unsigned)((rows + 31) / 32);
-  size_t smem = (size_t)2 * c * 33 * sizeof(float);
+  size_t smem = (size_t)(colsum ? 6 : 2) * c * 33 * sizeof(float);
+  float *part = colsum ? ws : nullptr;
   if (dt == EVO_F32)
-    trimul_gate_bwd_kernel<float><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd);
+    trimul_gate_bwd_kernel<float><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd,
+                                                         part);
   else
-    trimul_gate_bwd_kernel<bf16><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd);
+    trimul_gate_bwd_kernel<bf16><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd,
+                                                        part);
   EVO_LAUNCHED("trimul_gate_bwd_kernel");
+  if (colsum) {
+    colsum_stage2<<<(unsigned)((4 * c + 31) / 32), 1024, 0, st>>>((int)nb, 4 * c, part, colsum, 0);
+    EVO_LAUNCHED("colsum_stage2");
+  }
   return EVO_OK;
+}
+
+size_t trimul_gate_bwd_ws(int64_t rows, int c) {
+  return (size_t)((rows + 31) / 32) * 4 * c * sizeof(float);
 }
 
 int outgate_fwd(int dt, int64_t rows, int64_t cols, const float *z, const void *g, int64_t g_rs,
@@ -701,13 +757,47 @@ int outgate_fwd(int dt, int64_t rows, int64_t cols, const float *z, const void *
   return EVO_OK;
 }
 
+static int64_t outgate_colsum_blocks(int64_t rows, int64_t cols, int64_t &rpb) {
+  const int64_t col_tiles = (cols + 255) / 256;
+  int64_t nblk = std::max<int64_t>(1, std::min<int64_t>(256, (4 * num_sms() + col_tiles - 1) /
+                                                                 col_tiles));
+  nblk = std::min<int64_t>(nblk, std::max<int64_t>(1, rows / 64));
+  rpb = (rows + nblk - 1) / nblk;
+  return (rows + rpb - 1) / rpb;
+}
+
+size_t outgate_bwd_ws(int64_t rows, int64_t cols) {
+  int64_t rpb;
+  return (size_t)outgate_colsum_blocks(rows, cols, rpb) * 2 * cols * sizeof(float);
+}
+
 int outgate_bwd(int dt, int64_t rows, int64_t cols, const float *dz, const void *g, int64_t g_rs,
                 const void *o, int64_t o_rs, void *do_, int64_t do_rs, void *dgp, int64_t dg_rs,
-                cudaStream_t st) {
+                float *do_colsum, float *dg_colsum, float *ws, cudaStream_t st) {
   int nb = ew_blocks(rows * cols);
   auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-  if (dt == EVO_BF16 && cols % 8 == 0 && g_rs % 8 == 0 && o_rs % 8 == 0 && do_rs % 8 == 0 &&
-      dg_rs % 8 == 0 && al16(dz) && al16(g) && al16(o) && al16(do_) && al16(dgp)) {
+  const bool vec = dt == EVO_BF16 && cols % 8 == 0 && g_rs % 8 == 0 && o_rs % 8 == 0 &&
+                   do_rs % 8 == 0 && dg_rs % 8 == 0 && al16(dz) && al16(g) && al16(o) &&
+                   al16(do_) && al16(dgp);
+  if (do_colsum || dg_colsum) {
+    EVO_REQUIRE(vec && do_colsum && dg_colsum && ws, EVO_EUNSUP,
+                "outgate_bwd: fused column sums need bf16, cols %% 8 == 0, aligned rows");
+    int64_t rpb;
+    const int64_t nblk = outgate_colsum_blocks(rows, cols, rpb);
+    const int64_t col_tiles = (cols + 255) / 256;
+    float *pdo = ws, *pdg = ws + nblk * cols;
+    outgate_bwd_colsum_kernel<<<dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st>>>(
+        rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
+        o_rs, reinterpret_cast<bf16 *>(do_), do_rs, reinterpret_cast<bf16 *>(dgp), dg_rs, rpb, pdo,
+        pdg);
+    EVO_LAUNCHED("outgate_bwd_colsum_kernel");
+    colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, pdo, do_colsum, 0);
+    EVO_LAUNCHED("colsum_stage2");
+    colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, pdg, dg_colsum, 0);
+    EVO_LAUNCHED("colsum_stage2");
+    return EVO_OK;
+  }
+  if (vec) {
     outgate_bwd_bf16x8_kernel<<<ew_blocks(rows * cols / 8), 256, 0, st>>>(
         rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs,
         reinterpret_cast<const bf16 *>(o), o_rs, reinterpret_cast<bf16 *>(do_), do_rs,
@@ -774,6 +864,41 @@ int sq_mean(int64_t n, const float *x, float *out, float *dx, void *ws, cudaStre
   EVO_LAUNCHED("sq_partial_kernel");
   sq_final_kernel<<<1, 256, 0, st>>>(SQ_BLOCKS, n, part, out);
   EVO_LAUNCHED("sq_final_kernel");
+  return EVO_OK;
+}
+
+// x (fp32) = hi + lo with hi = bf16(x), lo = bf16(x - hi): the split operand
+// of a 3-product bf16 GEMM (hi*hi' + lo*hi' + hi*lo' ~ fp32 product).  hi is
+// written to hi (and hi2 when given), lo to lo; 4 columns per thread.
+__global__ void split_bf16_kernel(int64_t rows, int64_t cols, const float *__restrict__ x,
+                                  int64_t x_rs, bf16 *__restrict__ hi, int64_t h_rs,
+                                  bf16 *__restrict__ lo, int64_t l_rs, bf16 *__restrict__ hi2,
+                                  int64_t h2_rs) {
+  const int64_t c4 = (cols + 3) / 4;
+  const int64_t total = rows * c4;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = e / c4, c0 = (e - r * c4) * 4;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int64_t c = c0 + u;
+      if (c >= cols) break;
+      const float v = x[r * x_rs + c];
+      const bf16 h = __float2bfloat16(v);
+      const bf16 l = __float2bfloat16(v - __bfloat162float(h));
+      hi[r * h_rs + c] = h;
+      lo[r * l_rs + c] = l;
+      if (hi2) hi2[r * h2_rs + c] = h;
+    }
+  }
+}
+
+int split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *hi, int64_t h_rs,
+               void *lo, int64_t l_rs, void *hi2, int64_t h2_rs, cudaStream_t st) {
+  split_bf16_kernel<<<ew_blocks(rows * ((cols + 3) / 4)), 256, 0, st>>>(
+      rows, cols, x, x_rs, reinterpret_cast<bf16 *>(hi), h_rs, reinterpret_cast<bf16 *>(lo), l_rs,
+      reinterpret_cast<bf16 *>(hi2), h2_rs);
+  EVO_LAUNCHED("split_bf16_kernel");
   return EVO_OK;
 }
 

@@ -414,8 +414,10 @@ bool tallk_ok(const evo_gemm_desc *d, bool &wide_is_m) {
 Kind classify(const evo_gemm_desc *d) {
   if (d->K < 1) return SK_NONE;
   const int64_t nb = d->B1 * d->B2;
-  if (nb == 1 && d->N <= 16 && d->M >= 4096 && d->K <= 2048) return SK_ROWDOT;
-  if (nb == 1 && d->K <= 16 && d->M >= 4096 && d->N >= 32 && d->N <= 2048) return SK_EXPAND;
+  // any M: a narrow side (N <= 16 outputs, or K <= 16) would waste most of a
+  // 128-wide tensor-core tile, and N < 8 does not fit the TMA operand maps
+  if (nb == 1 && d->N <= 16 && d->K <= 2048) return SK_ROWDOT;
+  if (nb == 1 && d->K <= 16 && d->N >= 32 && d->N <= 2048) return SK_EXPAND;
   bool wm;
   if (tallk_ok(d, wm)) return SK_TALLK;
   return SK_NONE;

@@ -1208,19 +1208,6 @@ int layernorm_bwd_ex(int64_t rows, int cols, const float *dy, const void *x, int
                                            dx_colsum);
 }
 
-int layernorm_fwd_proj(int64_t rows, int cols, const float *x, const float *gamma,
-                       const float *beta, void *y, float *mean, float *rstd, float eps,
-                       const void *Wp, int nh, float *proj, int64_t p_rs, cudaStream_t st) {
-  EVO_REQUIRE(cols == 128 && nh >= 1 && nh <= 8, EVO_EUNSUP,
-              "layernorm_fwd_proj: cols=%d nh=%d (fused path: cols 128, nh <= 8)", cols, nh);
-  EVO_REQUIRE(aligned16(x) && aligned16(gamma) && aligned16(beta) && (!y || aligned16(y)), EVO_EARG,
-              "layernorm_fwd_proj: operands must be 16-byte aligned");
-  if (rows == 0) return EVO_OK;
-  return ln_fwd_tma_launch<1, 8, bf16>(rows, x, gamma, beta, reinterpret_cast<bf16 *>(y), mean,
-                                       rstd, eps, reinterpret_cast<const bf16 *>(Wp), nh, proj,
-                                       p_rs, st);
-}
-
 int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, const float *mean,
                        const float *rstd, const float *gamma, const float *beta,
                        const float *dres, const float *dproj, int64_t p_rs, const void *Wp, int nh,

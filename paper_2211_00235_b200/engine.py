@@ -25,7 +25,13 @@ from . import kernels as K
 from ._native import EPI_NONE, EPI_RELU, EPI_SIGMOID_FROM
 from .kernels import Mat
 
+import os
+
 MSA_SUBOPS = ("row_attn", "col_attn", "msa_transition", "opm")
+MSA_TRACK = ("row_attn", "col_attn", "msa_transition")
+# 3-product bf16 first projection in the transitions (see transition_fwd);
+# EVO_SPLIT_TRANSITION=0 turns it off (plain bf16 operands)
+SPLIT_TRANSITION = os.environ.get("EVO_SPLIT_TRANSITION", "1") != "0"
 PAIR_SUBOPS = ("tri_mult_out", "tri_mult_in", "tri_attn_start", "tri_attn_end",
                "pair_transition")
 F32 = torch.float32
@@ -106,6 +112,14 @@ def pack_subop(P, px, name, cfg, act, dev):
     elif name in ("msa_transition", "pair_transition"):
         pk["W1"] = _to_act(dev, act, g("w1"))
         pk["W2"] = _to_act(dev, act, g("w2"))
+        if act != F32 and SPLIT_TRANSITION:
+            # [W_hi; W_hi; W_lo] for the 3-product first projection
+            w1 = g("w1")
+            cx, tc = w1.shape
+            w3 = _empty((3 * cx, tc), act, dev)
+            K.split_bf16(w1, cx, tc, w3, w3, h_rs=tc, l_rs=tc, hi2=w3, h2_rs=tc,
+                         l_off=2 * cx * tc, h2_off=cx * tc)
+            pk["W1x3"] = w3
     elif name == "opm":
         c_m = g("a_w").shape[0]
         pk["Wab"] = _cat_cols(dev, act, c_m, [g("a_w"), g("b_w")])
@@ -289,8 +303,10 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     lse = _empty((nb, h, L), F32, dev)
     bq, bk = (cfg.r, 1) if name != "tri_attn_end" else (1, cfg.r)
     # GEMM-composed path (bf16, L > 256 or c_head not 16 / 32): keep the
-    # forward's probabilities for the backward instead of recomputing them
-    p_store = _empty(K.long_p_elems(nb, h, L), act, dev) if K.use_long(act, L, ch) else None
+    # forward's probabilities for the backward instead of recomputing them,
+    # when they fit the per-call byte cap (K.KEEP_P_MAX_BYTES)
+    p_store = (_empty(K.long_p_elems(nb, h, L), act, dev)
+               if K.use_long(act, L, ch) and K.keep_p(nb, h, L) else None)
     K.attention(proj=proj, hc=hc, nb=nb, H=h, L=L, D=ch, scale=ch ** -0.5,
                 sb=rb * 4 * hc, sl=rl * 4 * hc, o=o, gm=gm, o_sb=rb * hc, o_sl=rl * hc,
                 lse=lse, bias=bias, bh=r2, bq=bq, bk=bk, p_store=p_store)
@@ -391,18 +407,39 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
 # ---------------------------------------------------------------------------
 
 def transition_fwd(P, px, pk, x, cfg, act, resid=True):
+    """relu(LN(x) W1 + b1) W2 + b2 (+ x).  On the bf16 path the first
+    projection runs as a 3-product bf16 GEMM ([hi | lo | hi] LN(x) against
+    [W_hi; W_hi; W_lo], K tripled): fp32-grade pre-activations, so the ReLU
+    mask the backward applies is the reference's.  With plain bf16 operands
+    near-zero pre-activations flip sign, and every flipped unit drops or
+    adds a whole dhid entry in the cancellation-heavy column sums of the
+    b1 / LN gradients (measured: the C3 extra stack's msa_transition
+    gradients at 5e-2 rel-L2, the same as an oracle with bf16-rounded
+    matmul operands; 1.3e-2 with this split)."""
     dev = x.device
     rows, cx = x.shape[0], x.shape[1]
     tc = cfg.t_factor * cx
-    xh = _empty((rows, cx), act, dev)
     mu, rs = _empty(rows, F32, dev), _empty(rows, F32, dev)
-    K.layernorm(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
     hid = _empty((rows, tc), act, dev)
-    K.linear(xh, rows, cx, pk["W1"], tc, tc, hid, tc, bias=P[f"{px}.b1"], epi=EPI_RELU)
+    if "W1x3" in pk:
+        x32 = _empty((rows, cx), F32, dev)
+        K.layernorm(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], x32, mu, rs, cfg.eps)
+        xh = _empty((rows, 3 * cx), act, dev)      # [hi | lo | hi]
+        K.split_bf16(x32, rows, cx, xh, xh, h_rs=3 * cx, l_rs=3 * cx, hi2=xh, h2_rs=3 * cx,
+                     l_off=cx, h2_off=2 * cx)
+        del x32
+        xh_ld = 3 * cx
+        K.linear(xh, rows, 3 * cx, pk["W1x3"], tc, tc, hid, tc, bias=P[f"{px}.b1"],
+                 epi=EPI_RELU)
+    else:
+        xh = _empty((rows, cx), act, dev)
+        K.layernorm(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs, cfg.eps)
+        xh_ld = cx
+        K.linear(xh, rows, cx, pk["W1"], tc, tc, hid, tc, bias=P[f"{px}.b1"], epi=EPI_RELU)
     x_new = _empty(x.shape, F32, dev)
     K.linear(hid, rows, tc, pk["W2"], cx, cx, x_new, cx, bias=P[f"{px}.b2"],
              residual=x if resid else None)
-    return x_new, dict(x=x, xh=xh, mu=mu, rs=rs, hid=hid, resid=resid)
+    return x_new, dict(x=x, xh=xh, xh_ld=xh_ld, mu=mu, rs=rs, hid=hid, resid=resid)
 
 
 def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None):
@@ -417,10 +454,10 @@ def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
     K.linear_dx(dxa, rows, cx, pk["W2"], cx, tc, dhid)
     if act != F32 and tc % 8 == 0:
         K.relu_bwd_colsum(dhid, ctx["hid"], dhid, rows, tc, G["b1"])
-        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc)
+        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
     else:
         K.relu_bwd(dhid, ctx["hid"], dhid, rows * tc)
-        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc)
+        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
         K.colsum(dhid, rows, tc, G["b1"])
     dxh = _empty((rows, cx), F32, dev)
     K.linear_dx(dhid, rows, tc, pk["W1"], tc, cx, dxh)
@@ -540,9 +577,18 @@ def trimul_bwd(P, px, pk, G, ctx, dz_new, cfg, act):
     proj = ctx["proj"]
     dproj = _empty((r2, ldp), act, dev)
     do = _empty((r2, cz), act, dev)
-    K.outgate_bwd(dz_new, r2, cz, proj, ldp, 4 * c, ctx["o"], do, dproj, ldp, 4 * c)
+    # bf16: the out_b / out_gate_b / a,b value and gate bias gradients are
+    # column sums of the fp32 values inside the gate kernels (not of the
+    # bf16-rounded dproj / do: those sums cancel heavily at small widths)
+    fused_cs = act != F32 and cz % 8 == 0 and ldp % 8 == 0
+    if fused_cs:
+        K.outgate_bwd(dz_new, r2, cz, proj, ldp, 4 * c, ctx["o"], do, dproj, ldp, 4 * c,
+                      do_colsum=G["bo"], dg_colsum=G["bp"][4 * c:])
+    else:
+        K.outgate_bwd(dz_new, r2, cz, proj, ldp, 4 * c, ctx["o"], do, dproj, ldp, 4 * c)
     K.linear_dw(ctx["pn"], r2, c, do, cz, G["Wo"], cz)
-    K.colsum(do, r2, cz, G["bo"])
+    if not fused_cs:
+        K.colsum(do, r2, cz, G["bo"])
     dpn = _empty((r2, c), F32, dev)
     K.linear_dx(do, r2, cz, pk["Wo"], cz, c, dpn)
     dp_cf = _empty((c, r, r), act, dev)
@@ -563,10 +609,12 @@ def trimul_bwd(P, px, pk, G, ctx, dz_new, cfg, act):
                r, r, r, B1=c)
         K.gemm(Mat(a_cf, r, 1, bs1=r2), Mat(dp_cf, 1, r, bs1=r2), Mat(db_cf, r, 1, bs1=r2),
                r, r, r, B1=c)
-    K.trimul_gate_bwd(proj, r2, c, ldp, da_cf, db_cf, dproj, ldp)
+    K.trimul_gate_bwd(proj, r2, c, ldp, da_cf, db_cf, dproj, ldp,
+                      colsum=G["bp"][:4 * c] if fused_cs else None)
     zh = ctx["zh"]
     K.linear_dw(zh, r2, cz, dproj, ldp, G["Wp"], ldp)
-    K.colsum(dproj, r2, ldp, G["bp"])
+    if not fused_cs:
+        K.colsum(dproj, r2, ldp, G["bp"])
     dzh = _empty((r2, cz), F32, dev)
     K.linear_dx(dproj, r2, ldp, pk["Wp"], ldp, cz, dzh)
     dz = _empty((r2, cz), F32, dev)
@@ -676,7 +724,10 @@ def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None, dz_pair=None
 
 
 def block_fwd(P, blk, pk, m, z, cfg, act):
-    """Parallel block: (m', z') with z' = pair_track(z) + opm(msa_track(m, z))."""
+    """Parallel block: (m', z') with z' = pair_track(z) + opm(msa_track(m, z));
+    the af2 / multimer wirings dispatch to variant_block_fwd."""
+    if cfg.variant != "parallel":
+        return variant_block_fwd(P, blk, pk, m, z, cfg, act)
     m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z, cfg, act)
     z_pair, cp_ = pair_branch_fwd(P, blk, pk, z, cfg, act)
     z_new, co = opm_fwd(P, f"blk{blk}.opm", pk["opm"], m_new, z_pair, cfg, act)
@@ -692,9 +743,44 @@ def cast_act(x, act):
     return out
 
 
+def variant_block_fwd(P, blk, pk, m, z, cfg, act):
+    """The serial wirings (src/evoformer.py:448-455), same native sub-op
+    launches with every residual add fused into the producing GEMM:
+      af2:      m' = msa_track(m, z); z1 = z + opm(m'); z' = pair_track(z1)
+      multimer: z1 = z + opm(m);  m' = msa_track(m, z1); z' = pair_track(z1)"""
+    if cfg.variant == "af2":
+        m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z, cfg, act)
+        z1, co = opm_fwd(P, f"blk{blk}.opm", pk["opm"], m_new, z, cfg, act)
+    else:
+        z1, co = opm_fwd(P, f"blk{blk}.opm", pk["opm"], m, z, cfg, act)
+        m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z1, cfg, act)
+    z_new, cp_ = pair_branch_fwd(P, blk, pk, z1, cfg, act)
+    return m_new, z_new, dict(msa=cm_, pair=cp_, opm=co)
+
+
+def variant_block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act):
+    """VJP of variant_block_fwd; returns (dm_in, dz_in)."""
+    dz1 = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act,
+                          dz_act=cast_act(dz_out, act))
+    if cfg.variant == "af2":
+        e0 = msa_emit(G)
+        dm1 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz1,
+                      cast_act(dz1, act), dm_out, cfg, act, emit=e0)
+        # dz_in = dz1 (residual of z1 = z + opm) + dz_row (row attention's bias)
+        return msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm1, cfg, act, handoff=e0,
+                              dz_pair=dz1)
+    # multimer: the MSA track read z1, so its dz_row joins dz1 before the OPM
+    dm1, dz1 = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm_out, cfg, act, dz_pair=dz1)
+    dm = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz1, cast_act(dz1, act),
+                 dm1, cfg, act)
+    return dm, dz1
+
+
 def block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act):
     """Returns (dm_in, dz_in) with dz_in = dz_pair + dz_row: the same two
     operands, in the same order, as the BP allreduce (src/comm.py:206-210)."""
+    if cfg.variant != "parallel":
+        return variant_block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act)
     dz_act = cast_act(dz_out, act)
     e0 = msa_emit(G)
     dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act, dm_out,

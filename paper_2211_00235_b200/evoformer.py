@@ -385,20 +385,68 @@ def tri_attn(P, px, z, cfg, ending: bool, shard=None):
     return _run_subop("tri_attn_end" if ending else "tri_attn_start", P, px, None, z, cfg)
 
 
+class _Track(torch.autograd.Function):
+    """One track of a block (residual adds fused into the native launches):
+    which = "msa" (m, z) -> m'  or  "pair" (z) -> z'."""
+
+    @staticmethod
+    def forward(ctx, which, blk, cfg, names, m, z, *params):
+        act = _state["act"]
+        P = dict(zip(names, [p.detach().contiguous() for p in params]))
+        subops = E.MSA_TRACK if which == "msa" else PAIR_SUBOPS
+        pk = E.pack_block(P, blk, cfg, act, z.device, subops)
+        s, r = cfg.s, cfg.r
+        z2 = z.detach().contiguous().reshape(r * r, cfg.c_z)
+        with torch.no_grad():
+            if which == "msa":
+                out, c = E.msa_branch_fwd(P, blk, pk, m.detach().contiguous(), z2, cfg, act)
+                shape = m.shape
+            else:
+                out, c = E.pair_branch_fwd(P, blk, pk, z2, cfg, act)
+                shape = z.shape
+        ctx.state = (which, blk, cfg, act, P, pk, c, names)
+        return out.reshape(shape)
+
+    @staticmethod
+    def backward(ctx, dout):
+        which, blk, cfg, act, P, pk, c, names = ctx.state
+        s, r = cfg.s, cfg.r
+        BG = E.BlockGrads(blk, cfg, dout.device)
+        d = dout.detach().float().contiguous()
+        with torch.no_grad():
+            if which == "msa":
+                dm, dz = E.msa_branch_bwd(P, blk, pk, BG.packed, c, d.reshape(s * r, cfg.c_m),
+                                          cfg, act)
+                dm, dz = dm.reshape(s, r, cfg.c_m), dz.reshape(r, r, cfg.c_z)
+            else:
+                dm = None
+                dz = E.pair_branch_bwd(P, blk, pk, BG.packed, c, d.reshape(r * r, cfg.c_z),
+                                       cfg, act).reshape(r, r, cfg.c_z)
+        grads = [BG.names[n] for n in names]
+        return (None, None, None, None, dm, dz, *grads)
+
+
+def _track_names(cfg, blk, subops):
+    return [f"blk{blk}.{sub}.{s}" for sub in subops for s, _, _ in _subop_param_specs(cfg, sub)]
+
+
 def msa_track(P, blk: int, m, z, cfg, shard=None):
-    """src/evoformer.py:427-432."""
-    m = m + row_attn(P, f"blk{blk}.row_attn", m, z, cfg, shard)
-    m = m + col_attn(P, f"blk{blk}.col_attn", m, cfg, shard)
-    return m + msa_transition(P, f"blk{blk}.msa_transition", m, cfg, shard)
+    """Row attention, column attention and the MSA transition, residually
+    (src/evoformer.py:427-432); one native forward / backward."""
+    _no_shard(shard)
+    _check(m, (cfg.s, cfg.r, cfg.c_m), "msa_track: m")
+    _check(z, (cfg.r, cfg.r, cfg.c_z), "msa_track: z")
+    names = _track_names(cfg, blk, E.MSA_TRACK)
+    return _Track.apply("msa", blk, cfg, names, m, z, *[P[n] for n in names])
 
 
 def pair_track(P, blk: int, z, cfg, shard=None):
-    """src/evoformer.py:435-443."""
-    z = z + tri_mult(P, f"blk{blk}.tri_mult_out", z, cfg, False, shard)
-    z = z + tri_mult(P, f"blk{blk}.tri_mult_in", z, cfg, True, shard)
-    z = z + tri_attn(P, f"blk{blk}.tri_attn_start", z, cfg, False, shard)
-    z = z + tri_attn(P, f"blk{blk}.tri_attn_end", z, cfg, True, shard)
-    return z + pair_transition(P, f"blk{blk}.pair_transition", z, cfg, shard)
+    """Both triangle multiplications, both triangle attentions and the pair
+    transition, residually (src/evoformer.py:435-443)."""
+    _no_shard(shard)
+    _check(z, (cfg.r, cfg.r, cfg.c_z), "pair_track: z")
+    names = _track_names(cfg, blk, PAIR_SUBOPS)
+    return _Track.apply("pair", blk, cfg, names, None, z, *[P[n] for n in names])
 
 
 class _Block(torch.autograd.Function):
@@ -441,20 +489,11 @@ def block_param_names(cfg, blk):
 
 
 def evoformer_block(P, blk: int, m, z, cfg, shard=None):
-    """One block (src/evoformer.py:446-461).  The 'parallel' wiring runs
-    as one fused native forward/backward; 'af2' and 'multimer' are
-    composed from the sub-ops in the reference's order."""
+    """One block (src/evoformer.py:446-461) in the configured wiring
+    (parallel / af2 / multimer), one fused native forward/backward."""
     _no_shard(shard)
     _check(m, (cfg.s, cfg.r, cfg.c_m), "evoformer_block: m")
     _check(z, (cfg.r, cfg.r, cfg.c_z), "evoformer_block: z")
-    if cfg.variant == "af2":
-        m = msa_track(P, blk, m, z, cfg)
-        z = z + opm(P, f"blk{blk}.opm", m, cfg)
-        return m, pair_track(P, blk, z, cfg)
-    if cfg.variant == "multimer":
-        z = z + opm(P, f"blk{blk}.opm", m, cfg)
-        m = msa_track(P, blk, m, z, cfg)
-        return m, pair_track(P, blk, z, cfg)
     names = block_param_names(cfg, blk)
     return _Block.apply(blk, cfg, names, m, z, *[P[n] for n in names])
 

@@ -196,16 +196,6 @@ def layernorm_bwd_ex(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma,
           "evo_layernorm_bwd_ex")
 
 
-def layernorm_proj(x, rows: int, gamma, beta, y, mean, rstd, eps: float, Wp, nh: int, proj,
-                   p_rs: int):
-    """y = LN(x) (bf16, or None) with the pair-bias projection
-    proj[hh*p_rs + row] = y[row] . Wp[:, hh] fused in (c_z = 128 rows)."""
-    check(lib().evo_layernorm_fwd_proj(rows, 128, ptr(x), ptr(gamma), ptr(beta), ptr(y),
-                                       ptr(mean), ptr(rstd), eps, ptr(Wp), nh, ptr(proj), p_rs,
-                                       stream()),
-          "evo_layernorm_fwd_proj")
-
-
 def layernorm_bwd_proj(dy, x, rows: int, mean, rstd, gamma, beta, dproj, p_rs: int, Wp, nh: int,
                        dx, dgamma, dbeta, dWp, *, dres=None, dx_act=None, dx_colsum=None):
     """LayerNorm backward with the pair-bias projection's backward fused in
@@ -224,6 +214,11 @@ def layernorm_bwd_proj(dy, x, rows: int, mean, rstd, gamma, beta, dproj, p_rs: i
 LONG_L = 256
 # fp32 logits elements per chunk of batch rows in the long-key path
 LONG_CHUNK_ELEMS = 1 << 27
+# bytes of bf16 probabilities one forward call may keep for its backward
+# (the kept-P path); larger calls recompute P from the logits and lse in the
+# backward.  Env EVO_KEEP_P_MAX_BYTES overrides; 0 disables keeping P.
+import os as _os
+KEEP_P_MAX_BYTES = int(_os.environ.get("EVO_KEEP_P_MAX_BYTES", str(8 << 30)))
 
 
 def use_long(dtype, L: int, D: int) -> bool:
@@ -233,9 +228,20 @@ def use_long(dtype, L: int, D: int) -> bool:
     return dtype == torch.bfloat16 and (L > LONG_L or D not in (16, 32))
 
 
+def long_ld(L: int) -> int:
+    """Row stride of the long path's [.., L, ld] logits / probabilities: L
+    rounded up to 8 (16-byte aligned bf16 GEMM operand rows)."""
+    return (L + 7) // 8 * 8
+
+
 def long_p_elems(nb, H, L):
     """bf16 elements of the forward probabilities kept for the backward."""
-    return nb * H * L * L
+    return nb * H * L * long_ld(L)
+
+
+def keep_p(nb, H, L) -> bool:
+    """Keep this call's forward P for the backward (within the byte cap)?"""
+    return 2 * long_p_elems(nb, H, L) <= KEEP_P_MAX_BYTES
 
 
 def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias=None,
@@ -255,15 +261,17 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
     rows = nb * L
     dev = proj.device
     Lb = lib()
-    nbc_max = max(1, LONG_CHUNK_ELEMS // (H * L * L))
-    csz = min(nb, nbc_max)
+    ld = long_ld(L)
+    HLL = H * L * ld                      # one batch row's logits, row stride ld
+    nbc_max = max(1, LONG_CHUNK_ELEMS // HLL)
+    # the batched GEMMs take at most 65535 (row, head) batches per call
+    csz = max(1, min(nb, nbc_max, 65535 // H))
     if p_store is not None and p_store.numel() < long_p_elems(nb, H, L):
         raise N.ContractError("attention_long: p_store too small")
-    S = (torch.empty(csz * H * L * L, dtype=torch.float32, device=dev)
+    S = (torch.empty(csz * HLL, dtype=torch.float32, device=dev)
          if dgm is None or p_store is None else None)
-    P = (torch.empty(csz * H * L * L, dtype=torch.bfloat16, device=dev)
+    P = (torch.empty(csz * HLL, dtype=torch.bfloat16, device=dev)
          if p_store is None else None)
-    HLL = H * L * L
     lse_f = lse.view(-1)
 
     # the softmax reads the bias once per batch row: give it a plain
@@ -282,13 +290,14 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
             nbc = min(csz, nb - b0)
             # S = scale * Q K^T
             gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
-                 Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+                 Mat(S, ld, 1, HLL, L * ld), L, L, D, alpha=scale, B1=nbc, B2=H)
             Pc, poff = (P, 0) if p_store is None else (p_store, b0 * HLL)
-            check(Lb.evo_attn_long_softmax(nbc, H, L, ptr(S), ptr(sbias), sbh, sbq, sbk,
+            check(Lb.evo_attn_long_softmax(nbc, H, L, ld, ptr(S), ptr(sbias), sbh, sbq, sbk,
                                            ptr(Pc, poff), ptr(lse_f, b0 * H * L), stream()),
                   "evo_attn_long_softmax")
             # O[row(b,q), h*D+d] = sum_k P[b,h,q,k] V[row(b,k), 2hc + h*D + d]
-            gemm(Mat(Pc, L, 1, HLL, L * L, off=poff), Mat(proj, 1, sl, sb, D, off=b0 * sb + 2 * hc),
+            gemm(Mat(Pc, ld, 1, HLL, L * ld, off=poff),
+                 Mat(proj, 1, sl, sb, D, off=b0 * sb + 2 * hc),
                  Mat(O32, rl * hc, 1, rb * hc, D, off=b0 * rb * hc), L, D, L, B1=nbc, B2=H)
         check(Lb.evo_attn_long_gate(rows, hc, ptr(O32), ptr(proj, 3 * hc), four, ptr(o), ptr(gm),
                                     stream()), "evo_attn_long_gate")
@@ -304,29 +313,58 @@ def attention_long(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, l
         nbc = min(csz, nb - b0)
         if p_store is None:
             gemm(Mat(proj, sl, 1, sb, D, off=b0 * sb), Mat(proj, sl, 1, sb, D, off=b0 * sb + hc),
-                 Mat(S, L, 1, HLL, L * L), L, L, D, alpha=scale, B1=nbc, B2=H)
+                 Mat(S, ld, 1, HLL, L * ld), L, L, D, alpha=scale, B1=nbc, B2=H)
             Pc, poff, Sp = P, 0, ptr(S)
         else:
             Pc, poff, Sp = p_store, b0 * HLL, None
         # dP[b,h,q,k] = sum_d dO[row(b,q), h*D+d] V[row(b,k), 2hc + h*D + d]
         gemm(Mat(dO, rl * hc, 1, rb * hc, D, off=b0 * rb * hc),
              Mat(proj, sl, 1, sb, D, off=b0 * sb + 2 * hc),
-             Mat(dP, L, 1, HLL, L * L), L, L, D, B1=nbc, B2=H)
-        check(Lb.evo_attn_long_dsoftmax(nbc, H, L, Sp, ptr(dP), ptr(bias), bh, bq, bk,
+             Mat(dP, ld, 1, HLL, L * ld), L, L, D, B1=nbc, B2=H)
+        check(Lb.evo_attn_long_dsoftmax(nbc, H, L, ld, Sp, ptr(dP), ptr(bias), bh, bq, bk,
                                         ptr(lse_f, b0 * H * L), ptr(Dq), b0 * rb, rb, rl,
                                         ptr(Pc, poff), ptr(dS), ptr(dbias), 1 if b0 > 0 else 0,
                                         stream()),
               "evo_attn_long_dsoftmax")
         # dV[row(b,k), 2hc+h*D+d] = sum_q P[b,h,q,k] dO[row(b,q), h*D+d]
-        gemm(Mat(Pc, 1, L, HLL, L * L, off=poff), Mat(dO, 1, rl * hc, rb * hc, D, off=b0 * rb * hc),
+        gemm(Mat(Pc, 1, ld, HLL, L * ld, off=poff),
+             Mat(dO, 1, rl * hc, rb * hc, D, off=b0 * rb * hc),
              Mat(dproj, sl, 1, sb, D, off=b0 * sb + 2 * hc), L, D, L, B1=nbc, B2=H)
         # dQ = scale * dS K ;  dK = scale * dS^T Q
-        gemm(Mat(dS, L, 1, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb + hc),
+        gemm(Mat(dS, ld, 1, HLL, L * ld), Mat(proj, 1, sl, sb, D, off=b0 * sb + hc),
              Mat(dproj, sl, 1, sb, D, off=b0 * sb), L, D, L, alpha=scale, B1=nbc, B2=H)
-        gemm(Mat(dS, 1, L, HLL, L * L), Mat(proj, 1, sl, sb, D, off=b0 * sb),
+        gemm(Mat(dS, 1, ld, HLL, L * ld), Mat(proj, 1, sl, sb, D, off=b0 * sb),
              Mat(dproj, sl, 1, sb, D, off=b0 * sb + hc), L, D, L, alpha=scale, B1=nbc, B2=H)
     if dgate_bias is not None:
         colsum(dproj, rows, hc, dgate_bias, rs=four, off=3 * hc)
+
+
+def _tc_bias_layout_ok(bh, bq, bk, L) -> bool:
+    """The tensor-core attention reads bias rows as 16-byte vectors: plain
+    (bk = 1) or transposed (bq = 1) rows whose strides are multiples of 4,
+    one head's rows tiling its bh span."""
+    if bh < L * max(bq, bk):
+        return False
+    return ((bk == 1 and bq % 4 == 0 and bh % 4 == 0)
+            or (bq == 1 and bk % 4 == 0 and bh % 4 == 0))
+
+
+def _attention_padded_bias(*, bias, bh, bq, bk, dbias=None, L, H, **kw):
+    """Crops with r % 4 != 0: run the tensor-core attention on a plain
+    [H, L, Lp] copy of the bias (Lp = L rounded up to 4) and scatter its
+    gradient back to the caller's layout."""
+    Lp = (L + 3) // 4 * 4
+    dev = bias.device
+    bpad = torch.zeros(H * L * Lp, dtype=torch.float32, device=dev)
+    for hh in range(H):
+        copy2d(bias, L, L, bpad, s_rs=bq, s_cs=bk, d_rs=Lp, s_off=hh * bh, d_off=hh * L * Lp)
+    dpad = (torch.empty(H * L * Lp, dtype=torch.float32, device=dev)
+            if dbias is not None else None)
+    attention(bias=bpad, bh=L * Lp, bq=Lp, bk=1, dbias=dpad, L=L, H=H, **kw)
+    if dbias is not None:
+        for hh in range(H):
+            copy2d(dpad, L, L, dbias, s_rs=Lp, d_rs=bq, d_cs=bk, s_off=hh * L * Lp,
+                   d_off=hh * bh)
 
 
 def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, sb: int,
@@ -340,6 +378,12 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
                               sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,
                               bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj, dbias=dbias,
                               dgate_bias=dgate_bias, p_store=p_store)
+    if (bias is not None and proj.dtype == torch.bfloat16
+            and not _tc_bias_layout_ok(bh, bq, bk, L)):
+        return _attention_padded_bias(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale,
+                                      sb=sb, sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse,
+                                      bias=bias, bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj,
+                                      dbias=dbias, dgate_bias=dgate_bias)
     d = AttnDesc()
     d.dtype = dt(proj)
     d.nb, d.H, d.L, d.D, d.scale = nb, H, L, D, scale
@@ -388,9 +432,19 @@ def trimul_gate_fwd(proj, rows: int, c: int, ldp: int, a_cf, b_cf):
                                     stream()), "evo_trimul_gate_fwd")
 
 
-def trimul_gate_bwd(proj, rows: int, c: int, ldp: int, da_cf, db_cf, dproj, ldd: int):
-    check(lib().evo_trimul_gate_bwd(dt(proj), rows, c, ptr(proj), ldp, ptr(da_cf), ptr(db_cf),
-                                    ptr(dproj), ldd, stream()), "evo_trimul_gate_bwd")
+def trimul_gate_bwd(proj, rows: int, c: int, ldp: int, da_cf, db_cf, dproj, ldd: int,
+                    colsum=None):
+    """dproj[:, :4c] from da/db; colsum (fp32 [4c]) = their column sums taken
+    from the fp32 values (the gate / value bias gradients)."""
+    L = lib()
+    ws = None
+    nbytes = 0
+    if colsum is not None:
+        nbytes = L.evo_trimul_gate_bwd_workspace_bytes(rows, c)
+        ws = _ws(nbytes, dproj.device)
+    check(L.evo_trimul_gate_bwd(dt(proj), rows, c, ptr(proj), ldp, ptr(da_cf), ptr(db_cf),
+                                ptr(dproj), ldd, ptr(colsum), ptr(ws), nbytes, stream()),
+          "evo_trimul_gate_bwd")
 
 
 def outgate_fwd(z, rows: int, cols: int, g, g_rs: int, g_off: int, o, znew):
@@ -399,9 +453,16 @@ def outgate_fwd(z, rows: int, cols: int, g, g_rs: int, g_off: int, o, znew):
 
 
 def outgate_bwd(dz, rows: int, cols: int, g, g_rs: int, g_off: int, o, do_, dgpre,
-                dg_rs: int, dg_off: int):
-    check(lib().evo_outgate_bwd(dt(o), rows, cols, ptr(dz), ptr(g, g_off), g_rs, ptr(o), cols,
-                                ptr(do_), cols, ptr(dgpre, dg_off), dg_rs, stream()),
+                dg_rs: int, dg_off: int, do_colsum=None, dg_colsum=None):
+    L = lib()
+    ws = None
+    nbytes = 0
+    if do_colsum is not None or dg_colsum is not None:
+        nbytes = L.evo_outgate_bwd_workspace_bytes(rows, cols)
+        ws = _ws(nbytes, dz.device)
+    check(L.evo_outgate_bwd(dt(o), rows, cols, ptr(dz), ptr(g, g_off), g_rs, ptr(o), cols,
+                            ptr(do_), cols, ptr(dgpre, dg_off), dg_rs, ptr(do_colsum),
+                            ptr(dg_colsum), ptr(ws), nbytes, stream()),
           "evo_outgate_bwd")
 
 
@@ -428,6 +489,18 @@ def sq_mean(x, out, dx=None):
     ws = torch.empty(4096, dtype=torch.uint8, device=x.device)
     check(lib().evo_sq_mean(x.numel(), ptr(x), ptr(out), ptr(dx), ptr(ws), stream()),
           "evo_sq_mean")
+
+
+def split_bf16(x, rows: int, cols: int, hi, lo, *, x_rs=None, h_rs=None, l_rs=None, hi2=None,
+               h2_rs=None, h_off=0, l_off=0, h2_off=0):
+    """hi = bf16(x), lo = bf16(x - hi) (hi also into hi2), row strides given."""
+    x_rs = cols if x_rs is None else x_rs
+    h_rs = cols if h_rs is None else h_rs
+    l_rs = cols if l_rs is None else l_rs
+    h2_rs = cols if h2_rs is None else h2_rs
+    check(lib().evo_split_bf16(rows, cols, ptr(x), x_rs, ptr(hi, h_off), h_rs, ptr(lo, l_off),
+                               l_rs, ptr(hi2, h2_off) if hi2 is not None else None, h2_rs,
+                               stream()), "evo_split_bf16")
 
 
 def add(a, b, out):

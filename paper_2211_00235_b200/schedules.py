@@ -148,9 +148,10 @@ class StepState:
         return out
 
 
-def full_step(st: StepState, m, z):
+def full_step(st: StepState, m, z, fwd_events=None):
     """Forward + loss + backward of the whole stack on one device.
-    Returns (m_out, z_out, loss_tensor[1], dm, dz, fwd_events)."""
+    Returns (m_out, z_out, loss_tensor[1], dm, dz); fwd_events (two CUDA
+    events) are recorded around the forward when given."""
     cfg, act = st.cfg, st.act
     s, r = cfg.s, cfg.r
     if st.packs is None:
@@ -158,9 +159,13 @@ def full_step(st: StepState, m, z):
     m_c = m.reshape(s * r, cfg.c_m)
     z_c = z.reshape(r * r, cfg.c_z)
     ctxs = []
+    if fwd_events is not None:
+        fwd_events[0].record()
     for blk in range(cfg.n_blocks):
         m_c, z_c, c = E.block_fwd(st.P, blk, st.packs[blk], m_c, z_c, cfg, act)
         ctxs.append(c)
+    if fwd_events is not None:
+        fwd_events[1].record()
     loss = torch.zeros(1, dtype=F32, device=m.device)
     dm = torch.empty_like(m_c)
     dz = torch.empty_like(z_c)
@@ -221,36 +226,18 @@ def composed_step(extra: StepState, main: StepState, m_e, m, z):
 
 def run_single(cfg: EvoConfig, store: ParamStore, seed: int = 32,
                precision: str | None = None) -> RunResult:
-    """Reference step on one GPU (src/schedules.py:387-399)."""
-    if cfg.variant != "parallel":
-        return _run_single_autograd(cfg, store, seed)
+    """Reference step on one GPU (src/schedules.py:387-399), any wiring
+    (parallel / af2 / multimer).  rank_fwd_seconds = the forward's device
+    time (CUDA events), wall_seconds = the whole step."""
     m, z = make_batch(cfg, seed, 1, store.device)[0]
     st = StepState(cfg, store, precision)
     t0 = time.perf_counter()
-    m_out, z_out, loss, dm, dz = full_step(st, m, z)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+    m_out, z_out, loss, dm, dz = full_step(st, m, z, fwd_events=ev)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     return RunResult(m_out, z_out, float(loss.item()), dm, dz, st.grad_dict(), None,
-                     {0: wall}, wall)
-
-
-def _run_single_autograd(cfg, store, seed):
-    """af2 / multimer wirings: composed from the differentiable sub-ops."""
-    from .evoformer import evoformer_stack
-    m, z = make_batch(cfg, seed, 1, store.device)[0]
-    params = {n: t.detach().clone().requires_grad_(True) for n, t in store.items()}
-    m = m.clone().requires_grad_(True)
-    z = z.clone().requires_grad_(True)
-    t0 = time.perf_counter()
-    mo, zo = evoformer_stack(params, m, z, cfg)
-    loss = (mo * mo).mean() + (zo * zo).mean()
-    loss.backward()
-    torch.cuda.synchronize()
-    wall = time.perf_counter() - t0
-    grads = {n: (p.grad if p.grad is not None else torch.zeros_like(p))
-             for n, p in params.items()}
-    return RunResult(mo.detach(), zo.detach(), float(loss.item()), m.grad, z.grad, grads,
-                     None, {0: wall}, wall)
+                     {0: ev[0].elapsed_time(ev[1]) / 1e3}, wall)
 
 
 # ---------------------------------------------------------------------------

@@ -12,6 +12,8 @@ Outputs (committed, small):
                    forward ("madds_block") and the reference's own
                    float32-vs-float64 rel-L2 per field ("f32err:<field>").  run_bp is asserted bitwise
                    equal to run_single before saving.
+  step_<cfg>_<variant>.npz   the same for the af2 and multimer wirings
+                   (toy and c1 dims; no BP check: BP needs the parallel wiring).
   subops_toy.npz   every sub-op of block 0 at the toy dims: forward delta
                    and the VJP of a seeded random cotangent R with respect
                    to m, z and the sub-op's parameters
@@ -39,46 +41,64 @@ CONFIGS = {
 }
 
 
-def main():
-    sys.path.insert(0, REF)
+def step_golden(tag, kw, variant="parallel"):
     from branchpar import tensor as T
     from branchpar import evoformer as E
     from branchpar.schedules import compare_runs, run_bp, run_single
 
-    for tag, kw in CONFIGS.items():
-        cfg = E.EvoConfig(**kw)
-        store = E.init_params(cfg, 32)
-        a = run_single(cfg, store, seed=32)
+    cfg = E.EvoConfig(**kw, variant=variant)
+    store = E.init_params(cfg, 32)
+    a = run_single(cfg, store, seed=32)
+    if variant == "parallel":
         b = run_bp(cfg, store, seed=32)
         assert compare_runs(a, b, rtol=0.0).bitwise, tag
-        g = T.Graph()
-        P = store.bind(g)
-        m, z = E.seeded_inputs(cfg, 32)
-        E.evoformer_block(P, 0, g.leaf(m), g.leaf(z), cfg)
-        out = dict(m_out=a.m_out, z_out=a.z_out, loss=np.float64(a.loss),
-                   dm=a.dm, dz=a.dz, madds_block=np.int64(g.madds))
-        for name, arr in a.grads.items():
-            out[f"grad:{name}"] = arr
-        # the reference's OWN float32 deviation from its float64 run, per
-        # field: the floor any fp32 implementation is measured against
-        f = run_single(cfg, E.init_params(cfg, 32, dtype=np.float32), seed=32)
-        m_in, z_in = E.seeded_inputs(cfg, 32)
+    g = T.Graph()
+    P = store.bind(g)
+    m, z = E.seeded_inputs(cfg, 32)
+    E.evoformer_block(P, 0, g.leaf(m), g.leaf(z), cfg)
+    out = dict(m_out=a.m_out, z_out=a.z_out, loss=np.float64(a.loss),
+               dm=a.dm, dz=a.dz, madds_block=np.int64(g.madds))
+    for name, arr in a.grads.items():
+        out[f"grad:{name}"] = arr
+    # the reference's OWN float32 deviation from its float64 run, per
+    # field: the floor any fp32 implementation is measured against
+    f = run_single(cfg, E.init_params(cfg, 32, dtype=np.float32), seed=32)
+    m_in, z_in = E.seeded_inputs(cfg, 32)
 
-        def rl(x, y):
-            x = np.asarray(x, np.float64)
-            y = np.asarray(y, np.float64)
-            return np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
+    def rl(x, y):
+        x = np.asarray(x, np.float64)
+        y = np.asarray(y, np.float64)
+        return np.linalg.norm(x - y) / max(np.linalg.norm(y), 1e-300)
 
-        m32 = m_in.astype(np.float32).astype(np.float64)
-        z32 = z_in.astype(np.float32).astype(np.float64)
-        out["f32err:m_delta"] = rl(f.m_out.astype(np.float64) - m32, a.m_out - m_in)
-        out["f32err:z_delta"] = rl(f.z_out.astype(np.float64) - z32, a.z_out - z_in)
-        out["f32err:dm"] = rl(f.dm, a.dm)
-        out["f32err:dz"] = rl(f.dz, a.dz)
-        for name in a.grads:
-            out[f"f32err:grad:{name}"] = rl(f.grads[name], a.grads[name])
-        np.savez_compressed(os.path.join(HERE, f"step_{tag}.npz"), **out)
-        print(tag, "saved", len(out), "arrays; madds/block", g.madds)
+    m32 = m_in.astype(np.float32).astype(np.float64)
+    z32 = z_in.astype(np.float32).astype(np.float64)
+    out["f32err:m_delta"] = rl(f.m_out.astype(np.float64) - m32, a.m_out - m_in)
+    out["f32err:z_delta"] = rl(f.z_out.astype(np.float64) - z32, a.z_out - z_in)
+    out["f32err:dm"] = rl(f.dm, a.dm)
+    out["f32err:dz"] = rl(f.dz, a.dz)
+    for name in a.grads:
+        out[f"f32err:grad:{name}"] = rl(f.grads[name], a.grads[name])
+    name = f"step_{tag}.npz" if variant == "parallel" else f"step_{tag}_{variant}.npz"
+    np.savez_compressed(os.path.join(HERE, name), **out)
+    print(name, "saved", len(out), "arrays; madds/block", g.madds)
+
+
+def main():
+    sys.path.insert(0, REF)
+    from branchpar import tensor as T
+    from branchpar import evoformer as E
+
+    only = sys.argv[1:]
+    for tag, kw in CONFIGS.items():
+        if not only or tag in only:
+            step_golden(tag, kw)
+    # the af2 and multimer wirings (src/evoformer.py:448-455), SURVEY.md 8(f)
+    for tag in ("toy", "c1"):
+        for variant in ("af2", "multimer"):
+            if not only or f"{tag}_{variant}" in only:
+                step_golden(tag, CONFIGS[tag], variant)
+    if only and "subops" not in only:
+        return
 
     cfg = E.EvoConfig(**CONFIGS["toy"])
     store = E.init_params(cfg, 32)

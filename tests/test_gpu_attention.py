@@ -49,6 +49,8 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=Fals
                bh=bh, bq=bq, bk=bk)
     if keep_p:
         geo["p_store"] = torch.empty(K.long_p_elems(nb, H, L), device="cuda", dtype=dtype)
+    from paper_2211_00235_b200 import _native
+    before = _native.backend_counts()
     K.attention(**geo)
     dgm = torch.randn(rows, hc, device="cuda").to(dtype)
     dproj = torch.zeros(rows, 4 * hc, device="cuda", dtype=dtype)
@@ -56,6 +58,18 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=Fals
     dgb = torch.empty(hc, device="cuda") if gate_bias else None
     K.attention(**geo, dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=dgb)
     torch.cuda.synchronize()
+    after = _native.backend_counts()
+    # which engine ran: the fused tcgen05 kernels, the GEMM-composed long-key
+    # path (tcgen05 GEMMs) or the SIMT kernels (fp32 parity path)
+    d_tc = after["attn_tc"] - before["attn_tc"]
+    d_simt = after["attn_simt"] - before["attn_simt"]
+    d_gemm = after["gemm_tc"] - before["gemm_tc"]
+    if dtype == torch.float32:
+        assert (d_tc, d_simt) == (0, 2), (d_tc, d_simt)
+    elif K.use_long(dtype, L, D):
+        assert (d_tc, d_simt) == (0, 0) and d_gemm >= 6, (d_tc, d_simt, d_gemm)
+    else:
+        assert (d_tc, d_simt) == (2, 0), (d_tc, d_simt)
 
     # ---- torch fp32 reference on the same (rounded) inputs
     pf = proj.float()
@@ -162,5 +176,20 @@ def test_attention_long_keys(K, case, dtype, tol):
 def test_attention_long_keys_forward_p_kept(K, case):
     """The engine's long-key path: the forward keeps P for the backward."""
     errs = run_case(K, *case, dtype=torch.bfloat16, gate_bias=True, keep_p=True)
+    bad = {k: v for k, v in errs.items() if v > 1.5e-2}
+    assert not bad, errs
+
+
+@pytest.mark.parametrize("case", [(7, 384, 2, 32, False, "plain"),
+                                  (5, 384, 2, 32, True, "transposed"),
+                                  (10, 320, 2, 16, True, "none")])
+@pytest.mark.parametrize("keep_p", [False, True])
+def test_attention_long_keys_multi_chunk(K, case, keep_p, monkeypatch):
+    """The long-key path's batch-row chunk loop: chunks of 3 rows (uneven
+    last chunk), so dbias accumulates across chunks and the P / lse / Dq
+    offsets advance."""
+    nb, L, H = case[0], case[1], case[2]
+    monkeypatch.setattr(K, "LONG_CHUNK_ELEMS", 3 * H * L * L)
+    errs = run_case(K, *case, dtype=torch.bfloat16, gate_bias=True, keep_p=keep_p)
     bad = {k: v for k, v in errs.items() if v > 1.5e-2}
     assert not bad, errs

@@ -1,13 +1,14 @@
 """C3 composition: an extra-MSA stack (its own EvoConfig,
 more sequences, narrower c_e, c_head = c_e / h) whose pair output feeds the
 main stack, fwd+bwd on the native path vs the pinned oracle composition
-(oracle.evoformer_np.composed_step).  Bars: rel-L2 <= 1e-5 fp32 for every field; bf16 <= 2e-2 for the outputs,
-dm, dz, dm_e and every main-stack gradient.  The extra stack's parameter
-gradients on the bf16 path get 6e-2: its MSA output is dropped, so its MSA
-track is trained only through the outer-product-mean coupling and each of
-those gradients is a small, cancellation-heavy sum of bf16-rounded products
-(measured worst 5.3e-2, extra msa_transition.ln_b at these toy dims, while
-the same tensors agree to 1e-5 on the fp32 path through the same kernels).
+(oracle.evoformer_np.composed_step).  Bars: rel-L2 <= 1e-5 fp32 and <= 2e-2
+bf16 for the outputs, dm, dz, dm_e and every parameter gradient of both
+stacks.  (The extra stack's MSA track is trained only through the outer
+product mean, so its transition gradients are small, cancellation-heavy
+column sums; with plain bf16 operands the ReLU mask flips on near-zero
+pre-activations and those gradients sit at 5e-2 -- the same as the oracle
+with bf16-rounded matmul operands.  The bf16 path therefore runs the
+transitions' first projection as a 3-product bf16 GEMM, engine.transition_fwd.)
 """
 
 import numpy as np
@@ -32,7 +33,7 @@ def _grad_errs(got, want, prefix):
 
 
 @pytest.mark.parametrize("precision,tol,tol_extra",
-                         [("fp32", 1e-5, 1e-5), ("bf16", 2e-2, 6e-2)])
+                         [("fp32", 1e-5, 1e-5), ("bf16", 2e-2, 2e-2)])
 def test_extra_stack_feeds_main_stack(precision, tol, tol_extra):
     import paper_2211_00235_b200 as pkg
     from paper_2211_00235_b200 import schedules as S

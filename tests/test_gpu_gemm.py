@@ -37,11 +37,31 @@ def make_operand(rows, k, kmajor, batch=1, dtype=torch.bfloat16):
 @pytest.mark.parametrize("force_simt", [False, True])
 @pytest.mark.parametrize("out", [torch.float32, torch.bfloat16])
 def test_gemm_majors_and_ragged(K, a_k, b_k, M, N, Kd, force_simt, out):
+    from paper_2211_00235_b200 import _native
     A, Af, ars, acs, _ = make_operand(M, Kd, a_k)
     B, Bf, brs, bcs, _ = make_operand(N, Kd, b_k)
     C = torch.empty(M, N, device="cuda", dtype=out)
-    K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd,
-           force_simt=force_simt)
+
+    def call():
+        K.gemm(K.Mat(A, ars, acs), K.Mat(B, brs, bcs), K.Mat(C, N, 1), M, N, Kd,
+               force_simt=force_simt)
+
+    # the tensor-core kernel takes 16-byte-aligned K-major rows (K % 8 == 0)
+    # or MN-major columns (rows % 8 == 0); the rest is SIMT-only
+    tc_ok = ((Kd % 8 == 0) if a_k else (M % 8 == 0)) and ((Kd % 8 == 0) if b_k else (N % 8 == 0))
+    if force_simt:
+        call()
+        assert _native.last_backend() == "gemm_simt"
+    elif tc_ok:
+        call()
+        assert _native.last_backend() == "gemm_tc"
+    else:
+        # strict tensor-core mode (the default) refuses the SIMT fallback
+        with pytest.raises(RuntimeError, match="strict tensor-core"):
+            call()
+        with _native.strict_tc(False):
+            call()
+        assert _native.last_backend() == "gemm_simt"
     want = Af[0] @ Bf[0].T
     assert rel(C.float(), want) < (1e-5 if out == torch.float32 else 4e-3)
 
@@ -124,13 +144,12 @@ def test_gemm_tc_path_is_taken(K):
     A = torch.randn(512, 256, device="cuda").to(torch.bfloat16)
     B = torch.randn(256, 256, device="cuda").to(torch.bfloat16)
     C = torch.empty(512, 256, device="cuda")
-    prof = []
-    K.PROFILE = prof
-    try:
-        K.gemm(K.Mat(A, 256, 1), K.Mat(B, 256, 1), K.Mat(C, 256, 1), 512, 256, 256)
-    finally:
-        K.PROFILE = None
+    before = _native.backend_counts()
+    K.gemm(K.Mat(A, 256, 1), K.Mat(B, 256, 1), K.Mat(C, 256, 1), 512, 256, 256)
+    after = _native.backend_counts()
     torch.cuda.synchronize()
+    assert after["gemm_tc"] == before["gemm_tc"] + 1
+    assert after["gemm_simt"] == before["gemm_simt"]
     assert rel(C, A.float() @ B.float().T) < 1e-5
 
 
@@ -173,9 +192,26 @@ def test_gemm_skinny_tall_k(K, dtype, M, N, Kd, nb, a_k, b_k):
     """Weight gradients of the narrow layers: tiny M*N, K = r*r rows."""
     A, Af, ars, acs, abs_ = make_operand(M, Kd, a_k, nb, dtype=dtype)
     B, Bf, brs, bcs, bbs = make_operand(N, Kd, b_k, nb, dtype=dtype)
+    from paper_2211_00235_b200 import _native
     C = torch.empty(nb, M, N, device="cuda")
-    K.gemm(K.Mat(A, ars, acs, bs1=abs_), K.Mat(B, brs, bcs, bs1=bbs), K.Mat(C, N, 1, bs1=M * N),
-           M, N, Kd, B1=nb)
+
+    def call():
+        K.gemm(K.Mat(A, ars, acs, bs1=abs_), K.Mat(B, brs, bcs, bs1=bbs),
+               K.Mat(C, N, 1, bs1=M * N), M, N, Kd, B1=nb)
+
+    if dtype == torch.bfloat16 and a_k and not b_k:
+        # K-major wide operand with a 12-wide MN-major narrow one: neither the
+        # streaming tall-K kernel nor the tensor-core maps take this layout
+        # (the product never forms it); strict mode refuses the SIMT fallback
+        with pytest.raises(RuntimeError, match="strict tensor-core"):
+            call()
+        with _native.strict_tc(False):
+            call()
+        assert _native.last_backend() == "gemm_simt"
+    else:
+        call()
+        if dtype == torch.bfloat16:
+            assert _native.last_backend() in ("gemm_skinny", "gemm_tc")
     want = torch.stack([Af[i].double() @ Bf[i].double().T for i in range(nb)])
     # fp32 accumulation over K >= 8192 terms (tensor-core or SIMT partials)
     assert rel(C, want) < 5e-5

@@ -107,7 +107,7 @@ def test_relu_bwd_and_sq_mean(K):
 
 @pytest.mark.parametrize("rows,h", [(4096, 8), (1004, 4)])
 def test_layernorm_pair_bias_projection_fused(K, rows, h):
-    """LN(z) + bias = LN(z) Wb and its backward, fused vs unfused kernels."""
+    """Backward of LN(z) followed by bias = LN(z) Wb, fused vs unfused kernels."""
     torch.manual_seed(2)
     cols = 128
     bf = torch.bfloat16
@@ -115,18 +115,11 @@ def test_layernorm_pair_bias_projection_fused(K, rows, h):
     g = torch.randn(cols, device="cuda")
     b = torch.randn(cols, device="cuda")
     Wb = (torch.randn(cols, h, device="cuda") * 0.1).to(bf)
-    # unfused reference path
+    # forward LayerNorm (its statistics feed the fused backward)
     y0 = torch.empty(rows, cols, device="cuda", dtype=bf)
     mu0, rs0 = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
     K.layernorm(x, rows, cols, g, b, y0, mu0, rs0, 1e-5)
-    bias0 = y0.float() @ Wb.float()                       # [rows, h]
-    # fused
-    y = torch.empty(rows, cols, device="cuda", dtype=bf)
-    mu, rs = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
-    bias = torch.empty(h, rows, device="cuda")
-    K.layernorm_proj(x, rows, g, b, y, mu, rs, 1e-5, Wb, h, bias, rows)
-    assert torch.equal(y, y0) and torch.equal(mu, mu0) and torch.equal(rs, rs0)
-    assert rel(bias, bias0.T) < 1e-5
+    mu, rs = mu0, rs0
     # backward: dz = LN_bwd(dy + dbias Wb^T), dWb = y^T dbias
     dy = torch.randn(rows, cols, device="cuda")
     dbias = torch.randn(h, rows, device="cuda")

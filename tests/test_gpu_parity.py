@@ -46,11 +46,19 @@ def test_step_fp32_matches_reference_golden(pkg, tag):
     assert abs(res.loss - float(gold["loss"])) <= 1e-5 * abs(float(gold["loss"]))
 
 
-def _oracle_step(tag):
-    from oracle import evoformer_np as O
-    d = O.Dims(**CONFIGS[tag])
-    P = O.init_params(d, 32)
-    return O.run_single(d, P, seed=32)
+_ORACLE = {}
+
+
+def _oracle_step(tag, **over):
+    """The pinned oracle's step (float64), cached per configuration."""
+    key = (tag, tuple(sorted(over.items())))
+    if key not in _ORACLE:
+        from oracle import evoformer_np as O
+        d = O.Dims(**{**CONFIGS[tag], **over})
+        P = O.init_params(d, 32)
+        _ORACLE.clear()       # keep at most one large oracle result alive
+        _ORACLE[key] = O.run_single(d, P, seed=32)
+    return _ORACLE[key]
 
 
 @pytest.mark.parametrize("precision,tol", [("fp32", FP32_TOL), ("bf16", BF16_TOL)])
@@ -89,6 +97,130 @@ def test_step_af2_bf16_matches_oracle(pkg):
     errs = step_errors(res, want, m_in, z_in, bar=BF16_TOL)
     k, v = _worst(errs)
     assert v <= BF16_TOL, f"worst {k} rel-L2 {v:.3e}"
+
+
+def test_step_af2_fp32_matches_oracle(pkg):
+    """C2 on the fp32 parity path (SIMT FFMA kernels) at the 1e-5 bar; the
+    output deltas get the fp32 storage floor rule (helpers.quant_floor)."""
+    cfg = pkg.EvoConfig(**CONFIGS["af2"])
+    store = pkg.init_params(cfg, 32)
+    res = pkg.run_single(cfg, store, seed=32, precision="fp32")
+    want = _oracle_step("af2")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, want, m_in, z_in, bar=FP32_TOL)
+    k, v = _worst(errs)
+    assert v <= FP32_TOL, f"worst {k} rel-L2 {v:.3e}"
+
+
+def test_step_crop384_bf16_matches_oracle(pkg):
+    """C5 r = 384 (s = 128, AF2 widths): the row and triangle attentions
+    attend over 384 keys (long-key path), bf16 vs the float64 oracle."""
+    from paper_2211_00235_b200 import _native
+    cfg = pkg.EvoConfig(**{**CONFIGS["af2"], "r": 384})
+    store = pkg.init_params(cfg, 32)
+    b0 = _native.backend_counts()
+    res = pkg.run_single(cfg, store, seed=32, precision="bf16")
+    b1 = _native.backend_counts()
+    assert b1["gemm_simt"] == b0["gemm_simt"] and b1["attn_simt"] == b0["attn_simt"]
+    want = _oracle_step("af2", r=384)
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, want, m_in, z_in, bar=BF16_TOL)
+    k, v = _worst(errs)
+    assert v <= BF16_TOL, f"worst {k} rel-L2 {v:.3e}"
+
+
+@pytest.mark.parametrize("tag", ["toy", "c1"])
+@pytest.mark.parametrize("variant", ["af2", "multimer"])
+def test_variant_step_fp32_matches_reference_golden(pkg, tag, variant):
+    """The af2 and multimer wirings (src/evoformer.py:448-455) on the native
+    path vs the reference's own step."""
+    cfg = pkg.EvoConfig(**CONFIGS[tag], variant=variant)
+    store = pkg.init_params(cfg, 32)
+    res = pkg.run_single(cfg, store, seed=32, precision="fp32")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    gold = load_golden(f"{tag}_{variant}")
+    want = golden_as_want(gold)
+    errs = normalise_by_reference_f32(step_errors(res, want, m_in, z_in, bar=FP32_TOL), want,
+                                      FP32_TOL)
+    k, v = _worst(errs)
+    assert v <= FP32_TOL, f"{tag}/{variant}: worst {k} rel-L2 {v:.3e}"
+    assert abs(res.loss - float(gold["loss"])) <= 1e-5 * abs(float(gold["loss"]))
+
+
+@pytest.mark.parametrize("variant", ["af2", "multimer"])
+def test_variant_step_bf16(pkg, variant):
+    """bf16 wirings: c1 vs the reference golden, mid vs the oracle."""
+    cfg = pkg.EvoConfig(**CONFIGS["c1"], variant=variant)
+    res = pkg.run_single(cfg, pkg.init_params(cfg, 32), seed=32, precision="bf16")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, golden_as_want(load_golden(f"c1_{variant}")), m_in, z_in,
+                       bar=BF16_TOL)
+    k, v = _worst(errs)
+    assert v <= BF16_TOL, f"c1/{variant}: worst {k} rel-L2 {v:.3e}"
+    cfg = pkg.EvoConfig(**CONFIGS["mid"], variant=variant)
+    res = pkg.run_single(cfg, pkg.init_params(cfg, 32), seed=32, precision="bf16")
+    m_in, z_in = pkg.make_batch(cfg, 32, 1)[0]
+    errs = step_errors(res, _oracle_step("mid", variant=variant), m_in, z_in, bar=BF16_TOL)
+    k, v = _worst(errs)
+    assert v <= BF16_TOL, f"mid/{variant}: worst {k} rel-L2 {v:.3e}"
+
+
+def test_bp_rejects_serial_wirings(pkg):
+    from paper_2211_00235_b200.schedules import ParallelLayout
+    for variant in ("af2", "multimer"):
+        cfg = pkg.EvoConfig(**CONFIGS["toy"], variant=variant)
+        with pytest.raises(pkg.ConfigError):
+            ParallelLayout(bp=2).validate_model(cfg)
+
+
+@pytest.mark.parametrize("precision,tol", [("fp32", 1e-5), ("bf16", 2e-2)])
+def test_tracks_autograd_match_oracle(pkg, precision, tol):
+    """msa_track / pair_track (src/evoformer.py:427-443) as native autograd
+    functions: outputs and the VJP of a random cotangent vs the oracle."""
+    import numpy as np
+    from oracle import evoformer_np as O
+    tag = "toy" if precision == "fp32" else "mid"
+    pkg.set_precision(precision)
+    try:
+        cfg = pkg.EvoConfig(**CONFIGS[tag])
+        store = pkg.init_params(cfg, 32)
+        d = O.Dims(**CONFIGS[tag])
+        Pn = O.init_params(d, 32)
+        rng = np.random.default_rng(7)
+        m0 = rng.standard_normal((cfg.s, cfg.r, cfg.c_m)).astype(np.float32)
+        z0 = rng.standard_normal((cfg.r, cfg.r, cfg.c_z)).astype(np.float32)
+        Rm = rng.standard_normal(m0.shape)
+        Rz = rng.standard_normal(z0.shape)
+        # oracle
+        cm, cp = {}, {}
+        mo = O._msa_track_fwd(Pn, 0, m0.astype(np.float64), z0.astype(np.float64), d, cm)
+        zo = O._pair_track_fwd(Pn, 0, z0.astype(np.float64), d, cp)
+        G = O.Grads()
+        dm_w, dz_row = O._msa_track_vjp(Rm, cm, Pn, 0, d, G)
+        dz_w = O._pair_track_vjp(Rz, cp, Pn, 0, d, G) + dz_row
+        # native
+        P = {n: t.clone().requires_grad_(True) for n, t in store.items()}
+        m = torch.tensor(m0, device="cuda", requires_grad=True)
+        z = torch.tensor(z0, device="cuda", requires_grad=True)
+        mt = pkg.msa_track(P, 0, m, z, cfg)
+        zt = pkg.pair_track(P, 0, z, cfg)
+        ((mt * torch.tensor(Rm, device="cuda", dtype=torch.float32)).sum()
+         + (zt * torch.tensor(Rz, device="cuda", dtype=torch.float32)).sum()).backward()
+        # outputs (the deltas only for bf16: fp32 storage of m + delta floors
+        # the delta's rel-L2 near 1e-5 at these dims, helpers.quant_floor)
+        if precision == "fp32":
+            assert rel_l2(mt, mo) <= tol and rel_l2(zt, zo) <= tol
+        else:
+            assert rel_l2(mt - m, mo - m0) <= tol
+            assert rel_l2(zt - z, zo - z0) <= tol
+        assert rel_l2(m.grad, dm_w) <= tol
+        assert rel_l2(z.grad, dz_w) <= tol
+        for n, g in G.items():
+            if n.endswith("lnz_b") or np.linalg.norm(g) < 1e-15:
+                continue
+            assert rel_l2(P[n].grad, g) <= tol, n
+    finally:
+        pkg.set_precision("fp32")
 
 
 def test_step_c1_bf16_matches_reference(pkg):

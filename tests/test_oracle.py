@@ -32,9 +32,13 @@ def load(name):
     return np.load(os.path.join(GOLD, name))
 
 
-@pytest.mark.parametrize("tag", list(CONFIGS))
+VARIANT_TAGS = ["toy_af2", "toy_multimer", "c1_af2", "c1_multimer"]
+
+
+@pytest.mark.parametrize("tag", list(CONFIGS) + VARIANT_TAGS)
 def test_step_matches_reference_golden(tag):
-    d = O.Dims(**CONFIGS[tag])
+    base, _, variant = tag.partition("_")
+    d = O.Dims(**CONFIGS[base], variant=variant or "parallel")
     P = O.init_params(d, 32)
     res = O.run_single(d, P, seed=32)
     gold = load(f"step_{tag}.npz")

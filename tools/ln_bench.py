@@ -59,11 +59,6 @@ def main():
                          rows * cols * 6 + rows * 8)
     cases["fwd_f32"] = (lambda: K.layernorm(x, rows, cols, g, b, y, mu, rs, 1e-5),
                         rows * cols * 8 + rows * 8)
-    cases["fwd_proj"] = (lambda: K.layernorm_proj(x, rows, g, b, yb, mu, rs, 1e-5, Wb, h, pb, rows),
-                         rows * cols * 6 + rows * 8 + h * rows * 4)
-    cases["fwd_proj_noy"] = (lambda: K.layernorm_proj(x, rows, g, b, None, mu, rs, 1e-5, Wb, h, pb,
-                                                      rows),
-                             rows * cols * 4 + rows * 8 + h * rows * 4)
     cases["fwd_rowdot"] = (lambda: K.gemm(Mat(yb, cols, 1), Mat(Wb, 1, h), Mat(pb, 1, rows), rows, h,
                                           cols),
                            rows * cols * 2 + h * rows * 4)
