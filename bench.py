@@ -168,6 +168,71 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------
+# BP=2 prediction from one GPU: the two branches timed separately
+# ---------------------------------------------------------------------------
+
+NVLINK_GBS = 750.0   # assumed achievable NVLink 5 bandwidth per direction (900 nominal)
+
+
+def bp2_prediction(cfg, store, precision, dev, bp1_block_ms, reps=20):
+    """Per block: the MSA branch (row / column attention, MSA transition,
+    outer product mean; fwd + bwd) and the pair branch (triangle updates,
+    triangle attentions, pair transition; fwd + bwd) each replayed as a CUDA
+    graph and timed with events, plus the block's four fp32 Z-sized BP
+    messages (fwd: o, z''; bwd: dz'', the dz_in allreduce) at NVLINK_GBS.
+    BP=2 block time = max(branches) + exchange (src/schedules.py:214-297:
+    the exchange is not overlapped)."""
+    import torch
+    from paper_2211_00235_b200 import distributed as D
+    ex = D.CudaExec(cfg, store, precision, dev)
+    ex.pack("all")
+    s, r = cfg.s, cfg.r
+    g = torch.Generator(device=dev).manual_seed(0)
+    m = torch.randn(s * r, cfg.c_m, device=dev, generator=g)
+    z = torch.randn(r * r, cfg.c_z, device=dev, generator=g)
+    dm = torch.randn(s * r, cfg.c_m, device=dev, generator=g) * 1e-3
+    dz = torch.randn(r * r, cfg.c_z, device=dev, generator=g) * 1e-3
+
+    def msa():
+        _, _, ctx = ex.msa_fwd(0, m, z)
+        ex.msa_bwd(0, ctx, dm, dz)
+
+    def pair():
+        _, ctx = ex.pair_fwd(0, z)
+        ex.pair_bwd(0, ctx, dz)
+
+    out = {}
+    for name, fn in (("msa_branch_ms", msa), ("pair_branch_ms", pair)):
+        fn()
+        torch.cuda.synchronize()
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            fn()
+        graph.replay()
+        torch.cuda.synchronize()
+        e0 = torch.cuda.Event(enable_timing=True)
+        e1 = torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(reps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+        out[name] = e0.elapsed_time(e1) / reps
+        del graph
+    zbytes = r * r * cfg.c_z * 4
+    exch_ms = 4 * zbytes / (NVLINK_GBS * 1e9) * 1e3
+    bp2 = max(out["msa_branch_ms"], out["pair_branch_ms"]) + exch_ms
+    out.update(bp1_block_ms=bp1_block_ms, exchange_bytes_per_block=4 * zbytes,
+               exchange_ms_at_assumed_nvlink=exch_ms, assumed_nvlink_gbs=NVLINK_GBS,
+               predicted_bp2_block_ms=bp2, predicted_bp2_speedup=bp1_block_ms / bp2,
+               paper_bp2_speedup="1.37-1.39x (PAPER.md, UniFold/PPFold on A100)",
+               method="each branch's fwd+bwd of one block replayed as a CUDA graph on this "
+                      "GPU; BP=2 block = max(branches) + 4 fp32 Z messages at the assumed "
+                      "NVLink rate")
+    return out
+
+
+# ---------------------------------------------------------------------------
 # native arm
 # ---------------------------------------------------------------------------
 
@@ -199,8 +264,12 @@ def run_native(args):
     layout = S.ParallelLayout(dp=dp, bp=bp)
     runner = None
     if world > 1:
+        # BP=2 x DP (or DP only): each compute segment between two collectives
+        # replays as a CUDA graph (distributed.GraphedExec); the collectives
+        # are host-issued NCCL calls
         from paper_2211_00235_b200 import distributed as D
-        runner = D.DistributedStep(cfg, store, layout, precision=args.precision)
+        runner = D.DistributedStep(cfg, store, layout, precision=args.precision,
+                                   graphs=args.graph)
     else:
         st = S.StepState(cfg, store, args.precision, dev)
         st.pack()
@@ -210,47 +279,27 @@ def run_native(args):
     m_d, z_d = m_h.to(dev), z_h.to(dev)
     loss_h = torch.empty(1, dtype=torch.float32).pin_memory()
 
-    def step(m, z):
+    def step_eager(m, z):
         if runner is not None:
             return runner.step(m, z)
         return S.full_step(st, m, z)
 
-    # warm-up (also first-touch allocations)
+    # warm-up (first-touch allocations; for N > 1 the first two steps are the
+    # eager warm-up and the segment capture)
     for _ in range(args.warmup):
-        step(m_d, z_d)
+        step_eager(m_d, z_d)
     torch.cuda.synchronize()
 
-    use_graph = args.graph and world == 1
-    graph = graph_e2e = None
-    if use_graph:
-        # one step captured as a CUDA graph (all native launches go to the
-        # capturing stream); inputs are static device buffers
-        m_s, z_s = m_d.clone(), z_d.clone()
-        side = torch.cuda.Stream()
-        side.wait_stream(torch.cuda.current_stream())
-        with torch.cuda.stream(side):
-            step(m_s, z_s)
-        torch.cuda.current_stream().wait_stream(side)
-        graph = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(graph):
-            step(m_s, z_s)
-        # end-to-end: two input buffer sets, one graph each (step + loss D2H);
-        # the H2D of step i+1's inputs runs on a copy stream while step i
-        # computes (a double-buffered input pipeline)
-        graph_e2e = []
-        e2e_in = []
-        for _ in range(2):
-            mb, zb = m_d.clone(), z_d.clone()
-            g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                out_e = step(mb, zb)
-                loss_h.copy_(out_e[2].reshape(1), non_blocking=True)
-            graph_e2e.append(g)
-            e2e_in.append((mb, zb))
-        graph.replay()
-        for g in graph_e2e:
-            g.replay()
-        torch.cuda.synchronize()
+    use_graph = args.graph
+    gs = None
+    if use_graph and runner is None:
+        # one train step captured as a CUDA graph by the package
+        # (StepState.capture), two slots with their own static inputs for the
+        # double-buffered end-to-end input pipeline
+        gs = st.capture(m_d, z_d, warmup=0, slots=2)
+        step_graph = lambda: gs.step(*gs.inputs(0), slot=0)
+    else:
+        step_graph = lambda: step_eager(m_d, z_d)
 
     def timed(fn, k):
         if world > 1:
@@ -276,10 +325,7 @@ def run_native(args):
     clocks = Clocks(local)
     clocks.start()
     time.sleep(0.3)
-    if use_graph:
-        ms = timed(graph.replay, args.steps)
-    else:
-        ms = timed(lambda: step(m_d, z_d), args.steps)
+    ms = timed(step_graph, args.steps)
     clk = clocks.stop()
 
     # kernel-family breakdown: CUDA events around every GEMM / attention
@@ -289,7 +335,7 @@ def run_native(args):
     shapes = [] if args.detail else None
     K.PROFILE_SHAPES = shapes
     n0 = _native.launch_count()
-    ms_eager = timed(lambda: step(m_d, z_d), args.steps)
+    ms_eager = timed(lambda: step_eager(m_d, z_d), args.steps)
     launches = _native.launch_count() - n0
     K.PROFILE = None
     K.PROFILE_SHAPES = None
@@ -314,12 +360,14 @@ def run_native(args):
 
     # end-to-end: pinned host inputs -> device, step, loss -> host, every step
     def e2e_eager():
-        m_e = m_h.to(dev, non_blocking=True)
-        z_e = z_h.to(dev, non_blocking=True)
-        out = step(m_e, z_e)
+        m_d.copy_(m_h, non_blocking=True)
+        z_d.copy_(z_h, non_blocking=True)
+        out = step_graph() if runner is not None else step_eager(m_d, z_d)
         loss_h.copy_(out[2].reshape(1), non_blocking=True)
 
     def e2e_pipelined(k):
+        # the H2D of step i+1 runs on a copy stream into the other graph slot's
+        # static inputs while step i computes (double-buffered input pipeline)
         comp = torch.cuda.current_stream()
         copy = torch.cuda.Stream()
         h2d = [torch.cuda.Event() for _ in range(2)]
@@ -334,9 +382,9 @@ def run_native(args):
             with torch.cuda.stream(copy):
                 if i >= 2:
                     copy.wait_event(free[i % 2])  # step i-2 done with this buffer set
-                mb, zb = e2e_in[i % 2]
-                mb.copy_(m_h, non_blocking=True)
-                zb.copy_(z_h, non_blocking=True)
+                mb, zb = gs.inputs(i % 2)
+                mb.copy_(m_h.view(mb.shape), non_blocking=True)
+                zb.copy_(z_h.view(zb.shape), non_blocking=True)
                 h2d[i % 2].record(copy)
 
         load(0)
@@ -344,27 +392,28 @@ def run_native(args):
             if i + 1 < k:
                 load(i + 1)
             comp.wait_event(h2d[i % 2])
-            graph_e2e[i % 2].replay()
+            out = gs.step(*gs.inputs(i % 2), slot=i % 2)
+            loss_h.copy_(out[2].reshape(1), non_blocking=True)
             free[i % 2].record(comp)
         a1.record(comp)
         torch.cuda.synchronize()
         return a0.elapsed_time(a1) / k
 
-    if use_graph:
+    if gs is not None:
         e2e_pipelined(2)
         ms_e2e = e2e_pipelined(args.steps)
         e2e_mode = "double-buffered H2D on a copy stream overlapping the previous step"
     else:
         ms_e2e = timed(e2e_eager, args.steps)
-        e2e_mode = "serial H2D -> step -> D2H"
+        e2e_mode = "serial H2D -> step -> loss D2H"
 
     # roofline timing: one step's launches of each kernel family re-issued
     # back to back inside a CUDA graph (device time, no host gaps)
     fam_graph = {}
-    if use_graph:
+    if use_graph and runner is None:
         rec = []
         K.RECORD = rec
-        step(m_d, z_d)
+        step_eager(m_d, z_d)
         K.RECORD = None
         torch.cuda.synchronize()
         for famname in sorted({r[0] for r in rec}):
@@ -441,6 +490,9 @@ def run_native(args):
                          "(oracle/evoformer_np.py, numpy fp32, all host cores); "
                          f"block time = sum = {t_cpu:.1f} s"}
     h2d = (m_h.numel() + z_h.numel()) * 4
+    bp2 = None
+    if world == 1 and not args.no_bp2:
+        bp2 = bp2_prediction(cfg, store, args.precision, dev, ms / cfg.n_blocks)
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -457,9 +509,11 @@ def run_native(args):
                 "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": 4, "ms_per_step": ms_e2e,
                 "mode": e2e_mode},
         "gpu_launches": launches, "gpu_launches_per_step": launches / args.steps,
-        "launch_mode": "cuda_graph" if use_graph else "eager", "ms_per_step_eager": ms_eager,
+        "launch_mode": ("cuda_graph" if runner is None else "cuda_graph_segments")
+        if use_graph else "eager", "ms_per_step_eager": ms_eager,
         "clocks": clk,
         "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+        "bp2_prediction": bp2,
     }
     print(json.dumps(line))
     if world > 1:
@@ -579,6 +633,8 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-bp2", action="store_true",
+                    help="skip the one-GPU BP=2 branch-split prediction")
     ap.add_argument("--detail", action="store_true", help="per-call GEMM/attention table on stderr")
     args = ap.parse_args()
     if args.impl == "reference":

@@ -302,6 +302,10 @@ EVO_API int evo_sq_mean(int64_t n, const float *x, float *out, float *dx,
 EVO_API int evo_add(int64_t n, const float *a, const float *b, float *out,
             void *stream);
 
+/* out = x / d (fp32, n elements; out may alias x): the division by dp of the
+ * DP gradient mean (src/schedules.py:324-328).                           */
+EVO_API int evo_div_scalar(int64_t n, const float *x, float d, float *out, void *stream);
+
 /* Split an fp32 [rows, cols] operand into bf16 hi = bf16(x) and
  * lo = bf16(x - hi) (hi also to hi2 when non-NULL), element strides per row.
  * Used for the 3-product bf16 GEMM (A3 = [hi | lo | hi], W3 = [W_hi; W_hi;

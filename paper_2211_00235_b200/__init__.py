@@ -10,7 +10,7 @@ from .evoformer import (EvoConfig, ParamStore, col_attn, evoformer_block, evofor
                         pair_track, pair_transition, param_count, row_attn, seeded_inputs,
                         set_precision, tri_attn, tri_mult)
 from .schedules import (ParallelLayout, RunResult, compare_runs, expected_comm_volume,
-                        make_batch, run_single)
-from .distributed import run_bp, run_distributed, run_dp
+                        make_batch, run_single, trace_volume)
+from .distributed import CommRecord, CommTrace, run_bp, run_dap, run_distributed, run_dp
 
 __version__ = "0.1.0"

@@ -93,6 +93,7 @@ _SIGS = {
     "evo_relu_bwd": (c_i32, [c_i32, c_i64, c_vp, c_vp, c_vp, c_vp]),
     "evo_sq_mean": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp, c_vp]),
     "evo_add": (c_i32, [c_i64, c_vp, c_vp, c_vp, c_vp]),
+    "evo_div_scalar": (c_i32, [c_i64, c_vp, c_f32, c_vp, c_vp]),
     "evo_split_bf16": (c_i32, [c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp, c_i64,
                                c_vp]),
     "evo_last_error": (C.c_char_p, []),

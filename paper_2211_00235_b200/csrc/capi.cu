@@ -70,6 +70,7 @@ int relu_bwd_colsum(int64_t, int64_t, const void *, const void *, void *, float 
                     cudaStream_t);
 int sq_mean(int64_t, const float *, float *, float *, void *, cudaStream_t);
 int add(int64_t, const float *, const float *, float *, cudaStream_t);
+int div_scalar(int64_t, const float *, float, float *, cudaStream_t);
 int split_bf16(int64_t, int64_t, const float *, int64_t, void *, int64_t, void *, int64_t, void *,
                int64_t, cudaStream_t);
 
@@ -404,6 +405,12 @@ int evo_add(int64_t n, const float *a, const float *b, float *out, void *stream)
   if (n == 0) return EVO_OK;
   CHECK_PTR(a); CHECK_PTR(b); CHECK_PTR(out);
   return add(n, a, b, out, as_stream(stream));
+}
+
+int evo_div_scalar(int64_t n, const float *x, float d, float *out, void *stream) {
+  if (n == 0) return EVO_OK;
+  CHECK_PTR(x); CHECK_PTR(out);
+  return div_scalar(n, x, d, out, as_stream(stream));
 }
 
 int evo_split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *hi,

@@ -597,6 +597,12 @@ __global__ void add_kernel(int64_t n, const float *a, const float *b, float *o) 
     o[e] = a[e] + b[e];
 }
 
+__global__ void div_scalar_kernel(int64_t n, const float *x, float d, float *o) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
+       e += (int64_t)gridDim.x * blockDim.x)
+    o[e] = x[e] / d;
+}
+
 }  // namespace
 
 // ------------------------------------------------------------------ API impl
@@ -899,6 +905,12 @@ int split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *h
       rows, cols, x, x_rs, reinterpret_cast<bf16 *>(hi), h_rs, reinterpret_cast<bf16 *>(lo), l_rs,
       reinterpret_cast<bf16 *>(hi2), h2_rs);
   EVO_LAUNCHED("split_bf16_kernel");
+  return EVO_OK;
+}
+
+int div_scalar(int64_t n, const float *x, float d, float *o, cudaStream_t st) {
+  div_scalar_kernel<<<ew_blocks(n), 256, 0, st>>>(n, x, d, o);
+  EVO_LAUNCHED("div_scalar_kernel");
   return EVO_OK;
 }
 

@@ -26,8 +26,9 @@ and run the same schedule under the gloo backend).
 
 from __future__ import annotations
 
+import os
 import time
-from dataclasses import dataclass, field
+from dataclasses import dataclass
 
 import torch
 import torch.distributed as dist
@@ -38,8 +39,11 @@ from .schedules import ParallelLayout, RunResult, make_batch
 F32 = torch.float32
 
 
-@dataclass
+@dataclass(frozen=True)
 class CommRecord:
+    """One completed collective (src/comm.py:41-50)."""
+
+    seq: int
     kind: str
     group: tuple
     src: int | None
@@ -48,9 +52,69 @@ class CommRecord:
     phase: str
 
 
+PHASES = ("fwd", "bwd", "param")
+
+
+class CommTrace:
+    """Log of the world's collectives, one record per collective (src/comm.py:52-110):
+    ``records``, ``canonical()``, ``totals()``, ``by_phase()``, ``to_csv()``,
+    ``csv_text()``.  Built by ``Comm.world_trace()`` from every rank's log
+    (each collective counted once, by the lowest rank of its group)."""
+
+    def __init__(self, records=()):
+        self.records: list[CommRecord] = []
+        self._order: list[int] = []
+        for r in records:
+            self.add(r.kind, r.group, r.src, r.elements, r.bytes, r.phase)
+
+    def add(self, kind, group, src, elements, nbytes, phase) -> None:
+        group = tuple(group)
+        idx = sum(1 for r in self.records if r.group == group)
+        self.records.append(CommRecord(len(self.records), kind, group, src, int(elements),
+                                       int(nbytes), phase))
+        self._order.append(idx)
+
+    def canonical(self) -> list:
+        """Records ordered by (group, issue order within the group)."""
+        pairs = sorted(zip(self.records, self._order), key=lambda p: (p[0].group, p[1]))
+        return [r for r, _ in pairs]
+
+    def totals(self, phase: str | None = None, kind: str | None = None):
+        """(count, elements, bytes) over matching records."""
+        n = el = by = 0
+        for r in self.records:
+            if (phase is None or r.phase == phase) and (kind is None or r.kind == kind):
+                n, el, by = n + 1, el + r.elements, by + r.bytes
+        return n, el, by
+
+    def by_phase(self) -> dict:
+        return {p: self.totals(phase=p) for p in PHASES}
+
+    def to_csv(self, target) -> None:
+        import csv
+        own = isinstance(target, (str, os.PathLike))
+        fh = open(target, "w", newline="") if own else target
+        try:
+            w = csv.writer(fh)
+            w.writerow(["seq", "kind", "group", "src", "elements", "bytes", "phase"])
+            for r in self.canonical():
+                w.writerow([r.seq, r.kind, "|".join(map(str, r.group)),
+                            "" if r.src is None else r.src, r.elements, r.bytes, r.phase])
+        finally:
+            if own:
+                fh.close()
+
+    def csv_text(self) -> str:
+        import io
+        buf = io.StringIO()
+        self.to_csv(buf)
+        return buf.getvalue()
+
+
 class Comm:
-    """Collectives over the BP-pair and DP groups of a layout, with a
-    trace of every call (the CommTrace equivalent, src/comm.py:41-110)."""
+    """Collectives over the BP-pair and DP groups of a layout, with a log of
+    every call this rank joined (``trace``; ``world_trace()`` merges the
+    ranks' logs into the reference's world-level CommTrace)."""
 
     def __init__(self, layout: ParallelLayout, rank: int | None = None):
         if not dist.is_initialized():
@@ -73,7 +137,9 @@ class Comm:
         self.trace: list[CommRecord] = []
 
     def _rec(self, kind, group, src, t, phase):
-        self.trace.append(CommRecord(kind, tuple(group), src, int(t.numel()),
+        if phase is None:       # result assembly: not part of the step's ledger
+            return
+        self.trace.append(CommRecord(len(self.trace), kind, tuple(group), src, int(t.numel()),
                                      int(t.numel() * t.element_size()), phase))
 
     def broadcast(self, group, src, t, phase):
@@ -87,6 +153,18 @@ class Comm:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.groups[tuple(group)])
         self._rec("allreduce_sum", group, None, t, phase)
         return t
+
+    def world_trace(self) -> CommTrace:
+        """Every rank's records of the groups it leads (lowest rank), merged
+        in rank order: one record per collective of the world."""
+        mine = [r for r in self.trace if r.group[0] == self.rank]
+        every = [None] * dist.get_world_size()
+        dist.all_gather_object(every, mine)
+        out = CommTrace()
+        for recs in every:
+            for r in recs:
+                out.add(r.kind, r.group, r.src, r.elements, r.bytes, r.phase)
+        return out
 
     def volume(self, world_reduce=True) -> dict:
         """{(phase, kind): (count, elements)} over the whole world (summed over
@@ -157,6 +235,9 @@ class CudaExec:
         self.K.add(a, b, out)
         return out
 
+    def div_scalar(self, x, d):
+        self.K.div_scalar(x, float(d), x)
+
     def msa_bwd(self, blk, ctx, dm, d_o):
         E, st = self.E, self.st
         ctxs, co = ctx
@@ -172,9 +253,9 @@ class CudaExec:
         return E.pair_branch_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctx, dz,
                                  self.cfg, self.act, dz_act=E.cast_act(dz, self.act))
 
-    def full_step(self, m, z):
+    def full_step(self, m, z, ev=None):
         from .schedules import full_step
-        return full_step(self.st, m, z)
+        return full_step(self.st, m, z, fwd_events=ev)
 
     def sq_mean(self, x):
         loss = torch.zeros(1, dtype=F32, device=self.dev)
@@ -183,13 +264,55 @@ class CudaExec:
         return loss, dx
 
 
-def bp_msa_step(ex, comm, m, z, K_blocks, zshape_numel):
-    """Rank bp_i = 0 (src/schedules.py:214-258).  Returns dict."""
+class GraphedExec:
+    """Executor wrapper that replays each compute segment of the BP / DP
+    schedule (a branch forward, a branch backward, the join add, the loss)
+    as a CUDA graph (schedules.SegmentGraphs); the collectives between the
+    segments stay host-issued (NCCL / gloo).  The first step runs eagerly
+    (warm-up), the second captures, later steps replay."""
+
+    COMPUTE = ("msa_fwd", "pair_fwd", "add", "msa_bwd", "pair_bwd", "sq_mean", "full_step")
+
+    def __init__(self, ex):
+        from .schedules import SegmentGraphs
+        self.ex = ex
+        self.seg = SegmentGraphs()
+        self.steps = 0
+
+    def __getattr__(self, name):
+        fn = getattr(self.ex, name)
+        if name not in self.COMPUTE:
+            return fn
+        if self.steps == 0:
+            return fn
+        counter = self._count.setdefault(name, 0)
+        self._count[name] = counter + 1
+
+        def call(*args):
+            return self.seg((name, counter), fn, *args)
+        return call
+
+    def begin_step(self):
+        self._count = {}
+
+    def end_step(self):
+        self.steps += 1
+
+
+def _mark(ev, i):
+    if ev is not None:
+        ev[i].record()
+
+
+def bp_msa_step(ex, comm, m, z, K_blocks, zshape_numel, ev=None):
+    """Rank bp_i = 0 (src/schedules.py:214-258).  Returns dict.  ev: two
+    CUDA events recorded around the forward (rank_fwd_seconds)."""
     pair = comm.pair
     r0, r1 = pair
     z_cur = z
     ctxs = []
     m_cur = m
+    _mark(ev, 0)
     for blk in range(K_blocks):
         m_cur, o, ctx = ex.msa_fwd(blk, m_cur, z_cur)
         ctxs.append(ctx)
@@ -197,6 +320,7 @@ def bp_msa_step(ex, comm, m, z, K_blocks, zshape_numel):
         z_next = torch.empty_like(z_cur)
         comm.broadcast(pair, r1, z_next, "fwd")
         z_cur = z_next
+    _mark(ev, 1)
     loss_m, dm = ex.sq_mean(m_cur)
     for blk in reversed(range(K_blocks)):
         d_o = torch.empty_like(z_cur)
@@ -208,12 +332,13 @@ def bp_msa_step(ex, comm, m, z, K_blocks, zshape_numel):
     return dict(m_out=m_cur, z_out=z_cur, loss=loss_m, dm=dm, dz=dz_row)
 
 
-def bp_pair_step(ex, comm, z, K_blocks, mshape):
+def bp_pair_step(ex, comm, z, K_blocks, mshape, ev=None):
     """Rank bp_i = 1 (src/schedules.py:261-297)."""
     pair = comm.pair
     r0, r1 = pair
     z_cur = z
     ctxs = []
+    _mark(ev, 0)
     for blk in range(K_blocks):
         z_b, ctx = ex.pair_fwd(blk, z_cur)
         ctxs.append(ctx)
@@ -221,6 +346,7 @@ def bp_pair_step(ex, comm, z, K_blocks, mshape):
         comm.broadcast(pair, r0, o, "fwd")
         z_cur = ex.add(z_b, o)                     # z'' = z_pair + o (:276-280)
         comm.broadcast(pair, r1, z_cur, "fwd")
+    _mark(ev, 1)
     loss_z, dz = ex.sq_mean(z_cur)
     for blk in reversed(range(K_blocks)):
         comm.broadcast(pair, r1, dz, "bwd")        # dz'' -> seeds o on rank 0
@@ -247,69 +373,100 @@ def sync_param_grads(ex, comm, K_blocks):
             for br in ("msa", "pair"):
                 g = ex.grad_bank(blk, br)
                 comm.allreduce_sum(comm.dpg, g, "param")
-                g.div_(lay.dp)
+                ex.div_scalar(g, lay.dp)
 
 
 class DistributedStep:
     """One train step of the (dp, bp) layout on this rank's GPU."""
 
     def __init__(self, cfg, store, layout: ParallelLayout, precision=None, comm=None,
-                 executor=None):
+                 executor=None, graphs: bool = False):
         layout.validate_model(cfg)
         self.cfg, self.layout = cfg, layout
         self.comm = comm or Comm(layout)
         self.rank = self.comm.rank
         self.dp_i, self.bp_i, _ = layout.coords(self.rank)
         self.ex = executor or CudaExec(cfg, store, precision)
+        if graphs:
+            self.ex = GraphedExec(self.ex)
         if layout.bp == 2:
             self.ex.pack("msa" if self.bp_i == 0 else "pair")
         else:
             self.ex.pack("all")
 
-    def step(self, m, z):
+    def step(self, m, z, ev=None):
         """m [s, r, c_m], z [r, r, c_z] on this rank's device.  Returns the
         tuple (m_out, z_out, loss, dm, dz) of fields this rank owns (others
-        None); parameter gradients are left synchronised in the executor."""
+        None); parameter gradients are left synchronised in the executor.
+        ev: optional two CUDA events recorded around the forward."""
         cfg, lay, ex = self.cfg, self.layout, self.ex
         s, r = cfg.s, cfg.r
         m2 = m.reshape(s * r, cfg.c_m)
         z2 = z.reshape(r * r, cfg.c_z)
+        graphed = isinstance(ex, GraphedExec)
+        if graphed:
+            ex.begin_step()
+            if ex.steps > 0:
+                ev = None      # events are not recorded inside the graphs
+        try:
+            return self._step(ex, cfg, lay, s, r, m, z, m2, z2, ev)
+        finally:
+            if graphed:
+                ex.end_step()
+
+    def _step(self, ex, cfg, lay, s, r, m, z, m2, z2, ev):
         if lay.bp == 1:
-            out = ex.full_step(m, z)
+            out = ex.full_step(m, z, ev) if ev is not None else ex.full_step(m, z)
             sync_param_grads(ex, self.comm, cfg.n_blocks)
             return out
         if self.bp_i == 0:
-            res = bp_msa_step(ex, self.comm, m2, z2, cfg.n_blocks, None)
+            res = bp_msa_step(ex, self.comm, m2, z2, cfg.n_blocks, None, ev)
             out = (res["m_out"].reshape(s, r, cfg.c_m), None, res["loss"],
                    res["dm"].reshape(s, r, cfg.c_m), None)
         else:
-            res = bp_pair_step(ex, self.comm, z2, cfg.n_blocks, (s * r, cfg.c_m))
+            res = bp_pair_step(ex, self.comm, z2, cfg.n_blocks, (s * r, cfg.c_m), ev)
             out = (None, res["z_out"].reshape(r, r, cfg.c_z), res["loss"], None,
                    res["dz"].reshape(r, r, cfg.c_z))
         sync_param_grads(ex, self.comm, cfg.n_blocks)
         return out
 
 
-def run_distributed(cfg, store, layout: ParallelLayout, seed: int = 32, precision=None,
-                    comm=None, executor=None) -> RunResult:
-    """SPMD train step under `layout` (src/schedules.py:332-384).  Call on
-    every rank of an initialised process group.  The returned RunResult
-    carries the dp_idx = 0 replica's outputs and input gradients (gathered
-    within its BP pair) on every rank of that replica, the dp-mean loss, and
-    the synchronised parameter gradients."""
+def run_distributed(cfg, store, layout: ParallelLayout, seed: int = 32,
+                    max_threads: int | None = None, *, precision=None, comm=None,
+                    executor=None) -> RunResult:
+    """SPMD train step under `layout` (src/schedules.py:332-384).
+
+    Inside an initialised process group (torchrun, one rank per GPU) call it
+    on every rank.  Without one it launches the world itself, like the
+    reference (src/schedules.py:338-361): layout.world_size processes, rank r
+    on cuda:(r % device_count), NCCL when every rank has its own GPU and gloo
+    otherwise; the RunResult comes back to the caller.  max_threads is the
+    reference's thread cap for its simulated world and has no effect here.
+
+    The RunResult carries the dp_idx = 0 replica's outputs and input
+    gradients (gathered within its BP pair), the dp-mean loss, the
+    synchronised parameter gradients, the world's CommTrace (one record per
+    collective of the step, src/comm.py:52-110) and each rank's forward
+    device time in rank_fwd_seconds."""
     layout.validate_model(cfg)
+    if comm is None and executor is None and not dist.is_initialized():
+        return _spawn_world(cfg, store, layout, seed, precision)
     runner = DistributedStep(cfg, store, layout, precision, comm, executor)
     dev = runner.ex.dev
     samples = make_batch(cfg, seed, layout.dp, device=dev)
     m, z = samples[runner.dp_i]
+    ev = ([torch.cuda.Event(enable_timing=True) for _ in range(2)]
+          if dev.type == "cuda" else None)
     t0 = time.perf_counter()
-    m_out, z_out, loss, dm, dz = runner.step(m, z)
-    # replica loss = loss_m + loss_z (pair), then mean over dp
-    lt = loss.reshape(1).to(torch.float64)
+    m_out, z_out, loss, dm, dz = runner.step(m, z, ev)
+    # replica loss = loss_m + loss_z in the loss dtype (the BP=1 step adds the
+    # two means into one fp32 accumulator in the same order: bitwise equal),
+    # then the mean over dp
+    lt = loss.reshape(1).clone()
     if layout.bp == 2:
-        runner.comm.allreduce_sum(runner.comm.pair, lt, "result")
+        runner.comm.allreduce_sum(runner.comm.pair, lt, None)
     if layout.dp > 1:
-        runner.comm.allreduce_sum(runner.comm.dpg, lt, "result")
+        runner.comm.allreduce_sum(runner.comm.dpg, lt, None)
         lt /= layout.dp
     if layout.bp == 2:
         # complete the pair's view: rank0 owns m_out/dm, rank1 z_out/dz
@@ -321,18 +478,105 @@ def run_distributed(cfg, store, layout: ParallelLayout, seed: int = 32, precisio
             m_out_t, dm_t = torch.empty_like(m), torch.empty_like(m)
             z_out_t, dz_t = z_out.contiguous(), dz.contiguous()
         for t, src in ((m_out_t, r0), (dm_t, r0), (z_out_t, r1), (dz_t, r1)):
-            runner.comm.broadcast(runner.comm.pair, src, t, "result")
+            runner.comm.broadcast(runner.comm.pair, src, t, None)
         m_out, dm, z_out, dz = m_out_t, dm_t, z_out_t, dz_t
     if dev.type == "cuda":
         torch.cuda.synchronize(dev)
     wall = time.perf_counter() - t0
+    fwd = ev[0].elapsed_time(ev[1]) / 1e3 if ev is not None else float("nan")
+    every = [None] * dist.get_world_size()
+    dist.all_gather_object(every, fwd)
     return RunResult(m_out, z_out, float(lt.item()), dm, dz, runner.ex.grad_dict(),
-                     runner.comm.trace, None, wall)
+                     runner.comm.world_trace(), dict(enumerate(every)), wall)
 
 
-def run_bp(cfg, store, seed: int = 32, precision=None) -> RunResult:
-    return run_distributed(cfg, store, ParallelLayout(bp=2), seed, precision)
+def run_bp(cfg, store, seed: int = 32, max_threads=None, *, precision=None) -> RunResult:
+    """Branch parallelism, BP=2 (src/schedules.py:402-403)."""
+    return run_distributed(cfg, store, ParallelLayout(bp=2), seed, max_threads,
+                           precision=precision)
 
 
-def run_dp(cfg, store, dp: int, seed: int = 32, precision=None) -> RunResult:
-    return run_distributed(cfg, store, ParallelLayout(dp=dp), seed, precision)
+def run_dp(cfg, store, dp: int, seed: int = 32, max_threads=None, *, precision=None) -> RunResult:
+    """Data parallelism over dp replicas (src/schedules.py:410-411)."""
+    return run_distributed(cfg, store, ParallelLayout(dp=dp), seed, max_threads,
+                           precision=precision)
+
+
+def run_dap(cfg, store, dap: int, seed: int = 32, max_threads=None, *, precision=None):
+    """DAP axial sharding (src/schedules.py:406-407): outside this build's
+    scope; raises ConfigError via ParallelLayout."""
+    return run_distributed(cfg, store, ParallelLayout(dap=dap), seed, max_threads,
+                           precision=precision)
+
+
+# ---------------------------------------------------------------------------
+# self-launched world (no process group yet): the reference's World.run
+# ---------------------------------------------------------------------------
+
+def _world_main(rank, world, init_file, backend, cfg, store_np, layout, seed, precision, q):
+    import traceback
+    try:
+        ndev = torch.cuda.device_count()
+        dev = torch.device("cuda", rank % ndev)
+        torch.cuda.set_device(dev)
+        kw = dict(backend=backend, init_method=f"file://{init_file}", rank=rank,
+                  world_size=world)
+        if backend == "nccl":
+            kw["device_id"] = dev
+        dist.init_process_group(**kw)
+        try:
+            from .evoformer import ParamStore
+            store = ParamStore()
+            for name, (arr, branch) in store_np.items():
+                store.add(name, torch.as_tensor(arr, device=dev), branch)
+            res = run_distributed(cfg, store, layout, seed, precision=precision)
+            if rank == 0:
+                q.put(("ok", rank, res.numpy()))
+            else:
+                q.put(("ok", rank, None))
+        finally:
+            dist.destroy_process_group()
+    except Exception:  # pragma: no cover - reported to the parent
+        q.put(("err", rank, traceback.format_exc()))
+
+
+def _spawn_world(cfg, store, layout, seed, precision):
+    import tempfile
+    import torch.multiprocessing as mp
+    world = layout.world_size
+    if not torch.cuda.is_available():
+        raise WorldError("run_distributed needs CUDA devices (the native kernels)")
+    ndev = torch.cuda.device_count()
+    backend = "nccl" if ndev >= world else "gloo"
+    store_np = {n: (t.detach().cpu().numpy(), store.branch(n)) for n, t in store.items()}
+    fd, init_file = tempfile.mkstemp(prefix="evo_world_")
+    os.close(fd)
+    os.unlink(init_file)
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_world_main, args=(r, world, init_file, backend, cfg, store_np,
+                                                   layout, seed, precision, q))
+             for r in range(world)]
+    t0 = time.perf_counter()
+    for p in procs:
+        p.start()
+    result, errors = None, []
+    for _ in range(world):
+        status, rank, payload = q.get()
+        if status == "ok" and rank == 0:
+            result = payload
+        elif status == "err":
+            errors.append(f"rank {rank}:\n{payload}")
+    for p in procs:
+        p.join(timeout=120)
+    if os.path.exists(init_file):
+        os.unlink(init_file)
+    if errors or result is None:
+        raise WorldError("self-launched world failed:\n" + "\n".join(errors))
+    dev = store.device
+
+    def back(x):
+        return torch.as_tensor(x, device=dev)
+    return RunResult(back(result.m_out), back(result.z_out), result.loss, back(result.dm),
+                     back(result.dz), {k: back(v) for k, v in result.grads.items()},
+                     result.trace, result.rank_fwd_seconds, time.perf_counter() - t0)

@@ -503,6 +503,11 @@ def split_bf16(x, rows: int, cols: int, hi, lo, *, x_rs=None, h_rs=None, l_rs=No
                                stream()), "evo_split_bf16")
 
 
+def div_scalar(x, d: float, out):
+    """out = x / d (fp32, contiguous; in place when out is x)."""
+    check(lib().evo_div_scalar(x.numel(), ptr(x), d, ptr(out), stream()), "evo_div_scalar")
+
+
 def add(a, b, out):
     check(lib().evo_add(a.numel(), ptr(a), ptr(b), ptr(out), stream()), "evo_add")
 

@@ -147,6 +147,95 @@ class StepState:
             out.update(bg.names)
         return out
 
+    def capture(self, m, z, warmup: int = 1, slots: int = 1) -> "GraphedStep":
+        """The step as a CUDA graph (one per slot): `warmup` eager steps
+        (first-touch allocations, kernel attributes), then capture on (m, z).
+        Replay with the returned object's ``step(m, z, slot)``."""
+        if self.packs is None:
+            self.pack()
+        for _ in range(warmup):
+            full_step(self, m, z)
+        torch.cuda.synchronize()
+        gs = GraphedStep(self)
+        for slot in range(slots):
+            gs.step(m, z, slot)
+        torch.cuda.synchronize()
+        return gs
+
+
+def _tensors_of(x, out=None):
+    out = [] if out is None else out
+    if isinstance(x, torch.Tensor):
+        out.append(x)
+    elif isinstance(x, (tuple, list)):
+        for v in x:
+            _tensors_of(v, out)
+    elif isinstance(x, dict):
+        for v in x.values():
+            _tensors_of(v, out)
+    return out
+
+
+class SegmentGraphs:
+    """CUDA graphs of the native launch sequences between two host-side
+    events (collectives, or a whole step).  The first call of a key captures
+    ``fn`` on static copies of its tensor arguments and replays it; later
+    calls copy arguments whose storage changed into those buffers and
+    replay.  Segment outputs are static buffers, rewritten by the next replay
+    of the same key.  All segments share one memory pool, so a step must
+    replay its segments in the order they were captured (the BP / DP
+    schedules issue the same sequence every step).  Arguments that are
+    outputs of an earlier segment are used in place (no copy)."""
+
+    def __init__(self):
+        self.graphs = {}
+        self.pool = None
+        self.static = set()
+
+    def __call__(self, key, fn, *args):
+        tens = [a for a in args if isinstance(a, torch.Tensor)]
+        ent = self.graphs.get(key)
+        if ent is None:
+            sin = [t if t.data_ptr() in self.static else t.clone() for t in tens]
+            it = iter(sin)
+            cargs = [next(it) if isinstance(a, torch.Tensor) else a for a in args]
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g, pool=self.pool):
+                out = fn(*cargs)
+            if self.pool is None:
+                self.pool = g.pool()
+            for t in _tensors_of(out):
+                self.static.add(t.data_ptr())
+            ent = (g, sin, out)
+            self.graphs[key] = ent
+        g, sin, out = ent
+        for s_, t in zip(sin, tens):
+            if s_.data_ptr() != t.data_ptr():
+                s_.copy_(t)
+        g.replay()
+        return out
+
+
+class GraphedStep:
+    """A BP=1 train step replayed as one CUDA graph (StepState.capture):
+    ``step(m, z, slot)`` -> (m_out, z_out, loss[1], dm, dz) as static
+    buffers (valid until the next call).  Each slot is one captured graph
+    with its own static inputs (``inputs(slot)``), so a caller can stage the
+    next step's inputs into one slot while the other computes.  Parameter
+    gradients land in the StepState's gradient banks as in the eager step."""
+
+    def __init__(self, st: "StepState"):
+        self.st = st
+        self.seg = SegmentGraphs()
+
+    def step(self, m, z, slot: int = 0):
+        return self.seg(("step", slot), lambda a, b: full_step(self.st, a, b), m, z)
+
+    def inputs(self, slot: int = 0):
+        """The static (m, z) device buffers of a slot: write inputs there
+        and call step() with them to skip the input copy."""
+        return tuple(self.seg.graphs[("step", slot)][1])
+
 
 def full_step(st: StepState, m, z, fwd_events=None):
     """Forward + loss + backward of the whole stack on one device.
@@ -361,4 +450,14 @@ def expected_comm_volume(cfg: EvoConfig, layout: ParallelLayout) -> dict:
         g = layout.bp
         n = (MSA_PARAM_TENSORS + PAIR_PARAM_TENSORS) * Kb
         bump("param", "allreduce_sum", n * g, (msa + pair) * g)
+    return out
+
+
+def trace_volume(trace) -> dict:
+    """Same shape as expected_comm_volume, read off a recorded CommTrace
+    (src/schedules.py:575-581)."""
+    out = {}
+    for r in trace.records:
+        c0, e0 = out.get((r.phase, r.kind), (0, 0))
+        out[(r.phase, r.kind)] = (c0 + 1, e0 + r.elements)
     return out

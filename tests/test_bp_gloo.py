@@ -93,6 +93,9 @@ class OracleExec:
     def add(self, a, b):
         return a + b
 
+    def div_scalar(self, x, d):
+        x.div_(d)
+
     def msa_bwd(self, blk, caches, dm, d_o):
         d, P = self.d, self.P
         G = O.Grads()
@@ -117,7 +120,7 @@ class OracleExec:
         self._fill(blk, "pair", G)
         return torch.from_numpy(dzn.reshape(d.r * d.r, d.c_z))
 
-    def full_step(self, m, z):
+    def full_step(self, m, z, ev=None):
         res = O.train_step(self.P, m.numpy(), z.numpy(), self.d)
         for blk in range(self.d.n_blocks):
             self._fill(blk, "msa", res["grads"])
@@ -162,8 +165,9 @@ def _worker(rank, world, port, dp, bp, out_q):
         m, z = samples[runner.dp_i]
         res = runner.step(torch.from_numpy(m), torch.from_numpy(z))
         vol = comm.volume()
+        tv = S.trace_volume(comm.world_trace())   # world-level CommTrace
         out_q.put((rank, [None if t is None else t.numpy().copy() for t in res],
-                   ex.grad_dict(), vol))
+                   ex.grad_dict(), (vol, tv)))
     finally:
         dist.destroy_process_group()
 
@@ -177,7 +181,8 @@ def _run(world, dp, bp):
         p.start()
     outs = {}
     for _ in range(world):
-        rank, fields, grads, vol = q.get(timeout=240)
+        rank, fields, grads, (vol, tv) = q.get(timeout=240)
+        assert tv == vol, (tv, vol)
         outs[rank] = (fields, grads, vol)
     for p in procs:
         p.join(timeout=60)
