@@ -299,6 +299,95 @@ class GraphedExec:
         self.steps += 1
 
 
+class ComposedExec:
+    """Executor over the C3 composition (schedules.composed_step):
+    global block b < K_e is block b of the extra-MSA stack (its own EvoConfig),
+    b >= K_e block b - K_e of the main stack.  At the boundary the MSA branch
+    drops the extra stack's m_e' and starts the main stack on its own m; in
+    the backward the main stack's input gradient dm is kept (``dm_main``) and
+    the extra stack's MSA backward is seeded with dm_e' = 0 (the loss reads
+    only the main outputs).  The pair stream z runs through both stacks."""
+
+    def __init__(self, ex_extra, ex_main, m_main):
+        self.e, self.m, self.m_main = ex_extra, ex_main, m_main
+        self.Ke = ex_extra.cfg.n_blocks
+        self.dev = ex_main.dev
+        self.dm_main = None
+
+    def _pick(self, blk):
+        return (self.e, blk) if blk < self.Ke else (self.m, blk - self.Ke)
+
+    def pack(self, branch):
+        self.e.pack(branch)
+        self.m.pack(branch)
+
+    def grad_bank(self, blk, branch):
+        ex, b = self._pick(blk)
+        return ex.grad_bank(b, branch)
+
+    def msa_fwd(self, blk, m, z):
+        ex, b = self._pick(blk)
+        if blk == self.Ke:
+            m = self.m_main      # the extra stack's m_e' is dropped
+        return ex.msa_fwd(b, m, z)
+
+    def pair_fwd(self, blk, z):
+        ex, b = self._pick(blk)
+        return ex.pair_fwd(b, z)
+
+    def msa_bwd(self, blk, ctx, dm, d_o):
+        ex, b = self._pick(blk)
+        dm_in, dz_row = ex.msa_bwd(b, ctx, dm, d_o)
+        if blk == self.Ke:
+            self.dm_main = dm_in
+            cfg = self.e.cfg
+            dm_in = torch.zeros(cfg.s * cfg.r, cfg.c_m, dtype=F32, device=self.dev)
+        return dm_in, dz_row
+
+    def pair_bwd(self, blk, ctx, dz):
+        ex, b = self._pick(blk)
+        return ex.pair_bwd(b, ctx, dz)
+
+    def add(self, a, b):
+        return self.m.add(a, b)
+
+    def sq_mean(self, x):
+        return self.m.sq_mean(x)
+
+    def div_scalar(self, x, d):
+        self.m.div_scalar(x, d)
+
+
+def composed_bp_step(ex_extra, ex_main, comm, m_e, m, z):
+    """C3 under branch parallelism (BP=2 in the pair ``comm.pair``): the
+    extra-MSA stack feeding the main stack through the same per-block
+    schedule as bp_msa_step / bp_pair_step, K_e + K_m blocks.  Call on both
+    ranks of the pair; returns (m_out, z_out, loss, dm_e, dm, dz) with the
+    fields this rank owns (rank bp 0: m_out, dm_e, dm; rank bp 1: z_out, dz;
+    the loss is the rank's half, loss_m or loss_z), and leaves both stacks'
+    parameter gradients owner-broadcast over the pair."""
+    ce, cm = ex_extra.cfg, ex_main.cfg
+    if (ce.r, ce.c_z) != (cm.r, cm.c_z):
+        raise ConfigError(f"extra stack (r={ce.r}, c_z={ce.c_z}) does not feed the main "
+                          f"stack (r={cm.r}, c_z={cm.c_z})")
+    bp_i = comm.layout.coords(comm.rank)[1]
+    ex = ComposedExec(ex_extra, ex_main, m.reshape(cm.s * cm.r, cm.c_m))
+    ex.pack("msa" if bp_i == 0 else "pair")
+    Kt = ce.n_blocks + cm.n_blocks
+    z2 = z.reshape(cm.r * cm.r, cm.c_z)
+    if bp_i == 0:
+        res = bp_msa_step(ex, comm, m_e.reshape(ce.s * ce.r, ce.c_m), z2, Kt, None)
+        out = (res["m_out"].reshape(cm.s, cm.r, cm.c_m), None, res["loss"],
+               res["dm"].reshape(ce.s, ce.r, ce.c_m), ex.dm_main.reshape(cm.s, cm.r, cm.c_m),
+               None)
+    else:
+        res = bp_pair_step(ex, comm, z2, Kt, (ce.s * ce.r, ce.c_m))
+        out = (None, res["z_out"].reshape(cm.r, cm.r, cm.c_z), res["loss"], None, None,
+               res["dz"].reshape(cm.r, cm.r, cm.c_z))
+    sync_param_grads(ex, comm, Kt)
+    return out
+
+
 def _mark(ev, i):
     if ev is not None:
         ev[i].record()

@@ -178,3 +178,79 @@ def test_graphed_single_step_matches_eager(pkg):
             assert torch.equal(a, b)
         for k, v in st.grad_dict().items():
             assert torch.equal(v, g_eager[k]), k
+
+
+EXTRA = dict(s=64, r=64, c_m=32, c_z=32, h=4, c_opm=16, t_factor=4, n_blocks=2)
+MAIN = dict(s=32, r=64, c_m=64, c_z=32, h=4, c_opm=16, t_factor=4, n_blocks=1)
+
+
+def _c3_inputs(cfg_e, cfg_m):
+    rng = np.random.default_rng(32)
+    return [torch.as_tensor(rng.standard_normal(shape).astype(np.float32), device="cuda")
+            for shape in ((cfg_e.s, cfg_e.r, cfg_e.c_m), (cfg_m.s, cfg_m.r, cfg_m.c_m),
+                          (cfg_m.r, cfg_m.r, cfg_m.c_z))]
+
+
+def _c3_worker(rank, init_file, precision, q):
+    import traceback
+    import torch.distributed as dist
+    try:
+        torch.cuda.set_device(0)
+        dist.init_process_group("gloo", init_method=f"file://{init_file}", rank=rank,
+                                world_size=2)
+        import paper_2211_00235_b200 as pkg
+        from paper_2211_00235_b200 import distributed as D
+        ce, cm = pkg.EvoConfig(**EXTRA), pkg.EvoConfig(**MAIN)
+        lay = pkg.ParallelLayout(bp=2)
+        comm = D.Comm(lay)
+        ex_e = D.CudaExec(ce, pkg.init_params(ce, 33, device="cuda:0"), precision)
+        ex_m = D.CudaExec(cm, pkg.init_params(cm, 32, device="cuda:0"), precision)
+        out = D.composed_bp_step(ex_e, ex_m, comm, *_c3_inputs(ce, cm))
+        torch.cuda.synchronize()
+        grads = {**{"extra." + k: v.cpu().numpy() for k, v in ex_e.grad_dict().items()},
+                 **{"main." + k: v.cpu().numpy() for k, v in ex_m.grad_dict().items()}}
+        q.put(("ok", rank, [None if t is None else t.float().cpu().numpy() for t in out], grads))
+        dist.destroy_process_group()
+    except Exception:
+        q.put(("err", rank, traceback.format_exc(), None))
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_c3_composed_stack_bp2_bitwise_equals_bp1(pkg, precision):
+    """C3 (extra-MSA stack -> main stack) under BP=2: bitwise equal to the
+    one-GPU composition (schedules.composed_step)."""
+    import os
+    import tempfile
+    import torch.multiprocessing as mp
+    from paper_2211_00235_b200 import schedules as S
+    fd, init_file = tempfile.mkstemp()
+    os.close(fd)
+    os.unlink(init_file)
+    ctx = mp.get_context("spawn")
+    q = ctx.SimpleQueue()
+    procs = [ctx.Process(target=_c3_worker, args=(r, init_file, precision, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    got = {}
+    for _ in range(2):
+        status, rank, out, grads = q.get()
+        assert status == "ok", out
+        got[rank] = (out, grads)
+    for p in procs:
+        p.join(timeout=60)
+    ce, cm = pkg.EvoConfig(**EXTRA), pkg.EvoConfig(**MAIN)
+    ste = S.StepState(ce, pkg.init_params(ce, 33), precision)
+    stm = S.StepState(cm, pkg.init_params(cm, 32), precision)
+    m_out, z_out, loss, dm_e, dm, dz = S.composed_step(ste, stm, *_c3_inputs(ce, cm))
+    torch.cuda.synchronize()
+    (r0, g0), (r1, g1) = got[0], got[1]
+    assert np.array_equal(r0[0], m_out.cpu().numpy())
+    assert np.array_equal(r0[3], dm_e.cpu().numpy())
+    assert np.array_equal(r0[4], dm.cpu().numpy())
+    assert np.array_equal(r1[1], z_out.cpu().numpy())
+    assert np.array_equal(r1[5], dz.cpu().numpy())
+    assert np.float32(r0[2][0] + r1[2][0]) == np.float32(loss.item())
+    want = {**{"extra." + k: v.cpu().numpy() for k, v in ste.grad_dict().items()},
+            **{"main." + k: v.cpu().numpy() for k, v in stm.grad_dict().items()}}
+    for n, g in want.items():
+        assert np.array_equal(g0[n], g) and np.array_equal(g1[n], g), n
