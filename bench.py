@@ -541,10 +541,16 @@ def run_stack(args):
     kw_m = {**CONFIGS["af2"], "n_blocks": args.blocks or 48}
     if args.crop:
         kw_m["r"] = args.crop
+    if args.seqs:
+        kw_m["s"] = args.seqs
     kw_e = {**EXTRA_AF2, "r": kw_m["r"]}
+    if args.extra_seqs:
+        kw_e["s"] = args.extra_seqs
     ce, cm = pkg.EvoConfig(**kw_e), pkg.EvoConfig(**kw_m)
-    ste = S.StepState(ce, pkg.init_params(ce, 33, device=dev), args.precision, dev)
-    stm = S.StepState(cm, pkg.init_params(cm, 32, device=dev), args.precision, dev)
+    ste = S.StepState(ce, pkg.init_params(ce, 33, device=dev), args.precision, dev,
+                      checkpoint=args.checkpoint)
+    stm = S.StepState(cm, pkg.init_params(cm, 32, device=dev), args.precision, dev,
+                      checkpoint=args.checkpoint)
     ste.pack()
     stm.pack()
     rng = np.random.default_rng(32)
@@ -598,8 +604,10 @@ def run_stack(args):
         "ms_per_block_fwd_bwd": ms / (ce.n_blocks + cm.n_blocks),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
-        "config": {"workload": "evoformer_stack_c3", "main": kw_m, "extra": kw_e,
+        "config": {"workload": ("evoformer_stack_c4_finetune" if kw_e["s"] > 1024
+                                else "evoformer_stack_c3"), "main": kw_m, "extra": kw_e,
                    "precision": args.precision, "parallelism": "bp1xdp1", "global_batch": 1,
+                   "activation_checkpointing": args.checkpoint,
                    "l2": "step working set exceeds the 126 MB L2"},
         "flops_per_step": flops, "step_tflops": tflops, "step_frac_of_peak": tflops / peak,
         "peak_source": src,
@@ -628,6 +636,12 @@ def main():
     ap.add_argument("--stack", action="store_true",
                     help="C3: 4-block extra-MSA stack (s_e=1024, c_e=64) feeding a "
                          "--blocks (default 48) main stack, one GPU")
+    ap.add_argument("--seqs", type=int, default=0, help="--stack: main-stack MSA depth s")
+    ap.add_argument("--extra-seqs", type=int, default=0,
+                    help="--stack: extra-MSA depth s_e (C4: 5120)")
+    ap.add_argument("--checkpoint", action="store_true",
+                    help="per-block activation checkpointing (recompute each block's "
+                         "forward before its backward)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
     ap.add_argument("--dp-only", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",

@@ -306,6 +306,14 @@ EVO_API int evo_add(int64_t n, const float *a, const float *b, float *out,
  * DP gradient mean (src/schedules.py:324-328).                           */
 EVO_API int evo_div_scalar(int64_t n, const float *x, float d, float *out, void *stream);
 
+/* LayerNorm forward of contiguous fp32 rows of 128 / 256 (c_z / c_m) into
+ * the split bf16 operand y3 [rows, 3*cols] = hi | lo | hi (hi = bf16(y),
+ * lo = bf16(y - hi)) of the 3-product transition projection; mean/rstd as
+ * evo_layernorm_fwd.  EVO_EUNSUP for other shapes.                       */
+EVO_API int evo_layernorm_fwd_split(int64_t rows, int cols, const float *x, const float *gamma,
+                                    const float *beta, void *y3, float *mean, float *rstd,
+                                    float eps, void *stream);
+
 /* Split an fp32 [rows, cols] operand into bf16 hi = bf16(x) and
  * lo = bf16(x - hi) (hi also to hi2 when non-NULL), element strides per row.
  * Used for the 3-product bf16 GEMM (A3 = [hi | lo | hi], W3 = [W_hi; W_hi;

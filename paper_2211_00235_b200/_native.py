@@ -56,6 +56,8 @@ _SIGS = {
                                   c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_i64, c_i64, c_vp, c_vp,
                                   c_i32, c_vp, c_sz, c_vp]),
     "evo_layernorm_bwd_workspace_bytes": (c_sz, [c_i64, c_i32]),
+    "evo_layernorm_fwd_split": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_f32,
+                                        c_vp]),
     "evo_relu_bwd_colsum": (c_i32, [c_i64, c_i64, c_vp, c_vp, c_vp, c_vp, c_vp, c_sz, c_vp]),
     "evo_layernorm_bwd_proj": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp, c_vp,
                                        c_vp, c_i64, c_vp, c_i32, c_vp, c_vp, c_vp, c_vp, c_vp,

@@ -34,6 +34,8 @@ int layernorm_fwd(int, int, int64_t, int, const void *, int64_t, int64_t, const 
 int layernorm_bwd(int, int, int, int64_t, int, const void *, int64_t, const void *, int64_t,
                   int64_t, const float *, const float *, const float *, const float *, void *,
                   int64_t, int64_t, float *, float *, int, void *, size_t, cudaStream_t);
+int layernorm_fwd_split(int64_t, int, const float *, const float *, const float *, void *, float *,
+                        float *, float, cudaStream_t);
 int layernorm_bwd_ex(int64_t, int, const float *, const void *, int, const float *, const float *,
                      const float *, const float *, float *, void *, float *, float *, float *,
                      void *, size_t, cudaStream_t);
@@ -159,6 +161,17 @@ int evo_layernorm_fwd(int dtype_x, int dtype_y, int64_t rows, int cols, const vo
   CHECK_PTR(x); CHECK_PTR(gamma); CHECK_PTR(beta); CHECK_PTR(y); CHECK_PTR(mean); CHECK_PTR(rstd);
   return layernorm_fwd(dtype_x, dtype_y, rows, cols, x, x_rs, x_cs, gamma, beta, y, y_rs, mean,
                        rstd, eps, as_stream(stream));
+}
+
+int evo_layernorm_fwd_split(int64_t rows, int cols, const float *x, const float *gamma,
+                            const float *beta, void *y3, float *mean, float *rstd, float eps,
+                            void *stream) {
+  EVO_REQUIRE(rows >= 0 && cols >= 1, EVO_EDIM, "evo_layernorm_fwd_split: rows=%lld cols=%d",
+              (long long)rows, cols);
+  EVO_REQUIRE(eps > 0.f, EVO_EARG, "evo_layernorm_fwd_split: eps must be > 0");
+  if (rows == 0) return EVO_OK;
+  CHECK_PTR(x); CHECK_PTR(gamma); CHECK_PTR(beta); CHECK_PTR(y3); CHECK_PTR(mean); CHECK_PTR(rstd);
+  return layernorm_fwd_split(rows, cols, x, gamma, beta, y3, mean, rstd, eps, as_stream(stream));
 }
 
 size_t evo_layernorm_bwd_workspace_bytes(int64_t rows, int cols) {

@@ -603,8 +603,8 @@ template <int NV>
 struct LnfLayout {
   static constexpr int cols = NV * 128, RCH = 4 * LNF_CW / NV;
   static constexpr uint32_t STAGE = RCH * cols * 4;
-  static constexpr uint32_t OFF_P = LNF_NS * STAGE;  // gamma, beta, per-warp y rows
-  static constexpr uint32_t OFF_BAR = OFF_P + 2 * cols * 4 + LNF_CW * 4 * 32 * 8;
+  static constexpr uint32_t OFF_P = LNF_NS * STAGE;  // gamma, beta
+  static constexpr uint32_t OFF_BAR = OFF_P + 2 * cols * 4;
   static constexpr uint32_t SMEM = OFF_BAR + 2 * LNF_NS * 8;
 };
 
@@ -637,17 +637,19 @@ __device__ __forceinline__ float group8_sum(float v) {
   return v;
 }
 
-template <int NV, int NH, typename TY>
+// SPLIT: y is bf16 [rows, 3*cols] = hi | lo | hi with hi = bf16(LN(x)),
+// lo = bf16(LN(x) - hi): the A operand of the transitions' 3-product bf16
+// first projection (engine.transition_fwd)
+template <int NV, int SPLIT, typename TY>
 __global__ void __launch_bounds__((LNF_CW + 1) * 32, 1)
 ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__restrict__ gamma,
                   const float *__restrict__ beta, TY *__restrict__ y, float *__restrict__ mean_out,
-                  float *__restrict__ rstd_out, float eps, const bf16 *__restrict__ Wp, int nh,
-                  float *__restrict__ proj, int64_t p_rs) {
+                  float *__restrict__ rstd_out, float eps) {
   using Lay = LnfLayout<NV>;
   constexpr int cols = Lay::cols, RCH = Lay::RCH, NI = 4 * NV;
-  static_assert(NH == 0 || (NH == 8 && NV == 1), "projection: c_z = 128, 8 heads");
+  static_assert(!SPLIT || std::is_same<TY, bf16>::value, "split output is bf16");
   extern __shared__ __align__(128) uint8_t sm[];
-  float *sg = reinterpret_cast<float *>(sm + Lay::OFF_P), *sbt = sg + cols, *sW = sbt + cols;  // sW: y staging
+  float *sg = reinterpret_cast<float *>(sm + Lay::OFF_P), *sbt = sg + cols;
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + Lay::OFF_BAR);
   uint64_t *empty = full + LNF_NS;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -680,18 +682,6 @@ ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__rest
   }
   const int l8 = lane & 7, rg = lane >> 3;
   constexpr float inv_n = 1.f / cols;
-  // projection: 32-lane layout (lane owns columns 4*lane..+3, W in registers)
-  // over the warp's four bf16 y rows staged in smem
-  float W[4][NH > 0 ? NH : 1];
-  uint2 *sy = reinterpret_cast<uint2 *>(sW) + warp * 4 * 32;  // [4 rows][32 lanes] x 4 bf16
-  if constexpr (NH > 0) {
-#pragma unroll
-    for (int j = 0; j < 4; ++j)
-#pragma unroll
-      for (int hh = 0; hh < NH; ++hh)
-        W[j][hh] = hh < nh ? __bfloat162float(Wp[(4 * lane + j) * nh + hh]) : 0.f;
-  }
-  const int hsel = ((lane >> 4) & 1) * 4 + ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
   int it = 0;
   for (int64_t c = blockIdx.x; c < nchunks; c += gridDim.x, ++it) {
     const int s = it % LNF_NS;
@@ -729,34 +719,21 @@ ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__rest
         const float4 b4 = *reinterpret_cast<const float4 *>(sbt + cc);
         float o[4] = {(v[i][0] - mu) * rs * g4.x + b4.x, (v[i][1] - mu) * rs * g4.y + b4.y,
                       (v[i][2] - mu) * rs * g4.z + b4.z, (v[i][3] - mu) * rs * g4.w + b4.w};
-        if (y && ok) Vec<TY, 4>::store(y + row * cols + cc, o);
-        if constexpr (NH > 0) {  // column group cc/4 = l8 + 8 i of row rg
-          __nv_bfloat162 lo = __floats2bfloat162_rn(o[0], o[1]);
-          __nv_bfloat162 hi = __floats2bfloat162_rn(o[2], o[3]);
-          sy[rg * 32 + l8 + 8 * i] = make_uint2(*reinterpret_cast<uint32_t *>(&lo),
-                                                *reinterpret_cast<uint32_t *>(&hi));
+        if (!ok) continue;
+        if constexpr (SPLIT) {
+          float hi[4], lo[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            hi[j] = __bfloat162float(__float2bfloat16(o[j]));
+            lo[j] = o[j] - hi[j];
+          }
+          TY *yr = y + row * (3 * cols) + cc;
+          Vec<TY, 4>::store(yr, hi);
+          Vec<TY, 4>::store(yr + cols, lo);
+          Vec<TY, 4>::store(yr + 2 * cols, hi);
+        } else {
+          Vec<TY, 4>::store(y + row * cols + cc, o);
         }
-      }
-      if constexpr (NH > 0) {
-        __syncwarp();
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          if (4 * q4 + rr >= nr) break;  // warp-uniform
-          const uint2 u = sy[rr * 32 + lane];
-          const float2 f01 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.x));
-          const float2 f23 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162 *>(&u.y));
-          const float yv[4] = {f01.x, f01.y, f23.x, f23.y};
-          float pr[8];
-#pragma unroll
-          for (int hh = 0; hh < 8; ++hh) pr[hh] = 0.f;
-#pragma unroll
-          for (int j = 0; j < 4; ++j)
-#pragma unroll
-            for (int hh = 0; hh < NH; ++hh) pr[hh] = fmaf(yv[j], W[j][hh], pr[hh]);
-          const float tot = warp_sum8_scatter(pr, lane);
-          if ((lane & 3) == 0 && hsel < nh) proj[(int64_t)hsel * p_rs + r0 + 4 * q4 + rr] = tot;
-        }
-        __syncwarp();
       }
       if (ok && l8 == 0) {
         mean_out[row] = mu;
@@ -768,17 +745,15 @@ ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__rest
   }
 }
 
-template <int NV, int NH, typename TY>
+template <int NV, int SPLIT, typename TY>
 int ln_fwd_tma_launch(int64_t rows, const float *x, const float *gamma, const float *beta, TY *y,
-                      float *mean, float *rstd, float eps, const bf16 *Wp, int nh, float *proj,
-                      int64_t p_rs, cudaStream_t st) {
+                      float *mean, float *rstd, float eps, cudaStream_t st) {
   using Lay = LnfLayout<NV>;
   const int64_t nchunks = (rows + Lay::RCH - 1) / Lay::RCH;
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), nchunks));
-  auto kfn = ln_fwd_tma_kernel<NV, NH, TY>;
+  auto kfn = ln_fwd_tma_kernel<NV, SPLIT, TY>;
   EVO_MAX_SMEM_ONCE(kfn);
-  kfn<<<nb, (LNF_CW + 1) * 32, Lay::SMEM, st>>>(rows, x, gamma, beta, y, mean, rstd, eps, Wp, nh,
-                                                proj, p_rs);
+  kfn<<<nb, (LNF_CW + 1) * 32, Lay::SMEM, st>>>(rows, x, gamma, beta, y, mean, rstd, eps);
   EVO_LAUNCHED("ln_fwd_tma_kernel");
   return EVO_OK;
 }
@@ -1025,10 +1000,8 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   if constexpr (std::is_same<TX, float>::value) {
     if (vec && x_rs == cols && y_rs == cols) {
       if (cols == 128)
-        return ln_fwd_tma_launch<1, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, nullptr, 0,
-                                           nullptr, 0, st);
-      return ln_fwd_tma_launch<2, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, nullptr, 0,
-                                         nullptr, 0, st);
+        return ln_fwd_tma_launch<1, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, st);
+      return ln_fwd_tma_launch<2, 0, TY>(rows, xp, gamma, beta, yp, mean, rstd, eps, st);
     }
   }
   if (vec) {
@@ -1187,6 +1160,18 @@ int layernorm_fwd(int tx, int ty, int64_t rows, int cols, const void *x, int64_t
   if (tx == EVO_BF16 && ty == EVO_BF16)
     return ln_fwd_launch<bf16, bf16>(rows, cols, x, x_rs, x_cs, gamma, beta, y, y_rs, mean, rstd, eps, st);
   return ln_fwd_launch<bf16, float>(rows, cols, x, x_rs, x_cs, gamma, beta, y, y_rs, mean, rstd, eps, st);
+}
+
+int layernorm_fwd_split(int64_t rows, int cols, const float *x, const float *gamma,
+                        const float *beta, void *y3, float *mean, float *rstd, float eps,
+                        cudaStream_t st) {
+  EVO_REQUIRE((cols == 128 || cols == 256) && aligned16(x) && aligned16(y3) && aligned16(gamma) &&
+                  aligned16(beta),
+              EVO_EUNSUP, "layernorm_fwd_split: contiguous fp32 rows of 128 / 256, aligned");
+  if (rows == 0) return EVO_OK;
+  bf16 *y = reinterpret_cast<bf16 *>(y3);
+  if (cols == 128) return ln_fwd_tma_launch<1, 1, bf16>(rows, x, gamma, beta, y, mean, rstd, eps, st);
+  return ln_fwd_tma_launch<2, 1, bf16>(rows, x, gamma, beta, y, mean, rstd, eps, st);
 }
 
 int layernorm_bwd_ex(int64_t rows, int cols, const float *dy, const void *x, int tx,

@@ -422,12 +422,14 @@ def transition_fwd(P, px, pk, x, cfg, act, resid=True):
     mu, rs = _empty(rows, F32, dev), _empty(rows, F32, dev)
     hid = _empty((rows, tc), act, dev)
     if "W1x3" in pk:
-        x32 = _empty((rows, cx), F32, dev)
-        K.layernorm(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], x32, mu, rs, cfg.eps)
         xh = _empty((rows, 3 * cx), act, dev)      # [hi | lo | hi]
-        K.split_bf16(x32, rows, cx, xh, xh, h_rs=3 * cx, l_rs=3 * cx, hi2=xh, h2_rs=3 * cx,
-                     l_off=cx, h2_off=2 * cx)
-        del x32
+        if not K.layernorm_split(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], xh, mu, rs,
+                                 cfg.eps):
+            x32 = _empty((rows, cx), F32, dev)
+            K.layernorm(x, rows, cx, P[f"{px}.ln_g"], P[f"{px}.ln_b"], x32, mu, rs, cfg.eps)
+            K.split_bf16(x32, rows, cx, xh, xh, h_rs=3 * cx, l_rs=3 * cx, hi2=xh, h2_rs=3 * cx,
+                         l_off=cx, h2_off=2 * cx)
+            del x32
         xh_ld = 3 * cx
         K.linear(xh, rows, 3 * cx, pk["W1x3"], tc, tc, hid, tc, bias=P[f"{px}.b1"],
                  epi=EPI_RELU)

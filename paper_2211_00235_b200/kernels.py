@@ -166,6 +166,18 @@ def layernorm(x, rows: int, cols: int, gamma, beta, y, mean, rstd, eps: float, *
           "evo_layernorm_fwd")
 
 
+def layernorm_split(x, rows: int, cols: int, gamma, beta, y3, mean, rstd, eps: float) -> bool:
+    """LN(x) into the split bf16 operand y3 [rows, 3*cols] = hi | lo | hi in
+    one pass (contiguous fp32 rows of 128 / 256); False for other shapes
+    (the caller composes LN + split_bf16 then)."""
+    if cols not in (128, 256) or not x.is_contiguous() or x.dtype != torch.float32:
+        return False
+    check(lib().evo_layernorm_fwd_split(rows, cols, ptr(x), ptr(gamma), ptr(beta), ptr(y3),
+                                        ptr(mean), ptr(rstd), eps, stream()),
+          "evo_layernorm_fwd_split")
+    return True
+
+
 def layernorm_bwd(dy, x, rows: int, cols: int, mean, rstd, gamma, dx, dgamma, dbeta, *,
                   dres=None, dy_rs=None, x_rs=None, x_cs=1, dx_rs=None, dx_cs=1,
                   accumulate_params=False):

@@ -129,10 +129,16 @@ class StepState:
     after a parameter update."""
 
     def __init__(self, cfg: EvoConfig, store: ParamStore, precision: str | None = None,
-                 device=None):
+                 device=None, checkpoint: bool = False):
         self.cfg = cfg
         self.act = act_dtype(precision)
         self.dev = device or store.device
+        # per-block activation checkpointing: keep only each block's inputs
+        # (m, z) through the forward and recompute the block's forward right
+        # before its backward (bitwise the same values: every kernel is
+        # deterministic), for stacks whose saved activations exceed HBM
+        # (C4: 48 blocks at s = 512, r = 384)
+        self.checkpoint = checkpoint
         self.P = store.bind()
         self.grads = [E.BlockGrads(b, cfg, self.dev) for b in range(cfg.n_blocks)]
         self.packs = None
@@ -237,6 +243,31 @@ class GraphedStep:
         return tuple(self.seg.graphs[("step", slot)][1])
 
 
+def _stack_fwd(st: StepState, m_c, z_c):
+    """Forward through st's blocks; returns (m, z, per-block saved state):
+    the block's ctx, or with st.checkpoint only its inputs (m, z)."""
+    cfg, act = st.cfg, st.act
+    saved = []
+    for blk in range(cfg.n_blocks):
+        m_in, z_in = m_c, z_c
+        m_c, z_c, c = E.block_fwd(st.P, blk, st.packs[blk], m_c, z_c, cfg, act)
+        saved.append((m_in, z_in) if st.checkpoint else c)
+        del c
+    return m_c, z_c, saved
+
+
+def _stack_bwd(st: StepState, saved, dm, dz):
+    cfg, act = st.cfg, st.act
+    for blk in reversed(range(cfg.n_blocks)):
+        c = saved[blk]
+        saved[blk] = None
+        if st.checkpoint:   # recompute the block's forward state
+            _, _, c = E.block_fwd(st.P, blk, st.packs[blk], c[0], c[1], cfg, act)
+        dm, dz = E.block_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, c, dm, dz, cfg, act)
+        del c
+    return dm, dz
+
+
 def full_step(st: StepState, m, z, fwd_events=None):
     """Forward + loss + backward of the whole stack on one device.
     Returns (m_out, z_out, loss_tensor[1], dm, dz); fwd_events (two CUDA
@@ -247,12 +278,9 @@ def full_step(st: StepState, m, z, fwd_events=None):
         st.pack()
     m_c = m.reshape(s * r, cfg.c_m)
     z_c = z.reshape(r * r, cfg.c_z)
-    ctxs = []
     if fwd_events is not None:
         fwd_events[0].record()
-    for blk in range(cfg.n_blocks):
-        m_c, z_c, c = E.block_fwd(st.P, blk, st.packs[blk], m_c, z_c, cfg, act)
-        ctxs.append(c)
+    m_c, z_c, ctxs = _stack_fwd(st, m_c, z_c)
     if fwd_events is not None:
         fwd_events[1].record()
     loss = torch.zeros(1, dtype=F32, device=m.device)
@@ -260,10 +288,7 @@ def full_step(st: StepState, m, z, fwd_events=None):
     dz = torch.empty_like(z_c)
     K.sq_mean(m_c, loss, dm)
     K.sq_mean(z_c, loss, dz)
-    for blk in reversed(range(cfg.n_blocks)):
-        dm, dz = E.block_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctxs[blk], dm, dz,
-                             cfg, act)
-        ctxs[blk] = None
+    dm, dz = _stack_bwd(st, ctxs, dm, dz)
     return (m_c.reshape(s, r, cfg.c_m), z_c.reshape(r, r, cfg.c_z), loss,
             dm.reshape(s, r, cfg.c_m), dz.reshape(r, r, cfg.c_z))
 
@@ -285,29 +310,17 @@ def composed_step(extra: StepState, main: StepState, m_e, m, z):
             st.pack()
     me_c = m_e.reshape(ce.s * ce.r, ce.c_m)
     z_c = z.reshape(ce.r * ce.r, ce.c_z)
-    ctx_e = []
-    for blk in range(ce.n_blocks):
-        me_c, z_c, c = E.block_fwd(extra.P, blk, extra.packs[blk], me_c, z_c, ce, extra.act)
-        ctx_e.append(c)
+    me_c, z_c, ctx_e = _stack_fwd(extra, me_c, z_c)
     m_c = m.reshape(cm.s * cm.r, cm.c_m)
-    ctx_m = []
-    for blk in range(cm.n_blocks):
-        m_c, z_c, c = E.block_fwd(main.P, blk, main.packs[blk], m_c, z_c, cm, main.act)
-        ctx_m.append(c)
+    m_c, z_c, ctx_m = _stack_fwd(main, m_c, z_c)
     loss = torch.zeros(1, dtype=F32, device=m.device)
     dm = torch.empty_like(m_c)
     dz = torch.empty_like(z_c)
     K.sq_mean(m_c, loss, dm)
     K.sq_mean(z_c, loss, dz)
-    for blk in reversed(range(cm.n_blocks)):
-        dm, dz = E.block_bwd(main.P, blk, main.packs[blk], main.grads[blk].packed, ctx_m[blk],
-                             dm, dz, cm, main.act)
-        ctx_m[blk] = None
+    dm, dz = _stack_bwd(main, ctx_m, dm, dz)
     dm_e = torch.zeros(me_c.shape, dtype=F32, device=m.device)
-    for blk in reversed(range(ce.n_blocks)):
-        dm_e, dz = E.block_bwd(extra.P, blk, extra.packs[blk], extra.grads[blk].packed,
-                               ctx_e[blk], dm_e, dz, ce, extra.act)
-        ctx_e[blk] = None
+    dm_e, dz = _stack_bwd(extra, ctx_e, dm_e, dz)
     return (m_c.reshape(cm.s, cm.r, cm.c_m), z_c.reshape(cm.r, cm.r, cm.c_z), loss,
             dm_e.reshape(ce.s, ce.r, ce.c_m), dm.reshape(cm.s, cm.r, cm.c_m),
             dz.reshape(cm.r, cm.r, cm.c_z))

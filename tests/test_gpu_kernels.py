@@ -152,3 +152,28 @@ def test_relu_bwd_colsum_fused(K):
     want = torch.where(h > 0, dh, torch.zeros_like(dh))
     assert torch.equal(out, want)
     assert rel(cs, want.double().sum(0)) < 1e-6
+
+
+@pytest.mark.parametrize("rows,cols", [(4096, 128), (1003, 256)])
+def test_layernorm_split_operand(K, rows, cols):
+    """LN(x) straight into the [hi | lo | hi] bf16 operand of the 3-product
+    transition projection == LN into fp32, then split."""
+    torch.manual_seed(3)
+    x = torch.randn(rows, cols, device="cuda")
+    g, b = torch.randn(cols, device="cuda"), torch.randn(cols, device="cuda")
+    y32 = torch.empty(rows, cols, device="cuda")
+    mu0, rs0 = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    K.layernorm(x, rows, cols, g, b, y32, mu0, rs0, 1e-5)
+    y3 = torch.empty(rows, 3 * cols, device="cuda", dtype=torch.bfloat16)
+    mu, rs = torch.empty(rows, device="cuda"), torch.empty(rows, device="cuda")
+    assert K.layernorm_split(x, rows, cols, g, b, y3, mu, rs, 1e-5)
+    hi = y32.to(torch.bfloat16)
+    lo = (y32 - hi.float()).to(torch.bfloat16)
+    assert torch.equal(y3[:, :cols], hi) and torch.equal(y3[:, 2 * cols:], hi)
+    assert torch.equal(y3[:, cols:2 * cols], lo)
+    assert torch.equal(mu, mu0) and torch.equal(rs, rs0)
+    # the split kernel composes to the same operand
+    y3b = torch.empty_like(y3)
+    K.split_bf16(y32, rows, cols, y3b, y3b, h_rs=3 * cols, l_rs=3 * cols, hi2=y3b,
+                 h2_rs=3 * cols, l_off=cols, h2_off=2 * cols)
+    assert torch.equal(y3, y3b)

@@ -254,3 +254,22 @@ def test_c3_composed_stack_bp2_bitwise_equals_bp1(pkg, precision):
             **{"main." + k: v.cpu().numpy() for k, v in stm.grad_dict().items()}}
     for n, g in want.items():
         assert np.array_equal(g0[n], g) and np.array_equal(g1[n], g), n
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_activation_checkpointing_bitwise(pkg, precision):
+    """StepState(checkpoint=True) recomputes each block's forward before its
+    backward: same kernels, same inputs -> bitwise the same step."""
+    from paper_2211_00235_b200 import schedules as S
+    cfg = pkg.EvoConfig(**KW)
+    store = pkg.init_params(cfg, 32)
+    m, z = S.make_batch(cfg, 32, 1)[0]
+    a = S.StepState(cfg, store, precision)
+    b = S.StepState(cfg, store, precision, checkpoint=True)
+    out_a = [t.clone() for t in S.full_step(a, m, z)]
+    out_b = S.full_step(b, m, z)
+    for x, y in zip(out_a, out_b):
+        assert torch.equal(x, y)
+    ga, gb = a.grad_dict(), b.grad_dict()
+    for k in ga:
+        assert torch.equal(ga[k], gb[k]), k
