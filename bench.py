@@ -493,6 +493,14 @@ def run_native(args):
     bp2 = None
     if world == 1 and not args.no_bp2:
         bp2 = bp2_prediction(cfg, store, args.precision, dev, ms / cfg.n_blocks)
+    peak_mem = torch.cuda.max_memory_allocated(dev) / 1e9
+    c3 = None
+    if world == 1 and not args.no_c3 and args.config == "af2" and not args.crop:
+        import gc
+        del gs, st
+        gc.collect()
+        torch.cuda.empty_cache()
+        c3 = c3_summary(args)
     line = {
         "metric": METRIC, "value": value, "unit": "samples/s", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -512,8 +520,9 @@ def run_native(args):
         "launch_mode": ("cuda_graph" if runner is None else "cuda_graph_segments")
         if use_graph else "eager", "ms_per_step_eager": ms_eager,
         "clocks": clk,
-        "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+        "peak_mem_gb": peak_mem,
         "bp2_prediction": bp2,
+        "c3_stack_1gpu": c3,
     }
     print(json.dumps(line))
     if world > 1:
@@ -619,8 +628,25 @@ def run_stack(args):
         "gpu_launches_per_step": launches_per_step, "launch_mode": "cuda_graph",
         "clocks": clk, "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
     }
-    print(json.dumps(line))
-    return 0
+    if not getattr(args, "quiet", False):
+        print(json.dumps(line))
+    return line
+
+
+def c3_summary(args):
+    """SURVEY.md §8(d) C3 on this GPU (48 main + 4 extra-MSA blocks, one
+    train step graph-replayed), as a key of the default bench line."""
+    import copy
+    a = copy.copy(args)
+    a.blocks, a.crop, a.seqs, a.extra_seqs, a.checkpoint = 48, 0, 0, 0, False
+    a.steps, a.warmup, a.quiet = 5, 2, True
+    line = run_stack(a)
+    keep = ("value", "unit", "ms_per_step", "ms_per_block_fwd_bwd", "step_tflops",
+            "step_frac_of_peak", "e2e", "gpu_launches_per_step", "clocks", "peak_mem_gb",
+            "config")
+    out = {k: line[k] for k in keep}
+    out["steps"], out["warmup"] = a.steps, a.warmup
+    return out
 
 
 def main():
@@ -647,6 +673,8 @@ def main():
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager launches instead of CUDA-graph replay")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-c3", action="store_true",
+                    help="skip the C3 (48 + 4 block stack) measurement key")
     ap.add_argument("--no-bp2", action="store_true",
                     help="skip the one-GPU BP=2 branch-split prediction")
     ap.add_argument("--detail", action="store_true", help="per-call GEMM/attention table on stderr")
@@ -654,8 +682,10 @@ def main():
     if args.impl == "reference":
         return run_reference(args)
     if args.stack:
-        return run_stack(args)
-    return run_native(args)
+        run_stack(args)
+        return 0
+    run_native(args)
+    return 0
 
 
 if __name__ == "__main__":

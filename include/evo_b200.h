@@ -216,6 +216,19 @@ EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, int64_t ld, const floa
                                    int64_t rl, void *P, void *dS, float *dbias, int acc,
                                    void *stream);
 
+/* Long-key fused attention (tcgen05, keys streamed in 64-wide tiles with an
+ * online softmax; no logits in HBM), bf16, head dim 16 / 32, any L: the same
+ * op and descriptor as evo_attention_fwd/bwd (src/evoformer.py:268-286).
+ * The bias (when present) must be plain rows: bk = 1, bq % 4 == 0,
+ * bh >= L*bq.  Backward: dO / Dq are evo_attn_long_prep's outputs (rows by
+ * activation row id b*rb + l*rl); dbias_part = fp32 [ceil(nb/chunk)][H][L][L]
+ * chunk partials of dbias (batch rows summed in order; the caller reduces the
+ * chunks in order); writes desc.dq / dk / dv.                            */
+EVO_API int evo_attn_flash_fwd(const evo_attn_desc *d, void *stream);
+EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq,
+                               int64_t rb, int64_t rl, float *dbias_part, int64_t chunk,
+                               void *stream);
+
 /* Deterministic reduction over the leading axis:
  * dst(i, j) (+)= sum_{b<nb} src[b*n1*n2 + i*n2 + j], dst at
  * dst[i*d_s1 + j*d_s2] fp32.  src dtype_src.  Replaces the bias-gradient
@@ -339,7 +352,8 @@ EVO_API int evo_tc_available(void);
 #define EVO_BK_GEMM_SKINNY 2
 #define EVO_BK_ATTN_TC 3
 #define EVO_BK_ATTN_SIMT 4
-#define EVO_BK_COUNT 5
+#define EVO_BK_ATTN_FLASH 5
+#define EVO_BK_COUNT 6
 EVO_API int64_t evo_backend_count(int backend);
 EVO_API int evo_last_backend(void);
 /* Strict tensor-core mode (default ON): a bf16 evo_gemm / evo_attention_*

@@ -71,6 +71,9 @@ _SIGS = {
                                 c_vp]),
     "evo_attn_long_softmax": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_vp, c_vp, c_i64, c_i64,
                                       c_i64, c_vp, c_vp, c_vp]),
+    "evo_attn_flash_fwd": (c_i32, [C.POINTER(AttnDesc), c_vp]),
+    "evo_attn_flash_bwd": (c_i32, [C.POINTER(AttnDesc), c_vp, c_vp, c_i64, c_i64, c_vp, c_i64,
+                                   c_vp]),
     "evo_attn_long_gate": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "evo_attn_long_prep": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_vp]),
@@ -149,7 +152,7 @@ def launch_count() -> int:
 
 
 # engines (include/evo_b200.h EVO_BK_*)
-BACKENDS = ("gemm_tc", "gemm_simt", "gemm_skinny", "attn_tc", "attn_simt")
+BACKENDS = ("gemm_tc", "gemm_simt", "gemm_skinny", "attn_tc", "attn_simt", "attn_flash")
 
 
 def backend_counts() -> dict:

@@ -15,7 +15,7 @@ static std::atomic<int> g_strict_tc{1};
 static std::atomic<int64_t> g_backend[EVO_BK_COUNT];
 static thread_local int g_last_backend = -1;
 
-static void note_backend(int b) {
+void note_backend(int b) {
   g_backend[b].fetch_add(1, std::memory_order_relaxed);
   g_last_backend = b;
 }

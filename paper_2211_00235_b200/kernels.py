@@ -233,11 +233,93 @@ import os as _os
 KEEP_P_MAX_BYTES = int(_os.environ.get("EVO_KEEP_P_MAX_BYTES", str(8 << 30)))
 
 
+def use_flash(dtype, L: int, D: int) -> bool:
+    """bf16, L > 256 keys, head dim 16 / 32: the streamed-key fused attention
+    (csrc/attention_flash.cu)."""
+    return dtype == torch.bfloat16 and L > LONG_L and D in (16, 32)
+
+
 def use_long(dtype, L: int, D: int) -> bool:
-    """bf16 shapes the fused tcgen05 attention does not take (L > 256 keys,
-    or head dims other than 16 / 32: the extra-MSA stack's c_head = 8) run
-    on the GEMM-composed path instead of the SIMT kernels."""
-    return dtype == torch.bfloat16 and (L > LONG_L or D not in (16, 32))
+    """bf16 shapes no fused tcgen05 attention takes (head dims other than
+    16 / 32: the extra-MSA stack's c_head = 8) run on the GEMM-composed path
+    instead of the SIMT kernels."""
+    return (dtype == torch.bfloat16 and (L > LONG_L or D not in (16, 32))
+            and not use_flash(dtype, L, D))
+
+
+def _attn_desc(proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias, bh, bq, bk):
+    d = AttnDesc()
+    d.dtype = dt(proj)
+    d.nb, d.H, d.L, d.D, d.scale = nb, H, L, D, scale
+    d.q, d.k, d.v, d.g = (ptr(proj, 0), ptr(proj, hc), ptr(proj, 2 * hc), ptr(proj, 3 * hc))
+    d.sb, d.sl = sb, sl
+    d.o, d.gm = ptr(o), ptr(gm)
+    d.o_sb, d.o_sl = o_sb, o_sl
+    d.bias, d.bh, d.bq, d.bk = ptr(bias), bh, bq, bk
+    d.lse = ptr(lse)
+    return d
+
+
+def attention_flash(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias=None,
+                    bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None):
+    """L > 256 keys on the bf16 path, head dim 16 / 32: csrc/attention_flash.cu
+    (keys streamed through TMEM with an online softmax; the backward's dS
+    never leaves the SM either).  Same argument meaning as ``attention``.
+    The prep pass and the dbias chunk reduction are attention_long's."""
+    four = 4 * hc
+    if sb % four or sl % four or o_sb != sb // 4 or o_sl != sl // 4:
+        raise N.ContractError("attention_flash: proj / o row maps must be the same row ids")
+    rb, rl = sb // four, sl // four
+    rows = nb * L
+    dev = proj.device
+    Lb = lib()
+    # the kernels read plain bias rows (bk = 1, 16-byte aligned): copy a
+    # transposed (triangle end) or unaligned bias once per call
+    pb, pbh, pbq = bias, bh, bq
+    if bias is not None and not (bk == 1 and bq % 4 == 0 and bh % 4 == 0 and bh >= L * bq):
+        Lp = (L + 3) // 4 * 4
+        pb = torch.zeros(H * L * Lp, dtype=torch.float32, device=dev)
+        for hh in range(H):
+            copy2d(bias, L, L, pb, s_rs=bq, s_cs=bk, d_rs=Lp, s_off=hh * bh, d_off=hh * L * Lp)
+        pbh, pbq = L * Lp, Lp
+    d = _attn_desc(proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, pb, pbh, pbq, 1)
+    flops = 4.0 * nb * H * L * L * D
+    if dgm is None:
+        _timed("attention_fwd", flops,
+               lambda: check(Lb.evo_attn_flash_fwd(C.byref(d), stream()), "evo_attn_flash_fwd"),
+               keep=(proj, o, gm, lse, pb))
+        return
+    dO = torch.empty(rows * hc + 8, dtype=torch.bfloat16, device=dev)
+    Dq = torch.empty(rows, H, dtype=torch.float32, device=dev)
+    check(Lb.evo_attn_long_prep(rows, H, D, ptr(dgm), ptr(proj, 3 * hc), four, ptr(o), ptr(dO),
+                                ptr(dproj, 3 * hc), four, ptr(Dq), stream()), "evo_attn_long_prep")
+    d.dgm = ptr(dgm)
+    d.dq, d.dk, d.dv, d.dgpre = (ptr(dproj, 0), ptr(dproj, hc), ptr(dproj, 2 * hc),
+                                 ptr(dproj, 3 * hc))
+    part, chunk, nch = None, 1, nb
+    if bias is not None:
+        # chunks of batch rows per dq CTA: ~2 waves of CTAs, one fp32 dbias
+        # partial per chunk (reduced in chunk order below)
+        qt = (L + 127) // 128
+        nch = max(1, min(nb, (2 * 148) // max(1, qt * H)))
+        chunk = (nb + nch - 1) // nch
+        nch = (nb + chunk - 1) // chunk
+        part = torch.empty(nch * H * L * L, dtype=torch.float32, device=dev)
+    _timed("attention_bwd", 2.0 * flops,
+           lambda: check(Lb.evo_attn_flash_bwd(C.byref(d), ptr(dO), ptr(Dq), rb, rl, ptr(part),
+                                               chunk, stream()), "evo_attn_flash_bwd"),
+           keep=(proj, o, gm, lse, pb, dgm, dproj, dO, Dq, part))
+    if bias is not None:
+        if bk == 1 and bh == L * bq:
+            reduce_lead(part, nch, H * L, L, dbias, bq, 1)
+        else:
+            dense = torch.empty(H * L * L, dtype=torch.float32, device=dev)
+            reduce_lead(part, nch, H * L, L, dense, L, 1)
+            for hh in range(H):
+                copy2d(dense, L, L, dbias, s_rs=L, d_rs=bq, d_cs=bk, s_off=hh * L * L,
+                       d_off=hh * bh)
+    if dgate_bias is not None:
+        colsum(dproj, rows, hc, dgate_bias, rs=four, off=3 * hc)
 
 
 def long_ld(L: int) -> int:
@@ -385,6 +467,11 @@ def attention(*, proj, hc: int, nb: int, H: int, L: int, D: int, scale: float, s
     """Fused gated attention on the packed [rows, 4*hc] projection buffer
     (cols q | k | v | sigmoid(gate)).  Forward when dgm is None, else
     backward into dproj (same packing) and dbias."""
+    if use_flash(proj.dtype, L, D):
+        return attention_flash(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb,
+                               sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,
+                               bh=bh, bq=bq, bk=bk, dgm=dgm, dproj=dproj, dbias=dbias,
+                               dgate_bias=dgate_bias)
     if use_long(proj.dtype, L, D):
         return attention_long(proj=proj, hc=hc, nb=nb, H=H, L=L, D=D, scale=scale, sb=sb,
                               sl=sl, o=o, gm=gm, o_sb=o_sb, o_sl=o_sl, lse=lse, bias=bias,

@@ -64,8 +64,11 @@ def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=Fals
     d_tc = after["attn_tc"] - before["attn_tc"]
     d_simt = after["attn_simt"] - before["attn_simt"]
     d_gemm = after["gemm_tc"] - before["gemm_tc"]
+    d_fl = after["attn_flash"] - before["attn_flash"]
     if dtype == torch.float32:
         assert (d_tc, d_simt) == (0, 2), (d_tc, d_simt)
+    elif K.use_flash(dtype, L, D):
+        assert (d_tc, d_simt, d_fl) == (0, 0, 2), (d_tc, d_simt, d_fl)
     elif K.use_long(dtype, L, D):
         assert (d_tc, d_simt) == (0, 0) and d_gemm >= 6, (d_tc, d_simt, d_gemm)
     else:
@@ -193,3 +196,31 @@ def test_attention_long_keys_multi_chunk(K, case, keep_p, monkeypatch):
     errs = run_case(K, *case, dtype=torch.bfloat16, gate_bias=True, keep_p=keep_p)
     bad = {k: v for k, v in errs.items() if v > 1.5e-2}
     assert not bad, errs
+
+
+# keys beyond 256 on the streamed-key fused kernels (csrc/attention_flash.cu):
+# partial key / query tiles, both bias layouts, no bias, head dims 16 / 32,
+# batch-row chunks for the dbias partials
+FLASH = [
+    (3, 384, 2, 32, False, "plain"),      # crop r = 384 row / triangle-start attention
+    (2, 384, 3, 32, True, "transposed"),  # triangle end
+    (4, 512, 2, 32, True, "none"),        # MSA column attention at s = 512
+    (2, 300, 2, 16, False, "plain"),      # partial last key tile
+    (3, 333, 2, 32, True, "transposed"),  # ragged L: padded plain bias copy
+    (2, 1024, 2, 16, True, "none"),
+    (40, 320, 4, 32, False, "plain"),     # several batch rows per dq CTA
+]
+
+
+@pytest.mark.parametrize("case", FLASH)
+def test_attention_flash_bf16(K, case):
+    assert K.use_flash(torch.bfloat16, case[1], case[3])
+    errs = run_case(K, *case, dtype=torch.bfloat16, gate_bias=True)
+    bad = {k: v for k, v in errs.items() if v > 1.5e-2}
+    assert not bad, errs
+
+
+def test_attention_flash_deterministic(K):
+    a = run_case(K, 5, 384, 2, 32, False, "plain", dtype=torch.bfloat16, seed=4)
+    b = run_case(K, 5, 384, 2, 32, False, "plain", dtype=torch.bfloat16, seed=4)
+    assert a == b
