@@ -220,14 +220,13 @@ EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, int64_t ld, const floa
  * online softmax; no logits in HBM), bf16, head dim 16 / 32, any L: the same
  * op and descriptor as evo_attention_fwd/bwd (src/evoformer.py:268-286).
  * The bias (when present) must be plain rows: bk = 1, bq % 4 == 0,
- * bh >= L*bq.  Backward: dO / Dq are evo_attn_long_prep's outputs (rows by
- * activation row id b*rb + l*rl); dbias_part = fp32 [ceil(nb/chunk)][H][L][L]
- * chunk partials of dbias (batch rows summed in order; the caller reduces the
- * chunks in order); writes desc.dq / dk / dv.                            */
+ * bh >= L*bq; dbias is written in the same layout.  The backward runs the
+ * prep pass (dO, dGpre, Dq, the gate-bias sums), the dq kernel (dbias as
+ * fp32 partials over chunks of batch rows, summed in order) and the dk/dv
+ * kernel; desc.workspace >= evo_attn_flash_bwd_workspace_bytes.          */
 EVO_API int evo_attn_flash_fwd(const evo_attn_desc *d, void *stream);
-EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq,
-                               int64_t rb, int64_t rl, float *dbias_part, int64_t chunk,
-                               void *stream);
+EVO_API size_t evo_attn_flash_bwd_workspace_bytes(const evo_attn_desc *d);
+EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, void *stream);
 
 /* Deterministic reduction over the leading axis:
  * dst(i, j) (+)= sum_{b<nb} src[b*n1*n2 + i*n2 + j], dst at

@@ -72,8 +72,8 @@ _SIGS = {
     "evo_attn_long_softmax": (c_i32, [c_i64, c_i32, c_i32, c_i64, c_vp, c_vp, c_i64, c_i64,
                                       c_i64, c_vp, c_vp, c_vp]),
     "evo_attn_flash_fwd": (c_i32, [C.POINTER(AttnDesc), c_vp]),
-    "evo_attn_flash_bwd": (c_i32, [C.POINTER(AttnDesc), c_vp, c_vp, c_i64, c_i64, c_vp, c_i64,
-                                   c_vp]),
+    "evo_attn_flash_bwd": (c_i32, [C.POINTER(AttnDesc), c_vp]),
+    "evo_attn_flash_bwd_workspace_bytes": (c_sz, [C.POINTER(AttnDesc)]),
     "evo_attn_long_gate": (c_i32, [c_i64, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp]),
     "evo_attn_long_prep": (c_i32, [c_i64, c_i32, c_i32, c_vp, c_vp, c_i64, c_vp, c_vp, c_vp,
                                    c_i64, c_vp, c_vp]),

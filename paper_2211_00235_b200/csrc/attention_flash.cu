@@ -21,19 +21,27 @@
 //   dV += P^T dO_j, dK += dS^T Q_j (TS MMAs).
 // The prep pass (dO = dGM G, dGpre, Dq = rowsum(dO O)) is attention_long's.
 // Bias: plain [H][L][bq] fp32 (the caller copies a transposed bias plain).
+#include <algorithm>
+
 #include "common.cuh"
 #include "tc_common.cuh"
 
 namespace evo {
 void note_backend(int b);
+int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart, cudaStream_t st);
+int reduce_lead(int, int64_t, int64_t, int64_t, const void *, float *, int64_t, int64_t, int,
+                cudaStream_t);
 namespace {
 using namespace tc;
 
 constexpr float LOG2E_F = 1.4426950408889634f;
 constexpr int QT = 128;    // queries (fwd / dq) or keys (dkv) per CTA = UMMA M
 constexpr int KT = 64;     // streamed tile (keys, or queries in dkv) = UMMA N
-constexpr int NEW = 8;     // elementwise warps: two threads per TMEM lane (row)
-constexpr int NTH = (NEW + 1) * 32;
+// each kernel: TPR elementwise threads per TMEM lane (row), EPT = KT / TPR
+// elements each, NEW = 4 TPR elementwise warps + 1 issuer warp
+constexpr int TPR_FWD = 2, TPR_BWD = 4;   // fwd: 2 CTAs / SM; dq, dkv: 1 (512 TMEM cols)
+constexpr int NS_FWD = 2, NS_BWD = 4;     // streamed-tile stages
+constexpr int nth_of(int tpr) { return (4 * tpr + 1) * 32; }
 constexpr uint32_t BIAS_TILE = 2 * 16384;  // two [128 x 32] fp32 SW128 boxes
 
 struct FlashArgs {
@@ -45,8 +53,7 @@ struct FlashArgs {
   bf16 *o, *gm;             // [rows, hc] with o_sb / o_sl
   int64_t o_sb, o_sl;
   float *lse;               // [nb, H, L]
-  const float *Dq;          // [rows, H] by activation row id
-  int64_t rb, rl;           // activation row id = b*rb + l*rl
+  const float *Dq;          // [nb, H, L]
   bf16 *dq, *dk, *dv;       // proj-gradient columns (q's strides)
   float *dbias_part;        // [chunks][H][L][L] (dq kernel)
   int64_t chunk;
@@ -82,38 +89,48 @@ __device__ __forceinline__ float2 upk2(uint32_t u) {
 }
 template <int N>
 __device__ __forceinline__ void tld(uint32_t taddr, uint32_t (&v)[N]) {
-  static_assert(N == 8 || N == 16 || N == 32, "tmem load width");
+  static_assert(N == 4 || N == 8 || N == 16 || N == 32, "tmem load width");
   if constexpr (N == 32) {
     tmem_ld32_nw(taddr, v);
   } else if constexpr (N == 16) {
     tmem_ld16_nw(taddr, v);
-  } else {
+  } else if constexpr (N == 8) {
     asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
                  : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]),
                    "=r"(v[6]), "=r"(v[7])
+                 : "r"(taddr));
+  } else {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
                  : "r"(taddr));
   }
 }
 template <int N>
 __device__ __forceinline__ void tst(uint32_t taddr, const uint32_t (&v)[N]) {
-  static_assert(N == 8 || N == 16, "tmem store width");
+  static_assert(N == 4 || N == 8 || N == 16, "tmem store width");
   if constexpr (N == 16) {
     tmem_st16(taddr, v);
-  } else {
+  } else if constexpr (N == 8) {
     asm volatile(
         "tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(taddr),
         "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7])
         : "memory");
+  } else {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(taddr),
+                 "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3])
+                 : "memory");
   }
 }
 
-// 32 bias values of query row `row` (keys kk*32 .. +31 of the tile) from a
-// [128 rows x 32] fp32 SW128 box
-__device__ __forceinline__ void bias_row(const uint8_t *box, int row, float (&out)[32]) {
-  const uint8_t *base = box + row * 128;
+// EPT bias values of query row `row`, tile keys k0 .. k0+EPT-1 (k0 % EPT ==
+// 0), from the stage's two [128 rows x 32] fp32 SW128 boxes
+template <int EPT>
+__device__ __forceinline__ void bias_row(const uint8_t *tile, int row, int k0, float (&out)[EPT]) {
+  const uint8_t *base = tile + (k0 >> 5) * 16384 + row * 128;
+  const int c0 = (k0 & 31) >> 2;
 #pragma unroll
-  for (int c = 0; c < 8; ++c) {
-    const float4 v = *reinterpret_cast<const float4 *>(base + ((c ^ (row & 7)) << 4));
+  for (int c = 0; c < EPT / 4; ++c) {
+    const float4 v = *reinterpret_cast<const float4 *>(base + (((c0 + c) ^ (row & 7)) << 4));
     out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
   }
 }
@@ -125,22 +142,24 @@ __device__ __forceinline__ float bias_at(const uint8_t *box, int q, int kk) {
 
 // ======================================================================= fwd
 // TMEM: buffer i at 96 i: S (64 fp32) | P (32 bf16 pairs);  O at 192.
+// Softmax warp w: lane quadrant w & 3 (rows), part w >> 2 (EPT keys).
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(nth_of(TPR_FWD), 1)
 attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                       const FlashArgs a) {
-  constexpr int NS = 2;                                // K/V(/bias) stages
+  constexpr int TPR = TPR_FWD, EPT = KT / TPR, NEW = 4 * TPR;
+  constexpr int NS = NS_FWD;                           // K/V(/bias) stages
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;                          // NS x [bias | K | V]
   uint8_t *sQ = sStage + NS * STG;
-  float *sX = reinterpret_cast<float *>(sQ + QB);      // [2 parity][2 half][128] max exchange
-  float *sL = sX + 2 * 2 * 128;                        // [2 half][128] row sums
-  // 0 Q, 1-2 stage full, 3-4 S done, 5-6 P packed (8 warps), 7-8 PV done
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sL + 2 * 128);
+  float *sX = reinterpret_cast<float *>(sQ + QB);      // [2 parity][TPR][128] max exchange
+  float *sL = sX + 2 * TPR * 128;                      // [TPR][128] row sums
+  // 0 Q, 1-2 stage full, 3-4 S done, 5-6 P packed (NEW warps), 7-8 PV done
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sL + TPR * 128);
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 9);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -216,7 +235,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     }
   } else {
     // ------------------------------------------------------------ softmax
-    const int quad = warp & 3, hf = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;
     const int t = quad * 32 + lane;
     const int q = q0 + t;
     const bool qv = q < L;
@@ -225,28 +244,29 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     float m_run = -INFINITY, l = 0.f;
     for (int j = 0; j < T; ++j) {
       const int bi = j & 1, st = j % NS;
-      const int kb = j * KT + hf * 32;          // first key of this thread's 32
+      const int kb = j * KT + part * EPT;        // first key of this thread's EPT
       if (BIAS) mbar_wait(&bars[1 + st], (uint32_t)((j / NS) & 1));  // bias tile landed
       mbar_wait(&bars[3 + bi], (uint32_t)((j >> 1) & 1));
       fence_after();
-      uint32_t sv[32];
-      tld<32>(lane_addr + bi * 96 + hf * 32, sv);
-      float bb[32];
-      if (BIAS) bias_row(sStage + st * STG + hf * 16384, t, bb);
+      uint32_t sv[EPT];
+      tld<EPT>(lane_addr + bi * 96 + part * EPT, sv);
+      float bb[EPT];
+      if (BIAS) bias_row(sStage + st * STG, t, part * EPT, bb);
       tmem_wait_ld();
-      float x[32];
+      float x[EPT];
       float mt = -INFINITY;
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
+      for (int k = 0; k < EPT; ++k) {
         float v = __uint_as_float(sv[k]) * sc_l2;
         if (BIAS) v = fmaf(bb[k], LOG2E_F, v);
         x[k] = (kb + k < L) ? v : -INFINITY;
         mt = fmaxf(mt, x[k]);
       }
-      float *sx = sX + bi * 256;
-      sx[hf * 128 + t] = mt;
-      named_bar_sync(1 + quad, 64);             // the row's two halves
-      mt = fmaxf(sx[t], sx[128 + t]);
+      float *sx = sX + bi * (TPR * 128);
+      sx[part * 128 + t] = mt;
+      named_bar_sync(1 + quad, 32 * TPR);       // the row's TPR parts
+#pragma unroll
+      for (int p2 = 0; p2 < TPR; ++p2) mt = fmaxf(mt, sx[p2 * 128 + t]);
       const bool grow = mt > m_run + 8.f;
       float alpha = 1.f;
       if (grow) {
@@ -254,29 +274,29 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         m_run = mt;
       }
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
-        // rescale this row's half of O once PV of the previous tile is done
+        // rescale this row's part of O once PV of the previous tile is done
         const int i = j - 1;
         mbar_wait(&bars[7 + (i & 1)], (uint32_t)((i >> 1) & 1));
         fence_after();
-        constexpr int HD = D / 2;
-        uint32_t ov[HD];
-        tld<HD>(lane_addr + 192 + hf * HD, ov);
+        constexpr int OD = D / TPR;
+        uint32_t ov[OD];
+        tld<OD>(lane_addr + 192 + part * OD, ov);
         tmem_wait_ld();
         if (grow) {
 #pragma unroll
-          for (int c = 0; c < HD; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
+          for (int c = 0; c < OD; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
         }
-        tst<HD>(lane_addr + 192 + hf * HD, ov);
+        tst<OD>(lane_addr + 192 + part * OD, ov);
       }
       l *= alpha;
-      uint32_t pk[16];
+      uint32_t pk[EPT / 2];
 #pragma unroll
-      for (int k = 0; k < 32; k += 2) {
+      for (int k = 0; k < EPT; k += 2) {
         const float p0 = ex2f(x[k] - m_run), p1 = ex2f(x[k + 1] - m_run);
         l += p0 + p1;
         pk[k >> 1] = pk2(p0, p1);
       }
-      tst<16>(lane_addr + bi * 96 + 64 + hf * 16, pk);
+      tst<EPT / 2>(lane_addr + bi * 96 + 64 + part * (EPT / 2), pk);
       tmem_st_wait();
       fence_before();
       __syncwarp();
@@ -286,39 +306,49 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     const int i = T - 1;
     mbar_wait(&bars[7 + (i & 1)], (uint32_t)((i >> 1) & 1));
     fence_after();
-    sL[hf * 128 + t] = l;
-    named_bar_sync(1 + quad, 64);
-    const float lt = sL[t] + sL[128 + t];
-    constexpr int HD = D / 2;
-    uint32_t ov[HD];
-    tld<HD>(lane_addr + 192 + hf * HD, ov);
+    sL[part * 128 + t] = l;
+    named_bar_sync(1 + quad, 32 * TPR);
+    float lt = 0.f;
+#pragma unroll
+    for (int p2 = 0; p2 < TPR; ++p2) lt += sL[p2 * 128 + t];
+    constexpr int OD = D / TPR;
+    uint32_t ov[OD];
+    tld<OD>(lane_addr + 192 + part * OD, ov);
     tmem_wait_ld();
     if (qv) {
       const float inv = 1.f / lt;
-      const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D + hf * HD;
-      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D + hf * HD;
-      uint32_t o2[HD / 2], g2[HD / 2];
+      const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D + part * OD;
+      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D + part * OD;
+      // OD = D / TPR consecutive columns: 16-byte chunks (OD % 8 == 0) or one
+      // 8-byte chunk (OD == 4)
+      constexpr int CW = OD % 8 == 0 ? 8 : 4;
 #pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        const uint4 gq = *reinterpret_cast<const uint4 *>(gp + 8 * c);
-        const uint32_t gw[4] = {gq.x, gq.y, gq.z, gq.w};
+      for (int c0 = 0; c0 < OD; c0 += CW) {
+        uint32_t gw[CW / 2], o2[CW / 2], g2[CW / 2];
+        if constexpr (CW == 8) {
+          const uint4 gq = *reinterpret_cast<const uint4 *>(gp + c0);
+          gw[0] = gq.x; gw[1] = gq.y; gw[2] = gq.z; gw[3] = gq.w;
+        } else {
+          const uint2 gq = *reinterpret_cast<const uint2 *>(gp + c0);
+          gw[0] = gq.x; gw[1] = gq.y;
+        }
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const float v0 = __uint_as_float(ov[8 * c + 2 * e]) * inv;
-          const float v1 = __uint_as_float(ov[8 * c + 2 * e + 1]) * inv;
+        for (int e = 0; e < CW / 2; ++e) {
+          const float v0 = __uint_as_float(ov[c0 + 2 * e]) * inv;
+          const float v1 = __uint_as_float(ov[c0 + 2 * e + 1]) * inv;
           const float2 gg = upk2(gw[e]);
-          o2[4 * c + e] = pk2(v0, v1);
-          g2[4 * c + e] = pk2(gg.x * v0, gg.y * v1);
+          o2[e] = pk2(v0, v1);
+          g2[e] = pk2(gg.x * v0, gg.y * v1);
+        }
+        if constexpr (CW == 8) {
+          *reinterpret_cast<uint4 *>(a.o + ooff + c0) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+          *reinterpret_cast<uint4 *>(a.gm + ooff + c0) = make_uint4(g2[0], g2[1], g2[2], g2[3]);
+        } else {
+          *reinterpret_cast<uint2 *>(a.o + ooff + c0) = make_uint2(o2[0], o2[1]);
+          *reinterpret_cast<uint2 *>(a.gm + ooff + c0) = make_uint2(g2[0], g2[1]);
         }
       }
-#pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        *reinterpret_cast<uint4 *>(a.o + ooff + 8 * c) =
-            make_uint4(o2[4 * c], o2[4 * c + 1], o2[4 * c + 2], o2[4 * c + 3]);
-        *reinterpret_cast<uint4 *>(a.gm + ooff + 8 * c) =
-            make_uint4(g2[4 * c], g2[4 * c + 1], g2[4 * c + 2], g2[4 * c + 3]);
-      }
-      if (hf == 0) a.lse[(b * a.H + h) * (int64_t)L + q] = m_run * (1.f / LOG2E_F) + logf(lt);
+      if (part == 0) a.lse[(b * a.H + h) * (int64_t)L + q] = m_run * (1.f / LOG2E_F) + logf(lt);
     }
   }
   fence_before();
@@ -326,24 +356,46 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
+// store OD fp32 TMEM values (x scale) as bf16 at dst (OD = 8: 16 B, 4: 8 B)
+template <int OD>
+__device__ __forceinline__ void store_row_bf16(bf16 *dst, const uint32_t (&v)[OD], float scale) {
+  constexpr int CW = OD % 8 == 0 ? 8 : 4;
+#pragma unroll
+  for (int c0 = 0; c0 < OD; c0 += CW) {
+    uint32_t w[CW / 2];
+#pragma unroll
+    for (int e = 0; e < CW / 2; ++e)
+      w[e] = pk2(__uint_as_float(v[c0 + 2 * e]) * scale,
+                 __uint_as_float(v[c0 + 2 * e + 1]) * scale);
+    if constexpr (CW == 8)
+      *reinterpret_cast<uint4 *>(dst + c0) = make_uint4(w[0], w[1], w[2], w[3]);
+    else
+      *reinterpret_cast<uint2 *>(dst + c0) = make_uint2(w[0], w[1]);
+  }
+}
+
 // ======================================================================== dq
 // TMEM: buffer i at 160 i: S (64) | dP (64) | dS (32 bf16 pairs); dQ at 320.
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(nth_of(TPR_BWD), 1)
 attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                      const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
-  constexpr int NS = 2;
+  constexpr int TPR = TPR_BWD, EPT = KT / TPR, NEW = 4 * TPR;
+  constexpr int NS = NS_BWD;
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;
   uint8_t *sQ = sStage + NS * STG;                     // Q | dO of the current row
-  // 0 row Q/dO, 1-2 stage full, 3-4 S/dP done, 5-6 dS packed (8 warps),
-  // 7-8 dQ MMA done, 9 row's dQ read back (8 warps)
+  // 0 row Q/dO, 1-2 stage full, 3-4 S/dP done, 5-6 dS packed (NEW warps),
+  // 7-8 dQ MMA done, 9 row's dQ read back (NEW warps)
   uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + 2 * QB);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 10);
+  uint64_t *fullb = bars + 1, *sdone = fullb + NS, *dsp = sdone + 2, *dqd = dsp + 2,
+           *dqr = dqd + 2;
+  constexpr int NBAR = 1 + NS + 7;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
@@ -355,8 +407,10 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   const int G = nrows * T;                             // tiles over the chunk
 
   if (tid == NEW * 32) {
-    for (int i = 0; i < 10; ++i)
-      mbar_init(&bars[i], (i == 5 || i == 6 || i == 9) ? NEW : 1);
+    for (int i = 0; i < NBAR; ++i) {
+      uint64_t *bb = &bars[i];
+      mbar_init(bb, (bb == &dsp[0] || bb == &dsp[1] || bb == dqr) ? NEW : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -370,7 +424,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       const int64_t b = b_lo + g / T;
       const int j = g % T;
       uint8_t *st = sStage + (g % NS) * STG;
-      uint64_t *bar = &bars[1 + (g % NS)];
+      uint64_t *bar = &fullb[g % NS];
       if (lane == 0) {
         mbar_expect_tx(bar, STG);
         if (BIAS) {
@@ -404,7 +458,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         const int j = g % T;
         if (j == 0) mbar_wait(&bars[0], (uint32_t)(r & 1));   // row's Q / dO landed
         const int st = g % NS;
-        mbar_wait(&bars[1 + st], (uint32_t)((g / NS) & 1));
+        mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0), sV = sK + KB;
         const uint32_t d = tmem + (g & 1) * 160;
@@ -414,40 +468,40 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d + 64, desc_k<D>(sdOa, ks), desc_k<D>(sV, ks), idesc_s, ks > 0);
-        umma_commit_el(&bars[3 + (g & 1)]);
+        umma_commit_el(&sdone[g & 1]);
         if (j == T - 1 && r + 1 < nrows) {
           // the row's last S/dP MMAs read Q / dO: reload them for the next row
-          mbar_wait(&bars[3 + (g & 1)], (uint32_t)((g >> 1) & 1));
+          mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));
           load_row(b_lo + r + 1);
         }
       }
       if (g >= 1) {
         const int i = g - 1, bi = i & 1, st = i % NS;
         const int ji = i % T;
-        mbar_wait(&bars[5 + bi], (uint32_t)((i >> 1) & 1));   // dS_i packed
-        if (ji == 0 && i > 0) mbar_wait(&bars[9], (uint32_t)(((i / T) - 1) & 1));  // dQ read
+        mbar_wait(&dsp[bi], (uint32_t)((i >> 1) & 1));   // dS_i packed
+        if (ji == 0 && i > 0) mbar_wait(dqr, (uint32_t)(((i / T) - 1) & 1));  // dQ read
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
           umma_bf16_ts_el(tmem + 320, tmem + bi * 160 + 128 + 8 * ks, desc_mn<D>(sK, ks), idesc_o,
                           (ji > 0 || ks > 0) ? 1u : 0u);
-        umma_commit_el(&bars[7 + bi]);
+        umma_commit_el(&dqd[bi]);
         if (i + NS < G) {
-          mbar_wait(&bars[7 + bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
+          mbar_wait(&dqd[bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
           load_tile(i + NS);
         }
       }
     }
   } else {
-    const int quad = warp & 3, hf = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;
     const int t = quad * 32 + lane;
     const int q = q0 + t;
     const bool qv = q < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
     float lse_l2 = 0.f, dq_ = 0.f;
-    float *part = BIAS ? a.dbias_part + (int64_t)blockIdx.z * a.H * L * (int64_t)L +
+    float *prow = BIAS ? a.dbias_part + (int64_t)blockIdx.z * a.H * L * (int64_t)L +
                              ((int64_t)h * L + q) * L
                        : nullptr;
     for (int g = 0; g < G; ++g) {
@@ -455,75 +509,77 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       const int64_t b = b_lo + r;
       if (j == 0) {
         lse_l2 = qv ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E_F : 0.f;
-        dq_ = qv ? a.Dq[(b * a.rb + (int64_t)q * a.rl) * a.H + h] : 0.f;
+        dq_ = qv ? a.Dq[(b * a.H + h) * (int64_t)L + q] : 0.f;
       }
-      const int kb = j * KT + hf * 32;
-      if (BIAS) mbar_wait(&bars[1 + st], (uint32_t)((g / NS) & 1));  // bias tile landed
-      mbar_wait(&bars[3 + bi], (uint32_t)((g >> 1) & 1));
-      fence_after();
-      uint32_t sv[32], dv[32];
-      tld<32>(lane_addr + bi * 160 + hf * 32, sv);
-      tld<32>(lane_addr + bi * 160 + 64 + hf * 32, dv);
-      float bb[32];
-      if (BIAS) bias_row(sStage + st * STG + hf * 16384, t, bb);
-      tmem_wait_ld();
-      uint32_t pk[16];
-      float ds[32];
+      const int kb = j * KT + part * EPT;
+      float *dst = prow + kb;
+      // the chunk's dbias partial of this thread's keys, loaded before the
+      // wait so its L2 latency overlaps the MMAs (one owner thread per element)
+      const bool pvec = BIAS && qv && r > 0 && kb + EPT <= L &&
+                        (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
+      float old[EPT];
+      if (pvec) {
 #pragma unroll
-      for (int k = 0; k < 32; ++k) {
+        for (int c = 0; c < EPT / 4; ++c) {
+          const float4 o = *reinterpret_cast<const float4 *>(dst + 4 * c);
+          old[4 * c] = o.x; old[4 * c + 1] = o.y; old[4 * c + 2] = o.z; old[4 * c + 3] = o.w;
+        }
+      }
+      if (BIAS) mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));  // bias tile landed
+      mbar_wait(&sdone[bi], (uint32_t)((g >> 1) & 1));
+      fence_after();
+      uint32_t sv[EPT], dv[EPT];
+      tld<EPT>(lane_addr + bi * 160 + part * EPT, sv);
+      tld<EPT>(lane_addr + bi * 160 + 64 + part * EPT, dv);
+      float bb[EPT];
+      if (BIAS) bias_row(sStage + st * STG, t, part * EPT, bb);
+      tmem_wait_ld();
+      uint32_t pk[EPT / 2];
+      float ds[EPT];
+#pragma unroll
+      for (int k = 0; k < EPT; ++k) {
         float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
         if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
         const float p = (qv && kb + k < L) ? ex2f(x) : 0.f;
         ds[k] = p * (__uint_as_float(dv[k]) - dq_);
       }
 #pragma unroll
-      for (int k = 0; k < 32; k += 2) pk[k >> 1] = pk2(ds[k], ds[k + 1]);
-      tst<16>(lane_addr + bi * 160 + 128 + hf * 16, pk);
+      for (int k = 0; k < EPT; k += 2) pk[k >> 1] = pk2(ds[k], ds[k + 1]);
+      tst<EPT / 2>(lane_addr + bi * 160 + 128 + part * (EPT / 2), pk);
       if (BIAS && qv) {
-        float *dst = part + kb;
-        if (kb + 32 <= L && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        if (kb + EPT <= L && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
 #pragma unroll
-          for (int c = 0; c < 8; ++c) {
+          for (int c = 0; c < EPT / 4; ++c) {
             float4 v = make_float4(ds[4 * c], ds[4 * c + 1], ds[4 * c + 2], ds[4 * c + 3]);
-            if (r > 0) {
-              const float4 o = *reinterpret_cast<const float4 *>(dst + 4 * c);
-              v.x += o.x; v.y += o.y; v.z += o.z; v.w += o.w;
+            if (pvec) {
+              v.x += old[4 * c]; v.y += old[4 * c + 1]; v.z += old[4 * c + 2];
+              v.w += old[4 * c + 3];
             }
             *reinterpret_cast<float4 *>(dst + 4 * c) = v;
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < 32; ++k)
+          for (int k = 0; k < EPT; ++k)
             if (kb + k < L) dst[k] = r > 0 ? dst[k] + ds[k] : ds[k];
         }
       }
       tmem_st_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[5 + bi]);
+      if (lane == 0) mbar_arrive(&dsp[bi]);
       if (j == T - 1) {
         // the row's dQ: wait for its last dQ MMA, scale, store
-        mbar_wait(&bars[7 + bi], (uint32_t)((g >> 1) & 1));
+        mbar_wait(&dqd[bi], (uint32_t)((g >> 1) & 1));
         fence_after();
-        constexpr int HD = D / 2;
-        uint32_t v[HD];
-        tld<HD>(lane_addr + 320 + hf * HD, v);
+        constexpr int OD = D / TPR;
+        uint32_t v[OD];
+        tld<OD>(lane_addr + 320 + part * OD, v);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&bars[9]);
-        if (qv) {
-          bf16 *dst = a.dq + b * a.sb + (int64_t)q * a.sl + h * D + hf * HD;
-#pragma unroll
-          for (int c = 0; c < HD / 8; ++c) {
-            uint32_t w[4];
-#pragma unroll
-            for (int e = 0; e < 4; ++e)
-              w[e] = pk2(__uint_as_float(v[8 * c + 2 * e]) * a.scale,
-                         __uint_as_float(v[8 * c + 2 * e + 1]) * a.scale);
-            *reinterpret_cast<uint4 *>(dst + 8 * c) = make_uint4(w[0], w[1], w[2], w[3]);
-          }
-        }
+        if (lane == 0) mbar_arrive(dqr);
+        if (qv) store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v,
+                                   a.scale);
       }
     }
   }
@@ -535,34 +591,44 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
 // ======================================================================= dkv
 // CTA = 128 keys; the queries stream in tiles of 64.  TMEM: buffer i at
 // 192 i: S^T (64) | dP^T (64) | P^T (32 pairs) | dS^T (32 pairs);
-// dK at 384, dV at 384 + D.
+// dK at 384, dV at 384 + D.  lse (log2 units) and Dq of all L queries are
+// staged in smem once per CTA.
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(NTH, 1)
+__global__ void __launch_bounds__(nth_of(TPR_BWD), 1)
 attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                       const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
-  constexpr int NS = 2;
+  constexpr int TPR = TPR_BWD, EPT = KT / TPR, NEW = 4 * TPR;
+  constexpr int NS = NS_BWD;
   constexpr uint32_t KB = QT * Sw<D>::bytes, QB = KT * Sw<D>::bytes;
-  // stage: bias [64 q x 128 k] as four [64 x 32] SW128 boxes | Q | dO | lse | Dq
+  // stage: bias [64 q x 128 k] as four [64 x 32] SW128 boxes | Q | dO
   constexpr uint32_t BT = BIAS ? 4 * 8192 : 0;
-  constexpr uint32_t STG = (BT + 2 * QB + 2 * KT * 4 + 1023) / 1024 * 1024;
+  constexpr uint32_t STG = (BT + 2 * QB + 1023) / 1024 * 1024;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;
   uint8_t *sK = sStage + NS * STG;                     // K | V of the CTA's keys
-  // 0 K/V, 1-2 stage TMA full, 3-4 stage lse/Dq staged, 5-6 S/dP done,
-  // 7-8 P/dS packed (8 warps), 9-10 dK/dV MMAs done
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sK + 2 * KB);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 11);
+  const int L = a.L;
+  const int T = (L + KT - 1) / KT;
+  float *sLse = reinterpret_cast<float *>(sK + 2 * KB);  // [T*KT] each
+  float *sDq = sLse + T * KT;
+  // 0 K/V, 1-2 stage TMA full, 3 lse/Dq staged, 5-6 S/dP done,
+  // 7-8 P/dS packed (NEW warps), 9-10 dK/dV MMAs done
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + T * KT);
+  uint64_t *fullb = bars + 1, *lsb = fullb + NS, *sdone = lsb + 1, *pp2 = sdone + 2,
+           *mmd = pp2 + 2;
+  constexpr int NBAR = 1 + NS + 7;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = blockIdx.x * QT, h = blockIdx.y;
   const int64_t b = blockIdx.z;
-  const int L = a.L;
-  const int T = (L + KT - 1) / KT;
 
   if (tid == NEW * 32) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i == 7 || i == 8) ? NEW : 1);
+    for (int i = 0; i < NBAR; ++i) {
+      uint64_t *bb = &bars[i];
+      mbar_init(bb, (bb == &pp2[0] || bb == &pp2[1]) ? NEW : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 512);
@@ -574,7 +640,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   if (warp == NEW) {
     auto load_tile = [&](int j) {
       uint8_t *st = sStage + (j % NS) * STG;
-      uint64_t *bar = &bars[1 + (j % NS)];
+      uint64_t *bar = &fullb[j % NS];
       if (lane == 0) {
         mbar_expect_tx(bar, BT + 2 * QB);
         if (BIAS) {
@@ -584,16 +650,6 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         tma_load_4d(st + BT, &mQ, bar, 0, j * KT, (int)b, h);
         tma_load_4d(st + BT + QB, &mdO, bar, 0, j * KT, (int)b, h);
       }
-      // lse (log2 units) and Dq of the tile's 64 queries
-      float *sl = reinterpret_cast<float *>(st + BT + 2 * QB), *sd = sl + KT;
-#pragma unroll
-      for (int e = 0; e < 2; ++e) {
-        const int qi = lane + 32 * e, q = j * KT + qi;
-        sl[qi] = q < L ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E_F : 0.f;
-        sd[qi] = q < L ? a.Dq[(b * a.rb + (int64_t)q * a.rl) * a.H + h] : 0.f;
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[3 + (j % NS)]);
       __syncwarp();
     };
     if (lane == 0) {
@@ -603,6 +659,17 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     }
     __syncwarp();
     for (int j = 0; j < NS && j < T; ++j) load_tile(j);
+    {
+      const float *lp = a.lse + (b * a.H + h) * (int64_t)L;
+      const float *dp = a.Dq + (b * a.H + h) * (int64_t)L;
+      for (int qi = lane; qi < T * KT; qi += 32) {
+        sLse[qi] = qi < L ? lp[qi] * LOG2E_F : 0.f;
+        sDq[qi] = qi < L ? dp[qi] : 0.f;
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(lsb);
+      __syncwarp();
+    }
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
     const uint32_t sKa = smem_u32(sK), sVa = sKa + KB;
@@ -610,7 +677,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     for (int j = 0; j <= T; ++j) {
       if (j < T) {
         const int st = j % NS;
-        mbar_wait(&bars[1 + st], (uint32_t)((j / NS) & 1));
+        mbar_wait(&fullb[st], (uint32_t)((j / NS) & 1));
         fence_after();
         const uint32_t sQ = smem_u32(sStage + st * STG) + BT, sdO = sQ + QB;
         const uint32_t d = tmem + (j & 1) * 192;
@@ -620,11 +687,11 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d + 64, desc_k<D>(sVa, ks), desc_k<D>(sdO, ks), idesc_s, ks > 0);
-        umma_commit_el(&bars[5 + (j & 1)]);
+        umma_commit_el(&sdone[j & 1]);
       }
       if (j >= 1) {
         const int i = j - 1, bi = i & 1, st = i % NS;
-        mbar_wait(&bars[7 + bi], (uint32_t)((i >> 1) & 1));   // P^T / dS^T packed
+        mbar_wait(&pp2[bi], (uint32_t)((i >> 1) & 1));   // P^T / dS^T packed
         fence_after();
         const uint32_t sQ = smem_u32(sStage + st * STG) + BT, sdO = sQ + QB;
         const uint32_t base = tmem + bi * 192;
@@ -636,37 +703,36 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         for (int ks = 0; ks < KT / 16; ++ks)
           umma_bf16_ts_el(tmem + 384, base + 160 + 8 * ks, desc_mn<D>(sQ, ks), idesc_o,
                           (i > 0 || ks > 0) ? 1u : 0u);
-        umma_commit_el(&bars[9 + bi]);
+        umma_commit_el(&mmd[bi]);
         if (i + NS < T) {
-          mbar_wait(&bars[9 + bi], (uint32_t)((i >> 1) & 1));
+          mbar_wait(&mmd[bi], (uint32_t)((i >> 1) & 1));
           load_tile(i + NS);
         }
       }
     }
   } else {
-    const int quad = warp & 3, hf = warp >> 2;
+    const int quad = warp & 3, part = warp >> 2;
     const int t = quad * 32 + lane;                    // key row of the tile
     const int k = k0 + t;
     const bool kv = k < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
+    mbar_wait(lsb, 0);
     for (int j = 0; j < T; ++j) {
       const int bi = j & 1, st = j % NS;
-      const int qb = j * KT + hf * 32;          // first query of this thread's 32
-      mbar_wait(&bars[3 + st], (uint32_t)((j / NS) & 1));
-      if (BIAS) mbar_wait(&bars[1 + st], (uint32_t)((j / NS) & 1));  // bias tile landed
-      mbar_wait(&bars[5 + bi], (uint32_t)((j >> 1) & 1));
+      const int qb = j * KT + part * EPT;        // first query of this thread's EPT
+      if (BIAS) mbar_wait(&fullb[st], (uint32_t)((j / NS) & 1));  // bias tile landed
+      mbar_wait(&sdone[bi], (uint32_t)((j >> 1) & 1));
       fence_after();
-      uint32_t sv[32], dv[32];
-      tld<32>(lane_addr + bi * 192 + hf * 32, sv);
-      tld<32>(lane_addr + bi * 192 + 64 + hf * 32, dv);
+      uint32_t sv[EPT], dv[EPT];
+      tld<EPT>(lane_addr + bi * 192 + part * EPT, sv);
+      tld<EPT>(lane_addr + bi * 192 + 64 + part * EPT, dv);
       const uint8_t *stg = sStage + st * STG;
-      const float *sl = reinterpret_cast<const float *>(stg + BT + 2 * QB) + hf * 32;
-      const float *sd = sl + KT;
+      const float *sl = sLse + qb, *sd = sDq + qb;
       tmem_wait_ld();
-      uint32_t pp[16], pd[16];
+      uint32_t pp[EPT / 2], pd[EPT / 2];
 #pragma unroll
-      for (int c = 0; c < 32; c += 4) {
+      for (int c = 0; c < EPT; c += 4) {
         const float4 l4 = *reinterpret_cast<const float4 *>(sl + c);
         const float4 d4 = *reinterpret_cast<const float4 *>(sd + c);
         const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dq4[4] = {d4.x, d4.y, d4.z, d4.w};
@@ -675,7 +741,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         for (int e = 0; e < 4; ++e) {
           const int qq = c + e;
           float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lv[e]);
-          if (BIAS) x = fmaf(bias_at(stg + (t >> 5) * 8192, hf * 32 + qq, t & 31), LOG2E_F, x);
+          if (BIAS) x = fmaf(bias_at(stg + (t >> 5) * 8192, part * EPT + qq, t & 31), LOG2E_F, x);
           p[e] = (kv && qb + qq < L) ? ex2f(x) : 0.f;
           ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq4[e]);
         }
@@ -684,37 +750,26 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         pd[c >> 1] = pk2(ds[0], ds[1]);
         pd[(c >> 1) + 1] = pk2(ds[2], ds[3]);
       }
-      tst<16>(lane_addr + bi * 192 + 128 + hf * 16, pp);
-      tst<16>(lane_addr + bi * 192 + 160 + hf * 16, pd);
+      tst<EPT / 2>(lane_addr + bi * 192 + 128 + part * (EPT / 2), pp);
+      tst<EPT / 2>(lane_addr + bi * 192 + 160 + part * (EPT / 2), pd);
       tmem_st_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[7 + bi]);
+      if (lane == 0) mbar_arrive(&pp2[bi]);
     }
     // dK = scale * acc, dV = acc
     const int i = T - 1;
-    mbar_wait(&bars[9 + (i & 1)], (uint32_t)((i >> 1) & 1));
+    mbar_wait(&mmd[i & 1], (uint32_t)((i >> 1) & 1));
     fence_after();
-    constexpr int HD = D / 2;
-    uint32_t vk[HD], vv[HD];
-    tld<HD>(lane_addr + 384 + hf * HD, vk);
-    tld<HD>(lane_addr + 384 + D + hf * HD, vv);
+    constexpr int OD = D / TPR;
+    uint32_t vk[OD], vv[OD];
+    tld<OD>(lane_addr + 384 + part * OD, vk);
+    tld<OD>(lane_addr + 384 + D + part * OD, vv);
     tmem_wait_ld();
     if (kv) {
-      bf16 *dk = a.dk + b * a.sb + (int64_t)k * a.sl + h * D + hf * HD;
-      bf16 *dvp = a.dv + b * a.sb + (int64_t)k * a.sl + h * D + hf * HD;
-#pragma unroll
-      for (int c = 0; c < HD / 8; ++c) {
-        uint32_t wk[4], wv[4];
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          wk[e] = pk2(__uint_as_float(vk[8 * c + 2 * e]) * a.scale,
-                      __uint_as_float(vk[8 * c + 2 * e + 1]) * a.scale);
-          wv[e] = pk2(__uint_as_float(vv[8 * c + 2 * e]), __uint_as_float(vv[8 * c + 2 * e + 1]));
-        }
-        *reinterpret_cast<uint4 *>(dk + 8 * c) = make_uint4(wk[0], wk[1], wk[2], wk[3]);
-        *reinterpret_cast<uint4 *>(dvp + 8 * c) = make_uint4(wv[0], wv[1], wv[2], wv[3]);
-      }
+      const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D + part * OD;
+      store_row_bf16<OD>(a.dk + off, vk, a.scale);
+      store_row_bf16<OD>(a.dv + off, vv, 1.f);
     }
   }
   fence_before();
@@ -758,7 +813,7 @@ FlashArgs flash_args(const evo_attn_desc *d) {
   a.o = reinterpret_cast<bf16 *>(d->o); a.gm = reinterpret_cast<bf16 *>(d->gm);
   a.o_sb = d->o_sb; a.o_sl = d->o_sl;
   a.lse = d->lse;
-  a.Dq = nullptr; a.rb = 0; a.rl = 0;
+  a.Dq = nullptr;
   a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
   a.dv = reinterpret_cast<bf16 *>(d->dv);
   a.dbias_part = nullptr; a.chunk = 1;
@@ -775,12 +830,39 @@ int check_flash(const evo_attn_desc *d, bool bwd) {
   EVO_REQUIRE(d->sb % 8 == 0 && d->sl % 8 == 0 && d->o_sb % 8 == 0 && d->o_sl % 8 == 0 &&
                   al16(d->q) && al16(d->k) && al16(d->v) && al16(d->g) && al16(d->o),
               EVO_EUNSUP, "attention_flash: 16-byte aligned rows required");
-  EVO_REQUIRE(!d->bias || (d->bk == 1 && d->bq % 4 == 0 && d->bh % 4 == 0 && al16(d->bias)),
+  EVO_REQUIRE(!d->bias || (d->bk == 1 && d->bq % 4 == 0 && d->bh % 4 == 0 &&
+                           d->bh >= (int64_t)d->L * d->bq && al16(d->bias)),
               EVO_EUNSUP, "attention_flash: plain bias rows (bk = 1, bq %% 4 == 0) required");
   if (bwd)
     EVO_REQUIRE(al16(d->dq) && al16(d->dk) && al16(d->dv) && al16(d->dgm), EVO_EUNSUP,
                 "attention_flash: 16-byte aligned gradient rows required");
   return EVO_OK;
+}
+
+// batch rows per dq CTA: about two CTAs per SM over (q tiles x heads x chunks)
+int64_t flash_chunk(const evo_attn_desc *d, int64_t &nch) {
+  const int64_t qt = (d->L + QT - 1) / QT;
+  nch = std::max<int64_t>(1, std::min<int64_t>(d->nb, 2 * num_sms() / std::max<int64_t>(1, qt * d->H)));
+  const int64_t chunk = (d->nb + nch - 1) / nch;
+  nch = (d->nb + chunk - 1) / chunk;
+  return chunk;
+}
+
+struct FlashWs {
+  size_t dO, Dq, gate, part, total;
+};
+FlashWs flash_ws(const evo_attn_desc *d) {
+  FlashWs w;
+  auto pad = [](size_t x) { return (x + 255) / 256 * 256; };
+  const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * d->D;
+  w.dO = 0;
+  w.Dq = pad((size_t)span * 2);
+  w.gate = w.Dq + pad((size_t)d->nb * d->H * d->L * 4);
+  w.part = w.gate + pad((size_t)num_sms() * 8 * d->H * d->D * 4);
+  int64_t nch;
+  flash_chunk(d, nch);
+  w.total = w.part + (d->bias ? pad((size_t)nch * d->H * d->L * d->L * 4) : 0);
+  return w;
 }
 
 template <int D, bool BIAS>
@@ -797,27 +879,34 @@ int flash_fwd(const evo_attn_desc *d, cudaStream_t st) {
     mb = mq;
   }
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-  const size_t smem = 2 * STG + QT * 2 * D + (4 * 128 + 2 * 128) * 4 + 9 * 8 + 16;
+  const size_t smem = NS_FWD * STG + QT * 2 * D + (3 * TPR_FWD * 128) * 4 + 9 * 8 + 16;
   auto kfn = attn_flash_fwd_kernel<D, BIAS>;
   EVO_MAX_SMEM_ONCE(kfn);
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
-  kfn<<<grid, NTH, smem, st>>>(mq, mk, mv, mb, a);
+  kfn<<<grid, nth_of(TPR_FWD), smem, st>>>(mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_flash_fwd_kernel");
   return EVO_OK;
 }
 
 template <int D, bool BIAS>
-int flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq, int64_t rb, int64_t rl,
-              float *dbias_part, int64_t chunk, cudaStream_t st) {
+int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   FlashArgs a = flash_args(d);
-  a.Dq = Dq; a.rb = rb; a.rl = rl;
-  a.dbias_part = dbias_part;
-  a.chunk = chunk;
-  const int64_t hc = (int64_t)d->H * D;
+  const FlashWs w = flash_ws(d);
+  EVO_REQUIRE(d->workspace && d->workspace_bytes >= w.total, EVO_EARG,
+              "attention_flash bwd: workspace needs %zu bytes", w.total);
+  uint8_t *ws = reinterpret_cast<uint8_t *>(d->workspace);
+  bf16 *dO = reinterpret_cast<bf16 *>(ws + w.dO);
+  float *Dq = reinterpret_cast<float *>(ws + w.Dq);
+  int rc = attn_prep_run(d, dO, Dq, reinterpret_cast<float *>(ws + w.gate), st);
+  if (rc != EVO_OK) return rc;
+  int64_t nch;
+  a.chunk = flash_chunk(d, nch);
+  a.Dq = Dq;
+  a.dbias_part = BIAS ? reinterpret_cast<float *>(ws + w.part) : nullptr;
   CUtensorMap mq, mk, mv, mdo, mb, mq2, mdo2, mk2, mv2, mb2;
   // dq kernel: Q / dO tiles of 128 queries, K / V tiles of 64 keys
   if (!flash_head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
-      !flash_head_map(&mdo, dO, D, d->L, d->nb, d->H, rl * hc, rb * hc, QT) ||
+      !flash_head_map(&mdo, dO, D, d->L, d->nb, d->H, d->o_sl, d->o_sb, QT) ||
       !flash_head_map(&mk, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, KT) ||
       !flash_head_map(&mv, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, KT))
     return EVO_EUNSUP;
@@ -825,7 +914,7 @@ int flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq, int64_t r
   if (!flash_head_map(&mk2, d->k, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !flash_head_map(&mv2, d->v, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
       !flash_head_map(&mq2, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, KT) ||
-      !flash_head_map(&mdo2, dO, D, d->L, d->nb, d->H, rl * hc, rb * hc, KT))
+      !flash_head_map(&mdo2, dO, D, d->L, d->nb, d->H, d->o_sl, d->o_sb, KT))
     return EVO_EUNSUP;
   if (BIAS) {
     if (!flash_bias_map(&mb, d->bias, d->L, d->H, d->bq, d->bh, QT) ||
@@ -837,23 +926,31 @@ int flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq, int64_t r
   }
   {
     constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-    const size_t smem = 2 * STG + 2 * QT * 2 * D + 10 * 8 + 16;
+    const size_t smem = NS_BWD * STG + 2 * QT * 2 * D + (1 + NS_BWD + 7) * 8 + 16;
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
-    const int64_t nch = (d->nb + chunk - 1) / chunk;
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-    kfn<<<grid, NTH, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    kfn<<<grid, nth_of(TPR_BWD), smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_flash_dq_kernel");
   }
   {
     constexpr uint32_t BT = BIAS ? 4 * 8192 : 0;
-    constexpr uint32_t STG = (BT + 2 * KT * 2 * D + 2 * KT * 4 + 1023) / 1024 * 1024;
-    const size_t smem = 2 * STG + 2 * QT * 2 * D + 11 * 8 + 16;
+    constexpr uint32_t STG = (BT + 2 * KT * 2 * D + 1023) / 1024 * 1024;
+    const int64_t T = (d->L + KT - 1) / KT;
+    const size_t smem = NS_BWD * STG + 2 * QT * 2 * D + 2 * (size_t)T * KT * 4 +
+                        (1 + NS_BWD + 7) * 8 + 16;
+    EVO_REQUIRE(smem <= 227 * 1024, EVO_EUNSUP, "attention_flash: L=%d too long for the dkv "
+                "kernel's staged lse / Dq", d->L);
     auto kfn = attn_flash_dkv_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
-    kfn<<<grid, NTH, smem, st>>>(mq2, mk2, mv2, mdo2, mb2, a);
+    kfn<<<grid, nth_of(TPR_BWD), smem, st>>>(mq2, mk2, mv2, mdo2, mb2, a);
     EVO_LAUNCHED("attn_flash_dkv_kernel");
+  }
+  if (BIAS) {
+    // dbias = sum of the chunk partials in chunk order, into the plain layout
+    return reduce_lead(EVO_F32, nch, (int64_t)d->H * d->L, d->L, a.dbias_part, d->dbias,
+                       d->bq, 1, 0, st);
   }
   return EVO_OK;
 }
@@ -874,20 +971,19 @@ EVO_API int evo_attn_flash_fwd(const evo_attn_desc *d, void *stream) {
   return d->bias ? flash_fwd<16, true>(d, st) : flash_fwd<16, false>(d, st);
 }
 
-EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, const void *dO, const float *Dq,
-                               int64_t rb, int64_t rl, float *dbias_part, int64_t chunk,
-                               void *stream) {
+EVO_API size_t evo_attn_flash_bwd_workspace_bytes(const evo_attn_desc *d) {
+  if (check_flash(d, false) != EVO_OK) return 0;
+  return flash_ws(d).total;
+}
+
+EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, void *stream) {
   int rc = check_flash(d, true);
   if (rc != EVO_OK) return rc;
-  EVO_REQUIRE(dO && Dq && al16(dO) && chunk >= 1, EVO_EARG, "attn_flash_bwd: bad arguments");
-  EVO_REQUIRE(!d->bias || dbias_part, EVO_EARG, "attn_flash_bwd: bias needs dbias partials");
+  EVO_REQUIRE(!d->bias || d->dbias, EVO_EARG, "attn_flash_bwd: bias needs dbias");
   cudaStream_t st = as_stream(stream);
   note_backend(EVO_BK_ATTN_FLASH);
-  if (d->D == 32)
-    return d->bias ? flash_bwd<32, true>(d, dO, Dq, rb, rl, dbias_part, chunk, st)
-                   : flash_bwd<32, false>(d, dO, Dq, rb, rl, dbias_part, chunk, st);
-  return d->bias ? flash_bwd<16, true>(d, dO, Dq, rb, rl, dbias_part, chunk, st)
-                 : flash_bwd<16, false>(d, dO, Dq, rb, rl, dbias_part, chunk, st);
+  if (d->D == 32) return d->bias ? flash_bwd<32, true>(d, st) : flash_bwd<32, false>(d, st);
+  return d->bias ? flash_bwd<16, true>(d, st) : flash_bwd<16, false>(d, st);
 }
 
 }  // extern "C"

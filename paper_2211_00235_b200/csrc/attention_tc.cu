@@ -2163,6 +2163,32 @@ int attention_tc_fwd(const evo_attn_desc *d, cudaStream_t st) {
   return EVO_EUNSUP;
 }
 
+// The backward's prep pass for other kernels (attention_flash.cu): dO (o's
+// strides) -> dO_out, dGpre -> d->dgpre, Dq [nb, H, L]; the gate-bias sums
+// into d->dgate_bias when set (gpart: SMs*8*H*D fp32 of workspace).
+int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
+                  cudaStream_t st) {
+  if (d->D != 16 && d->D != 32) return EVO_EUNSUP;
+  AttnTcArgs a = make_args(d);
+  int64_t total = d->nb * (int64_t)d->L * d->H * (d->D / 8);
+  const bool fuse_gb = d->dgate_bias && (256 % (d->H * (d->D / 8)) == 0);
+  EVO_REQUIRE(!d->dgate_bias || fuse_gb, EVO_EUNSUP,
+              "attention bwd: gate-bias sums need 256 %% (H*D/8) == 0");
+  int blocks = (int)std::min<int64_t>((total + 255) / 256,
+                                      (int64_t)num_sms() * (fuse_gb ? 8 : 32));
+  bf16 *dO = reinterpret_cast<bf16 *>(dO_out);
+  const bf16 *dgm = reinterpret_cast<const bf16 *>(d->dgm);
+  bf16 *dgp = reinterpret_cast<bf16 *>(d->dgpre);
+  float *gp = fuse_gb ? gpart : nullptr;
+  if (d->D == 32)
+    attn_bwd_prep_kernel<32><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+  else
+    attn_bwd_prep_kernel<16><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+  EVO_LAUNCHED("attn_bwd_prep_kernel");
+  if (fuse_gb) return colsum_partials(blocks, (int64_t)d->H * d->D, gp, d->dgate_bias, 0, st);
+  return EVO_OK;
+}
+
 int attention_tc_bwd(const evo_attn_desc *d, cudaStream_t st) {
   EVO_REQUIRE(d->workspace && d->workspace_bytes >= attention_tc_bwd_ws(d), EVO_EARG,
               "attention bwd (tc): workspace too small");

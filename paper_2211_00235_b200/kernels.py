@@ -264,8 +264,7 @@ def attention_flash(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, 
                     bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None):
     """L > 256 keys on the bf16 path, head dim 16 / 32: csrc/attention_flash.cu
     (keys streamed through TMEM with an online softmax; the backward's dS
-    never leaves the SM either).  Same argument meaning as ``attention``.
-    The prep pass and the dbias chunk reduction are attention_long's."""
+    never leaves the SM either).  Same argument meaning as ``attention``."""
     four = 4 * hc
     if sb % four or sl % four or o_sb != sb // 4 or o_sl != sl // 4:
         raise N.ContractError("attention_flash: proj / o row maps must be the same row ids")
@@ -289,37 +288,29 @@ def attention_flash(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, 
                lambda: check(Lb.evo_attn_flash_fwd(C.byref(d), stream()), "evo_attn_flash_fwd"),
                keep=(proj, o, gm, lse, pb))
         return
-    dO = torch.empty(rows * hc + 8, dtype=torch.bfloat16, device=dev)
-    Dq = torch.empty(rows, H, dtype=torch.float32, device=dev)
-    check(Lb.evo_attn_long_prep(rows, H, D, ptr(dgm), ptr(proj, 3 * hc), four, ptr(o), ptr(dO),
-                                ptr(dproj, 3 * hc), four, ptr(Dq), stream()), "evo_attn_long_prep")
     d.dgm = ptr(dgm)
     d.dq, d.dk, d.dv, d.dgpre = (ptr(dproj, 0), ptr(dproj, hc), ptr(dproj, 2 * hc),
                                  ptr(dproj, 3 * hc))
-    part, chunk, nch = None, 1, nb
-    if bias is not None:
-        # chunks of batch rows per dq CTA: ~2 waves of CTAs, one fp32 dbias
-        # partial per chunk (reduced in chunk order below)
-        qt = (L + 127) // 128
-        nch = max(1, min(nb, (2 * 148) // max(1, qt * H)))
-        chunk = (nb + nch - 1) // nch
-        nch = (nb + chunk - 1) // chunk
-        part = torch.empty(nch * H * L * L, dtype=torch.float32, device=dev)
+    # the prep pass fuses the gate-bias sums when its column groups tile a
+    # 256-thread block; otherwise they are a separate column sum below
+    fuse_gb = dgate_bias is not None and 256 % (H * D // 8) == 0
+    d.dgate_bias = ptr(dgate_bias) if fuse_gb else None
+    # dbias in the kernel's plain layout: the caller's, or a padded copy
+    pdb = dbias
+    if bias is not None and pb is not bias:
+        pdb = torch.empty(H * pbh, dtype=torch.float32, device=dev)
+    d.dbias = ptr(pdb)
+    nbytes = Lb.evo_attn_flash_bwd_workspace_bytes(C.byref(d))
+    ws = _ws(nbytes, dev)
+    d.workspace, d.workspace_bytes = ptr(ws), nbytes
     _timed("attention_bwd", 2.0 * flops,
-           lambda: check(Lb.evo_attn_flash_bwd(C.byref(d), ptr(dO), ptr(Dq), rb, rl, ptr(part),
-                                               chunk, stream()), "evo_attn_flash_bwd"),
-           keep=(proj, o, gm, lse, pb, dgm, dproj, dO, Dq, part))
-    if bias is not None:
-        if bk == 1 and bh == L * bq:
-            reduce_lead(part, nch, H * L, L, dbias, bq, 1)
-        else:
-            dense = torch.empty(H * L * L, dtype=torch.float32, device=dev)
-            reduce_lead(part, nch, H * L, L, dense, L, 1)
-            for hh in range(H):
-                copy2d(dense, L, L, dbias, s_rs=L, d_rs=bq, d_cs=bk, s_off=hh * L * L,
-                       d_off=hh * bh)
-    if dgate_bias is not None:
-        colsum(dproj, rows, hc, dgate_bias, rs=four, off=3 * hc)
+           lambda: check(Lb.evo_attn_flash_bwd(C.byref(d), stream()), "evo_attn_flash_bwd"),
+           keep=(proj, o, gm, lse, pb, dgm, dproj, pdb, dgate_bias, ws))
+    if bias is not None and pdb is not dbias:
+        for hh in range(H):
+            copy2d(pdb, L, L, dbias, s_rs=pbq, d_rs=bq, d_cs=bk, s_off=hh * pbh, d_off=hh * bh)
+    if dgate_bias is not None and not fuse_gb:
+        colsum(dproj, nb * L, hc, dgate_bias, rs=four, off=3 * hc)
 
 
 def long_ld(L: int) -> int:

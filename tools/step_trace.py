@@ -26,7 +26,10 @@ def run(args):
     from paper_2211_00235_b200 import kernels as K, schedules as S
 
     dev = torch.device("cuda", 0)
-    cfg = pkg.EvoConfig(**CONFIGS[args.config])
+    kw = dict(CONFIGS[args.config])
+    if args.crop:
+        kw["r"] = args.crop
+    cfg = pkg.EvoConfig(**kw)
     store = pkg.init_params(cfg, 32, device=dev)
     st = S.StepState(cfg, store, args.precision, dev)
     st.pack()
@@ -49,9 +52,9 @@ def run(args):
 def family_of(name):
     if "gemm_tc_kernel" in name or "gemm_simt_kernel" in name or "skinny_" in name:
         return "gemm"
-    if "attn_fwd" in name:
+    if "attn_fwd" in name or "attn_flash_fwd" in name:
         return "attention_fwd"
-    if "attn_bwd_prep" in name:
+    if "attn_bwd_prep" in name or "long_prep" in name:
         return "attention_bwd"
     return None
 
@@ -89,7 +92,8 @@ def join(csv_path, shapes_path):
             groups.append(cur)
         elif fam is not None or cur is None or not (
                 (cur[0] == "gemm" and ("splitk_reduce" in name or "skinny_reduce" in name)) or
-                (cur[0] == "attention_bwd" and ("attn_bwd" in name or "reduce_lead" in name))):
+                (cur[0] == "attention_bwd" and ("attn_bwd" in name or "attn_flash" in name
+                                                or "reduce_lead" in name))):
             cur = [name.split("(")[0][:48], None, 0.0, 0.0, [], 0.0]
             groups.append(cur)
         cur[3] += us
@@ -124,6 +128,7 @@ if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", default="af2")
     ap.add_argument("--precision", default="bf16")
+    ap.add_argument("--crop", type=int, default=0)
     ap.add_argument("--shapes", default="gpurun_out/trace_shapes.json")
     ap.add_argument("--join", nargs=2, metavar=("CSV", "SHAPES"))
     a = ap.parse_args()
