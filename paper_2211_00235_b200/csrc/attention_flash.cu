@@ -39,7 +39,7 @@ constexpr int QT = 128;    // queries (fwd / dq) or keys (dkv) per CTA = UMMA M
 constexpr int KT = 64;     // streamed tile (keys, or queries in dkv) = UMMA N
 // each kernel: TPR elementwise threads per TMEM lane (row), EPT = KT / TPR
 // elements each, NEW = 4 TPR elementwise warps + 1 issuer warp
-constexpr int TPR_FWD = 2, TPR_BWD = 4;   // fwd: 2 CTAs / SM; dq, dkv: 1 (512 TMEM cols)
+constexpr int TPR_FWD = 2, TPR_DQ = 2, TPR_DKV = 4;  // fwd: 2 CTAs / SM; dq, dkv: 1 (512 TMEM cols)
 constexpr int NS_FWD = 2, NS_BWD = 4;     // streamed-tile stages
 constexpr int nth_of(int tpr) { return (4 * tpr + 1) * 32; }
 constexpr uint32_t BIAS_TILE = 2 * 16384;  // two [128 x 32] fp32 SW128 boxes
@@ -141,35 +141,50 @@ __device__ __forceinline__ float bias_at(const uint8_t *box, int q, int kk) {
 }
 
 // ======================================================================= fwd
-// TMEM: buffer i at 96 i: S (64 fp32) | P (32 bf16 pairs);  O at 192.
+// Persistent over a chunk of batch rows: tile g = (row r, key tile j), the
+// K/V(/bias) stage ring and the S/P double buffer run continuously across
+// rows; Q tiles and the O accumulators are double-buffered by row parity so
+// a row's epilogue overlaps the next row's MMAs.
+// TMEM (256): S/P buffer g&1 at 96 (g&1): S (64 fp32) | P (32 bf16 pairs);
+// O of row parity p at 192 + D p.
 // Softmax warp w: lane quadrant w & 3 (rows), part w >> 2 (EPT keys).
+// two CTAs per SM: 18 warps over 4 SMSPs put 5 on one, so <= 96 registers
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(nth_of(TPR_FWD), 1)
+__global__ void __maxnreg__(96)
 attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                       const FlashArgs a) {
   constexpr int TPR = TPR_FWD, EPT = KT / TPR, NEW = 4 * TPR;
-  constexpr int NS = NS_FWD;                           // K/V(/bias) stages
+  constexpr int NS = NS_FWD;
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;                          // NS x [bias | K | V]
-  uint8_t *sQ = sStage + NS * STG;
-  float *sX = reinterpret_cast<float *>(sQ + QB);      // [2 parity][TPR][128] max exchange
+  uint8_t *sQ = sStage + NS * STG;                     // 2 x Q (row parity)
+  float *sX = reinterpret_cast<float *>(sQ + 2 * QB);  // [2 parity][TPR][128] max exchange
   float *sL = sX + 2 * TPR * 128;                      // [TPR][128] row sums
-  // 0 Q, 1-2 stage full, 3-4 S done, 5-6 P packed (NEW warps), 7-8 PV done
   uint64_t *bars = reinterpret_cast<uint64_t *>(sL + TPR * 128);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 9);
+  uint64_t *qfull = bars, *fullb = qfull + 2, *sdone = fullb + NS, *pp = sdone + 2,
+           *pvd = pp + 2, *ord = pvd + 2;
+  constexpr int NBAR = 2 + NS + 8;
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
-  const int64_t b = blockIdx.z;
   const int L = a.L;
   const int T = (L + KT - 1) / KT;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  const int nrows = b_hi > b_lo ? (int)(b_hi - b_lo) : 0;
+  const int G = nrows * T;
 
   if (tid == NEW * 32) {
-    for (int i = 0; i < 9; ++i) mbar_init(&bars[i], (i == 5 || i == 6) ? NEW : 1);
+    for (int i = 0; i < NBAR; ++i) {
+      uint64_t *bb = &bars[i];
+      const bool warps = bb == &pp[0] || bb == &pp[1] || bb == &ord[0] || bb == &ord[1];
+      mbar_init(bb, warps ? NEW : 1);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (warp == 0) tmem_alloc(tslot, 256);
@@ -180,9 +195,11 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
 
   if (warp == NEW) {
     // ------------------------------------------------------------ issuer
-    auto load_tile = [&](int j) {
-      uint8_t *st = sStage + (j % NS) * STG;
-      uint64_t *bar = &bars[1 + (j % NS)];
+    auto load_tile = [&](int g) {
+      const int64_t b = b_lo + g / T;
+      const int j = g % T;
+      uint8_t *st = sStage + (g % NS) * STG;
+      uint64_t *bar = &fullb[g % NS];
       if (lane == 0) {
         mbar_expect_tx(bar, STG);
         if (BIAS) {
@@ -195,42 +212,59 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       }
       __syncwarp();
     };
-    if (lane == 0) {
-      mbar_expect_tx(&bars[0], QB);
-      tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
-    }
-    __syncwarp();
-    for (int j = 0; j < NS && j < T; ++j) load_tile(j);
+    auto load_q = [&](int r) {
+      if (lane == 0) {
+        mbar_expect_tx(&qfull[r & 1], QB);
+        tma_load_4d(sQ + (r & 1) * QB, &mQ, &qfull[r & 1], 0, q0, (int)(b_lo + r), h);
+      }
+      __syncwarp();
+    };
+    for (int r = 0; r < 2 && r < nrows; ++r) load_q(r);
+    for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-    const uint32_t sQa = smem_u32(sQ);
-    mbar_wait(&bars[0], 0);
-    for (int j = 0; j <= T; ++j) {
-      if (j < T) {
-        const int st = j % NS;
-        mbar_wait(&bars[1 + st], (uint32_t)((j / NS) & 1));
+    int r = 0, j = 0;          // coordinates of tile g
+    int ri = 0, ji = -1;       // coordinates of tile g - 1
+    for (int g = 0; g <= G; ++g) {
+      if (g < G) {
+        if (j == 0) mbar_wait(&qfull[r & 1], (uint32_t)((r >> 1) & 1));
+        const int st = g % NS;
+        mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0);
-        const uint32_t d = tmem + (j & 1) * 96;
+        const uint32_t sQa = smem_u32(sQ) + (r & 1) * QB;
+        const uint32_t d = tmem + (g & 1) * 96;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d, desc_k<D>(sQa, ks), desc_k<D>(sK, ks), idesc_s, ks > 0);
-        umma_commit_el(&bars[3 + (j & 1)]);
+        umma_commit_el(&sdone[g & 1]);
+        if (j == T - 1 && r + 2 < nrows) {
+          mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));   // row r's S MMAs read Q
+          load_q(r + 2);
+        }
       }
-      if (j >= 1) {
-        const int i = j - 1, bi = i & 1, st = i % NS;
-        mbar_wait(&bars[5 + bi], (uint32_t)((i >> 1) & 1));   // P_i packed
+      if (g >= 1) {
+        const int i = g - 1, bi = i & 1, st = i % NS;
+        mbar_wait(&pp[bi], (uint32_t)((i >> 1) & 1));   // P_i packed
+        if (ji == 0 && ri >= 2) mbar_wait(&ord[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
         fence_after();
         const uint32_t sV = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0) + KB;
+        const uint32_t oc = tmem + 192 + D * (ri & 1);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 192, tmem + bi * 96 + 64 + 8 * ks, desc_mn<D>(sV, ks), idesc_o,
-                          (i > 0 || ks > 0) ? 1u : 0u);
-        umma_commit_el(&bars[7 + bi]);
-        if (i + NS < T) {
-          mbar_wait(&bars[7 + bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
+          umma_bf16_ts_el(oc, tmem + bi * 96 + 64 + 8 * ks, desc_mn<D>(sV, ks), idesc_o,
+                          (ji > 0 || ks > 0) ? 1u : 0u);
+        umma_commit_el(&pvd[bi]);
+        if (i + NS < G) {
+          mbar_wait(&pvd[bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
           load_tile(i + NS);
         }
+      }
+      ri = r;
+      ji = j;
+      if (++j == T) {
+        j = 0;
+        ++r;
       }
     }
   } else {
@@ -241,12 +275,19 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     const bool qv = q < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
+    constexpr int OD = D / TPR;
     float m_run = -INFINITY, l = 0.f;
-    for (int j = 0; j < T; ++j) {
-      const int bi = j & 1, st = j % NS;
+    int r = 0, j = 0;
+    for (int g = 0; g < G; ++g) {
+      const int bi = g & 1, st = g % NS;
       const int kb = j * KT + part * EPT;        // first key of this thread's EPT
-      if (BIAS) mbar_wait(&bars[1 + st], (uint32_t)((j / NS) & 1));  // bias tile landed
-      mbar_wait(&bars[3 + bi], (uint32_t)((j >> 1) & 1));
+      const uint32_t oc = lane_addr + 192 + D * (r & 1) + part * OD;
+      if (j == 0) {
+        m_run = -INFINITY;
+        l = 0.f;
+      }
+      if (BIAS) mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));  // bias tile landed
+      mbar_wait(&sdone[bi], (uint32_t)((g >> 1) & 1));
       fence_after();
       uint32_t sv[EPT];
       tld<EPT>(lane_addr + bi * 96 + part * EPT, sv);
@@ -257,10 +298,17 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       float mt = -INFINITY;
 #pragma unroll
       for (int k = 0; k < EPT; ++k) {
-        float v = __uint_as_float(sv[k]) * sc_l2;
-        if (BIAS) v = fmaf(bb[k], LOG2E_F, v);
-        x[k] = (kb + k < L) ? v : -INFINITY;
+        x[k] = BIAS ? fmaf(bb[k], LOG2E_F, __uint_as_float(sv[k]) * sc_l2)
+                    : __uint_as_float(sv[k]) * sc_l2;
         mt = fmaxf(mt, x[k]);
+      }
+      if (kb + EPT > L) {  // the last key tile: mask keys beyond L
+        mt = -INFINITY;
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          if (kb + k >= L) x[k] = -INFINITY;
+          mt = fmaxf(mt, x[k]);
+        }
       }
       float *sx = sX + bi * (TPR * 128);
       sx[part * 128 + t] = mt;
@@ -270,23 +318,21 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       const bool grow = mt > m_run + 8.f;
       float alpha = 1.f;
       if (grow) {
-        alpha = ex2f(m_run - mt);               // 0 on the first tile
+        alpha = ex2f(m_run - mt);               // 0 on the row's first tile
         m_run = mt;
       }
       if (j > 0 && __any_sync(0xffffffffu, grow)) {
         // rescale this row's part of O once PV of the previous tile is done
-        const int i = j - 1;
-        mbar_wait(&bars[7 + (i & 1)], (uint32_t)((i >> 1) & 1));
+        mbar_wait(&pvd[(g - 1) & 1], (uint32_t)(((g - 1) >> 1) & 1));
         fence_after();
-        constexpr int OD = D / TPR;
         uint32_t ov[OD];
-        tld<OD>(lane_addr + 192 + part * OD, ov);
+        tld<OD>(oc, ov);
         tmem_wait_ld();
         if (grow) {
 #pragma unroll
           for (int c = 0; c < OD; ++c) ov[c] = __float_as_uint(__uint_as_float(ov[c]) * alpha);
         }
-        tst<OD>(lane_addr + 192 + part * OD, ov);
+        tst<OD>(oc, ov);
       }
       l *= alpha;
       uint32_t pk[EPT / 2];
@@ -300,55 +346,63 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       tmem_st_wait();
       fence_before();
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bars[5 + bi]);
-    }
-    // epilogue: O / l, gate, lse
-    const int i = T - 1;
-    mbar_wait(&bars[7 + (i & 1)], (uint32_t)((i >> 1) & 1));
-    fence_after();
-    sL[part * 128 + t] = l;
-    named_bar_sync(1 + quad, 32 * TPR);
-    float lt = 0.f;
+      if (lane == 0) mbar_arrive(&pp[bi]);
+      if (j == T - 1) {
+        // epilogue of row r: O / l, gate, lse (overlaps the next row's MMAs)
+        const int64_t b = b_lo + r;
+        mbar_wait(&pvd[bi], (uint32_t)((g >> 1) & 1));
+        fence_after();
+        uint32_t ov[OD];
+        tld<OD>(oc, ov);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&ord[r & 1]);
+        sL[part * 128 + t] = l;
+        named_bar_sync(1 + quad, 32 * TPR);
+        float lt = 0.f;
 #pragma unroll
-    for (int p2 = 0; p2 < TPR; ++p2) lt += sL[p2 * 128 + t];
-    constexpr int OD = D / TPR;
-    uint32_t ov[OD];
-    tld<OD>(lane_addr + 192 + part * OD, ov);
-    tmem_wait_ld();
-    if (qv) {
-      const float inv = 1.f / lt;
-      const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D + part * OD;
-      const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D + part * OD;
-      // OD = D / TPR consecutive columns: 16-byte chunks (OD % 8 == 0) or one
-      // 8-byte chunk (OD == 4)
-      constexpr int CW = OD % 8 == 0 ? 8 : 4;
+        for (int p2 = 0; p2 < TPR; ++p2) lt += sL[p2 * 128 + t];
+        if (qv) {
+          const float inv = 1.f / lt;
+          const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D + part * OD;
+          const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D + part * OD;
+          // OD = D / TPR consecutive columns: 16-byte chunks (OD % 8 == 0) or
+          // one 8-byte chunk (OD == 4)
+          constexpr int CW = OD % 8 == 0 ? 8 : 4;
 #pragma unroll
-      for (int c0 = 0; c0 < OD; c0 += CW) {
-        uint32_t gw[CW / 2], o2[CW / 2], g2[CW / 2];
-        if constexpr (CW == 8) {
-          const uint4 gq = *reinterpret_cast<const uint4 *>(gp + c0);
-          gw[0] = gq.x; gw[1] = gq.y; gw[2] = gq.z; gw[3] = gq.w;
-        } else {
-          const uint2 gq = *reinterpret_cast<const uint2 *>(gp + c0);
-          gw[0] = gq.x; gw[1] = gq.y;
-        }
+          for (int c0 = 0; c0 < OD; c0 += CW) {
+            uint32_t gw[CW / 2], o2[CW / 2], g2[CW / 2];
+            if constexpr (CW == 8) {
+              const uint4 gq = *reinterpret_cast<const uint4 *>(gp + c0);
+              gw[0] = gq.x; gw[1] = gq.y; gw[2] = gq.z; gw[3] = gq.w;
+            } else {
+              const uint2 gq = *reinterpret_cast<const uint2 *>(gp + c0);
+              gw[0] = gq.x; gw[1] = gq.y;
+            }
 #pragma unroll
-        for (int e = 0; e < CW / 2; ++e) {
-          const float v0 = __uint_as_float(ov[c0 + 2 * e]) * inv;
-          const float v1 = __uint_as_float(ov[c0 + 2 * e + 1]) * inv;
-          const float2 gg = upk2(gw[e]);
-          o2[e] = pk2(v0, v1);
-          g2[e] = pk2(gg.x * v0, gg.y * v1);
-        }
-        if constexpr (CW == 8) {
-          *reinterpret_cast<uint4 *>(a.o + ooff + c0) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
-          *reinterpret_cast<uint4 *>(a.gm + ooff + c0) = make_uint4(g2[0], g2[1], g2[2], g2[3]);
-        } else {
-          *reinterpret_cast<uint2 *>(a.o + ooff + c0) = make_uint2(o2[0], o2[1]);
-          *reinterpret_cast<uint2 *>(a.gm + ooff + c0) = make_uint2(g2[0], g2[1]);
+            for (int e = 0; e < CW / 2; ++e) {
+              const float v0 = __uint_as_float(ov[c0 + 2 * e]) * inv;
+              const float v1 = __uint_as_float(ov[c0 + 2 * e + 1]) * inv;
+              const float2 gg = upk2(gw[e]);
+              o2[e] = pk2(v0, v1);
+              g2[e] = pk2(gg.x * v0, gg.y * v1);
+            }
+            if constexpr (CW == 8) {
+              *reinterpret_cast<uint4 *>(a.o + ooff + c0) = make_uint4(o2[0], o2[1], o2[2], o2[3]);
+              *reinterpret_cast<uint4 *>(a.gm + ooff + c0) = make_uint4(g2[0], g2[1], g2[2], g2[3]);
+            } else {
+              *reinterpret_cast<uint2 *>(a.o + ooff + c0) = make_uint2(o2[0], o2[1]);
+              *reinterpret_cast<uint2 *>(a.gm + ooff + c0) = make_uint2(g2[0], g2[1]);
+            }
+          }
+          if (part == 0) a.lse[(b * a.H + h) * (int64_t)L + q] = m_run * (1.f / LOG2E_F) + logf(lt);
         }
       }
-      if (part == 0) a.lse[(b * a.H + h) * (int64_t)L + q] = m_run * (1.f / LOG2E_F) + logf(lt);
+      if (++j == T) {
+        j = 0;
+        ++r;
+      }
     }
   }
   fence_before();
@@ -356,7 +410,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   if (warp == 0) tmem_dealloc(tmem, 256);
 }
 
-// store OD fp32 TMEM values (x scale) as bf16 at dst (OD = 8: 16 B, 4: 8 B)
+// store OD fp32 TMEM values (x scale) as bf16 at dst (16-byte or 8-byte chunks)
 template <int OD>
 __device__ __forceinline__ void store_row_bf16(bf16 *dst, const uint32_t (&v)[OD], float scale) {
   constexpr int CW = OD % 8 == 0 ? 8 : 4;
@@ -374,27 +428,43 @@ __device__ __forceinline__ void store_row_bf16(bf16 *dst, const uint32_t (&v)[OD
   }
 }
 
+// N consecutive fp32 values at p: 16-byte loads when aligned, else scalar
+template <int N>
+__device__ __forceinline__ void load_f32(const float *p, bool vec, float (&out)[N]) {
+  if (vec) {
+#pragma unroll
+    for (int c = 0; c < N / 4; ++c) {
+      const float4 v = *reinterpret_cast<const float4 *>(p + 4 * c);
+      out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
+    }
+  } else {
+#pragma unroll
+    for (int c = 0; c < N; ++c) out[c] = p[c];
+  }
+}
+
 // ======================================================================== dq
-// TMEM: buffer i at 160 i: S (64) | dP (64) | dS (32 bf16 pairs); dQ at 320.
+// Persistent over a chunk of batch rows (tile g = (row r, key tile j)); Q / dO
+// and the dQ accumulators double-buffered by row parity.
+// TMEM: buffer g&1 at 160 (g&1): S (64) | dP (64) | dS (32 bf16 pairs);
+// dQ of row parity p at 320 + D p.
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(nth_of(TPR_BWD), 1)
+__global__ void __launch_bounds__(nth_of(TPR_DQ), 1)
 attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                      const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
-  constexpr int TPR = TPR_BWD, EPT = KT / TPR, NEW = 4 * TPR;
+  constexpr int TPR = TPR_DQ, EPT = KT / TPR, NEW = 4 * TPR;
   constexpr int NS = NS_BWD;
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;
-  uint8_t *sQ = sStage + NS * STG;                     // Q | dO of the current row
-  // 0 row Q/dO, 1-2 stage full, 3-4 S/dP done, 5-6 dS packed (NEW warps),
-  // 7-8 dQ MMA done, 9 row's dQ read back (NEW warps)
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + 2 * QB);
-  uint64_t *fullb = bars + 1, *sdone = fullb + NS, *dsp = sdone + 2, *dqd = dsp + 2,
-           *dqr = dqd + 2;
-  constexpr int NBAR = 1 + NS + 7;
+  uint8_t *sQ = sStage + NS * STG;                     // 2 x [Q | dO] (row parity)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + 4 * QB);
+  uint64_t *qfull = bars, *fullb = qfull + 2, *sdone = fullb + NS, *dsp = sdone + 2,
+           *dqd = dsp + 2, *dqr = dqd + 2;
+  constexpr int NBAR = 2 + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -409,7 +479,8 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   if (tid == NEW * 32) {
     for (int i = 0; i < NBAR; ++i) {
       uint64_t *bb = &bars[i];
-      mbar_init(bb, (bb == &dsp[0] || bb == &dsp[1] || bb == dqr) ? NEW : 1);
+      const bool warps = bb == &dsp[0] || bb == &dsp[1] || bb == &dqr[0] || bb == &dqr[1];
+      mbar_init(bb, warps ? NEW : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -437,30 +508,28 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       }
       __syncwarp();
     };
-    auto load_row = [&](int64_t b) {
+    auto load_row = [&](int r) {
       if (lane == 0) {
-        mbar_expect_tx(&bars[0], 2 * QB);
-        tma_load_4d(sQ, &mQ, &bars[0], 0, q0, (int)b, h);
-        tma_load_4d(sQ + QB, &mdO, &bars[0], 0, q0, (int)b, h);
+        uint8_t *dst = sQ + (r & 1) * 2 * QB;
+        mbar_expect_tx(&qfull[r & 1], 2 * QB);
+        tma_load_4d(dst, &mQ, &qfull[r & 1], 0, q0, (int)(b_lo + r), h);
+        tma_load_4d(dst + QB, &mdO, &qfull[r & 1], 0, q0, (int)(b_lo + r), h);
       }
       __syncwarp();
     };
-    if (G > 0) {
-      load_row(b_lo);
-      for (int g = 0; g < NS && g < G; ++g) load_tile(g);
-    }
+    for (int r = 0; r < 2 && r < nrows; ++r) load_row(r);
+    for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-    const uint32_t sQa = smem_u32(sQ), sdOa = sQa + QB;
+    int r = 0, j = 0, ri = 0, ji = -1;
     for (int g = 0; g <= G; ++g) {
       if (g < G) {
-        const int64_t r = g / T;
-        const int j = g % T;
-        if (j == 0) mbar_wait(&bars[0], (uint32_t)(r & 1));   // row's Q / dO landed
+        if (j == 0) mbar_wait(&qfull[r & 1], (uint32_t)((r >> 1) & 1));   // row's Q / dO
         const int st = g % NS;
         mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0), sV = sK + KB;
+        const uint32_t sQa = smem_u32(sQ) + (r & 1) * 2 * QB, sdOa = sQa + QB;
         const uint32_t d = tmem + (g & 1) * 160;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
@@ -469,28 +538,33 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d + 64, desc_k<D>(sdOa, ks), desc_k<D>(sV, ks), idesc_s, ks > 0);
         umma_commit_el(&sdone[g & 1]);
-        if (j == T - 1 && r + 1 < nrows) {
-          // the row's last S/dP MMAs read Q / dO: reload them for the next row
+        if (j == T - 1 && r + 2 < nrows) {
+          // row r's last S/dP MMAs read Q / dO: load row r + 2 into its buffer
           mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));
-          load_row(b_lo + r + 1);
+          load_row(r + 2);
         }
       }
       if (g >= 1) {
         const int i = g - 1, bi = i & 1, st = i % NS;
-        const int ji = i % T;
         mbar_wait(&dsp[bi], (uint32_t)((i >> 1) & 1));   // dS_i packed
-        if (ji == 0 && i > 0) mbar_wait(dqr, (uint32_t)(((i / T) - 1) & 1));  // dQ read
+        if (ji == 0 && ri >= 2) mbar_wait(&dqr[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 320, tmem + bi * 160 + 128 + 8 * ks, desc_mn<D>(sK, ks), idesc_o,
-                          (ji > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_ts_el(tmem + 320 + D * (ri & 1), tmem + bi * 160 + 128 + 8 * ks,
+                          desc_mn<D>(sK, ks), idesc_o, (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&dqd[bi]);
         if (i + NS < G) {
           mbar_wait(&dqd[bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
           load_tile(i + NS);
         }
+      }
+      ri = r;
+      ji = j;
+      if (++j == T) {
+        j = 0;
+        ++r;
       }
     }
   } else {
@@ -500,31 +574,33 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     const bool qv = q < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
-    float lse_l2 = 0.f, dq_ = 0.f;
+    constexpr int OD = D / TPR;
     float *prow = BIAS ? a.dbias_part + (int64_t)blockIdx.z * a.H * L * (int64_t)L +
                              ((int64_t)h * L + q) * L
                        : nullptr;
+    // lse / Dq of this thread's query row, one batch row ahead
+    float lse_n = 0.f, dq_n = 0.f;
+    if (qv && nrows > 0) {
+      lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
+      dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + q];
+    }
+    float lse_l2 = 0.f, dq_ = 0.f;
+    int r = 0, j = 0;
     for (int g = 0; g < G; ++g) {
-      const int r = g / T, j = g % T, bi = g & 1, st = g % NS;
+      const int bi = g & 1, st = g % NS;
       const int64_t b = b_lo + r;
       if (j == 0) {
-        lse_l2 = qv ? a.lse[(b * a.H + h) * (int64_t)L + q] * LOG2E_F : 0.f;
-        dq_ = qv ? a.Dq[(b * a.H + h) * (int64_t)L + q] : 0.f;
+        lse_l2 = lse_n * LOG2E_F;
+        dq_ = dq_n;
+        if (qv && r + 1 < nrows) {
+          lse_n = a.lse[((b + 1) * a.H + h) * (int64_t)L + q];
+          dq_n = a.Dq[((b + 1) * a.H + h) * (int64_t)L + q];
+        }
       }
       const int kb = j * KT + part * EPT;
       float *dst = prow + kb;
-      // the chunk's dbias partial of this thread's keys, loaded before the
-      // wait so its L2 latency overlaps the MMAs (one owner thread per element)
-      const bool pvec = BIAS && qv && r > 0 && kb + EPT <= L &&
-                        (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
-      float old[EPT];
-      if (pvec) {
-#pragma unroll
-        for (int c = 0; c < EPT / 4; ++c) {
-          const float4 o = *reinterpret_cast<const float4 *>(dst + 4 * c);
-          old[4 * c] = o.x; old[4 * c + 1] = o.y; old[4 * c + 2] = o.z; old[4 * c + 3] = o.w;
-        }
-      }
+      const bool full_k = kb + EPT <= L;
+      const bool vec = full_k && (reinterpret_cast<uintptr_t>(dst) & 15) == 0;
       if (BIAS) mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));  // bias tile landed
       mbar_wait(&sdone[bi], (uint32_t)((g >> 1) & 1));
       fence_after();
@@ -536,31 +612,50 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       tmem_wait_ld();
       uint32_t pk[EPT / 2];
       float ds[EPT];
+      if (qv && full_k) {
 #pragma unroll
-      for (int k = 0; k < EPT; ++k) {
-        float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
-        if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
-        const float p = (qv && kb + k < L) ? ex2f(x) : 0.f;
-        ds[k] = p * (__uint_as_float(dv[k]) - dq_);
+        for (int k = 0; k < EPT; ++k) {
+          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
+          if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
+          ds[k] = ex2f(x) * (__uint_as_float(dv[k]) - dq_);
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < EPT; ++k) {
+          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
+          if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
+          const float p = (qv && kb + k < L) ? ex2f(x) : 0.f;
+          ds[k] = p * (__uint_as_float(dv[k]) - dq_);
+        }
       }
 #pragma unroll
       for (int k = 0; k < EPT; k += 2) pk[k >> 1] = pk2(ds[k], ds[k + 1]);
       tst<EPT / 2>(lane_addr + bi * 160 + 128 + part * (EPT / 2), pk);
       if (BIAS && qv) {
-        if (kb + EPT <= L && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+        // the chunk's dbias partial: the first row stores, later rows add
+        // with fire-and-forget reductions (one owner thread per element and
+        // program order per address: the sum runs over the rows in order)
+        if (vec) {
 #pragma unroll
           for (int c = 0; c < EPT / 4; ++c) {
-            float4 v = make_float4(ds[4 * c], ds[4 * c + 1], ds[4 * c + 2], ds[4 * c + 3]);
-            if (pvec) {
-              v.x += old[4 * c]; v.y += old[4 * c + 1]; v.z += old[4 * c + 2];
-              v.w += old[4 * c + 3];
+            float *d4 = dst + 4 * c;
+            if (r == 0) {
+              *reinterpret_cast<float4 *>(d4) =
+                  make_float4(ds[4 * c], ds[4 * c + 1], ds[4 * c + 2], ds[4 * c + 3]);
+            } else {
+              asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(d4),
+                           "f"(ds[4 * c]), "f"(ds[4 * c + 1]), "f"(ds[4 * c + 2]),
+                           "f"(ds[4 * c + 3])
+                           : "memory");
             }
-            *reinterpret_cast<float4 *>(dst + 4 * c) = v;
           }
         } else {
 #pragma unroll
-          for (int k = 0; k < EPT; ++k)
-            if (kb + k < L) dst[k] = r > 0 ? dst[k] + ds[k] : ds[k];
+          for (int k2 = 0; k2 < EPT; ++k2) {
+            if (kb + k2 >= L) continue;
+            if (r == 0) dst[k2] = ds[k2];
+            else asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + k2), "f"(ds[k2]) : "memory");
+          }
         }
       }
       tmem_st_wait();
@@ -571,15 +666,18 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         // the row's dQ: wait for its last dQ MMA, scale, store
         mbar_wait(&dqd[bi], (uint32_t)((g >> 1) & 1));
         fence_after();
-        constexpr int OD = D / TPR;
         uint32_t v[OD];
-        tld<OD>(lane_addr + 320 + part * OD, v);
+        tld<OD>(lane_addr + 320 + D * (r & 1) + part * OD, v);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(dqr);
+        if (lane == 0) mbar_arrive(&dqr[r & 1]);
         if (qv) store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v,
                                    a.scale);
+      }
+      if (++j == T) {
+        j = 0;
+        ++r;
       }
     }
   }
@@ -589,45 +687,49 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
 }
 
 // ======================================================================= dkv
-// CTA = 128 keys; the queries stream in tiles of 64.  TMEM: buffer i at
-// 192 i: S^T (64) | dP^T (64) | P^T (32 pairs) | dS^T (32 pairs);
-// dK at 384, dV at 384 + D.  lse (log2 units) and Dq of all L queries are
-// staged in smem once per CTA.
+// CTA = 128 keys x a chunk of batch rows; the queries stream in tiles of 64
+// (tile g = (row r, query tile j)); K / V and the dK / dV accumulators are
+// double-buffered by row parity.  TMEM: buffer g&1 at 192 (g&1): S^T (64) |
+// dP^T (64) | P^T (32 pairs) | dS^T (32 pairs); dK / dV of row parity p at
+// 384 + 2 D p (+ D).  lse / Dq of the thread's queries: global loads, one
+// tile ahead.
 template <int D, bool BIAS>
-__global__ void __launch_bounds__(nth_of(TPR_BWD), 1)
+__global__ void __launch_bounds__(nth_of(TPR_DKV), 1)
 attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                       const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
-  constexpr int TPR = TPR_BWD, EPT = KT / TPR, NEW = 4 * TPR;
+  constexpr int TPR = TPR_DKV, EPT = KT / TPR, NEW = 4 * TPR;
   constexpr int NS = NS_BWD;
   constexpr uint32_t KB = QT * Sw<D>::bytes, QB = KT * Sw<D>::bytes;
-  // stage: bias [64 q x 128 k] as four [64 x 32] SW128 boxes | Q | dO
+  // stage: bias [64 q x 128 k] as four [64 x 32] SW128 boxes | Q | dO |
+  // lse [64] | Dq [64] (fp32, by cp.async: any L)
   constexpr uint32_t BT = BIAS ? 4 * 8192 : 0;
-  constexpr uint32_t STG = (BT + 2 * QB + 1023) / 1024 * 1024;
+  constexpr uint32_t STG = (BT + 2 * QB + 2 * KT * 4 + 1023) / 1024 * 1024;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;
-  uint8_t *sK = sStage + NS * STG;                     // K | V of the CTA's keys
-  const int L = a.L;
-  const int T = (L + KT - 1) / KT;
-  float *sLse = reinterpret_cast<float *>(sK + 2 * KB);  // [T*KT] each
-  float *sDq = sLse + T * KT;
-  // 0 K/V, 1-2 stage TMA full, 3 lse/Dq staged, 5-6 S/dP done,
-  // 7-8 P/dS packed (NEW warps), 9-10 dK/dV MMAs done
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sDq + T * KT);
-  uint64_t *fullb = bars + 1, *lsb = fullb + NS, *sdone = lsb + 1, *pp2 = sdone + 2,
-           *mmd = pp2 + 2;
-  constexpr int NBAR = 1 + NS + 7;
+  uint8_t *sK = sStage + NS * STG;                     // 2 x [K | V] (row parity)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sK + 4 * KB);
+  uint64_t *kvfull = bars, *fullb = kvfull + 2, *sdone = fullb + NS, *pp2 = sdone + 2,
+           *mmd = pp2 + 2, *accr = mmd + 2;
+  constexpr int NBAR = 2 + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = blockIdx.x * QT, h = blockIdx.y;
-  const int64_t b = blockIdx.z;
+  const int L = a.L;
+  const int T = (L + KT - 1) / KT;
+  const int64_t b_lo = blockIdx.z * a.chunk;
+  const int64_t b_hi = min(a.nb, b_lo + a.chunk);
+  const int nrows = b_hi > b_lo ? (int)(b_hi - b_lo) : 0;
+  const int G = nrows * T;
 
   if (tid == NEW * 32) {
     for (int i = 0; i < NBAR; ++i) {
       uint64_t *bb = &bars[i];
-      mbar_init(bb, (bb == &pp2[0] || bb == &pp2[1]) ? NEW : 1);
+      const bool warps = bb == &pp2[0] || bb == &pp2[1] || bb == &accr[0] || bb == &accr[1];
+      const bool stage = bb >= fullb && bb < fullb + NS;   // TMA + 32 cp.async lanes
+      mbar_init(bb, warps ? NEW : (stage ? 33 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -638,9 +740,11 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
   const uint32_t tmem = *tslot;
 
   if (warp == NEW) {
-    auto load_tile = [&](int j) {
-      uint8_t *st = sStage + (j % NS) * STG;
-      uint64_t *bar = &fullb[j % NS];
+    auto load_tile = [&](int g) {
+      const int64_t b = b_lo + g / T;
+      const int j = g % T;
+      uint8_t *st = sStage + (g % NS) * STG;
+      uint64_t *bar = &fullb[g % NS];
       if (lane == 0) {
         mbar_expect_tx(bar, BT + 2 * QB);
         if (BIAS) {
@@ -650,64 +754,88 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         tma_load_4d(st + BT, &mQ, bar, 0, j * KT, (int)b, h);
         tma_load_4d(st + BT + QB, &mdO, bar, 0, j * KT, (int)b, h);
       }
+      // lse / Dq of the tile's 64 queries (zero past L)
+      const int64_t rowo = (b * a.H + h) * (int64_t)L;
+      float *sl = reinterpret_cast<float *>(st + BT + 2 * QB);
+#pragma unroll
+      for (int e = 0; e < 2; ++e) {
+        const int qi = lane + 32 * e, q = j * KT + qi;
+        const uint32_t n = q < L ? 4u : 0u;
+        const float *src1 = a.lse + rowo + (q < L ? q : 0);
+        const float *src2 = a.Dq + rowo + (q < L ? q : 0);
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(sl + qi)),
+                     "l"(src1), "r"(n)
+                     : "memory");
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(smem_u32(sl + KT + qi)),
+                     "l"(src2), "r"(n)
+                     : "memory");
+      }
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(smem_u32(bar))
+                   : "memory");
       __syncwarp();
     };
-    if (lane == 0) {
-      mbar_expect_tx(&bars[0], 2 * KB);
-      tma_load_4d(sK, &mK, &bars[0], 0, k0, (int)b, h);
-      tma_load_4d(sK + KB, &mV, &bars[0], 0, k0, (int)b, h);
-    }
-    __syncwarp();
-    for (int j = 0; j < NS && j < T; ++j) load_tile(j);
-    {
-      const float *lp = a.lse + (b * a.H + h) * (int64_t)L;
-      const float *dp = a.Dq + (b * a.H + h) * (int64_t)L;
-      for (int qi = lane; qi < T * KT; qi += 32) {
-        sLse[qi] = qi < L ? lp[qi] * LOG2E_F : 0.f;
-        sDq[qi] = qi < L ? dp[qi] : 0.f;
+    auto load_kv = [&](int r) {
+      if (lane == 0) {
+        uint8_t *dst = sK + (r & 1) * 2 * KB;
+        mbar_expect_tx(&kvfull[r & 1], 2 * KB);
+        tma_load_4d(dst, &mK, &kvfull[r & 1], 0, k0, (int)(b_lo + r), h);
+        tma_load_4d(dst + KB, &mV, &kvfull[r & 1], 0, k0, (int)(b_lo + r), h);
       }
       __syncwarp();
-      if (lane == 0) mbar_arrive(lsb);
-      __syncwarp();
-    }
+    };
+    for (int r = 0; r < 2 && r < nrows; ++r) load_kv(r);
+    for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-    const uint32_t sKa = smem_u32(sK), sVa = sKa + KB;
-    mbar_wait(&bars[0], 0);
-    for (int j = 0; j <= T; ++j) {
-      if (j < T) {
-        const int st = j % NS;
-        mbar_wait(&fullb[st], (uint32_t)((j / NS) & 1));
+    int r = 0, j = 0, ri = 0, ji = -1;
+    for (int g = 0; g <= G; ++g) {
+      if (g < G) {
+        if (j == 0) mbar_wait(&kvfull[r & 1], (uint32_t)((r >> 1) & 1));
+        const int st = g % NS;
+        mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));
         fence_after();
         const uint32_t sQ = smem_u32(sStage + st * STG) + BT, sdO = sQ + QB;
-        const uint32_t d = tmem + (j & 1) * 192;
+        const uint32_t sKa = smem_u32(sK) + (r & 1) * 2 * KB, sVa = sKa + KB;
+        const uint32_t d = tmem + (g & 1) * 192;
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d, desc_k<D>(sKa, ks), desc_k<D>(sQ, ks), idesc_s, ks > 0);
 #pragma unroll
         for (int ks = 0; ks < D / 16; ++ks)
           umma_bf16_el(d + 64, desc_k<D>(sVa, ks), desc_k<D>(sdO, ks), idesc_s, ks > 0);
-        umma_commit_el(&sdone[j & 1]);
+        umma_commit_el(&sdone[g & 1]);
+        if (j == T - 1 && r + 2 < nrows) {
+          mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));   // row r's K / V read
+          load_kv(r + 2);
+        }
       }
-      if (j >= 1) {
-        const int i = j - 1, bi = i & 1, st = i % NS;
+      if (g >= 1) {
+        const int i = g - 1, bi = i & 1, st = i % NS;
         mbar_wait(&pp2[bi], (uint32_t)((i >> 1) & 1));   // P^T / dS^T packed
+        if (ji == 0 && ri >= 2) mbar_wait(&accr[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
         fence_after();
         const uint32_t sQ = smem_u32(sStage + st * STG) + BT, sdO = sQ + QB;
         const uint32_t base = tmem + bi * 192;
+        const uint32_t acc = tmem + 384 + 2 * D * (ri & 1);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 384 + D, base + 128 + 8 * ks, desc_mn<D>(sdO, ks), idesc_o,
-                          (i > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_ts_el(acc + D, base + 128 + 8 * ks, desc_mn<D>(sdO, ks), idesc_o,
+                          (ji > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 384, base + 160 + 8 * ks, desc_mn<D>(sQ, ks), idesc_o,
-                          (i > 0 || ks > 0) ? 1u : 0u);
+          umma_bf16_ts_el(acc, base + 160 + 8 * ks, desc_mn<D>(sQ, ks), idesc_o,
+                          (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&mmd[bi]);
-        if (i + NS < T) {
+        if (i + NS < G) {
           mbar_wait(&mmd[bi], (uint32_t)((i >> 1) & 1));
           load_tile(i + NS);
         }
+      }
+      ri = r;
+      ji = j;
+      if (++j == T) {
+        j = 0;
+        ++r;
       }
     }
   } else {
@@ -717,38 +845,58 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     const bool kv = k < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
-    mbar_wait(lsb, 0);
-    for (int j = 0; j < T; ++j) {
-      const int bi = j & 1, st = j % NS;
+    constexpr int OD = D / TPR;
+    // transposed bias reads: element (q, kk = t & 31) of a [64 q x 32 k]
+    // SW128 box sits at q*128 + ((kk/4 ^ q%8) << 4) + (kk%4)*4; q % 8 is the
+    // compile-time qq % 8 (part*EPT is a multiple of 8)
+    uint32_t boff[8];
+#pragma unroll
+    for (int e = 0; e < 8; ++e) boff[e] = ((((t & 31) >> 2) ^ e) << 4) + (t & 3) * 4;
+    int r = 0, j = 0;
+    for (int g = 0; g < G; ++g) {
+      const int bi = g & 1, st = g % NS;
       const int qb = j * KT + part * EPT;        // first query of this thread's EPT
-      if (BIAS) mbar_wait(&fullb[st], (uint32_t)((j / NS) & 1));  // bias tile landed
-      mbar_wait(&sdone[bi], (uint32_t)((j >> 1) & 1));
+      mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));   // bias, lse, Dq landed
+      mbar_wait(&sdone[bi], (uint32_t)((g >> 1) & 1));
       fence_after();
       uint32_t sv[EPT], dv[EPT];
       tld<EPT>(lane_addr + bi * 192 + part * EPT, sv);
       tld<EPT>(lane_addr + bi * 192 + 64 + part * EPT, dv);
       const uint8_t *stg = sStage + st * STG;
-      const float *sl = sLse + qb, *sd = sDq + qb;
-      tmem_wait_ld();
-      uint32_t pp[EPT / 2], pd[EPT / 2];
+      const float *sl = reinterpret_cast<const float *>(stg + BT + 2 * QB) + part * EPT;
+      const float *sd = sl + KT;
+      const uint8_t *bx = stg + (t >> 5) * 8192 + part * EPT * 128;
+      float lq[EPT], dq[EPT], bq[EPT];
 #pragma unroll
       for (int c = 0; c < EPT; c += 4) {
         const float4 l4 = *reinterpret_cast<const float4 *>(sl + c);
         const float4 d4 = *reinterpret_cast<const float4 *>(sd + c);
-        const float lv[4] = {l4.x, l4.y, l4.z, l4.w}, dq4[4] = {d4.x, d4.y, d4.z, d4.w};
-        float p[4], ds[4];
+        lq[c] = l4.x * LOG2E_F; lq[c + 1] = l4.y * LOG2E_F;
+        lq[c + 2] = l4.z * LOG2E_F; lq[c + 3] = l4.w * LOG2E_F;
+        dq[c] = d4.x; dq[c + 1] = d4.y; dq[c + 2] = d4.z; dq[c + 3] = d4.w;
+      }
+      if (BIAS) {
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
+        for (int qq = 0; qq < EPT; ++qq)
+          bq[qq] = *reinterpret_cast<const float *>(bx + qq * 128 + boff[qq & 7]) * LOG2E_F;
+      }
+      tmem_wait_ld();
+      uint32_t pp[EPT / 2], pd[EPT / 2];
+      const bool full = kv && qb + EPT <= L;
+#pragma unroll
+      for (int c = 0; c < EPT; c += 2) {
+        float p[2], ds[2];
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
           const int qq = c + e;
-          float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lv[e]);
-          if (BIAS) x = fmaf(bias_at(stg + (t >> 5) * 8192, part * EPT + qq, t & 31), LOG2E_F, x);
-          p[e] = (kv && qb + qq < L) ? ex2f(x) : 0.f;
-          ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq4[e]);
+          float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
+          if (BIAS) x += bq[qq];
+          p[e] = ex2f(x);
+          if (!full && !(kv && qb + qq < L)) p[e] = 0.f;
+          ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
         }
         pp[c >> 1] = pk2(p[0], p[1]);
-        pp[(c >> 1) + 1] = pk2(p[2], p[3]);
         pd[c >> 1] = pk2(ds[0], ds[1]);
-        pd[(c >> 1) + 1] = pk2(ds[2], ds[3]);
       }
       tst<EPT / 2>(lane_addr + bi * 192 + 128 + part * (EPT / 2), pp);
       tst<EPT / 2>(lane_addr + bi * 192 + 160 + part * (EPT / 2), pd);
@@ -756,20 +904,28 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       fence_before();
       __syncwarp();
       if (lane == 0) mbar_arrive(&pp2[bi]);
-    }
-    // dK = scale * acc, dV = acc
-    const int i = T - 1;
-    mbar_wait(&mmd[i & 1], (uint32_t)((i >> 1) & 1));
-    fence_after();
-    constexpr int OD = D / TPR;
-    uint32_t vk[OD], vv[OD];
-    tld<OD>(lane_addr + 384 + part * OD, vk);
-    tld<OD>(lane_addr + 384 + D + part * OD, vv);
-    tmem_wait_ld();
-    if (kv) {
-      const int64_t off = b * a.sb + (int64_t)k * a.sl + h * D + part * OD;
-      store_row_bf16<OD>(a.dk + off, vk, a.scale);
-      store_row_bf16<OD>(a.dv + off, vv, 1.f);
+      if (j == T - 1) {
+        // dK = scale * acc, dV = acc of row r
+        mbar_wait(&mmd[bi], (uint32_t)((g >> 1) & 1));
+        fence_after();
+        const uint32_t acc = lane_addr + 384 + 2 * D * (r & 1);
+        uint32_t vk[OD], vv[OD];
+        tld<OD>(acc + part * OD, vk);
+        tld<OD>(acc + D + part * OD, vv);
+        tmem_wait_ld();
+        fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&accr[r & 1]);
+        if (kv) {
+          const int64_t off = (b_lo + r) * a.sb + (int64_t)k * a.sl + h * D + part * OD;
+          store_row_bf16<OD>(a.dk + off, vk, a.scale);
+          store_row_bf16<OD>(a.dv + off, vv, 1.f);
+        }
+      }
+      if (++j == T) {
+        j = 0;
+        ++r;
+      }
     }
   }
   fence_before();
@@ -839,10 +995,12 @@ int check_flash(const evo_attn_desc *d, bool bwd) {
   return EVO_OK;
 }
 
-// batch rows per dq CTA: about two CTAs per SM over (q tiles x heads x chunks)
-int64_t flash_chunk(const evo_attn_desc *d, int64_t &nch) {
+// batch rows per persistent CTA: `per_sm` CTAs per SM over (tiles x heads x
+// chunks)
+int64_t flash_chunk(const evo_attn_desc *d, int per_sm, int64_t &nch) {
   const int64_t qt = (d->L + QT - 1) / QT;
-  nch = std::max<int64_t>(1, std::min<int64_t>(d->nb, 2 * num_sms() / std::max<int64_t>(1, qt * d->H)));
+  nch = std::max<int64_t>(1, std::min<int64_t>(d->nb, (int64_t)per_sm * num_sms() /
+                                                          std::max<int64_t>(1, qt * d->H)));
   const int64_t chunk = (d->nb + nch - 1) / nch;
   nch = (d->nb + chunk - 1) / chunk;
   return chunk;
@@ -860,7 +1018,7 @@ FlashWs flash_ws(const evo_attn_desc *d) {
   w.gate = w.Dq + pad((size_t)d->nb * d->H * d->L * 4);
   w.part = w.gate + pad((size_t)num_sms() * 8 * d->H * d->D * 4);
   int64_t nch;
-  flash_chunk(d, nch);
+  flash_chunk(d, 1, nch);
   w.total = w.part + (d->bias ? pad((size_t)nch * d->H * d->L * d->L * 4) : 0);
   return w;
 }
@@ -879,10 +1037,15 @@ int flash_fwd(const evo_attn_desc *d, cudaStream_t st) {
     mb = mq;
   }
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-  const size_t smem = NS_FWD * STG + QT * 2 * D + (3 * TPR_FWD * 128) * 4 + 9 * 8 + 16;
+  const size_t smem = NS_FWD * STG + 2 * QT * 2 * D + (3 * TPR_FWD * 128) * 4 +
+                      (2 + NS_FWD + 8) * 8 + 16;
   auto kfn = attn_flash_fwd_kernel<D, BIAS>;
   EVO_MAX_SMEM_ONCE(kfn);
-  dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
+  // one batch row per CTA (measured faster than persistent chunks: the
+  // softmax warps' per-row epilogue would serialise with the next row)
+  const int64_t nch = d->nb;
+  a.chunk = 1;
+  dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
   kfn<<<grid, nth_of(TPR_FWD), smem, st>>>(mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_flash_fwd_kernel");
   return EVO_OK;
@@ -900,7 +1063,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   int rc = attn_prep_run(d, dO, Dq, reinterpret_cast<float *>(ws + w.gate), st);
   if (rc != EVO_OK) return rc;
   int64_t nch;
-  a.chunk = flash_chunk(d, nch);
+  a.chunk = flash_chunk(d, 1, nch);
   a.Dq = Dq;
   a.dbias_part = BIAS ? reinterpret_cast<float *>(ws + w.part) : nullptr;
   CUtensorMap mq, mk, mv, mdo, mb, mq2, mdo2, mk2, mv2, mb2;
@@ -926,25 +1089,21 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   }
   {
     constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-    const size_t smem = NS_BWD * STG + 2 * QT * 2 * D + (1 + NS_BWD + 7) * 8 + 16;
+    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16;
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-    kfn<<<grid, nth_of(TPR_BWD), smem, st>>>(mq, mk, mv, mdo, mb, a);
+    kfn<<<grid, nth_of(TPR_DQ), smem, st>>>(mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_flash_dq_kernel");
   }
   {
     constexpr uint32_t BT = BIAS ? 4 * 8192 : 0;
-    constexpr uint32_t STG = (BT + 2 * KT * 2 * D + 1023) / 1024 * 1024;
-    const int64_t T = (d->L + KT - 1) / KT;
-    const size_t smem = NS_BWD * STG + 2 * QT * 2 * D + 2 * (size_t)T * KT * 4 +
-                        (1 + NS_BWD + 7) * 8 + 16;
-    EVO_REQUIRE(smem <= 227 * 1024, EVO_EUNSUP, "attention_flash: L=%d too long for the dkv "
-                "kernel's staged lse / Dq", d->L);
+    constexpr uint32_t STG = (BT + 2 * KT * 2 * D + 2 * KT * 4 + 1023) / 1024 * 1024;
+    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16;
     auto kfn = attn_flash_dkv_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
-    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)d->nb);
-    kfn<<<grid, nth_of(TPR_BWD), smem, st>>>(mq2, mk2, mv2, mdo2, mb2, a);
+    dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
+    kfn<<<grid, nth_of(TPR_DKV), smem, st>>>(mq2, mk2, mv2, mdo2, mb2, a);
     EVO_LAUNCHED("attn_flash_dkv_kernel");
   }
   if (BIAS) {
