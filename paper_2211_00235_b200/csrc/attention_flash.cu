@@ -59,18 +59,32 @@ struct FlashArgs {
   int64_t chunk;
 };
 
-// swizzle of a [rows x D] bf16 tile with 2D-byte rows (TMA: 32B / 64B)
+// swizzle of a [rows x D] bf16 tile with 2D-byte rows (TMA: none / 32B / 64B)
 template <int D> struct Sw {
   static constexpr uint32_t bytes = 2 * D;
-  static constexpr uint32_t layout = D == 32 ? 4 : 6;
+  static constexpr uint32_t layout = D == 32 ? 4 : (D == 16 ? 6 : 0);
   static constexpr uint32_t sbo = 8 * bytes;
 };
+// K steps (16 wide) of a head-dim contraction; D = 8 runs one step whose
+// upper 8 columns come from a zero region (c_head = 8: the extra-MSA stack)
+template <int D> constexpr int ksteps() { return D < 16 ? 1 : D / 16; }
+// accumulator width (UMMA N >= 16): D = 8 accumulates 16 columns, the upper
+// 8 of which are never read
+template <int D> constexpr int dacc() { return D < 16 ? 16 : D; }
+// K-major [rows x D] operand, K step ks.  D = 8 (no swizzle, 16-byte rows):
+// the second 8-column core matrix sits `zlbo` bytes on (a zero region for the
+// padded operand, 0 = itself for the other one)
 template <int D>
-__device__ __forceinline__ uint64_t desc_k(uint32_t base, int ks) {
+__device__ __forceinline__ uint64_t desc_k(uint32_t base, int ks, uint32_t zlbo = 0) {
+  if constexpr (D == 8) return umma_desc(base, zlbo, 128, 0);
   return umma_desc(base + ks * 32, 16, Sw<D>::sbo, Sw<D>::layout);
 }
+// MN-major B(n = d, k = row) from a [rows x D] tile, K step ks (16 rows).
+// D = 8: core matrices of 8 rows x 16 B, K groups 128 B apart; the second N
+// group (columns 8..15) repeats the first (never read)
 template <int D>
 __device__ __forceinline__ uint64_t desc_mn(uint32_t base, int ks) {
+  if constexpr (D == 8) return umma_desc(base + ks * 256, 128, 0, 0);
   return umma_desc(base + ks * 16 * Sw<D>::bytes, 16, Sw<D>::sbo, Sw<D>::layout);
 }
 
@@ -169,6 +183,9 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
            *pvd = pp + 2, *ord = pvd + 2;
   constexpr int NBAR = 2 + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
+  // 2 KB of zeros above every operand: the padded head-dim half (D = 8)
+  uint8_t *sZ = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(tslot + 4) + 1023) & ~static_cast<uintptr_t>(1023));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
@@ -186,6 +203,10 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       mbar_init(bb, warps ? NEW : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (D == 8) {
+    for (int i = tid; i < 512; i += blockDim.x) reinterpret_cast<uint32_t *>(sZ)[i] = 0u;
+    fence_proxy_async_smem();
   }
   if (warp == 0) tmem_alloc(tslot, 256);
   fence_before();
@@ -222,7 +243,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     for (int r = 0; r < 2 && r < nrows; ++r) load_q(r);
     for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
-    const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    const uint32_t idesc_o = idesc_bf16(128, dacc<D>(), false, true);
     int r = 0, j = 0;          // coordinates of tile g
     int ri = 0, ji = -1;       // coordinates of tile g - 1
     for (int g = 0; g <= G; ++g) {
@@ -235,8 +256,9 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         const uint32_t sQa = smem_u32(sQ) + (r & 1) * QB;
         const uint32_t d = tmem + (g & 1) * 96;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16_el(d, desc_k<D>(sQa, ks), desc_k<D>(sK, ks), idesc_s, ks > 0);
+        for (int ks = 0; ks < ksteps<D>(); ++ks)
+          umma_bf16_el(d, desc_k<D>(sQa, ks, smem_u32(sZ) - sQa), desc_k<D>(sK, ks), idesc_s,
+                       ks > 0);
         umma_commit_el(&sdone[g & 1]);
         if (j == T - 1 && r + 2 < nrows) {
           mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));   // row r's S MMAs read Q
@@ -249,7 +271,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         if (ji == 0 && ri >= 2) mbar_wait(&ord[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
         fence_after();
         const uint32_t sV = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0) + KB;
-        const uint32_t oc = tmem + 192 + D * (ri & 1);
+        const uint32_t oc = tmem + 192 + dacc<D>() * (ri & 1);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
           umma_bf16_ts_el(oc, tmem + bi * 96 + 64 + 8 * ks, desc_mn<D>(sV, ks), idesc_o,
@@ -275,13 +297,13 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     const bool qv = q < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
-    constexpr int OD = D / TPR;
+    constexpr int OD = D / TPR < 4 ? 4 : D / TPR;   // epilogue columns per thread
     float m_run = -INFINITY, l = 0.f;
     int r = 0, j = 0;
     for (int g = 0; g < G; ++g) {
       const int bi = g & 1, st = g % NS;
       const int kb = j * KT + part * EPT;        // first key of this thread's EPT
-      const uint32_t oc = lane_addr + 192 + D * (r & 1) + part * OD;
+      const uint32_t oc = lane_addr + 192 + dacc<D>() * (r & 1) + part * OD;
       if (j == 0) {
         m_run = -INFINITY;
         l = 0.f;
@@ -466,6 +488,9 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
            *dqd = dsp + 2, *dqr = dqd + 2;
   constexpr int NBAR = 2 + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
+  // 2 KB of zeros above every operand: the padded head-dim half (D = 8)
+  uint8_t *sZ = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(tslot + 4) + 1023) & ~static_cast<uintptr_t>(1023));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
@@ -483,6 +508,10 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       mbar_init(bb, warps ? NEW : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (D == 8) {
+    for (int i = tid; i < 512; i += blockDim.x) reinterpret_cast<uint32_t *>(sZ)[i] = 0u;
+    fence_proxy_async_smem();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
@@ -520,7 +549,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     for (int r = 0; r < 2 && r < nrows; ++r) load_row(r);
     for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
-    const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    const uint32_t idesc_o = idesc_bf16(128, dacc<D>(), false, true);
     int r = 0, j = 0, ri = 0, ji = -1;
     for (int g = 0; g <= G; ++g) {
       if (g < G) {
@@ -532,11 +561,13 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         const uint32_t sQa = smem_u32(sQ) + (r & 1) * 2 * QB, sdOa = sQa + QB;
         const uint32_t d = tmem + (g & 1) * 160;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16_el(d, desc_k<D>(sQa, ks), desc_k<D>(sK, ks), idesc_s, ks > 0);
+        for (int ks = 0; ks < ksteps<D>(); ++ks)
+          umma_bf16_el(d, desc_k<D>(sQa, ks, smem_u32(sZ) - sQa), desc_k<D>(sK, ks), idesc_s,
+                       ks > 0);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16_el(d + 64, desc_k<D>(sdOa, ks), desc_k<D>(sV, ks), idesc_s, ks > 0);
+        for (int ks = 0; ks < ksteps<D>(); ++ks)
+          umma_bf16_el(d + 64, desc_k<D>(sdOa, ks, smem_u32(sZ) - sdOa), desc_k<D>(sV, ks),
+                       idesc_s, ks > 0);
         umma_commit_el(&sdone[g & 1]);
         if (j == T - 1 && r + 2 < nrows) {
           // row r's last S/dP MMAs read Q / dO: load row r + 2 into its buffer
@@ -552,7 +583,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 320 + D * (ri & 1), tmem + bi * 160 + 128 + 8 * ks,
+          umma_bf16_ts_el(tmem + 320 + dacc<D>() * (ri & 1), tmem + bi * 160 + 128 + 8 * ks,
                           desc_mn<D>(sK, ks), idesc_o, (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&dqd[bi]);
         if (i + NS < G) {
@@ -574,7 +605,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     const bool qv = q < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
-    constexpr int OD = D / TPR;
+    constexpr int OD = D / TPR < 4 ? 4 : D / TPR;   // epilogue columns per thread
     float *prow = BIAS ? a.dbias_part + (int64_t)blockIdx.z * a.H * L * (int64_t)L +
                              ((int64_t)h * L + q) * L
                        : nullptr;
@@ -667,7 +698,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         mbar_wait(&dqd[bi], (uint32_t)((g >> 1) & 1));
         fence_after();
         uint32_t v[OD];
-        tld<OD>(lane_addr + 320 + D * (r & 1) + part * OD, v);
+        tld<OD>(lane_addr + 320 + dacc<D>() * (r & 1) + part * OD, v);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
@@ -714,6 +745,9 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
            *mmd = pp2 + 2, *accr = mmd + 2;
   constexpr int NBAR = 2 + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
+  // 2 KB of zeros above every operand: the padded head-dim half (D = 8)
+  uint8_t *sZ = reinterpret_cast<uint8_t *>(
+      (reinterpret_cast<uintptr_t>(tslot + 4) + 1023) & ~static_cast<uintptr_t>(1023));
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int k0 = blockIdx.x * QT, h = blockIdx.y;
@@ -732,6 +766,10 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       mbar_init(bb, warps ? NEW : (stage ? 33 : 1));
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (D == 8) {
+    for (int i = tid; i < 512; i += blockDim.x) reinterpret_cast<uint32_t *>(sZ)[i] = 0u;
+    fence_proxy_async_smem();
   }
   if (warp == 0) tmem_alloc(tslot, 512);
   fence_before();
@@ -786,7 +824,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     for (int r = 0; r < 2 && r < nrows; ++r) load_kv(r);
     for (int g = 0; g < NS && g < G; ++g) load_tile(g);
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
-    const uint32_t idesc_o = idesc_bf16(128, D, false, true);
+    const uint32_t idesc_o = idesc_bf16(128, dacc<D>(), false, true);
     int r = 0, j = 0, ri = 0, ji = -1;
     for (int g = 0; g <= G; ++g) {
       if (g < G) {
@@ -798,11 +836,13 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         const uint32_t sKa = smem_u32(sK) + (r & 1) * 2 * KB, sVa = sKa + KB;
         const uint32_t d = tmem + (g & 1) * 192;
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16_el(d, desc_k<D>(sKa, ks), desc_k<D>(sQ, ks), idesc_s, ks > 0);
+        for (int ks = 0; ks < ksteps<D>(); ++ks)
+          umma_bf16_el(d, desc_k<D>(sKa, ks, smem_u32(sZ) - sKa), desc_k<D>(sQ, ks), idesc_s,
+                       ks > 0);
 #pragma unroll
-        for (int ks = 0; ks < D / 16; ++ks)
-          umma_bf16_el(d + 64, desc_k<D>(sVa, ks), desc_k<D>(sdO, ks), idesc_s, ks > 0);
+        for (int ks = 0; ks < ksteps<D>(); ++ks)
+          umma_bf16_el(d + 64, desc_k<D>(sVa, ks, smem_u32(sZ) - sVa), desc_k<D>(sdO, ks),
+                       idesc_s, ks > 0);
         umma_commit_el(&sdone[g & 1]);
         if (j == T - 1 && r + 2 < nrows) {
           mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));   // row r's K / V read
@@ -816,10 +856,10 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         fence_after();
         const uint32_t sQ = smem_u32(sStage + st * STG) + BT, sdO = sQ + QB;
         const uint32_t base = tmem + bi * 192;
-        const uint32_t acc = tmem + 384 + 2 * D * (ri & 1);
+        const uint32_t acc = tmem + 384 + 2 * dacc<D>() * (ri & 1);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(acc + D, base + 128 + 8 * ks, desc_mn<D>(sdO, ks), idesc_o,
+          umma_bf16_ts_el(acc + dacc<D>(), base + 128 + 8 * ks, desc_mn<D>(sdO, ks), idesc_o,
                           (ji > 0 || ks > 0) ? 1u : 0u);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
@@ -845,7 +885,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
     const bool kv = k < L;
     const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16);
     const float sc_l2 = a.scale * LOG2E_F;
-    constexpr int OD = D / TPR;
+    constexpr int OD = D / TPR < 4 ? 4 : D / TPR;   // epilogue columns per thread
     // transposed bias reads: element (q, kk = t & 31) of a [64 q x 32 k]
     // SW128 box sits at q*128 + ((kk/4 ^ q%8) << 4) + (kk%4)*4; q % 8 is the
     // compile-time qq % 8 (part*EPT is a multiple of 8)
@@ -908,15 +948,15 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         // dK = scale * acc, dV = acc of row r
         mbar_wait(&mmd[bi], (uint32_t)((g >> 1) & 1));
         fence_after();
-        const uint32_t acc = lane_addr + 384 + 2 * D * (r & 1);
+        const uint32_t acc = lane_addr + 384 + 2 * dacc<D>() * (r & 1);
         uint32_t vk[OD], vv[OD];
         tld<OD>(acc + part * OD, vk);
-        tld<OD>(acc + D + part * OD, vv);
+        tld<OD>(acc + dacc<D>() + part * OD, vv);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&accr[r & 1]);
-        if (kv) {
+        if (kv && part * OD < D) {
           const int64_t off = (b_lo + r) * a.sb + (int64_t)k * a.sl + h * D + part * OD;
           store_row_bf16<OD>(a.dk + off, vk, a.scale);
           store_row_bf16<OD>(a.dv + off, vv, 1.f);
@@ -942,7 +982,8 @@ bool flash_head_map(CUtensorMap *m, const void *base, int D, int L, int64_t nb, 
   cuuint64_t strides[3] = {(cuuint64_t)sl * 2, (cuuint64_t)sb * 2, (cuuint64_t)D * 2};
   cuuint32_t box[4] = {(cuuint32_t)D, (cuuint32_t)box_rows, 1, 1};
   cuuint32_t es[4] = {1, 1, 1, 1};
-  CUtensorMapSwizzle sw = D == 32 ? CU_TENSOR_MAP_SWIZZLE_64B : CU_TENSOR_MAP_SWIZZLE_32B;
+  CUtensorMapSwizzle sw = D == 32 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : (D == 16 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE);
   return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, const_cast<void *>(base), dims, strides, box,
             es, CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
@@ -979,9 +1020,9 @@ FlashArgs flash_args(const evo_attn_desc *d) {
 bool al16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
 
 int check_flash(const evo_attn_desc *d, bool bwd) {
-  EVO_REQUIRE(d && d->dtype == EVO_BF16 && (d->D == 16 || d->D == 32) && d->L >= 1 &&
+  EVO_REQUIRE(d && d->dtype == EVO_BF16 && (d->D == 8 || d->D == 16 || d->D == 32) && d->L >= 1 &&
                   d->nb >= 1 && d->nb <= 65535 && d->H >= 1 && d->H <= 65535,
-              EVO_EUNSUP, "attention_flash: bf16, head dim 16 / 32, nb <= 65535 (D=%d L=%d nb=%lld)",
+              EVO_EUNSUP, "attention_flash: bf16, head dim 8 / 16 / 32, nb <= 65535 (D=%d L=%d nb=%lld)",
               d ? d->D : -1, d ? d->L : -1, d ? (long long)d->nb : -1ll);
   EVO_REQUIRE(d->sb % 8 == 0 && d->sl % 8 == 0 && d->o_sb % 8 == 0 && d->o_sl % 8 == 0 &&
                   al16(d->q) && al16(d->k) && al16(d->v) && al16(d->g) && al16(d->o),
@@ -1038,7 +1079,7 @@ int flash_fwd(const evo_attn_desc *d, cudaStream_t st) {
   }
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
   const size_t smem = NS_FWD * STG + 2 * QT * 2 * D + (3 * TPR_FWD * 128) * 4 +
-                      (2 + NS_FWD + 8) * 8 + 16;
+                      (2 + NS_FWD + 8) * 8 + 16 + 1024 + 2048;
   auto kfn = attn_flash_fwd_kernel<D, BIAS>;
   EVO_MAX_SMEM_ONCE(kfn);
   // one batch row per CTA (measured faster than persistent chunks: the
@@ -1089,7 +1130,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   }
   {
     constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16;
+    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16 + 1024 + 2048;
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
@@ -1099,7 +1140,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   {
     constexpr uint32_t BT = BIAS ? 4 * 8192 : 0;
     constexpr uint32_t STG = (BT + 2 * KT * 2 * D + 2 * KT * 4 + 1023) / 1024 * 1024;
-    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16;
+    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16 + 1024 + 2048;
     auto kfn = attn_flash_dkv_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
@@ -1127,7 +1168,8 @@ EVO_API int evo_attn_flash_fwd(const evo_attn_desc *d, void *stream) {
   cudaStream_t st = as_stream(stream);
   note_backend(EVO_BK_ATTN_FLASH);
   if (d->D == 32) return d->bias ? flash_fwd<32, true>(d, st) : flash_fwd<32, false>(d, st);
-  return d->bias ? flash_fwd<16, true>(d, st) : flash_fwd<16, false>(d, st);
+  if (d->D == 16) return d->bias ? flash_fwd<16, true>(d, st) : flash_fwd<16, false>(d, st);
+  return d->bias ? flash_fwd<8, true>(d, st) : flash_fwd<8, false>(d, st);
 }
 
 EVO_API size_t evo_attn_flash_bwd_workspace_bytes(const evo_attn_desc *d) {
@@ -1142,7 +1184,8 @@ EVO_API int evo_attn_flash_bwd(const evo_attn_desc *d, void *stream) {
   cudaStream_t st = as_stream(stream);
   note_backend(EVO_BK_ATTN_FLASH);
   if (d->D == 32) return d->bias ? flash_bwd<32, true>(d, st) : flash_bwd<32, false>(d, st);
-  return d->bias ? flash_bwd<16, true>(d, st) : flash_bwd<16, false>(d, st);
+  if (d->D == 16) return d->bias ? flash_bwd<16, true>(d, st) : flash_bwd<16, false>(d, st);
+  return d->bias ? flash_bwd<8, true>(d, st) : flash_bwd<8, false>(d, st);
 }
 
 }  // extern "C"

@@ -2168,7 +2168,7 @@ int attention_tc_fwd(const evo_attn_desc *d, cudaStream_t st) {
 // into d->dgate_bias when set (gpart: SMs*8*H*D fp32 of workspace).
 int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
                   cudaStream_t st) {
-  if (d->D != 16 && d->D != 32) return EVO_EUNSUP;
+  if (d->D != 8 && d->D != 16 && d->D != 32) return EVO_EUNSUP;
   AttnTcArgs a = make_args(d);
   int64_t total = d->nb * (int64_t)d->L * d->H * (d->D / 8);
   const bool fuse_gb = d->dgate_bias && (256 % (d->H * (d->D / 8)) == 0);
@@ -2182,8 +2182,10 @@ int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
   float *gp = fuse_gb ? gpart : nullptr;
   if (d->D == 32)
     attn_bwd_prep_kernel<32><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
-  else
+  else if (d->D == 16)
     attn_bwd_prep_kernel<16><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+  else
+    attn_bwd_prep_kernel<8><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
   EVO_LAUNCHED("attn_bwd_prep_kernel");
   if (fuse_gb) return colsum_partials(blocks, (int64_t)d->H * d->D, gp, d->dgate_bias, 0, st);
   return EVO_OK;

@@ -234,9 +234,10 @@ KEEP_P_MAX_BYTES = int(_os.environ.get("EVO_KEEP_P_MAX_BYTES", str(8 << 30)))
 
 
 def use_flash(dtype, L: int, D: int) -> bool:
-    """bf16, L > 256 keys, head dim 16 / 32: the streamed-key fused attention
+    """bf16 with L > 256 keys (head dim 8 / 16 / 32) or head dim 8 (any L:
+    the extra-MSA stack's c_head = 8): the streamed-key fused attention
     (csrc/attention_flash.cu)."""
-    return dtype == torch.bfloat16 and L > LONG_L and D in (16, 32)
+    return dtype == torch.bfloat16 and ((L > LONG_L and D in (8, 16, 32)) or D == 8)
 
 
 def use_long(dtype, L: int, D: int) -> bool:
@@ -262,7 +263,7 @@ def _attn_desc(proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bia
 
 def attention_flash(*, proj, hc, nb, H, L, D, scale, sb, sl, o, gm, o_sb, o_sl, lse, bias=None,
                     bh=0, bq=0, bk=0, dgm=None, dproj=None, dbias=None, dgate_bias=None):
-    """L > 256 keys on the bf16 path, head dim 16 / 32: csrc/attention_flash.cu
+    """L > 256 keys or head dim 8 on the bf16 path: csrc/attention_flash.cu
     (keys streamed through TMEM with an online softmax; the backward's dS
     never leaves the SM either).  Same argument meaning as ``attention``."""
     four = 4 * hc

@@ -209,6 +209,13 @@ FLASH = [
     (3, 333, 2, 32, True, "transposed"),  # ragged L: padded plain bias copy
     (2, 1024, 2, 16, True, "none"),
     (40, 320, 4, 32, False, "plain"),     # several batch rows per dq CTA
+    # head dim 8 (the extra-MSA stack, c_head = c_e / h = 8): zero-padded to
+    # the 16-wide MMA K step
+    (6, 64, 4, 8, False, "plain"),        # extra-MSA row attention (small r)
+    (4, 256, 8, 8, True, "none"),         # column attention
+    (3, 1024, 8, 8, True, "none"),        # C3 extra column attention over s_e = 1024
+    (5, 200, 4, 8, True, "transposed"),   # triangle end
+    (9, 130, 8, 8, False, "plain"),
 ]
 
 
