@@ -29,6 +29,21 @@ import os
 
 MSA_SUBOPS = ("row_attn", "col_attn", "msa_transition", "opm")
 MSA_TRACK = ("row_attn", "col_attn", "msa_transition")
+# the pair track on a second CUDA stream, concurrent with the MSA track
+# (block_fwd / block_bwd); EVO_BRANCH_STREAMS=0 runs them back to back
+BRANCH_STREAMS = os.environ.get("EVO_BRANCH_STREAMS", "1") != "0"
+_SIDE = {}
+
+
+def side_stream(dev):
+    """The per-device second stream of the two-track block."""
+    key = torch.device(dev)
+    s = _SIDE.get(key)
+    if s is None:
+        s = _SIDE[key] = torch.cuda.Stream(device=key)
+    return s
+
+
 # 3-product bf16 first projection in the transitions (see transition_fwd);
 # EVO_SPLIT_TRANSITION=0 turns it off (plain bf16 operands)
 SPLIT_TRANSITION = os.environ.get("EVO_SPLIT_TRANSITION", "1") != "0"
@@ -318,7 +333,8 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     return x_new, ctx
 
 
-def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None, dz_res=None):
+def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None, dz_res=None,
+             join=None):
     """Returns (dx [rows, c_io] fp32, dz_row or None).  handoff: the emit
     dict of the producer of dx_new (see _ln_bwd_out); emit: this sub-op's.
     dz_res (row attention, fused path only): added to dz_row inside its
@@ -357,6 +373,8 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
         # dbias) fuses into the LayerNorm backward of its input
         if name == "row_attn":
             dz_row = _empty((r2, cfg.c_z), F32, dev)
+            if join is not None and dz_res is not None:
+                join()      # dz_res comes from the pair branch's stream
             K.layernorm_bwd_proj(None, ctx["z"], r2, ctx["zmu"], ctx["zrs"], P[f"{px}.lnz_g"],
                                  P[f"{px}.lnz_b"], dbias, r2, pk["Wb"], h, dz_row, G["lnz_g"],
                                  G["lnz_b"], G["Wb"], dres=dz_res)
@@ -700,10 +718,12 @@ def msa_emit(G):
     return dict(bias=G["msa_transition"]["b2"])
 
 
-def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None, dz_pair=None):
+def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None, dz_pair=None, join=None):
     """dm: grad of the MSA-track output (incl. the OPM contribution; handoff:
     the OPM backward's emit dict); returns (dm_in, dz_row), or with dz_pair
-    given (single-process block) (dm_in, dz_in = dz_pair + dz_row)."""
+    given (single-process block) (dm_in, dz_in = dz_pair + dz_row).  join:
+    called right before the first launch that reads dz_pair (the pair
+    branch's stream joins there)."""
     e1 = dict(bias=G["col_attn"]["bo"])
     dm = transition_bwd(P, f"blk{blk}.msa_transition", pk["msa_transition"],
                         G["msa_transition"], ctxs["msa_transition"], dm, cfg, act,
@@ -717,8 +737,10 @@ def msa_branch_bwd(P, blk, pk, G, ctxs, dm, cfg, act, handoff=None, dz_pair=None
         return dm, dz_row
     dm, dz, joined = attn_bwd("row_attn", P, f"blk{blk}.row_attn", pk["row_attn"],
                               G["row_attn"], ctxs["row_attn"], dm, cfg, act, handoff=e2,
-                              dz_res=dz_pair)
+                              dz_res=dz_pair, join=join)
     if not joined:
+        if join is not None:
+            join()
         dz_in = torch.empty_like(dz_pair)
         K.add(dz_pair, dz, dz_in)
         dz = dz_in
@@ -730,8 +752,19 @@ def block_fwd(P, blk, pk, m, z, cfg, act):
     the af2 / multimer wirings dispatch to variant_block_fwd."""
     if cfg.variant != "parallel":
         return variant_block_fwd(P, blk, pk, m, z, cfg, act)
-    m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z, cfg, act)
-    z_pair, cp_ = pair_branch_fwd(P, blk, pk, z, cfg, act)
+    if BRANCH_STREAMS:
+        # the two tracks are independent inside a parallel block (the premise
+        # of branch parallelism): the pair track runs on a second stream of
+        # this GPU while the MSA track runs here, joined before the OPM
+        main, side = torch.cuda.current_stream(m.device), side_stream(m.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            z_pair, cp_ = pair_branch_fwd(P, blk, pk, z, cfg, act)
+        m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z, cfg, act)
+        main.wait_stream(side)
+    else:
+        m_new, cm_ = msa_branch_fwd(P, blk, pk, m, z, cfg, act)
+        z_pair, cp_ = pair_branch_fwd(P, blk, pk, z, cfg, act)
     z_new, co = opm_fwd(P, f"blk{blk}.opm", pk["opm"], m_new, z_pair, cfg, act)
     ctx = dict(msa=cm_, pair=cp_, opm=co)
     return m_new, z_new, ctx
@@ -785,11 +818,24 @@ def block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act):
         return variant_block_bwd(P, blk, pk, G, ctx, dm_out, dz_out, cfg, act)
     dz_act = cast_act(dz_out, act)
     e0 = msa_emit(G)
-    dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act, dm_out,
-                  cfg, act, emit=e0)
-    dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act, dz_act=dz_act)
+    join = None
+    if BRANCH_STREAMS:
+        # pair-track backward on the second stream, concurrent with the OPM
+        # and MSA-track backward; joined where dz_pair is consumed
+        main, side = torch.cuda.current_stream(dz_out.device), side_stream(dz_out.device)
+        side.wait_stream(main)
+        with torch.cuda.stream(side):
+            dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act,
+                                      dz_act=dz_act)
+        join = lambda: main.wait_stream(side)
+        dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act,
+                      dm_out, cfg, act, emit=e0)
+    else:
+        dm3 = opm_bwd(P, f"blk{blk}.opm", pk["opm"], G["opm"], ctx["opm"], dz_out, dz_act,
+                      dm_out, cfg, act, emit=e0)
+        dz_pair = pair_branch_bwd(P, blk, pk, G, ctx["pair"], dz_out, cfg, act, dz_act=dz_act)
     # dz_in = dz_pair + dz_row (the BP allreduce's two operands), joined
     # inside the row attention's LayerNorm backward when fused
     dm_in, dz_in = msa_branch_bwd(P, blk, pk, G, ctx["msa"], dm3, cfg, act, handoff=e0,
-                                  dz_pair=dz_pair)
+                                  dz_pair=dz_pair, join=join)
     return dm_in, dz_in

@@ -273,3 +273,33 @@ def test_activation_checkpointing_bitwise(pkg, precision):
     ga, gb = a.grad_dict(), b.grad_dict()
     for k in ga:
         assert torch.equal(ga[k], gb[k]), k
+
+
+@pytest.mark.parametrize("precision", ["fp32", "bf16"])
+def test_branch_streams_bitwise(pkg, precision, monkeypatch):
+    """The pair track on a second stream (engine.BRANCH_STREAMS) is the same
+    launches on the same inputs: bitwise equal to running them back to back,
+    eager and graph-captured."""
+    from paper_2211_00235_b200 import engine as E, schedules as S
+    cfg = pkg.EvoConfig(**KW)
+    store = pkg.init_params(cfg, 32)
+    m, z = S.make_batch(cfg, 32, 1)[0]
+    monkeypatch.setattr(E, "BRANCH_STREAMS", False)
+    a = S.StepState(cfg, store, precision)
+    ref = [t.clone() for t in S.full_step(a, m, z)]
+    g_ref = {k: v.clone() for k, v in a.grad_dict().items()}
+    monkeypatch.setattr(E, "BRANCH_STREAMS", True)
+    b = S.StepState(cfg, store, precision)
+    out = S.full_step(b, m, z)
+    torch.cuda.synchronize()
+    for x, y in zip(ref, out):
+        assert torch.equal(x, y)
+    for k, v in b.grad_dict().items():
+        assert torch.equal(v, g_ref[k]), k
+    gs = b.capture(m, z, warmup=0)
+    out = gs.step(m, z)
+    torch.cuda.synchronize()
+    for x, y in zip(ref, out):
+        assert torch.equal(x, y)
+    for k, v in b.grad_dict().items():
+        assert torch.equal(v, g_ref[k]), k
