@@ -452,14 +452,20 @@ def run_native(args):
         fl, tms, n = fam_graph[top]
         achieved = fl / (tms / 1e3) / 1e12
         traffic = None
-        try:  # DRAM bytes per launch of this family from the committed ncu capture
-            with open(os.path.join(ROOT, "profiles", "r01_family_dram.json")) as f:
-                traffic = json.load(f)["families"][top]["dram_bytes_per_launch"]
-        except Exception:
-            traffic = None
+        # DRAM bytes per launch of this family from the committed ncu capture
+        # of this configuration (tools/step_trace.py --family-json)
+        dram_file = {(256, 128): "r02_family_dram.json",
+                     (384, 128): "r02_family_dram_crop384.json"}.get((cfg.r, cfg.s))
+        if dram_file and cfg.n_blocks == 1 and cfg.c_m == 256:
+            try:
+                with open(os.path.join(ROOT, "profiles", dram_file)) as f:
+                    traffic = json.load(f)["families"][top]["dram_bytes_per_launch"]
+            except Exception:
+                traffic = None
         roof = {"bound": "tensor", "kernel": top, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
-                "traffic_unit": "DRAM bytes per launch (profiles/r01_family_dram.json)",
+                "traffic_unit": f"DRAM bytes per launch (profiles/{dram_file})" if traffic
+                else None,
                 "algorithmic_flops_per_launch": fl / n,
                 "peak_source": src, "launches": n, "share_of_step": tms / ms,
                 "timing": "CUDA events around one step's launches of this family, "

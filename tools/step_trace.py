@@ -59,7 +59,7 @@ def family_of(name):
     return None
 
 
-def join(csv_path, shapes_path):
+def join(csv_path, shapes_path, json_out=None):
     with open(shapes_path) as f:
         calls = json.load(f)
     rows = []
@@ -111,6 +111,12 @@ def join(csv_path, shapes_path):
     for k, (us, fl, n, byt) in fam_tot.items():
         print(f"family {k}: {n} launches, {us:.1f} us, {fl / us / 1e6:.1f} TF/s, "
               f"DRAM {byt / 1e6:.1f} MB ({byt / max(n, 1) / 1e6:.2f} MB per launch)")
+    if json_out:
+        with open(json_out, "w") as f:
+            json.dump({"source": os.path.basename(csv_path),
+                       "families": {k: {"launches": n, "us": us, "dram_bytes": byt,
+                                        "dram_bytes_per_launch": byt / max(n, 1)}
+                                    for k, (us, fl, n, byt) in fam_tot.items()}}, f, indent=1)
     agg = {}
     for fam, shp, fl, us, names, _b in groups:
         key = f"{fam} {shp}" if shp else fam
@@ -131,8 +137,10 @@ if __name__ == "__main__":
     ap.add_argument("--crop", type=int, default=0)
     ap.add_argument("--shapes", default="gpurun_out/trace_shapes.json")
     ap.add_argument("--join", nargs=2, metavar=("CSV", "SHAPES"))
+    ap.add_argument("--family-json", default=None,
+                    help="with --join: write per-family DRAM bytes per launch here")
     a = ap.parse_args()
     if a.join:
-        join(*a.join)
+        join(*a.join, json_out=a.family_json)
     else:
         run(a)
