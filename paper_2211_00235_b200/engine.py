@@ -44,6 +44,61 @@ def side_stream(dev):
     return s
 
 
+# weight-gradient GEMMs (and their bias column sums) off the critical path:
+# on a helper stream of the current stream, joined at the end of the sub-op
+# backward that forked them; EVO_DW_STREAMS=0 keeps them in line
+DW_STREAMS = os.environ.get("EVO_DW_STREAMS", "1") != "0"
+_HELPER = {}
+
+
+def helper_stream(cur):
+    key = (cur.device, cur.cuda_stream)
+    s = _HELPER.get(key)
+    if s is None:
+        s = _HELPER[key] = torch.cuda.Stream(device=cur.device)
+    return s
+
+
+class OffPath:
+    """``with off.path(): ...`` runs the enclosed launches (which only write
+    gradient banks) on the current stream's helper stream after everything
+    issued so far; ``off.join()`` makes the current stream wait for them.
+    The enclosed launches' inputs stay referenced by the caller until the
+    join, so the allocator cannot recycle them early."""
+
+    def __init__(self):
+        self.pending = []
+
+    def path(self):
+        return _OffCtx(self)
+
+    def join(self):
+        for cur, hs in self.pending:
+            cur.wait_stream(hs)
+        self.pending = []
+
+
+class _OffCtx:
+    def __init__(self, off):
+        self.off, self.ctx = off, None
+
+    def __enter__(self):
+        if not DW_STREAMS:
+            return self
+        cur = torch.cuda.current_stream()
+        hs = helper_stream(cur)
+        hs.wait_stream(cur)
+        self.off.pending.append((cur, hs))
+        self.ctx = torch.cuda.stream(hs)
+        self.ctx.__enter__()
+        return self
+
+    def __exit__(self, *exc):
+        if self.ctx is not None:
+            self.ctx.__exit__(*exc)
+        return False
+
+
 # 3-product bf16 first projection in the transitions (see transition_fwd);
 # EVO_SPLIT_TRANSITION=0 turns it off (plain bf16 operands)
 SPLIT_TRANSITION = os.environ.get("EVO_SPLIT_TRANSITION", "1") != "0"
@@ -346,10 +401,12 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
     c_io = dx_new.shape[-1]
     r2 = cfg.r * cfg.r
     dxa, bias_done = _grad_in(dx_new, rows, c_io, act, dev, handoff)
+    off = OffPath()
     # out-projection
-    K.linear_dw(ctx["gm"], rows, hc, dxa, c_io, G["Wo"], c_io)
-    if not bias_done:
-        K.colsum(dx_new, rows, c_io, G["bo"])
+    with off.path():
+        K.linear_dw(ctx["gm"], rows, hc, dxa, c_io, G["Wo"], c_io)
+        if not bias_done:
+            K.colsum(dx_new, rows, c_io, G["bo"])
     dgm = _empty((rows, hc), act, dev)
     K.linear_dx(dxa, rows, c_io, pk["Wo"], c_io, hc, dgm)
     # attention core (+ gate) backward
@@ -364,7 +421,8 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
                 dgm=dgm, dproj=dproj, dbias=dbias, dgate_bias=G["gate_b"],
                 p_store=ctx.get("p_store"))
     xh = ctx["xh"]
-    K.linear_dw(xh, rows, c_io, dproj, 4 * hc, G["Wqkvg"], 4 * hc)
+    with off.path():
+        K.linear_dw(xh, rows, c_io, dproj, 4 * hc, G["Wqkvg"], 4 * hc)
     dxh = _empty((rows, c_io), F32, dev)
     K.linear_dx(dproj, rows, 4 * hc, pk["Wqkvg"], 4 * hc, c_io, dxh)
     dz_row = None
@@ -392,6 +450,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
                                  dx_colsum=colsum)
             if emit is not None:
                 emit["act"], emit["done"] = dxa_out, True
+            off.join()
             return dx, None
     if dbias is not None and not ctx["fuse_bias"]:
         dbias_a = dbias if act == F32 else _empty((h, r2), act, dev)
@@ -413,6 +472,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
                    cfg.c_z, h, accumulate=True)
     dx = _ln_bwd_out(dxh, ctx["x"], rows, c_io, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
                      G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
+    off.join()
     if dz_res is not None:
         if ctx["fuse_bias"]:
             return dx, dz_row, True
@@ -467,22 +527,28 @@ def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
     rows, cx = dx_new.shape[0], dx_new.shape[1]
     tc = cfg.t_factor * cx
     dxa, bias_done = _grad_in(dx_new, rows, cx, act, dev, handoff)
-    K.linear_dw(ctx["hid"], rows, tc, dxa, cx, G["W2"], cx)
-    if not bias_done:
-        K.colsum(dx_new, rows, cx, G["b2"])
+    off = OffPath()
+    with off.path():
+        K.linear_dw(ctx["hid"], rows, tc, dxa, cx, G["W2"], cx)
+        if not bias_done:
+            K.colsum(dx_new, rows, cx, G["b2"])
     dhid = _empty((rows, tc), act, dev)
     K.linear_dx(dxa, rows, cx, pk["W2"], cx, tc, dhid)
     if act != F32 and tc % 8 == 0:
         K.relu_bwd_colsum(dhid, ctx["hid"], dhid, rows, tc, G["b1"])
-        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
+        with off.path():
+            K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
     else:
         K.relu_bwd(dhid, ctx["hid"], dhid, rows * tc)
-        K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
-        K.colsum(dhid, rows, tc, G["b1"])
+        with off.path():
+            K.linear_dw(ctx["xh"], rows, cx, dhid, tc, G["W1"], tc, x_ld=ctx["xh_ld"])
+            K.colsum(dhid, rows, tc, G["b1"])
     dxh = _empty((rows, cx), F32, dev)
     K.linear_dx(dhid, rows, tc, pk["W1"], tc, cx, dxh)
-    return _ln_bwd_out(dxh, ctx["x"], rows, cx, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
-                       G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
+    dx = _ln_bwd_out(dxh, ctx["x"], rows, cx, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                     G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
+    off.join()
+    return dx
 
 
 # ---------------------------------------------------------------------------
@@ -517,8 +583,10 @@ def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None):
     s, r, cm, c, cz = cfg.s, cfg.r, cfg.c_m, cfg.c_opm, cfg.c_z
     rows, rc, r2 = s * r, r * c, r * r
     o, ab = ctx["o"], ctx["ab"]
-    K.linear_dw(o, r2, c * c, dz_out_act, cz, G["Wo"], cz)
-    K.colsum(dz_out, r2, cz, G["bo"])
+    off = OffPath()
+    with off.path():
+        K.linear_dw(o, r2, c * c, dz_out_act, cz, G["Wo"], cz)
+        K.colsum(dz_out, r2, cz, G["bo"])
     # do'[i,p,j,q] = (1/s) dz_out[(i,j)] . Wo[(p,q)]   (raw layout [(i,p),(j,q)])
     dor = _empty((rc, rc), act, dev)
     K.gemm(Mat(dz_out_act, cz, 1), Mat(pk["Wo"], cz, 1),
@@ -532,17 +600,21 @@ def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None):
     # db[s,(j,q)] = sum_(i,p) a[s,(i,p)] do'[(i,p),(j,q)]
     K.gemm(Mat(ab[0], rc, 1), Mat(dor, 1, rc), Mat(dab[1], rc, 1), s, rc, rc, split_k=sk)
     mh = ctx["mh"]
-    # dWab[:, w*c:(w+1)*c] = mh^T dab[w]   (batched over w)
-    K.gemm(Mat(mh, 1, cm, bs1=0), Mat(dab, 1, c, bs1=rows * c), Mat(G["Wab"], 2 * c, 1, bs1=c),
-           cm, c, rows, B1=2, split_k=K.pick_split(rows, cm, c, 2))
-    K.colsum(dab[0], rows, c, G["bab"][:c])
-    K.colsum(dab[1], rows, c, G["bab"][c:])
+    with off.path():
+        # dWab[:, w*c:(w+1)*c] = mh^T dab[w]   (batched over w)
+        K.gemm(Mat(mh, 1, cm, bs1=0), Mat(dab, 1, c, bs1=rows * c),
+               Mat(G["Wab"], 2 * c, 1, bs1=c), cm, c, rows, B1=2,
+               split_k=K.pick_split(rows, cm, c, 2))
+        K.colsum(dab[0], rows, c, G["bab"][:c])
+        K.colsum(dab[1], rows, c, G["bab"][c:])
     dmh = _empty((rows, cm), F32, dev)
     K.gemm(Mat(dab[0], c, 1), Mat(pk["Wab"], 2 * c, 1), Mat(dmh, cm, 1), rows, cm, c)
     K.gemm(Mat(dab[1], c, 1), Mat(pk["Wab"], 2 * c, 1, off=c), Mat(dmh, cm, 1), rows, cm, c,
            accumulate=True)
-    return _ln_bwd_out(dmh, ctx["m"], rows, cm, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
-                       G["ln_g"], G["ln_b"], dm_res, act, emit, dev)
+    dm = _ln_bwd_out(dmh, ctx["m"], rows, cm, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
+                     G["ln_g"], G["ln_b"], dm_res, act, emit, dev)
+    off.join()
+    return dm
 
 
 # ---------------------------------------------------------------------------
@@ -606,9 +678,11 @@ def trimul_bwd(P, px, pk, G, ctx, dz_new, cfg, act):
                       do_colsum=G["bo"], dg_colsum=G["bp"][4 * c:])
     else:
         K.outgate_bwd(dz_new, r2, cz, proj, ldp, 4 * c, ctx["o"], do, dproj, ldp, 4 * c)
-    K.linear_dw(ctx["pn"], r2, c, do, cz, G["Wo"], cz)
-    if not fused_cs:
-        K.colsum(do, r2, cz, G["bo"])
+    off = OffPath()
+    with off.path():
+        K.linear_dw(ctx["pn"], r2, c, do, cz, G["Wo"], cz)
+        if not fused_cs:
+            K.colsum(do, r2, cz, G["bo"])
     dpn = _empty((r2, c), F32, dev)
     K.linear_dx(do, r2, cz, pk["Wo"], cz, c, dpn)
     dp_cf = _empty((c, r, r), act, dev)
@@ -632,14 +706,16 @@ def trimul_bwd(P, px, pk, G, ctx, dz_new, cfg, act):
     K.trimul_gate_bwd(proj, r2, c, ldp, da_cf, db_cf, dproj, ldp,
                       colsum=G["bp"][:4 * c] if fused_cs else None)
     zh = ctx["zh"]
-    K.linear_dw(zh, r2, cz, dproj, ldp, G["Wp"], ldp)
-    if not fused_cs:
-        K.colsum(dproj, r2, ldp, G["bp"])
+    with off.path():
+        K.linear_dw(zh, r2, cz, dproj, ldp, G["Wp"], ldp)
+        if not fused_cs:
+            K.colsum(dproj, r2, ldp, G["bp"])
     dzh = _empty((r2, cz), F32, dev)
     K.linear_dx(dproj, r2, ldp, pk["Wp"], ldp, cz, dzh)
     dz = _empty((r2, cz), F32, dev)
     K.layernorm_bwd(dzh, ctx["z"], r2, cz, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"], dz,
                     G["ln_g"], G["ln_b"], dres=dz_new if ctx["resid"] else None)
+    off.join()
     return dz
 
 
