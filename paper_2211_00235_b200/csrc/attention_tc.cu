@@ -1481,19 +1481,35 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
     }
     const bool full = kv && qb + 16 <= L;
     uint32_t pk[8], dk8[8];
+    if (full) {  // interior units: no per-element mask
 #pragma unroll
-    for (int j = 0; j < 16; j += 2) {
-      float pp2[2], ds[2];
+      for (int j = 0; j < 16; j += 2) {
+        float pp2[2], ds[2];
 #pragma unroll
-      for (int w2 = 0; w2 < 2; ++w2) {
-        float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -ls[j + w2]);
-        if (BIASMODE) x += bb[j + w2];
-        const float e = ex2(x);
-        pp2[w2] = full ? e : ((kv && qb + j + w2 < L) ? e : 0.f);
-        ds[w2] = pp2[w2] * (__uint_as_float(dv[j + w2]) - dq[j + w2]);
+        for (int w2 = 0; w2 < 2; ++w2) {
+          float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -ls[j + w2]);
+          if (BIASMODE) x += bb[j + w2];
+          pp2[w2] = ex2(x);
+          ds[w2] = pp2[w2] * (__uint_as_float(dv[j + w2]) - dq[j + w2]);
+        }
+        pk[j >> 1] = pack2(pp2[0], pp2[1]);
+        dk8[j >> 1] = pack2(ds[0], ds[1]);
       }
-      pk[j >> 1] = pack2(pp2[0], pp2[1]);
-      dk8[j >> 1] = pack2(ds[0], ds[1]);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        float pp2[2], ds[2];
+#pragma unroll
+        for (int w2 = 0; w2 < 2; ++w2) {
+          float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -ls[j + w2]);
+          if (BIASMODE) x += bb[j + w2];
+          const float e = ex2(x);
+          pp2[w2] = (kv && qb + j + w2 < L) ? e : 0.f;
+          ds[w2] = pp2[w2] * (__uint_as_float(dv[j + w2]) - dq[j + w2]);
+        }
+        pk[j >> 1] = pack2(pp2[0], pp2[1]);
+        dk8[j >> 1] = pack2(ds[0], ds[1]);
+      }
     }
     tmem_st8(rb + c0, pk);
     tmem_st8(rb + 64 + c0, dk8);
@@ -1773,18 +1789,32 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       if (BIASMODE) bias_row8<true>(sBias, t, kb, bb);  // row boxes in both modes
       const bool full = qv && kb + 8 <= L;
       uint32_t pk[4];
+      if (full) {  // interior units: no per-element mask
 #pragma unroll
-      for (int j = 0; j < 8; j += 2) {
-        float ds[2];
+        for (int j = 0; j < 8; j += 2) {
+          float ds[2];
 #pragma unroll
-        for (int w2 = 0; w2 < 2; ++w2) {
-          float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
-          if (BIASMODE) x += bb[j + w2];
-          const float e = ex2(x);
-          const float p = full ? e : ((qv && kb + j + w2 < L) ? e : 0.f);
-          ds[w2] = p * (__uint_as_float(dv[j + w2]) - Dq);
+          for (int w2 = 0; w2 < 2; ++w2) {
+            float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
+            if (BIASMODE) x += bb[j + w2];
+            ds[w2] = ex2(x) * (__uint_as_float(dv[j + w2]) - Dq);
+          }
+          pk[j >> 1] = pack2(ds[0], ds[1]);
         }
-        pk[j >> 1] = pack2(ds[0], ds[1]);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 8; j += 2) {
+          float ds[2];
+#pragma unroll
+          for (int w2 = 0; w2 < 2; ++w2) {
+            float x = fmaf(__uint_as_float(sv[j + w2]), sc_l2, -lse_l2);
+            if (BIASMODE) x += bb[j + w2];
+            const float e = ex2(x);
+            const float p = (qv && kb + j + w2 < L) ? e : 0.f;
+            ds[w2] = p * (__uint_as_float(dv[j + w2]) - Dq);
+          }
+          pk[j >> 1] = pack2(ds[0], ds[1]);
+        }
       }
       // the four warps of this lane quadrant have loaded the region's S
       // columns before any of them overwrites them with packed dS
