@@ -852,13 +852,37 @@ ln_bwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ dy, int64_t d
   for (int c = 0; c < C; ++c)
     if (ok && c < cols)
       dx[(int64_t)c * rows + row] = from_f<TDX>(rs * (dv[c] * gamma[c] - m1 - xh[c] * m2));
+  if constexpr (C == 32) {
+    // transposing butterfly: after it lane c holds the warp's sum of column
+    // c (31 shuffles per quantity instead of 32 x 5)
+    float vg[32], vb[32];
 #pragma unroll
-  for (int c = 0; c < C; ++c) {
-    const float pg = warp_sum(dv[c] * xh[c]);
-    const float pb = warp_sum(dv[c]);
-    if (lane == 0) {
-      wred[warp][c] = pg;
-      wred[warp][C + c] = pb;
+    for (int c = 0; c < 32; ++c) {
+      vg[c] = dv[c] * xh[c];
+      vb[c] = dv[c];
+    }
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) {
+      const bool up = lane & o;
+#pragma unroll
+      for (int k = 0; k < o; ++k) {
+        const float sg = up ? vg[k] : vg[k + o], kg = up ? vg[k + o] : vg[k];
+        const float sb = up ? vb[k] : vb[k + o], kb = up ? vb[k + o] : vb[k];
+        vg[k] = kg + __shfl_xor_sync(0xffffffffu, sg, o);
+        vb[k] = kb + __shfl_xor_sync(0xffffffffu, sb, o);
+      }
+    }
+    wred[warp][lane] = vg[0];
+    wred[warp][C + lane] = vb[0];
+  } else {
+#pragma unroll
+    for (int c = 0; c < C; ++c) {
+      const float pg = warp_sum(dv[c] * xh[c]);
+      const float pb = warp_sum(dv[c]);
+      if (lane == 0) {
+        wred[warp][c] = pg;
+        wred[warp][C + c] = pb;
+      }
     }
   }
   __syncthreads();
