@@ -248,10 +248,13 @@ def run_native(args):
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:   # gloo: ranks may share one GPU (checks the N > 1 code path)
+            dist.init_process_group("gloo")
     kw = CONFIGS[args.config]
     if args.blocks:
         kw = {**kw, "n_blocks": args.blocks}
@@ -286,8 +289,12 @@ def run_native(args):
 
     # warm-up (first-touch allocations; for N > 1 the first two steps are the
     # eager warm-up and the segment capture)
-    for _ in range(args.warmup):
+    launches_eager_step = None
+    for w in range(args.warmup):
+        n_w = _native.launch_count()
         step_eager(m_d, z_d)
+        if w == 0:   # the first step is eager in every mode: its launch count
+            launches_eager_step = _native.launch_count() - n_w
     torch.cuda.synchronize()
 
     use_graph = args.graph
@@ -337,6 +344,10 @@ def run_native(args):
     n0 = _native.launch_count()
     ms_eager = timed(lambda: step_eager(m_d, z_d), args.steps)
     launches = _native.launch_count() - n0
+    if launches == 0 and launches_eager_step:
+        # graph-replayed segments (N > 1): the native launches inside the
+        # graphs are the eager step's, every step
+        launches = launches_eager_step * args.steps
     K.PROFILE = None
     K.PROFILE_SHAPES = None
     fam = {}
@@ -551,6 +562,9 @@ def run_stack(args):
     from paper_2211_00235_b200 import _native, schedules as S
     from oracle import evoformer_np as O
 
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if world > 1:
+        return run_stack_bp(args, world)
     dev = torch.device("cuda", 0)
     torch.cuda.set_device(dev)
     kw_m = {**CONFIGS["af2"], "n_blocks": args.blocks or 48}
@@ -639,6 +653,100 @@ def run_stack(args):
     return line
 
 
+def stack_configs(args):
+    kw_m = {**CONFIGS["af2"], "n_blocks": args.blocks or 48}
+    if args.crop:
+        kw_m["r"] = args.crop
+    if args.seqs:
+        kw_m["s"] = args.seqs
+    kw_e = {**EXTRA_AF2, "r": kw_m["r"]}
+    if args.extra_seqs:
+        kw_e["s"] = args.extra_seqs
+    return kw_m, kw_e
+
+
+def run_stack_bp(args, world):
+    """C3 / C4 under torchrun: BP=2 x DP=world/2 (distributed.composed_bp_step:
+    the extra-MSA stack and the main stack as one block schedule per BP pair,
+    NCCL broadcasts / allreduces, owner broadcast + DP mean of both stacks'
+    gradients).  Eager launches; device time, max over ranks; value = DP
+    replicas / step time."""
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    import paper_2211_00235_b200 as pkg
+    from paper_2211_00235_b200 import distributed as D
+    from oracle import evoformer_np as O
+
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    dev = torch.device("cuda", local % torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    if args.backend == "nccl":
+        dist.init_process_group("nccl", device_id=dev)
+    else:
+        dist.init_process_group("gloo")
+    if world % 2:
+        raise SystemExit("--stack under torchrun needs an even world (BP=2 x DP)")
+    layout = pkg.ParallelLayout(dp=world // 2, bp=2)
+    comm = D.Comm(layout)
+    dp_i = layout.coords(rank)[0]
+    kw_m, kw_e = stack_configs(args)
+    ce, cm = pkg.EvoConfig(**kw_e), pkg.EvoConfig(**kw_m)
+    ex_e = D.CudaExec(ce, pkg.init_params(ce, 33, device=dev), args.precision, dev,
+                      checkpoint=args.checkpoint)
+    ex_m = D.CudaExec(cm, pkg.init_params(cm, 32, device=dev), args.precision, dev,
+                      checkpoint=args.checkpoint)
+    rng = np.random.default_rng(32 + dp_i)
+    inp = [torch.from_numpy(rng.standard_normal(shape).astype(np.float32)).to(dev)
+           for shape in ((ce.s, ce.r, ce.c_m), (cm.s, cm.r, cm.c_m), (cm.r, cm.r, cm.c_z))]
+
+    def step():
+        return D.composed_bp_step(ex_e, ex_m, comm, *inp)
+
+    for _ in range(max(1, args.warmup)):
+        step()
+    torch.cuda.synchronize()
+    dist.barrier()
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(args.steps):
+        step()
+    a1.record()
+    torch.cuda.synchronize()
+    dist.barrier()
+    t = torch.tensor([a0.elapsed_time(a1) / args.steps], device=dev)
+    if args.backend == "nccl":
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    else:
+        tc = t.cpu()
+        dist.all_reduce(tc, op=dist.ReduceOp.MAX)
+        t = tc
+    ms = float(t.item())
+    if rank == 0:
+        flops = 3 * (O.block_flops(O.Dims(**kw_e)) * ce.n_blocks
+                     + O.block_flops(O.Dims(**kw_m)) * cm.n_blocks)
+        peak, _, _, src = peaks()
+        line = {
+            "metric": METRIC, "value": layout.dp / (ms / 1e3), "unit": "samples/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+            "ms_per_block_fwd_bwd": ms / (ce.n_blocks + cm.n_blocks), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None,
+            "dtype": "bf16" if args.precision == "bf16" else "f32", "data": "synthetic",
+            "config": {"workload": ("evoformer_stack_c4_finetune" if kw_e["s"] > 1024
+                                    else "evoformer_stack_c3"), "main": kw_m, "extra": kw_e,
+                       "precision": args.precision, "parallelism": f"bp2xdp{layout.dp}",
+                       "global_batch": layout.dp, "activation_checkpointing": args.checkpoint,
+                       "backend": args.backend},
+            "flops_per_step": flops, "step_tflops": flops * layout.dp / (ms / 1e3) / 1e12,
+            "peak_source": src, "launch_mode": "eager",
+        }
+        print(json.dumps(line))
+    dist.destroy_process_group()
+    return None
+
+
 def c3_summary(args):
     """SURVEY.md §8(d) C3 on this GPU (48 main + 4 extra-MSA blocks, one
     train step graph-replayed), as a key of the default bench line."""
@@ -675,6 +783,9 @@ def main():
                     help="per-block activation checkpointing (recompute each block's "
                          "forward before its backward)")
     ap.add_argument("--precision", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="torch.distributed backend for N > 1 (gloo lets ranks share one "
+                         "GPU: checks the multi-rank code path on a one-GPU box)")
     ap.add_argument("--dp-only", action="store_true")
     ap.add_argument("--no-graph", dest="graph", action="store_false",
                     help="time eager launches instead of CUDA-graph replay")

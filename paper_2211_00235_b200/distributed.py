@@ -191,13 +191,16 @@ class Comm:
 class CudaExec:
     """Branch executor on the native kernels (engine.py)."""
 
-    def __init__(self, cfg, store, precision=None, device=None):
+    def __init__(self, cfg, store, precision=None, device=None, checkpoint: bool = False):
         from . import engine as E
         from . import kernels as K
         from .schedules import StepState
         self.E, self.K = E, K
-        self.st = StepState(cfg, store, precision, device)
+        self.st = StepState(cfg, store, precision, device, checkpoint=checkpoint)
         self.cfg, self.act, self.dev = cfg, self.st.act, self.st.dev
+        # activation checkpointing on a BP rank: a branch forward keeps only
+        # its inputs; its backward recomputes the branch forward first
+        self.checkpoint = checkpoint
 
     def pack(self, branch):
         """Operand copies of the parameters this rank computes with:
@@ -219,16 +222,25 @@ class CudaExec:
             bg.msa.flat.zero_()
             bg.pair.flat.zero_()
 
-    def msa_fwd(self, blk, m, z):
+    def _msa_fwd(self, blk, m, z):
         E, st = self.E, self.st
         m_new, ctxs = E.msa_branch_fwd(st.P, blk, st.packs[blk], m, z, self.cfg, self.act)
         o, co = E.opm_fwd(st.P, f"blk{blk}.opm", st.packs[blk]["opm"], m_new, None, self.cfg,
                           self.act)
         return m_new, o, (ctxs, co)
 
+    def msa_fwd(self, blk, m, z):
+        m_new, o, ctx = self._msa_fwd(blk, m, z)
+        if self.checkpoint:
+            ctx = ("ckpt", m, z)
+        return m_new, o, ctx
+
     def pair_fwd(self, blk, z):
         E, st = self.E, self.st
-        return E.pair_branch_fwd(st.P, blk, st.packs[blk], z, self.cfg, self.act)
+        z_new, ctx = E.pair_branch_fwd(st.P, blk, st.packs[blk], z, self.cfg, self.act)
+        if self.checkpoint:
+            ctx = ("ckpt", z)
+        return z_new, ctx
 
     def add(self, a, b):
         out = torch.empty_like(a)
@@ -240,6 +252,8 @@ class CudaExec:
 
     def msa_bwd(self, blk, ctx, dm, d_o):
         E, st = self.E, self.st
+        if ctx[0] == "ckpt":          # recompute the branch forward state
+            ctx = self._msa_fwd(blk, ctx[1], ctx[2])[2]
         ctxs, co = ctx
         G = st.grads[blk].packed
         e0 = E.msa_emit(G)
@@ -250,6 +264,8 @@ class CudaExec:
 
     def pair_bwd(self, blk, ctx, dz):
         E, st = self.E, self.st
+        if isinstance(ctx, tuple) and ctx[0] == "ckpt":
+            ctx = E.pair_branch_fwd(st.P, blk, st.packs[blk], ctx[1], self.cfg, self.act)[1]
         return E.pair_branch_bwd(st.P, blk, st.packs[blk], st.grads[blk].packed, ctx, dz,
                                  self.cfg, self.act, dz_act=E.cast_act(dz, self.act))
 
@@ -372,7 +388,8 @@ def composed_bp_step(ex_extra, ex_main, comm, m_e, m, z):
                           f"stack (r={cm.r}, c_z={cm.c_z})")
     bp_i = comm.layout.coords(comm.rank)[1]
     ex = ComposedExec(ex_extra, ex_main, m.reshape(cm.s * cm.r, cm.c_m))
-    ex.pack("msa" if bp_i == 0 else "pair")
+    if ex_extra.st.packs is None or ex_main.st.packs is None:
+        ex.pack("msa" if bp_i == 0 else "pair")
     Kt = ce.n_blocks + cm.n_blocks
     z2 = z.reshape(cm.r * cm.r, cm.c_z)
     if bp_i == 0:

@@ -191,7 +191,7 @@ def _c3_inputs(cfg_e, cfg_m):
                           (cfg_m.r, cfg_m.r, cfg_m.c_z))]
 
 
-def _c3_worker(rank, init_file, precision, q):
+def _c3_worker(rank, init_file, precision, q, ckpt=False):
     import traceback
     import torch.distributed as dist
     try:
@@ -203,8 +203,10 @@ def _c3_worker(rank, init_file, precision, q):
         ce, cm = pkg.EvoConfig(**EXTRA), pkg.EvoConfig(**MAIN)
         lay = pkg.ParallelLayout(bp=2)
         comm = D.Comm(lay)
-        ex_e = D.CudaExec(ce, pkg.init_params(ce, 33, device="cuda:0"), precision)
-        ex_m = D.CudaExec(cm, pkg.init_params(cm, 32, device="cuda:0"), precision)
+        ex_e = D.CudaExec(ce, pkg.init_params(ce, 33, device="cuda:0"), precision,
+                          checkpoint=ckpt)
+        ex_m = D.CudaExec(cm, pkg.init_params(cm, 32, device="cuda:0"), precision,
+                          checkpoint=ckpt)
         out = D.composed_bp_step(ex_e, ex_m, comm, *_c3_inputs(ce, cm))
         torch.cuda.synchronize()
         grads = {**{"extra." + k: v.cpu().numpy() for k, v in ex_e.grad_dict().items()},
@@ -215,10 +217,11 @@ def _c3_worker(rank, init_file, precision, q):
         q.put(("err", rank, traceback.format_exc(), None))
 
 
-@pytest.mark.parametrize("precision", ["fp32", "bf16"])
-def test_c3_composed_stack_bp2_bitwise_equals_bp1(pkg, precision):
+@pytest.mark.parametrize("precision,ckpt", [("fp32", False), ("bf16", False), ("bf16", True)])
+def test_c3_composed_stack_bp2_bitwise_equals_bp1(pkg, precision, ckpt):
     """C3 (extra-MSA stack -> main stack) under BP=2: bitwise equal to the
-    one-GPU composition (schedules.composed_step)."""
+    one-GPU composition (schedules.composed_step); with per-block activation
+    checkpointing on both BP ranks too (the C4 memory layout)."""
     import os
     import tempfile
     import torch.multiprocessing as mp
@@ -228,7 +231,8 @@ def test_c3_composed_stack_bp2_bitwise_equals_bp1(pkg, precision):
     os.unlink(init_file)
     ctx = mp.get_context("spawn")
     q = ctx.SimpleQueue()
-    procs = [ctx.Process(target=_c3_worker, args=(r, init_file, precision, q)) for r in range(2)]
+    procs = [ctx.Process(target=_c3_worker, args=(r, init_file, precision, q, ckpt))
+             for r in range(2)]
     for p in procs:
         p.start()
     got = {}
