@@ -103,8 +103,13 @@ __device__ __forceinline__ float2 upk2(uint32_t u) {
 }
 template <int N>
 __device__ __forceinline__ void tld(uint32_t taddr, uint32_t (&v)[N]) {
-  static_assert(N == 4 || N == 8 || N == 16 || N == 32, "tmem load width");
-  if constexpr (N == 32) {
+  static_assert(N == 4 || N == 8 || N == 16 || N == 32 || N == 64, "tmem load width");
+  if constexpr (N == 64) {
+    uint32_t (&lo)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[0]);
+    uint32_t (&hi)[32] = *reinterpret_cast<uint32_t(*)[32]>(&v[32]);
+    tmem_ld32_nw(taddr, lo);
+    tmem_ld32_nw(taddr + 32, hi);
+  } else if constexpr (N == 32) {
     tmem_ld32_nw(taddr, v);
   } else if constexpr (N == 16) {
     tmem_ld16_nw(taddr, v);
@@ -121,8 +126,10 @@ __device__ __forceinline__ void tld(uint32_t taddr, uint32_t (&v)[N]) {
 }
 template <int N>
 __device__ __forceinline__ void tst(uint32_t taddr, const uint32_t (&v)[N]) {
-  static_assert(N == 4 || N == 8 || N == 16, "tmem store width");
-  if constexpr (N == 16) {
+  static_assert(N == 4 || N == 8 || N == 16 || N == 32, "tmem store width");
+  if constexpr (N == 32) {
+    tmem_st32(taddr, v);
+  } else if constexpr (N == 16) {
     tmem_st16(taddr, v);
   } else if constexpr (N == 8) {
     asm volatile(
@@ -140,11 +147,11 @@ __device__ __forceinline__ void tst(uint32_t taddr, const uint32_t (&v)[N]) {
 // 0), from the stage's two [128 rows x 32] fp32 SW128 boxes
 template <int EPT>
 __device__ __forceinline__ void bias_row(const uint8_t *tile, int row, int k0, float (&out)[EPT]) {
-  const uint8_t *base = tile + (k0 >> 5) * 16384 + row * 128;
-  const int c0 = (k0 & 31) >> 2;
 #pragma unroll
   for (int c = 0; c < EPT / 4; ++c) {
-    const float4 v = *reinterpret_cast<const float4 *>(base + (((c0 + c) ^ (row & 7)) << 4));
+    const int kk = k0 + 4 * c;   // box kk / 32, 16-byte chunk (kk % 32) / 4
+    const uint8_t *base = tile + (kk >> 5) * 16384 + row * 128;
+    const float4 v = *reinterpret_cast<const float4 *>(base + ((((kk & 31) >> 2) ^ (row & 7)) << 4));
     out[4 * c] = v.x; out[4 * c + 1] = v.y; out[4 * c + 2] = v.z; out[4 * c + 3] = v.w;
   }
 }
@@ -334,7 +341,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       }
       float *sx = sX + bi * (TPR * 128);
       sx[part * 128 + t] = mt;
-      named_bar_sync(1 + quad, 32 * TPR);       // the row's TPR parts
+      if (TPR > 1) named_bar_sync(1 + quad, 32 * TPR);   // the row's TPR parts
 #pragma unroll
       for (int p2 = 0; p2 < TPR; ++p2) mt = fmaxf(mt, sx[p2 * 128 + t]);
       const bool grow = mt > m_run + 8.f;
@@ -381,11 +388,11 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
         __syncwarp();
         if (lane == 0) mbar_arrive(&ord[r & 1]);
         sL[part * 128 + t] = l;
-        named_bar_sync(1 + quad, 32 * TPR);
+        if (TPR > 1) named_bar_sync(1 + quad, 32 * TPR);
         float lt = 0.f;
 #pragma unroll
         for (int p2 = 0; p2 < TPR; ++p2) lt += sL[p2 * 128 + t];
-        if (qv) {
+        if (qv && part * OD < D) {
           const float inv = 1.f / lt;
           const int64_t ooff = b * a.o_sb + (int64_t)q * a.o_sl + h * D + part * OD;
           const bf16 *gp = a.g + b * a.sb + (int64_t)q * a.sl + h * D + part * OD;
@@ -703,8 +710,8 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&dqr[r & 1]);
-        if (qv) store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v,
-                                   a.scale);
+        if (qv && part * OD < D)
+          store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v, a.scale);
       }
       if (++j == T) {
         j = 0;
@@ -923,20 +930,36 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       tmem_wait_ld();
       uint32_t pp[EPT / 2], pd[EPT / 2];
       const bool full = kv && qb + EPT <= L;
+      if (full) {  // interior tiles: no per-element mask
 #pragma unroll
-      for (int c = 0; c < EPT; c += 2) {
-        float p[2], ds[2];
+        for (int c = 0; c < EPT; c += 2) {
+          float p[2], ds[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-          const int qq = c + e;
-          float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
-          if (BIAS) x += bq[qq];
-          p[e] = ex2f(x);
-          if (!full && !(kv && qb + qq < L)) p[e] = 0.f;
-          ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
+          for (int e = 0; e < 2; ++e) {
+            const int qq = c + e;
+            float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
+            if (BIAS) x += bq[qq];
+            p[e] = ex2f(x);
+            ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
+          }
+          pp[c >> 1] = pk2(p[0], p[1]);
+          pd[c >> 1] = pk2(ds[0], ds[1]);
         }
-        pp[c >> 1] = pk2(p[0], p[1]);
-        pd[c >> 1] = pk2(ds[0], ds[1]);
+      } else {
+#pragma unroll
+        for (int c = 0; c < EPT; c += 2) {
+          float p[2], ds[2];
+#pragma unroll
+          for (int e = 0; e < 2; ++e) {
+            const int qq = c + e;
+            float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
+            if (BIAS) x += bq[qq];
+            p[e] = (kv && qb + qq < L) ? ex2f(x) : 0.f;
+            ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
+          }
+          pp[c >> 1] = pk2(p[0], p[1]);
+          pd[c >> 1] = pk2(ds[0], ds[1]);
+        }
       }
       tst<EPT / 2>(lane_addr + bi * 192 + 128 + part * (EPT / 2), pp);
       tst<EPT / 2>(lane_addr + bi * 192 + 160 + part * (EPT / 2), pd);
