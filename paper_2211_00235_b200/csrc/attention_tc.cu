@@ -156,6 +156,12 @@ static const bool g_attn_no_pipe = [] {
   const char *e = getenv("EVO_ATTN_NO_PIPE");
   return e && e[0] == '1';
 }();
+// elementwise warps of the pipelined dq kernel (EVO_DQ_EWW=16: the previous
+// 8-keys-per-thread layout; default 8 warps, 16 keys per thread per unit)
+static const int g_dq_eww = [] {
+  const char *e = getenv("EVO_DQ_EWW");
+  return e && atoi(e) == 16 ? 16 : 8;
+}();
 
 template <bool TBIAS>
 __device__ __forceinline__ float bias_smem(const uint8_t *sb, int row, int k) {
@@ -508,20 +514,22 @@ __device__ __forceinline__ void scale_tile(uint8_t *sb, int nfloat4, int nthread
 // a thread's consecutive bias values as 16-byte vectors instead of one
 // strided scalar per element (once per CTA; the tile serves every batch row).
 // All 512 elementwise threads call it (named barrier 1).
+template <int NT = 512>
 __device__ __forceinline__ void transpose_scale_bias_boxes(uint8_t *sb, int nbox, int tid) {
+  constexpr int PER = 4096 / NT;
   for (int j = 0; j < nbox; ++j) {
     float *box = reinterpret_cast<float *>(sb + j * 16384);
-    float v[8];
+    float v[PER];
 #pragma unroll
-    for (int i = 0; i < 8; ++i) v[i] = box[tid + 512 * i] * LOG2E;
-    named_bar_sync(1, 512);
+    for (int i = 0; i < PER; ++i) v[i] = box[tid + NT * i] * LOG2E;
+    named_bar_sync(1, NT);
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      const int e = tid + 512 * i, o = e >> 7, in = e & 127;
+    for (int i = 0; i < PER; ++i) {
+      const int e = tid + NT * i, o = e >> 7, in = e & 127;
       *reinterpret_cast<float *>(sb + j * 16384 + in * 128 + ((((o >> 2) ^ (in & 7))) << 4) +
                                  (o & 3) * 4) = v[i];
     }
-    named_bar_sync(1, 512);
+    named_bar_sync(1, NT);
   }
 }
 
@@ -1559,14 +1567,17 @@ __device__ __forceinline__ void bias_row8(const uint8_t *sb, int row, int k0, fl
   }
 }
 
-template <int D, int BIASMODE, int NU>
-__global__ void __launch_bounds__(576, 1)
+template <int D, int BIASMODE, int NU, int EWW>
+__global__ void __launch_bounds__(32 * EWW + 64, 1)
 attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
                         const __grid_constant__ CUtensorMap mK,
                         const __grid_constant__ CUtensorMap mV,
                         const __grid_constant__ CUtensorMap mdO,
                         const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
   constexpr int UW = 32, LPC = NU * UW;           // Lp = 32 NU (128 or 256)
+  constexpr int QW = EWW / 4;                     // elementwise warps per lane quadrant
+  constexpr int KPT = UW / QW;                    // keys per thread per unit
+  constexpr int NEW = 32 * EWW;                   // elementwise threads
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = LPC * Sw<D>::bytes;
   constexpr uint32_t ROWB = 2 * TILE + 2 * FULL;  // Q | dO | K | V of one batch row
@@ -1590,7 +1601,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row in the tile
-  const int qr = warp >> 2;              // 8-key quarter of each unit
+  const int qr = warp >> 2;              // KPT-key slice of each unit
   const int q0 = blockIdx.x * QT, h = blockIdx.y;
   const int L = a.L;
   const int q = q0 + t;
@@ -1600,11 +1611,11 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   const int64_t nrows = b_hi - b_lo;
   const int64_t U = nrows > 0 ? nrows * NU : 0;
 
-  if (tid == 512) {
+  if (tid == NEW) {
     for (int i = 0; i < 16; ++i) {
       const bool ewd = &bars_all[i] == ewdone(0) || &bars_all[i] == ewdone(1) ||
                        &bars_all[i] == ewdone(2);
-      mbar_init(&bars_all[i], ewd ? 16 : 1);
+      mbar_init(&bars_all[i], ewd ? EWW : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars_all[0], h, q0, LPC);
@@ -1632,7 +1643,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
   const uint32_t lane_addr = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   auto rowbuf = [&](int64_t r) -> uint8_t * { return sRow + ((r - b_lo) % NBUF) * ROWB; };
 
-  if (warp >= 16) {
+  if (warp >= EWW) {
     // ------------------------------------------------------------ issuers
     const uint32_t idesc_s = idesc_bf16(128, UW, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
@@ -1646,7 +1657,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       tma_load_4d(rb + 2 * TILE, &mK, bar, 0, 0, (int)r, h);
       tma_load_4d(rb + 2 * TILE + FULL, &mV, bar, 0, 0, (int)r, h);
     };
-    if (warp == 16 && nrows > 0) {
+    if (warp == EWW && nrows > 0) {
       // S/dP MMAs: unit v into region v%3 once unit v-3's dQ/dbias MMAs
       // (the region's previous readers) completed
       if (lane == 0)
@@ -1677,8 +1688,8 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
         umma_commit_el(&bars[3 + reg]);
         reg = reg == 2 ? 0 : reg + 1;
       }
-    } else if (warp == 17 && nrows > 0) {
-      // dQ / dbias MMAs of unit u once all 16 warps packed its dS
+    } else if (warp == EWW + 1 && nrows > 0) {
+      // dQ / dbias MMAs of unit u once all EWW warps packed its dS
       const uint32_t sIa = smem_u32(sI);
       int reg = 0;
       for (int u = 0; u < (int)U; ++u) {
@@ -1718,11 +1729,13 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       const int pp = (int)((rr - b_lo) & 1);
       mbar_wait(&bars[6 + pp], (uint32_t)(((rr - b_lo) >> 1) & 1));
       fence_after();
-      constexpr int QD = D / 4;
+      constexpr int QD = D / QW;
       const uint32_t acc = lane_addr + 192 + pp * 32;
-      uint32_t v[8];
-      if constexpr (QD == 8) {
-        tmem_ld8_nw(acc + qr * 8, v);
+      uint32_t v[16];
+      if constexpr (QD == 16) {
+        tmem_ld16_nw(acc + qr * 16, v);
+      } else if constexpr (QD == 8) {
+        tmem_ld8_nw(acc + qr * 8, *reinterpret_cast<uint32_t(*)[8]>(v));
       } else {
         asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
                      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3])
@@ -1731,7 +1744,15 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       tmem_wait_ld();
       if (qv) {
         bf16 *dst = a.dq + rr * a.sb + (int64_t)q * a.sl + h * D + qr * QD;
-        if constexpr (QD == 8) {
+        if constexpr (QD == 16) {
+          uint32_t w8[8];
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            w8[j] = pack2(__uint_as_float(v[2 * j]) * a.scale,
+                          __uint_as_float(v[2 * j + 1]) * a.scale);
+          *reinterpret_cast<uint4 *>(dst) = make_uint4(w8[0], w8[1], w8[2], w8[3]);
+          *reinterpret_cast<uint4 *>(dst + 8) = make_uint4(w8[4], w8[5], w8[6], w8[7]);
+        } else if constexpr (QD == 8) {
           uint32_t w4[4];
 #pragma unroll
           for (int j = 0; j < 4; ++j)
@@ -1750,9 +1771,9 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
     };
     if (BIASMODE) {
       mbar_wait(&bars_all[0], 0);
-      if constexpr (TB) transpose_scale_bias_boxes(sBias, LPC / 32, tid);
-      else scale_tile(sBias, (LPC / 32) * 16384 / 16, 512);
-      named_bar_sync(1, 512);
+      if constexpr (TB) transpose_scale_bias_boxes<NEW>(sBias, LPC / 32, tid);
+      else scale_tile(sBias, (LPC / 32) * 16384 / 16, NEW);
+      named_bar_sync(1, NEW);
     }
     const float sc_l2 = a.scale * LOG2E;
     float lse_n = 0.f, Dq_n = 0.f;
@@ -1779,19 +1800,26 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
       ph3 ^= 1u << reg;
       fence_after();
       const uint32_t rb = lane_addr + reg * 64;
-      const int c0 = qr * 8;
-      const int kb = ui * UW + c0;  // first key of this thread's 8
-      uint32_t sv[8], dv[8];
-      tmem_ld8_nw(rb + c0, sv);
-      tmem_ld8_nw(rb + 32 + c0, dv);
-      tmem_wait_ld();
-      float bb[8];
-      if (BIASMODE) bias_row8<true>(sBias, t, kb, bb);  // row boxes in both modes
-      const bool full = qv && kb + 8 <= L;
-      uint32_t pk[4];
+      const int c0 = qr * KPT;
+      const int kb = ui * UW + c0;  // first key of this thread's KPT
+      uint32_t sv[KPT], dv[KPT];
+      float bb[KPT];
+      if constexpr (KPT == 16) {
+        tmem_ld16_nw(rb + c0, sv);
+        tmem_ld16_nw(rb + 32 + c0, dv);
+        tmem_wait_ld();
+        if (BIASMODE) bias_row16<true>(sBias, t, kb, bb);  // row boxes in both modes
+      } else {
+        tmem_ld8_nw(rb + c0, sv);
+        tmem_ld8_nw(rb + 32 + c0, dv);
+        tmem_wait_ld();
+        if (BIASMODE) bias_row8<true>(sBias, t, kb, bb);
+      }
+      const bool full = qv && kb + KPT <= L;
+      uint32_t pk[KPT / 2];
       if (full) {  // interior units: no per-element mask
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
+        for (int j = 0; j < KPT; j += 2) {
           float ds[2];
 #pragma unroll
           for (int w2 = 0; w2 < 2; ++w2) {
@@ -1803,7 +1831,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
         }
       } else {
 #pragma unroll
-        for (int j = 0; j < 8; j += 2) {
+        for (int j = 0; j < KPT; j += 2) {
           float ds[2];
 #pragma unroll
           for (int w2 = 0; w2 < 2; ++w2) {
@@ -1816,13 +1844,17 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
           pk[j >> 1] = pack2(ds[0], ds[1]);
         }
       }
-      // the four warps of this lane quadrant have loaded the region's S
+      // the QW warps of this lane quadrant have loaded the region's S
       // columns before any of them overwrites them with packed dS
-      named_bar_sync(2 + (warp & 3), 128);
-      asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
-                       rb + qr * 4),
-                   "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
-                   : "memory");
+      named_bar_sync(2 + (warp & 3), 32 * QW);
+      if constexpr (KPT == 16) {
+        tmem_st8(rb + qr * 8, pk);
+      } else {
+        asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1, %2, %3, %4};" ::"r"(
+                         rb + qr * 4),
+                     "r"(pk[0]), "r"(pk[1]), "r"(pk[2]), "r"(pk[3])
+                     : "memory");
+      }
       if (ui == 0 && r > b_lo) readout(r - 1);
       tmem_st_wait();
       fence_before();
@@ -1839,8 +1871,8 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
         float *dst = a.dbias_part + (int64_t)blockIdx.z * a.H * a.bh +
                      (int64_t)h * a.bh + (int64_t)q * a.bq;
 #pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          const int kb = qr * 64 + 32 * c;
+        for (int c = 0; c < 8 / QW; ++c) {
+          const int kb = qr * (256 / QW) + 32 * c;
           uint32_t v[32];
           tmem_ld32(lane_addr + 256 + kb, v);
           if (qv) {
@@ -2093,12 +2125,22 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         nbuf * (2 * (size_t)QT * 2 * D + 2 * (size_t)Lp * 2 * D) + 2048 + 16 * 8 +
                         16;
     dim3 grid(tiles, d->H, (unsigned)nch);
-    if (Lp == 256) {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8>));
-      attn_bwd_dq_pipe_kernel<D, BM_, 8><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    if (g_dq_eww == 16) {
+      if (Lp == 256) {
+        EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8, 16>));
+        attn_bwd_dq_pipe_kernel<D, BM_, 8, 16><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+      } else {
+        EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4, 16>));
+        attn_bwd_dq_pipe_kernel<D, BM_, 4, 16><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+      }
     } else {
-      EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4>));
-      attn_bwd_dq_pipe_kernel<D, BM_, 4><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+      if (Lp == 256) {
+        EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8, 8>));
+        attn_bwd_dq_pipe_kernel<D, BM_, 8, 8><<<grid, 320, smem, st>>>(mq, mk, mv, mdo, mb, a);
+      } else {
+        EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4, 8>));
+        attn_bwd_dq_pipe_kernel<D, BM_, 4, 8><<<grid, 320, smem, st>>>(mq, mk, mv, mdo, mb, a);
+      }
     }
     EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
   } else {
