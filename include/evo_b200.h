@@ -251,6 +251,18 @@ EVO_API int evo_copy2d(int dtype_src, int dtype_dst, int64_t rows, int64_t cols,
                const void *src, int64_t s_rs, int64_t s_cs, void *dst,
                int64_t d_rs, int64_t d_cs, void *stream);
 
+/* Batched 3-D strided copy with dtype conversion:
+ * dst[b*d_bs + r*d_rs + c*d_cs] = src[b*s_bs + r*s_rs + c*s_cs].  The axis
+ * permutations and shard placements of DAP (src/schedules.py:96-154:
+ * allgather along an axis, the column shards of col_attn / tri_attn_end). */
+EVO_API int evo_copy3d(int dtype_src, int dtype_dst, int64_t n0, int64_t rows, int64_t cols,
+               const void *src, int64_t s_bs, int64_t s_rs, int64_t s_cs, void *dst,
+               int64_t d_bs, int64_t d_rs, int64_t d_cs, void *stream);
+
+/* bytes zero bytes at ptr, stream-ordered (the zero-padded shard gradients
+ * DAP allreduces, src/schedules.py:122-128).                              */
+EVO_API int evo_zero(void *ptr, size_t bytes, void *stream);
+
 /* out(r,c) = a(r,c) * b(r,c); every operand 2-D strided, own dtype. */
 EVO_API int evo_mul2d(int dtype_a, int dtype_b, int dtype_out, int64_t rows,
               int64_t cols, const void *a, int64_t a_rs, const void *b,

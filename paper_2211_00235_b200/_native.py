@@ -84,6 +84,9 @@ _SIGS = {
     "evo_colsum_workspace_bytes": (c_sz, [c_i64]),
     "evo_copy2d": (c_i32, [c_i32, c_i32, c_i64, c_i64, c_vp, c_i64, c_i64, c_vp, c_i64, c_i64,
                            c_vp]),
+    "evo_copy3d": (c_i32, [c_i32, c_i32, c_i64, c_i64, c_i64, c_vp, c_i64, c_i64, c_i64, c_vp,
+                           c_i64, c_i64, c_i64, c_vp]),
+    "evo_zero": (c_i32, [c_vp, c_sz, c_vp]),
     "evo_mul2d": (c_i32, [c_i32, c_i32, c_i32, c_i64, c_i64, c_vp, c_i64, c_vp, c_i64, c_vp,
                           c_i64, c_vp]),
     "evo_trimul_gate_fwd": (c_i32, [c_i32, c_i64, c_i32, c_vp, c_i64, c_vp, c_vp, c_vp]),

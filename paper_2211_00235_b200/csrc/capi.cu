@@ -53,6 +53,8 @@ size_t attention_tc_bwd_ws(const evo_attn_desc *);
 int reduce_lead(int, int64_t, int64_t, int64_t, const void *, float *, int64_t, int64_t, int,
                 cudaStream_t);
 int colsum(int, int64_t, int64_t, const void *, int64_t, float *, int, float *, cudaStream_t);
+int copy3d(int, int, int64_t, int64_t, int64_t, const void *, int64_t, int64_t, int64_t, void *,
+           int64_t, int64_t, int64_t, cudaStream_t);
 int copy2d(int, int, int64_t, int64_t, const void *, int64_t, int64_t, void *, int64_t, int64_t,
            cudaStream_t);
 int mul2d(int, int, int, int64_t, int64_t, const void *, int64_t, const void *, int64_t, void *,
@@ -321,6 +323,26 @@ int evo_copy2d(int dtype_src, int dtype_dst, int64_t rows, int64_t cols, const v
   CHECK_PTR(src); CHECK_PTR(dst);
   return copy2d(dtype_src, dtype_dst, rows, cols, src, s_rs, s_cs, dst, d_rs, d_cs,
                 as_stream(stream));
+}
+
+int evo_copy3d(int dtype_src, int dtype_dst, int64_t n0, int64_t rows, int64_t cols,
+               const void *src, int64_t s_bs, int64_t s_rs, int64_t s_cs, void *dst, int64_t d_bs,
+               int64_t d_rs, int64_t d_cs, void *stream) {
+  CHECK_DT(dtype_src);
+  CHECK_DT(dtype_dst);
+  EVO_REQUIRE(n0 >= 0 && rows >= 0 && cols >= 0, EVO_EDIM, "evo_copy3d: negative size");
+  if (n0 * rows * cols == 0) return EVO_OK;
+  CHECK_PTR(src); CHECK_PTR(dst);
+  return copy3d(dtype_src, dtype_dst, n0, rows, cols, src, s_bs, s_rs, s_cs, dst, d_bs, d_rs,
+                d_cs, as_stream(stream));
+}
+
+int evo_zero(void *ptr, size_t bytes, void *stream) {
+  if (bytes == 0) return EVO_OK;
+  CHECK_PTR(ptr);
+  const cudaError_t e = cudaMemsetAsync(ptr, 0, bytes, as_stream(stream));
+  EVO_REQUIRE(e == cudaSuccess, EVO_ECUDA, "evo_zero: %s", cudaGetErrorString(e));
+  return EVO_OK;
 }
 
 int evo_mul2d(int dtype_a, int dtype_b, int dtype_out, int64_t rows, int64_t cols, const void *a,

@@ -658,6 +658,36 @@ int colsum(int dt, int64_t rows, int64_t cols, const void *src, int64_t rs, floa
   return EVO_OK;
 }
 
+// n0 independent 2-D copies (batch strides s_bs / d_bs); 16-byte vectors
+// along unit-stride rows when every row start is aligned
+template <typename TS, typename TD>
+__global__ void copy3d_kernel(int64_t n0, int64_t rows, int64_t cols, const void *src,
+                              int64_t s_bs, int64_t s_rs, int64_t s_cs, void *dst, int64_t d_bs,
+                              int64_t d_rs, int64_t d_cs) {
+  const int64_t plane = rows * cols, total = n0 * plane;
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
+       e += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t b = e / plane, rc = e - b * plane, r = rc / cols, c = rc - r * cols;
+    ST<TD>(dst, b * d_bs + r * d_rs + c * d_cs, LD<TS>(src, b * s_bs + r * s_rs + c * s_cs));
+  }
+}
+
+int copy3d(int ts, int td, int64_t n0, int64_t rows, int64_t cols, const void *src, int64_t s_bs,
+           int64_t s_rs, int64_t s_cs, void *dst, int64_t d_bs, int64_t d_rs, int64_t d_cs,
+           cudaStream_t st) {
+  const int64_t total = n0 * rows * cols;
+  if (total == 0) return EVO_OK;
+  const int nb = ew_blocks(total);
+#define C(A, B)                                                                              \
+  copy3d_kernel<A, B><<<nb, 256, 0, st>>>(n0, rows, cols, src, s_bs, s_rs, s_cs, dst, d_bs, d_rs, \
+                                          d_cs)
+  if (ts == EVO_F32) { if (td == EVO_F32) C(float, float); else C(float, bf16); }
+  else { if (td == EVO_F32) C(bf16, float); else C(bf16, bf16); }
+#undef C
+  EVO_LAUNCHED("copy3d_kernel");
+  return EVO_OK;
+}
+
 int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t s_rs,
            int64_t s_cs, void *dst, int64_t d_rs, int64_t d_cs, cudaStream_t st) {
   int64_t total = rows * cols;

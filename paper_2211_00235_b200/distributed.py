@@ -127,13 +127,20 @@ class Comm:
         self.groups = {}
         # every rank creates every group, in the same order
         for dp_i in range(layout.dp):
-            g = tuple(layout.rank_of(dp_i, b) for b in range(layout.bp))
-            self.groups[g] = dist.new_group(list(g)) if layout.bp > 1 else None
+            for k in range(layout.dap):
+                g = tuple(layout.rank_of(dp_i, b, k) for b in range(layout.bp))
+                self.groups[g] = dist.new_group(list(g)) if layout.bp > 1 else None
         for bp_i in range(layout.bp):
-            g = tuple(layout.rank_of(d, bp_i) for d in range(layout.dp))
-            self.groups[g] = dist.new_group(list(g)) if layout.dp > 1 else None
+            for k in range(layout.dap):
+                g = tuple(layout.rank_of(d, bp_i, k) for d in range(layout.dp))
+                self.groups[g] = dist.new_group(list(g)) if layout.dp > 1 else None
+        for dp_i in range(layout.dp):
+            for bp_i in range(layout.bp):
+                g = tuple(layout.rank_of(dp_i, bp_i, k) for k in range(layout.dap))
+                self.groups[g] = dist.new_group(list(g)) if layout.dap > 1 else None
         self.pair = layout.bp_group(self.rank)
         self.dpg = layout.dp_group(self.rank)
+        self.dapg = layout.dap_group(self.rank)
         self.trace: list[CommRecord] = []
 
     def _rec(self, kind, group, src, t, phase):
@@ -153,6 +160,15 @@ class Comm:
         dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.groups[tuple(group)])
         self._rec("allreduce_sum", group, None, t, phase)
         return t
+
+    def allgather(self, group, t, out, phase):
+        """out = the group's shards t concatenated along axis 0 in rank order
+        (src/comm.py:241-243; out has len(group) * t.shape[0] rows)."""
+        n = len(group)
+        parts = list(out.view(n, *t.shape).unbind(0))
+        dist.all_gather(parts, t.contiguous(), group=self.groups[tuple(group)])
+        self._rec("allgather", group, None, out, phase)
+        return out
 
     def world_trace(self) -> CommTrace:
         """Every rank's records of the groups it leads (lowest rank), merged
@@ -177,8 +193,7 @@ class Comm:
             mine[(r.phase, r.kind)] = (c0 + 1, e0 + r.elements)
         if not world_reduce:
             return mine
-        keys = [("fwd", "broadcast"), ("bwd", "broadcast"), ("bwd", "allreduce_sum"),
-                ("param", "broadcast"), ("param", "allreduce_sum")]
+        keys = [(p, k) for p in PHASES for k in ("broadcast", "allreduce_sum", "allgather")]
         vec = torch.tensor([[mine.get(k, (0, 0))[0], mine.get(k, (0, 0))[1]] for k in keys],
                            dtype=torch.float64)
         dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
@@ -278,6 +293,92 @@ class CudaExec:
         dx = torch.empty_like(x)
         self.K.sq_mean(x, loss, dx)
         return loss, dx
+
+
+class DapExec(CudaExec):
+    """Branch executor with every sub-op sharded over this rank's DAP group
+    (dap.py; src/schedules.py:96-154).  Same interface as CudaExec: the BP
+    schedules run on it unchanged, and full_step is the BP=1 step of any
+    block wiring (src/evoformer.py:446-458) with the shard hooks."""
+
+    def __init__(self, cfg, store, comm, precision=None, device=None):
+        super().__init__(cfg, store, precision, device)
+        from . import dap as D
+        self.D = D
+        self.sh = D.DapShard(comm, comm.dapg)
+
+    def msa_fwd(self, blk, m, z):
+        D, st = self.D, self.st
+        m_new, c = D.msa_track_fwd(st, self.sh, blk, m, z)
+        o, co = D.opm_fwd(st, self.sh, blk, m_new)
+        return m_new, o, (c, co)
+
+    def msa_bwd(self, blk, ctx, dm, d_o):
+        D, st = self.D, self.st
+        c, co = ctx
+        dm = self.add(dm, D.opm_bwd(st, self.sh, blk, co, d_o))
+        return D.msa_track_bwd(st, self.sh, blk, c, dm)
+
+    def pair_fwd(self, blk, z):
+        return self.D.pair_track_fwd(self.st, self.sh, blk, z)
+
+    def pair_bwd(self, blk, ctx, dz):
+        return self.D.pair_track_bwd(self.st, self.sh, blk, ctx, dz)
+
+    def replicated(self, blk, branch):
+        return self.D.replicated_slices(self.st, blk) if branch == "msa" else []
+
+    def full_step(self, m, z, ev=None):
+        D, st, sh, cfg = self.D, self.st, self.sh, self.cfg
+        if st.packs is None:
+            st.pack()
+        s, r = cfg.s, cfg.r
+        mc = m.reshape(s * r, cfg.c_m)
+        zc = z.reshape(r * r, cfg.c_z)
+        _mark(ev, 0)
+        ctxs = []
+        for blk in range(cfg.n_blocks):
+            if cfg.variant == "af2":
+                mc, cm = D.msa_track_fwd(st, sh, blk, mc, zc)
+                o, co = D.opm_fwd(st, sh, blk, mc)
+                zc, cp = D.pair_track_fwd(st, sh, blk, self.add(zc, o))
+            elif cfg.variant == "multimer":
+                o, co = D.opm_fwd(st, sh, blk, mc)
+                zc = self.add(zc, o)
+                mc, cm = D.msa_track_fwd(st, sh, blk, mc, zc)
+                zc, cp = D.pair_track_fwd(st, sh, blk, zc)
+            else:
+                m_new, cm = D.msa_track_fwd(st, sh, blk, mc, zc)
+                z_b, cp = D.pair_track_fwd(st, sh, blk, zc)
+                o, co = D.opm_fwd(st, sh, blk, m_new)
+                mc, zc = m_new, self.add(z_b, o)
+            ctxs.append((cm, co, cp))
+        _mark(ev, 1)
+        loss = torch.zeros(1, dtype=F32, device=mc.device)
+        dm, dz = torch.empty_like(mc), torch.empty_like(zc)
+        self.K.sq_mean(mc, loss, dm)
+        self.K.sq_mean(zc, loss, dz)
+        for blk in reversed(range(cfg.n_blocks)):
+            cm, co, cp = ctxs[blk]
+            ctxs[blk] = None
+            if cfg.variant == "af2":
+                dz1 = D.pair_track_bwd(st, sh, blk, cp, dz)
+                dm = self.add(dm, D.opm_bwd(st, sh, blk, co, dz1))
+                dm, dz_row = D.msa_track_bwd(st, sh, blk, cm, dm)
+                dz = self.add(dz1, dz_row)
+            elif cfg.variant == "multimer":
+                dz1 = D.pair_track_bwd(st, sh, blk, cp, dz)
+                dm, dz_row = D.msa_track_bwd(st, sh, blk, cm, dm)
+                dz1 = self.add(dz1, dz_row)
+                dm = self.add(dm, D.opm_bwd(st, sh, blk, co, dz1))
+                dz = dz1
+            else:
+                dz_pair = D.pair_track_bwd(st, sh, blk, cp, dz)
+                dm = self.add(dm, D.opm_bwd(st, sh, blk, co, dz))
+                dm, dz_row = D.msa_track_bwd(st, sh, blk, cm, dm)
+                dz = self.add(dz_pair, dz_row)
+        return (mc.reshape(s, r, cfg.c_m), zc.reshape(r, r, cfg.c_z), loss,
+                dm.reshape(s, r, cfg.c_m), dz.reshape(r, r, cfg.c_z))
 
 
 class GraphedExec:
@@ -466,9 +567,21 @@ def bp_pair_step(ex, comm, z, K_blocks, mshape, ev=None):
 
 
 def sync_param_grads(ex, comm, K_blocks):
-    """src/schedules.py:300-329: owner broadcast over the BP pair (one
-    bucket per branch per block), then sum / dp over the DP group."""
+    """src/schedules.py:300-329: the DAP group's sum of the shard partials
+    (every parameter but the replicated ones), owner broadcast over the BP
+    pair (one bucket per branch per block), then sum / dp over the DP group."""
     lay = comm.layout
+    if lay.dap > 1:
+        bp_i = lay.coords(comm.rank)[1]
+        mine = ("msa", "pair") if lay.bp == 1 else (("msa",) if bp_i == 0 else ("pair",))
+        for blk in range(K_blocks):
+            for br in mine:
+                g = ex.grad_bank(blk, br)
+                pos = 0
+                for off, n in sorted(ex.replicated(blk, br)) + [(g.numel(), 0)]:
+                    if off > pos:
+                        comm.allreduce_sum(comm.dapg, g[pos:off], "param")
+                    pos = off + n
     if lay.bp == 2:
         r0, r1 = comm.pair
         for blk in range(K_blocks):
@@ -492,8 +605,12 @@ class DistributedStep:
         self.comm = comm or Comm(layout)
         self.rank = self.comm.rank
         self.dp_i, self.bp_i, _ = layout.coords(self.rank)
-        self.ex = executor or CudaExec(cfg, store, precision)
-        if graphs:
+        if executor is None:
+            executor = (DapExec(cfg, store, self.comm, precision) if layout.dap > 1
+                        else CudaExec(cfg, store, precision))
+        self.ex = executor
+        # DAP segments hold collectives: no per-segment graph capture
+        if graphs and layout.dap == 1:
             self.ex = GraphedExec(self.ex)
         if layout.bp == 2:
             self.ex.pack("msa" if self.bp_i == 0 else "pair")
@@ -609,8 +726,7 @@ def run_dp(cfg, store, dp: int, seed: int = 32, max_threads=None, *, precision=N
 
 
 def run_dap(cfg, store, dap: int, seed: int = 32, max_threads=None, *, precision=None):
-    """DAP axial sharding (src/schedules.py:406-407): outside this build's
-    scope; raises ConfigError via ParallelLayout."""
+    """DAP axial sharding over dap ranks (src/schedules.py:406-407)."""
     return run_distributed(cfg, store, ParallelLayout(dap=dap), seed, max_threads,
                            precision=precision)
 

@@ -333,12 +333,16 @@ def attn_geometry(name, cfg):
 # gated attention sub-ops (row, col, tri start/end)
 # ---------------------------------------------------------------------------
 
-def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
+def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True, geom=None, bias_fn=None):
     """x_new = x + attn(x) (fp32 residual fused in the out-projection);
-    resid=False returns the delta alone (the reference sub-op's value)."""
+    resid=False returns the delta alone (the reference sub-op's value).
+    DAP (dap.py): geom overrides attn_geometry (a row shard of the
+    triangle attention: nb = local rows, L = r), and bias_fn maps the
+    shard's pair-bias rows [h, rows] to the full [h, r*r] bias
+    (the allgather of src/evoformer.py:406-407)."""
     dev = x.device
     h, hc, ch = cfg.h, cfg.hc, cfg.c_head
-    nb, L, rb, rl, rows = attn_geometry(name, cfg)
+    nb, L, rb, rl, rows = geom if geom is not None else attn_geometry(name, cfg)
     c_io = x.shape[-1]
     r2 = cfg.r * cfg.r
     ctx = {}
@@ -359,11 +363,16 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
             K.layernorm(z, r2, cfg.c_z, P[f"{px}.lnz_g"], P[f"{px}.lnz_b"], zh, zmu, zrs,
                         cfg.eps)
             ctx.update(z=z, zh=zh, zmu=zmu, zrs=zrs)
+            brows = r2
         else:
             zh = xh
-        bias = _empty((h, r2), F32, dev)
-        # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*r2 + row)
-        K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, r2), r2, h, cfg.c_z)
+            brows = rows
+        bias = _empty((h, brows), F32, dev)
+        # bias[hh, row] = zh[row] . Wb[:, hh]   (C(m=row, n=hh) at hh*brows + row)
+        K.gemm(Mat(zh, cfg.c_z, 1), Mat(pk["Wb"], 1, h), Mat(bias, 1, brows), brows, h,
+               cfg.c_z)
+        if bias_fn is not None:
+            bias = bias_fn(bias)
         ctx["bias"] = bias
     proj = _empty((rows, 4 * hc), act, dev)
     K.linear(xh, rows, c_io, pk["Wqkvg"], 4 * hc, 4 * hc, proj, 4 * hc, bias=pk["bqkvg"],
@@ -384,12 +393,12 @@ def attn_fwd(name, P, px, pk, x, z, cfg, act, resid=True):
     x_new = _empty(x.shape, F32, dev)
     K.linear(gm, rows, hc, pk["Wo"], c_io, c_io, x_new, c_io, bias=P[f"{px}.out_b"],
              residual=x if resid else None)
-    ctx.update(proj=proj, o=o, gm=gm, lse=lse, resid=resid)
+    ctx.update(proj=proj, o=o, gm=gm, lse=lse, resid=resid, geom=(nb, L, rb, rl, rows))
     return x_new, ctx
 
 
 def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None, dz_res=None,
-             join=None):
+             join=None, dbias_fn=None):
     """Returns (dx [rows, c_io] fp32, dz_row or None).  handoff: the emit
     dict of the producer of dx_new (see _ln_bwd_out); emit: this sub-op's.
     dz_res (row attention, fused path only): added to dz_row inside its
@@ -397,7 +406,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
     addition either way); returns (dx, dz_row + dz_res, True) then."""
     dev = dx_new.device
     h, hc, ch = cfg.h, cfg.hc, cfg.c_head
-    nb, L, rb, rl, rows = attn_geometry(name, cfg)
+    nb, L, rb, rl, rows = ctx["geom"]
     c_io = dx_new.shape[-1]
     r2 = cfg.r * cfg.r
     dxa, bias_done = _grad_in(dx_new, rows, c_io, act, dev, handoff)
@@ -425,6 +434,12 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
         K.linear_dw(xh, rows, c_io, dproj, 4 * hc, G["Wqkvg"], 4 * hc)
     dxh = _empty((rows, c_io), F32, dev)
     K.linear_dx(dproj, rows, 4 * hc, pk["Wqkvg"], 4 * hc, c_io, dxh)
+    # pair-bias gradient rows: r*r (row attention: the bias comes from all of
+    # z), or this sub-op's rows (triangle attention; under DAP dbias_fn
+    # turns the full dbias into the shard's rows: allreduce + own-row slice)
+    bstride = r2 if name == "row_attn" else rows
+    if dbias is not None and dbias_fn is not None:
+        dbias = dbias_fn(dbias)
     dz_row = None
     if dbias is not None and ctx["fuse_bias"]:
         # the pair-bias projection's backward (dz += dbias Wb^T, dWb = LN(z)^T
@@ -445,7 +460,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
                 dxa_out = _empty((rows, c_io), act, dev)
                 colsum = emit["bias"]
             K.layernorm_bwd_proj(dxh, ctx["x"], rows, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
-                                 P[f"{px}.ln_b"], dbias, r2, pk["Wb"], h, dx, G["ln_g"],
+                                 P[f"{px}.ln_b"], dbias, bstride, pk["Wb"], h, dx, G["ln_g"],
                                  G["ln_b"], G["Wb"], dres=dres, dx_act=dxa_out,
                                  dx_colsum=colsum)
             if emit is not None:
@@ -453,13 +468,13 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
             off.join()
             return dx, None
     if dbias is not None and not ctx["fuse_bias"]:
-        dbias_a = dbias if act == F32 else _empty((h, r2), act, dev)
+        dbias_a = dbias if act == F32 else _empty((h, bstride), act, dev)
         if act != F32:
-            K.copy2d(dbias, h, r2, dbias_a, s_rs=r2, d_rs=r2)
+            K.copy2d(dbias, h, bstride, dbias_a, s_rs=bstride, d_rs=bstride)
         zh = ctx.get("zh", xh)
         # dWb[c, hh] = sum_row zh[row, c] dbias[hh, row]
-        K.gemm(Mat(zh, 1, cfg.c_z), Mat(dbias_a, r2, 1), Mat(G["Wb"], h, 1), cfg.c_z, h, r2,
-               split_k=K.pick_split(r2, cfg.c_z, h))
+        K.gemm(Mat(zh, 1, cfg.c_z), Mat(dbias_a, bstride, 1), Mat(G["Wb"], h, 1), cfg.c_z, h,
+               bstride, split_k=K.pick_split(bstride, cfg.c_z, h))
         if name == "row_attn":
             dzh = _empty((r2, cfg.c_z), F32, dev)
             K.gemm(Mat(dbias_a, 1, r2), Mat(pk["Wb"], h, 1), Mat(dzh, cfg.c_z, 1), r2,
@@ -468,7 +483,7 @@ def attn_bwd(name, P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None,
             K.layernorm_bwd(dzh, ctx["z"], r2, cfg.c_z, ctx["zmu"], ctx["zrs"],
                             P[f"{px}.lnz_g"], dz_row, G["lnz_g"], G["lnz_b"])
         else:
-            K.gemm(Mat(dbias_a, 1, r2), Mat(pk["Wb"], h, 1), Mat(dxh, cfg.c_z, 1), r2,
+            K.gemm(Mat(dbias_a, 1, bstride), Mat(pk["Wb"], h, 1), Mat(dxh, cfg.c_z, 1), bstride,
                    cfg.c_z, h, accumulate=True)
     dx = _ln_bwd_out(dxh, ctx["x"], rows, c_io, ctx["mu"], ctx["rs"], P[f"{px}.ln_g"],
                      G["ln_g"], G["ln_b"], dx_new if ctx["resid"] else None, act, emit, dev)
@@ -555,9 +570,12 @@ def transition_bwd(P, px, pk, G, ctx, dx_new, cfg, act, handoff=None, emit=None)
 # outer product mean (src/evoformer.py:332-352)
 # ---------------------------------------------------------------------------
 
-def opm_fwd(P, px, pk, m, z_pair, cfg, act):
+def opm_fwd(P, px, pk, m, z_pair, cfg, act, s_norm=None, with_bias=True):
     """z_out = z_pair + opm(m): the block-end join (src/evoformer.py:460)
-    fused as the out-projection's residual."""
+    fused as the out-projection's residual.  DAP (dap.py): m is an s-row
+    shard (cfg.s = its rows), s_norm the full s of the mean, and only one
+    rank of the group adds out_b before the partial sums are allreduced
+    (src/evoformer.py:350-356)."""
     dev = m.device
     s, r, cm, c, cz = cfg.s, cfg.r, cfg.c_m, cfg.c_opm, cfg.c_z
     rows, rc = s * r, r * c
@@ -570,15 +588,17 @@ def opm_fwd(P, px, pk, m, z_pair, cfg, act):
     # o[i,j,p,q] = (1/s) sum_s a[s,i,p] b[s,j,q];  m=(i,p), n=(j,q)
     o = _empty((r, r, c, c), act, dev)
     K.gemm(Mat(ab[0], 1, rc), Mat(ab[1], 1, rc),
-           Mat(o, r * c * c, c * c, rdiv=c, rs0=c, cdiv=c, cs0=1), rc, rc, s, alpha=1.0 / s)
+           Mat(o, r * c * c, c * c, rdiv=c, rs0=c, cdiv=c, cs0=1), rc, rc, s,
+           alpha=1.0 / (s_norm or s))
     z_out = _empty((r * r, cz), F32, dev)
-    K.linear(o, r * r, c * c, pk["Wo"], cz, cz, z_out, cz, bias=P[f"{px}.out_b"],
+    K.linear(o, r * r, c * c, pk["Wo"], cz, cz, z_out, cz,
+             bias=P[f"{px}.out_b"] if with_bias else None,
              residual=z_pair)  # z_pair None => the delta alone
     return z_out, dict(m=m, mh=mh, mu=mu, rs=rs, ab=ab, o=o)
 
 
-def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None):
-    """Returns dm = dm_res + d(opm)/dm."""
+def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None, s_norm=None):
+    """Returns dm = dm_res + d(opm)/dm (s_norm: see opm_fwd)."""
     dev = dz_out.device
     s, r, cm, c, cz = cfg.s, cfg.r, cfg.c_m, cfg.c_opm, cfg.c_z
     rows, rc, r2 = s * r, r * c, r * r
@@ -591,7 +611,7 @@ def opm_bwd(P, px, pk, G, ctx, dz_out, dz_out_act, dm_res, cfg, act, emit=None):
     dor = _empty((rc, rc), act, dev)
     K.gemm(Mat(dz_out_act, cz, 1), Mat(pk["Wo"], cz, 1),
            Mat(dor, c * r * c, r * c, rdiv=r, rs0=c, cdiv=c, cs0=1), r2, c * c, cz,
-           alpha=1.0 / s)
+           alpha=1.0 / (s_norm or s))
     dab = _empty((2, rows, c), act, dev)
     # da[s,(i,p)] = sum_(j,q) b[s,(j,q)] do'[(i,p),(j,q)]   (m = s: row-major
     # output for the TMA store; split-K fills the SMs: only s/128 x rc/128 tiles)

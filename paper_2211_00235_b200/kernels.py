@@ -518,6 +518,18 @@ def copy2d(src, rows: int, cols: int, dst, *, s_rs, s_cs=1, d_rs, d_cs=1, s_off=
                            ptr(dst, d_off), d_rs, d_cs, stream()), "evo_copy2d")
 
 
+def copy3d(src, n0: int, rows: int, cols: int, dst, *, s_bs, s_rs, s_cs=1, d_bs, d_rs, d_cs=1,
+           s_off=0, d_off=0):
+    """dst[b, r, c] = src[b, r, c] over explicit element strides (any dtype pair)."""
+    check(lib().evo_copy3d(dt(src), dt(dst), n0, rows, cols, ptr(src, s_off), s_bs, s_rs, s_cs,
+                           ptr(dst, d_off), d_bs, d_rs, d_cs, stream()), "evo_copy3d")
+
+
+def zero(t):
+    """t[:] = 0 (stream-ordered memset of a contiguous tensor)."""
+    check(lib().evo_zero(ptr(t), t.numel() * t.element_size(), stream()), "evo_zero")
+
+
 def trimul_gate_fwd(proj, rows: int, c: int, ldp: int, a_cf, b_cf):
     check(lib().evo_trimul_gate_fwd(dt(proj), rows, c, ptr(proj), ldp, ptr(a_cf), ptr(b_cf),
                                     stream()), "evo_trimul_gate_fwd")

@@ -29,7 +29,7 @@ F32 = torch.float32
 @dataclass(frozen=True)
 class ParallelLayout:
     """(dp, bp, dap) layout; rank = ((dp_i*bp)+bp_i)*dap + dap_i
-    (src/schedules.py:43-93).  dap must be 1 in this build."""
+    (src/schedules.py:43-93)."""
 
     dp: int = 1
     bp: int = 1
@@ -70,9 +70,10 @@ class ParallelLayout:
         return tuple(self.rank_of(d, bp_i, dap_i) for d in range(self.dp))
 
     def validate_model(self, cfg: EvoConfig) -> None:
-        if self.dap > 1:
-            raise ConfigError("DAP (axial sharding) is outside this build's scope "
-                              "(SURVEY.md 8(f)); use dap=1")
+        if self.dap > 1 and (cfg.s % self.dap or cfg.r % self.dap):
+            raise ConfigError(
+                f"layout.dap={self.dap} must divide both model.s={cfg.s} "
+                f"and model.r={cfg.r}")
         if self.bp == 2 and cfg.variant != "parallel":
             raise ConfigError(
                 "branch parallelism needs the parallel block wiring; the "
@@ -435,13 +436,15 @@ def branch_param_elems(cfg: EvoConfig):
 
 def expected_comm_volume(cfg: EvoConfig, layout: ParallelLayout) -> dict:
     """{(phase, kind): (count, elements)} for one step over the whole world,
-    using the reference's accounting (per-tensor parameter collectives).
-    This build buckets the parameter collectives per branch and block; the
-    element totals are identical."""
+    using the reference's accounting (per-tensor parameter collectives,
+    src/schedules.py:515-572).  This build buckets the parameter collectives
+    per branch and block; the element totals are identical."""
     layout.validate_model(cfg)
     Kb = cfg.n_blocks
     M = cfg.s * cfg.r * cfg.c_m
     Z = cfg.r * cfg.r * cfg.c_z
+    O = cfg.r * cfg.r * cfg.c_opm
+    B = cfg.r * cfg.r * cfg.h
     msa, pair = branch_param_elems(cfg)
     msa *= Kb
     pair *= Kb
@@ -453,14 +456,28 @@ def expected_comm_volume(cfg: EvoConfig, layout: ParallelLayout) -> dict:
             out[(phase, kind)] = (c0 + count, e0 + elements)
 
     if layout.bp == 2:
-        g = layout.dp
+        g = layout.dp * layout.dap       # one branch pair per (dp_i, dap_i)
         bump("fwd", "broadcast", 2 * Kb * g, 2 * Kb * Z * g)
         bump("bwd", "broadcast", (Kb + 1) * g, (Kb * Z + M) * g)
         bump("bwd", "allreduce_sum", Kb * g, Kb * Z * g)
         n = (MSA_PARAM_TENSORS + PAIR_PARAM_TENSORS) * Kb
         bump("param", "broadcast", n * g, (msa + pair) * g)
+    if layout.dap > 1:
+        # per block: gathers of 3 MSA deltas, 5 pair deltas, 3 partner
+        # projections (O) and 2 pair-bias row sets (B); the OPM reduce_sum;
+        # the enter allreduces of every sub-op input, the gathered partner
+        # projections and bias rows; every parameter but opm.out_b
+        g = layout.dp
+        msa_ar, pair_ar = (MSA_PARAM_TENSORS - 1) * Kb, PAIR_PARAM_TENSORS * Kb
+        bump("fwd", "allgather", 3 * Kb * g, 3 * Kb * M * g)
+        bump("fwd", "allreduce_sum", Kb * g, Kb * Z * g)
+        bump("bwd", "allreduce_sum", 5 * Kb * g, Kb * (4 * M + Z) * g)
+        bump("param", "allreduce_sum", msa_ar * g, (msa - Kb * cfg.c_z) * g)
+        bump("fwd", "allgather", 10 * Kb * g, Kb * (5 * Z + 3 * O + 2 * B) * g)
+        bump("bwd", "allreduce_sum", 10 * Kb * g, Kb * (5 * Z + 3 * O + 2 * B) * g)
+        bump("param", "allreduce_sum", pair_ar * g, pair * g)
     if layout.dp > 1:
-        g = layout.bp
+        g = layout.bp * layout.dap
         n = (MSA_PARAM_TENSORS + PAIR_PARAM_TENSORS) * Kb
         bump("param", "allreduce_sum", n * g, (msa + pair) * g)
     return out

@@ -82,15 +82,13 @@ def test_bp2_dp2_four_ranks_matches_replica_mean(pkg):
     assert sorted(res.rank_fwd_seconds) == [0, 1, 2, 3]
 
 
-def test_run_dp_and_dap_rejection(pkg):
+def test_run_dp(pkg):
     cfg = pkg.EvoConfig(**{**KW, "n_blocks": 1})
     store = pkg.init_params(cfg, 32)
     res = pkg.run_dp(cfg, store, 2, precision="fp32")
     assert np.isfinite(res.loss)
     assert pkg.trace_volume(res.trace)[("param", "allreduce_sum")][1] == \
         pkg.expected_comm_volume(cfg, pkg.ParallelLayout(dp=2))[("param", "allreduce_sum")][1]
-    with pytest.raises(pkg.ConfigError):
-        pkg.run_dap(cfg, store, 2)
 
 
 def _graphed_worker(rank, init_file, q):

@@ -90,10 +90,12 @@ def test_comm_volume_matches_reference_closed_form():
         pytest.skip("reference not present on this machine")
     import paper_2211_00235_b200 as pkg
     kw = dict(s=8, r=16, c_m=8, c_z=8, h=2, c_opm=4, t_factor=4, n_blocks=2)
-    for dp, bp in ((1, 2), (2, 1), (4, 2), (2, 2)):
-        mine = pkg.expected_comm_volume(pkg.EvoConfig(**kw), pkg.ParallelLayout(dp=dp, bp=bp))
-        ref = RS.expected_comm_volume(RE.EvoConfig(**kw), RS.ParallelLayout(dp=dp, bp=bp))
-        assert mine == ref, (dp, bp)
+    for dp, bp, dap in ((1, 2, 1), (2, 1, 1), (4, 2, 1), (2, 2, 1), (1, 1, 2), (1, 1, 4),
+                        (1, 2, 2), (2, 2, 2), (2, 1, 4)):
+        mine = pkg.expected_comm_volume(pkg.EvoConfig(**kw),
+                                        pkg.ParallelLayout(dp=dp, bp=bp, dap=dap))
+        ref = RS.expected_comm_volume(RE.EvoConfig(**kw), RS.ParallelLayout(dp=dp, bp=bp, dap=dap))
+        assert mine == ref, (dp, bp, dap)
 
 
 def test_product_path_fails_loudly_without_library(monkeypatch, tmp_path):
