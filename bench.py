@@ -540,6 +540,9 @@ def run_native(args):
         "peak_mem_gb": peak_mem,
         "bp2_prediction": bp2,
         "c3_stack_1gpu": c3,
+        # the last timed step's loss (read back every e2e step): a non-finite
+        # loss invalidates the line
+        "loss": float(loss_h[0]), "loss_finite": bool(np.isfinite(float(loss_h[0]))),
     }
     print(json.dumps(line))
     if world > 1:
@@ -647,6 +650,7 @@ def run_stack(args):
         "gpu_launches": launches_per_step * args.steps,
         "gpu_launches_per_step": launches_per_step, "launch_mode": "cuda_graph",
         "clocks": clk, "peak_mem_gb": torch.cuda.max_memory_allocated(dev) / 1e9,
+        "loss": float(loss_h[0]), "loss_finite": bool(np.isfinite(float(loss_h[0]))),
     }
     if not getattr(args, "quiet", False):
         print(json.dumps(line))

@@ -747,51 +747,30 @@ int choose_split(const evo_gemm_desc *d, int BN, int64_t &k_chunk) {
   return split < 1 ? 1 : split;
 }
 
+// Bulk-copy fallback for the outer-product-mean layouts o[i,j,p,q] and
+// do'[i,p,j,q] when their 4-D tensor map cannot be built (mode 4): every
+// warp chunk (32 rows x 32 columns) is one contiguous 2 KiB bf16 block --
+// rows 32 elements apart inside a 32-aligned row group, columns unit-stride
+// inside a 32-aligned column group.  (The 4-D map with two 32-column SW64
+// boxes per 64-column unit measured 47 us against 54 us for this at the C2
+// OPM GEMM; a single {32 q, 2 j, 32 p, 1 i} box with 128-byte swizzle -- a
+// 64-byte inner box -- does NOT match the SW128 staging image and was
+// removed.)
+static int bulk_block_mode(const evo_gemm_desc *d) {
+  const evo_mat &c = d->C;
+  if (d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate && c.rdiv > 0 &&
+      c.rdiv % 32 == 0 && c.rs0 == 32 && c.cdiv > 0 && c.cdiv % 32 == 0 && c.cs0 == 1 &&
+      d->M % 32 == 0 && d->N % 32 == 0 && (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0 &&
+      (c.rs % 8) == 0 && (c.cs % 8) == 0)
+    return 4;
+  return 0;
+}
+
 // TMA store map for C when its index map is expressible (no batching; a
 // residual only for fp32 plain 2-D outputs, accumulate only for fp32, done
 // as a bulk reduce-add): returns the store mode (0 = not expressible).
 int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   if (d->B1 * d->B2 != 1) return 0;
-  {
-    // 32-column groups (the outer-product-mean o[i,j,p,q], c = 32): a 4-D
-    // box {32 q, 2 j, 32 p, 1 i} stores a whole 64-column unit (4 KiB) per
-    // TMA op from the same SW128 staging image as a plain 64-wide box (the
-    // two 64-byte q runs of a row p form one 128-byte swizzle row); the
-    // 2 KiB bulk-copy blocks of mode 4 measured ~1.7x slower
-    const evo_mat &c = d->C;
-    const int64_t es = 2;
-    auto ok16 = [&](int64_t st) { return st > 0 && (st * es) % 16 == 0; };
-    if (d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate && c.cdiv == 32 &&
-        c.cs0 == 1 && c.rdiv > 0 && c.rdiv % 32 == 0 && d->M % c.rdiv == 0 &&
-        d->N % 64 == 0 && ok16(c.cs) && ok16(c.rs0) && ok16(c.rs) &&
-        (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0) {
-      cuuint64_t dims[4] = {32, (cuuint64_t)(d->N / 32), (cuuint64_t)c.rdiv,
-                            (cuuint64_t)(d->M / c.rdiv)};
-      cuuint64_t strides[3] = {(cuuint64_t)(c.cs * es), (cuuint64_t)(c.rs0 * es),
-                               (cuuint64_t)(c.rs * es)};
-      cuuint32_t box[4] = {32, 2, 32, 1}, estr[4] = {1, 1, 1, 1};
-      EncodeTiledFn fn = encode_fn();
-      if (fn && fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, c.ptr, dims, strides, box, estr,
-                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
-        *box_w = 64;
-        return 3;
-      }
-    }
-  }
-  {
-    // mode 4: every warp chunk (32 rows x 32 columns) is one contiguous
-    // 2 KiB bf16 block (the outer-product-mean layouts o[i,j,p,q] and
-    // do'[i,p,j,q]): rows 32 elements apart inside a 32-aligned row group,
-    // columns unit-stride inside a 32-aligned column group
-    const evo_mat &c = d->C;
-    if (d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate && c.rdiv > 0 &&
-        c.rdiv % 32 == 0 && c.rs0 == 32 && c.cdiv > 0 && c.cdiv % 32 == 0 && c.cs0 == 1 &&
-        d->M % 32 == 0 && d->N % 32 == 0 &&
-        (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0 && (c.rs % 8) == 0 && (c.cs % 8) == 0)
-      return 4;
-  }
   if ((d->residual || d->accumulate) && d->dtype_c != EVO_F32) return 0;
   if (d->residual && (d->accumulate || d->C.cdiv || d->C.rdiv ||
                       (reinterpret_cast<uintptr_t>(d->residual) & 15) != 0))
@@ -823,7 +802,7 @@ int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   } else if (c.cdiv > 0 && c.rdiv > 0) {
     if (c.cs0 != 1 || c.cdiv % 32 || d->N % c.cdiv || c.rdiv % 32 || d->M % c.rdiv ||
         !ok16(c.cs) || !ok16(c.rs0) || !ok16(c.rs))
-      return 0;
+      return bulk_block_mode(d);
     dims[0] = c.cdiv; dims[1] = d->N / c.cdiv; dims[2] = c.rdiv; dims[3] = d->M / c.rdiv;
     strides[0] = c.cs * es; strides[1] = c.rs0 * es; strides[2] = c.rs * es;
     box[0] = bw; box[1] = 1; box[2] = 32; box[3] = 1;
@@ -833,14 +812,15 @@ int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   }
   *box_w = (int)bw;
   EncodeTiledFn fn = encode_fn();
-  if (!fn) return 0;
+  if (!fn) return mode == 3 ? bulk_block_mode(d) : 0;
   CUresult r = fn(map, d->dtype_c == EVO_BF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
                                              : CU_TENSOR_MAP_DATA_TYPE_FLOAT32,
                   rank, c.ptr, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
                   (d->dtype_c == EVO_BF16 && bw == 32) ? CU_TENSOR_MAP_SWIZZLE_64B
                                                        : CU_TENSOR_MAP_SWIZZLE_128B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  return r == CUDA_SUCCESS ? mode : 0;
+  if (r != CUDA_SUCCESS) return mode == 3 ? bulk_block_mode(d) : 0;
+  return mode;
 }
 
 template <int BN, int STAGES, int EPI>

@@ -27,6 +27,7 @@ the zero padding a memset (evo_zero).
 from __future__ import annotations
 
 import dataclasses
+import os
 
 import torch
 
@@ -37,6 +38,14 @@ from .errors import DimensionError
 from .kernels import Mat
 
 F32 = torch.float32
+_DEBUG = os.environ.get("EVO_DAP_DEBUG") == "1"
+
+
+def _chk(tag, t):
+    """EVO_DAP_DEBUG=1: report non-finite sub-op results (diagnostics only)."""
+    if _DEBUG and not bool(torch.isfinite(t).all()):
+        print(f"[dap] non-finite {tag} {tuple(t.shape)}", flush=True)
+    return t
 
 
 class DapShard:
@@ -140,7 +149,7 @@ def row_attn_fwd(st, sh, blk, m, z):
     px = f"blk{blk}.row_attn"
     d, ctx = E.attn_fwd("row_attn", st.P, px, st.packs[blk]["row_attn"], m[lo * r:hi * r], z,
                         _cfg(cfg, s=hi - lo), act, resid=False)
-    return _add(m, sh.gather_rows(d)), (ctx, lo, hi)
+    return _add(m, sh.gather_rows(_chk("row_attn", d))), (ctx, lo, hi)
 
 
 def row_attn_bwd(st, sh, blk, c, dm):
@@ -187,7 +196,7 @@ def transition_fwd(st, sh, blk, name, x, rows_axis):
     lo, hi = sh.bounds(rows_axis)
     d, ctx = E.transition_fwd(st.P, f"blk{blk}.{name}", st.packs[blk][name], x[lo * R:hi * R],
                               cfg, act, resid=False)
-    return _add(x, sh.gather_rows(d)), (ctx, lo, hi, R)
+    return _add(x, sh.gather_rows(_chk(name, d))), (ctx, lo, hi, R)
 
 
 def transition_bwd(st, sh, blk, name, c, dx_out):
@@ -206,6 +215,7 @@ def opm_fwd(st, sh, blk, m):
     lo, hi = sh.bounds(s)
     o, ctx = E.opm_fwd(st.P, f"blk{blk}.opm", st.packs[blk]["opm"], m[lo * r:hi * r], None,
                        _cfg(cfg, s=hi - lo), act, s_norm=s, with_bias=sh.index == 0)
+    _chk("opm part", o)
     sh.allreduce(o, "fwd")
     return o, (ctx, lo, hi)
 
@@ -283,6 +293,9 @@ def trimul_fwd(st, sh, blk, name, z):
     K.linear(pn, R, c, pk["Wo"], cz, cz, o, cz, bias=P[f"{px}.out_b"])
     d = torch.empty((R, cz), dtype=F32, device=dev)
     K.mul2d(proj, ldp, 4 * c, o, cz, d, R, cz)
+    _chk(name + " proj", proj)
+    _chk(name + " p", p_cf)
+    _chk(name, d)
     ctx = dict(zl=zl, zh=zh, mu=mu, rs=rs, proj=proj, a_cf=a_cf, b_cf=b_cf, a_full=a_full,
                b_full=b_full, p_cf=p_cf, pn=pn, pmu=pmu, prs=prs, o=o, lo=lo, w=w)
     return _add(z, sh.gather_rows(d)), ctx
@@ -384,6 +397,7 @@ def tri_attn_fwd(st, sh, blk, name, z):
     gather, dgather = _bias_fns(sh, h, R, r * r, lo * r)
     d, ctx = E.attn_fwd("tri_attn_start", st.P, f"blk{blk}.{name}", st.packs[blk][name], x,
                         None, cfg, act, resid=False, geom=(w, r, r, 1, R), bias_fn=gather)
+    _chk(name, d)
     if not ending:
         return _add(z, sh.gather_rows(d)), (ctx, lo, w, dgather)
     buf = sh.gather_rows(d)                                  # [n, w, r, cz] (z^T rows)

@@ -37,7 +37,8 @@ def to_np(x):
 def rel_l2(a, b):
     a, b = to_np(a), to_np(b)
     den = np.linalg.norm(b)
-    return float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+    v = float(np.linalg.norm(a - b) / (den if den > 0 else 1.0))
+    return v if np.isfinite(v) else float("inf")    # NaN must never pass a max() / <=
 
 
 def load_golden(tag):

@@ -18,7 +18,8 @@ def K():
 
 def rel(a, b):
     a, b = a.double(), b.double()
-    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+    v = float((a - b).norm() / b.norm().clamp_min(1e-30))
+    return v if v == v and v != float("inf") else float("inf")
 
 
 def run_case(K, nb, L, H, D, seq_major, bias_mode, dtype, seed=0, gate_bias=False,

@@ -18,7 +18,8 @@ def K():
 
 def rel(a, b):
     a, b = a.double(), b.double()
-    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+    v = float((a - b).norm() / b.norm().clamp_min(1e-30))
+    return v if v == v and v != float("inf") else float("inf")
 
 
 def make_operand(rows, k, kmajor, batch=1, dtype=torch.bfloat16):

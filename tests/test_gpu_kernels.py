@@ -16,7 +16,8 @@ def K():
 
 def rel(a, b):
     a, b = a.detach().double(), b.detach().double()
-    return float((a - b).norm() / b.norm().clamp_min(1e-30))
+    v = float((a - b).norm() / b.norm().clamp_min(1e-30))
+    return v if v == v and v != float("inf") else float("inf")
 
 
 def ln_ref(x, g, b, eps=1e-5):

@@ -27,8 +27,10 @@ def pkg():
 
 
 def _worst(errs):
-    k = max(errs, key=errs.get)
-    return k, errs[k]
+    # NaN sorts as the worst (max() with a NaN key would skip it)
+    k = max(errs, key=lambda n: errs[n] if errs[n] == errs[n] else float("inf"))
+    v = errs[k]
+    return k, (v if v == v else float("inf"))
 
 
 @pytest.mark.parametrize("tag", ["toy", "odd", "c1"])

@@ -25,7 +25,8 @@ def rel(a, b):
     a = np.asarray(a, np.float64)
     b = np.asarray(b, np.float64)
     den = np.linalg.norm(b)
-    return np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+    v = np.linalg.norm(a - b) / (den if den > 0 else 1.0)
+    return v if np.isfinite(v) else np.inf
 
 
 def load(name):
