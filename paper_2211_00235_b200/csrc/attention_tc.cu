@@ -398,21 +398,24 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm,
                                                             bf16 *dO_out, bf16 *dgpre, float *Dq,
                                                             float *gpart) {
-  constexpr int CH = D / 8;  // chunks per head (2 or 4)
-  const int64_t total = a.nb * (int64_t)a.L * a.H * CH;
+  constexpr int CH = D / 8;  // chunks per head (1, 2 or 4)
+  // 32-bit index math (the host checks total < 2^31): the per-element
+  // 64-bit divisions by H and L were the kernel's issue bottleneck
+  const uint32_t HC = (uint32_t)a.H * CH, L = (uint32_t)a.L;
+  const uint32_t total = (uint32_t)(a.nb * (int64_t)a.L) * HC;
   const int lane = threadIdx.x & 31;
   float gacc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
   // warp-uniform trip count (the shuffles below need every lane)
-  for (int64_t e0 = blockIdx.x * (int64_t)blockDim.x + (threadIdx.x - lane); e0 < total;
-       e0 += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t e = e0 + lane;
+  for (uint32_t e0 = blockIdx.x * blockDim.x + (threadIdx.x - lane); e0 < total;
+       e0 += gridDim.x * blockDim.x) {
+    const uint32_t e = e0 + lane;
     const bool ok = e < total;
-    const int c = (int)(e % CH);
-    const int64_t eh = e / CH;
-    const int h = (int)(eh % a.H);
-    const int64_t r = eh / a.H;
-    const int l = (int)(r % a.L);
-    const int64_t b = r / a.L;
+    const uint32_t r = e / HC, hc = e - r * HC;
+    const int c = (int)(hc % CH);
+    const int h = (int)(hc / CH);
+    const uint32_t b32 = r / L;
+    const int l = (int)(r - b32 * L);
+    const int64_t b = b32;
     const int64_t ooff = b * a.o_sb + (int64_t)l * a.o_sl + h * D + 8 * c;
     const int64_t goff = b * a.sb + (int64_t)l * a.sl + h * D + 8 * c;
     const uint4 z4 = make_uint4(0u, 0u, 0u, 0u);
@@ -2243,6 +2246,8 @@ int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
   if (d->D != 8 && d->D != 16 && d->D != 32) return EVO_EUNSUP;
   AttnTcArgs a = make_args(d);
   int64_t total = d->nb * (int64_t)d->L * d->H * (d->D / 8);
+  EVO_REQUIRE(total + 256LL * num_sms() * 32 < (1LL << 31), EVO_EUNSUP,
+              "attention bwd prep: more than 2^31 chunks");
   const bool fuse_gb = d->dgate_bias && (256 % (d->H * (d->D / 8)) == 0);
   EVO_REQUIRE(!d->dgate_bias || fuse_gb, EVO_EUNSUP,
               "attention bwd: gate-bias sums need 256 %% (H*D/8) == 0");
