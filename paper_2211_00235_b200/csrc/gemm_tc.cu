@@ -63,7 +63,8 @@ struct TcParams {
   int store_mode;  // 0: thread stores, 1: TMA 2-D, 2: TMA {cdiv, N/cdiv, M}, 3: TMA 4-D
   int64_t cdiv, rdiv;
   int bias_smem;   // bias[0..N) staged in smem by the epilogue warps
-  int box_w;       // TMA store box width in columns (64: bf16, 128-byte rows)
+  int box_w;       // TMA store box width in columns (64: bf16, 128-byte rows;
+                   // 65: 64 columns as two 64-byte SW64 rows per output row)
   int res_tma;     // fp32 residual TMA-loaded into the staging boxes
 };
 constexpr int BIAS_SMEM_MAX = 2048;
@@ -454,6 +455,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           // byte offset of 16-byte chunk c (0..7) of this lane's row
           auto off = [&](int c) -> int {
             if (p.box_w == 64) return lane * 128 + ((c ^ (lane & 7)) << 4);
+            if (p.box_w == 65)  // rows 2*lane + j of 64 B, SW64: chunk ^ ((row >> 1) & 3)
+              return (2 * lane + (c >> 2)) * 64 + (((c & 3) ^ (lane & 3)) << 4);
             const int hh = c >> 2, cc = c & 3;
             const int sw = p.store_mode == 4 ? 0 : ((lane >> 1) & 3);
             return hh * 2048 + lane * 64 + ((cc ^ sw) << 4);
@@ -480,7 +483,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           __syncwarp();
           if (lane == 0) {
             const int mrow = (int)(mt * BM + q * 32);
-            const int nsub = p.box_w == 64 ? 1 : (second ? 2 : 1);
+            const int nsub = p.box_w >= 64 ? 1 : (second ? 2 : 1);
             for (int sb = 0; sb < nsub; ++sb) {
               const int64_t nbs = nb + 32 * sb;
               const uint8_t *bx = box + sb * 2048;
@@ -766,11 +769,45 @@ static int bulk_block_mode(const evo_gemm_desc *d) {
   return 0;
 }
 
+// EVO_GEMM_OPM_BOX=0: the OPM layouts as two 32-column boxes per unit
+static const bool g_opm_box = [] {
+  const char *e = getenv("EVO_GEMM_OPM_BOX");
+  return !(e && e[0] == '0');
+}();
+
 // TMA store map for C when its index map is expressible (no batching; a
 // residual only for fp32 plain 2-D outputs, accumulate only for fp32, done
 // as a bulk reduce-add): returns the store mode (0 = not expressible).
 int make_store_map(CUtensorMap *map, const evo_gemm_desc *d, int *box_w) {
   if (d->B1 * d->B2 != 1) return 0;
+  {
+    // 32-column groups (the outer-product-mean layouts, c = 32): one 4-D box
+    // {32 q, 2 j, 32 p, 1 i} per 64-column unit.  Its inner dimension is 64
+    // bytes, so the swizzle must be the 64-byte one (a 64-byte box row under
+    // SW128 is not the SW128 image of a 128-byte row); the staging writes
+    // each output row p as box rows 2p, 2p+1 (box_w code 65)
+    const evo_mat &c = d->C;
+    const int64_t es = 2;
+    auto ok16 = [&](int64_t st) { return st > 0 && (st * es) % 16 == 0; };
+    if (g_opm_box && d->dtype_c == EVO_BF16 && !d->residual && !d->accumulate &&
+        c.cdiv == 32 && c.cs0 == 1 && c.rdiv > 0 && c.rdiv % 32 == 0 && d->M % c.rdiv == 0 &&
+        d->N % 64 == 0 && ok16(c.cs) && ok16(c.rs0) && ok16(c.rs) &&
+        (reinterpret_cast<uintptr_t>(c.ptr) & 15) == 0) {
+      cuuint64_t dims[4] = {32, (cuuint64_t)(d->N / 32), (cuuint64_t)c.rdiv,
+                            (cuuint64_t)(d->M / c.rdiv)};
+      cuuint64_t strides[3] = {(cuuint64_t)(c.cs * es), (cuuint64_t)(c.rs0 * es),
+                               (cuuint64_t)(c.rs * es)};
+      cuuint32_t box[4] = {32, 2, 32, 1}, estr[4] = {1, 1, 1, 1};
+      EncodeTiledFn fn = encode_fn();
+      if (fn && fn(map, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 4, c.ptr, dims, strides, box, estr,
+                   CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_64B,
+                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS) {
+        *box_w = 65;
+        return 3;
+      }
+    }
+  }
   if ((d->residual || d->accumulate) && d->dtype_c != EVO_F32) return 0;
   if (d->residual && (d->accumulate || d->C.cdiv || d->C.rdiv ||
                       (reinterpret_cast<uintptr_t>(d->residual) & 15) != 0))

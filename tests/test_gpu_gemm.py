@@ -239,3 +239,41 @@ def test_gemm_tc_accumulate_two_level_map(K):
     got = C.view(r, r, c).permute(1, 0, 2).reshape(r, rc)  # [m, (j,q)]
     want2 = C0.view(r, r, c).permute(1, 0, 2).reshape(r, rc) + a.float()[:, :r].T @ b.float()
     assert rel(got, want2) < 1e-6
+
+
+def test_gemm_opm_layouts_bf16_out(K):
+    """The outer-product-mean GEMMs exactly as the engine issues them, bf16
+    output with c = 32 (the 4-D TMA-store box of the production path,
+    engine.opm_fwd / opm_bwd): o[i,j,p,q] and the input-gradient layout
+    do'[(i,p),(j,q)].  Every element is checked (a wrong store layout once
+    passed a NaN-blind aggregate)."""
+    from paper_2211_00235_b200 import _native
+    c, s = 32, 128
+    for r in (64, 96):
+        rc = r * c
+        ab = (torch.randn(2, s * r, c, device="cuda") * 0.5).to(torch.bfloat16)
+        o = torch.full((r, r, c, c), float("nan"), device="cuda", dtype=torch.bfloat16)
+        before = _native.backend_counts()["gemm_tc"]
+        K.gemm(K.Mat(ab[0], 1, rc), K.Mat(ab[1], 1, rc),
+               K.Mat(o, r * c * c, c * c, rdiv=c, rs0=c, cdiv=c, cs0=1), rc, rc, s,
+               alpha=1.0 / s)
+        torch.cuda.synchronize()
+        assert _native.backend_counts()["gemm_tc"] == before + 1
+        want = torch.einsum("sip,sjq->ijpq", ab[0].float().view(s, r, c),
+                            ab[1].float().view(s, r, c)) / s
+        err = (o.float() - want).abs()
+        assert bool(torch.isfinite(o.float()).all())
+        assert float(err.max()) <= 1e-2 * float(want.abs().max()), float(err.max())
+        # do'[(i,p),(j,q)] = (1/s) dz[(i,j)] . Wo[(p,q)]
+        cz = 128
+        dz = (torch.randn(r * r, cz, device="cuda") * 0.5).to(torch.bfloat16)
+        Wo = (torch.randn(c * c, cz, device="cuda") * 0.05).to(torch.bfloat16)
+        dor = torch.full((rc, rc), float("nan"), device="cuda", dtype=torch.bfloat16)
+        K.gemm(K.Mat(dz, cz, 1), K.Mat(Wo, cz, 1),
+               K.Mat(dor, c * r * c, r * c, rdiv=r, rs0=c, cdiv=c, cs0=1), r * r, c * c, cz,
+               alpha=1.0 / s)
+        torch.cuda.synchronize()
+        full = (dz.float() @ Wo.float().t()) / s
+        want2 = full.reshape(r, r, c, c).permute(0, 2, 1, 3).reshape(rc, rc)
+        assert bool(torch.isfinite(dor.float()).all())
+        assert float((dor.float() - want2).abs().max()) <= 1e-2 * float(want2.abs().max())

@@ -93,7 +93,8 @@ def join(csv_path, shapes_path, json_out=None):
         elif fam is not None or cur is None or not (
                 (cur[0] == "gemm" and ("splitk_reduce" in name or "skinny_reduce" in name)) or
                 (cur[0] == "attention_bwd" and ("attn_bwd" in name or "attn_flash" in name
-                                                or "reduce_lead" in name))):
+                                                or "reduce_lead" in name
+                                                or "colsum_stage2" in name))):
             cur = [name.split("(")[0][:48], None, 0.0, 0.0, [], 0.0]
             groups.append(cur)
         cur[3] += us
