@@ -305,3 +305,19 @@ def test_branch_streams_bitwise(pkg, precision, monkeypatch):
         assert torch.equal(x, y)
     for k, v in b.grad_dict().items():
         assert torch.equal(v, g_ref[k]), k
+
+
+def test_self_launched_world_of_one_runs_over_nccl(pkg):
+    """A one-rank layout self-launches a world of one process with one GPU,
+    so the NCCL backend is the one initialised (process group, groups,
+    world ledger gather); the step equals run_single bitwise."""
+    cfg = pkg.EvoConfig(**{**KW, "n_blocks": 1})
+    store = pkg.init_params(cfg, 32)
+    from paper_2211_00235_b200 import distributed as D
+    assert torch.cuda.device_count() >= 1
+    res = pkg.run_distributed(cfg, store, pkg.ParallelLayout(), 32, precision="bf16")
+    single = pkg.run_single(cfg, store, seed=32, precision="bf16")
+    rep = pkg.compare_runs(single, res, rtol=0.0)
+    assert rep.bitwise, str(rep)
+    assert sorted(res.rank_fwd_seconds) == [0]
+    assert D.dist.is_available()
