@@ -57,6 +57,7 @@ struct FlashArgs {
   bf16 *dq, *dk, *dv;       // proj-gradient columns (q's strides)
   float *dbias_part;        // [chunks][H][L][L] (dq kernel)
   int64_t chunk;
+  int pairs;                // dq kernel: batch rows in pairs (bias)
 };
 
 // swizzle of a [rows x D] bf16 tile with 2D-byte rows (TMA: none / 32B / 64B)
@@ -473,27 +474,35 @@ __device__ __forceinline__ void load_f32(const float *p, bool vec, float (&out)[
 }
 
 // ======================================================================== dq
-// Persistent over a chunk of batch rows (tile g = (row r, key tile j)); Q / dO
-// and the dQ accumulators double-buffered by row parity.
+// Persistent over a chunk of batch rows.  The rows run in PAIRS, tile by
+// tile: tile g -> (row 2p + (w & 1), key tile w >> 1) with w = g mod 2T (a
+// last odd row alone), so a thread meets the pair's two dS tiles of the
+// same keys back to back and reduces their sum into the dbias partial: half
+// the L2 reduction traffic of one reduction per row, the limit of this
+// kernel with a bias (nb H L^2 fp32 reductions per call otherwise).
+// Q / dO in three row buffers (row mod 3: the next pair's first row loads
+// while this pair runs), dQ in two accumulators by row parity.
 // TMEM: buffer g&1 at 160 (g&1): S (64) | dP (64) | dS (32 bf16 pairs);
 // dQ of row parity p at 320 + D p.
+constexpr int DQ_QBUF = 3;
+
 template <int D, bool BIAS>
 __global__ void __launch_bounds__(nth_of(TPR_DQ), 1)
 attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                      const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
   constexpr int TPR = TPR_DQ, EPT = KT / TPR, NEW = 4 * TPR;
-  constexpr int NS = NS_BWD;
+  constexpr int NS = NS_BWD, NQB = DQ_QBUF;
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   if ((smem_u32(smem_raw) & 1023u) != 0) __trap();
   uint8_t *sStage = smem_raw;
-  uint8_t *sQ = sStage + NS * STG;                     // 2 x [Q | dO] (row parity)
-  uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + 4 * QB);
-  uint64_t *qfull = bars, *fullb = qfull + 2, *sdone = fullb + NS, *dsp = sdone + 2,
+  uint8_t *sQ = sStage + NS * STG;                     // NQB x [Q | dO] (row mod NQB)
+  uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + NQB * 2 * QB);
+  uint64_t *qfull = bars, *fullb = qfull + NQB, *sdone = fullb + NS, *dsp = sdone + 2,
            *dqd = dsp + 2, *dqr = dqd + 2;
-  constexpr int NBAR = 2 + NS + 8;
+  constexpr int NBAR = NQB + NS + 8;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
   // 2 KB of zeros above every operand: the padded head-dim half (D = 8)
   uint8_t *sZ = reinterpret_cast<uint8_t *>(
@@ -507,6 +516,23 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
   const int nrows = b_hi > b_lo ? (int)(b_hi - b_lo) : 0;
   const int G = nrows * T;                             // tiles over the chunk
+  // the tile order, stepped incrementally (no divisions on the issue path):
+  // (row r, key tile j, first row pb of r's pair); a pair has two rows when
+  // pb + 1 < nrows, a last odd row (or every row, without a.pairs) is alone
+  struct TIt { int r, j, pb; };
+  auto paired = [&](const TIt &t) { return a.pairs && t.pb + 1 < nrows; };
+  auto adv = [&](TIt &t) {
+    if (paired(t)) {
+      if (t.r == t.pb) {
+        t.r = t.pb + 1;
+      } else {
+        t.r = t.pb;
+        if (++t.j == T) { t.j = 0; t.pb += 2; t.r = t.pb; }
+      }
+    } else if (++t.j == T) {
+      t.j = 0; t.pb += 1; t.r = t.pb;
+    }
+  };
 
   if (tid == NEW * 32) {
     for (int i = 0; i < NBAR; ++i) {
@@ -527,9 +553,9 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   const uint32_t tmem = *tslot;
 
   if (warp == NEW) {
-    auto load_tile = [&](int g) {
-      const int64_t b = b_lo + g / T;
-      const int j = g % T;
+    auto load_tile = [&](int g, const TIt &it) {
+      const int r = it.r, j = it.j;
+      const int64_t b = b_lo + r;
       uint8_t *st = sStage + (g % NS) * STG;
       uint64_t *bar = &fullb[g % NS];
       if (lane == 0) {
@@ -546,26 +572,31 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     };
     auto load_row = [&](int r) {
       if (lane == 0) {
-        uint8_t *dst = sQ + (r & 1) * 2 * QB;
-        mbar_expect_tx(&qfull[r & 1], 2 * QB);
-        tma_load_4d(dst, &mQ, &qfull[r & 1], 0, q0, (int)(b_lo + r), h);
-        tma_load_4d(dst + QB, &mdO, &qfull[r & 1], 0, q0, (int)(b_lo + r), h);
+        uint8_t *dst = sQ + (r % NQB) * 2 * QB;
+        mbar_expect_tx(&qfull[r % NQB], 2 * QB);
+        tma_load_4d(dst, &mQ, &qfull[r % NQB], 0, q0, (int)(b_lo + r), h);
+        tma_load_4d(dst + QB, &mdO, &qfull[r % NQB], 0, q0, (int)(b_lo + r), h);
       }
       __syncwarp();
     };
-    for (int r = 0; r < 2 && r < nrows; ++r) load_row(r);
-    for (int g = 0; g < NS && g < G; ++g) load_tile(g);
+    for (int r = 0; r < NQB && r < nrows; ++r) load_row(r);
+    TIt tl{0, 0, 0}, ts{0, 0, 0}, tq{0, 0, 0};   // next load, S/dP, dQ tiles
+    for (int g = 0; g < NS && g < G; ++g) {
+      load_tile(g, tl);
+      adv(tl);
+    }
     const uint32_t idesc_s = idesc_bf16(128, KT, false, false);
     const uint32_t idesc_o = idesc_bf16(128, dacc<D>(), false, true);
-    int r = 0, j = 0, ri = 0, ji = -1;
     for (int g = 0; g <= G; ++g) {
       if (g < G) {
-        if (j == 0) mbar_wait(&qfull[r & 1], (uint32_t)((r >> 1) & 1));   // row's Q / dO
+        const int r = ts.r, j = ts.j;
+        adv(ts);
+        if (j == 0) mbar_wait(&qfull[r % NQB], (uint32_t)((r / NQB) & 1));   // row's Q / dO
         const int st = g % NS;
         mbar_wait(&fullb[st], (uint32_t)((g / NS) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0), sV = sK + KB;
-        const uint32_t sQa = smem_u32(sQ) + (r & 1) * 2 * QB, sdOa = sQa + QB;
+        const uint32_t sQa = smem_u32(sQ) + (r % NQB) * 2 * QB, sdOa = sQa + QB;
         const uint32_t d = tmem + (g & 1) * 160;
 #pragma unroll
         for (int ks = 0; ks < ksteps<D>(); ++ks)
@@ -576,14 +607,16 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           umma_bf16_el(d + 64, desc_k<D>(sdOa, ks, smem_u32(sZ) - sdOa), desc_k<D>(sV, ks),
                        idesc_s, ks > 0);
         umma_commit_el(&sdone[g & 1]);
-        if (j == T - 1 && r + 2 < nrows) {
-          // row r's last S/dP MMAs read Q / dO: load row r + 2 into its buffer
+        if (j == T - 1 && r + NQB < nrows) {
+          // row r's last S/dP MMAs read Q / dO: load row r + NQB into its buffer
           mbar_wait(&sdone[g & 1], (uint32_t)((g >> 1) & 1));
-          load_row(r + 2);
+          load_row(r + NQB);
         }
       }
       if (g >= 1) {
         const int i = g - 1, bi = i & 1, st = i % NS;
+        const int ri = tq.r, ji = tq.j;
+        adv(tq);
         mbar_wait(&dsp[bi], (uint32_t)((i >> 1) & 1));   // dS_i packed
         if (ji == 0 && ri >= 2) mbar_wait(&dqr[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
         fence_after();
@@ -595,14 +628,9 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         umma_commit_el(&dqd[bi]);
         if (i + NS < G) {
           mbar_wait(&dqd[bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
-          load_tile(i + NS);
+          load_tile(i + NS, tl);
+          adv(tl);
         }
-      }
-      ri = r;
-      ji = j;
-      if (++j == T) {
-        j = 0;
-        ++r;
       }
     }
   } else {
@@ -616,25 +644,42 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
     float *prow = BIAS ? a.dbias_part + (int64_t)blockIdx.z * a.H * L * (int64_t)L +
                              ((int64_t)h * L + q) * L
                        : nullptr;
-    // lse / Dq of this thread's query row, one batch row ahead
-    float lse_n = 0.f, dq_n = 0.f;
-    if (qv && nrows > 0) {
-      lse_n = a.lse[(b_lo * a.H + h) * (int64_t)L + q];
-      dq_n = a.Dq[(b_lo * a.H + h) * (int64_t)L + q];
-    }
-    float lse_l2 = 0.f, dq_ = 0.f;
-    int r = 0, j = 0;
+    // lse / Dq of this thread's query row for the pair's rows (slot 0 / 1),
+    // the next pair's fetched one pair ahead
+    auto fetch = [&](int r, float &l, float &d) {
+      if (qv && r < nrows) {
+        l = a.lse[((b_lo + r) * a.H + h) * (int64_t)L + q];
+        d = a.Dq[((b_lo + r) * a.H + h) * (int64_t)L + q];
+      } else {
+        l = 0.f;
+        d = 0.f;
+      }
+    };
+    float lse_n[2], dq_n[2], lse_l2[2] = {0.f, 0.f}, dq_[2] = {0.f, 0.f};
+    fetch(0, lse_n[0], dq_n[0]);
+    fetch(1, lse_n[1], dq_n[1]);
+    // dS (fp32) of the pair's first row parks in TMEM columns 384 + 32 part
+    // (free past the dQ accumulators) until the second row's tile of the
+    // same keys: registers would spill
+    const uint32_t park = lane_addr + 384 + part * EPT;
+    TIt te{0, 0, 0};
     for (int g = 0; g < G; ++g) {
       const int bi = g & 1, st = g % NS;
-      const int64_t b = b_lo + r;
-      if (j == 0) {
-        lse_l2 = lse_n * LOG2E_F;
-        dq_ = dq_n;
-        if (qv && r + 1 < nrows) {
-          lse_n = a.lse[((b + 1) * a.H + h) * (int64_t)L + q];
-          dq_n = a.Dq[((b + 1) * a.H + h) * (int64_t)L + q];
+      const int r = te.r, j = te.j, pb = te.pb;
+      const bool two = paired(te);                   // this pair has two rows
+      adv(te);
+      const int slot = r - pb;
+      if (j == 0 && slot == 0) {                     // a new pair: its rows' lse / Dq
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          lse_l2[u] = lse_n[u] * LOG2E_F;
+          dq_[u] = dq_n[u];
         }
+        const int nx = pb + (two ? 2 : 1);           // the next pair's first row
+        fetch(nx, lse_n[0], dq_n[0]);
+        fetch(nx + 1, lse_n[1], dq_n[1]);            // (past the last row: zeros)
       }
+      const int64_t b = b_lo + r;
       const int kb = j * KT + part * EPT;
       float *dst = prow + kb;
       const bool full_k = kb + EPT <= L;
@@ -650,34 +695,53 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       tmem_wait_ld();
       uint32_t pk[EPT / 2];
       float ds[EPT];
+      // selects, not an indexed load: a runtime index would put the arrays
+      // in local memory
+      const float ll = slot ? lse_l2[1] : lse_l2[0], dqv = slot ? dq_[1] : dq_[0];
       if (qv && full_k) {
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
-          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
+          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -ll);
           if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
-          ds[k] = ex2f(x) * (__uint_as_float(dv[k]) - dq_);
+          ds[k] = ex2f(x) * (__uint_as_float(dv[k]) - dqv);
         }
       } else {
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
-          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -lse_l2);
+          float x = fmaf(__uint_as_float(sv[k]), sc_l2, -ll);
           if (BIAS) x = fmaf(bb[k], LOG2E_F, x);
           const float p = (qv && kb + k < L) ? ex2f(x) : 0.f;
-          ds[k] = p * (__uint_as_float(dv[k]) - dq_);
+          ds[k] = p * (__uint_as_float(dv[k]) - dqv);
         }
       }
 #pragma unroll
       for (int k = 0; k < EPT; k += 2) pk[k >> 1] = pk2(ds[k], ds[k + 1]);
       tst<EPT / 2>(lane_addr + bi * 160 + 128 + part * (EPT / 2), pk);
       if (BIAS && qv) {
-        // the chunk's dbias partial: the first row stores, later rows add
-        // with fire-and-forget reductions (one owner thread per element and
-        // program order per address: the sum runs over the rows in order)
-        if (vec) {
+        // the chunk's dbias partial: the pair's two rows summed in registers,
+        // then the chunk's first pair stores and later pairs add with
+        // fire-and-forget reductions (one owner thread per element, program
+        // order per address: the sum runs over the pairs in order)
+        bool emit = true;
+        if (two && slot == 0) {
+          uint32_t u[EPT];
+#pragma unroll
+          for (int k = 0; k < EPT; ++k) u[k] = __float_as_uint(ds[k]);
+          tst<EPT>(park, u);
+          emit = false;
+        } else if (two) {
+          uint32_t u[EPT];
+          tld<EPT>(park, u);
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < EPT; ++k) ds[k] += __uint_as_float(u[k]);
+        }
+        const bool first = pb == 0;
+        if (emit && vec) {
 #pragma unroll
           for (int c = 0; c < EPT / 4; ++c) {
             float *d4 = dst + 4 * c;
-            if (r == 0) {
+            if (first) {
               *reinterpret_cast<float4 *>(d4) =
                   make_float4(ds[4 * c], ds[4 * c + 1], ds[4 * c + 2], ds[4 * c + 3]);
             } else {
@@ -687,11 +751,11 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
                            : "memory");
             }
           }
-        } else {
+        } else if (emit) {
 #pragma unroll
           for (int k2 = 0; k2 < EPT; ++k2) {
             if (kb + k2 >= L) continue;
-            if (r == 0) dst[k2] = ds[k2];
+            if (first) dst[k2] = ds[k2];
             else asm volatile("red.global.add.f32 [%0], %1;" ::"l"(dst + k2), "f"(ds[k2]) : "memory");
           }
         }
@@ -712,10 +776,6 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         if (lane == 0) mbar_arrive(&dqr[r & 1]);
         if (qv && part * OD < D)
           store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v, a.scale);
-      }
-      if (++j == T) {
-        j = 0;
-        ++r;
       }
     }
   }
@@ -1025,6 +1085,13 @@ bool flash_bias_map(CUtensorMap *m, const float *bias, int L, int H, int64_t bq,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// EVO_FLASH_DQ_PAIRS=0/1 forces the dq kernel's row order (default: pairs
+// with a bias, single rows without)
+static const int g_dq_pairs = [] {
+  const char *e = getenv("EVO_FLASH_DQ_PAIRS");
+  return e ? (e[0] == '1' ? 1 : 0) : -1;
+}();
+
 FlashArgs flash_args(const evo_attn_desc *d) {
   FlashArgs a;
   a.nb = d->nb; a.H = d->H; a.L = d->L; a.D = d->D; a.scale = d->scale;
@@ -1037,6 +1104,7 @@ FlashArgs flash_args(const evo_attn_desc *d) {
   a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
   a.dv = reinterpret_cast<bf16 *>(d->dv);
   a.dbias_part = nullptr; a.chunk = 1;
+  a.pairs = 0;
   return a;
 }
 
@@ -1130,6 +1198,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   a.chunk = flash_chunk(d, 1, nch);
   a.Dq = Dq;
   a.dbias_part = BIAS ? reinterpret_cast<float *>(ws + w.part) : nullptr;
+  a.pairs = g_dq_pairs < 0 ? (BIAS ? 1 : 0) : g_dq_pairs;
   CUtensorMap mq, mk, mv, mdo, mb, mq2, mdo2, mk2, mv2, mb2;
   // dq kernel: Q / dO tiles of 128 queries, K / V tiles of 64 keys
   if (!flash_head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
@@ -1153,7 +1222,8 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   }
   {
     constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-    const size_t smem = NS_BWD * STG + 4 * QT * 2 * D + (2 + NS_BWD + 8) * 8 + 16 + 1024 + 2048;
+    const size_t smem = NS_BWD * STG + DQ_QBUF * 2 * QT * 2 * D +
+                        (DQ_QBUF + NS_BWD + 8) * 8 + 16 + 1024 + 2048;
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
