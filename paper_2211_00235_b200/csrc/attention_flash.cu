@@ -57,7 +57,7 @@ struct FlashArgs {
   bf16 *dq, *dk, *dv;       // proj-gradient columns (q's strides)
   float *dbias_part;        // [chunks][H][L][L] (dq kernel)
   int64_t chunk;
-  int pairs;                // dq kernel: batch rows in pairs (bias)
+  int group;                // dq kernel: batch rows per group (1, 2 or 4; bias)
 };
 
 // swizzle of a [rows x D] bf16 tile with 2D-byte rows (TMA: none / 32B / 64B)
@@ -474,17 +474,17 @@ __device__ __forceinline__ void load_f32(const float *p, bool vec, float (&out)[
 }
 
 // ======================================================================== dq
-// Persistent over a chunk of batch rows.  The rows run in PAIRS, tile by
-// tile: tile g -> (row 2p + (w & 1), key tile w >> 1) with w = g mod 2T (a
-// last odd row alone), so a thread meets the pair's two dS tiles of the
-// same keys back to back and reduces their sum into the dbias partial: half
-// the L2 reduction traffic of one reduction per row, the limit of this
-// kernel with a bias (nb H L^2 fp32 reductions per call otherwise).
-// Q / dO in three row buffers (row mod 3: the next pair's first row loads
-// while this pair runs), dQ in two accumulators by row parity.
+// Persistent over a chunk of batch rows.  With a pair bias the rows run in
+// GROUPS of a.group (4), tile by tile: (row pb, key tile j), (pb+1, j), ...,
+// (pb+3, j), (pb, j+1), ..., so a thread meets the group's dS tiles of the
+// same keys back to back; their sum (parked in TMEM) is the one dbias
+// reduction: a quarter of the L2 reduction traffic of one reduction per row,
+// which bounds this kernel with a bias (nb H L^2 fp32 reductions per call).
+// Q / dO in four row buffers (row mod 4: the next group's rows load as this
+// group's rows finish), dQ in four accumulators (row mod 4).
 // TMEM: buffer g&1 at 160 (g&1): S (64) | dP (64) | dS (32 bf16 pairs);
-// dQ of row parity p at 320 + D p.
-constexpr int DQ_QBUF = 3;
+// dQ of row r at 320 + dacc (r mod 4); the parked dS sum past them.
+constexpr int DQ_QBUF = 4, DQ_ACC = 4, DQ_GROUP = 4;
 
 template <int D, bool BIAS>
 __global__ void __launch_bounds__(nth_of(TPR_DQ), 1)
@@ -501,8 +501,8 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   uint8_t *sQ = sStage + NS * STG;                     // NQB x [Q | dO] (row mod NQB)
   uint64_t *bars = reinterpret_cast<uint64_t *>(sQ + NQB * 2 * QB);
   uint64_t *qfull = bars, *fullb = qfull + NQB, *sdone = fullb + NS, *dsp = sdone + 2,
-           *dqd = dsp + 2, *dqr = dqd + 2;
-  constexpr int NBAR = NQB + NS + 8;
+           *dqd = dsp + 2, *dqr = dqd + 2;               // dqr: DQ_ACC
+  constexpr int NBAR = NQB + NS + 6 + DQ_ACC;
   uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + NBAR);
   // 2 KB of zeros above every operand: the padded head-dim half (D = 8)
   uint8_t *sZ = reinterpret_cast<uint8_t *>(
@@ -517,27 +517,29 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   const int nrows = b_hi > b_lo ? (int)(b_hi - b_lo) : 0;
   const int G = nrows * T;                             // tiles over the chunk
   // the tile order, stepped incrementally (no divisions on the issue path):
-  // (row r, key tile j, first row pb of r's pair); a pair has two rows when
-  // pb + 1 < nrows, a last odd row (or every row, without a.pairs) is alone
-  struct TIt { int r, j, pb; };
-  auto paired = [&](const TIt &t) { return a.pairs && t.pb + 1 < nrows; };
+  // (row r, key tile j, first row pb and size gs of r's group; the last
+  // group may be short, a.group 1 = one row at a time)
+  struct TIt { int r, j, pb, gs; };
+  const int GR = a.group;
+  auto first_it = [&]() { return TIt{0, 0, 0, min(GR, nrows)}; };
   auto adv = [&](TIt &t) {
-    if (paired(t)) {
-      if (t.r == t.pb) {
-        t.r = t.pb + 1;
-      } else {
+    if (t.r + 1 < t.pb + t.gs) {
+      ++t.r;
+    } else {
+      t.r = t.pb;
+      if (++t.j == T) {
+        t.j = 0;
+        t.pb += t.gs;
+        t.gs = min(GR, nrows - t.pb);
         t.r = t.pb;
-        if (++t.j == T) { t.j = 0; t.pb += 2; t.r = t.pb; }
       }
-    } else if (++t.j == T) {
-      t.j = 0; t.pb += 1; t.r = t.pb;
     }
   };
 
   if (tid == NEW * 32) {
     for (int i = 0; i < NBAR; ++i) {
       uint64_t *bb = &bars[i];
-      const bool warps = bb == &dsp[0] || bb == &dsp[1] || bb == &dqr[0] || bb == &dqr[1];
+      const bool warps = bb == &dsp[0] || bb == &dsp[1] || (bb >= dqr && bb < dqr + DQ_ACC);
       mbar_init(bb, warps ? NEW : 1);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -551,6 +553,8 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
   __syncthreads();
   fence_after();
   const uint32_t tmem = *tslot;
+  constexpr uint32_t DQC = 320;                        // dQ accumulators
+  constexpr uint32_t PARK = DQC + DQ_ACC * dacc<D>();  // parked dS sums
 
   if (warp == NEW) {
     auto load_tile = [&](int g, const TIt &it) {
@@ -580,7 +584,7 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       __syncwarp();
     };
     for (int r = 0; r < NQB && r < nrows; ++r) load_row(r);
-    TIt tl{0, 0, 0}, ts{0, 0, 0}, tq{0, 0, 0};   // next load, S/dP, dQ tiles
+    TIt tl = first_it(), ts = first_it(), tq = first_it();   // next load, S/dP, dQ tiles
     for (int g = 0; g < NS && g < G; ++g) {
       load_tile(g, tl);
       adv(tl);
@@ -618,12 +622,14 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         const int ri = tq.r, ji = tq.j;
         adv(tq);
         mbar_wait(&dsp[bi], (uint32_t)((i >> 1) & 1));   // dS_i packed
-        if (ji == 0 && ri >= 2) mbar_wait(&dqr[ri & 1], (uint32_t)(((ri >> 1) - 1) & 1));
+        // row ri's accumulator was read out (row ri - DQ_ACC)
+        if (ji == 0 && ri >= DQ_ACC)
+          mbar_wait(&dqr[ri % DQ_ACC], (uint32_t)(((ri / DQ_ACC) - 1) & 1));
         fence_after();
         const uint32_t sK = smem_u32(sStage + st * STG) + (BIAS ? BIAS_TILE : 0);
 #pragma unroll
         for (int ks = 0; ks < KT / 16; ++ks)
-          umma_bf16_ts_el(tmem + 320 + dacc<D>() * (ri & 1), tmem + bi * 160 + 128 + 8 * ks,
+          umma_bf16_ts_el(tmem + DQC + dacc<D>() * (ri % DQ_ACC), tmem + bi * 160 + 128 + 8 * ks,
                           desc_mn<D>(sK, ks), idesc_o, (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&dqd[bi]);
         if (i + NS < G) {
@@ -655,29 +661,32 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         d = 0.f;
       }
     };
-    float lse_n[2], dq_n[2], lse_l2[2] = {0.f, 0.f}, dq_[2] = {0.f, 0.f};
-    fetch(0, lse_n[0], dq_n[0]);
-    fetch(1, lse_n[1], dq_n[1]);
-    // dS (fp32) of the pair's first row parks in TMEM columns 384 + 32 part
-    // (free past the dQ accumulators) until the second row's tile of the
-    // same keys: registers would spill
-    const uint32_t park = lane_addr + 384 + part * EPT;
-    TIt te{0, 0, 0};
+    float lse_n[DQ_GROUP], dq_n[DQ_GROUP], lse_l2[DQ_GROUP], dq_[DQ_GROUP];
+#pragma unroll
+    for (int u = 0; u < DQ_GROUP; ++u) {
+      fetch(u < GR ? u : nrows, lse_n[u], dq_n[u]);
+      lse_l2[u] = dq_[u] = 0.f;
+    }
+    // the running dS sum of a group's rows parks in TMEM past the dQ
+    // accumulators until the group's last row: registers would spill
+    const uint32_t park = lane_addr + PARK + part * EPT;
+    TIt te = first_it();
     for (int g = 0; g < G; ++g) {
       const int bi = g & 1, st = g % NS;
-      const int r = te.r, j = te.j, pb = te.pb;
-      const bool two = paired(te);                   // this pair has two rows
+      const int r = te.r, j = te.j, pb = te.pb, gs = te.gs;
       adv(te);
       const int slot = r - pb;
-      if (j == 0 && slot == 0) {                     // a new pair: its rows' lse / Dq
+      if (j == 0 && slot == 0) {                     // a new group: its rows' lse / Dq
 #pragma unroll
-        for (int u = 0; u < 2; ++u) {
+        for (int u = 0; u < DQ_GROUP; ++u) {
           lse_l2[u] = lse_n[u] * LOG2E_F;
           dq_[u] = dq_n[u];
         }
-        const int nx = pb + (two ? 2 : 1);           // the next pair's first row
-        fetch(nx, lse_n[0], dq_n[0]);
-        fetch(nx + 1, lse_n[1], dq_n[1]);            // (past the last row: zeros)
+        const int nx = pb + gs;                      // the next group's first row
+        const int ngs = min(GR, nrows - nx);
+#pragma unroll
+        for (int u = 0; u < DQ_GROUP; ++u)           // (past the group: zeros)
+          fetch(u < ngs ? nx + u : nrows, lse_n[u], dq_n[u]);
       }
       const int64_t b = b_lo + r;
       const int kb = j * KT + part * EPT;
@@ -697,7 +706,8 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       float ds[EPT];
       // selects, not an indexed load: a runtime index would put the arrays
       // in local memory
-      const float ll = slot ? lse_l2[1] : lse_l2[0], dqv = slot ? dq_[1] : dq_[0];
+      const float ll = slot < 2 ? (slot ? lse_l2[1] : lse_l2[0]) : (slot == 2 ? lse_l2[2] : lse_l2[3]);
+      const float dqv = slot < 2 ? (slot ? dq_[1] : dq_[0]) : (slot == 2 ? dq_[2] : dq_[3]);
       if (qv && full_k) {
 #pragma unroll
         for (int k = 0; k < EPT; ++k) {
@@ -722,19 +732,20 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         // then the chunk's first pair stores and later pairs add with
         // fire-and-forget reductions (one owner thread per element, program
         // order per address: the sum runs over the pairs in order)
-        bool emit = true;
-        if (two && slot == 0) {
+        const bool emit = slot == gs - 1;            // the group's last row
+        if (gs > 1) {
           uint32_t u[EPT];
+          if (slot > 0) {                            // add the parked sum
+            tld<EPT>(park, u);
+            tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < EPT; ++k) u[k] = __float_as_uint(ds[k]);
-          tst<EPT>(park, u);
-          emit = false;
-        } else if (two) {
-          uint32_t u[EPT];
-          tld<EPT>(park, u);
-          tmem_wait_ld();
+            for (int k = 0; k < EPT; ++k) ds[k] += __uint_as_float(u[k]);
+          }
+          if (!emit) {                               // park the running sum
 #pragma unroll
-          for (int k = 0; k < EPT; ++k) ds[k] += __uint_as_float(u[k]);
+            for (int k = 0; k < EPT; ++k) u[k] = __float_as_uint(ds[k]);
+            tst<EPT>(park, u);
+          }
         }
         const bool first = pb == 0;
         if (emit && vec) {
@@ -769,11 +780,11 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
         mbar_wait(&dqd[bi], (uint32_t)((g >> 1) & 1));
         fence_after();
         uint32_t v[OD];
-        tld<OD>(lane_addr + 320 + dacc<D>() * (r & 1) + part * OD, v);
+        tld<OD>(lane_addr + DQC + dacc<D>() * (r % DQ_ACC) + part * OD, v);
         tmem_wait_ld();
         fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&dqr[r & 1]);
+        if (lane == 0) mbar_arrive(&dqr[r % DQ_ACC]);
         if (qv && part * OD < D)
           store_row_bf16<OD>(a.dq + b * a.sb + (int64_t)q * a.sl + h * D + part * OD, v, a.scale);
       }
@@ -1085,11 +1096,13 @@ bool flash_bias_map(CUtensorMap *m, const float *bias, int L, int H, int64_t bq,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// EVO_FLASH_DQ_PAIRS=0/1 forces the dq kernel's row order (default: pairs
-// with a bias, single rows without)
-static const int g_dq_pairs = [] {
-  const char *e = getenv("EVO_FLASH_DQ_PAIRS");
-  return e ? (e[0] == '1' ? 1 : 0) : -1;
+// EVO_FLASH_DQ_GROUP=1/2/4 forces the dq kernel's rows per group (default 4:
+// with a bias a quarter of the dbias reductions; without one, measured
+// 1.53 -> 1.41 ms at 1024 keys, D = 8, too)
+static const int g_dq_group = [] {
+  const char *e = getenv("EVO_FLASH_DQ_GROUP");
+  const int v = e ? atoi(e) : 0;
+  return (v == 1 || v == 2 || v == 4) ? v : 0;
 }();
 
 FlashArgs flash_args(const evo_attn_desc *d) {
@@ -1104,7 +1117,7 @@ FlashArgs flash_args(const evo_attn_desc *d) {
   a.dq = reinterpret_cast<bf16 *>(d->dq); a.dk = reinterpret_cast<bf16 *>(d->dk);
   a.dv = reinterpret_cast<bf16 *>(d->dv);
   a.dbias_part = nullptr; a.chunk = 1;
-  a.pairs = 0;
+  a.group = 1;
   return a;
 }
 
@@ -1198,7 +1211,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   a.chunk = flash_chunk(d, 1, nch);
   a.Dq = Dq;
   a.dbias_part = BIAS ? reinterpret_cast<float *>(ws + w.part) : nullptr;
-  a.pairs = g_dq_pairs < 0 ? (BIAS ? 1 : 0) : g_dq_pairs;
+  a.group = g_dq_group ? g_dq_group : DQ_GROUP;
   CUtensorMap mq, mk, mv, mdo, mb, mq2, mdo2, mk2, mv2, mb2;
   // dq kernel: Q / dO tiles of 128 queries, K / V tiles of 64 keys
   if (!flash_head_map(&mq, d->q, D, d->L, d->nb, d->H, d->sl, d->sb, QT) ||
@@ -1222,8 +1235,9 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   }
   {
     constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
+    // (the 2 KiB zero block and its alignment only for D = 8)
     const size_t smem = NS_BWD * STG + DQ_QBUF * 2 * QT * 2 * D +
-                        (DQ_QBUF + NS_BWD + 8) * 8 + 16 + 1024 + 2048;
+                        (DQ_QBUF + NS_BWD + 6 + DQ_ACC) * 8 + 16 + (D == 8 ? 1024 + 2048 : 0);
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
