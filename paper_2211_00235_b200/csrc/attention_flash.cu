@@ -632,11 +632,13 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
           umma_bf16_ts_el(tmem + DQC + dacc<D>() * (ri % DQ_ACC), tmem + bi * 160 + 128 + 8 * ks,
                           desc_mn<D>(sK, ks), idesc_o, (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&dqd[bi]);
-        if (i + NS < G) {
-          mbar_wait(&dqd[bi], (uint32_t)((i >> 1) & 1));  // stage of tile i free
-          load_tile(i + NS, tl);
-          adv(tl);
-        }
+      }
+      // refill the stage of tile g - 2 (see the dk/dv kernel)
+      if (g >= 2 && g - 2 + NS < G) {
+        const int i2 = g - 2;
+        mbar_wait(&dqd[i2 & 1], (uint32_t)((i2 >> 1) & 1));  // stage of tile g - 2 free
+        load_tile(i2 + NS, tl);
+        adv(tl);
       }
     }
   } else {
@@ -944,10 +946,14 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
           umma_bf16_ts_el(acc, base + 160 + 8 * ks, desc_mn<D>(sQ, ks), idesc_o,
                           (ji > 0 || ks > 0) ? 1u : 0u);
         umma_commit_el(&mmd[bi]);
-        if (i + NS < G) {
-          mbar_wait(&mmd[bi], (uint32_t)((i >> 1) & 1));
-          load_tile(i + NS);
-        }
+      }
+      // refill the stage of tile g - 2 (its dV/dK MMAs were issued an
+      // iteration ago: by now they are usually done, so this wait no longer
+      // sits between the tile's dV/dK MMAs and the next S MMA)
+      if (g >= 2 && g - 2 + NS < G) {
+        const int i2 = g - 2;
+        mbar_wait(&mmd[i2 & 1], (uint32_t)((i2 >> 1) & 1));
+        load_tile(i2 + NS);
       }
       ri = r;
       ji = j;
