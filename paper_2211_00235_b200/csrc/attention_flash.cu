@@ -41,6 +41,10 @@ constexpr int KT = 64;     // streamed tile (keys, or queries in dkv) = UMMA N
 // elements each, NEW = 4 TPR elementwise warps + 1 issuer warp
 constexpr int TPR_FWD = 2, TPR_DQ = 2, TPR_DKV = 4;  // fwd: 2 CTAs / SM; dq, dkv: 1 (512 TMEM cols)
 constexpr int NS_FWD = 2, NS_BWD = 4;     // streamed-tile stages
+// forward stages: two with a bias tile (40 KB each, two CTAs per SM), four
+// without one (the K/V tiles alone are small): the extra depth hides the
+// TMA latency of the next tiles behind the softmax
+template <bool BIAS> constexpr int ns_fwd() { return BIAS ? NS_FWD : 4; }
 constexpr int nth_of(int tpr) { return (4 * tpr + 1) * 32; }
 constexpr uint32_t BIAS_TILE = 2 * 16384;  // two [128 x 32] fp32 SW128 boxes
 
@@ -177,7 +181,7 @@ attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                       const FlashArgs a) {
   constexpr int TPR = TPR_FWD, EPT = KT / TPR, NEW = 4 * TPR;
-  constexpr int NS = NS_FWD;
+  constexpr int NS = ns_fwd<BIAS>();
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KB;
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -1188,8 +1192,8 @@ int flash_fwd(const evo_attn_desc *d, cudaStream_t st) {
     mb = mq;
   }
   constexpr uint32_t STG = (BIAS ? BIAS_TILE : 0) + 2 * KT * 2 * D;
-  const size_t smem = NS_FWD * STG + 2 * QT * 2 * D + (3 * TPR_FWD * 128) * 4 +
-                      (2 + NS_FWD + 8) * 8 + 16 + 1024 + 2048;
+  const size_t smem = ns_fwd<BIAS>() * STG + 2 * QT * 2 * D + (3 * TPR_FWD * 128) * 4 +
+                      (2 + ns_fwd<BIAS>() + 8) * 8 + 16 + 1024 + 2048;
   auto kfn = attn_flash_fwd_kernel<D, BIAS>;
   EVO_MAX_SMEM_ONCE(kfn);
   // one batch row per CTA (measured faster than persistent chunks: the
