@@ -289,7 +289,7 @@ class CudaExec:
         return full_step(self.st, m, z, fwd_events=ev)
 
     def sq_mean(self, x):
-        loss = torch.zeros(1, dtype=F32, device=self.dev)
+        loss = self.K.zeros(1, F32, self.dev)
         dx = torch.empty_like(x)
         self.K.sq_mean(x, loss, dx)
         return loss, dx
@@ -354,7 +354,7 @@ class DapExec(CudaExec):
                 mc, zc = m_new, self.add(z_b, o)
             ctxs.append((cm, co, cp))
         _mark(ev, 1)
-        loss = torch.zeros(1, dtype=F32, device=mc.device)
+        loss = self.K.zeros(1, F32, mc.device)
         dm, dz = torch.empty_like(mc), torch.empty_like(zc)
         self.K.sq_mean(mc, loss, dm)
         self.K.sq_mean(zc, loss, dz)
@@ -458,7 +458,7 @@ class ComposedExec:
         if blk == self.Ke:
             self.dm_main = dm_in
             cfg = self.e.cfg
-            dm_in = torch.zeros(cfg.s * cfg.r, cfg.c_m, dtype=F32, device=self.dev)
+            dm_in = self.m.K.zeros((cfg.s * cfg.r, cfg.c_m), F32, self.dev)
         return dm_in, dz_row
 
     def pair_bwd(self, blk, ctx, dz):

@@ -528,6 +528,12 @@ def copy3d(src, n0: int, rows: int, cols: int, dst, *, s_bs, s_rs, s_cs=1, d_bs,
 def zero(t):
     """t[:] = 0 (stream-ordered memset of a contiguous tensor)."""
     check(lib().evo_zero(ptr(t), t.numel() * t.element_size(), stream()), "evo_zero")
+    return t
+
+
+def zeros(shape, dtype=torch.float32, device="cuda"):
+    """A zero-filled tensor by memset (no framework kernel on the step path)."""
+    return zero(torch.empty(shape, dtype=dtype, device=device))
 
 
 def trimul_gate_fwd(proj, rows: int, c: int, ldp: int, a_cf, b_cf):

@@ -284,7 +284,7 @@ def full_step(st: StepState, m, z, fwd_events=None):
     m_c, z_c, ctxs = _stack_fwd(st, m_c, z_c)
     if fwd_events is not None:
         fwd_events[1].record()
-    loss = torch.zeros(1, dtype=F32, device=m.device)
+    loss = K.zeros(1, F32, m.device)
     dm = torch.empty_like(m_c)
     dz = torch.empty_like(z_c)
     K.sq_mean(m_c, loss, dm)
@@ -314,13 +314,13 @@ def composed_step(extra: StepState, main: StepState, m_e, m, z):
     me_c, z_c, ctx_e = _stack_fwd(extra, me_c, z_c)
     m_c = m.reshape(cm.s * cm.r, cm.c_m)
     m_c, z_c, ctx_m = _stack_fwd(main, m_c, z_c)
-    loss = torch.zeros(1, dtype=F32, device=m.device)
+    loss = K.zeros(1, F32, m.device)
     dm = torch.empty_like(m_c)
     dz = torch.empty_like(z_c)
     K.sq_mean(m_c, loss, dm)
     K.sq_mean(z_c, loss, dz)
     dm, dz = _stack_bwd(main, ctx_m, dm, dz)
-    dm_e = torch.zeros(me_c.shape, dtype=F32, device=m.device)
+    dm_e = K.zeros(me_c.shape, F32, m.device)
     dm_e, dz = _stack_bwd(extra, ctx_e, dm_e, dz)
     return (m_c.reshape(cm.s, cm.r, cm.c_m), z_c.reshape(cm.r, cm.r, cm.c_z), loss,
             dm_e.reshape(ce.s, ce.r, ce.c_m), dm.reshape(cm.s, cm.r, cm.c_m),
