@@ -139,3 +139,18 @@ def test_dap2_c2_bf16_tensor_core_shards(pkg):
     worst = sorted(ge.items(), key=lambda kv: -kv[1])[:4]
     print("C2 dap2 bf16 vs bp1 bf16:", errs, "worst grads", worst)
     assert max(errs.values()) <= 2e-2 and worst[0][1] <= 2e-2, (errs, worst)
+
+
+def test_dap2_long_keys_bf16(pkg):
+    """DAP=2 with more than 256 keys (r = 384): the sharded triangle and
+    row attentions run the streamed-key kernels with a shard's batch rows
+    and the full (gathered) pair bias."""
+    kw = dict(s=16, r=384, c_m=64, c_z=64, h=2, c_opm=8, t_factor=2, n_blocks=1)
+    cfg = pkg.EvoConfig(**kw)
+    store = pkg.init_params(cfg, 32)
+    one = pkg.run_single(cfg, store, seed=32, precision="bf16")
+    got = pkg.run_dap(cfg, store, 2, 32, precision="bf16")
+    errs = {f: _rel_l2(getattr(got, f), getattr(one, f)) for f in ("m_out", "z_out", "dm", "dz")}
+    ge = max(_rel_l2(got.grads[n], one.grads[n]) for n in one.grads if not n.endswith("lnz_b"))
+    print("r384 dap2 bf16 vs bp1 bf16:", errs, "worst grad", ge)
+    assert max(errs.values()) <= 2e-2 and ge <= 2e-2, (errs, ge)
