@@ -573,10 +573,10 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   uint8_t *sRow = sBias + (BIASMODE ? BIAS_BYTES : 0);
   float *sMax = reinterpret_cast<float *>(sRow + 2 * ROWB);  // [parity][quarter][128]
   float *sSum = sMax + 2 * 4 * 128;
-  // 0 bias, 1-2 row data, 3-4 S MMA done, 5-6 PV MMA done, 7-8 P packed
-  // (16 warps), 9-10 epilogue read O (16 warps)   [all by row parity]
+  // 0 bias, 1-2 row Q|K, 3-4 S MMA done, 5-6 PV MMA done, 7-8 P packed
+  // (16 warps), 9-10 epilogue read O (16 warps), 11-12 row V  [by row parity]
   uint64_t *bars = reinterpret_cast<uint64_t *>(sSum + 2 * 4 * 128);
-  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 11);
+  uint32_t *tslot = reinterpret_cast<uint32_t *>(bars + 13);
 
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int t = (warp & 3) * 32 + lane;  // query row (TMEM lane)
@@ -589,7 +589,7 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
   const int64_t b_hi = min(a.nb, b_lo + a.chunk);
 
   if (tid == 512) {
-    for (int i = 0; i < 11; ++i) mbar_init(&bars[i], (i >= 7) ? 16 : 1);
+    for (int i = 0; i < 13; ++i) mbar_init(&bars[i], (i >= 7 && i < 11) ? 16 : 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     if (BIASMODE) load_bias_tile<TB>(sBias, &mB, &bars[0], h, q0, LPC);
   }
@@ -605,12 +605,20 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     {
     const uint32_t idesc_s = idesc_bf16(128, LPC, false, false);
     const uint32_t idesc_o = idesc_bf16(128, D, false, true);
-    auto load_row = [&](int64_t r) {
+    // Q|K and V of a row load separately: Q|K of row r+2 as soon as S(r)
+    // is done (its S MMA then waits on nothing but the epilogue of row r),
+    // V of row r+2 once PV(r) has read row r's V
+    auto load_qk = [&](int64_t r) {
       uint8_t *rb = rowbuf(r);
       uint64_t *bar = &bars[1 + ((r - b_lo) & 1)];
-      mbar_expect_tx(bar, ROWB);
+      mbar_expect_tx(bar, TILE + FULL);
       tma_load_4d(rb, &mQ, bar, 0, q0, (int)r, h);
       tma_load_4d(rb + TILE, &mK, bar, 0, 0, (int)r, h);
+    };
+    auto load_v = [&](int64_t r) {
+      uint8_t *rb = rowbuf(r);
+      uint64_t *bar = &bars[11 + ((r - b_lo) & 1)];
+      mbar_expect_tx(bar, FULL);
       tma_load_4d(rb + TILE + FULL, &mV, bar, 0, 0, (int)r, h);
     };
     auto issue_s = [&](int64_t r) {
@@ -627,8 +635,12 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
     };
     if (b_lo < b_hi) {
       if (lane == 0) {
-        load_row(b_lo);
-        if (b_lo + 1 < b_hi) load_row(b_lo + 1);
+        load_qk(b_lo);
+        load_v(b_lo);
+        if (b_lo + 1 < b_hi) {
+          load_qk(b_lo + 1);
+          load_v(b_lo + 1);
+        }
       }
       __syncwarp();
       issue_s(b_lo);
@@ -636,7 +648,13 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
       for (int64_t r = b_lo; r < b_hi; ++r) {
         const int p = (int)((r - b_lo) & 1);
         const uint32_t ph = (uint32_t)(((r - b_lo) >> 1) & 1);
+        if (r + 2 < b_hi) {
+          mbar_wait(&bars[3 + p], ph);  // S(r) done: row r's Q|K is free
+          if (lane == 0) load_qk(r + 2);
+          __syncwarp();
+        }
         mbar_wait(&bars[7 + p], ph);  // P(r) packed by all 16 warps
+        mbar_wait(&bars[11 + p], ph);  // V(r) landed
         fence_after();
         const uint32_t sV = smem_u32(rowbuf(r)) + TILE + FULL;
         const uint32_t slot = tmem + 256 * p;
@@ -647,8 +665,8 @@ attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constan
                           desc_mnmajor_tile<D>(sV, ks), idesc_o, ks > 0);
         umma_commit_el(&bars[5 + p]);
         if (r + 2 < b_hi) {
-          mbar_wait(&bars[5 + p], ph);  // PV(r) done: row r's smem is free
-          if (lane == 0) load_row(r + 2);
+          mbar_wait(&bars[5 + p], ph);  // PV(r) done: row r's V is free
+          if (lane == 0) load_v(r + 2);
           __syncwarp();
           mbar_wait(&bars[9 + p], ph);  // epilogue(r) read O: slot p is free
           fence_after();
@@ -2015,7 +2033,7 @@ int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
   if ((a.Lp == 256 || a.Lp == 128) && D <= 32 && !g_attn_no_pipe) {
     const size_t smem2 = (BM_ ? BIAS_BYTES : 0) + 2 * ((size_t)QT * 2 * D + 2 * (size_t)a.Lp * 2 * D) +
-                         2 * 2 * 4 * 128 * 4 + 11 * 8 + 16;
+                         2 * 2 * 4 * 128 * 4 + 13 * 8 + 16;
     if (a.Lp == 256) {
       EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_, 256>));
       attn_fwd_tc2_kernel<D, BM_, 256><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
