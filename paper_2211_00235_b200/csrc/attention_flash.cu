@@ -180,6 +180,7 @@ __global__ void __maxnreg__(96)
 attn_flash_fwd_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                       const FlashArgs a) {
+  evo_pdl_enter();
   constexpr int TPR = TPR_FWD, EPT = KT / TPR, NEW = 4 * TPR;
   constexpr int NS = ns_fwd<BIAS>();
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
@@ -495,6 +496,7 @@ __global__ void __launch_bounds__(nth_of(TPR_DQ), 1)
 attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                      const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                      const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
+  evo_pdl_enter();
   constexpr int TPR = TPR_DQ, EPT = KT / TPR, NEW = 4 * TPR;
   constexpr int NS = NS_BWD, NQB = DQ_QBUF;
   constexpr uint32_t QB = QT * Sw<D>::bytes, KB = KT * Sw<D>::bytes;
@@ -813,6 +815,7 @@ __global__ void __launch_bounds__(nth_of(TPR_DKV), 1)
 attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                       const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mdO,
                       const __grid_constant__ CUtensorMap mB, const FlashArgs a) {
+  evo_pdl_enter();
   constexpr int TPR = TPR_DKV, EPT = KT / TPR, NEW = 4 * TPR;
   constexpr int NS = NS_BWD;
   constexpr uint32_t KB = QT * Sw<D>::bytes, QB = KT * Sw<D>::bytes;
@@ -1201,7 +1204,7 @@ int flash_fwd(const evo_attn_desc *d, cudaStream_t st) {
   const int64_t nch = d->nb;
   a.chunk = 1;
   dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-  kfn<<<grid, nth_of(TPR_FWD), smem, st>>>(mq, mk, mv, mb, a);
+  launch_k(kfn, grid, nth_of(TPR_FWD), smem, st, mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_flash_fwd_kernel");
   return EVO_OK;
 }
@@ -1251,7 +1254,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
     auto kfn = attn_flash_dq_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-    kfn<<<grid, nth_of(TPR_DQ), smem, st>>>(mq, mk, mv, mdo, mb, a);
+    launch_k(kfn, grid, nth_of(TPR_DQ), smem, st, mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_flash_dq_kernel");
   }
   {
@@ -1261,7 +1264,7 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
     auto kfn = attn_flash_dkv_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-    kfn<<<grid, nth_of(TPR_DKV), smem, st>>>(mq2, mk2, mv2, mdo2, mb2, a);
+    launch_k(kfn, grid, nth_of(TPR_DKV), smem, st, mq2, mk2, mv2, mdo2, mb2, a);
     EVO_LAUNCHED("attn_flash_dkv_kernel");
   }
   if (BIAS) {

@@ -37,6 +37,7 @@ __global__ void long_softmax_kernel(int64_t nrows, int H, int L, int64_t ld,
                                     const float *__restrict__ S, const float *__restrict__ bias,
                                     int64_t bh, int64_t bq, int64_t bk, bf16 *__restrict__ P,
                                     float *__restrict__ lse) {
+  evo_pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (row >= nrows) return;
@@ -83,6 +84,7 @@ __global__ void long_softmax_kernel(int64_t nrows, int H, int L, int64_t ld,
 __global__ void long_gate_kernel(int64_t n, int hc, const float *__restrict__ O,
                                  const bf16 *__restrict__ g, int64_t g_rs, bf16 *__restrict__ o,
                                  bf16 *__restrict__ gm) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = e / hc;
@@ -100,6 +102,7 @@ __global__ void long_prep_kernel(int64_t rows, int H, int D, const bf16 *__restr
                                  const bf16 *__restrict__ o, bf16 *__restrict__ dO,
                                  bf16 *__restrict__ dgpre, int64_t dg_rs,
                                  float *__restrict__ Dq) {
+  evo_pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t w = blockIdx.x * (int64_t)(blockDim.x >> 5) + (threadIdx.x >> 5);
   if (w >= rows * H) return;
@@ -131,6 +134,7 @@ __global__ void long_dsoftmax_kernel(int nbc, int H, int L, int64_t ld,
                                      const float *__restrict__ Dq, int64_t row0, int64_t rb,
                                      int64_t rl, bf16 *__restrict__ P, bf16 *__restrict__ dS,
                                      float *__restrict__ dbias, int acc) {
+  evo_pdl_enter();
   const int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t LL = (int64_t)L * L;
   if (e >= H * LL) return;
@@ -177,7 +181,7 @@ EVO_API int evo_attn_long_softmax(int64_t nbc, int H, int L, int64_t ld, const f
   const int64_t rows = nbc * H * L;
   if (rows == 0) return EVO_OK;
 #define EVO_LONG_SOFTMAX(NJ)                                                            \
-  long_softmax_kernel<NJ><<<warps_grid(rows, 8), 256, 0, (cudaStream_t)stream>>>(        \
+  launch_k(long_softmax_kernel<NJ>, warps_grid(rows, 8), 256, 0, (cudaStream_t)stream, \
       rows, H, L, ld, S, bias, bh, bq, bk, reinterpret_cast<bf16 *>(P), lse)
   if (L <= 256) EVO_LONG_SOFTMAX(8);
   else if (L <= 512) EVO_LONG_SOFTMAX(16);
@@ -194,8 +198,7 @@ EVO_API int evo_attn_long_gate(int64_t rows, int hc, const float *O, const void 
               "attn_long_gate: bad arguments");
   const int64_t n = rows * hc;
   if (n == 0) return EVO_OK;
-  long_gate_kernel<<<(unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0,
-                     (cudaStream_t)stream>>>(n, hc, O, reinterpret_cast<const bf16 *>(g), g_rs,
+  launch_k(long_gate_kernel, (unsigned)std::min<int64_t>((n + 255) / 256, 148 * 32), 256, 0, (cudaStream_t)stream, n, hc, O, reinterpret_cast<const bf16 *>(g), g_rs,
                                              reinterpret_cast<bf16 *>(o),
                                              reinterpret_cast<bf16 *>(gm));
   EVO_LAUNCHED("long_gate_kernel");
@@ -208,8 +211,7 @@ EVO_API int evo_attn_long_prep(int64_t rows, int H, int D, const void *dgm, cons
   EVO_REQUIRE(rows >= 0 && H >= 1 && D >= 1 && dgm && g && o && dO && dgpre && Dq, EVO_EARG,
               "attn_long_prep: bad arguments");
   if (rows == 0) return EVO_OK;
-  long_prep_kernel<<<warps_grid(rows * H, 8), 256, 0, (cudaStream_t)stream>>>(
-      rows, H, D, reinterpret_cast<const bf16 *>(dgm), reinterpret_cast<const bf16 *>(g), g_rs,
+  launch_k(long_prep_kernel, warps_grid(rows * H, 8), 256, 0, (cudaStream_t)stream, rows, H, D, reinterpret_cast<const bf16 *>(dgm), reinterpret_cast<const bf16 *>(g), g_rs,
       reinterpret_cast<const bf16 *>(o), reinterpret_cast<bf16 *>(dO),
       reinterpret_cast<bf16 *>(dgpre), dg_rs, Dq);
   EVO_LAUNCHED("long_prep_kernel");
@@ -227,8 +229,7 @@ EVO_API int evo_attn_long_dsoftmax(int nbc, int H, int L, int64_t ld, const floa
               "attn_long_dsoftmax: bad arguments");
   if (nbc == 0) return EVO_OK;
   const int64_t n = (int64_t)H * L * L;
-  long_dsoftmax_kernel<<<(unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream>>>(
-      nbc, H, L, ld, S, dP, bias, bh, bq, bk, lse, Dq, row0, rb, rl, reinterpret_cast<bf16 *>(P),
+  launch_k(long_dsoftmax_kernel, (unsigned)((n + 255) / 256), 256, 0, (cudaStream_t)stream, nbc, H, L, ld, S, dP, bias, bh, bq, bk, lse, Dq, row0, rb, rl, reinterpret_cast<bf16 *>(P),
       reinterpret_cast<bf16 *>(dS), dbias, acc);
   EVO_LAUNCHED("long_dsoftmax_kernel");
   return EVO_OK;

@@ -49,6 +49,7 @@ __device__ void load_rows(float *dst, const void *src, int64_t base, int64_t sl,
 
 template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
+  evo_pdl_enter();
   extern __shared__ float sm[];
   const int L = a.L, D = a.D, Dp = D + 1;
   float *Ks = sm;
@@ -120,6 +121,7 @@ __global__ void __launch_bounds__(AW * 32) attn_fwd_kernel(evo_attn_desc a) {
 template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32)
 attn_bwd_dq_kernel(evo_attn_desc a, int64_t chunk, float *dbias_part) {
+  evo_pdl_enter();
   extern __shared__ float sm[];
   const int L = a.L, D = a.D, Dp = D + 1;
   float *Ks = sm;
@@ -205,6 +207,7 @@ attn_bwd_dq_kernel(evo_attn_desc a, int64_t chunk, float *dbias_part) {
 // dk, dv.  grid (ceil(L/QT) key tiles, H, nb).
 template <typename T, int ML>
 __global__ void __launch_bounds__(AW * 32) attn_bwd_dkv_kernel(evo_attn_desc a) {
+  evo_pdl_enter();
   extern __shared__ float sm[];
   const int L = a.L, D = a.D, Dp = D + 1;
   float *Qs = sm;                  // [L][Dp]
@@ -312,7 +315,7 @@ int attention_simt_fwd(const evo_attn_desc *a, cudaStream_t st) {
 #define EVO_SIMT_FWD(T, ML)                                             \
   {                                                                    \
     EVO_MAX_SMEM_ONCE((attn_fwd_kernel<T, ML>));                       \
-    attn_fwd_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a);           \
+    launch_k(attn_fwd_kernel<T, ML>, grid, AW * 32, smem, st, *a);           \
   }
   const bool f32 = a->dtype == EVO_F32;
   if (a->L <= 256) { if (f32) EVO_SIMT_FWD(float, 256) else EVO_SIMT_FWD(bf16, 256) }
@@ -328,6 +331,7 @@ int attention_simt_fwd(const evo_attn_desc *a, cudaStream_t st) {
 // columns), then colsum_partials adds the GB_PARTS partials in order.
 template <typename T>
 __global__ void gate_bias_part_kernel(const evo_attn_desc a, int64_t rpp, float *part) {
+  evo_pdl_enter();
   const int cols = a.H * a.D;
   const int64_t n = a.nb * (int64_t)a.L;
   const int64_t r0 = blockIdx.x * rpp, r1 = min(n, r0 + rpp);
@@ -366,7 +370,7 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
 #define EVO_SIMT_DQ(T, ML)                                                   \
   {                                                                         \
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_kernel<T, ML>));                         \
-    attn_bwd_dq_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a, chunk, part); \
+    launch_k(attn_bwd_dq_kernel<T, ML>, grid, AW * 32, smem, st, *a, chunk, part); \
   }
     const bool f32 = a->dtype == EVO_F32;
     if (L <= 256) { if (f32) EVO_SIMT_DQ(float, 256) else EVO_SIMT_DQ(bf16, 256) }
@@ -383,7 +387,7 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
 #define EVO_SIMT_DKV(T, ML)                                      \
   {                                                             \
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_kernel<T, ML>));            \
-    attn_bwd_dkv_kernel<T, ML><<<grid, AW * 32, smem, st>>>(*a); \
+    launch_k(attn_bwd_dkv_kernel<T, ML>, grid, AW * 32, smem, st, *a); \
   }
     const bool f32 = a->dtype == EVO_F32;
     if (L <= 256) { if (f32) EVO_SIMT_DKV(float, 256) else EVO_SIMT_DKV(bf16, 256) }
@@ -408,9 +412,9 @@ int attention_simt_bwd(const evo_attn_desc *a, cudaStream_t st) {
     const int parts = (int)((n + rpp - 1) / rpp);
     const int thr = std::min(256, ((cols + 31) / 32) * 32);
     if (a->dtype == EVO_F32)
-      gate_bias_part_kernel<float><<<parts, thr, 0, st>>>(*a, rpp, gpart);
+      launch_k(gate_bias_part_kernel<float>, parts, thr, 0, st, *a, rpp, gpart);
     else
-      gate_bias_part_kernel<bf16><<<parts, thr, 0, st>>>(*a, rpp, gpart);
+      launch_k(gate_bias_part_kernel<bf16>, parts, thr, 0, st, *a, rpp, gpart);
     EVO_LAUNCHED("gate_bias_part_kernel");
     int rc = colsum_partials(parts, cols, gpart, a->dgate_bias, 0, st);
     if (rc != EVO_OK) return rc;

@@ -213,6 +213,7 @@ __global__ void __launch_bounds__(256)
 attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                    const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                    const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
   constexpr uint32_t WGB = TILE + 2 * FULL;  // per-warpgroup Q | K | V
@@ -398,6 +399,7 @@ template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm,
                                                             bf16 *dO_out, bf16 *dgpre, float *Dq,
                                                             float *gpart) {
+  evo_pdl_enter();
   constexpr int CH = D / 8;  // chunks per head (1, 2 or 4)
   // 32-bit index math (the host checks total < 2^31): the per-element
   // 64-bit divisions by H and L were the kernel's issue bottleneck
@@ -559,6 +561,7 @@ __global__ void __launch_bounds__(544, 1)
 attn_fwd_tc2_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant__ CUtensorMap mK,
                     const __grid_constant__ CUtensorMap mV, const __grid_constant__ CUtensorMap mB,
                     const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   // LPC = Lp (128 or 256): each thread owns KQ = LPC/4 keys; O sits in
   // quarter 0's freed half (Lp 256) or past S (Lp 128)
@@ -821,6 +824,7 @@ attn_bwd_dq_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
                       const __grid_constant__ CUtensorMap mV,
                       const __grid_constant__ CUtensorMap mdO,
                       const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
   constexpr bool TB = BIASMODE == 2;
@@ -1043,6 +1047,7 @@ attn_bwd_dkv_tc_kernel(const __grid_constant__ CUtensorMap mKt, const __grid_con
                        const __grid_constant__ CUtensorMap mQa,
                        const __grid_constant__ CUtensorMap mdOa,
                        const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = 256 * Sw<D>::bytes;
   // plain bias (bk == 1): smem [q][128 k], read by column;
@@ -1270,6 +1275,7 @@ attn_bwd_dkv_pipe_kernel(const __grid_constant__ CUtensorMap mKt,
                          const __grid_constant__ CUtensorMap mQa,
                          const __grid_constant__ CUtensorMap mdOa,
                          const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr int UW = 64, LPC = NU * UW;           // Lp = 64 NU (128 or 256)
   constexpr uint32_t TILE = QT * Sw<D>::bytes;
   constexpr uint32_t FULL = LPC * Sw<D>::bytes;
@@ -1595,6 +1601,7 @@ attn_bwd_dq_pipe_kernel(const __grid_constant__ CUtensorMap mQ,
                         const __grid_constant__ CUtensorMap mV,
                         const __grid_constant__ CUtensorMap mdO,
                         const __grid_constant__ CUtensorMap mB, const AttnTcArgs a) {
+  evo_pdl_enter();
   constexpr int UW = 32, LPC = NU * UW;           // Lp = 32 NU (128 or 256)
   constexpr int QW = EWW / 4;                     // elementwise warps per lane quadrant
   constexpr int KPT = UW / QW;                    // keys per thread per unit
@@ -2036,16 +2043,16 @@ int fwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                          2 * 2 * 4 * 128 * 4 + 13 * 8 + 16;
     if (a.Lp == 256) {
       EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_, 256>));
-      attn_fwd_tc2_kernel<D, BM_, 256><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+      launch_k(attn_fwd_tc2_kernel<D, BM_, 256>, grid, 544, smem2, st, mq, mk, mv, mb, a);
     } else {
       EVO_MAX_SMEM_ONCE((attn_fwd_tc2_kernel<D, BM_, 128>));
-      attn_fwd_tc2_kernel<D, BM_, 128><<<grid, 544, smem2, st>>>(mq, mk, mv, mb, a);
+      launch_k(attn_fwd_tc2_kernel<D, BM_, 128>, grid, 544, smem2, st, mq, mk, mv, mb, a);
     }
     EVO_LAUNCHED("attn_fwd_tc2_kernel");
     return EVO_OK;
   }
   EVO_MAX_SMEM_ONCE((attn_fwd_tc_kernel<D, BM_>));
-  attn_fwd_tc_kernel<D, BM_><<<grid, 256, smem, st>>>(mq, mk, mv, mb, a);
+  launch_k(attn_fwd_tc_kernel<D, BM_>, grid, 256, smem, st, mq, mk, mv, mb, a);
   EVO_LAUNCHED("attn_fwd_tc_kernel");
   return EVO_OK;
 }
@@ -2105,7 +2112,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     int blocks = (int)std::min<int64_t>((total + 255) / 256,
                                         (int64_t)num_sms() * (fuse_gb ? 8 : 32));
     float *gpart = fuse_gb ? reinterpret_cast<float *>(ws + gate_part_offset(d)) : nullptr;
-    attn_bwd_prep_kernel<D><<<blocks, 256, 0, st>>>(a, reinterpret_cast<const bf16 *>(d->dgm),
+    launch_k(attn_bwd_prep_kernel<D>, blocks, 256, 0, st, a, reinterpret_cast<const bf16 *>(d->dgm),
                                                      dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq,
                                                      gpart);
     EVO_LAUNCHED("attn_bwd_prep_kernel");
@@ -2149,18 +2156,18 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     if (g_dq_eww == 16) {
       if (Lp == 256) {
         EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8, 16>));
-        attn_bwd_dq_pipe_kernel<D, BM_, 8, 16><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+        launch_k(attn_bwd_dq_pipe_kernel<D, BM_, 8, 16>, grid, 576, smem, st, mq, mk, mv, mdo, mb, a);
       } else {
         EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4, 16>));
-        attn_bwd_dq_pipe_kernel<D, BM_, 4, 16><<<grid, 576, smem, st>>>(mq, mk, mv, mdo, mb, a);
+        launch_k(attn_bwd_dq_pipe_kernel<D, BM_, 4, 16>, grid, 576, smem, st, mq, mk, mv, mdo, mb, a);
       }
     } else {
       if (Lp == 256) {
         EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 8, 8>));
-        attn_bwd_dq_pipe_kernel<D, BM_, 8, 8><<<grid, 320, smem, st>>>(mq, mk, mv, mdo, mb, a);
+        launch_k(attn_bwd_dq_pipe_kernel<D, BM_, 8, 8>, grid, 320, smem, st, mq, mk, mv, mdo, mb, a);
       } else {
         EVO_MAX_SMEM_ONCE((attn_bwd_dq_pipe_kernel<D, BM_, 4, 8>));
-        attn_bwd_dq_pipe_kernel<D, BM_, 4, 8><<<grid, 320, smem, st>>>(mq, mk, mv, mdo, mb, a);
+        launch_k(attn_bwd_dq_pipe_kernel<D, BM_, 4, 8>, grid, 320, smem, st, mq, mk, mv, mdo, mb, a);
       }
     }
     EVO_LAUNCHED("attn_bwd_dq_pipe_kernel");
@@ -2169,7 +2176,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         3 * 256 * 2 * D + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dq_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dq_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mq, mk, mv, mdo, mb, a);
+    launch_k(attn_bwd_dq_tc_kernel<D, BM_>, grid, 512, smem, st, mq, mk, mv, mdo, mb, a);
     EVO_LAUNCHED("attn_bwd_dq_tc_kernel");
   }
   if (pipe) {
@@ -2179,10 +2186,10 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     dim3 grid(tiles, d->H, (unsigned)nch);
     if (Lp == 256) {
       EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_, 4>));
-      attn_bwd_dkv_pipe_kernel<D, BM_, 4><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+      launch_k(attn_bwd_dkv_pipe_kernel<D, BM_, 4>, grid, 576, smem, st, mkt, mvt, mqa, mdoa, mbk, a);
     } else {
       EVO_MAX_SMEM_ONCE((attn_bwd_dkv_pipe_kernel<D, BM_, 2>));
-      attn_bwd_dkv_pipe_kernel<D, BM_, 2><<<grid, 576, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+      launch_k(attn_bwd_dkv_pipe_kernel<D, BM_, 2>, grid, 576, smem, st, mkt, mvt, mqa, mdoa, mbk, a);
     }
     EVO_LAUNCHED("attn_bwd_dkv_pipe_kernel");
   } else {
@@ -2190,7 +2197,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
                         2 * (size_t)QT * 2 * D + 2 * 256 * 4 + 128;
     EVO_MAX_SMEM_ONCE((attn_bwd_dkv_tc_kernel<D, BM_>));
     dim3 grid(tiles, d->H, (unsigned)nch);
-    attn_bwd_dkv_tc_kernel<D, BM_><<<grid, 512, smem, st>>>(mkt, mvt, mqa, mdoa, mbk, a);
+    launch_k(attn_bwd_dkv_tc_kernel<D, BM_>, grid, 512, smem, st, mkt, mvt, mqa, mdoa, mbk, a);
     EVO_LAUNCHED("attn_bwd_dkv_tc_kernel");
   }
   if (d->dbias)
@@ -2276,11 +2283,11 @@ int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
   bf16 *dgp = reinterpret_cast<bf16 *>(d->dgpre);
   float *gp = fuse_gb ? gpart : nullptr;
   if (d->D == 32)
-    attn_bwd_prep_kernel<32><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<32>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
   else if (d->D == 16)
-    attn_bwd_prep_kernel<16><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<16>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
   else
-    attn_bwd_prep_kernel<8><<<blocks, 256, 0, st>>>(a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<8>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
   EVO_LAUNCHED("attn_bwd_prep_kernel");
   if (fuse_gb) return colsum_partials(blocks, (int64_t)d->H * d->D, gp, d->dgate_bias, 0, st);
   return EVO_OK;

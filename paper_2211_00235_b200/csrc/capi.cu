@@ -85,6 +85,14 @@ static bool use_tc(const evo_gemm_desc *d) {
   return !d->force_simt && !gemm_skinny_accepts(d) && gemm_tc_accepts(d);
 }
 
+bool pdl_enabled() {
+  static const bool on = [] {
+    const char *e = getenv("EVO_PDL");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
 }  // namespace evo
 
 using namespace evo;

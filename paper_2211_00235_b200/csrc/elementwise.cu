@@ -27,6 +27,7 @@ __device__ __forceinline__ void ST(void *p, int64_t i, float v) {
 template <typename T>
 __global__ void reduce_lead_kernel(int64_t nb, int64_t n1, int64_t n2, const void *src,
                                    float *dst, int64_t d_s1, int64_t d_s2, int acc) {
+  evo_pdl_enter();
   const int64_t total = n1 * n2;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -42,6 +43,7 @@ __global__ void reduce_lead_kernel(int64_t nb, int64_t n1, int64_t n2, const voi
 // per thread, the nb partial slabs summed in order with four loads in flight.
 __global__ void reduce_lead_vec_kernel(int64_t nb, int64_t total4, const float4 *src, float4 *dst,
                                        int acc) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total4;
        e += (int64_t)gridDim.x * blockDim.x) {
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
@@ -65,6 +67,7 @@ __global__ void reduce_lead_vec_kernel(int64_t nb, int64_t total4, const float4 
 template <typename T>
 __global__ void colsum_stage1(int64_t rows, int64_t cols, const void *src, int64_t rs,
                               int64_t rpb, float *part) {
+  evo_pdl_enter();
   __shared__ float red[8][33];
   const int64_t c = blockIdx.y * 32 + threadIdx.x;
   const int64_t r0 = blockIdx.x * rpb;
@@ -96,6 +99,7 @@ __global__ void colsum_stage1(int64_t rows, int64_t cols, const void *src, int64
 template <typename T>
 __global__ void colsum_stage1_vec(int64_t rows, int64_t cols, const void *src, int64_t rs,
                                   int64_t rpb, float *part) {
+  evo_pdl_enter();
   constexpr int VW = 16 / sizeof(T);
   __shared__ float red[8][32 * VW + 4];
   const int64_t c0 = (blockIdx.y * 32 + threadIdx.x) * VW;
@@ -143,6 +147,7 @@ __global__ void colsum_stage1_vec(int64_t rows, int64_t cols, const void *src, i
 // warp sums are combined in order.  Deterministic.
 __global__ void __launch_bounds__(1024) colsum_stage2(int nblk, int64_t cols, const float *part,
                                                       float *dst, int acc) {
+  evo_pdl_enter();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t c = blockIdx.x * 32 + lane;
@@ -164,6 +169,7 @@ __global__ void __launch_bounds__(1024) colsum_stage2(int nblk, int64_t cols, co
 template <typename TS, typename TD>
 __global__ void copy2d_kernel(int64_t rows, int64_t cols, const void *src, int64_t s_rs,
                               int64_t s_cs, void *dst, int64_t d_rs, int64_t d_cs) {
+  evo_pdl_enter();
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -177,6 +183,7 @@ __global__ void copy2d_kernel(int64_t rows, int64_t cols, const void *src, int64
 template <typename TS, typename TD>
 __global__ void copy2d_vec_kernel(int64_t rows, int64_t cols, const void *src, int64_t s_rs,
                                   void *dst, int64_t d_rs) {
+  evo_pdl_enter();
   const int64_t per_row = cols / 8;
   const int64_t total = rows * per_row;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -220,6 +227,7 @@ __global__ void copy2d_vec_kernel(int64_t rows, int64_t cols, const void *src, i
 template <typename TS, typename TD>
 __global__ void transpose_kernel(int64_t rows, int64_t cols, const void *src, int64_t s_rs,
                                  void *dst, int64_t d_cs) {
+  evo_pdl_enter();
   __shared__ float tile[32][33];
   int64_t r0 = blockIdx.y * 32, c0 = blockIdx.x * 32;
   for (int i = threadIdx.y; i < 32; i += blockDim.y) {
@@ -236,6 +244,7 @@ __global__ void transpose_kernel(int64_t rows, int64_t cols, const void *src, in
 template <typename TA, typename TB, typename TO>
 __global__ void mul2d_kernel(int64_t rows, int64_t cols, const void *a, int64_t a_rs,
                              const void *b, int64_t b_rs, void *o, int64_t o_rs) {
+  evo_pdl_enter();
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -251,6 +260,7 @@ __global__ void mul2d_kernel(int64_t rows, int64_t cols, const void *a, int64_t 
 template <typename T>
 __global__ void trimul_gate_fwd_kernel(int64_t rows, int c, const void *proj, int64_t ldp,
                                        void *a_cf, void *b_cf) {
+  evo_pdl_enter();
   extern __shared__ float t2[];  // [2][c][33]
   const int64_t r0 = blockIdx.x * 32;
   for (int e = threadIdx.x; e < 32 * c; e += blockDim.x) {
@@ -280,6 +290,7 @@ template <typename T>
 __global__ void trimul_gate_bwd_kernel(int64_t rows, int c, const void *proj, int64_t ldp,
                                        const float *da_cf, const float *db_cf, void *dproj,
                                        int64_t ldd, float *part) {
+  evo_pdl_enter();
   extern __shared__ float t2[];  // [2][c][33], then (part) [4c][33] fp32 outputs
   const int64_t r0 = blockIdx.x * 32;
   for (int e = threadIdx.x; e < 32 * c; e += blockDim.x) {
@@ -332,6 +343,7 @@ __global__ void trimul_gate_bwd_kernel(int64_t rows, int c, const void *proj, in
 template <typename T>
 __global__ void outgate_fwd_kernel(int64_t rows, int64_t cols, const float *z, const void *g,
                                    int64_t g_rs, const void *o, int64_t o_rs, float *znew) {
+  evo_pdl_enter();
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -344,6 +356,7 @@ template <typename T>
 __global__ void outgate_bwd_kernel(int64_t rows, int64_t cols, const float *dz, const void *g,
                                    int64_t g_rs, const void *o, int64_t o_rs, void *do_,
                                    int64_t do_rs, void *dgp, int64_t dg_rs) {
+  evo_pdl_enter();
   const int64_t total = rows * cols;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -377,6 +390,7 @@ __device__ __forceinline__ uint4 pack8(const float (&f)[8]) {
 __global__ void outgate_fwd_bf16x8_kernel(int64_t rows, int64_t cols, const float *z,
                                           const bf16 *g, int64_t g_rs, const bf16 *o,
                                           int64_t o_rs, float *znew) {
+  evo_pdl_enter();
   const int64_t per_row = cols / 8, total = rows * per_row;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -397,6 +411,7 @@ __global__ void outgate_bwd_bf16x8_kernel(int64_t rows, int64_t cols, const floa
                                           const bf16 *g, int64_t g_rs, const bf16 *o,
                                           int64_t o_rs, bf16 *do_, int64_t do_rs, bf16 *dgp,
                                           int64_t dg_rs) {
+  evo_pdl_enter();
   const int64_t per_row = cols / 8, total = rows * per_row;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -427,6 +442,7 @@ __global__ void outgate_bwd_colsum_kernel(int64_t rows, int64_t cols, const floa
                                           int64_t o_rs, bf16 *do_, int64_t do_rs, bf16 *dgp,
                                           int64_t dg_rs, int64_t rpb, float *part_do,
                                           float *part_dg) {
+  evo_pdl_enter();
   __shared__ float red[8][32 * 8 + 4];
   const int64_t c0 = (blockIdx.y * 32 + threadIdx.x) * 8;
   const int64_t r0 = blockIdx.x * rpb;
@@ -476,6 +492,7 @@ __global__ void outgate_bwd_colsum_kernel(int64_t rows, int64_t cols, const floa
 // the block's row chunk), so stage 2 is shared.
 __global__ void relu_bwd_colsum_kernel(int64_t rows, int64_t cols, const bf16 *dh, const bf16 *h,
                                        bf16 *dpre, int64_t rpb, float *part) {
+  evo_pdl_enter();
   __shared__ float red[8][32 * 8 + 4];
   const int64_t c0 = (blockIdx.y * 32 + threadIdx.x) * 8;
   const int64_t r0 = blockIdx.x * rpb;
@@ -517,6 +534,7 @@ __global__ void relu_bwd_colsum_kernel(int64_t rows, int64_t cols, const bf16 *d
 }
 
 __global__ void relu_bwd_bf16x8_kernel(int64_t n8, const uint4 *dh, const uint4 *h, uint4 *dpre) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n8;
        e += (int64_t)gridDim.x * blockDim.x) {
     uint4 a = dh[e], b = h[e];
@@ -537,6 +555,7 @@ __global__ void relu_bwd_bf16x8_kernel(int64_t n8, const uint4 *dh, const uint4 
 
 template <typename T>
 __global__ void relu_bwd_kernel(int64_t n, const void *dh, const void *h, void *dpre) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x) {
     float hv = LD<T>(h, e);
@@ -549,6 +568,7 @@ constexpr int SQ_BLOCKS = 512;
 // One pass over x: per-block partial sums of x^2 and (dx != NULL) the
 // gradient dx = (2/n) x of mean(x^2), 16-byte vectors when aligned.
 __global__ void sq_partial_kernel(int64_t n, const float *x, float *part, float *dx) {
+  evo_pdl_enter();
   __shared__ float red[32];
   float s = 0.f;
   const float sc = 2.0f / (float)n;
@@ -579,6 +599,7 @@ __global__ void sq_partial_kernel(int64_t n, const float *x, float *part, float 
 // Fixed-order double-precision sum of the block partials (one 256-thread
 // block: strided per-thread sums, then an ordered tree).
 __global__ void sq_final_kernel(int nblk, int64_t n, const float *part, float *out) {
+  evo_pdl_enter();
   __shared__ double red[256];
   double s = 0.0;
   for (int b = threadIdx.x; b < nblk; b += blockDim.x) s += part[b];
@@ -592,12 +613,14 @@ __global__ void sq_final_kernel(int nblk, int64_t n, const float *part, float *o
 }
 
 __global__ void add_kernel(int64_t n, const float *a, const float *b, float *o) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     o[e] = a[e] + b[e];
 }
 
 __global__ void div_scalar_kernel(int64_t n, const float *x, float d, float *o) {
+  evo_pdl_enter();
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n;
        e += (int64_t)gridDim.x * blockDim.x)
     o[e] = x[e] / d;
@@ -616,15 +639,14 @@ int reduce_lead(int dt, int64_t nb, int64_t n1, int64_t n2, const void *src, flo
   }
   if (dt == EVO_F32 && (n1 == 1 || d_s1 == n2) && d_s2 == 1 && total % 4 == 0 &&
       (reinterpret_cast<uintptr_t>(src) & 15) == 0 && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
-    reduce_lead_vec_kernel<<<ew_blocks(total / 4), 256, 0, st>>>(
-        nb, total / 4, reinterpret_cast<const float4 *>(src), reinterpret_cast<float4 *>(dst), acc);
+    launch_k(reduce_lead_vec_kernel, ew_blocks(total / 4), 256, 0, st, nb, total / 4, reinterpret_cast<const float4 *>(src), reinterpret_cast<float4 *>(dst), acc);
     EVO_LAUNCHED("reduce_lead_vec_kernel");
     return EVO_OK;
   }
   if (dt == EVO_F32)
-    reduce_lead_kernel<float><<<ew_blocks(total), 256, 0, st>>>(nb, n1, n2, src, dst, d_s1, d_s2, acc);
+    launch_k(reduce_lead_kernel<float>, ew_blocks(total), 256, 0, st, nb, n1, n2, src, dst, d_s1, d_s2, acc);
   else
-    reduce_lead_kernel<bf16><<<ew_blocks(total), 256, 0, st>>>(nb, n1, n2, src, dst, d_s1, d_s2, acc);
+    launch_k(reduce_lead_kernel<bf16>, ew_blocks(total), 256, 0, st, nb, n1, n2, src, dst, d_s1, d_s2, acc);
   EVO_LAUNCHED("reduce_lead_kernel");
   return EVO_OK;
 }
@@ -645,15 +667,15 @@ int colsum(int dt, int64_t rows, int64_t cols, const void *src, int64_t rs, floa
   nblk = (rows + rpb - 1) / rpb;
   dim3 grid((unsigned)nblk, (unsigned)col_tiles), blk(32, 8);
   if (vec) {
-    if (dt == EVO_F32) colsum_stage1_vec<float><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
-    else colsum_stage1_vec<bf16><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
+    if (dt == EVO_F32) launch_k(colsum_stage1_vec<float>, grid, blk, 0, st, rows, cols, src, rs, rpb, ws);
+    else launch_k(colsum_stage1_vec<bf16>, grid, blk, 0, st, rows, cols, src, rs, rpb, ws);
     EVO_LAUNCHED("colsum_stage1_vec");
   } else {
-    if (dt == EVO_F32) colsum_stage1<float><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
-    else colsum_stage1<bf16><<<grid, blk, 0, st>>>(rows, cols, src, rs, rpb, ws);
+    if (dt == EVO_F32) launch_k(colsum_stage1<float>, grid, blk, 0, st, rows, cols, src, rs, rpb, ws);
+    else launch_k(colsum_stage1<bf16>, grid, blk, 0, st, rows, cols, src, rs, rpb, ws);
     EVO_LAUNCHED("colsum_stage1");
   }
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, ws, dst, acc);
+  launch_k(colsum_stage2, (unsigned)((cols + 31) / 32), 1024, 0, st, (int)nblk, cols, ws, dst, acc);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
@@ -664,6 +686,7 @@ template <typename TS, typename TD>
 __global__ void copy3d_kernel(int64_t n0, int64_t rows, int64_t cols, const void *src,
                               int64_t s_bs, int64_t s_rs, int64_t s_cs, void *dst, int64_t d_bs,
                               int64_t d_rs, int64_t d_cs) {
+  evo_pdl_enter();
   const int64_t plane = rows * cols, total = n0 * plane;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -679,7 +702,7 @@ int copy3d(int ts, int td, int64_t n0, int64_t rows, int64_t cols, const void *s
   if (total == 0) return EVO_OK;
   const int nb = ew_blocks(total);
 #define C(A, B)                                                                              \
-  copy3d_kernel<A, B><<<nb, 256, 0, st>>>(n0, rows, cols, src, s_bs, s_rs, s_cs, dst, d_bs, d_rs, \
+  launch_k(copy3d_kernel<A, B>, nb, 256, 0, st, n0, rows, cols, src, s_bs, s_rs, s_cs, dst, d_bs, d_rs, \
                                           d_cs)
   if (ts == EVO_F32) { if (td == EVO_F32) C(float, float); else C(float, bf16); }
   else { if (td == EVO_F32) C(bf16, float); else C(bf16, bf16); }
@@ -695,7 +718,7 @@ int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t 
   if (s_cs == 1 && d_rs == 1 && d_cs != 1 && rows >= 32 && cols >= 32) {
     dim3 grid((unsigned)((cols + 31) / 32), (unsigned)((rows + 31) / 32));
     dim3 blk(32, 8);
-#define T(A, B) transpose_kernel<A, B><<<grid, blk, 0, st>>>(rows, cols, src, s_rs, dst, d_cs)
+#define T(A, B) launch_k(transpose_kernel<A, B>, grid, blk, 0, st, rows, cols, src, s_rs, dst, d_cs)
     if (ts == EVO_F32) { if (td == EVO_F32) T(float, float); else T(float, bf16); }
     else { if (td == EVO_F32) T(bf16, float); else T(bf16, bf16); }
 #undef T
@@ -706,7 +729,7 @@ int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t 
   if (s_cs == 1 && d_cs == 1 && cols % 8 == 0 && s_rs % 8 == 0 && d_rs % 8 == 0 && al16(src) &&
       al16(dst)) {
     int nb = ew_blocks(total / 8);
-#define CV(A, B) copy2d_vec_kernel<A, B><<<nb, 256, 0, st>>>(rows, cols, src, s_rs, dst, d_rs)
+#define CV(A, B) launch_k(copy2d_vec_kernel<A, B>, nb, 256, 0, st, rows, cols, src, s_rs, dst, d_rs)
     if (ts == EVO_F32) { if (td == EVO_F32) CV(float, float); else CV(float, bf16); }
     else { if (td == EVO_F32) CV(bf16, float); else CV(bf16, bf16); }
 #undef CV
@@ -714,7 +737,7 @@ int copy2d(int ts, int td, int64_t rows, int64_t cols, const void *src, int64_t 
     return EVO_OK;
   }
   int nb = ew_blocks(total);
-#define C(A, B) copy2d_kernel<A, B><<<nb, 256, 0, st>>>(rows, cols, src, s_rs, s_cs, dst, d_rs, d_cs)
+#define C(A, B) launch_k(copy2d_kernel<A, B>, nb, 256, 0, st, rows, cols, src, s_rs, s_cs, dst, d_rs, d_cs)
   if (ts == EVO_F32) { if (td == EVO_F32) C(float, float); else C(float, bf16); }
   else { if (td == EVO_F32) C(bf16, float); else C(bf16, bf16); }
 #undef C
@@ -727,7 +750,7 @@ int mul2d(int ta, int tb, int to, int64_t rows, int64_t cols, const void *a, int
   int64_t total = rows * cols;
   if (total == 0) return EVO_OK;
   int nb = ew_blocks(total);
-#define M3(A, B, O) mul2d_kernel<A, B, O><<<nb, 256, 0, st>>>(rows, cols, a, a_rs, b, b_rs, o, o_rs)
+#define M3(A, B, O) launch_k(mul2d_kernel<A, B, O>, nb, 256, 0, st, rows, cols, a, a_rs, b, b_rs, o, o_rs)
   if (ta == EVO_F32 && tb == EVO_F32 && to == EVO_F32) M3(float, float, float);
   else if (ta == EVO_BF16 && tb == EVO_BF16 && to == EVO_BF16) M3(bf16, bf16, bf16);
   else if (ta == EVO_BF16 && tb == EVO_BF16 && to == EVO_F32) M3(bf16, bf16, float);
@@ -744,9 +767,9 @@ int trimul_gate_fwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, 
   unsigned nb = (unsigned)((rows + 31) / 32);
   size_t smem = (size_t)2 * c * 33 * sizeof(float);
   if (dt == EVO_F32)
-    trimul_gate_fwd_kernel<float><<<nb, 256, smem, st>>>(rows, c, proj, ldp, a_cf, b_cf);
+    launch_k(trimul_gate_fwd_kernel<float>, nb, 256, smem, st, rows, c, proj, ldp, a_cf, b_cf);
   else
-    trimul_gate_fwd_kernel<bf16><<<nb, 256, smem, st>>>(rows, c, proj, ldp, a_cf, b_cf);
+    launch_k(trimul_gate_fwd_kernel<bf16>, nb, 256, smem, st, rows, c, proj, ldp, a_cf, b_cf);
   EVO_LAUNCHED("trimul_gate_fwd_kernel");
   return EVO_OK;
 }
@@ -758,14 +781,14 @@ int trimul_gate_bwd(int dt, int64_t rows, int c, const void *proj, int64_t ldp, 
   size_t smem = (size_t)(colsum ? 6 : 2) * c * 33 * sizeof(float);
   float *part = colsum ? ws : nullptr;
   if (dt == EVO_F32)
-    trimul_gate_bwd_kernel<float><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd,
+    launch_k(trimul_gate_bwd_kernel<float>, nb, 256, smem, st, rows, c, proj, ldp, da, db, dproj, ldd,
                                                          part);
   else
-    trimul_gate_bwd_kernel<bf16><<<nb, 256, smem, st>>>(rows, c, proj, ldp, da, db, dproj, ldd,
+    launch_k(trimul_gate_bwd_kernel<bf16>, nb, 256, smem, st, rows, c, proj, ldp, da, db, dproj, ldd,
                                                         part);
   EVO_LAUNCHED("trimul_gate_bwd_kernel");
   if (colsum) {
-    colsum_stage2<<<(unsigned)((4 * c + 31) / 32), 1024, 0, st>>>((int)nb, 4 * c, part, colsum, 0);
+    launch_k(colsum_stage2, (unsigned)((4 * c + 31) / 32), 1024, 0, st, (int)nb, 4 * c, part, colsum, 0);
     EVO_LAUNCHED("colsum_stage2");
   }
   return EVO_OK;
@@ -781,14 +804,13 @@ int outgate_fwd(int dt, int64_t rows, int64_t cols, const float *z, const void *
   auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (dt == EVO_BF16 && cols % 8 == 0 && g_rs % 8 == 0 && o_rs % 8 == 0 && al16(z) && al16(g) &&
       al16(o) && al16(znew)) {
-    outgate_fwd_bf16x8_kernel<<<ew_blocks(rows * cols / 8), 256, 0, st>>>(
-        rows, cols, z, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
+    launch_k(outgate_fwd_bf16x8_kernel, ew_blocks(rows * cols / 8), 256, 0, st, rows, cols, z, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
         o_rs, znew);
     EVO_LAUNCHED("outgate_fwd_bf16x8_kernel");
     return EVO_OK;
   }
-  if (dt == EVO_F32) outgate_fwd_kernel<float><<<nb, 256, 0, st>>>(rows, cols, z, g, g_rs, o, o_rs, znew);
-  else outgate_fwd_kernel<bf16><<<nb, 256, 0, st>>>(rows, cols, z, g, g_rs, o, o_rs, znew);
+  if (dt == EVO_F32) launch_k(outgate_fwd_kernel<float>, nb, 256, 0, st, rows, cols, z, g, g_rs, o, o_rs, znew);
+  else launch_k(outgate_fwd_kernel<bf16>, nb, 256, 0, st, rows, cols, z, g, g_rs, o, o_rs, znew);
   EVO_LAUNCHED("outgate_fwd_kernel");
   return EVO_OK;
 }
@@ -822,29 +844,27 @@ int outgate_bwd(int dt, int64_t rows, int64_t cols, const float *dz, const void 
     const int64_t nblk = outgate_colsum_blocks(rows, cols, rpb);
     const int64_t col_tiles = (cols + 255) / 256;
     float *pdo = ws, *pdg = ws + nblk * cols;
-    outgate_bwd_colsum_kernel<<<dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st>>>(
-        rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
+    launch_k(outgate_bwd_colsum_kernel, dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st, rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs, reinterpret_cast<const bf16 *>(o),
         o_rs, reinterpret_cast<bf16 *>(do_), do_rs, reinterpret_cast<bf16 *>(dgp), dg_rs, rpb, pdo,
         pdg);
     EVO_LAUNCHED("outgate_bwd_colsum_kernel");
-    colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, pdo, do_colsum, 0);
+    launch_k(colsum_stage2, (unsigned)((cols + 31) / 32), 1024, 0, st, (int)nblk, cols, pdo, do_colsum, 0);
     EVO_LAUNCHED("colsum_stage2");
-    colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, pdg, dg_colsum, 0);
+    launch_k(colsum_stage2, (unsigned)((cols + 31) / 32), 1024, 0, st, (int)nblk, cols, pdg, dg_colsum, 0);
     EVO_LAUNCHED("colsum_stage2");
     return EVO_OK;
   }
   if (vec) {
-    outgate_bwd_bf16x8_kernel<<<ew_blocks(rows * cols / 8), 256, 0, st>>>(
-        rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs,
+    launch_k(outgate_bwd_bf16x8_kernel, ew_blocks(rows * cols / 8), 256, 0, st, rows, cols, dz, reinterpret_cast<const bf16 *>(g), g_rs,
         reinterpret_cast<const bf16 *>(o), o_rs, reinterpret_cast<bf16 *>(do_), do_rs,
         reinterpret_cast<bf16 *>(dgp), dg_rs);
     EVO_LAUNCHED("outgate_bwd_bf16x8_kernel");
     return EVO_OK;
   }
   if (dt == EVO_F32)
-    outgate_bwd_kernel<float><<<nb, 256, 0, st>>>(rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgp, dg_rs);
+    launch_k(outgate_bwd_kernel<float>, nb, 256, 0, st, rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgp, dg_rs);
   else
-    outgate_bwd_kernel<bf16><<<nb, 256, 0, st>>>(rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgp, dg_rs);
+    launch_k(outgate_bwd_kernel<bf16>, nb, 256, 0, st, rows, cols, dz, g, g_rs, o, o_rs, do_, do_rs, dgp, dg_rs);
   EVO_LAUNCHED("outgate_bwd_kernel");
   return EVO_OK;
 }
@@ -852,15 +872,14 @@ int outgate_bwd(int dt, int64_t rows, int64_t cols, const float *dz, const void 
 int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaStream_t st) {
   auto al16 = [](const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
   if (dt == EVO_BF16 && n % 8 == 0 && al16(dh) && al16(h) && al16(dpre)) {
-    relu_bwd_bf16x8_kernel<<<ew_blocks(n / 8), 256, 0, st>>>(
-        n / 8, reinterpret_cast<const uint4 *>(dh), reinterpret_cast<const uint4 *>(h),
+    launch_k(relu_bwd_bf16x8_kernel, ew_blocks(n / 8), 256, 0, st, n / 8, reinterpret_cast<const uint4 *>(dh), reinterpret_cast<const uint4 *>(h),
         reinterpret_cast<uint4 *>(dpre));
     EVO_LAUNCHED("relu_bwd_bf16x8_kernel");
     return EVO_OK;
   }
   int nb = ew_blocks(n);
-  if (dt == EVO_F32) relu_bwd_kernel<float><<<nb, 256, 0, st>>>(n, dh, h, dpre);
-  else relu_bwd_kernel<bf16><<<nb, 256, 0, st>>>(n, dh, h, dpre);
+  if (dt == EVO_F32) launch_k(relu_bwd_kernel<float>, nb, 256, 0, st, n, dh, h, dpre);
+  else launch_k(relu_bwd_kernel<bf16>, nb, 256, 0, st, n, dh, h, dpre);
   EVO_LAUNCHED("relu_bwd_kernel");
   return EVO_OK;
 }
@@ -868,7 +887,7 @@ int relu_bwd(int dt, int64_t n, const void *dh, const void *h, void *dpre, cudaS
 // Ordered column sums of [nblk, cols] fp32 partials (coalesced stage 2).
 int colsum_partials(int nblk, int64_t cols, const float *part, float *dst, int acc,
                     cudaStream_t st) {
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>(nblk, cols, part, dst, acc);
+  launch_k(colsum_stage2, (unsigned)((cols + 31) / 32), 1024, 0, st, nblk, cols, part, dst, acc);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
@@ -885,20 +904,19 @@ int relu_bwd_colsum(int64_t rows, int64_t cols, const void *dh, const void *h, v
   nblk = std::min<int64_t>(nblk, std::max<int64_t>(1, rows / 64));
   const int64_t rpb = (rows + nblk - 1) / nblk;
   nblk = (rows + rpb - 1) / rpb;
-  relu_bwd_colsum_kernel<<<dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st>>>(
-      rows, cols, reinterpret_cast<const bf16 *>(dh), reinterpret_cast<const bf16 *>(h),
+  launch_k(relu_bwd_colsum_kernel, dim3((unsigned)nblk, (unsigned)col_tiles), dim3(32, 8), 0, st, rows, cols, reinterpret_cast<const bf16 *>(dh), reinterpret_cast<const bf16 *>(h),
       reinterpret_cast<bf16 *>(dpre), rpb, ws);
   EVO_LAUNCHED("relu_bwd_colsum_kernel");
-  colsum_stage2<<<(unsigned)((cols + 31) / 32), 1024, 0, st>>>((int)nblk, cols, ws, dst, 0);
+  launch_k(colsum_stage2, (unsigned)((cols + 31) / 32), 1024, 0, st, (int)nblk, cols, ws, dst, 0);
   EVO_LAUNCHED("colsum_stage2");
   return EVO_OK;
 }
 
 int sq_mean(int64_t n, const float *x, float *out, float *dx, void *ws, cudaStream_t st) {
   float *part = reinterpret_cast<float *>(ws);
-  sq_partial_kernel<<<SQ_BLOCKS, 256, 0, st>>>(n, x, part, dx);
+  launch_k(sq_partial_kernel, SQ_BLOCKS, 256, 0, st, n, x, part, dx);
   EVO_LAUNCHED("sq_partial_kernel");
-  sq_final_kernel<<<1, 256, 0, st>>>(SQ_BLOCKS, n, part, out);
+  launch_k(sq_final_kernel, 1, 256, 0, st, SQ_BLOCKS, n, part, out);
   EVO_LAUNCHED("sq_final_kernel");
   return EVO_OK;
 }
@@ -910,6 +928,7 @@ __global__ void split_bf16_kernel(int64_t rows, int64_t cols, const float *__res
                                   int64_t x_rs, bf16 *__restrict__ hi, int64_t h_rs,
                                   bf16 *__restrict__ lo, int64_t l_rs, bf16 *__restrict__ hi2,
                                   int64_t h2_rs) {
+  evo_pdl_enter();
   const int64_t c4 = (cols + 3) / 4;
   const int64_t total = rows * c4;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
@@ -931,21 +950,20 @@ __global__ void split_bf16_kernel(int64_t rows, int64_t cols, const float *__res
 
 int split_bf16(int64_t rows, int64_t cols, const float *x, int64_t x_rs, void *hi, int64_t h_rs,
                void *lo, int64_t l_rs, void *hi2, int64_t h2_rs, cudaStream_t st) {
-  split_bf16_kernel<<<ew_blocks(rows * ((cols + 3) / 4)), 256, 0, st>>>(
-      rows, cols, x, x_rs, reinterpret_cast<bf16 *>(hi), h_rs, reinterpret_cast<bf16 *>(lo), l_rs,
+  launch_k(split_bf16_kernel, ew_blocks(rows * ((cols + 3) / 4)), 256, 0, st, rows, cols, x, x_rs, reinterpret_cast<bf16 *>(hi), h_rs, reinterpret_cast<bf16 *>(lo), l_rs,
       reinterpret_cast<bf16 *>(hi2), h2_rs);
   EVO_LAUNCHED("split_bf16_kernel");
   return EVO_OK;
 }
 
 int div_scalar(int64_t n, const float *x, float d, float *o, cudaStream_t st) {
-  div_scalar_kernel<<<ew_blocks(n), 256, 0, st>>>(n, x, d, o);
+  launch_k(div_scalar_kernel, ew_blocks(n), 256, 0, st, n, x, d, o);
   EVO_LAUNCHED("div_scalar_kernel");
   return EVO_OK;
 }
 
 int add(int64_t n, const float *a, const float *b, float *o, cudaStream_t st) {
-  add_kernel<<<ew_blocks(n), 256, 0, st>>>(n, a, b, o);
+  launch_k(add_kernel, ew_blocks(n), 256, 0, st, n, a, b, o);
   EVO_LAUNCHED("add_kernel");
   return EVO_OK;
 }

@@ -48,6 +48,7 @@ __device__ __forceinline__ void epilogue_store(const SimtArgs &a, int64_t m, int
 
 template <typename TA, typename TC>
 __global__ void __launch_bounds__(NT) gemm_simt_kernel(SimtArgs a) {
+  evo_pdl_enter();
   __shared__ float As[BK][BM + 4];
   __shared__ float Bs[BK][BN + 4];
   const int t = threadIdx.x;
@@ -160,6 +161,7 @@ template <int P>
 __global__ void __launch_bounds__(256) splitk_reduce_kernel(EpiArgs e, int64_t M, int64_t N,
                                                             int64_t B2, int64_t nbatch, int split,
                                                             const float *partial) {
+  evo_pdl_enter();
   constexpr int G = 256 / P;
   __shared__ float red[G][P + 1];
   const int o = threadIdx.x % P, grp = threadIdx.x / P;
@@ -191,6 +193,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_vec_kernel(EpiArgs e, int64
                                                                 int64_t B2, int64_t nbatch,
                                                                 int split,
                                                                 const float *__restrict__ partial) {
+  evo_pdl_enter();
   const int64_t total = nbatch * M * N;
   const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   const int64_t idx = 4 * q;
@@ -218,14 +221,11 @@ int gemm_splitk_reduce(const evo_gemm_desc *d, int split, const float *partial,
   const int64_t total = d->B1 * d->B2 * d->M * d->N;
   EVO_REQUIRE((total + 31) / 32 < (1ll << 31), EVO_EDIM, "evo_gemm: split-K output too large");
   if (split <= 32 && d->N % 4 == 0 && (reinterpret_cast<uintptr_t>(partial) & 15) == 0) {
-    splitk_reduce_vec_kernel<<<(unsigned)((total / 4 + 255) / 256), 256, 0, st>>>(
-        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+    launch_k(splitk_reduce_vec_kernel, (unsigned)((total / 4 + 255) / 256), 256, 0, st, epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
   } else if (total / 32 < 2 * (int64_t)num_sms() && split > 32) {
-    splitk_reduce_kernel<8><<<(unsigned)((total + 7) / 8), 256, 0, st>>>(
-        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+    launch_k(splitk_reduce_kernel<8>, (unsigned)((total + 7) / 8), 256, 0, st, epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
   } else {
-    splitk_reduce_kernel<32><<<(unsigned)((total + 31) / 32), 256, 0, st>>>(
-        epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
+    launch_k(splitk_reduce_kernel<32>, (unsigned)((total + 31) / 32), 256, 0, st, epi_args_of(d), d->M, d->N, d->B2, d->B1 * d->B2, split, partial);
   }
   EVO_LAUNCHED("splitk_reduce_kernel");
   return EVO_OK;
@@ -259,7 +259,7 @@ int gemm_simt(const evo_gemm_desc *d, cudaStream_t st) {
     split = 1;
   }
 #define LAUNCH(TA, TCT)                                                        \
-  gemm_simt_kernel<TA, TCT><<<grid, NT, 0, st>>>(a);                          \
+  launch_k(gemm_simt_kernel<TA, TCT>, grid, NT, 0, st, a);                          \
   EVO_LAUNCHED("gemm_simt_kernel");                                           \
   if (split > 1) return gemm_splitk_reduce(d, split, a.partial, st);
   if (d->dtype_ab == EVO_F32) {

@@ -42,6 +42,7 @@ struct SkArgs {
 // One thread per output row; B staged in smem as fp32 [K][16].
 template <typename T, int NMAX>
 __global__ void __launch_bounds__(256) skinny_rowdot_kernel(const SkArgs a) {
+  evo_pdl_enter();
   extern __shared__ float sB[];  // [K][NMAX]
   const T *A = reinterpret_cast<const T *>(a.A);
   const T *B = reinterpret_cast<const T *>(a.B);
@@ -95,6 +96,7 @@ __global__ void __launch_bounds__(256) skinny_rowdot_kernel(const SkArgs a) {
 // fully coalesced 512-byte warp store.
 template <typename T, int KK, bool NREG>
 __global__ void __launch_bounds__(256) skinny_expand_kernel(const SkArgs a) {
+  evo_pdl_enter();
   extern __shared__ float sB[];  // [KK][Np], Np = N rounded up to 4
   const T *A = reinterpret_cast<const T *>(a.A);
   const T *B = reinterpret_cast<const T *>(a.B);
@@ -191,6 +193,7 @@ constexpr int TK_SLAB = 64;
 
 template <typename T, int NN>
 __global__ void __launch_bounds__(256) skinny_tallk_kernel(const SkArgs a, int wide_is_m) {
+  evo_pdl_enter();
   extern __shared__ float sm[];
   float *sN = sm;  // [TK_SLAB][NN]
   const int W = (int)(wide_is_m ? a.M : a.N), Nn = (int)(wide_is_m ? a.N : a.M);
@@ -278,6 +281,7 @@ struct BulkPlan {
 template <typename T, int NN>
 __global__ void __launch_bounds__(256) skinny_tallk_bulk_kernel(const SkArgs a, int wide_is_m,
                                                                 BulkPlan pl) {
+  evo_pdl_enter();
   extern __shared__ __align__(128) uint8_t smem_raw[];
   constexpr int E = sizeof(T);
   const int W = (int)(wide_is_m ? a.M : a.N), Nn = (int)(wide_is_m ? a.N : a.M);
@@ -481,9 +485,9 @@ int run(const evo_gemm_desc *d, Kind kind, cudaStream_t st) {
     EVO_MAX_SMEM_ONCE((skinny_rowdot_kernel<T, 8>));
     const int blocks = (int)std::min<int64_t>((d->M + 255) / 256, (int64_t)num_sms() * 4);
     if (d->N <= 8) {
-      skinny_rowdot_kernel<T, 8><<<blocks, 256, (size_t)d->K * 8 * sizeof(float), st>>>(a);
+      launch_k(skinny_rowdot_kernel<T, 8>, blocks, 256, (size_t)d->K * 8 * sizeof(float), st, a);
     } else {
-      skinny_rowdot_kernel<T, 16><<<blocks, 256, smem, st>>>(a);
+      launch_k(skinny_rowdot_kernel<T, 16>, blocks, 256, smem, st, a);
     }
     EVO_LAUNCHED("skinny_rowdot_kernel");
     return EVO_OK;
@@ -496,7 +500,7 @@ int run(const evo_gemm_desc *d, Kind kind, cudaStream_t st) {
     const bool nreg = d->N <= 128;
 #define EXPAND(KK, NR)                                                   \
   EVO_MAX_SMEM_ONCE((skinny_expand_kernel<T, KK, NR>));                  \
-  skinny_expand_kernel<T, KK, NR><<<blocks, 256, smem, st>>>(a);
+  launch_k(skinny_expand_kernel<T, KK, NR>, blocks, 256, smem, st, a);
     if (kk == 8) {
       if (nreg) { EXPAND(8, true) } else { EXPAND(8, false) }
     } else {
@@ -523,21 +527,21 @@ int run(const evo_gemm_desc *d, Kind kind, cudaStream_t st) {
     EVO_MAX_SMEM_ONCE((skinny_tallk_bulk_kernel<T, 16>));
     EVO_MAX_SMEM_ONCE((skinny_tallk_bulk_kernel<T, 32>));
     if (Nn <= 8)
-      skinny_tallk_bulk_kernel<T, 8><<<grid, 256, pl.smem, st>>>(a, wm ? 1 : 0, pl);
+      launch_k(skinny_tallk_bulk_kernel<T, 8>, grid, 256, pl.smem, st, a, wm ? 1 : 0, pl);
     else if (Nn <= 16)
-      skinny_tallk_bulk_kernel<T, 16><<<grid, 256, pl.smem, st>>>(a, wm ? 1 : 0, pl);
+      launch_k(skinny_tallk_bulk_kernel<T, 16>, grid, 256, pl.smem, st, a, wm ? 1 : 0, pl);
     else
-      skinny_tallk_bulk_kernel<T, 32><<<grid, 256, pl.smem, st>>>(a, wm ? 1 : 0, pl);
+      launch_k(skinny_tallk_bulk_kernel<T, 32>, grid, 256, pl.smem, st, a, wm ? 1 : 0, pl);
     EVO_LAUNCHED("skinny_tallk_bulk_kernel");
     return gemm_splitk_reduce(d, g, a.partial, st);
   }
   const size_t smem = (size_t)256 * 32 * sizeof(float);  // >= slab and k-group combine
   if (Nn <= 8) {
-    skinny_tallk_kernel<T, 8><<<grid, 256, smem, st>>>(a, wm ? 1 : 0);
+    launch_k(skinny_tallk_kernel<T, 8>, grid, 256, smem, st, a, wm ? 1 : 0);
   } else if (Nn <= 16) {
-    skinny_tallk_kernel<T, 16><<<grid, 256, smem, st>>>(a, wm ? 1 : 0);
+    launch_k(skinny_tallk_kernel<T, 16>, grid, 256, smem, st, a, wm ? 1 : 0);
   } else {
-    skinny_tallk_kernel<T, 32><<<grid, 256, smem, st>>>(a, wm ? 1 : 0);
+    launch_k(skinny_tallk_kernel<T, 32>, grid, 256, smem, st, a, wm ? 1 : 0);
   }
   EVO_LAUNCHED("skinny_tallk_kernel");
   return gemm_splitk_reduce(d, g, a.partial, st);

@@ -251,6 +251,7 @@ __global__ void __launch_bounds__(NTHREADS, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmC, const __grid_constant__ CUtensorMap tmR,
                const TcParams p) {
+  evo_pdl_enter();
   constexpr int SMEM_B = BN * BK * 2;
   constexpr uint32_t STAGE_BYTES = SMEM_A + SMEM_B;
   constexpr uint32_t TMEM_COLS = 2 * BN;  // double-buffered accumulator
@@ -918,7 +919,7 @@ int launch(const evo_gemm_desc *d, cudaStream_t st) {
   }
   int64_t grid = std::min<int64_t>(p.num_tiles, (int64_t)num_sms());
   if (!p.res_tma) mr = mc;  // unused
-  gemm_tc_kernel<BN, STAGES, EPI><<<(unsigned)grid, NTHREADS, smem, st>>>(ma, mb, mc, mr, p);
+  launch_k(gemm_tc_kernel<BN, STAGES, EPI>, (unsigned)grid, NTHREADS, smem, st, ma, mb, mc, mr, p);
   EVO_LAUNCHED("gemm_tc_kernel");
   if (p.split > 1) return gemm_splitk_reduce(d, p.split, p.partial, st);
   return EVO_OK;

@@ -51,6 +51,7 @@ ln_fwd_vec_kernel(int64_t rows, const TX *__restrict__ x, int64_t x_rs,
                   const float *__restrict__ gamma, const float *__restrict__ beta,
                   TY *__restrict__ y, int64_t y_rs, float *__restrict__ mean_out,
                   float *__restrict__ rstd_out, float eps) {
+  evo_pdl_enter();
   // RPW rows per warp, all loads issued before the first reduction
   constexpr int cols = NV * 128, RPW = 4;
   const int lane = threadIdx.x & 31;
@@ -132,6 +133,7 @@ __global__ void __launch_bounds__(LN_WARPS * 32)
 ln_fwd_kernel(int64_t rows, int cols, const TX *__restrict__ x, int64_t x_rs, int64_t x_cs,
               const float *__restrict__ gamma, const float *__restrict__ beta, TY *__restrict__ y,
               int64_t y_rs, float *__restrict__ mean_out, float *__restrict__ rstd_out, float eps) {
+  evo_pdl_enter();
   const int lane = threadIdx.x & 31;
   const int64_t row = (int64_t)blockIdx.x * LN_WARPS + (threadIdx.x >> 5);
   if (row >= rows) return;
@@ -173,6 +175,7 @@ ln_bwd_vec_kernel(int64_t rows, const TDY *__restrict__ dy, int64_t dy_rs,
                   const float *__restrict__ dres, TDX *__restrict__ dx, int64_t dx_rs,
                   bf16 *__restrict__ dxa, int64_t dxa_rs, float *__restrict__ partial,
                   int nparts) {
+  evo_pdl_enter();
   // partial[block][0..nparts)[cols]: dgamma, dbeta, and (nparts == 3) the
   // column sums of dx itself (the next consumer's bias gradient)
   constexpr int cols = NV * 128;
@@ -288,6 +291,7 @@ ln_bwd_proj_kernel(int64_t rows, const float *__restrict__ dy, const float *__re
                    const float *__restrict__ dres, const float *__restrict__ dproj, int64_t p_rs,
                    const bf16 *__restrict__ Wp, int nh, float *__restrict__ dx,
                    bf16 *__restrict__ dxa, float *__restrict__ partial) {
+  evo_pdl_enter();
   constexpr int cols = 128, NP = 3 + NH;
   __shared__ float red[LN_WARPS][NP][cols];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -402,6 +406,7 @@ ln_bwd_tma_kernel(int64_t rows, const float *__restrict__ dy, const float *__res
                   const float *__restrict__ dres, const float *__restrict__ dproj, int64_t p_rs,
                   const bf16 *__restrict__ Wp, int nh, float *__restrict__ dx,
                   bf16 *__restrict__ dxa, float *__restrict__ partial, int nparts) {
+  evo_pdl_enter();
   using Lay = LntLayout<NV, NH>;
   constexpr int LNT_CW = Lay::CW, LNT_NS = Lay::NS;
   constexpr int cols = Lay::cols, RCH = Lay::RCH;
@@ -645,6 +650,7 @@ __global__ void __launch_bounds__((LNF_CW + 1) * 32, 1)
 ln_fwd_tma_kernel(int64_t rows, const float *__restrict__ x, const float *__restrict__ gamma,
                   const float *__restrict__ beta, TY *__restrict__ y, float *__restrict__ mean_out,
                   float *__restrict__ rstd_out, float eps) {
+  evo_pdl_enter();
   using Lay = LnfLayout<NV>;
   constexpr int cols = Lay::cols, RCH = Lay::RCH, NI = 4 * NV;
   static_assert(!SPLIT || std::is_same<TY, bf16>::value, "split output is bf16");
@@ -753,7 +759,7 @@ int ln_fwd_tma_launch(int64_t rows, const float *x, const float *gamma, const fl
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(num_sms(), nchunks));
   auto kfn = ln_fwd_tma_kernel<NV, SPLIT, TY>;
   EVO_MAX_SMEM_ONCE(kfn);
-  kfn<<<nb, (LNF_CW + 1) * 32, Lay::SMEM, st>>>(rows, x, gamma, beta, y, mean, rstd, eps);
+  launch_k(kfn, nb, (LNF_CW + 1) * 32, Lay::SMEM, st, rows, x, gamma, beta, y, mean, rstd, eps);
   EVO_LAUNCHED("ln_fwd_tma_kernel");
   return EVO_OK;
 }
@@ -768,6 +774,7 @@ ln_fwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ x,
                  const float *__restrict__ gamma, const float *__restrict__ beta,
                  TY *__restrict__ y, int64_t y_rs, float *__restrict__ mean_out,
                  float *__restrict__ rstd_out, float eps) {
+  evo_pdl_enter();
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
   if (row >= rows) return;
   float v[C];
@@ -820,6 +827,7 @@ ln_bwd_cf_kernel(int64_t rows, int cols, const float *__restrict__ dy, int64_t d
                  const float *__restrict__ x, const float *__restrict__ mean,
                  const float *__restrict__ rstd, const float *__restrict__ gamma,
                  TDX *__restrict__ dx, float *__restrict__ partial) {
+  evo_pdl_enter();
   __shared__ float wred[4][2 * C];
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t row = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -902,6 +910,7 @@ ln_bwd_kernel(int64_t rows, int cols, const TDY *__restrict__ dy, int64_t dy_rs,
               const float *__restrict__ rstd, const float *__restrict__ gamma,
               const float *__restrict__ dres, TDX *__restrict__ dx, int64_t dx_rs, int64_t dx_cs,
               float *__restrict__ partial /* [gridDim.x][2][cols] */, int want_params) {
+  evo_pdl_enter();
   extern __shared__ float red[];  // [LN_WARPS][2][cols]
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   float pg[V], pb[V], g[V];
@@ -977,6 +986,7 @@ __global__ void __launch_bounds__(1024) ln_param_reduce_kernel(int nblk, int col
                                                               int accumulate,
                                                               float *__restrict__ dWp = nullptr,
                                                               int nh = 0) {
+  evo_pdl_enter();
   __shared__ float red[32][33];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int width = nparts * cols;
@@ -1013,8 +1023,7 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   TY *yp = reinterpret_cast<TY *>(y);
   if constexpr (std::is_same<TX, float>::value) {
     if (x_rs == 1 && x_cs == rows && cols <= 32) {  // channel-first
-      ln_fwd_cf_kernel<32, TY><<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(
-          rows, cols, xp, gamma, beta, yp, y_rs, mean, rstd, eps);
+      launch_k(ln_fwd_cf_kernel<32, TY>, (unsigned)((rows + 127) / 128), 128, 0, st, rows, cols, xp, gamma, beta, yp, y_rs, mean, rstd, eps);
       EVO_LAUNCHED("ln_fwd_cf_kernel");
       return EVO_OK;
     }
@@ -1031,16 +1040,16 @@ int ln_fwd_launch(int64_t rows, int cols, const void *x, int64_t x_rs, int64_t x
   if (vec) {
     dim3 vgrid((unsigned)((rows + 4 * LN_WARPS - 1) / (4 * LN_WARPS)));  // 4 rows per warp
     if (cols == 128)
-      ln_fwd_vec_kernel<TX, TY, 1><<<vgrid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+      launch_k(ln_fwd_vec_kernel<TX, TY, 1>, vgrid, LN_WARPS * 32, 0, st, rows, xp, x_rs, gamma, beta, yp,
                                                                    y_rs, mean, rstd, eps);
     else
-      ln_fwd_vec_kernel<TX, TY, 2><<<vgrid, LN_WARPS * 32, 0, st>>>(rows, xp, x_rs, gamma, beta, yp,
+      launch_k(ln_fwd_vec_kernel<TX, TY, 2>, vgrid, LN_WARPS * 32, 0, st, rows, xp, x_rs, gamma, beta, yp,
                                                                    y_rs, mean, rstd, eps);
     EVO_LAUNCHED("ln_fwd_vec_kernel");
     return EVO_OK;
   }
 #define L(Vn)                                                                                \
-  ln_fwd_kernel<TX, TY, Vn><<<grid, LN_WARPS * 32, 0, st>>>(rows, cols, xp, x_rs, x_cs, gamma, \
+  launch_k(ln_fwd_kernel<TX, TY, Vn>, grid, LN_WARPS * 32, 0, st, rows, cols, xp, x_rs, x_cs, gamma, \
                                                             beta, yp, y_rs, mean, rstd, eps)
   if (cols <= 32) L(1);
   else if (cols <= 64) L(2);
@@ -1065,7 +1074,7 @@ int ln_bwd_tma_launch(int64_t rows, int cols, const float *dy, const float *x, c
   do {                                                                                      \
     auto kfn = ln_bwd_tma_kernel<NV_, NH_>;                                                 \
     EVO_MAX_SMEM_ONCE(kfn);                                                                 \
-    kfn<<<nb, (LntLayout<NV_, NH_>::CW + 1) * 32, LntLayout<NV_, NH_>::SMEM, st>>>(                          \
+    launch_k(kfn, nb, (LntLayout<NV_, NH_>::CW + 1) * 32, LntLayout<NV_, NH_>::SMEM, st, \
         rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs, Wp, nh, dx, dxa, ws, nparts); \
   } while (0)
   if (dproj) LT(1, 8);
@@ -1100,12 +1109,13 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
       const int nb = (int)((rows + 127) / 128);
       EVO_REQUIRE(!want || nb * 2 <= LN_BWD_BLOCKS * 11, EVO_EUNSUP,
                   "layernorm_bwd: channel-first rows=%lld exceed the workspace", (long long)rows);
-      ln_bwd_cf_kernel<32, TDX><<<nb, 128, 0, st>>>(rows, cols, dyp, dy_rs, xp, mean, rstd, gamma,
+      launch_k(ln_bwd_cf_kernel<32, TDX>, nb, 128, 0, st, rows, cols, dyp, dy_rs, xp, mean, rstd, gamma,
                                                   dxp, ws);
       EVO_LAUNCHED("ln_bwd_cf_kernel");
       if (want) {
-        ln_param_reduce_kernel<<<(2 * cols + 31) / 32, 1024, 0, st>>>(nb, cols, 2, ws, dgamma,
-                                                                     dbeta, nullptr, acc);
+        launch_k(ln_param_reduce_kernel, (2 * cols + 31) / 32, 1024, 0, st, nb, cols, 2, ws, dgamma,
+                                                                     dbeta, nullptr, acc,
+                                                                     nullptr, 0);
         EVO_LAUNCHED("ln_param_reduce_kernel");
       }
       return EVO_OK;
@@ -1122,9 +1132,9 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
                                        reinterpret_cast<bf16 *>(dx_act), ws, nparts, st, &nb);
       if (rc != EVO_OK) return rc;
       if (want) {
-        ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(nb, cols, nparts, ws,
+        launch_k(ln_param_reduce_kernel, (nparts * cols + 31) / 32, 1024, 0, st, nb, cols, nparts, ws,
                                                                           dgamma, dbeta,
-                                                                          dx_colsum, acc);
+                                                                          dx_colsum, acc, nullptr, 0);
         EVO_LAUNCHED("ln_param_reduce_kernel");
       }
       return EVO_OK;
@@ -1134,18 +1144,16 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
     bf16 *dxa = reinterpret_cast<bf16 *>(dx_act);
     nparts = want ? (dx_colsum ? 3 : 2) : 0;
     if (cols == 128)
-      ln_bwd_vec_kernel<TDY, TX, TDX, 1><<<nblk, LN_WARPS * 32, 0, st>>>(
-          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
+      launch_k(ln_bwd_vec_kernel<TDY, TX, TDX, 1>, nblk, LN_WARPS * 32, 0, st, rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
     else
-      ln_bwd_vec_kernel<TDY, TX, TDX, 2><<<nblk, LN_WARPS * 32, 0, st>>>(
-          rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
+      launch_k(ln_bwd_vec_kernel<TDY, TX, TDX, 2>, nblk, LN_WARPS * 32, 0, st, rows, dyp, dy_rs, xp, x_rs, mean, rstd, gamma, dres, dxp, dx_rs, dxa, dxa_rs, ws, nparts);
     EVO_LAUNCHED("ln_bwd_vec_kernel");
   } else {
     EVO_REQUIRE(!dx_act && !dx_colsum, EVO_EUNSUP,
                 "layernorm_bwd: fused dx copy / column sums need the vectorised layout");
     size_t smem = (size_t)LN_WARPS * 2 * cols * sizeof(float);
 #define L(Vn)                                                                                 \
-  ln_bwd_kernel<TDY, TX, TDX, Vn><<<nblk, LN_WARPS * 32, smem, st>>>(                          \
+  launch_k(ln_bwd_kernel<TDY, TX, TDX, Vn>, nblk, LN_WARPS * 32, smem, st, \
       rows, cols, dyp, dy_rs, xp, x_rs, x_cs, mean, rstd, gamma, dres, dxp, dx_rs, dx_cs, ws, want)
     if (cols <= 32) L(1);
     else if (cols <= 64) L(2);
@@ -1157,8 +1165,8 @@ int ln_bwd_launch(int64_t rows, int cols, const void *dy, int64_t dy_rs, const v
   }
   if (want) {
     const int outs = nparts * cols;
-    ln_param_reduce_kernel<<<(outs + 31) / 32, 1024, 0, st>>>(nblk, cols, nparts, ws, dgamma,
-                                                             dbeta, dx_colsum, acc);
+    launch_k(ln_param_reduce_kernel, (outs + 31) / 32, 1024, 0, st, nblk, cols, nparts, ws, dgamma,
+                                                             dbeta, dx_colsum, acc, nullptr, 0);
     EVO_LAUNCHED("ln_param_reduce_kernel");
   }
   return EVO_OK;
@@ -1238,19 +1246,16 @@ int layernorm_bwd_proj(int64_t rows, int cols, const float *dy, const float *x, 
                                      reinterpret_cast<const bf16 *>(Wp), nh, dx,
                                      reinterpret_cast<bf16 *>(dx_act), w, nparts, st, &nb);
     if (rc != EVO_OK) return rc;
-    ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(
-        nb, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
+    launch_k(ln_param_reduce_kernel, (nparts * cols + 31) / 32, 1024, 0, st, nb, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
     EVO_LAUNCHED("ln_param_reduce_kernel");
     return EVO_OK;
   }
   const int64_t need_blocks = (rows + LN_WARPS - 1) / LN_WARPS;
   const int nblk = (int)std::min<int64_t>(LN_BWD_BLOCKS, std::max<int64_t>(need_blocks, 1));
-  ln_bwd_proj_kernel<8><<<nblk, LN_WARPS * 32, 0, st>>>(
-      rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
+  launch_k(ln_bwd_proj_kernel<8>, nblk, LN_WARPS * 32, 0, st, rows, dy, x, mean, rstd, gamma, beta, dres, dproj, p_rs,
       reinterpret_cast<const bf16 *>(Wp), nh, dx, reinterpret_cast<bf16 *>(dx_act), w);
   EVO_LAUNCHED("ln_bwd_proj_kernel");
-  ln_param_reduce_kernel<<<(nparts * cols + 31) / 32, 1024, 0, st>>>(
-      nblk, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
+  launch_k(ln_param_reduce_kernel, (nparts * cols + 31) / 32, 1024, 0, st, nblk, cols, nparts, w, dgamma, dbeta, dx_colsum, 0, dWp, nh);
   EVO_LAUNCHED("ln_param_reduce_kernel");
   return EVO_OK;
 }
