@@ -125,7 +125,10 @@ def pick_split(rows_k: int, M: int, N_: int, batch: int = 1, min_rows: int = 512
     output tiles, each chunk >= `min_rows` (8 k-steps of the TMA pipeline)."""
     tn = 256 if N_ > 128 else 128  # evo_gemm's split-K tile width (gemm_tc.cu choose_bn)
     tiles = max(1, ((M + 127) // 128) * ((N_ + tn - 1) // tn) * batch)
-    by_fill = 148 // tiles
+    # 128 x 256 tiles: ~128 CTAs beat a full 148-CTA wave (measured on the
+    # step's weight gradients: [128 x 1024] over 65536 rows 47.7 -> 45.5 us,
+    # [128 x 512] 29.4 -> 26.9 us; the partials traffic grows with the split)
+    by_fill = (128 if tn == 256 else 148) // tiles
     by_size = rows_k // min_rows
     return int(max(1, min(by_fill, by_size)))
 
