@@ -28,7 +28,8 @@
 
 namespace evo {
 void note_backend(int b);
-int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart, cudaStream_t st);
+int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart, float *lse2,
+                  cudaStream_t st);
 int reduce_lead(int, int64_t, int64_t, int64_t, const void *, float *, int64_t, int64_t, int,
                 cudaStream_t);
 namespace {
@@ -1002,14 +1003,13 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
       for (int c = 0; c < EPT; c += 4) {
         const float4 l4 = *reinterpret_cast<const float4 *>(sl + c);
         const float4 d4 = *reinterpret_cast<const float4 *>(sd + c);
-        lq[c] = l4.x * LOG2E_F; lq[c + 1] = l4.y * LOG2E_F;
-        lq[c + 2] = l4.z * LOG2E_F; lq[c + 3] = l4.w * LOG2E_F;
+        lq[c] = l4.x; lq[c + 1] = l4.y; lq[c + 2] = l4.z; lq[c + 3] = l4.w;  // log2 units
         dq[c] = d4.x; dq[c + 1] = d4.y; dq[c + 2] = d4.z; dq[c + 3] = d4.w;
       }
       if (BIAS) {
 #pragma unroll
         for (int qq = 0; qq < EPT; ++qq)
-          bq[qq] = *reinterpret_cast<const float *>(bx + qq * 128 + boff[qq & 7]) * LOG2E_F;
+          bq[qq] = *reinterpret_cast<const float *>(bx + qq * 128 + boff[qq & 7]);
       }
       tmem_wait_ld();
       uint32_t pp[EPT / 2], pd[EPT / 2];
@@ -1022,7 +1022,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
           for (int e = 0; e < 2; ++e) {
             const int qq = c + e;
             float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
-            if (BIAS) x += bq[qq];
+            if (BIAS) x = fmaf(bq[qq], LOG2E_F, x);
             p[e] = ex2f(x);
             ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
           }
@@ -1037,7 +1037,7 @@ attn_flash_dkv_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_const
           for (int e = 0; e < 2; ++e) {
             const int qq = c + e;
             float x = fmaf(__uint_as_float(sv[qq]), sc_l2, -lq[qq]);
-            if (BIAS) x += bq[qq];
+            if (BIAS) x = fmaf(bq[qq], LOG2E_F, x);
             p[e] = (kv && qb + qq < L) ? ex2f(x) : 0.f;
             ds[e] = p[e] * (__uint_as_float(dv[qq]) - dq[qq]);
           }
@@ -1165,7 +1165,7 @@ int64_t flash_chunk(const evo_attn_desc *d, int per_sm, int64_t &nch) {
 }
 
 struct FlashWs {
-  size_t dO, Dq, gate, part, total;
+  size_t dO, Dq, lse2, gate, part, total;
 };
 FlashWs flash_ws(const evo_attn_desc *d) {
   FlashWs w;
@@ -1173,7 +1173,8 @@ FlashWs flash_ws(const evo_attn_desc *d) {
   const int64_t span = (d->nb - 1) * d->o_sb + (int64_t)(d->L - 1) * d->o_sl + (int64_t)d->H * d->D;
   w.dO = 0;
   w.Dq = pad((size_t)span * 2);
-  w.gate = w.Dq + pad((size_t)d->nb * d->H * d->L * 4);
+  w.lse2 = w.Dq + pad((size_t)d->nb * d->H * d->L * 4);   // lse in log2 units (dk/dv)
+  w.gate = w.lse2 + pad((size_t)d->nb * d->H * d->L * 4);
   w.part = w.gate + pad((size_t)num_sms() * 8 * d->H * d->D * 4);
   int64_t nch;
   flash_chunk(d, 1, nch);
@@ -1218,7 +1219,8 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
   uint8_t *ws = reinterpret_cast<uint8_t *>(d->workspace);
   bf16 *dO = reinterpret_cast<bf16 *>(ws + w.dO);
   float *Dq = reinterpret_cast<float *>(ws + w.Dq);
-  int rc = attn_prep_run(d, dO, Dq, reinterpret_cast<float *>(ws + w.gate), st);
+  float *lse2 = reinterpret_cast<float *>(ws + w.lse2);
+  int rc = attn_prep_run(d, dO, Dq, reinterpret_cast<float *>(ws + w.gate), lse2, st);
   if (rc != EVO_OK) return rc;
   int64_t nch;
   a.chunk = flash_chunk(d, 1, nch);
@@ -1264,7 +1266,9 @@ int flash_bwd(const evo_attn_desc *d, cudaStream_t st) {
     auto kfn = attn_flash_dkv_kernel<D, BIAS>;
     EVO_MAX_SMEM_ONCE(kfn);
     dim3 grid((d->L + QT - 1) / QT, d->H, (unsigned)nch);
-    launch_k(kfn, grid, nth_of(TPR_DKV), smem, st, mq2, mk2, mv2, mdo2, mb2, a);
+    FlashArgs a2 = a;
+    a2.lse = lse2;      // staged as log2 units: no per-logit rescale in the dk/dv pass
+    launch_k(kfn, grid, nth_of(TPR_DKV), smem, st, mq2, mk2, mv2, mdo2, mb2, a2);
     EVO_LAUNCHED("attn_flash_dkv_kernel");
   }
   if (BIAS) {

@@ -398,7 +398,7 @@ attn_fwd_tc_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_constant
 template <int D>
 __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, const bf16 *dgm,
                                                             bf16 *dO_out, bf16 *dgpre, float *Dq,
-                                                            float *gpart) {
+                                                            float *gpart, float *lse2) {
   evo_pdl_enter();
   constexpr int CH = D / 8;  // chunks per head (1, 2 or 4)
   // 32-bit index math (the host checks total < 2^31): the per-element
@@ -452,7 +452,11 @@ __global__ void __launch_bounds__(256) attn_bwd_prep_kernel(const AttnTcArgs a, 
     // fixed-order reduction over the CH chunk lanes (aligned groups of CH)
 #pragma unroll
     for (int off = 1; off < CH; off <<= 1) acc += __shfl_xor_sync(0xffffffffu, acc, off);
-    if (ok && c == 0) Dq[(b * a.H + h) * (int64_t)a.L + l] = acc;
+    if (ok && c == 0) {
+      const int64_t i = (b * a.H + h) * (int64_t)a.L + l;
+      Dq[i] = acc;
+      if (lse2) lse2[i] = a.lse[i] * LOG2E;  // the streamed-key dk/dv stages log2 units
+    }
   }
   if (gpart) {
     // threads t, t + G, t + 2G, ... (G = H*CH column groups) share columns
@@ -2114,7 +2118,7 @@ int bwd_launch_mode(const evo_attn_desc *d, cudaStream_t st) {
     float *gpart = fuse_gb ? reinterpret_cast<float *>(ws + gate_part_offset(d)) : nullptr;
     launch_k(attn_bwd_prep_kernel<D>, blocks, 256, 0, st, a, reinterpret_cast<const bf16 *>(d->dgm),
                                                      dObuf, reinterpret_cast<bf16 *>(d->dgpre), Dq,
-                                                     gpart);
+                                                     gpart, static_cast<float *>(nullptr));
     EVO_LAUNCHED("attn_bwd_prep_kernel");
     if (d->dgate_bias) {
       if (fuse_gb) {
@@ -2266,7 +2270,7 @@ int attention_tc_fwd(const evo_attn_desc *d, cudaStream_t st) {
 // The backward's prep pass for other kernels (attention_flash.cu): dO (o's
 // strides) -> dO_out, dGpre -> d->dgpre, Dq [nb, H, L]; the gate-bias sums
 // into d->dgate_bias when set (gpart: SMs*8*H*D fp32 of workspace).
-int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
+int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart, float *lse2,
                   cudaStream_t st) {
   if (d->D != 8 && d->D != 16 && d->D != 32) return EVO_EUNSUP;
   AttnTcArgs a = make_args(d);
@@ -2283,11 +2287,11 @@ int attn_prep_run(const evo_attn_desc *d, void *dO_out, float *Dq, float *gpart,
   bf16 *dgp = reinterpret_cast<bf16 *>(d->dgpre);
   float *gp = fuse_gb ? gpart : nullptr;
   if (d->D == 32)
-    launch_k(attn_bwd_prep_kernel<32>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<32>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp, lse2);
   else if (d->D == 16)
-    launch_k(attn_bwd_prep_kernel<16>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<16>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp, lse2);
   else
-    launch_k(attn_bwd_prep_kernel<8>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp);
+    launch_k(attn_bwd_prep_kernel<8>, blocks, 256, 0, st, a, dgm, dO, dgp, Dq, gp, lse2);
   EVO_LAUNCHED("attn_bwd_prep_kernel");
   if (fuse_gb) return colsum_partials(blocks, (int64_t)d->H * d->D, gp, d->dgate_bias, 0, st);
   return EVO_OK;
