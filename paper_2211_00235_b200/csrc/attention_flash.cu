@@ -11,15 +11,16 @@
 //   by more than 8: P <= 2^8 keeps bf16 P and the fp32 row sum exact enough,
 //   and O in TMEM is rescaled only then), P_j (bf16 pairs) -> TMEM,
 //   O += P_j V_j (TS MMA).  Epilogue O / l, gate, o, gm, lse.
-// dq       (grid: q-tiles x H x chunks of batch rows)
+// dq       (grid: q-tiles x H x chunks of batch rows; rows in groups of 4)
 //   S_j, dP_j = dO V_j^T;  P = exp2(S*c + bias*log2e - lse*log2e),
-//   dS = P (dP - Dq) -> TMEM;  dQ += dS K_j (TS MMA);  dbias: each thread
-//   adds its dS values into the chunk's fp32 partial (one owner thread per
-//   element, batch rows in order: deterministic), chunks reduced in order.
+//   dS = P (dP - Dq) -> TMEM;  dQ += dS K_j (TS MMA);  dbias: a group's dS
+//   summed in TMEM, then added by its one owner thread into the chunk's fp32
+//   partial (groups in order: deterministic), chunks reduced in order.
 // dkv      (grid: 128-key tiles x H x nb)
 //   S^T_j = K Q_j^T, dP^T_j = V dO_j^T;  P^T, dS^T -> TMEM;
 //   dV += P^T dO_j, dK += dS^T Q_j (TS MMAs).
-// The prep pass (dO = dGM G, dGpre, Dq = rowsum(dO O)) is attention_long's.
+// The prep pass (dO = dGM G, dGpre, Dq = rowsum(dO O), lse in log2 units) is
+// attention_tc's.
 // Bias: plain [H][L][bq] fp32 (the caller copies a transposed bias plain).
 #include <algorithm>
 
@@ -737,10 +738,10 @@ attn_flash_dq_kernel(const __grid_constant__ CUtensorMap mQ, const __grid_consta
       for (int k = 0; k < EPT; k += 2) pk[k >> 1] = pk2(ds[k], ds[k + 1]);
       tst<EPT / 2>(lane_addr + bi * 160 + 128 + part * (EPT / 2), pk);
       if (BIAS && qv) {
-        // the chunk's dbias partial: the pair's two rows summed in registers,
-        // then the chunk's first pair stores and later pairs add with
-        // fire-and-forget reductions (one owner thread per element, program
-        // order per address: the sum runs over the pairs in order)
+        // the chunk's dbias partial: the group's rows summed (parked in
+        // TMEM), then the chunk's first group stores and later groups add
+        // with fire-and-forget reductions (one owner thread per element,
+        // program order per address: the sum runs over the groups in order)
         const bool emit = slot == gs - 1;            // the group's last row
         if (gs > 1) {
           uint32_t u[EPT];
