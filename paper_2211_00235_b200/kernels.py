@@ -156,6 +156,12 @@ def linear_dw(x, rows: int, d_in: int, dy, d_out: int, dW, ldd: int, *, x_ld=Non
     """dW[d_in, d_out] (+)= x^T @ dy over `rows` (split-K, deterministic)."""
     x_ld = d_in if x_ld is None else x_ld
     dy_ld = d_out if dy_ld is None else dy_ld
+    if d_in <= 128 < d_out and rows >= 16384:
+        # narrow input, wide output: compute dW^T = dy^T x (the wide side on
+        # the MMA's M, 128-wide N tiles): [128 x 1024] over 65536 rows 43 -> 39 us
+        gemm(Mat(dy, 1, dy_ld, off=dy_off), Mat(x, 1, x_ld), Mat(dW, 1, ldd, off=dw_off),
+             d_out, d_in, rows, split_k=pick_split(rows, d_out, d_in), accumulate=accumulate)
+        return
     gemm(Mat(x, 1, x_ld), Mat(dy, 1, dy_ld, off=dy_off), Mat(dW, ldd, 1, off=dw_off),
          d_in, d_out, rows, split_k=pick_split(rows, d_in, d_out), accumulate=accumulate)
 
